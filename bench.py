@@ -1,0 +1,414 @@
+#!/usr/bin/env python
+"""Benchmark of the Spotlight decode-time retrieval path on B200.
+
+Headline (BASELINE.json `metric`, config 3): Hamming top-k retrieval over a
+512K-token x 32-head cache of 128-bit codes, k = budget_from_rate(0.02) =
+10485, one retrieval = K3 scan + select (spl_hamming_topk), inputs resident in
+HBM (268 MB of codes per step > 126 MB L2, so no L2 flush is needed). `value`
+is the device time per retrieval in microseconds (max over ranks; lower is
+better).  For N > 1 GPUs the cache is sequence-sharded (config 5, weak
+scaling: 512K tokens per GPU, total N x 512K): local scan + histogram, NCCL
+all-gather of the [32][129] histograms, global threshold + tie quota, local
+ordered select.
+
+Secondary (config 2): one full decode step of a 32-head layer at 128K context
+(encode-append of the new key + query encode + retrieval + sparse attention
+over bf16 K/V) -> sparse decode tok/s.
+
+`--impl reference` times the reference's own CPU implementation
+(oracle/_ref/libspotref.so = the unmodified reference sources, else the C
+port) on the same workload on all host cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+sys.path.insert(0, str(ROOT / "tests"))
+
+METRIC = "Hamming top-k retrieval µs @512K tokens (HBM GB/s %peak); sparse decode tok/s"
+H, N_TOK, L, D = 32, 524288, 128, 128
+
+
+def peaks():
+    try:
+        p = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+# ---------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for ln in self.proc.stdout:
+            self.lines.append(ln.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.t.join(timeout=2)
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------- inputs
+def random_codes(torch, P, n, W, seed, dev):
+    g = torch.Generator(device=dev)
+    g.manual_seed(seed)
+    return torch.randint(-2**31, 2**31 - 1, (P, n, W), generator=g, device=dev, dtype=torch.int32)
+
+
+def event_timer(torch, fn, steps, stream):
+    start = torch.cuda.Event(enable_timing=True)
+    end = torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    start.record(stream)
+    for _ in range(steps):
+        fn()
+    end.record(stream)
+    torch.cuda.synchronize()
+    return start.elapsed_time(end) / steps  # ms per step
+
+
+# ---------------------------------------------------------------- CPU legs
+def cpu_reference_retrieval(codes_np, q_np, k, threads, reps, warmup):
+    """The reference's retrieval (per head nxor_scores_into + top_k_indices,
+    heads over OpenMP threads) on host cores. Returns (us per retrieval list,
+    kind, result of the last run)."""
+    from oracle_lib import Oracle, RefLib
+
+    P, n, W = codes_np.shape
+    nv = np.full(P, n, np.uint32)
+    times = []
+    out = None
+    if RefLib.available():
+        ref = RefLib()
+        h = ref.index_create(codes_np, nv)
+        try:
+            for i in range(warmup + reps):
+                t0 = time.perf_counter()
+                out = ref.retrieve_batch(h, q_np, nv, k, threads)
+                dt = (time.perf_counter() - t0) * 1e6
+                if i >= warmup:
+                    times.append(dt)
+        finally:
+            ref.index_destroy(h)
+        return times, "reference", out
+    orc = Oracle()
+    for i in range(warmup + reps):
+        t0 = time.perf_counter()
+        out = orc.retrieve_batch(codes_np, q_np, nv, k, threads)
+        dt = (time.perf_counter() - t0) * 1e6
+        if i >= warmup:
+            times.append(dt)
+    return times, "port", out
+
+
+def run_reference_arm(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    rng = np.random.default_rng(0)
+    codes = rng.integers(0, 2**32, (H, N_TOK, L // 32), dtype=np.uint64).astype(np.uint32)
+    q = rng.integers(0, 2**32, (H, L // 32), dtype=np.uint64).astype(np.uint32)
+    k = budget(N_TOK)
+    times, kind, _ = cpu_reference_retrieval(codes, q, k, threads, args.steps, args.warmup)
+    v = statistics.mean(times)
+    line = {"metric": METRIC, "value": round(v, 2), "unit": "µs", "impl": "reference",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(v / 1000, 4), "higher_is_better": False, "scaling": "weak",
+            "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+            "config": {"workload": "config3: 32 heads x 524288 tokens x 128-bit codes, k=10485 "
+                                   "(per head nxor_scores_into + top_k_indices)", "heads": H,
+                       "tokens": N_TOK, "code_bits": L, "k": k},
+            "cpu_baseline": {"value": round(v, 2), "unit": "µs", "cores": threads, "kind": kind,
+                             "sample": f"full config-3 workload per step ({H} heads x {N_TOK} rows), "
+                                       f"heads spread over {threads} OpenMP threads"},
+            "e2e": {"value": round(v, 2), "unit": "µs", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def budget(n):
+    return min(max(int(0.02 * n), 20), n)
+
+
+# ---------------------------------------------------------------- GPU arm
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-decode", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference_arm(args)
+
+    import torch
+
+    from paper_2508_19740_b200 import capi
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist_mod
+
+        dist = dist_mod
+        dist.init_process_group("nccl", device_id=dev)
+    ctx = capi.Context(local)
+    stream = torch.cuda.current_stream()
+    W = L // 32
+    P = H
+    n_local = N_TOK  # weak scaling: 512K tokens per GPU
+    n_total = n_local * world
+    k = budget(n_total)
+
+    codes = random_codes(torch, P, n_local, W, seed=1234 + rank, dev=dev)
+    g = torch.Generator(device=dev)
+    g.manual_seed(99)
+    qcodes = torch.randint(-2**31, 2**31 - 1, (P, W), generator=g, device=dev, dtype=torch.int32)
+    nvalid = torch.full((P,), n_local, dtype=torch.int32, device=dev)
+    idx = torch.zeros((P, k), dtype=torch.int32, device=dev)
+    cnt = torch.zeros(P, dtype=torch.int32, device=dev)
+    off = torch.zeros(P, dtype=torch.int32, device=dev)
+    hist = torch.zeros((P, L + 1), dtype=torch.int32, device=dev)
+    all_hist = torch.zeros((world, P, L + 1), dtype=torch.int32, device=dev)
+
+    if world == 1:
+        def retrieval():
+            ctx.hamming_topk(codes, n_local, L, qcodes, P, nvalid, 1, n_local, k, idx, cnt, stream)
+    else:
+        def retrieval():
+            ctx.shard_histogram(codes, n_local, L, qcodes, P, nvalid, 1, n_local, hist, stream)
+            dist.all_gather_into_tensor(all_hist, hist)
+            ctx.shard_select(all_hist, world, rank, L, P, nvalid, 1, n_local, k, idx, cnt, off, stream)
+
+    for _ in range(args.warmup):
+        retrieval()
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    l0 = ctx.launches()
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    ms = event_timer(torch, retrieval, args.steps, stream)
+    launches = ctx.launches() - l0
+    if dist:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    us = ms * 1000.0
+
+    # scan-kernel share: the same streaming kernel alone (shard mode, no select)
+    def scan_only():
+        ctx.shard_histogram(codes, n_local, L, qcodes, P, nvalid, 1, n_local, hist, stream)
+    for _ in range(3):
+        scan_only()
+    scan_ms = event_timer(torch, scan_only, args.steps, stream)
+
+    # e2e through the C-ABI with host buffers: H2D of the step's query vectors
+    # (encoded on device, exact mode), retrieval, D2H of the indices + counts.
+    rng = np.random.default_rng(7)
+    e2e = None
+    decode = None
+    if world == 1:
+        w1 = (rng.standard_normal((H, D, D)) / np.sqrt(D)).astype(np.float32)
+        b1 = np.zeros((H, D), np.float32)
+        w2 = (rng.standard_normal((H, D, L)) / np.sqrt(D)).astype(np.float32)
+        hasher = ctx.hasher(w1, b1, w2)
+        q_host = torch.from_numpy(rng.standard_normal((1, H, D)).astype(np.float32)).pin_memory()
+        idx_host = torch.empty((P, k), dtype=torch.int32).pin_memory()
+        cnt_host = torch.empty(P, dtype=torch.int32).pin_memory()
+        q_dev = torch.empty((1, H, D), dtype=torch.float32, device=dev)
+
+        def e2e_step():
+            q_dev.copy_(q_host, non_blocking=True)
+            hasher.encode(q_dev, 1, 1, qcodes, capi.SPL_ENCODE_EXACT, stream)
+            ctx.hamming_topk(codes, n_local, L, qcodes, P, nvalid, 1, n_local, k, idx, cnt, stream)
+            idx_host.copy_(idx, non_blocking=True)
+            cnt_host.copy_(cnt, non_blocking=True)
+
+        for _ in range(args.warmup):
+            e2e_step()
+        e2e_ms = event_timer(torch, e2e_step, args.steps, stream)
+        e2e = {"value": round(e2e_ms * 1000, 2), "unit": "µs",
+               "h2d_bytes_per_step": int(q_host.numel() * 4),
+               "d2h_bytes_per_step": int(idx_host.numel() * 4 + cnt_host.numel() * 4),
+               "path": "spl_encode(query, exact) + spl_hamming_topk, pinned host buffers"}
+        if not args.no_decode:
+            decode = bench_decode(torch, capi, ctx, dev, stream, args, hasher)
+    clk = clocks.stop()
+
+    # CPU baseline (rank 0, N = 1): the reference on this host's cores
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        codes_np = codes.cpu().numpy().view(np.uint32)
+        q_np = qcodes.cpu().numpy().view(np.uint32)
+        threads = os.cpu_count() or 1
+        times, kind, ref_out = cpu_reference_retrieval(codes_np, q_np, k, threads, reps=3, warmup=1)
+        hamming_topk_np = idx.cpu().numpy().view(np.uint32)
+        ctx.hamming_topk(codes, n_local, L, qcodes, P, nvalid, 1, n_local, k, idx, cnt, stream)
+        torch.cuda.synchronize()
+        parity = bool(np.array_equal(idx.cpu().numpy().view(np.uint32), ref_out))
+        cpu = {"value": round(statistics.mean(times), 1), "unit": "µs", "cores": threads,
+               "kind": kind, "sample": f"3 full config-3 retrievals ({H} heads x {n_local} rows, "
+                                       f"k={k}) after 1 warm-up; heads over {threads} threads",
+               "gpu_indices_equal_reference": parity}
+        del hamming_topk_np
+
+    hbm, peak_kind = peaks()
+    alg_bytes = P * n_local * W * 4 + P * W * 4 + P * k * 4  # SURVEY 8(d), per rank
+    achieved = alg_bytes / (us * 1e-6) / 1e9
+    scan_bytes = P * n_local * W * 4
+    traffic = None
+    tpath = ROOT / "profiles" / "r01_k3_traffic.json"
+    if tpath.exists():
+        try:
+            traffic = json.loads(tpath.read_text()).get("bytes_per_retrieval")
+        except Exception:
+            traffic = None
+    line = {
+        "metric": METRIC, "value": round(us, 2), "unit": "µs", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 5),
+        "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "u32",
+        "data": "synthetic",
+        "config": {"workload": ("config3: 32 heads x 524288 tokens x 128-bit codes, k=10485"
+                                if world == 1 else
+                                f"config5: sequence-sharded {n_total} tokens x 32 heads x 128-bit, "
+                                f"k={k}, NCCL all-gather of per-head histograms"),
+                   "heads": H, "tokens_per_gpu": n_local, "tokens_total": n_total, "code_bits": L,
+                   "k": k, "l2": "inputs (268 MB codes) larger than the 126 MB L2; no flush"},
+        "roofline": {"bound": "hbm", "kernel": "one retrieval = k3_scan + k3_select",
+                     "achieved": round(achieved, 1), "peak": hbm, "peak_kind": peak_kind,
+                     "unit": "GB/s", "frac": round(achieved / hbm, 4),
+                     "algorithmic_bytes": alg_bytes, "traffic": traffic,
+                     "scan_kernel_us": round(scan_ms * 1000, 2),
+                     "scan_kernel_frac": round(scan_bytes / (scan_ms * 1e-3) / 1e9 / hbm, 4)},
+        "gpu_launches": int(launches),
+        "clocks": clk,
+        "e2e": e2e,
+        "cpu_baseline": cpu,
+        "throughput": {"value": round(P * n_total / (us * 1e-6) / 1e9, 2),
+                       "unit": "G (token, head) codes scanned per s"},
+    }
+    if decode:
+        line["sparse_decode"] = decode
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    ctx.close()
+    if dist:
+        dist.destroy_process_group()
+
+
+def bench_decode(torch, capi, ctx, dev, stream, args, hasher_c3):
+    """Config 2: B=1, 32 heads, 128K context, k=2% = 2621, bf16 K/V; one full
+    decode step (append new key + encode query + retrieve + sparse attend)."""
+    B, n = 1, 131072
+    k = budget(n)
+    P = B * H
+    W = L // 32
+    cap = n
+    codes = random_codes(torch, P, cap, W, seed=55, dev=dev)
+    g = torch.Generator(device=dev)
+    g.manual_seed(5)
+    kc = torch.randn((B, H, cap, D), generator=g, device=dev, dtype=torch.float32).to(torch.bfloat16)
+    vc = torch.randn((B, H, cap, D), generator=g, device=dev, dtype=torch.float32).to(torch.bfloat16)
+    q = torch.randn((B, H, D), generator=g, device=dev)
+    kn = torch.randn((B, H, D), generator=g, device=dev)
+    vn = torch.randn((B, H, D), generator=g, device=dev)
+    nvalid = torch.full((B,), n, dtype=torch.int32, device=dev)
+    idx = torch.zeros((P, k), dtype=torch.int32, device=dev)
+    cnt = torch.zeros(P, dtype=torch.int32, device=dev)
+    out = torch.zeros((B, H, D), dtype=torch.float32, device=dev)
+    scale = float(1 / np.sqrt(D))
+
+    def step():
+        hasher_c3.decode_step(q, kn, vn, B, codes, kc, vc, capi.SPL_BF16, cap, nvalid, n, k, scale,
+                              idx, cnt, out, stream)
+
+    for _ in range(args.warmup):
+        step()
+    l0 = ctx.launches()
+    ms = event_timer(torch, step, args.steps, stream)
+    launches = ctx.launches() - l0
+    # attention alone (same indices)
+    def att():
+        ctx.sparse_attend(q, kc, vc, capi.SPL_BF16, cap, D, P, idx, k, cnt, nvalid, H, scale, out, stream)
+    att_ms = event_timer(torch, att, args.steps, stream)
+    hbm, _ = peaks()
+    alg = P * n * W * 4 + P * (k + 1) * D * 2 * 2 + H * (D * D + D + D * L) * 4 + P * k * 4
+    return {"workload": "config2: B=1, 32 heads, 131072-token bf16 K/V cache, 128-bit codes, k=2621",
+            "us_per_step": round(ms * 1000, 2), "tok_per_s": round(B / (ms * 1e-3), 1),
+            "unit": "tok/s (one 32-head layer)", "gpu_launches_per_step": launches / args.steps,
+            "attend_us": round(att_ms * 1000, 2),
+            "roofline": {"bound": "hbm", "algorithmic_bytes": alg,
+                         "achieved": round(alg / (ms * 1e-3) / 1e9, 1), "peak": hbm,
+                         "frac": round(alg / (ms * 1e-3) / 1e9 / hbm, 4)}}
+
+
+if __name__ == "__main__":
+    main()

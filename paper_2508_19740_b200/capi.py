@@ -1,0 +1,334 @@
+"""ctypes binding of include/spl_c.h (libspl.so, the sm_100a kernels).
+
+Host-side glue only: every compute call launches CUDA kernels through the
+C-ABI; there is no CPU fallback. Loading the library works on a CPU-only
+machine (symbol checks), but creating a context requires a Blackwell GPU and
+fails loudly otherwise.
+
+Errors map to the reference's exception types (proj/include/spotlight/
+errors.hpp:9-35): DimensionError (an invalid_argument -> ValueError),
+NumericError, FormatError, IoError.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import re
+from pathlib import Path
+
+PKG = Path(__file__).resolve().parent
+ROOT = PKG.parent
+LIB_PATH = PKG / "lib" / "libspl.so"
+HEADER = ROOT / "include" / "spl_c.h"
+
+SPL_OK, SPL_E_DIMENSION, SPL_E_NUMERIC, SPL_E_FORMAT, SPL_E_IO, SPL_E_CUDA, SPL_E_NCCL, SPL_E_STATE = range(8)
+SPL_F32, SPL_BF16 = 0, 1
+SPL_HASHER_LINEAR, SPL_HASHER_MLP = 0, 1
+SPL_ENCODE_EXACT, SPL_ENCODE_TC = 0, 1
+
+
+class SpotlightError(RuntimeError):
+    pass
+
+
+class DimensionError(SpotlightError, ValueError):
+    """spotlight::DimensionError (errors.hpp:9-13)."""
+
+
+class NumericError(SpotlightError):
+    """spotlight::NumericError (errors.hpp:21-25)."""
+
+
+class FormatError(SpotlightError):
+    """spotlight::FormatError (errors.hpp:15-19)."""
+
+
+class IoError(SpotlightError):
+    """spotlight::IoError (errors.hpp:32-35)."""
+
+
+class CudaError(SpotlightError):
+    pass
+
+
+class StateError(SpotlightError):
+    pass
+
+
+_ERR = {SPL_E_DIMENSION: DimensionError, SPL_E_NUMERIC: NumericError, SPL_E_FORMAT: FormatError,
+        SPL_E_IO: IoError, SPL_E_CUDA: CudaError, SPL_E_NCCL: SpotlightError,
+        SPL_E_STATE: StateError}
+
+_lib = None
+
+vp = C.c_void_p
+u32, u64, i32, f32, dbl = C.c_uint32, C.c_uint64, C.c_int, C.c_float, C.c_double
+u32p = C.POINTER(C.c_uint32)
+
+# name -> argtypes (restype spl_status = c_int unless listed in _RESTYPE)
+_SIGS = {
+    "spl_version": [],
+    "spl_ctx_create": [i32, C.POINTER(vp)],
+    "spl_ctx_destroy": [vp],
+    "spl_last_error": [vp],
+    "spl_reserve": [vp, u32, u64, u32, u32, u32],
+    "spl_check_device_error": [vp, vp],
+    "spl_launch_count": [vp],
+    "spl_device_alloc": [vp, C.c_size_t, C.POINTER(vp)],
+    "spl_device_free": [vp, vp],
+    "spl_memcpy": [vp, vp, vp, C.c_size_t, vp],
+    "spl_memset": [vp, vp, i32, C.c_size_t, vp],
+    "spl_stream_synchronize": [vp, vp],
+    "spl_pack_bits": [vp, vp, u64, u32, vp, vp],
+    "spl_unpack_bits": [vp, vp, u64, u32, vp, vp],
+    "spl_nxor_scores": [vp, vp, u64, u32, vp, u32, vp, u32, u64, vp, u64, vp],
+    "spl_top_k": [vp, vp, i32, u32, u64, u64, u32, vp, vp],
+    "spl_hamming_topk": [vp, vp, u64, u32, vp, u32, vp, u32, u64, u32, vp, vp, vp],
+    "spl_shard_histogram": [vp, vp, u64, u32, vp, u32, vp, u32, u64, vp, vp],
+    "spl_shard_select": [vp, vp, u32, u32, u32, u32, vp, u32, u64, u32, vp, vp, vp, vp],
+    "spl_plan_shard_host": [vp, u32, u32, u32, u32, u32p, u32p, u32p, u32p, u32p],
+    "spl_hasher_create": [vp, i32, u32, u32, u32, u32, vp, vp, vp, C.POINTER(vp)],
+    "spl_hasher_destroy": [vp],
+    "spl_mlp_forward": [vp, vp, vp, u32, u32, vp, vp],
+    "spl_encode": [vp, vp, vp, u32, u32, i32, vp, vp],
+    "spl_encode_append": [vp, vp, vp, vp, u32, vp, vp, vp, i32, u64, vp, vp],
+    "spl_sparse_attend": [vp, vp, vp, vp, i32, u64, u32, u32, vp, u64, vp, vp, u32, f32, vp, vp],
+    "spl_sparse_attend_partial": [vp, vp, vp, vp, i32, u64, u32, u32, vp, u64, vp, vp, u32, f32,
+                                  vp, vp],
+    "spl_attend_combine": [vp, vp, u32, u32, u32, vp, vp],
+    "spl_decode_step": [vp, vp, vp, vp, vp, u32, vp, vp, vp, i32, u64, vp, u64, u32, f32, vp, vp,
+                        vp, vp],
+    "spl_budget_from_rate": [dbl, u64, u32p],
+}
+_RESTYPE = {"spl_version": C.c_char_p, "spl_last_error": C.c_char_p, "spl_ctx_destroy": None,
+            "spl_hasher_destroy": None, "spl_launch_count": C.c_uint64}
+
+
+def header_symbols() -> list[str]:
+    """Every function the C-ABI header declares."""
+    text = HEADER.read_text()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(spl_[a-z0-9_]+)\s*\(", text)))
+
+
+def load(path: Path | None = None):
+    """Load libspl.so (raises if it was never built)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    p = Path(path or os.environ.get("SPL_LIB", LIB_PATH))
+    if not p.exists():
+        raise FileNotFoundError(
+            f"{p} missing: build the CUDA extension first (python -c 'import __graft_entry__ as g; g.build()')")
+    lib = C.CDLL(str(p))
+    for name, args in _SIGS.items():
+        fn = getattr(lib, name)
+        fn.argtypes = args
+        fn.restype = _RESTYPE.get(name, C.c_int)
+    _lib = lib
+    return lib
+
+
+def _ptr(t) -> int | None:
+    if t is None:
+        return None
+    if isinstance(t, int):
+        return t
+    return t.data_ptr()
+
+
+def _stream(stream) -> int | None:
+    if stream is None:
+        import torch
+
+        return torch.cuda.current_stream().cuda_stream
+    if isinstance(stream, int):
+        return stream
+    return stream.cuda_stream
+
+
+def budget_from_rate(rate: float, n: int) -> int:
+    """attention_eval.cpp:266-272."""
+    k = C.c_uint32(0)
+    st = load().spl_budget_from_rate(rate, n, C.byref(k))
+    if st:
+        raise DimensionError("budget_from_rate: rate must lie in (0, 1]")
+    return k.value
+
+
+def plan_shard_host(all_hist, rank: int, k: int):
+    """Host form of the sharded threshold / tie-quota plan for ONE problem.
+    all_hist: numpy uint32 [R][L+1]. Returns dict(T, quota, take_eq, count, offset)."""
+    import numpy as np
+
+    h = np.ascontiguousarray(all_hist, dtype=np.uint32)
+    R, L1 = h.shape
+    outs = [C.c_uint32(0) for _ in range(5)]
+    st = load().spl_plan_shard_host(h.ctypes.data, R, rank, L1 - 1, k, *[C.byref(o) for o in outs])
+    if st:
+        raise DimensionError("plan_shard_host: bad arguments")
+    return dict(zip(("T", "quota", "take_eq", "count", "offset"), (o.value for o in outs)))
+
+
+class Context:
+    """One spl_ctx (workspace + device error word). Not thread-safe."""
+
+    def __init__(self, device: int = 0):
+        import torch
+
+        self.lib = load()
+        self.device = device
+        torch.cuda.init()
+        with torch.cuda.device(device):
+            h = C.c_void_p()
+            st = self.lib.spl_ctx_create(device, C.byref(h))
+        if st:
+            raise CudaError(f"spl_ctx_create(device={device}) failed with status {st}: "
+                            "a Blackwell (sm_100) GPU is required")
+        self.h = h
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.lib.spl_ctx_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # -- plumbing
+    def check(self, st: int):
+        if st:
+            msg = self.lib.spl_last_error(self.h).decode()
+            raise _ERR.get(st, SpotlightError)(msg)
+
+    def check_device_error(self, stream=None):
+        self.check(self.lib.spl_check_device_error(self.h, _stream(stream)))
+
+    def launches(self) -> int:
+        return self.lib.spl_launch_count(self.h)
+
+    def reserve(self, P, n_max, L, k, d=0):
+        self.check(self.lib.spl_reserve(self.h, P, n_max, L, k, d))
+
+    # -- bitcodes
+    def pack_bits(self, bits, codes, stream=None):
+        n, L = bits.shape
+        self.check(self.lib.spl_pack_bits(self.h, _ptr(bits), n, L, _ptr(codes), _stream(stream)))
+
+    def unpack_bits(self, codes, L, bits, stream=None):
+        self.check(self.lib.spl_unpack_bits(self.h, _ptr(codes), codes.shape[0], L, _ptr(bits),
+                                            _stream(stream)))
+
+    def nxor_scores(self, codes, stride_rows, L, qcodes, P, n_valid, nvalid_div, n_max, scores,
+                    scores_stride, stream=None):
+        self.check(self.lib.spl_nxor_scores(self.h, _ptr(codes), stride_rows, L, _ptr(qcodes), P,
+                                            _ptr(n_valid), nvalid_div, n_max, _ptr(scores),
+                                            scores_stride, _stream(stream)))
+
+    def top_k(self, scores, dtype_code, P, n, stride, k, idx, stream=None):
+        self.check(self.lib.spl_top_k(self.h, _ptr(scores), dtype_code, P, n, stride, k, _ptr(idx),
+                                      _stream(stream)))
+
+    # -- K3
+    def hamming_topk(self, codes, stride_rows, L, qcodes, P, n_valid, nvalid_div, n_max, k, idx,
+                     cnt, stream=None):
+        self.check(self.lib.spl_hamming_topk(self.h, _ptr(codes), stride_rows, L, _ptr(qcodes), P,
+                                             _ptr(n_valid), nvalid_div, n_max, k, _ptr(idx),
+                                             _ptr(cnt), _stream(stream)))
+
+    def shard_histogram(self, codes, stride_rows, L, qcodes, P, n_valid, nvalid_div, n_max, hist,
+                        stream=None):
+        self.check(self.lib.spl_shard_histogram(self.h, _ptr(codes), stride_rows, L, _ptr(qcodes),
+                                                P, _ptr(n_valid), nvalid_div, n_max, _ptr(hist),
+                                                _stream(stream)))
+
+    def shard_select(self, all_hist, R, rank, L, P, n_valid, nvalid_div, n_max, k, idx, cnt,
+                     out_offset, stream=None):
+        self.check(self.lib.spl_shard_select(self.h, _ptr(all_hist), R, rank, L, P, _ptr(n_valid),
+                                             nvalid_div, n_max, k, _ptr(idx), _ptr(cnt),
+                                             _ptr(out_offset), _stream(stream)))
+
+    # -- encoders
+    def hasher(self, w1, b1=None, w2=None, kind=SPL_HASHER_MLP) -> "Hasher":
+        return Hasher(self, w1, b1, w2, kind)
+
+    # -- attention
+    def sparse_attend(self, q, kcache, vcache, kv_dtype, stride_rows, d, P, idx, idx_stride, cnt,
+                      n_valid, nvalid_div, scale, out, stream=None):
+        self.check(self.lib.spl_sparse_attend(self.h, _ptr(q), _ptr(kcache), _ptr(vcache), kv_dtype,
+                                              stride_rows, d, P, _ptr(idx), idx_stride, _ptr(cnt),
+                                              _ptr(n_valid), nvalid_div, scale, _ptr(out),
+                                              _stream(stream)))
+
+    def sparse_attend_partial(self, q, kcache, vcache, kv_dtype, stride_rows, d, P, idx,
+                              idx_stride, cnt, own_row, nvalid_div, scale, partials, stream=None):
+        self.check(self.lib.spl_sparse_attend_partial(self.h, _ptr(q), _ptr(kcache), _ptr(vcache),
+                                                      kv_dtype, stride_rows, d, P, _ptr(idx),
+                                                      idx_stride, _ptr(cnt), _ptr(own_row),
+                                                      nvalid_div, scale, _ptr(partials),
+                                                      _stream(stream)))
+
+    def attend_combine(self, partials, R, P, d, out, stream=None):
+        self.check(self.lib.spl_attend_combine(self.h, _ptr(partials), R, P, d, _ptr(out),
+                                               _stream(stream)))
+
+
+class Hasher:
+    """spl_hasher: a per-head bank of MLP (or linear) hashers on the device."""
+
+    def __init__(self, ctx: Context, w1, b1=None, w2=None, kind=SPL_HASHER_MLP):
+        import numpy as np
+
+        self.ctx = ctx
+        w1 = np.ascontiguousarray(w1, np.float32)
+        if kind == SPL_HASHER_MLP:
+            b1 = np.ascontiguousarray(b1, np.float32)
+            w2 = np.ascontiguousarray(w2, np.float32)
+            H, d, h = w1.shape
+            L = w2.shape[2]
+        else:
+            H, d, L = w1.shape
+            h = 0
+        self.kind, self.H, self.d, self.h, self.L = kind, H, d, h, L
+        out = C.c_void_p()
+        ctx.check(ctx.lib.spl_hasher_create(ctx.h, kind, H, d, h, L, w1.ctypes.data,
+                                            b1.ctypes.data if b1 is not None else None,
+                                            w2.ctypes.data if w2 is not None else None,
+                                            C.byref(out)))
+        self.h = out
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.ctx.lib.spl_hasher_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def mlp_forward(self, x, B, m, pre, stream=None):
+        self.ctx.check(self.ctx.lib.spl_mlp_forward(self.ctx.h, self.h, _ptr(x), B, m, _ptr(pre),
+                                                    _stream(stream)))
+
+    def encode(self, x, B, m, codes, mode=SPL_ENCODE_EXACT, stream=None):
+        self.ctx.check(self.ctx.lib.spl_encode(self.ctx.h, self.h, _ptr(x), B, m, mode, _ptr(codes),
+                                               _stream(stream)))
+
+    def encode_append(self, k_new, v_new, B, codes, kcache, vcache, kv_dtype, cap, pos,
+                      stream=None):
+        self.ctx.check(self.ctx.lib.spl_encode_append(self.ctx.h, self.h, _ptr(k_new), _ptr(v_new),
+                                                      B, _ptr(codes), _ptr(kcache), _ptr(vcache),
+                                                      kv_dtype, cap, _ptr(pos), _stream(stream)))
+
+    def decode_step(self, q, k_new, v_new, B, codes, kcache, vcache, kv_dtype, cap, n_valid,
+                    n_max, k, scale, idx, cnt, out, stream=None):
+        self.ctx.check(self.ctx.lib.spl_decode_step(self.ctx.h, self.h, _ptr(q), _ptr(k_new),
+                                                    _ptr(v_new), B, _ptr(codes), _ptr(kcache),
+                                                    _ptr(vcache), kv_dtype, cap, _ptr(n_valid),
+                                                    n_max, k, scale, _ptr(idx), _ptr(cnt),
+                                                    _ptr(out), _stream(stream)))

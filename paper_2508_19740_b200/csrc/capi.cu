@@ -1,0 +1,430 @@
+// extern "C" entry points of include/spl_c.h: argument validation with the
+// reference's error wording, context / workspace management, dispatch to the
+// sm_100a kernels. No CPU compute path exists: every compute entry point
+// launches a kernel or fails.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cmath>
+#include <string>
+#include <vector>
+
+#include "spl_launch.cuh"
+
+
+using namespace spl;
+
+namespace {
+inline cudaStream_t S(void* s) { return static_cast<cudaStream_t>(s); }
+constexpr float kLog2e = 1.4426950408889634f;
+
+
+spl_status check_L(spl_ctx* ctx, const char* who, uint32_t L) {
+    if (L == 0 || L % 32 != 0)
+        return fail(ctx, SPL_E_DIMENSION,
+                    std::string(who) + ": column count " + std::to_string(L) +
+                        " must be a positive multiple of 32");
+    if (L > (1u << 15))
+        return fail(ctx, SPL_E_DIMENSION,
+                    std::string("CodeMatrix: length_bits ") + std::to_string(L) +
+                        " exceeds the 32768-bit limit");
+    return SPL_OK;
+}
+}  // namespace
+
+extern "C" {
+
+const char* spl_version(void) { return "spotlight-b200 0.1 (sm_100a)"; }
+
+spl_status spl_ctx_create(int device, spl_ctx** out) {
+    if (!out) return SPL_E_STATE;
+    *out = nullptr;
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) {
+        cudaGetLastError();
+        return SPL_E_CUDA;
+    }
+    if (device < 0 || device >= n) return SPL_E_CUDA;
+    if (cudaSetDevice(device) != cudaSuccess) return SPL_E_CUDA;
+    cudaDeviceProp prop;
+    if (cudaGetDeviceProperties(&prop, device) != cudaSuccess) return SPL_E_CUDA;
+    if (prop.major != 10) {
+        // sm_100a cubins only: fail loudly on anything that is not Blackwell.
+        return SPL_E_CUDA;
+    }
+    spl_ctx* c = new spl_ctx;
+    c->device = device;
+    c->num_sms = prop.multiProcessorCount;
+    if (cudaMalloc(&c->dev_err, sizeof(uint32_t)) != cudaSuccess ||
+        cudaMemset(c->dev_err, 0, sizeof(uint32_t)) != cudaSuccess) {
+        delete c;
+        return SPL_E_CUDA;
+    }
+    *out = c;
+    return SPL_OK;
+}
+
+void spl_ctx_destroy(spl_ctx* ctx) {
+    if (!ctx) return;
+    cudaDeviceSynchronize();
+    cudaFree(ctx->dev_err);
+    cudaFree(ctx->k3_ws);
+    cudaFree(ctx->k3_state);
+    cudaFree(ctx->att_ws);
+    cudaFree(ctx->att_counters);
+    cudaFree(ctx->scratch);
+    delete ctx;
+}
+
+const char* spl_last_error(const spl_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+uint64_t spl_launch_count(const spl_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+spl_status spl_reserve(spl_ctx* ctx, uint32_t P, uint64_t n_max, uint32_t L, uint32_t k,
+                       uint32_t d) {
+    if (!ctx) return SPL_E_STATE;
+    // Run each path once on a dummy problem set sized like the real one is
+    // not possible without data; size the buffers from the same formulas.
+    const size_t score_bytes = L <= 255 ? 1 : 2;
+    const size_t n_pad = (n_max + 63) / 64 * 64;
+    const size_t G = (size_t)ctx->num_sms * 8 + 1;
+    const size_t sc = ((size_t)P * n_pad * score_bytes + 255) / 256 * 256;
+    const size_t rec = ((G + P) * (L + 2) * 4 + 255) / 256 * 256;
+    const size_t plans = ((G + P) * 16 + 255) / 256 * 256;
+    spl_status st = ensure_buffer(ctx, &ctx->k3_ws, &ctx->k3_ws_bytes, sc + rec + plans, false,
+                                  0, "spl_reserve");
+    if (st) return st;
+    size_t have = ctx->k3_state_words * 4;
+    st = ensure_buffer(ctx, reinterpret_cast<void**>(&ctx->k3_state), &have,
+                       (size_t)P * (1 + (L + 2)) * 4, true, 0, "spl_reserve");
+    if (st) return st;
+    ctx->k3_state_words = have / 4;
+    if (d > 0) {
+        const size_t splits_max = ((size_t)k + 1 + 63) / 64 + 1;
+        st = ensure_buffer(ctx, reinterpret_cast<void**>(&ctx->att_ws), &ctx->att_ws_bytes,
+                           (size_t)P * splits_max * (d + 2) * 4, false, 0, "spl_reserve");
+        if (st) return st;
+        have = ctx->att_counters_n * 4;
+        st = ensure_buffer(ctx, reinterpret_cast<void**>(&ctx->att_counters), &have,
+                           (size_t)P * 4, true, 0, "spl_reserve");
+        if (st) return st;
+        ctx->att_counters_n = have / 4;
+    }
+    return SPL_OK;
+}
+
+spl_status spl_check_device_error(spl_ctx* ctx, void* stream) {
+    if (!ctx) return SPL_E_STATE;
+    uint32_t flags = 0;
+    SPL_CUDA_TRY(ctx, cudaMemcpyAsync(&flags, ctx->dev_err, 4, cudaMemcpyDeviceToHost, S(stream)));
+    SPL_CUDA_TRY(ctx, cudaStreamSynchronize(S(stream)));
+    SPL_CUDA_TRY(ctx, cudaMemsetAsync(ctx->dev_err, 0, 4, S(stream)));
+    SPL_CUDA_TRY(ctx, cudaStreamSynchronize(S(stream)));
+    if (flags & SPL_DEV_ERR_NUMERIC)
+        return fail(ctx, SPL_E_NUMERIC, "mlp input contains non-finite values");
+    if (flags & SPL_DEV_ERR_DIMENSION)
+        return fail(ctx, SPL_E_DIMENSION, "attention: causal offset outside the cache");
+    return SPL_OK;
+}
+
+spl_status spl_device_alloc(spl_ctx* ctx, size_t bytes, void** out) {
+    if (!out) return SPL_E_STATE;
+    SPL_CUDA_TRY(ctx, cudaMalloc(out, bytes ? bytes : 1));
+    return SPL_OK;
+}
+spl_status spl_device_free(spl_ctx* ctx, void* p) {
+    SPL_CUDA_TRY(ctx, cudaFree(p));
+    return SPL_OK;
+}
+spl_status spl_memcpy(spl_ctx* ctx, void* dst, const void* src, size_t bytes, void* stream) {
+    if (bytes == 0) return SPL_OK;
+    SPL_CUDA_TRY(ctx, cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, S(stream)));
+    return SPL_OK;
+}
+spl_status spl_memset(spl_ctx* ctx, void* dst, int value, size_t bytes, void* stream) {
+    if (bytes == 0) return SPL_OK;
+    SPL_CUDA_TRY(ctx, cudaMemsetAsync(dst, value, bytes, S(stream)));
+    return SPL_OK;
+}
+spl_status spl_stream_synchronize(spl_ctx* ctx, void* stream) {
+    SPL_CUDA_TRY(ctx, cudaStreamSynchronize(S(stream)));
+    return SPL_OK;
+}
+
+// ------------------------------------------------------------ bitcodes
+spl_status spl_pack_bits(spl_ctx* ctx, const uint8_t* bits, uint64_t n, uint32_t L,
+                         uint32_t* codes, void* stream) {
+    if (!ctx) return SPL_E_STATE;
+    if (L == 0 || L % 32 != 0)
+        return fail(ctx, SPL_E_DIMENSION,
+                    "pack_bits: column count " + std::to_string(L) +
+                        " must be a positive multiple of 32");
+    if (spl_status st = check_L(ctx, "pack_bits", L)) return st;
+    return pack_bits_launch(ctx, bits, n, L, codes, S(stream));
+}
+
+spl_status spl_unpack_bits(spl_ctx* ctx, const uint32_t* codes, uint64_t n, uint32_t L,
+                           uint8_t* bits, void* stream) {
+    if (!ctx) return SPL_E_STATE;
+    if (spl_status st = check_L(ctx, "unpack_bits", L)) return st;
+    return unpack_bits_launch(ctx, codes, n, L, bits, S(stream));
+}
+
+spl_status spl_nxor_scores(spl_ctx* ctx, const uint32_t* codes, uint64_t problem_stride_rows,
+                           uint32_t L, const uint32_t* qcodes, uint32_t P,
+                           const uint32_t* n_valid, uint32_t nvalid_div, uint64_t n_max,
+                           int32_t* scores, uint64_t scores_stride, void* stream) {
+    if (!ctx) return SPL_E_STATE;
+    if (spl_status st = check_L(ctx, "nxor_scores", L)) return st;
+    if (nvalid_div == 0) return fail(ctx, SPL_E_DIMENSION, "nxor_scores: nvalid_div == 0");
+    return nxor_scores_launch(ctx, codes, problem_stride_rows, L, qcodes, P, n_valid, nvalid_div,
+                              n_max, scores, scores_stride, S(stream));
+}
+
+spl_status spl_top_k(spl_ctx* ctx, const void* scores, int dtype, uint32_t P, uint64_t n,
+                     uint64_t scores_stride, uint32_t k, uint32_t* idx, void* stream) {
+    if (!ctx) return SPL_E_STATE;
+    if (k == 0 || k > n)
+        return fail(ctx, SPL_E_DIMENSION,
+                    "top_k_indices: k=" + std::to_string(k) + " out of range for n=" +
+                        std::to_string(n));
+    return top_k_launch(ctx, scores, dtype, P, n, scores_stride, k, idx, S(stream));
+}
+
+// ------------------------------------------------------------ K3
+spl_status spl_hamming_topk(spl_ctx* ctx, const uint32_t* codes, uint64_t problem_stride_rows,
+                            uint32_t L, const uint32_t* qcodes, uint32_t P,
+                            const uint32_t* n_valid, uint32_t nvalid_div, uint64_t n_max,
+                            uint32_t k, uint32_t* idx, uint32_t* cnt, void* stream) {
+    return hamming_topk_impl(ctx, codes, problem_stride_rows, L, qcodes, P, n_valid, nvalid_div,
+                             n_max, k, idx, cnt, S(stream));
+}
+
+spl_status spl_shard_histogram(spl_ctx* ctx, const uint32_t* codes,
+                               uint64_t problem_stride_rows, uint32_t L,
+                               const uint32_t* qcodes, uint32_t P, const uint32_t* n_valid,
+                               uint32_t nvalid_div, uint64_t n_max, uint32_t* hist,
+                               void* stream) {
+    return shard_histogram_impl(ctx, codes, problem_stride_rows, L, qcodes, P, n_valid,
+                                nvalid_div, n_max, hist, S(stream));
+}
+
+spl_status spl_shard_select(spl_ctx* ctx, const uint32_t* all_hist, uint32_t R, uint32_t rank,
+                            uint32_t L, uint32_t P, const uint32_t* n_valid,
+                            uint32_t nvalid_div, uint64_t n_max, uint32_t k, uint32_t* idx,
+                            uint32_t* cnt, uint32_t* out_offset, void* stream) {
+    return shard_select_impl(ctx, all_hist, R, rank, L, P, n_valid, nvalid_div, n_max, k, idx,
+                             cnt, out_offset, S(stream));
+}
+
+// ------------------------------------------------------------ encoders
+spl_status spl_hasher_create(spl_ctx* ctx, int kind, uint32_t H, uint32_t d, uint32_t h,
+                             uint32_t L, const float* w1, const float* b1, const float* w2,
+                             spl_hasher** out) {
+    if (!ctx || !out) return SPL_E_STATE;
+    *out = nullptr;
+    if (kind != SPL_HASHER_MLP && kind != SPL_HASHER_LINEAR)
+        return fail(ctx, SPL_E_DIMENSION, "hasher: unknown kind");
+    if (H == 0 || d == 0 || (kind == SPL_HASHER_MLP && h == 0))
+        return fail(ctx, SPL_E_DIMENSION, "mlp_gaussian_init: dimensions must be >= 1");
+    if (spl_status st = check_L(ctx, "pack_bits", L)) return st;
+    if (!w1 || (kind == SPL_HASHER_MLP && (!b1 || !w2)))
+        return fail(ctx, SPL_E_STATE, "hasher: null weight pointer");
+    const size_t n1 = (size_t)H * d * (kind == SPL_HASHER_MLP ? h : L);
+    const size_t nb = kind == SPL_HASHER_MLP ? (size_t)H * h : 0;
+    const size_t n2 = kind == SPL_HASHER_MLP ? (size_t)H * h * L : 0;
+    // require_finite (hashers.cpp:14-17, :90-95) on a host copy
+    std::vector<float> h1(n1), hb(nb), h2(n2);
+    SPL_CUDA_TRY(ctx, cudaMemcpy(h1.data(), w1, n1 * 4, cudaMemcpyDefault));
+    if (nb) SPL_CUDA_TRY(ctx, cudaMemcpy(hb.data(), b1, nb * 4, cudaMemcpyDefault));
+    if (n2) SPL_CUDA_TRY(ctx, cudaMemcpy(h2.data(), w2, n2 * 4, cudaMemcpyDefault));
+    for (float v : h1)
+        if (!std::isfinite(v)) return fail(ctx, SPL_E_NUMERIC, "mlp w1 contains non-finite values");
+    for (float v : h2)
+        if (!std::isfinite(v)) return fail(ctx, SPL_E_NUMERIC, "mlp w2 contains non-finite values");
+    for (float v : hb)
+        if (!std::isfinite(v)) return fail(ctx, SPL_E_NUMERIC, "mlp b1 is non-finite");
+    spl_hasher* hs = new spl_hasher;
+    hs->kind = kind;
+    hs->H = H;
+    hs->d = d;
+    hs->h = kind == SPL_HASHER_MLP ? h : 0;
+    hs->L = L;
+    auto up = [&](float** dst, const std::vector<float>& src) -> bool {
+        if (src.empty()) return true;
+        if (cudaMalloc(dst, src.size() * 4) != cudaSuccess) return false;
+        return cudaMemcpy(*dst, src.data(), src.size() * 4, cudaMemcpyHostToDevice) == cudaSuccess;
+    };
+    if (!up(&hs->w1, h1) || !up(&hs->b1, hb) || !up(&hs->w2, h2)) {
+        spl_hasher_destroy(hs);
+        return fail(ctx, SPL_E_CUDA, "hasher: device allocation failed");
+    }
+    *out = hs;
+    return SPL_OK;
+}
+
+void spl_hasher_destroy(spl_hasher* hs) {
+    if (!hs) return;
+    cudaFree(hs->w1);
+    cudaFree(hs->b1);
+    cudaFree(hs->w2);
+    cudaFree(hs->w1_tc);
+    cudaFree(hs->w2_tc);
+    delete hs;
+}
+
+spl_status spl_mlp_forward(spl_ctx* ctx, const spl_hasher* hs, const float* x, uint32_t B,
+                           uint32_t m, float* pre, void* stream) {
+    if (!ctx || !hs) return SPL_E_STATE;
+    EncJob j{};
+    j.x = x;
+    j.m = m;
+    j.out_mode = ENC_PRE;
+    j.pre = pre;
+    return encode_exact_launch(ctx, hs, B, &j, 1, S(stream));
+}
+
+spl_status spl_encode(spl_ctx* ctx, const spl_hasher* hs, const float* x, uint32_t B, uint32_t m,
+                      int mode, uint32_t* codes, void* stream) {
+    if (!ctx || !hs) return SPL_E_STATE;
+    if (mode == SPL_ENCODE_TC) return encode_tc_launch(ctx, hs, x, B, m, codes, S(stream));
+    if (mode != SPL_ENCODE_EXACT) return fail(ctx, SPL_E_DIMENSION, "encode: unknown mode");
+    EncJob j{};
+    j.x = x;
+    j.m = m;
+    j.out_mode = ENC_CODES;
+    j.codes = codes;
+    return encode_exact_launch(ctx, hs, B, &j, 1, S(stream));
+}
+
+spl_status spl_encode_append(spl_ctx* ctx, const spl_hasher* hs, const float* k_new,
+                             const float* v_new, uint32_t B, uint32_t* codes, void* kcache,
+                             void* vcache, int kv_dtype, uint64_t cap, const uint32_t* pos,
+                             void* stream) {
+    if (!ctx || !hs) return SPL_E_STATE;
+    if (kv_dtype != SPL_F32 && kv_dtype != SPL_BF16)
+        return fail(ctx, SPL_E_DIMENSION, "encode_append: unknown kv dtype");
+    EncJob j{};
+    j.x = k_new;
+    j.m = 1;
+    j.out_mode = ENC_APPEND;
+    j.codes = codes;
+    j.cap = cap;
+    j.pos = pos;
+    j.v_new = v_new;
+    j.kcache = kcache;
+    j.vcache = vcache;
+    j.kv_dtype = kv_dtype;
+    return encode_exact_launch(ctx, hs, B, &j, 1, S(stream));
+}
+
+// ------------------------------------------------------------ attention
+spl_status spl_sparse_attend(spl_ctx* ctx, const float* q, const void* kcache,
+                             const void* vcache, int kv_dtype, uint64_t problem_stride_rows,
+                             uint32_t d, uint32_t P, const uint32_t* idx, uint64_t idx_stride,
+                             const uint32_t* cnt, const uint32_t* n_valid, uint32_t nvalid_div,
+                             float scale, float* out, void* stream) {
+    if (!ctx) return SPL_E_STATE;
+    if (!(scale > 0.0f)) return fail(ctx, SPL_E_DIMENSION, "attention: scale must be positive");
+    if (nvalid_div == 0) return fail(ctx, SPL_E_DIMENSION, "sparse_attend: nvalid_div == 0");
+    AttParams prm{};
+    prm.q = q;
+    prm.kc = kcache;
+    prm.vc = vcache;
+    prm.stride_rows = problem_stride_rows;
+    prm.d = d;
+    prm.P = P;
+    prm.idx = idx;
+    prm.idx_stride = idx_stride;
+    prm.cnt = cnt;
+    prm.n_valid = n_valid;
+    prm.nvalid_div = nvalid_div;
+    prm.qscale = scale * kLog2e;
+    prm.out = out;
+    prm.partial_mode = 0;
+    return sparse_attend_launch(ctx, prm, (uint32_t)idx_stride, kv_dtype, S(stream));
+}
+
+spl_status spl_sparse_attend_partial(spl_ctx* ctx, const float* q, const void* kcache,
+                                     const void* vcache, int kv_dtype,
+                                     uint64_t problem_stride_rows, uint32_t d, uint32_t P,
+                                     const uint32_t* idx, uint64_t idx_stride,
+                                     const uint32_t* cnt, const uint32_t* own_row,
+                                     uint32_t nvalid_div, float scale, float* partials,
+                                     void* stream) {
+    if (!ctx) return SPL_E_STATE;
+    if (!(scale > 0.0f)) return fail(ctx, SPL_E_DIMENSION, "attention: scale must be positive");
+    AttParams prm{};
+    prm.q = q;
+    prm.kc = kcache;
+    prm.vc = vcache;
+    prm.stride_rows = problem_stride_rows;
+    prm.d = d;
+    prm.P = P;
+    prm.idx = idx;
+    prm.idx_stride = idx_stride;
+    prm.cnt = cnt;
+    prm.own_row = own_row;
+    prm.nvalid_div = nvalid_div ? nvalid_div : 1;
+    prm.qscale = scale * kLog2e;
+    prm.out = partials;
+    prm.partial_mode = 1;
+    return sparse_attend_launch(ctx, prm, (uint32_t)idx_stride, kv_dtype, S(stream));
+}
+
+spl_status spl_attend_combine(spl_ctx* ctx, const float* partials, uint32_t R, uint32_t P,
+                              uint32_t d, float* out, void* stream) {
+    if (!ctx) return SPL_E_STATE;
+    return attend_combine_launch(ctx, partials, R, P, d, out, S(stream));
+}
+
+// ------------------------------------------------------------ decode step
+spl_status spl_decode_step(spl_ctx* ctx, const spl_hasher* hs, const float* q,
+                           const float* k_new, const float* v_new, uint32_t B,
+                           uint32_t* codes, void* kcache, void* vcache, int kv_dtype,
+                           uint64_t cap, const uint32_t* n_valid, uint64_t n_max, uint32_t k,
+                           float scale, uint32_t* idx, uint32_t* cnt, float* out, void* stream) {
+    if (!ctx || !hs) return SPL_E_STATE;
+    const uint32_t H = hs->H, W = hs->L / 32, P = B * H;
+    // query codes live in the context scratch
+    spl_status st = ensure_buffer(ctx, &ctx->scratch, &ctx->scratch_bytes,
+                                  (size_t)P * W * 4 + 4 * (size_t)B, false, S(stream),
+                                  "decode_step");
+    if (st) return st;
+    uint32_t* qcodes = static_cast<uint32_t*>(ctx->scratch);
+    // the appended key goes to slot n_valid[b] - 1 (its own token)
+    EncJob jobs[2]{};
+    jobs[0].x = k_new;
+    jobs[0].m = 1;
+    jobs[0].out_mode = ENC_APPEND;
+    jobs[0].codes = codes;
+    jobs[0].cap = cap;
+    jobs[0].pos = n_valid;
+    jobs[0].pos_minus_one = 1;
+    jobs[0].v_new = v_new;
+    jobs[0].kcache = kcache;
+    jobs[0].vcache = vcache;
+    jobs[0].kv_dtype = kv_dtype;
+    jobs[1].x = q;
+    jobs[1].m = 1;
+    jobs[1].out_mode = ENC_CODES;
+    jobs[1].codes = qcodes;
+    (void)W;
+    if ((st = encode_exact_launch(ctx, hs, B, jobs, 2, S(stream)))) return st;
+    if ((st = hamming_topk_impl(ctx, codes, cap, hs->L, qcodes, P, n_valid, H, n_max, k, idx,
+                                cnt, S(stream))))
+        return st;
+    return spl_sparse_attend(ctx, q, kcache, vcache, kv_dtype, cap, hs->d, P, idx, k, cnt,
+                             n_valid, H, scale, out, stream);
+}
+
+spl_status spl_budget_from_rate(double rate, uint64_t n, uint32_t* k) {
+    if (!k) return SPL_E_STATE;
+    if (!(rate > 0.0 && rate <= 1.0)) return SPL_E_DIMENSION;
+    const uint32_t raw = (uint32_t)(rate * (double)n);
+    const uint64_t kk = raw > 20 ? raw : 20;
+    *k = (uint32_t)(kk < n ? kk : n);
+    return SPL_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,121 @@
+// Internal shared definitions for the sm_100a kernels behind include/spl_c.h.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+
+#include "../../include/spl_c.h"
+
+#define SPL_DEV_ERR_NUMERIC 1u
+#define SPL_DEV_ERR_DIMENSION 2u
+
+// One context per caller (see spl_c.h). Owns the workspace and the device
+// error word. Workspace regions are sized by spl_reserve or lazily (never
+// during stream capture).
+struct spl_ctx {
+    int device = 0;
+    int num_sms = 148;
+    std::string err;
+    uint64_t launches = 0;
+
+    uint32_t* dev_err = nullptr;  // device error word (bit flags above)
+
+    // K3 workspace: scores + segment records + per-segment plans.
+    void* k3_ws = nullptr;
+    size_t k3_ws_bytes = 0;
+    // K3 per-problem persistent state, zero between launches (self-resetting):
+    // counters[P] + total histograms [P][Lmax+2].
+    uint32_t* k3_state = nullptr;
+    size_t k3_state_words = 0;
+
+    // K4 workspace: partials [P][splits][d+2] + per-problem counters.
+    float* att_ws = nullptr;
+    size_t att_ws_bytes = 0;
+    uint32_t* att_counters = nullptr;
+    size_t att_counters_n = 0;
+
+    // generic scratch for encoders / top_k keys.
+    void* scratch = nullptr;
+    size_t scratch_bytes = 0;
+
+    // last shard-histogram geometry (the select phase reuses its records).
+    uint64_t shard_n_max = 0;
+    uint32_t shard_P = 0, shard_L = 0, shard_G = 0;
+    uint64_t shard_S = 0;
+};
+
+struct spl_hasher {
+    int kind = SPL_HASHER_MLP;
+    uint32_t H = 0, d = 0, h = 0, L = 0;
+    float* w1 = nullptr;  // [H][d][h]  (linear: projection [H][d][L])
+    float* b1 = nullptr;  // [H][h]
+    float* w2 = nullptr;  // [H][h][L]
+    // bf16 copies for the tcgen05 bulk encoder (K-major packing, see encode_tc.cu)
+    void* w1_tc = nullptr;
+    void* w2_tc = nullptr;
+};
+
+namespace spl {
+
+inline spl_status fail(spl_ctx* ctx, spl_status st, const std::string& msg) {
+    if (ctx) ctx->err = msg;
+    return st;
+}
+
+inline spl_status cuda_fail(spl_ctx* ctx, cudaError_t e, const char* where) {
+    return fail(ctx, SPL_E_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+#define SPL_CUDA_TRY(ctx, expr)                                          \
+    do {                                                                 \
+        cudaError_t _e = (expr);                                         \
+        if (_e != cudaSuccess) return ::spl::cuda_fail((ctx), _e, #expr); \
+    } while (0)
+
+// After a launch: count it, surface launch-config errors.
+inline spl_status after_launch(spl_ctx* ctx, const char* name) {
+    ctx->launches++;
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(ctx, e, name);
+    return SPL_OK;
+}
+
+inline bool stream_capturing(cudaStream_t s) {
+    cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(s, &st) != cudaSuccess) return false;
+    return st != cudaStreamCaptureStatusNone;
+}
+
+// Grow a device buffer to at least `bytes` (zero-filled when `zero`).
+spl_status ensure_buffer(spl_ctx* ctx, void** buf, size_t* have, size_t bytes, bool zero,
+                         cudaStream_t s, const char* what);
+
+__device__ __forceinline__ void raise_dev_err(uint32_t* e, uint32_t flag) {
+    if (e) atomicOr(e, flag);
+}
+
+// Streaming 128-bit load: read-only path, no L1 allocation, L2 evict-first
+// (the code cache is read once per step; keep L2 for scores/plans/weights).
+__device__ __forceinline__ uint4 ld_stream_v4(const uint4* p) {
+    uint4 r;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::evict_first.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(p));
+    return r;
+}
+__device__ __forceinline__ uint2 ld_stream_v2(const uint2* p) {
+    uint2 r;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::evict_first.v2.u32 {%0,%1}, [%2];"
+                 : "=r"(r.x), "=r"(r.y)
+                 : "l"(p));
+    return r;
+}
+__device__ __forceinline__ uint32_t ld_stream_u32(const uint32_t* p) {
+    uint32_t r;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::evict_first.u32 %0, [%1];" : "=r"(r) : "l"(p));
+    return r;
+}
+
+}  // namespace spl

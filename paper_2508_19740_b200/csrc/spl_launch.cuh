@@ -1,0 +1,76 @@
+// Launch-level interfaces shared between the kernel files and capi.cu.
+#pragma once
+#include "spl_internal.cuh"
+
+namespace spl {
+
+enum EncOut { ENC_CODES = 0, ENC_PRE = 1, ENC_APPEND = 2 };
+
+struct EncJob {
+    const float* x;       // [B][H][m][d]
+    uint32_t m;
+    int out_mode;
+    uint32_t* codes;      // ENC_CODES: [B][H][m][W]; ENC_APPEND: [B][H][cap][W]
+    float* pre;           // ENC_PRE: [B][H][m][L]
+    uint64_t cap;
+    const uint32_t* pos;  // ENC_APPEND: slot per batch (pos[b] - pos_minus_one)
+    int pos_minus_one;    // 1: pos holds n_valid (slot = n_valid - 1)
+    const float* v_new;   // ENC_APPEND: copy k/v rows into the caches
+    void* kcache;
+    void* vcache;
+    int kv_dtype;
+};
+
+struct AttParams {
+    const float* q;
+    const void* kc;
+    const void* vc;
+    uint64_t stride_rows;
+    uint32_t d;
+    uint32_t P;
+    const uint32_t* idx;
+    uint64_t idx_stride;
+    const uint32_t* cnt;
+    const uint32_t* n_valid;   // own = n_valid[p / div] - 1   (normal mode)
+    const uint32_t* own_row;   // own row per problem, ~0u = none (partial mode)
+    uint32_t nvalid_div;
+    float qscale;              // scale * log2(e)
+    uint32_t rows_per_split;
+    uint32_t nsplit;
+    float* partials;           // [P][nsplit][d + 2]
+    uint32_t* counters;        // [P]
+    float* out;                // normal: [P][d]; partial mode: [P][d + 2] (m, l, o)
+    int partial_mode;
+};
+
+// hamming_topk.cu
+spl_status hamming_topk_impl(spl_ctx*, const uint32_t*, uint64_t, uint32_t, const uint32_t*,
+                             uint32_t, const uint32_t*, uint32_t, uint64_t, uint32_t, uint32_t*,
+                             uint32_t*, cudaStream_t);
+spl_status shard_histogram_impl(spl_ctx*, const uint32_t*, uint64_t, uint32_t, const uint32_t*,
+                                uint32_t, const uint32_t*, uint32_t, uint64_t, uint32_t*,
+                                cudaStream_t);
+spl_status shard_select_impl(spl_ctx*, const uint32_t*, uint32_t, uint32_t, uint32_t, uint32_t,
+                             const uint32_t*, uint32_t, uint64_t, uint32_t, uint32_t*, uint32_t*,
+                             uint32_t*, cudaStream_t);
+// bitcodes_misc.cu
+spl_status pack_bits_launch(spl_ctx*, const uint8_t*, uint64_t, uint32_t, uint32_t*, cudaStream_t);
+spl_status unpack_bits_launch(spl_ctx*, const uint32_t*, uint64_t, uint32_t, uint8_t*,
+                              cudaStream_t);
+spl_status nxor_scores_launch(spl_ctx*, const uint32_t*, uint64_t, uint32_t, const uint32_t*,
+                              uint32_t, const uint32_t*, uint32_t, uint64_t, int32_t*, uint64_t,
+                              cudaStream_t);
+spl_status top_k_launch(spl_ctx*, const void*, int, uint32_t, uint64_t, uint64_t, uint32_t,
+                        uint32_t*, cudaStream_t);
+// encode_exact.cu
+spl_status encode_exact_launch(spl_ctx*, const spl_hasher*, uint32_t, const EncJob*, int,
+                               cudaStream_t);
+// encode_tc.cu
+spl_status encode_tc_launch(spl_ctx*, const spl_hasher*, const float*, uint32_t, uint32_t,
+                            uint32_t*, cudaStream_t);
+// sparse_attend.cu
+spl_status sparse_attend_launch(spl_ctx*, AttParams, uint32_t, int, cudaStream_t);
+spl_status attend_combine_launch(spl_ctx*, const float*, uint32_t, uint32_t, uint32_t, float*,
+                                 cudaStream_t);
+
+}  // namespace spl

@@ -1,0 +1,350 @@
+"""ctypes bindings for the CPU checkers (TEST INFRASTRUCTURE ONLY).
+
+* ``Oracle``  -> oracle/liboracle.so, the C restatement (always built).
+* ``RefLib``  -> oracle/_ref/libspotref.so, the unmodified reference sources
+  compiled by oracle/Makefile (absent when /root/reference was never
+  present; callers skip).
+
+Only tests/, __graft_entry__.smoke() and bench.py's CPU legs import this.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parents[1]
+ORACLE_SO = ROOT / "oracle" / "liboracle.so"
+REF_SO = ROOT / "oracle" / "_ref" / "libspotref.so"
+
+u8p = np.ctypeslib.ndpointer(np.uint8, flags="C_CONTIGUOUS")
+u32p = np.ctypeslib.ndpointer(np.uint32, flags="C_CONTIGUOUS")
+u64p = np.ctypeslib.ndpointer(np.uint64, flags="C_CONTIGUOUS")
+i32p = np.ctypeslib.ndpointer(np.int32, flags="C_CONTIGUOUS")
+f32p = np.ctypeslib.ndpointer(np.float32, flags="C_CONTIGUOUS")
+
+
+class CheckerError(RuntimeError):
+    def __init__(self, code, msg=""):
+        super().__init__(f"status {code}: {msg}")
+        self.code = code
+        self.msg = msg
+
+
+def _c(a, dt):
+    return np.ascontiguousarray(a, dtype=dt)
+
+
+def build_checkers():
+    """make -C oracle (liboracle.so always; _ref when /root/reference exists)."""
+    import subprocess
+
+    subprocess.run(["make", "-s", "-C", str(ROOT / "oracle")], check=True)
+
+
+class _Base:
+    prefix = ""
+
+    def _err(self, code):
+        return CheckerError(code, "")
+
+    def _chk(self, code):
+        if code != 0:
+            raise self._err(code)
+
+
+class Oracle(_Base):
+    """The C restatement (oracle/spl_oracle.c)."""
+
+    def __init__(self, path: Path = ORACLE_SO):
+        if not path.exists():
+            build_checkers()
+        L = self.lib = C.CDLL(str(path))
+        L.orc_pack_bits.argtypes = [u8p, C.c_uint32, C.c_uint32, u32p]
+        L.orc_unpack_bits.argtypes = [u32p, C.c_uint32, C.c_uint32, u8p]
+        L.orc_nxor_scores_into.argtypes = [u32p, C.c_uint32, u32p, C.c_uint32, C.c_uint32,
+                                           C.c_uint32, i32p]
+        L.orc_top_k_i32.argtypes = [i32p, C.c_uint32, C.c_uint32, u32p]
+        L.orc_top_k_f32.argtypes = [f32p, C.c_uint32, C.c_uint32, u32p]
+        L.orc_mlp_forward.argtypes = [f32p, f32p, f32p, C.c_uint32, C.c_uint32, C.c_uint32,
+                                      f32p, C.c_uint32, f32p]
+        L.orc_mlp_hash_packed.argtypes = [f32p, f32p, f32p, C.c_uint32, C.c_uint32,
+                                          C.c_uint32, f32p, C.c_uint32, u32p]
+        L.orc_linear_hash_packed.argtypes = [f32p, C.c_uint32, C.c_uint32, f32p, C.c_uint32,
+                                             u32p]
+        L.orc_budget_from_rate.argtypes = [C.c_double, C.c_uint64, C.POINTER(C.c_int)]
+        L.orc_budget_from_rate.restype = C.c_uint32
+        L.orc_sparse_attention.argtypes = [f32p, C.c_uint32, f32p, f32p, C.c_uint32,
+                                           C.c_uint32, C.c_float, u32p, u32p, u64p, f32p]
+        L.orc_retrieve_batch.argtypes = [u32p, C.c_uint32, C.c_uint64, C.c_uint32, u32p, u32p,
+                                         C.c_uint32, u32p, C.c_int]
+
+    # -- bitcodes
+    def pack_bits(self, bits):
+        bits = _c(bits, np.uint8)
+        n, d = bits.shape
+        out = np.zeros((n, max(d // 32, 1)), np.uint32)
+        self._chk(self.lib.orc_pack_bits(bits, n, d, out))
+        return out
+
+    def unpack_bits(self, words, L):
+        words = _c(words, np.uint32)
+        n = words.shape[0]
+        out = np.zeros((n, L), np.uint8)
+        self._chk(self.lib.orc_unpack_bits(words, n, L, out))
+        return out
+
+    def nxor_scores(self, q, codes, n_valid=None):
+        q = _c(q, np.uint32).ravel()
+        codes = _c(codes, np.uint32)
+        n, W = codes.shape
+        nv = n if n_valid is None else n_valid
+        out = np.zeros(max(nv, 1), np.int32)
+        self._chk(self.lib.orc_nxor_scores_into(q, q.size, codes, n, W * 32, nv, out))
+        return out[:nv]
+
+    def top_k(self, scores, k):
+        if np.asarray(scores).dtype.kind == "f":
+            s = _c(scores, np.float32)
+            out = np.zeros(max(k, 1), np.uint32)
+            self._chk(self.lib.orc_top_k_f32(s, s.size, k, out))
+        else:
+            s = _c(scores, np.int32)
+            out = np.zeros(max(k, 1), np.uint32)
+            self._chk(self.lib.orc_top_k_i32(s, s.size, k, out))
+        return out[:k]
+
+    # -- hashers
+    def mlp_forward(self, w1, b1, w2, x):
+        w1, b1, w2, x = _c(w1, np.float32), _c(b1, np.float32), _c(w2, np.float32), _c(x, np.float32)
+        d, h = w1.shape
+        L = w2.shape[1]
+        m = x.shape[0]
+        out = np.zeros((m, L), np.float32)
+        self._chk(self.lib.orc_mlp_forward(w1, b1, w2, d, h, L, x, m, out))
+        return out
+
+    def mlp_hash_packed(self, w1, b1, w2, x):
+        w1, b1, w2, x = _c(w1, np.float32), _c(b1, np.float32), _c(w2, np.float32), _c(x, np.float32)
+        d, h = w1.shape
+        L = w2.shape[1]
+        m = x.shape[0]
+        out = np.zeros((m, L // 32), np.uint32)
+        self._chk(self.lib.orc_mlp_hash_packed(w1, b1, w2, d, h, L, x, m, out))
+        return out
+
+    def linear_hash_packed(self, proj, x):
+        proj, x = _c(proj, np.float32), _c(x, np.float32)
+        d, L = proj.shape
+        out = np.zeros((x.shape[0], L // 32), np.uint32)
+        self._chk(self.lib.orc_linear_hash_packed(proj, d, L, x, x.shape[0], out))
+        return out
+
+    # -- attention_eval
+    def budget_from_rate(self, rate, n):
+        st = C.c_int(0)
+        k = self.lib.orc_budget_from_rate(rate, n, C.byref(st))
+        self._chk(st.value)
+        return k
+
+    def sparse_attention(self, queries, keys, values, scale, offsets, picked_lists):
+        queries, keys, values = _c(queries, np.float32), _c(keys, np.float32), _c(values, np.float32)
+        q, d = queries.shape
+        n = keys.shape[0]
+        offs = _c(offsets, np.uint32)
+        flat = np.concatenate([np.asarray(p, np.uint32) for p in picked_lists] + [np.zeros(0, np.uint32)])
+        po = np.zeros(q + 1, np.uint64)
+        po[1:] = np.cumsum([len(p) for p in picked_lists])
+        flat = _c(flat if flat.size else np.zeros(1, np.uint32), np.uint32)
+        out = np.zeros((q, d), np.float32)
+        self._chk(self.lib.orc_sparse_attention(queries, q, keys, values, n, d, scale, offs, flat,
+                                                po, out))
+        return out
+
+    def retrieve_batch(self, codes, qcodes, n_valid, k, threads=None):
+        """codes [P][cap][W], qcodes [P][W], n_valid [P] -> out [P][k] (0-padded)."""
+        codes = _c(codes, np.uint32)
+        P, cap, W = codes.shape
+        out = np.zeros((P, k), np.uint32)
+        self._chk(self.lib.orc_retrieve_batch(codes, P, cap, W * 32, _c(qcodes, np.uint32),
+                                              _c(n_valid, np.uint32), k, out,
+                                              threads or os.cpu_count() or 1))
+        return out
+
+
+class RefLib(_Base):
+    """The unmodified reference (oracle/_ref/libspotref.so)."""
+
+    @staticmethod
+    def available() -> bool:
+        return REF_SO.exists()
+
+    def __init__(self, path: Path = REF_SO):
+        L = self.lib = C.CDLL(str(path))
+        L.spotref_last_error.restype = C.c_char_p
+        L.spotref_max_threads.restype = C.c_int
+        L.spotref_derive_seed.argtypes = [C.c_uint64, C.c_uint64]
+        L.spotref_derive_seed.restype = C.c_uint64
+        L.spotref_mlp_gaussian_init.argtypes = [C.c_uint32, C.c_uint32, C.c_uint32, C.c_float,
+                                                C.c_uint64, f32p, f32p, f32p]
+        L.spotref_qr_rotation_init.argtypes = [C.c_uint32, C.c_uint64, f32p]
+        L.spotref_pack_bits.argtypes = [u8p, C.c_uint32, C.c_uint32, u32p]
+        L.spotref_unpack_bits.argtypes = [u32p, C.c_uint32, C.c_uint32, u8p]
+        L.spotref_nxor_scores_into.argtypes = [u32p, C.c_uint32, u32p, C.c_uint32, C.c_uint32,
+                                               C.c_uint32, i32p]
+        L.spotref_top_k_i32.argtypes = [i32p, C.c_uint32, C.c_uint32, u32p]
+        L.spotref_top_k_f32.argtypes = [f32p, C.c_uint32, C.c_uint32, u32p]
+        L.spotref_mlp_forward.argtypes = [f32p, f32p, f32p, C.c_uint32, C.c_uint32, C.c_uint32,
+                                          f32p, C.c_uint32, f32p]
+        L.spotref_mlp_hash_packed.argtypes = [f32p, f32p, f32p, C.c_uint32, C.c_uint32,
+                                              C.c_uint32, f32p, C.c_uint32, u32p]
+        L.spotref_linear_hash_packed.argtypes = [f32p, C.c_uint32, C.c_uint32, f32p, C.c_uint32,
+                                                 u32p]
+        L.spotref_budget_from_rate.argtypes = [C.c_double, C.c_uint64, C.POINTER(C.c_int)]
+        L.spotref_budget_from_rate.restype = C.c_uint32
+        L.spotref_sparse_attention.argtypes = [f32p, C.c_uint32, f32p, f32p, C.c_uint32,
+                                               C.c_uint32, C.c_float, u32p, u32p, u64p, f32p]
+        L.spotref_full_attention.argtypes = [f32p, C.c_uint32, f32p, f32p, C.c_uint32,
+                                             C.c_uint32, C.c_float, u32p, f32p]
+        L.spotref_hash_topk_mlp.argtypes = [f32p, f32p, f32p, C.c_uint32, C.c_uint32, f32p,
+                                            C.c_uint32, f32p, f32p, C.c_uint32, C.c_uint32,
+                                            C.c_float, u32p, C.c_uint32, u32p, u32p]
+        L.spotref_index_create.argtypes = [u32p, C.c_uint32, C.c_uint64, C.c_uint32, u32p,
+                                           C.POINTER(C.c_void_p)]
+        L.spotref_index_destroy.argtypes = [C.c_void_p]
+        L.spotref_retrieve_batch.argtypes = [C.c_void_p, u32p, u32p, C.c_uint32, u32p, C.c_int]
+
+    def _err(self, code):
+        return CheckerError(code, self.lib.spotref_last_error().decode())
+
+    def max_threads(self):
+        return self.lib.spotref_max_threads()
+
+    def derive_seed(self, base, stream):
+        return self.lib.spotref_derive_seed(base, stream)
+
+    def mlp_gaussian_init(self, d, h, L, gamma=64.0, seed=0):
+        w1 = np.zeros((d, h), np.float32)
+        b1 = np.zeros(h, np.float32)
+        w2 = np.zeros((h, L), np.float32)
+        self._chk(self.lib.spotref_mlp_gaussian_init(d, h, L, gamma, seed, w1, b1, w2))
+        return w1, b1, w2
+
+    def qr_rotation_init(self, d, seed):
+        p = np.zeros((d, d), np.float32)
+        self._chk(self.lib.spotref_qr_rotation_init(d, seed, p))
+        return p
+
+    def pack_bits(self, bits):
+        bits = _c(bits, np.uint8)
+        n, d = bits.shape
+        out = np.zeros((n, max(d // 32, 1)), np.uint32)
+        self._chk(self.lib.spotref_pack_bits(bits, n, d, out))
+        return out
+
+    def unpack_bits(self, words, L):
+        words = _c(words, np.uint32)
+        out = np.zeros((words.shape[0], L), np.uint8)
+        self._chk(self.lib.spotref_unpack_bits(words, words.shape[0], L, out))
+        return out
+
+    def nxor_scores(self, q, codes, n_valid=None):
+        q = _c(q, np.uint32).ravel()
+        codes = _c(codes, np.uint32)
+        n, W = codes.shape
+        nv = n if n_valid is None else n_valid
+        out = np.zeros(max(nv, 1), np.int32)
+        self._chk(self.lib.spotref_nxor_scores_into(q, q.size, codes, n, W * 32, nv, out))
+        return out[:nv]
+
+    def top_k(self, scores, k):
+        if np.asarray(scores).dtype.kind == "f":
+            s = _c(scores, np.float32)
+            out = np.zeros(max(k, 1), np.uint32)
+            self._chk(self.lib.spotref_top_k_f32(s, s.size, k, out))
+        else:
+            s = _c(scores, np.int32)
+            out = np.zeros(max(k, 1), np.uint32)
+            self._chk(self.lib.spotref_top_k_i32(s, s.size, k, out))
+        return out[:k]
+
+    def mlp_forward(self, w1, b1, w2, x):
+        w1, b1, w2, x = _c(w1, np.float32), _c(b1, np.float32), _c(w2, np.float32), _c(x, np.float32)
+        d, h = w1.shape
+        L = w2.shape[1]
+        out = np.zeros((x.shape[0], L), np.float32)
+        self._chk(self.lib.spotref_mlp_forward(w1, b1, w2, d, h, L, x, x.shape[0], out))
+        return out
+
+    def mlp_hash_packed(self, w1, b1, w2, x):
+        w1, b1, w2, x = _c(w1, np.float32), _c(b1, np.float32), _c(w2, np.float32), _c(x, np.float32)
+        d, h = w1.shape
+        L = w2.shape[1]
+        out = np.zeros((x.shape[0], L // 32), np.uint32)
+        self._chk(self.lib.spotref_mlp_hash_packed(w1, b1, w2, d, h, L, x, x.shape[0], out))
+        return out
+
+    def linear_hash_packed(self, proj, x):
+        proj, x = _c(proj, np.float32), _c(x, np.float32)
+        d, L = proj.shape
+        out = np.zeros((x.shape[0], L // 32), np.uint32)
+        self._chk(self.lib.spotref_linear_hash_packed(proj, d, L, x, x.shape[0], out))
+        return out
+
+    def budget_from_rate(self, rate, n):
+        st = C.c_int(0)
+        k = self.lib.spotref_budget_from_rate(rate, n, C.byref(st))
+        self._chk(st.value)
+        return k
+
+    def sparse_attention(self, queries, keys, values, scale, offsets, picked_lists):
+        queries, keys, values = _c(queries, np.float32), _c(keys, np.float32), _c(values, np.float32)
+        q, d = queries.shape
+        flat = np.concatenate([np.asarray(p, np.uint32) for p in picked_lists] + [np.zeros(0, np.uint32)])
+        po = np.zeros(q + 1, np.uint64)
+        po[1:] = np.cumsum([len(p) for p in picked_lists])
+        flat = _c(flat if flat.size else np.zeros(1, np.uint32), np.uint32)
+        out = np.zeros((q, d), np.float32)
+        self._chk(self.lib.spotref_sparse_attention(queries, q, keys, values, keys.shape[0], d,
+                                                    scale, _c(offsets, np.uint32), flat, po, out))
+        return out
+
+    def full_attention(self, queries, keys, values, scale, offsets):
+        queries, keys, values = _c(queries, np.float32), _c(keys, np.float32), _c(values, np.float32)
+        q, d = queries.shape
+        out = np.zeros((q, d), np.float32)
+        self._chk(self.lib.spotref_full_attention(queries, q, keys, values, keys.shape[0], d, scale,
+                                                  _c(offsets, np.uint32), out))
+        return out
+
+    def hash_topk_mlp(self, w1, b1, w2, queries, keys, values, scale, offsets, k):
+        w1, b1, w2 = _c(w1, np.float32), _c(b1, np.float32), _c(w2, np.float32)
+        queries, keys, values = _c(queries, np.float32), _c(keys, np.float32), _c(values, np.float32)
+        q, d = queries.shape
+        out = np.zeros((q, k), np.uint32)
+        cnt = np.zeros(q, np.uint32)
+        self._chk(self.lib.spotref_hash_topk_mlp(w1, b1, w2, w1.shape[1], w2.shape[1], queries, q,
+                                                 keys, values, keys.shape[0], d, scale,
+                                                 _c(offsets, np.uint32), k, out, cnt))
+        return [out[i, :cnt[i]].copy() for i in range(q)]
+
+    def index_create(self, codes, n_rows):
+        codes = _c(codes, np.uint32)
+        P, cap, W = codes.shape
+        h = C.c_void_p()
+        self._chk(self.lib.spotref_index_create(codes, P, cap, W * 32, _c(n_rows, np.uint32),
+                                                C.byref(h)))
+        return h
+
+    def index_destroy(self, h):
+        self.lib.spotref_index_destroy(h)
+
+    def retrieve_batch(self, handle, qcodes, n_valid, k, threads=None):
+        qcodes = _c(qcodes, np.uint32)
+        P = qcodes.shape[0]
+        out = np.zeros((P, k), np.uint32)
+        self._chk(self.lib.spotref_retrieve_batch(handle, qcodes, _c(n_valid, np.uint32), k, out,
+                                                  threads or os.cpu_count() or 1))
+        return out
