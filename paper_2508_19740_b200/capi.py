@@ -292,7 +292,8 @@ class Hasher:
         else:
             H, d, L = w1.shape
             h = 0
-        self.kind, self.H, self.d, self.h, self.L = kind, H, d, h, L
+        self.kind, self.H, self.d, self.hidden, self.L = kind, H, d, h, L
+        self.h = None
         out = C.c_void_p()
         ctx.check(ctx.lib.spl_hasher_create(ctx.h, kind, H, d, h, L, w1.ctypes.data,
                                             b1.ctypes.data if b1 is not None else None,

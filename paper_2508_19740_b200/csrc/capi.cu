@@ -255,7 +255,18 @@ spl_status spl_hasher_create(spl_ctx* ctx, int kind, uint32_t H, uint32_t d, uin
         if (cudaMalloc(dst, src.size() * 4) != cudaSuccess) return false;
         return cudaMemcpy(*dst, src.data(), src.size() * 4, cudaMemcpyHostToDevice) == cudaSuccess;
     };
-    if (!up(&hs->w1, h1) || !up(&hs->b1, hb) || !up(&hs->w2, h2)) {
+    // layer-2 (linear: projection) columns permuted [p][c*W + w] -> [p][w*32 + c]
+    // so the encoder's warp on word w reads 32 consecutive floats per step
+    const std::vector<float>& src2 = kind == SPL_HASHER_MLP ? h2 : h1;
+    const uint32_t rows2 = kind == SPL_HASHER_MLP ? h : d, W = L / 32;
+    std::vector<float> hp(src2.size());
+    for (uint32_t hd = 0; hd < H; ++hd)
+        for (uint32_t p = 0; p < rows2; ++p)
+            for (uint32_t c = 0; c < 32; ++c)
+                for (uint32_t w = 0; w < W; ++w)
+                    hp[((size_t)hd * rows2 + p) * L + w * 32 + c] =
+                        src2[((size_t)hd * rows2 + p) * L + c * W + w];
+    if (!up(&hs->w1, h1) || !up(&hs->b1, hb) || !up(&hs->w2, h2) || !up(&hs->w2_perm, hp)) {
         spl_hasher_destroy(hs);
         return fail(ctx, SPL_E_CUDA, "hasher: device allocation failed");
     }
@@ -268,6 +279,7 @@ void spl_hasher_destroy(spl_hasher* hs) {
     cudaFree(hs->w1);
     cudaFree(hs->b1);
     cudaFree(hs->w2);
+    cudaFree(hs->w2_perm);
     cudaFree(hs->w1_tc);
     cudaFree(hs->w2_tc);
     delete hs;

@@ -17,6 +17,7 @@
 #include <stdint.h>
 #include <cuda_bf16.h>
 
+#include <algorithm>
 #include <string>
 
 #include "spl_expf.cuh"
@@ -30,11 +31,14 @@ constexpr int kVT = 8;  // vectors per CTA
 struct EncParams {
     const float* w1;
     const float* b1;
-    const float* w2;
+    const float* w2p;  // layer-2 (or linear projection) weights, columns permuted
+                       // to [p][w][c] so lane c of the warp on word w reads
+                       // consecutive words (see spl_hasher_create)
     uint32_t H, d, h, L, W;
     int kind;
     uint32_t B;
-    EncJob job[2];  // blockIdx.z selects the job (decode step: key append + query)
+    int staged;        // weights staged in shared memory by TMA bulk copies
+    EncJob job[2];     // blockIdx.z selects the job (decode step: key append + query)
     uint32_t* dev_err;
 };
 
@@ -43,112 +47,174 @@ __device__ __forceinline__ float silu_exact(float z) {
     return __fdiv_rn(z, __fadd_rn(1.0f, e));
 }
 
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+// 1-D TMA bulk copy global -> shared, completion on an mbarrier.
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+        :: "r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+
 __global__ void __launch_bounds__(kEncThreads) k1_encode_exact(EncParams prm) {
-    extern __shared__ float esm[];
+    extern __shared__ __align__(128) float esm[];
+    __shared__ __align__(8) uint64_t s_bar;
+    __shared__ uint32_t s_bad;
     const EncJob& job = prm.job[blockIdx.z];
     const uint32_t head = blockIdx.y;
     const uint32_t d = prm.d, h = prm.h, L = prm.L, W = prm.W, H = prm.H;
     const uint32_t nvec = prm.B * job.m;
-    const uint32_t v0 = blockIdx.x * kVT;
-    if (v0 >= nvec) return;
-    const uint32_t nv = min((uint32_t)kVT, nvec - v0);
+    const uint32_t ntiles = (nvec + kVT - 1) / kVT;
+    if (blockIdx.x >= ntiles) return;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    float* xs = esm;                         // [kVT][d]
-    float* a1 = esm + (size_t)kVT * d;       // [kVT][h]
-    __shared__ uint32_t s_bad;
-    if (tid == 0) s_bad = 0;
-    __syncthreads();
+    const bool mlp = prm.kind == SPL_HASHER_MLP;
+    const uint32_t act_dim = mlp ? h : d;
+    const float* gw1 = prm.w1 + (uint64_t)head * d * h;
+    const float* gb1 = mlp ? prm.b1 + (uint64_t)head * h : nullptr;
+    const float* gw2 = prm.w2p + (uint64_t)head * act_dim * L;
+    // shared layout: [W1 d*h | W2p act_dim*L] (staged only) | xs [kVT][d] | a1 [kVT][h]
+    const size_t w1n = mlp ? (size_t)d * h : 0, w2n = (size_t)act_dim * L;
+    float* sw1 = esm;
+    float* sw2 = esm + w1n;
+    float* xs = prm.staged ? esm + w1n + w2n : esm;
+    float* a1 = xs + (size_t)kVT * d;
+    const float* w1 = prm.staged ? sw1 : gw1;
+    const float* w2 = prm.staged ? sw2 : gw2;
 
-    // stage the inputs (zero-fill unused vector slots)
-    for (uint32_t i = tid; i < kVT * d; i += kEncThreads) {
-        const uint32_t v = i / d, c = i % d;
-        float val = 0.0f;
-        if (v < nv) {
-            const uint32_t vg = v0 + v, b = vg / job.m, mi = vg % job.m;
-            val = job.x[(((uint64_t)b * H + head) * job.m + mi) * d + c];
-            if (!isfinite(val)) s_bad = 1;
+    if (prm.staged) {
+        if (tid == 0) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"(smem_u32(&s_bar)));
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+            const uint32_t bytes = (uint32_t)((w1n + w2n) * 4);
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
+                         :: "r"(smem_u32(&s_bar)), "r"(bytes) : "memory");
+            constexpr uint32_t kChunk = 32768;
+            for (uint32_t off = 0; off < w1n * 4; off += kChunk)
+                bulk_g2s(reinterpret_cast<char*>(sw1) + off, reinterpret_cast<const char*>(gw1) + off,
+                         min(kChunk, (uint32_t)(w1n * 4) - off), &s_bar);
+            for (uint32_t off = 0; off < w2n * 4; off += kChunk)
+                bulk_g2s(reinterpret_cast<char*>(sw2) + off, reinterpret_cast<const char*>(gw2) + off,
+                         min(kChunk, (uint32_t)(w2n * 4) - off), &s_bar);
         }
-        xs[i] = val;
     }
-    __syncthreads();
-    if (s_bad && tid == 0) raise_dev_err(prm.dev_err, SPL_DEV_ERR_NUMERIC);
+    bool weights_ready = !prm.staged;
 
-    const float* act = xs;
-    uint32_t act_dim = d;
-    const float* w2 = prm.w2 + (uint64_t)head * h * L;
-    if (prm.kind == SPL_HASHER_MLP) {
-        const float* w1 = prm.w1 + (uint64_t)head * d * h;
-        const float* b1 = prm.b1 + (uint64_t)head * h;
-        for (uint32_t j = tid; j < h; j += kEncThreads) {
+    for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const uint32_t v0 = tile * kVT;
+        const uint32_t nv = min((uint32_t)kVT, nvec - v0);
+        if (tid == 0) s_bad = 0;
+        __syncthreads();
+        // stage the inputs (zero-fill unused vector slots)
+        for (uint32_t i = tid; i < kVT * d; i += kEncThreads) {
+            const uint32_t v = i / d, c = i % d;
+            float val = 0.0f;
+            if (v < nv) {
+                const uint32_t vg = v0 + v, b = vg / job.m, mi = vg % job.m;
+                val = job.x[(((uint64_t)b * H + head) * job.m + mi) * d + c];
+                if (!isfinite(val)) s_bad = 1;
+            }
+            xs[i] = val;
+        }
+        if (!weights_ready) {
+            // wait for the TMA bulk copies (phase 0)
+            uint32_t done = 0;
+            while (!done) {
+                asm volatile(
+                    "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0; "
+                    "selp.u32 %0, 1, 0, p; }"
+                    : "=r"(done) : "r"(smem_u32(&s_bar)) : "memory");
+            }
+            weights_ready = true;
+        }
+        __syncthreads();
+        if (s_bad && tid == 0) raise_dev_err(prm.dev_err, SPL_DEV_ERR_NUMERIC);
+
+        const float* act = xs;
+        if (mlp) {
+            for (uint32_t j = tid; j < h; j += kEncThreads) {
+                float acc[kVT];
+#pragma unroll
+                for (int v = 0; v < kVT; ++v) acc[v] = 0.0f;
+#pragma unroll 8
+                for (uint32_t p = 0; p < d; ++p) {
+                    const float w = w1[(size_t)p * h + j];
+#pragma unroll
+                    for (int v = 0; v < kVT; ++v) acc[v] = __fmaf_rn(xs[v * d + p], w, acc[v]);
+                }
+                const float bj = __ldg(gb1 + j);
+#pragma unroll
+                for (int v = 0; v < kVT; ++v) a1[v * h + j] = silu_exact(__fadd_rn(acc[v], bj));
+            }
+            __syncthreads();
+            act = a1;
+        }
+
+        // layer 2 (or the linear projection) + sign + pack; warp w owns word w,
+        // lane c computes column c*W + w (read at the permuted offset w*32 + c)
+        for (uint32_t w = warp; w < W; w += kEncThreads / 32) {
             float acc[kVT];
 #pragma unroll
             for (int v = 0; v < kVT; ++v) acc[v] = 0.0f;
-#pragma unroll 4
-            for (uint32_t p = 0; p < d; ++p) {
-                const float w = __ldg(w1 + (uint64_t)p * h + j);
+#pragma unroll 8
+            for (uint32_t p = 0; p < act_dim; ++p) {
+                const float wv = w2[(size_t)p * L + w * 32 + lane];
 #pragma unroll
-                for (int v = 0; v < kVT; ++v) acc[v] = __fmaf_rn(xs[v * d + p], w, acc[v]);
+                for (int v = 0; v < kVT; ++v) acc[v] = __fmaf_rn(act[v * act_dim + p], wv, acc[v]);
             }
-            const float bj = __ldg(b1 + j);
+            const uint32_t col = lane * W + w;
 #pragma unroll
-            for (int v = 0; v < kVT; ++v) a1[v * h + j] = silu_exact(__fadd_rn(acc[v], bj));
-        }
-        __syncthreads();
-        act = a1;
-        act_dim = h;
-    } else {
-        w2 = prm.w1 + (uint64_t)head * d * L;  // linear: projection d x L
-    }
-
-    // layer 2 (or the linear projection) + sign + pack
-    for (uint32_t w = warp; w < W; w += kEncThreads / 32) {
-        const uint32_t col = lane * W + w;
-        float acc[kVT];
-#pragma unroll
-        for (int v = 0; v < kVT; ++v) acc[v] = 0.0f;
-#pragma unroll 4
-        for (uint32_t p = 0; p < act_dim; ++p) {
-            const float wv = __ldg(w2 + (uint64_t)p * L + col);
-#pragma unroll
-            for (int v = 0; v < kVT; ++v) acc[v] = __fmaf_rn(act[v * act_dim + p], wv, acc[v]);
-        }
-#pragma unroll
-        for (int v = 0; v < kVT; ++v) {
-            if ((uint32_t)v >= nv) break;
-            const uint32_t vg = v0 + v, b = vg / job.m, mi = vg % job.m;
-            if (job.out_mode == ENC_PRE) {
-                job.pre[(((uint64_t)b * H + head) * job.m + mi) * L + col] = acc[v];
-            } else {
-                const uint32_t bits = __ballot_sync(0xffffffffu, acc[v] >= 0.0f);
-                if (lane == 0) {
-                    uint64_t row;
-                    if (job.out_mode == ENC_APPEND)
-                        row = ((uint64_t)b * H + head) * job.cap + (job.pos[b] - job.pos_minus_one);
-                    else
-                        row = ((uint64_t)b * H + head) * job.m + mi;
-                    job.codes[row * W + w] = __brev(bits);
+            for (int v = 0; v < kVT; ++v) {
+                if ((uint32_t)v >= nv) break;
+                const uint32_t vg = v0 + v, b = vg / job.m, mi = vg % job.m;
+                if (job.out_mode == ENC_PRE) {
+                    job.pre[(((uint64_t)b * H + head) * job.m + mi) * L + col] = acc[v];
+                } else {
+                    const uint32_t bits = __ballot_sync(0xffffffffu, acc[v] >= 0.0f);
+                    if (lane == 0) {
+                        uint64_t row;
+                        if (job.out_mode == ENC_APPEND)
+                            row = ((uint64_t)b * H + head) * job.cap + (job.pos[b] - job.pos_minus_one);
+                        else
+                            row = ((uint64_t)b * H + head) * job.m + mi;
+                        job.codes[row * W + w] = __brev(bits);
+                    }
                 }
             }
         }
-    }
 
-    // append: K/V rows into the caches at the same slot
-    if (job.out_mode == ENC_APPEND && job.kcache) {
-        for (uint32_t i = tid; i < nv * d; i += kEncThreads) {
-            const uint32_t v = i / d, c = i % d;
-            const uint32_t b = v0 + v;  // m == 1
-            const uint64_t src = ((uint64_t)b * H + head) * d + c;
-            const uint64_t dst =
-                (((uint64_t)b * H + head) * job.cap + (job.pos[b] - job.pos_minus_one)) * d + c;
-            const float kv = xs[v * d + c];
-            const float vv = job.v_new[src];
-            if (job.kv_dtype == SPL_BF16) {
-                static_cast<__nv_bfloat16*>(job.kcache)[dst] = __float2bfloat16_rn(kv);
-                static_cast<__nv_bfloat16*>(job.vcache)[dst] = __float2bfloat16_rn(vv);
-            } else {
-                static_cast<float*>(job.kcache)[dst] = kv;
-                static_cast<float*>(job.vcache)[dst] = vv;
+        // append: K/V rows into the caches at the same slot
+        if (job.out_mode == ENC_APPEND && job.kcache) {
+            for (uint32_t i = tid; i < nv * d; i += kEncThreads) {
+                const uint32_t v = i / d, c = i % d;
+                const uint32_t b = v0 + v;  // m == 1
+                const uint64_t src = ((uint64_t)b * H + head) * d + c;
+                const uint64_t dst =
+                    (((uint64_t)b * H + head) * job.cap + (job.pos[b] - job.pos_minus_one)) * d + c;
+                const float kv = xs[v * d + c];
+                const float vv = job.v_new[src];
+                if (job.kv_dtype == SPL_BF16) {
+                    static_cast<__nv_bfloat16*>(job.kcache)[dst] = __float2bfloat16_rn(kv);
+                    static_cast<__nv_bfloat16*>(job.vcache)[dst] = __float2bfloat16_rn(vv);
+                } else {
+                    static_cast<float*>(job.kcache)[dst] = kv;
+                    static_cast<float*>(job.vcache)[dst] = vv;
+                }
             }
+        }
+        __syncthreads();
+    }
+    if (prm.staged && !weights_ready) {
+        // never consumed the barrier (no tile): still wait before exiting so
+        // the async copies do not outlive the CTA's shared memory
+        uint32_t done = 0;
+        while (!done) {
+            asm volatile(
+                "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0; "
+                "selp.u32 %0, 1, 0, p; }"
+                : "=r"(done) : "r"(smem_u32(&s_bar)) : "memory");
         }
     }
 }
@@ -156,9 +222,10 @@ __global__ void __launch_bounds__(kEncThreads) k1_encode_exact(EncParams prm) {
 spl_status encode_exact_launch(spl_ctx* ctx, const spl_hasher* hs, uint32_t B,
                                const EncJob* jobs, int njobs, cudaStream_t s) {
     EncParams prm{};
+    const bool mlp = hs->kind == SPL_HASHER_MLP;
     prm.w1 = hs->w1;
     prm.b1 = hs->b1;
-    prm.w2 = hs->w2;
+    prm.w2p = hs->w2_perm;
     prm.H = hs->H;
     prm.d = hs->d;
     prm.h = hs->h;
@@ -174,12 +241,19 @@ spl_status encode_exact_launch(spl_ctx* ctx, const spl_hasher* hs, uint32_t B,
     prm.dev_err = ctx->dev_err;
     const uint32_t nvec = B * max_m;
     if (nvec == 0) return SPL_OK;
-    const size_t smem = sizeof(float) * kVT * ((size_t)hs->d + (hs->kind == SPL_HASHER_MLP ? hs->h : 0));
+    const size_t act_dim = mlp ? hs->h : hs->d;
+    const size_t io = sizeof(float) * kVT * ((size_t)hs->d + (mlp ? hs->h : 0));
+    const size_t wbytes = sizeof(float) * ((mlp ? (size_t)hs->d * hs->h : 0) + act_dim * hs->L);
+    prm.staged = (wbytes + io <= 200 * 1024) && wbytes % 16 == 0;
+    const size_t smem = io + (prm.staged ? wbytes : 0);
     if (smem > 48 * 1024)
         SPL_CUDA_TRY(ctx, cudaFuncSetAttribute(k1_encode_exact,
                                                cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                (int)smem));
-    dim3 grid((nvec + kVT - 1) / kVT, hs->H, njobs);
+    const uint32_t ntiles = (nvec + kVT - 1) / kVT;
+    // each CTA stages a head's weights once and loops over vector tiles
+    const uint32_t per_head = std::max<uint32_t>(1, (uint32_t)(2 * ctx->num_sms) / hs->H);
+    dim3 grid(std::min(ntiles, per_head), hs->H, njobs);
     k1_encode_exact<<<grid, kEncThreads, smem, s>>>(prm);
     return after_launch(ctx, "k1_encode_exact");
 }

@@ -6,20 +6,27 @@
 //
 // Layout: codes [P][stride][W] u32 (row = one 16 B / 32 B vector for
 // L = 128 / 256). The virtual row space P x n_max is cut into G equal
-// contiguous CTA ranges (G = SMs x resident CTAs, one wave, no tail); a
-// CTA's range is split at problem boundaries into "segments" (record index
+// contiguous CTA ranges (G = SMs x resident CTAs: exactly one wave); a CTA's
+// range is split at problem boundaries into "segments" (record index
 // cta + problem, unique because the (cta, problem) staircase is monotone).
 //
-// k3_scan   : per row score = L - sum popc(q ^ r) from 128-bit streaming
-//             loads (L2 evict-first), u8/u16 score to an L2-resident buffer,
-//             per-thread private u16 histograms in shared memory (LDS/STS,
-//             conflict-free, no atomics — a smem-atomic histogram cannot
-//             keep up with ~1.5 rows/clk/SM), reduced per segment to a
-//             suffix-cumulative record. The CTA finishing a problem's last
-//             segment plans it (T, tie quota, per-segment output offsets).
-// k3_select : re-reads the u8 scores (from L2) and does the ordered
-//             compaction: score > T, or score == T among the first `take`
-//             ties of the segment; output ascending, bit-exact.
+// Streaming: every thread keeps two sets of U 32-byte units in flight
+// (LDG.E.NA.EFL2.256: 256-bit, no L1 allocation, L2 evict-first; register
+// double buffering), score = L - sum popc(q ^ r), and counts scores in
+// per-thread private u8 counters in shared memory (LDS/STS, conflict-free,
+// flushed into a u32 histogram before they can wrap) — a shared-atomic
+// histogram cannot keep up with ~1.5 rows/clk/SM.
+//
+// Fused path (k3_scan<..., FUSED>): when a CTA's scores fit in shared memory
+// (the headline 32 x 512K case), the kernel is launched cooperatively: scores
+// stay on chip, per-segment suffix-cumulative histograms go to global, one
+// grid barrier, then every CTA derives T / tie quota / its output offset and
+// compacts its rows from shared memory. One launch, one HBM pass.
+// Two-pass path (k3_scan + k3_select): u8/u16 scores to an L2-resident
+// buffer; the CTA finishing a problem's last segment plans it; k3_select
+// compacts. Used for caches too large for on-chip scores and for the
+// sequence-sharded (multi-GPU) flow, whose plan needs a collective between
+// the two kernels.
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -35,7 +42,7 @@ struct K3Geom {
     uint64_t n_max;  // rows per problem (virtual)
     uint64_t total;  // P * n_max
     uint64_t S;      // rows per CTA
-    uint64_t n_pad;  // score row stride
+    uint64_t n_pad;  // global score row stride (two-pass)
     uint32_t G;      // CTAs
     uint32_t P;
 };
@@ -57,18 +64,23 @@ struct K3Params {
     uint32_t W;
     uint32_t k;
     K3Geom g;
-    void* scores;          // [P][n_pad] ScoreT
+    void* scores;          // two-pass: [P][n_pad] ScoreT
     uint32_t* records;     // [(G+P)][L+2] suffix-cumulative counts
-    uint32_t* tot_hist;    // [P][tot_stride]
+    uint32_t* tot_hist;    // [P][tot_stride] per-problem histogram (atomics)
     uint64_t tot_stride;
-    uint32_t* counters;    // [P]
-    uint4* plans;          // [(G+P)] {T, offset, take, 0}
+    uint32_t* counters;    // [P] two-pass segment completion
+    uint32_t* sync;        // [2] fused: grid barrier, completion
+    uint4* plans;          // [(G+P)] two-pass {T, offset, take, 0}
     uint32_t* cnt_out;     // [P]
+    uint32_t* idx_out;     // fused: [P][idx_stride]
+    uint64_t idx_stride;
     uint32_t* dev_err;
     int shard;             // 1: no planning; tot_hist = caller's histogram
+    uint32_t score_region; // fused: bytes of shared memory for scores
 };
 
 constexpr int kThreads = 256;
+constexpr int kU = 4;  // 32-byte units per thread per load batch
 
 // ------------------------------------------------------------ block scans
 __device__ __forceinline__ uint64_t warp_incl_scan_u64(uint64_t v) {
@@ -104,7 +116,6 @@ __device__ __forceinline__ uint64_t block_excl_scan_u64(uint64_t v, uint64_t* s_
 // In-place suffix sum over a[0..n) in shared memory: a[t] = sum_{b >= t} a[b].
 __device__ void block_suffix_sum(uint32_t* a, uint32_t n, uint64_t* s_warp) {
     uint64_t carry = 0;
-    // process from the top in chunks of kThreads, reversed index
     for (uint32_t base = 0; base < n; base += kThreads) {
         const uint32_t i = base + threadIdx.x;  // i-th from the top
         const uint32_t t = n - 1 - i;
@@ -117,9 +128,25 @@ __device__ void block_suffix_sum(uint32_t* a, uint32_t n, uint64_t* s_warp) {
     }
 }
 
-// Plan every segment of problem p given (T, quota): per segment output
-// offset + ties to take, from the segment records (read through L2: they
-// were written by other CTAs of this launch).
+// Threshold of one problem from its (global) histogram: s_cum <- suffix
+// sums, returns T (SPL_PLAN_SKIP when kk == 0) and the tie quota.
+__device__ void problem_threshold(const uint32_t* tot, uint32_t L, uint32_t kk, uint32_t* s_cum,
+                                  uint64_t* s_warp, uint32_t* s_T, uint32_t& T, uint32_t& quota) {
+    for (uint32_t t = threadIdx.x; t <= L + 1; t += kThreads) s_cum[t] = t <= L ? __ldcg(tot + t) : 0u;
+    __syncthreads();
+    block_suffix_sum(s_cum, L + 1, s_warp);
+    if (threadIdx.x == 0) *s_T = SPL_PLAN_SKIP;
+    __syncthreads();
+    if (kk > 0)
+        for (uint32_t t = threadIdx.x; t <= L; t += kThreads)
+            if (s_cum[t] >= kk && s_cum[t + 1] < kk) *s_T = t;
+    __syncthreads();
+    T = *s_T;
+    quota = (T == SPL_PLAN_SKIP) ? 0u : kk - s_cum[T + 1];
+    __syncthreads();
+}
+
+// Two-pass: plan every segment of problem p given (T, quota).
 __device__ void plan_segments(const K3Params& prm, uint32_t p, uint32_t T, uint32_t quota,
                               uint64_t* s_warp) {
     const uint32_t L2 = prm.L + 2;
@@ -149,37 +176,7 @@ __device__ void plan_segments(const K3Params& prm, uint32_t p, uint32_t T, uint3
     }
 }
 
-// Single-GPU planning by the CTA that completed problem p's last segment.
-__device__ void plan_problem_single(const K3Params& prm, uint32_t p, uint32_t nv,
-                                    uint32_t* s_cum, uint64_t* s_warp, uint32_t* s_T) {
-    const uint32_t L = prm.L;
-    uint32_t* tot = prm.tot_hist + (uint64_t)p * prm.tot_stride;
-    for (uint32_t t = threadIdx.x; t <= L + 1; t += kThreads) {
-        s_cum[t] = t <= L ? __ldcg(tot + t) : 0u;
-        if (t <= L) tot[t] = 0u;  // self-reset for the next launch
-    }
-    __syncthreads();
-    block_suffix_sum(s_cum, L + 1, s_warp);
-    const uint32_t kk = prm.k < nv ? prm.k : nv;
-    if (threadIdx.x == 0) *s_T = SPL_PLAN_SKIP;
-    __syncthreads();
-    if (kk > 0) {
-        for (uint32_t t = threadIdx.x; t <= L; t += kThreads)
-            if (s_cum[t] >= kk && s_cum[t + 1] < kk) *s_T = t;
-    }
-    __syncthreads();
-    const uint32_t T = *s_T;
-    const uint32_t quota = (T == SPL_PLAN_SKIP) ? 0u : kk - s_cum[T + 1];
-    plan_segments(prm, p, T, quota, s_warp);
-    if (threadIdx.x == 0) {
-        prm.cnt_out[p] = kk;
-        prm.counters[p] = 0u;
-    }
-}
-
-// ------------------------------------------------------------------ scan
-// One 32-byte unit per thread per load (LDG.E.NA.EFL2.256: 256-bit,
-// no L1 allocation, L2 evict-first) = 8 / W code rows.
+// ------------------------------------------------------------ streaming
 struct Unit32 {
     uint32_t w[8];
     __device__ __forceinline__ void load(const uint32_t* base, uint64_t unit) {
@@ -214,31 +211,287 @@ __device__ __forceinline__ void store_scores(ScoreT* dst, const uint32_t* s) {
     }
 }
 
-// HMODE 0: private per-thread u16 histograms [bins][kThreads]
-// HMODE 1: one shared u32 histogram with smem atomics (large L)
-template <int W, typename ScoreT, int HMODE>
+template <bool PRIV>
+__device__ __forceinline__ void count_score(uint8_t* priv, uint32_t* hist32, uint32_t s) {
+    if (PRIV)
+        priv[s * kThreads + threadIdx.x] += 1;
+    else
+        atomicAdd(hist32 + s, 1u);
+}
+
+// Add the private u8 counters [bins][kThreads] into hist32 and clear them.
+__device__ void flush_priv(uint8_t* priv, uint32_t* hist32, uint32_t bins) {
+    __syncthreads();
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (uint32_t b = warp; b < bins; b += kThreads / 32) {
+        uint2* row = reinterpret_cast<uint2*>(priv + (size_t)b * kThreads);  // 256 B = 32 x 8 B
+        const uint2 x = row[lane];
+        uint32_t sum = __vsadu4(x.x, 0u) + __vsadu4(x.y, 0u);
+        row[lane] = make_uint2(0u, 0u);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+        if (lane == 0) hist32[b] += sum;
+    }
+    __syncthreads();
+}
+
+// One row's agreement score from W words (edge rows: plain loads).
+template <int W>
+__device__ __forceinline__ uint32_t row_score(const uint32_t* row, const uint32_t* q, uint32_t L) {
+    uint32_t mism = 0;
+#pragma unroll
+    for (int w = 0; w < W; ++w) mism += __popc(__ldg(row + w) ^ q[w]);
+    return L - mism;
+}
+
+// Stream rows [r0, r1) of one problem: scores into dst[row - dst_row0],
+// counts into priv / hist32. Uniform control flow across the block (flushes
+// sync the block). The body of the loop is check-free: rows before the first
+// / after the last whole 32-byte unit are handled up front, and only the last
+// iteration (pair) tests unit bounds. Offsets inside a piece are 32-bit.
+template <int W, typename ScoreT, bool PRIV, bool DST_SMEM>
+__device__ void stream_piece(const uint32_t* base, const uint32_t* qp, uint32_t L, uint64_t r0,
+                             uint64_t r1, ScoreT* dst, uint64_t dst_row0, uint8_t* priv,
+                             uint32_t* hist32, uint32_t bins) {
+    const int tid = threadIdx.x;
+    if constexpr (W > 0) {
+        constexpr int R = 8 / W;  // rows per 32-byte unit
+        uint32_t q[W];
+#pragma unroll
+        for (int w = 0; w < W; ++w) q[w] = __ldg(qp + w);
+        // whole units [uh, ut); partial-unit rows [r0, uh*R) and [ut*R, r1)
+        const uint64_t uh = (r0 + R - 1) / R, ut = r1 / R;
+        {
+            const uint64_t head_end = min(r1, uh * R);
+            const uint64_t tail_beg = max(head_end, ut * R);
+            const uint32_t nhead = (uint32_t)(head_end - r0), ntail = (uint32_t)(r1 - tail_beg);
+            if ((uint32_t)tid < nhead + ntail) {
+                const uint64_t row = (uint32_t)tid < nhead ? r0 + tid : tail_beg + (tid - nhead);
+                const uint32_t sc = row_score<W>(base + row * W, q, L);
+                dst[row - dst_row0] = (ScoreT)sc;
+                count_score<PRIV>(priv, hist32, sc);
+            }
+        }
+        if (ut <= uh) {
+            if (PRIV) flush_priv(priv, hist32, bins);
+            __syncthreads();
+            return;
+        }
+        const uint32_t nu = (uint32_t)(ut - uh);
+        const uint32_t* ubase = base + uh * 8 + (size_t)tid * 8;  // this thread's unit 0
+        ScoreT* udst = dst + (uh * R - dst_row0) + (size_t)tid * R;  // its scores
+        // private counters through 32-bit shared-window addresses hoisted out
+        // of the loop (ld/st.shared.u8; asm volatile keeps their order)
+        const uint32_t priv_s = (uint32_t)__cvta_generic_to_shared(priv) + tid;
+        const uint32_t dst_s = DST_SMEM ? (uint32_t)__cvta_generic_to_shared(udst) : 0u;
+        constexpr uint32_t per_it = (uint32_t)kThreads * kU;
+        const uint32_t nit = (nu + per_it - 1) / per_it;
+        // private u8 counters: flush before any thread can add 256 to a bin
+        // (each iteration adds at most kU * R per thread; iterations go in pairs)
+        constexpr uint32_t kFlushPairs = (255 / (kU * R)) / 2 > 0 ? (255 / (kU * R)) / 2 : 1;
+        Unit32 a[kU], b[kU];
+        auto load = [&](Unit32* buf, uint32_t it, bool check) {
+            const uint32_t* p = ubase + (size_t)it * per_it * 8;
+#pragma unroll
+            for (int j = 0; j < kU; ++j)
+                if (!check || it * per_it + j * kThreads + tid < nu) buf[j].load(p, (uint32_t)j * kThreads);
+        };
+        auto count = [&](uint32_t sc) {
+            if (PRIV) {
+                const uint32_t addr = priv_s + sc * kThreads;
+                uint32_t v;
+                asm volatile("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(addr));
+                asm volatile("st.shared.u8 [%0], %1;" ::"r"(addr), "r"(v + 1));
+            } else {
+                atomicAdd(hist32 + sc, 1u);
+            }
+        };
+        auto process_unit = [&](const Unit32& u, uint32_t it, int j) {
+            uint32_t sc[R];
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                uint32_t mism = 0;
+#pragma unroll
+                for (int w = 0; w < W; ++w) mism += __popc(u.w[r * W + w] ^ q[w]);
+                sc[r] = L - mism;
+            }
+            const size_t off = ((size_t)it * per_it + (size_t)j * kThreads) * R;
+            if constexpr (DST_SMEM) {
+                uint32_t v = 0;
+#pragma unroll
+                for (int r = 0; r < R; ++r) v |= sc[r] << (r * 8 * sizeof(ScoreT));
+                const uint32_t ad = dst_s + (uint32_t)(off * sizeof(ScoreT));
+                if constexpr (sizeof(ScoreT) * R == 1)
+                    asm volatile("st.shared.u8 [%0], %1;" ::"r"(ad), "r"(v));
+                else if constexpr (sizeof(ScoreT) * R == 2)
+                    asm volatile("st.shared.u16 [%0], %1;" ::"r"(ad), "h"((unsigned short)v));
+                else if constexpr (sizeof(ScoreT) * R == 4)
+                    asm volatile("st.shared.u32 [%0], %1;" ::"r"(ad), "r"(v));
+                else
+                    store_scores<ScoreT, R>(udst + off, sc);
+            } else {
+                store_scores<ScoreT, R>(udst + off, sc);
+            }
+#pragma unroll
+            for (int r = 0; r < R; ++r) count(sc[r]);
+        };
+        auto process_full = [&](const Unit32* buf, uint32_t it) {
+#pragma unroll
+            for (int j = 0; j < kU; ++j) process_unit(buf[j], it, j);
+        };
+        auto process_tail = [&](const Unit32* buf, uint32_t it) {
+#pragma unroll
+            for (int j = 0; j < kU; ++j)
+                if (it * per_it + j * kThreads + tid < nu) process_unit(buf[j], it, j);
+        };
+        const uint32_t nfull = nu / per_it;  // iterations with every unit in range
+        load(a, 0, nfull == 0);
+        for (uint32_t it = 0; it < nit; it += 2) {
+            if (it + 1 < nit) load(b, it + 1, it + 1 >= nfull);
+            if (it < nfull) process_full(a, it); else process_tail(a, it);
+            if (it + 1 < nit) {
+                if (it + 2 < nit) load(a, it + 2, it + 2 >= nfull);
+                if (it + 1 < nfull) process_full(b, it + 1); else process_tail(b, it + 1);
+            }
+            if (PRIV && ((it / 2 + 1) % kFlushPairs) == 0) flush_priv(priv, hist32, bins);
+        }
+    } else {
+        // any W: 32-bit loads, one row per thread per step
+        const uint32_t Wr = L / 32;
+        uint32_t steps = 0;
+        for (uint64_t r = r0 + tid; r - tid < r1; r += kThreads) {
+            if (r < r1) {
+                const uint32_t* row = base + r * Wr;
+                uint32_t mism = 0;
+                for (uint32_t w = 0; w < Wr; ++w) mism += __popc(__ldg(row + w) ^ __ldg(qp + w));
+                const uint32_t s = L - mism;
+                dst[r - dst_row0] = (ScoreT)s;
+                count_score<PRIV>(priv, hist32, s);
+            }
+            if (PRIV && ++steps == 255) {
+                flush_priv(priv, hist32, bins);
+                steps = 0;
+            }
+        }
+    }
+    if (PRIV) flush_priv(priv, hist32, bins);
+    __syncthreads();
+}
+
+// ------------------------------------------------------------ ordered select
+// 4/2 packed scores per word -> per-row flags via SIMD byte/half compares.
+template <typename ScoreT>
+__device__ __forceinline__ void word_flags(uint32_t w, uint32_t Tw, uint32_t& gt, uint32_t& eq) {
+    if constexpr (sizeof(ScoreT) == 1) {
+        const uint32_t g = __vcmpgtu4(w, Tw) & 0x01010101u, e = __vcmpeq4(w, Tw) & 0x01010101u;
+        gt = (g * 0x01020408u) >> 24;
+        eq = (e * 0x01020408u) >> 24;
+    } else {
+        const uint32_t g = __vcmpgtu2(w, Tw), e = __vcmpeq2(w, Tw);
+        gt = (g & 1u) | ((g >> 15) & 2u);
+        eq = (e & 1u) | ((e >> 15) & 2u);
+    }
+}
+
+// Ordered compaction of rows [r0, r1) whose scores sit at sc[row - a0]
+// (a0 = r0 rounded down to 16 rows; sc 16-byte aligned): keep score > T and
+// the first `take` score == T rows, writing ascending row ids to out[0..).
+template <typename ScoreT, bool GLOBAL>
+__device__ void select_rows(const ScoreT* sc, uint64_t a0, uint64_t r0, uint64_t r1, uint32_t T,
+                            uint32_t take, uint32_t* out, uint64_t* s_warp) {
+    constexpr int PER = 16 / sizeof(ScoreT);  // scores per 16-byte vector
+    constexpr int NV = 4;
+    constexpr int CH = PER * NV;              // <= 64 rows per thread per round
+    constexpr int SPW = 4 / sizeof(ScoreT);   // scores per word
+    const uint32_t Tw = sizeof(ScoreT) == 1 ? T * 0x01010101u : T * 0x00010001u;
+    const int tid = threadIdx.x;
+    const uint64_t round_rows = (uint64_t)kThreads * CH;
+    uint64_t carry_gt = 0, carry_eq = 0;
+    for (uint64_t base = a0; base < r1; base += round_rows) {
+        const uint64_t my = base + (uint64_t)tid * CH;
+        uint64_t gtm = 0, eqm = 0;
+        if (my < r1) {
+#pragma unroll
+            for (int v = 0; v < NV; ++v) {
+                const uint64_t at = my + (uint64_t)v * PER;
+                uint4 x = make_uint4(0, 0, 0, 0);
+                if (at < r1) {
+                    const uint4* ptr = reinterpret_cast<const uint4*>(sc + (at - a0));
+                    x = GLOBAL ? __ldcg(ptr) : *ptr;
+                }
+                const uint32_t ws[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    uint32_t g, e;
+                    word_flags<ScoreT>(ws[i], Tw, g, e);
+                    gtm |= (uint64_t)g << (v * PER + i * SPW);
+                    eqm |= (uint64_t)e << (v * PER + i * SPW);
+                }
+            }
+            // rows outside [r0, r1)
+            const uint64_t lo = r0 > my ? r0 - my : 0;
+            const uint64_t hi = r1 - my < (uint64_t)CH ? r1 - my : (uint64_t)CH;
+            uint64_t valid = hi >= 64 ? ~0ull : ((1ull << hi) - 1);
+            valid &= lo >= 64 ? 0ull : ~((1ull << lo) - 1);
+            gtm &= valid;
+            eqm &= valid;
+        }
+        const uint32_t gt = __popcll(gtm), eq = __popcll(eqm);
+        uint64_t tot;
+        const uint64_t ex = block_excl_scan_u64(((uint64_t)eq << 32) | gt, s_warp, tot);
+        uint64_t m = gtm | eqm;
+        if (m) {
+            uint64_t eq_before = carry_eq + (ex >> 32);
+            uint64_t pos = carry_gt + (ex & 0xffffffffu) + (eq_before < take ? eq_before : take);
+            while (m) {
+                const int i = __ffsll((long long)m) - 1;
+                m &= m - 1;
+                if ((gtm >> i) & 1u) {
+                    out[pos++] = (uint32_t)(my + i);
+                } else {
+                    if (eq_before < take) out[pos++] = (uint32_t)(my + i);
+                    ++eq_before;
+                }
+            }
+        }
+        carry_gt += tot & 0xffffffffu;
+        carry_eq += tot >> 32;
+    }
+}
+
+// ------------------------------------------------------------------ scan
+__device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+template <int W, typename ScoreT, bool PRIV, bool FUSED>
 __global__ void __launch_bounds__(kThreads) k3_scan(K3Params prm) {
     extern __shared__ __align__(16) uint8_t smem[];
     __shared__ uint64_t s_warp[kThreads / 32 + 1];
-    __shared__ uint32_t s_flag;
-    __shared__ uint32_t s_T;
+    __shared__ uint32_t s_flag, s_T;
     const uint32_t L = prm.L;
     const uint32_t bins = L + 1;
     const uint32_t Wr = (W > 0) ? (uint32_t)W : prm.W;
-    const size_t hist_bytes =
-        HMODE == 0 ? (size_t)bins * kThreads * sizeof(uint16_t) : (size_t)bins * sizeof(uint32_t);
-    uint16_t* hist16 = reinterpret_cast<uint16_t*>(smem);
-    uint32_t* hist32 = reinterpret_cast<uint32_t*>(smem);
-    // HMODE 1 reduces in place: the shared histogram becomes the record.
-    uint32_t* s_cum = HMODE == 0
-                          ? reinterpret_cast<uint32_t*>(smem + ((hist_bytes + 15) & ~size_t(15)))
-                          : hist32;
+    const size_t priv_bytes = PRIV ? (((size_t)bins * kThreads + 15) & ~size_t(15)) : 0;
+    uint8_t* priv = smem;
+    uint32_t* hist32 = reinterpret_cast<uint32_t*>(smem + priv_bytes);  // [bins + 1]
+    uint8_t* sregion = smem + priv_bytes + (((size_t)(bins + 1) * 4 + 15) & ~size_t(15));
     const int tid = threadIdx.x;
     const K3Geom& g = prm.g;
 
     const uint64_t g0 = (uint64_t)blockIdx.x * g.S;
     const uint64_t g1 = min(g0 + g.S, g.total);
-    for (uint32_t p = (uint32_t)(g0 / g.n_max); p < g.P && (uint64_t)p * g.n_max < g1; ++p) {
+    const uint32_t p_first = (uint32_t)(g0 / g.n_max);
+    uint32_t region_off = 0;  // fused: byte offset of the current piece's scores
+
+    // zero the counters once (flush_priv re-zeroes them)
+    if constexpr (PRIV)
+        for (uint32_t i = tid; i < priv_bytes / 16; i += kThreads)
+            reinterpret_cast<uint4*>(priv)[i] = make_uint4(0, 0, 0, 0);
+
+    for (uint32_t p = p_first; p < g.P && (uint64_t)p * g.n_max < g1; ++p) {
         const uint64_t pbase = (uint64_t)p * g.n_max;
         const uint64_t lo = max(g0, pbase) - pbase;
         const uint64_t hi = min(g1, pbase + g.n_max) - pbase;
@@ -248,115 +501,36 @@ __global__ void __launch_bounds__(kThreads) k3_scan(K3Params prm) {
             nv = (uint32_t)g.n_max;
         }
         const uint64_t r0 = lo, r1 = min(hi, (uint64_t)nv);
-
-        // zero the histogram
-        if (HMODE == 0) {
-            uint4* h4 = reinterpret_cast<uint4*>(hist16);
-            for (uint32_t i = tid; i < hist_bytes / 16; i += kThreads) h4[i] = make_uint4(0, 0, 0, 0);
-        } else {
-            for (uint32_t i = tid; i < bins; i += kThreads) hist32[i] = 0;
-        }
+        for (uint32_t i = tid; i <= bins; i += kThreads) hist32[i] = 0;
         __syncthreads();
 
         if (r0 < r1) {
             const uint32_t* qp = prm.qcodes + (uint64_t)p * Wr;
             const uint32_t* base = prm.codes + (uint64_t)p * prm.stride_rows * Wr;
-            ScoreT* srow = reinterpret_cast<ScoreT*>(prm.scores) + (uint64_t)p * g.n_pad;
-            if constexpr (W > 0) {
-                constexpr int R = 8 / W;  // rows per 32-byte unit
-                uint32_t q[W];
-#pragma unroll
-                for (int w = 0; w < W; ++w) q[w] = __ldg(qp + w);
-                constexpr int U = 4;
-                const uint64_t u0 = r0 / R, u1 = (r1 + R - 1) / R;
-                for (uint64_t u = u0 + tid; u < u1; u += (uint64_t)kThreads * U) {
-                    Unit32 v[U];
-#pragma unroll
-                    for (int j = 0; j < U; ++j) {
-                        const uint64_t uu = u + (uint64_t)j * kThreads;
-                        if (uu < u1) v[j].load(base, uu);
-                    }
-#pragma unroll
-                    for (int j = 0; j < U; ++j) {
-                        const uint64_t uu = u + (uint64_t)j * kThreads;
-                        if (uu >= u1) continue;
-                        uint32_t sc[R];
-#pragma unroll
-                        for (int r = 0; r < R; ++r) {
-                            uint32_t mism = 0;
-#pragma unroll
-                            for (int w = 0; w < W; ++w) mism += __popc(v[j].w[r * W + w] ^ q[w]);
-                            sc[r] = L - mism;
-                        }
-                        const uint64_t row0 = uu * R;
-                        if (row0 >= r0 && row0 + R <= r1) {
-                            store_scores<ScoreT, R>(srow + row0, sc);
-#pragma unroll
-                            for (int r = 0; r < R; ++r) {
-                                if (HMODE == 0)
-                                    hist16[sc[r] * kThreads + tid] += 1;
-                                else
-                                    atomicAdd(&hist32[sc[r]], 1u);
-                            }
-                        } else {
-#pragma unroll
-                            for (int r = 0; r < R; ++r) {
-                                const uint64_t row = row0 + r;
-                                if (row < r0 || row >= r1) continue;
-                                srow[row] = (ScoreT)sc[r];
-                                if (HMODE == 0)
-                                    hist16[sc[r] * kThreads + tid] += 1;
-                                else
-                                    atomicAdd(&hist32[sc[r]], 1u);
-                            }
-                        }
-                    }
-                }
+            ScoreT* dst;
+            uint64_t dst_row0;
+            if (FUSED) {
+                dst_row0 = r0 & ~uint64_t(15);
+                dst = reinterpret_cast<ScoreT*>(sregion + region_off);
+                region_off += (uint32_t)((((r1 - dst_row0) * sizeof(ScoreT)) + 15) & ~uint64_t(15));
             } else {
-                for (uint64_t r = r0 + tid; r < r1; r += kThreads) {
-                    const uint32_t* row = base + r * Wr;
-                    uint32_t mism = 0;
-                    for (uint32_t w = 0; w < Wr; ++w) mism += __popc(__ldg(row + w) ^ __ldg(qp + w));
-                    const uint32_t s = L - mism;
-                    srow[r] = (ScoreT)s;
-                    if (HMODE == 0)
-                        hist16[s * kThreads + tid] += 1;
-                    else
-                        atomicAdd(&hist32[s], 1u);
-                }
+                dst_row0 = 0;
+                dst = reinterpret_cast<ScoreT*>(prm.scores) + (uint64_t)p * g.n_pad;
             }
+            stream_piece<W, ScoreT, PRIV, FUSED>(base, qp, L, r0, r1, dst, dst_row0, priv, hist32, bins);
         }
-        __syncthreads();
-
-        // reduce -> s_cum[b] = count of score b; s_cum[L+1] = 0
-        if (HMODE == 0) {
-            const int lane = tid & 31, warp = tid >> 5;
-            for (uint32_t b = warp; b < bins; b += kThreads / 32) {
-                const uint32_t* h32 = reinterpret_cast<const uint32_t*>(hist16 + (size_t)b * kThreads);
-                uint32_t sum = 0;
-#pragma unroll
-                for (int i = 0; i < kThreads / 64; ++i) {
-                    const uint32_t x = h32[lane + 32 * i];
-                    sum += (x & 0xffffu) + (x >> 16);
-                }
-#pragma unroll
-                for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
-                if (lane == 0) s_cum[b] = sum;
-            }
-        }
-        if (tid == 0) s_cum[bins] = 0;
         __syncthreads();
         // raw counts -> global per-problem histogram (integer atomics: the
         // sums are order-independent, so results stay deterministic)
         uint32_t* tot = prm.tot_hist + (uint64_t)p * prm.tot_stride;
         for (uint32_t b = tid; b < bins; b += kThreads)
-            if (s_cum[b]) atomicAdd(tot + b, s_cum[b]);
+            if (hist32[b]) atomicAdd(tot + b, hist32[b]);
         __syncthreads();
-        block_suffix_sum(s_cum, bins, s_warp);
+        block_suffix_sum(hist32, bins, s_warp);  // hist32[bins] stays 0
         uint32_t* rec = prm.records + (uint64_t)(blockIdx.x + p) * (L + 2);
-        for (uint32_t t = tid; t < L + 2; t += kThreads) rec[t] = s_cum[t];
+        for (uint32_t t = tid; t < L + 2; t += kThreads) rec[t] = hist32[t];
 
-        if (!prm.shard) {
+        if (!FUSED && !prm.shard) {
             __threadfence();
             __syncthreads();
             if (tid == 0) {
@@ -367,10 +541,87 @@ __global__ void __launch_bounds__(kThreads) k3_scan(K3Params prm) {
             __syncthreads();
             if (s_flag) {
                 __threadfence();
-                plan_problem_single(prm, p, nv, s_cum, s_warp, &s_T);
+                const uint32_t kk = prm.k < nv ? prm.k : nv;
+                uint32_t T, quota;
+                problem_threshold(tot, L, kk, hist32, s_warp, &s_T, T, quota);
+                for (uint32_t t = tid; t <= L; t += kThreads) tot[t] = 0u;  // self-reset
+                plan_segments(prm, p, T, quota, s_warp);
+                if (tid == 0) {
+                    prm.cnt_out[p] = kk;
+                    prm.counters[p] = 0u;
+                }
             }
         }
         __syncthreads();
+    }
+    if constexpr (!FUSED) return;
+
+    // ---------------- grid barrier (cooperative launch: all CTAs resident)
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) {
+        atomicAdd(prm.sync, 1u);
+        while (ld_acquire(prm.sync) < gridDim.x) __nanosleep(64);
+    }
+    __syncthreads();
+
+    // ---------------- plan + select from shared memory
+    region_off = 0;
+    for (uint32_t p = p_first; p < g.P && (uint64_t)p * g.n_max < g1; ++p) {
+        const uint64_t pbase = (uint64_t)p * g.n_max;
+        const uint64_t lo = max(g0, pbase) - pbase;
+        const uint64_t hi = min(g1, pbase + g.n_max) - pbase;
+        uint32_t nv = prm.n_valid[p / prm.nvalid_div];
+        if (nv > g.n_max) nv = (uint32_t)g.n_max;
+        const uint64_t r0 = lo, r1 = min(hi, (uint64_t)nv);
+        const uint32_t kk = prm.k < nv ? prm.k : nv;
+        uint32_t T, quota;
+        problem_threshold(prm.tot_hist + (uint64_t)p * prm.tot_stride, L, kk, hist32, s_warp, &s_T,
+                          T, quota);
+        const uint32_t c0 = seg_first(g, p);
+        if (tid == 0 && blockIdx.x == c0) prm.cnt_out[p] = kk;
+        if (r0 >= r1) continue;
+        const uint64_t a0 = r0 & ~uint64_t(15);
+        const ScoreT* sc = reinterpret_cast<const ScoreT*>(sregion + region_off);
+        region_off += (uint32_t)((((r1 - a0) * sizeof(ScoreT)) + 15) & ~uint64_t(15));
+        if (T == SPL_PLAN_SKIP) continue;
+        // counts of the earlier segments of this problem (their records)
+        uint64_t gt_before = 0, eq_before = 0;
+        for (uint32_t cb = c0; cb < blockIdx.x; cb += kThreads) {
+            const uint32_t c = cb + tid;
+            uint32_t gtv = 0, eqv = 0;
+            if (c < blockIdx.x) {
+                const uint32_t* r = prm.records + (uint64_t)(c + p) * (L + 2);
+                const uint32_t geT = __ldcg(r + T), geT1 = __ldcg(r + T + 1);
+                gtv = geT1;
+                eqv = geT - geT1;
+            }
+            uint64_t tot;
+            block_excl_scan_u64(((uint64_t)eqv << 32) | gtv, s_warp, tot);
+            gt_before += tot & 0xffffffffu;
+            eq_before += tot >> 32;
+        }
+        const uint64_t left = quota > eq_before ? quota - eq_before : 0;
+        const uint32_t* own = prm.records + (uint64_t)(blockIdx.x + p) * (L + 2);
+        const uint64_t eq_mine = (uint64_t)__ldcg(own + T) - __ldcg(own + T + 1);
+        const uint32_t take = (uint32_t)(eq_mine < left ? eq_mine : left);
+        const uint64_t off = gt_before + (eq_before < quota ? eq_before : quota);
+        select_rows<ScoreT, false>(sc, a0, r0, r1, T, take,
+                                   prm.idx_out + (uint64_t)p * prm.idx_stride + off, s_warp);
+    }
+
+    // ---------------- completion: the last CTA resets the shared state
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) s_flag = (atomicAdd(prm.sync + 1, 1u) + 1 == gridDim.x) ? 1u : 0u;
+    __syncthreads();
+    if (s_flag) {
+        __threadfence();
+        for (uint64_t i = tid; i < (uint64_t)g.P * prm.tot_stride; i += kThreads) prm.tot_hist[i] = 0u;
+        if (tid == 0) {
+            prm.sync[0] = 0u;
+            prm.sync[1] = 0u;
+        }
     }
 }
 
@@ -379,9 +630,7 @@ template <typename ScoreT>
 __global__ void __launch_bounds__(kThreads) k3_select(K3Params prm, uint32_t* idx,
                                                       uint64_t idx_stride) {
     __shared__ uint64_t s_warp[kThreads / 32 + 1];
-    constexpr int PER = 16 / sizeof(ScoreT);
     const K3Geom& g = prm.g;
-    const int tid = threadIdx.x;
     const uint64_t g0 = (uint64_t)blockIdx.x * g.S;
     const uint64_t g1 = min(g0 + g.S, g.total);
     for (uint32_t p = (uint32_t)(g0 / g.n_max); p < g.P && (uint64_t)p * g.n_max < g1; ++p) {
@@ -392,50 +641,11 @@ __global__ void __launch_bounds__(kThreads) k3_select(K3Params prm, uint32_t* id
         if (nv > g.n_max) nv = (uint32_t)g.n_max;
         const uint64_t r0 = lo, r1 = min(hi, (uint64_t)nv);
         const uint4 plan = prm.plans[blockIdx.x + p];
-        const uint32_t T = plan.x;
-        if (T == SPL_PLAN_SKIP || r0 >= r1) continue;  // uniform across the block
-        const uint32_t take = plan.z;
-        uint32_t* out = idx + (uint64_t)p * idx_stride + plan.y;
+        if (plan.x == SPL_PLAN_SKIP || r0 >= r1) continue;  // uniform across the block
         const ScoreT* srow = reinterpret_cast<const ScoreT*>(prm.scores) + (uint64_t)p * g.n_pad;
-        uint64_t carry_gt = 0, carry_eq = 0;
-        const uint64_t a0 = r0 & ~(uint64_t)(PER - 1);
-        for (uint64_t tile = a0; tile < r1; tile += (uint64_t)kThreads * PER) {
-            const uint64_t my = tile + (uint64_t)tid * PER;
-            ScoreT s[PER];
-            if (my < r1) {
-                const uint4 v = *reinterpret_cast<const uint4*>(srow + my);
-                const ScoreT* sv = reinterpret_cast<const ScoreT*>(&v);
-#pragma unroll
-                for (int i = 0; i < PER; ++i) s[i] = sv[i];
-            }
-            uint32_t gt = 0, eq = 0;
-#pragma unroll
-            for (int i = 0; i < PER; ++i) {
-                const uint64_t row = my + i;
-                const bool valid = row >= r0 && row < r1;
-                gt += (valid && s[i] > T) ? 1u : 0u;
-                eq += (valid && s[i] == T) ? 1u : 0u;
-            }
-            uint64_t tot;
-            const uint64_t ex = block_excl_scan_u64(((uint64_t)eq << 32) | gt, s_warp, tot);
-            if (gt | eq) {
-                uint64_t eq_before = carry_eq + (ex >> 32);
-                uint64_t pos = carry_gt + (ex & 0xffffffffu) + (eq_before < take ? eq_before : take);
-#pragma unroll
-                for (int i = 0; i < PER; ++i) {
-                    const uint64_t row = my + i;
-                    if (row < r0 || row >= r1) continue;
-                    if (s[i] > T) {
-                        out[pos++] = (uint32_t)row;
-                    } else if (s[i] == T) {
-                        if (eq_before < take) out[pos++] = (uint32_t)row;
-                        ++eq_before;
-                    }
-                }
-            }
-            carry_gt += tot & 0xffffffffu;
-            carry_eq += tot >> 32;
-        }
+        const uint64_t a0 = r0 & ~uint64_t(15);
+        select_rows<ScoreT, true>(srow + a0, a0, r0, r1, plan.x, plan.z,
+                                  idx + (uint64_t)p * idx_stride + plan.y, s_warp);
     }
 }
 
@@ -484,73 +694,107 @@ spl_status ensure_buffer(spl_ctx* ctx, void** buf, size_t* have, size_t bytes, b
 
 namespace {
 
+size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
 struct K3Plan {
     K3Geom g;
     bool vec;
-    int hmode;
+    bool priv;
+    bool fused;
     size_t smem;
     size_t score_bytes;
+    uint32_t score_region;
 };
 
-size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
-
-int hist_mode(uint32_t L) { return (size_t)(L + 1) * kThreads * 2 <= 150 * 1024 ? 0 : 1; }
-
-size_t scan_smem(uint32_t L, int hmode) {
-    if (hmode == 1) return (size_t)(L + 2) * 4;  // histogram reduced in place
-    return align_up((size_t)(L + 1) * kThreads * 2, 16) + (size_t)(L + 2) * 4;
-}
-
-template <int W, typename ScoreT, int HM>
+template <int W, typename ScoreT, bool PRIV, bool FUSED>
 const void* scan_fn() {
-    return reinterpret_cast<const void*>(&k3_scan<W, ScoreT, HM>);
+    return reinterpret_cast<const void*>(&k3_scan<W, ScoreT, PRIV, FUSED>);
 }
-
-template <typename ScoreT, int HM>
-const void* pick_scan_w(uint32_t W) {
+template <typename ScoreT, bool PRIV, bool FUSED>
+const void* pick_w(uint32_t W) {
     switch (W) {
-        case 1: return scan_fn<1, ScoreT, HM>();
-        case 2: return scan_fn<2, ScoreT, HM>();
-        case 4: return scan_fn<4, ScoreT, HM>();
-        case 8: return scan_fn<8, ScoreT, HM>();
-        default: return scan_fn<0, ScoreT, HM>();  // any W, 32-bit loads
+        case 1: return scan_fn<1, ScoreT, PRIV, FUSED>();
+        case 2: return scan_fn<2, ScoreT, PRIV, FUSED>();
+        case 4: return scan_fn<4, ScoreT, PRIV, FUSED>();
+        case 8: return scan_fn<8, ScoreT, PRIV, FUSED>();
+        default: return scan_fn<0, ScoreT, PRIV, FUSED>();  // any W, 32-bit loads
     }
 }
-
-// vec: problem bases are 32-byte aligned (required by the 256-bit path).
-const void* pick_scan(uint32_t L, int hmode, bool vec) {
-    const uint32_t W = vec && (L / 32) <= 8 ? L / 32 : 0;
-    if (L <= 255) return hmode == 0 ? pick_scan_w<uint8_t, 0>(W) : pick_scan_w<uint8_t, 1>(W);
-    return hmode == 0 ? pick_scan_w<uint16_t, 0>(W) : pick_scan_w<uint16_t, 1>(W);
+template <typename ScoreT>
+const void* pick_st(uint32_t W, bool priv, bool fused) {
+    if (priv) return fused ? pick_w<ScoreT, true, true>(W) : pick_w<ScoreT, true, false>(W);
+    return fused ? pick_w<ScoreT, false, true>(W) : pick_w<ScoreT, false, false>(W);
+}
+const void* pick_scan(const K3Plan& pl, uint32_t L) {
+    const uint32_t W = pl.vec ? L / 32 : 0;
+    return L <= 255 ? pick_st<uint8_t>(W, pl.priv, pl.fused) : pick_st<uint16_t>(W, pl.priv, pl.fused);
 }
 
+size_t base_smem(uint32_t L, bool priv) {
+    const size_t bins = L + 1;
+    return (priv ? align_up(bins * kThreads, 16) : 0) + align_up((bins + 1) * 4, 16);
+}
+
+// allow_fused: try the single-launch cooperative path first.
 spl_status make_plan(spl_ctx* ctx, uint32_t P, uint64_t n_max, uint32_t L, const void* codes,
-                     uint64_t stride_rows, K3Plan* out) {
+                     uint64_t stride_rows, bool allow_fused, K3Plan* out) {
     K3Plan pl{};
     const uint32_t W = L / 32;
     pl.vec = W <= 8 && 8 % W == 0 && (reinterpret_cast<uintptr_t>(codes) % 32) == 0 &&
              (stride_rows * W * 4) % 32 == 0;
-    pl.hmode = hist_mode(L);
-    pl.smem = scan_smem(L, pl.hmode);
-    const void* fn = pick_scan(L, pl.hmode, pl.vec);
+    pl.priv = (size_t)(L + 1) * kThreads <= 96 * 1024;
+    pl.score_bytes = L <= 255 ? 1 : 2;
+    const uint64_t total = (uint64_t)P * n_max;
+    const size_t base = base_smem(L, pl.priv);
+    int dev_max_smem = 0, sm_smem = 0;
+    SPL_CUDA_TRY(ctx, cudaDeviceGetAttribute(&dev_max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin,
+                                             ctx->device));
+    SPL_CUDA_TRY(ctx, cudaDeviceGetAttribute(&sm_smem, cudaDevAttrMaxSharedMemoryPerMultiprocessor,
+                                             ctx->device));
+    auto geom = [&](uint64_t G_target) {
+        K3Geom g{};
+        uint64_t S = (total + G_target - 1) / G_target;
+        S = align_up(std::max<uint64_t>(S, 1024), 256);
+        g.n_max = n_max;
+        g.total = total;
+        g.S = S;
+        g.G = (uint32_t)((total + S - 1) / S);
+        g.P = P;
+        g.n_pad = align_up(n_max, 64);
+        return g;
+    };
+    if (allow_fused) {
+        for (int cps = 3; cps >= 1; --cps) {
+            const K3Geom g = geom((uint64_t)ctx->num_sms * cps);
+            const uint64_t pieces = g.S / n_max + 2;
+            const size_t region =
+                align_up((size_t)(g.S + 16 * pieces) * pl.score_bytes + 16 * pieces, 16);
+            const size_t smem = base + region;
+            if (smem > (size_t)dev_max_smem || (smem + 1024 + 128) * cps > (size_t)sm_smem) continue;
+            K3Plan t = pl;
+            t.fused = true;
+            t.g = g;
+            t.smem = smem;
+            t.score_region = (uint32_t)region;
+            const void* fn = pick_scan(t, L);
+            SPL_CUDA_TRY(ctx, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                   (int)smem));
+            int per_sm = 0;
+            SPL_CUDA_TRY(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kThreads, smem));
+            if ((uint64_t)per_sm * ctx->num_sms < g.G) continue;
+            *out = t;
+            return SPL_OK;
+        }
+    }
+    pl.fused = false;
+    pl.smem = base;
+    const void* fn = pick_scan(pl, L);
     SPL_CUDA_TRY(ctx, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            (int)pl.smem));
     int per_sm = 0;
-    SPL_CUDA_TRY(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kThreads,
-                                                                    pl.smem));
+    SPL_CUDA_TRY(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kThreads, pl.smem));
     if (per_sm < 1) per_sm = 1;
-    const uint64_t total = (uint64_t)P * n_max;
-    const uint64_t target = (uint64_t)ctx->num_sms * per_sm;
-    uint64_t S = (total + target - 1) / target;
-    S = align_up(std::max<uint64_t>(S, 1024), 256);
-    S = std::min<uint64_t>(S, (uint64_t)65535 * kThreads);  // u16 private counters
-    pl.g.n_max = n_max;
-    pl.g.total = total;
-    pl.g.S = S;
-    pl.g.G = (uint32_t)((total + S - 1) / S);
-    pl.g.P = P;
-    pl.g.n_pad = align_up(n_max, 64);
-    pl.score_bytes = L <= 255 ? 1 : 2;
+    pl.g = geom((uint64_t)ctx->num_sms * per_sm);
     *out = pl;
     return SPL_OK;
 }
@@ -559,18 +803,19 @@ struct K3Ws {
     void* scores;
     uint32_t* records;
     uint4* plans;
+    uint32_t* sync;
     uint32_t* counters;
     uint32_t* tot;
 };
 
 spl_status k3_workspace(spl_ctx* ctx, const K3Plan& pl, uint32_t L, cudaStream_t s, K3Ws* ws) {
-    const size_t sc = align_up((size_t)pl.g.P * pl.g.n_pad * pl.score_bytes, 256);
+    const size_t sc = pl.fused ? 0 : align_up((size_t)pl.g.P * pl.g.n_pad * pl.score_bytes, 256);
     const size_t rec = align_up((size_t)(pl.g.G + pl.g.P) * (L + 2) * 4, 256);
     const size_t plans = align_up((size_t)(pl.g.G + pl.g.P) * 16, 256);
     spl_status st = ensure_buffer(ctx, &ctx->k3_ws, &ctx->k3_ws_bytes, sc + rec + plans, false, s,
                                   "hamming_topk");
     if (st) return st;
-    const size_t state_words = (size_t)pl.g.P * (1 + (L + 2));
+    const size_t state_words = 2 + (size_t)pl.g.P * (1 + (L + 2));
     size_t have = ctx->k3_state_words * 4;
     st = ensure_buffer(ctx, reinterpret_cast<void**>(&ctx->k3_state), &have, state_words * 4, true,
                        s, "hamming_topk");
@@ -580,8 +825,9 @@ spl_status k3_workspace(spl_ctx* ctx, const K3Plan& pl, uint32_t L, cudaStream_t
     ws->scores = b;
     ws->records = reinterpret_cast<uint32_t*>(b + sc);
     ws->plans = reinterpret_cast<uint4*>(b + sc + rec);
-    ws->counters = ctx->k3_state;
-    ws->tot = ctx->k3_state + pl.g.P;
+    ws->sync = ctx->k3_state;
+    ws->counters = ctx->k3_state + 2;
+    ws->tot = ctx->k3_state + 2 + pl.g.P;
     return SPL_OK;
 }
 
@@ -600,10 +846,13 @@ spl_status validate_common(spl_ctx* ctx, const char* who, const uint32_t* codes,
 }
 
 spl_status launch_scan(spl_ctx* ctx, const K3Plan& pl, const K3Params& prm, cudaStream_t s) {
-    const void* fn = pick_scan(prm.L, pl.hmode, pl.vec);
+    const void* fn = pick_scan(pl, prm.L);
     void* args[] = {const_cast<K3Params*>(&prm)};
-    SPL_CUDA_TRY(ctx, cudaLaunchKernel(fn, dim3(pl.g.G), dim3(kThreads), args, pl.smem, s));
-    return after_launch(ctx, "k3_scan");
+    if (pl.fused)
+        SPL_CUDA_TRY(ctx, cudaLaunchCooperativeKernel(fn, dim3(pl.g.G), dim3(kThreads), args, pl.smem, s));
+    else
+        SPL_CUDA_TRY(ctx, cudaLaunchKernel(fn, dim3(pl.g.G), dim3(kThreads), args, pl.smem, s));
+    return after_launch(ctx, pl.fused ? "k3_scan(fused)" : "k3_scan");
 }
 
 spl_status launch_select(spl_ctx* ctx, const K3Plan& pl, const K3Params& prm, uint32_t* idx,
@@ -615,28 +864,9 @@ spl_status launch_select(spl_ctx* ctx, const K3Plan& pl, const K3Params& prm, ui
     return after_launch(ctx, "k3_select");
 }
 
-}  // namespace
-
-spl_status hamming_topk_impl(spl_ctx* ctx, const uint32_t* codes, uint64_t stride_rows,
-                             uint32_t L, const uint32_t* qcodes, uint32_t P,
-                             const uint32_t* n_valid, uint32_t nvalid_div, uint64_t n_max,
-                             uint32_t k, uint32_t* idx, uint32_t* cnt, cudaStream_t s) {
-    spl_status st = validate_common(ctx, "hamming_topk", codes, qcodes, n_valid, L, nvalid_div);
-    if (st) return st;
-    if (k == 0) return fail(ctx, SPL_E_DIMENSION, "hash_topk: k must be >= 1");
-    if (!idx || !cnt) return fail(ctx, SPL_E_STATE, "hamming_topk: null output pointer");
-    if (P == 0) return SPL_OK;
-    if (n_max == 0 || n_max > 0xFFFFFFFFull) {
-        if (n_max == 0) {
-            SPL_CUDA_TRY(ctx, cudaMemsetAsync(cnt, 0, sizeof(uint32_t) * P, s));
-            return SPL_OK;
-        }
-        return fail(ctx, SPL_E_DIMENSION, "hamming_topk: n_max exceeds 2^32 rows");
-    }
-    K3Plan pl;
-    if ((st = make_plan(ctx, P, n_max, L, codes, stride_rows, &pl))) return st;
-    K3Ws ws;
-    if ((st = k3_workspace(ctx, pl, L, s, &ws))) return st;
+K3Params base_params(spl_ctx* ctx, const K3Plan& pl, const K3Ws& ws, const uint32_t* codes,
+                     uint64_t stride_rows, uint32_t L, const uint32_t* qcodes,
+                     const uint32_t* n_valid, uint32_t nvalid_div, uint32_t k) {
     K3Params prm{};
     prm.codes = codes;
     prm.stride_rows = stride_rows;
@@ -652,11 +882,46 @@ spl_status hamming_topk_impl(spl_ctx* ctx, const uint32_t* codes, uint64_t strid
     prm.tot_hist = ws.tot;
     prm.tot_stride = L + 2;
     prm.counters = ws.counters;
+    prm.sync = ws.sync;
     prm.plans = ws.plans;
-    prm.cnt_out = cnt;
     prm.dev_err = ctx->dev_err;
+    prm.score_region = pl.score_region;
+    return prm;
+}
+
+// SPL_K3_PATH=twopass forces the two-kernel path (A/B measurement, tests).
+bool fused_allowed() {
+    const char* e = getenv("SPL_K3_PATH");
+    return !(e && std::string(e) == "twopass");
+}
+
+}  // namespace
+
+spl_status hamming_topk_impl(spl_ctx* ctx, const uint32_t* codes, uint64_t stride_rows,
+                             uint32_t L, const uint32_t* qcodes, uint32_t P,
+                             const uint32_t* n_valid, uint32_t nvalid_div, uint64_t n_max,
+                             uint32_t k, uint32_t* idx, uint32_t* cnt, cudaStream_t s) {
+    spl_status st = validate_common(ctx, "hamming_topk", codes, qcodes, n_valid, L, nvalid_div);
+    if (st) return st;
+    if (k == 0) return fail(ctx, SPL_E_DIMENSION, "hash_topk: k must be >= 1");
+    if (!idx || !cnt) return fail(ctx, SPL_E_STATE, "hamming_topk: null output pointer");
+    if (P == 0) return SPL_OK;
+    if (n_max == 0) {
+        SPL_CUDA_TRY(ctx, cudaMemsetAsync(cnt, 0, sizeof(uint32_t) * P, s));
+        return SPL_OK;
+    }
+    if (n_max > 0xFFFFFFFFull) return fail(ctx, SPL_E_DIMENSION, "hamming_topk: n_max exceeds 2^32 rows");
+    K3Plan pl;
+    if ((st = make_plan(ctx, P, n_max, L, codes, stride_rows, fused_allowed(), &pl))) return st;
+    K3Ws ws;
+    if ((st = k3_workspace(ctx, pl, L, s, &ws))) return st;
+    K3Params prm = base_params(ctx, pl, ws, codes, stride_rows, L, qcodes, n_valid, nvalid_div, k);
+    prm.cnt_out = cnt;
+    prm.idx_out = idx;
+    prm.idx_stride = k;
     prm.shard = 0;
     if ((st = launch_scan(ctx, pl, prm, s))) return st;
+    if (pl.fused) return SPL_OK;
     return launch_select(ctx, pl, prm, idx, k, s);
 }
 
@@ -676,29 +941,14 @@ spl_status shard_histogram_impl(spl_ctx* ctx, const uint32_t* codes, uint64_t st
         return SPL_OK;
     }
     K3Plan pl;
-    if ((st = make_plan(ctx, P, n_max, L, codes, stride_rows, &pl))) return st;
+    if ((st = make_plan(ctx, P, n_max, L, codes, stride_rows, false, &pl))) return st;
     K3Ws ws;
     if ((st = k3_workspace(ctx, pl, L, s, &ws))) return st;
     ctx->shard_G = pl.g.G;
     ctx->shard_S = pl.g.S;
-    K3Params prm{};
-    prm.codes = codes;
-    prm.stride_rows = stride_rows;
-    prm.qcodes = qcodes;
-    prm.n_valid = n_valid;
-    prm.nvalid_div = nvalid_div;
-    prm.L = L;
-    prm.W = L / 32;
-    prm.k = 1;
-    prm.g = pl.g;
-    prm.scores = ws.scores;
-    prm.records = ws.records;
+    K3Params prm = base_params(ctx, pl, ws, codes, stride_rows, L, qcodes, n_valid, nvalid_div, 1);
     prm.tot_hist = hist;
     prm.tot_stride = L + 1;
-    prm.counters = ws.counters;
-    prm.plans = ws.plans;
-    prm.cnt_out = nullptr;
-    prm.dev_err = ctx->dev_err;
     prm.shard = 1;
     return launch_scan(ctx, pl, prm, s);
 }
@@ -728,18 +978,8 @@ spl_status shard_select_impl(spl_ctx* ctx, const uint32_t* all_hist, uint32_t R,
     pl.score_bytes = L <= 255 ? 1 : 2;
     K3Ws ws;
     if ((st = k3_workspace(ctx, pl, L, s, &ws))) return st;
-    K3Params prm{};
-    prm.n_valid = n_valid;
-    prm.nvalid_div = nvalid_div;
-    prm.L = L;
-    prm.W = L / 32;
-    prm.k = k;
-    prm.g = pl.g;
-    prm.scores = ws.scores;
-    prm.records = ws.records;
-    prm.plans = ws.plans;
+    K3Params prm = base_params(ctx, pl, ws, nullptr, 0, L, nullptr, n_valid, nvalid_div, k);
     prm.cnt_out = cnt;
-    prm.dev_err = ctx->dev_err;
     prm.shard = 1;
     k3_shard_plan<<<P, kThreads, 0, s>>>(prm, all_hist, R, rank, out_offset);
     if ((st = after_launch(ctx, "k3_shard_plan"))) return st;

@@ -24,56 +24,53 @@ constexpr int kAttThreads = 128;
 constexpr int kAttWarps = kAttThreads / 32;
 constexpr int kGroup = 8;  // rows in flight per warp
 
+// Raw (undecoded) row slice of one lane: E elements of a K or V row. Loaded
+// as one coalesced vector per lane (warp = one full row), decoded to fp32 at
+// use, so the double buffer costs E/2 (bf16) or E (f32) registers per row.
 template <int E, typename KV>
-struct RowVec;
+struct Raw;
 template <int E>
-struct RowVec<E, __nv_bfloat16> {
-    float f[E];
+struct Raw<E, __nv_bfloat16> {
+    static_assert(E == 1 || E == 2 || E == 4 || E == 8, "E");
+    uint32_t u[(E + 1) / 2];
     __device__ __forceinline__ void load(const __nv_bfloat16* row, int lane) {
         const __nv_bfloat16* p = row + lane * E;
-        if constexpr (E == 4) {
-            const uint2 u = __ldg(reinterpret_cast<const uint2*>(p));
-            const __nv_bfloat162 a = *reinterpret_cast<const __nv_bfloat162*>(&u.x);
-            const __nv_bfloat162 b = *reinterpret_cast<const __nv_bfloat162*>(&u.y);
-            f[0] = __low2float(a); f[1] = __high2float(a);
-            f[2] = __low2float(b); f[3] = __high2float(b);
-        } else if constexpr (E == 8) {
-            const uint4 u = __ldg(reinterpret_cast<const uint4*>(p));
-            const uint32_t w[4] = {u.x, u.y, u.z, u.w};
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-                const __nv_bfloat162 t = *reinterpret_cast<const __nv_bfloat162*>(&w[i]);
-                f[2 * i] = __low2float(t);
-                f[2 * i + 1] = __high2float(t);
-            }
+        if constexpr (E == 8) {
+            const uint4 v = __ldg(reinterpret_cast<const uint4*>(p));
+            u[0] = v.x; u[1] = v.y; u[2] = v.z; u[3] = v.w;
+        } else if constexpr (E == 4) {
+            const uint2 v = __ldg(reinterpret_cast<const uint2*>(p));
+            u[0] = v.x; u[1] = v.y;
         } else if constexpr (E == 2) {
-            const __nv_bfloat162 t = __ldg(reinterpret_cast<const __nv_bfloat162*>(p));
-            f[0] = __low2float(t); f[1] = __high2float(t);
+            u[0] = __ldg(reinterpret_cast<const unsigned int*>(p));
         } else {
-#pragma unroll
-            for (int i = 0; i < E; ++i) f[i] = __bfloat162float(p[i]);
+            u[0] = __ldg(reinterpret_cast<const unsigned short*>(p));
         }
+    }
+    __device__ __forceinline__ float get(int e) const {
+        const uint32_t w = u[e / 2];
+        return __uint_as_float((e & 1) ? (w & 0xffff0000u) : (w << 16));
     }
 };
 template <int E>
-struct RowVec<E, float> {
+struct Raw<E, float> {
     float f[E];
     __device__ __forceinline__ void load(const float* row, int lane) {
         const float* p = row + lane * E;
         if constexpr (E % 4 == 0) {
 #pragma unroll
             for (int i = 0; i < E; i += 4) {
-                const float4 u = __ldg(reinterpret_cast<const float4*>(p + i));
-                f[i] = u.x; f[i + 1] = u.y; f[i + 2] = u.z; f[i + 3] = u.w;
+                const float4 v = __ldg(reinterpret_cast<const float4*>(p + i));
+                f[i] = v.x; f[i + 1] = v.y; f[i + 2] = v.z; f[i + 3] = v.w;
             }
         } else if constexpr (E == 2) {
-            const float2 u = __ldg(reinterpret_cast<const float2*>(p));
-            f[0] = u.x; f[1] = u.y;
+            const float2 v = __ldg(reinterpret_cast<const float2*>(p));
+            f[0] = v.x; f[1] = v.y;
         } else {
-#pragma unroll
-            for (int i = 0; i < E; ++i) f[i] = __ldg(p + i);
+            f[0] = __ldg(p);
         }
     }
+    __device__ __forceinline__ float get(int e) const { return f[e]; }
 };
 
 __device__ __forceinline__ float warp_sum(float v) {
@@ -82,7 +79,69 @@ __device__ __forceinline__ float warp_sum(float v) {
     return v;
 }
 
-// E = d / 32 elements per lane (d in {32, 64, 128, 256}).
+constexpr uint32_t kInv = 0xFFFFFFFFu;
+constexpr uint32_t kWarpRows = 64;  // rows per warp per split (2 indices per lane)
+
+// rows per in-flight group: 8, or 4 when a lane's slice of a row is >= 32 B
+template <int E, typename KV>
+constexpr int group_rows() {
+    return E * (int)sizeof(KV) >= 32 ? 4 : kGroup;
+}
+
+template <int E, typename KV>
+struct Group {
+    static constexpr int G = group_rows<E, KV>();
+    Raw<E, KV> k[G], v[G];
+    uint32_t row[G];
+    __device__ __forceinline__ void issue(uint32_t rid, int sub, const KV* kb, const KV* vb,
+                                          int lane) {
+#pragma unroll
+        for (int r = 0; r < G; ++r) {
+            row[r] = __shfl_sync(0xffffffffu, rid, sub * G + r);
+            if (row[r] != kInv) {
+                k[r].load(kb + (uint64_t)row[r] * (32 * E), lane);
+                v[r].load(vb + (uint64_t)row[r] * (32 * E), lane);
+            }
+        }
+    }
+};
+
+template <int E, typename KV>
+__device__ __forceinline__ void consume(const Group<E, KV>& g, const float* qv, float& m, float& l,
+                                        float* o) {
+    constexpr int G = Group<E, KV>::G;
+    float s[G];
+    float gmax = -INFINITY;
+#pragma unroll
+    for (int r = 0; r < G; ++r) {
+        float part = 0.0f;
+#pragma unroll
+        for (int e = 0; e < E; ++e) part = fmaf(qv[e], g.k[r].get(e), part);
+        part = warp_sum(part);
+        s[r] = g.row[r] != kInv ? part : -INFINITY;
+        gmax = fmaxf(gmax, s[r]);
+    }
+    if (gmax == -INFINITY) return;
+    const float m_new = fmaxf(m, gmax);
+    const float corr = exp2f(m - m_new);  // m = -inf -> 0
+    l *= corr;
+#pragma unroll
+    for (int e = 0; e < E; ++e) o[e] *= corr;
+#pragma unroll
+    for (int r = 0; r < G; ++r) {
+        if (g.row[r] == kInv) continue;  // never touch unloaded registers
+        const float w = exp2f(s[r] - m_new);
+        l += w;
+#pragma unroll
+        for (int e = 0; e < E; ++e) o[e] = fmaf(w, g.v[r].get(e), o[e]);
+    }
+    m = m_new;
+}
+
+// E = d / 32 elements per lane (d in {32, 64, 128, 256}). A split is
+// kAttWarps x kWarpRows rows; each warp prefetches its 64 row ids (2 per
+// lane) once, then streams 8-row groups with the next group's K/V gathers in
+// flight while the current group is reduced.
 template <int E, typename KV>
 __global__ void __launch_bounds__(kAttThreads) k4_sparse_attend(AttParams prm) {
     constexpr int D = 32 * E;
@@ -96,70 +155,44 @@ __global__ void __launch_bounds__(kAttThreads) k4_sparse_attend(AttParams prm) {
     const uint32_t* list = prm.idx + (uint64_t)p * prm.idx_stride;
     uint32_t own;
     if (prm.partial_mode)
-        own = prm.own_row ? prm.own_row[p] : 0xFFFFFFFFu;
+        own = prm.own_row ? prm.own_row[p] : kInv;
     else
         own = prm.n_valid[p / prm.nvalid_div] - 1u;
-    const bool has_own = own != 0xFFFFFFFFu;
+    const bool has_own = own != kInv;
     const bool own_listed = has_own && c > 0 && __ldg(list + c - 1) == own;
     const uint32_t nrows = c + ((has_own && !own_listed) ? 1u : 0u);
-    const uint32_t start = split * prm.rows_per_split;
-    const uint32_t end = min(start + prm.rows_per_split, nrows);
 
     const KV* kbase = static_cast<const KV*>(prm.kc) + (uint64_t)p * prm.stride_rows * D;
     const KV* vbase = static_cast<const KV*>(prm.vc) + (uint64_t)p * prm.stride_rows * D;
+
+    const uint32_t wb = split * prm.rows_per_split + warp * kWarpRows;
+    const uint32_t we = min(wb + kWarpRows, nrows);
+    auto row_at = [&](uint32_t j) -> uint32_t {
+        return j < we ? (j < c ? __ldg(list + j) : own) : kInv;
+    };
+    const uint32_t rid0 = row_at(wb + lane), rid1 = row_at(wb + 32 + lane);
+
     float qv[E];
 #pragma unroll
     for (int e = 0; e < E; ++e) qv[e] = prm.q[(uint64_t)p * D + lane * E + e] * prm.qscale;
-
     float m = -INFINITY, l = 0.0f, o[E];
 #pragma unroll
     for (int e = 0; e < E; ++e) o[e] = 0.0f;
 
-    // warp w takes a contiguous chunk of this split's rows
-    const uint32_t span = end > start ? end - start : 0;
-    const uint32_t chunk = (span + kAttWarps - 1) / kAttWarps;
-    const uint32_t wb = start + min(span, chunk * warp), we = start + min(span, chunk * (warp + 1));
-    for (uint32_t j = wb; j < we; j += kGroup) {
-        // lanes 0..7 fetch the group's row ids
-        uint32_t rid = 0xFFFFFFFFu;
-        if (lane < kGroup && j + lane < we) rid = (j + lane < c) ? __ldg(list + j + lane) : own;
-        RowVec<E, KV> kr[kGroup], vr[kGroup];
-        uint32_t rows[kGroup];
-#pragma unroll
-        for (int r = 0; r < kGroup; ++r) {
-            rows[r] = __shfl_sync(0xffffffffu, rid, r);
-            if (rows[r] != 0xFFFFFFFFu) {
-                kr[r].load(kbase + (uint64_t)rows[r] * D, lane);
-                vr[r].load(vbase + (uint64_t)rows[r] * D, lane);
-            }
+    if (wb < we) {
+        constexpr int G = Group<E, KV>::G;
+        constexpr int PER_RID = 32 / G;  // groups per 32 prefetched ids
+        const int ngroups = (int)((we - wb + G - 1) / G);
+        Group<E, KV> ga, gb;
+        ga.issue(rid0, 0, kbase, vbase, lane);
+        for (int gi = 0; gi < ngroups; gi += 2) {
+            const int g1 = gi + 1, g2 = gi + 2;
+            if (g1 < ngroups) gb.issue(g1 < PER_RID ? rid0 : rid1, g1 % PER_RID, kbase, vbase, lane);
+            consume(ga, qv, m, l, o);
+            if (g1 >= ngroups) break;
+            if (g2 < ngroups) ga.issue(g2 < PER_RID ? rid0 : rid1, g2 % PER_RID, kbase, vbase, lane);
+            consume(gb, qv, m, l, o);
         }
-        float s[kGroup];
-        float gmax = -INFINITY;
-#pragma unroll
-        for (int r = 0; r < kGroup; ++r) {
-            float part = 0.0f;
-            if (rows[r] != 0xFFFFFFFFu) {
-#pragma unroll
-                for (int e = 0; e < E; ++e) part = fmaf(qv[e], kr[r].f[e], part);
-            }
-            part = warp_sum(part);
-            s[r] = rows[r] != 0xFFFFFFFFu ? part : -INFINITY;
-            gmax = fmaxf(gmax, s[r]);
-        }
-        const float m_new = fmaxf(m, gmax);
-        const float corr = exp2f(m - m_new);  // m = -inf -> 0
-        l *= corr;
-#pragma unroll
-        for (int e = 0; e < E; ++e) o[e] *= corr;
-#pragma unroll
-        for (int r = 0; r < kGroup; ++r) {
-            if (rows[r] == 0xFFFFFFFFu) continue;
-            const float w = exp2f(s[r] - m_new);
-            l += w;
-#pragma unroll
-            for (int e = 0; e < E; ++e) o[e] = fmaf(w, vr[r].f[e], o[e]);
-        }
-        m = m_new;
     }
 
     // merge warps
@@ -276,10 +309,7 @@ spl_status sparse_attend_launch(spl_ctx* ctx, AttParams prm, uint32_t kmax, int 
     }
     if (prm.P == 0) return SPL_OK;
     const uint64_t rows_max = (uint64_t)kmax + 1;
-    // enough CTAs to cover every SM several times, >= 32 rows per warp-group
-    const uint64_t target_ctas = (uint64_t)ctx->num_sms * 8;
-    uint64_t R = (rows_max * prm.P + target_ctas - 1) / target_ctas;
-    R = std::max<uint64_t>(64, std::min<uint64_t>(1024, (R + 31) / 32 * 32));
+    const uint64_t R = (uint64_t)kAttWarps * kWarpRows;  // rows per split (CTA)
     const uint32_t nsplit = (uint32_t)((rows_max + R - 1) / R);
     prm.rows_per_split = (uint32_t)R;
     prm.nsplit = nsplit;

@@ -52,6 +52,7 @@ struct spl_hasher {
     float* w1 = nullptr;  // [H][d][h]  (linear: projection [H][d][L])
     float* b1 = nullptr;  // [H][h]
     float* w2 = nullptr;  // [H][h][L]
+    float* w2_perm = nullptr;  // layer 2 (linear: projection) columns permuted, see capi.cu
     // bf16 copies for the tcgen05 bulk encoder (K-major packing, see encode_tc.cu)
     void* w1_tc = nullptr;
     void* w2_tc = nullptr;
@@ -94,28 +95,6 @@ spl_status ensure_buffer(spl_ctx* ctx, void** buf, size_t* have, size_t bytes, b
 
 __device__ __forceinline__ void raise_dev_err(uint32_t* e, uint32_t flag) {
     if (e) atomicOr(e, flag);
-}
-
-// Streaming 128-bit load: read-only path, no L1 allocation, L2 evict-first
-// (the code cache is read once per step; keep L2 for scores/plans/weights).
-__device__ __forceinline__ uint4 ld_stream_v4(const uint4* p) {
-    uint4 r;
-    asm volatile("ld.global.nc.L1::no_allocate.L2::evict_first.v4.u32 {%0,%1,%2,%3}, [%4];"
-                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
-                 : "l"(p));
-    return r;
-}
-__device__ __forceinline__ uint2 ld_stream_v2(const uint2* p) {
-    uint2 r;
-    asm volatile("ld.global.nc.L1::no_allocate.L2::evict_first.v2.u32 {%0,%1}, [%2];"
-                 : "=r"(r.x), "=r"(r.y)
-                 : "l"(p));
-    return r;
-}
-__device__ __forceinline__ uint32_t ld_stream_u32(const uint32_t* p) {
-    uint32_t r;
-    asm volatile("ld.global.nc.L1::no_allocate.L2::evict_first.u32 %0, [%1];" : "=r"(r) : "l"(p));
-    return r;
 }
 
 }  // namespace spl

@@ -26,6 +26,17 @@ def U(t):
     return a.view(np.uint32) if a.dtype == np.int32 else a
 
 
+@pytest.fixture(params=["fused", "twopass"])
+def k3_path(request, monkeypatch):
+    """Run K3 tests through both the single-launch cooperative kernel and the
+    two-kernel path (SPL_K3_PATH is read by libspl at every call)."""
+    if request.param == "twopass":
+        monkeypatch.setenv("SPL_K3_PATH", "twopass")
+    else:
+        monkeypatch.delenv("SPL_K3_PATH", raising=False)
+    return request.param
+
+
 def run_topk(ctx, codes, q, n_valid, k, stride_rows=None, nvalid_div=1, n_max=None):
     """codes [P][cap][W] (or [cap][W] shared), q [P][W] -> list of index arrays."""
     codes = np.ascontiguousarray(codes, np.uint32)
@@ -48,7 +59,7 @@ def run_topk(ctx, codes, q, n_valid, k, stride_rows=None, nvalid_div=1, n_max=No
 
 # ------------------------------------------------------------ K3 hamming top-k
 @pytest.mark.parametrize("ci", list(range(6)))
-def test_golden_topk(ctx, ci):
+def test_golden_topk(ctx, k3_path, ci):
     codes, q = G[f"topk{ci}_codes"], G[f"topk{ci}_q"]
     k = int(G[f"topk{ci}_k"][0])
     n = codes.shape[0]
@@ -57,7 +68,7 @@ def test_golden_topk(ctx, ci):
 
 
 @pytest.mark.parametrize("L", [32, 64, 96, 128, 160, 256, 512])
-def test_topk_vs_oracle_widths(ctx, oracle, L):
+def test_topk_vs_oracle_widths(ctx, k3_path, oracle, L):
     rng = np.random.default_rng(L)
     P, n, W = 3, 20000, L // 32
     codes = rng.integers(0, 2**32, (P, n, W), dtype=np.uint64).astype(np.uint32)
@@ -72,7 +83,7 @@ def test_topk_vs_oracle_widths(ctx, oracle, L):
             assert np.array_equal(got[p], want[p, :kk]), (L, k, p)
 
 
-def test_topk_edge_cases(ctx, oracle):
+def test_topk_edge_cases(ctx, k3_path, oracle):
     rng = np.random.default_rng(5)
     codes = rng.integers(0, 2**32, (4, 300, 4), dtype=np.uint64).astype(np.uint32)
     q = codes[:, 0].copy()
@@ -97,7 +108,7 @@ def test_topk_k_zero_rejected(ctx):
                          4, idx, idx)
 
 
-def test_topk_shared_cache_causal(ctx, oracle):
+def test_topk_shared_cache_causal(ctx, k3_path, oracle):
     """hash_topk's layout: q queries share one cache, query r sees rows < r+1."""
     rng = np.random.default_rng(9)
     n, W = 3000, 4
@@ -110,7 +121,7 @@ def test_topk_shared_cache_causal(ctx, oracle):
         assert np.array_equal(got[r], oracle.top_k(s, min(64, int(offs[r]))))
 
 
-def test_topk_nvalid_per_batch(ctx, oracle):
+def test_topk_nvalid_per_batch(ctx, k3_path, oracle):
     rng = np.random.default_rng(10)
     B, H, cap, W = 3, 4, 5000, 4
     codes = rng.integers(0, 2**32, (B * H, cap, W), dtype=np.uint64).astype(np.uint32)
@@ -122,7 +133,7 @@ def test_topk_nvalid_per_batch(ctx, oracle):
         assert np.array_equal(got[p], want[p, :min(100, nvb[p // H])])
 
 
-def test_topk_config3_shape(ctx, oracle):
+def test_topk_config3_shape(ctx, k3_path, oracle):
     """Headline shape: 32 heads x 524288 rows x 128-bit codes, k = 10485."""
     rng = np.random.default_rng(3)
     P, n, W = 32, 524288, 4
@@ -150,7 +161,7 @@ def test_topk_config4_shape_l256(ctx, oracle):
         assert np.array_equal(got[p], want[p])
 
 
-def test_topk_repeatable(ctx):
+def test_topk_repeatable(ctx, k3_path):
     rng = np.random.default_rng(12)
     codes = rng.integers(0, 2**32, (8, 50000, 4), dtype=np.uint64).astype(np.uint32)
     q = codes[:, 5]
