@@ -295,10 +295,13 @@ def main():
         for _ in range(args.warmup):
             e2e_step()
         e2e_ms = event_timer(torch, e2e_step, args.steps, stream)
+        enc_ms = event_timer(torch, lambda: hasher.encode(q_dev, 1, 1, qcodes, capi.SPL_ENCODE_EXACT, stream),
+                             args.steps, stream)
         e2e = {"value": round(e2e_ms * 1000, 2), "unit": "µs",
                "h2d_bytes_per_step": int(q_host.numel() * 4),
                "d2h_bytes_per_step": int(idx_host.numel() * 4 + cnt_host.numel() * 4),
-               "path": "spl_encode(query, exact) + spl_hamming_topk, pinned host buffers"}
+               "path": "spl_encode(query, exact) + spl_hamming_topk, pinned host buffers",
+               "encode_us": round(enc_ms * 1000, 2)}
         if not args.no_decode:
             decode = bench_decode(torch, capi, ctx, dev, stream, args, hasher)
     clk = clocks.stop()

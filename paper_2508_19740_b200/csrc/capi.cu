@@ -96,7 +96,7 @@ spl_status spl_reserve(spl_ctx* ctx, uint32_t P, uint64_t n_max, uint32_t L, uin
     if (st) return st;
     size_t have = ctx->k3_state_words * 4;
     st = ensure_buffer(ctx, reinterpret_cast<void**>(&ctx->k3_state), &have,
-                       (size_t)P * (1 + (L + 2)) * 4, true, 0, "spl_reserve");
+                       (2 + (size_t)P * (1 + (L + 2) + 4)) * 4, true, 0, "spl_reserve");
     if (st) return st;
     ctx->k3_state_words = have / 4;
     if (d > 0) {
@@ -266,7 +266,27 @@ spl_status spl_hasher_create(spl_ctx* ctx, int kind, uint32_t H, uint32_t d, uin
                 for (uint32_t w = 0; w < W; ++w)
                     hp[((size_t)hd * rows2 + p) * L + w * 32 + c] =
                         src2[((size_t)hd * rows2 + p) * L + c * W + w];
-    if (!up(&hs->w1, h1) || !up(&hs->b1, hb) || !up(&hs->w2, h2) || !up(&hs->w2_perm, hp)) {
+    // cluster-encoder layouts (encode_exact.cu): W1 column quarters, and
+    // layer 2 word-major [w][p][c] so each CTA's words are one contiguous block
+    std::vector<float> hs1, hw2(src2.size());
+    if (kind == SPL_HASHER_MLP && h % 4 == 0) {
+        const uint32_t q = h / 4;
+        hs1.resize(h1.size());
+        for (uint32_t hd = 0; hd < H; ++hd)
+            for (uint32_t r = 0; r < 4; ++r)
+                for (uint32_t p = 0; p < d; ++p)
+                    for (uint32_t jj = 0; jj < q; ++jj)
+                        hs1[(((size_t)hd * 4 + r) * d + p) * q + jj] =
+                            h1[((size_t)hd * d + p) * h + r * q + jj];
+    }
+    for (uint32_t hd = 0; hd < H; ++hd)
+        for (uint32_t w = 0; w < W; ++w)
+            for (uint32_t p = 0; p < rows2; ++p)
+                for (uint32_t c = 0; c < 32; ++c)
+                    hw2[(((size_t)hd * W + w) * rows2 + p) * 32 + c] =
+                        src2[((size_t)hd * rows2 + p) * L + c * W + w];
+    if (!up(&hs->w1, h1) || !up(&hs->b1, hb) || !up(&hs->w2, h2) || !up(&hs->w2_perm, hp) ||
+        !up(&hs->w1_slices, hs1) || !up(&hs->w2_words, hw2)) {
         spl_hasher_destroy(hs);
         return fail(ctx, SPL_E_CUDA, "hasher: device allocation failed");
     }
@@ -280,6 +300,8 @@ void spl_hasher_destroy(spl_hasher* hs) {
     cudaFree(hs->b1);
     cudaFree(hs->w2);
     cudaFree(hs->w2_perm);
+    cudaFree(hs->w1_slices);
+    cudaFree(hs->w2_words);
     cudaFree(hs->w1_tc);
     cudaFree(hs->w2_tc);
     delete hs;

@@ -219,8 +219,276 @@ __global__ void __launch_bounds__(kEncThreads) k1_encode_exact(EncParams prm) {
     }
 }
 
+// ---------------------------------------------------------------------------
+// Cluster form (decode latency path): a 4-CTA thread-block cluster per
+// (head, tile of <= 8 vectors). CTA r TMA-loads only its quarter of the
+// weights — W1 columns [r*h/4, (r+1)*h/4) and code words [r*W/4, (r+1)*W/4)
+// (pre-sliced contiguous at hasher creation) — computes its quarter of the
+// hidden units, broadcasts them to the other three CTAs through distributed
+// shared memory (st.shared::cluster), and after one cluster barrier computes
+// its code words. Every output keeps the reference's sequential FMA order;
+// the split is across outputs only, so the bits are unchanged.
+constexpr int kCS = 4;  // CTAs per cluster
+
+struct EncClusterParams {
+    const float* w1s;   // [H][kCS][d][h/kCS]
+    const float* b1;    // [H][h]
+    const float* w2w;   // [H][W][act_dim][32]  word-major, lane-contiguous
+    uint32_t H, d, h, L, W;
+    int kind;
+    uint32_t B;
+    EncJob job[2];
+    uint32_t* dev_err;
+};
+
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;"
+                 ::: "memory");
+}
+// execution-only cluster rendezvous (no memory ordering needed)
+__device__ __forceinline__ void cluster_sync_relaxed() {
+    asm volatile("barrier.cluster.arrive.relaxed.aligned;\n\tbarrier.cluster.wait.aligned;" ::: "memory");
+}
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+
+__device__ __forceinline__ void wait_parity0(uint64_t* bar) {
+    uint32_t done = 0;
+    while (!done)
+        asm volatile(
+            "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0; "
+            "selp.u32 %0, 1, 0, p; }"
+            : "=r"(done) : "r"(smem_u32(bar)) : "memory");
+}
+
+__global__ void __cluster_dims__(kCS, 1, 1) __launch_bounds__(kEncThreads)
+    k1_encode_cluster(EncClusterParams prm) {
+    extern __shared__ __align__(128) float csm[];
+    __shared__ __align__(8) uint64_t s_bar;
+    __shared__ uint32_t s_bad;
+    const EncJob& job = prm.job[blockIdx.z];
+    const uint32_t head = blockIdx.y;
+    const uint32_t rank = cluster_rank();
+    const uint32_t d = prm.d, h = prm.h, L = prm.L, W = prm.W, H = prm.H;
+    const bool mlp = prm.kind == SPL_HASHER_MLP;
+    const uint32_t act_dim = mlp ? h : d;
+    const uint32_t hs = h / kCS, Wc = W / kCS;
+    const uint32_t nvec = prm.B * job.m;
+    const uint32_t ntiles = (nvec + kVT - 1) / kVT;
+    const uint32_t group = blockIdx.x / kCS, ngroups = gridDim.x / kCS;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    // shared layout: sw1 [d][hs] | sw2 [Wc][act_dim][32] | xs [kVT][d] | a1 [kVT][h]
+    float* sw1 = csm;
+    float* sw2 = sw1 + (mlp ? (size_t)d * hs : 0);
+    float* xs = sw2 + (size_t)Wc * act_dim * 32;
+    float* a1 = xs + (size_t)kVT * d;
+
+    if (tid == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"(smem_u32(&s_bar)));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        const uint32_t b1n = mlp ? d * hs * 4 : 0, b2n = Wc * act_dim * 32 * 4;
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
+                     :: "r"(smem_u32(&s_bar)), "r"(b1n + b2n) : "memory");
+        if (mlp)
+            bulk_g2s(sw1, prm.w1s + ((size_t)head * kCS + rank) * d * hs, b1n, &s_bar);
+        bulk_g2s(sw2, prm.w2w + ((size_t)head * W + rank * Wc) * act_dim * 32, b2n, &s_bar);
+    }
+    cluster_sync_relaxed();  // peers' shared memory is live before any DSMEM store
+    uint32_t a1_peer[kCS];
+#pragma unroll
+    for (int r = 0; r < kCS; ++r)
+        asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(a1_peer[r]) : "r"(smem_u32(a1)), "r"(r));
+    bool ready = false;
+
+    for (uint32_t tile = group; tile < ntiles; tile += ngroups) {
+        const uint32_t v0 = tile * kVT;
+        const uint32_t nv = min((uint32_t)kVT, nvec - v0);
+        if (tid == 0) s_bad = 0;
+        __syncthreads();
+        for (uint32_t i = tid; i < kVT * d; i += kEncThreads) {
+            const uint32_t v = i / d, c = i % d;
+            float val = 0.0f;
+            if (v < nv) {
+                const uint32_t vg = v0 + v, b = vg / job.m, mi = vg % job.m;
+                val = job.x[(((uint64_t)b * H + head) * job.m + mi) * d + c];
+                if (!isfinite(val)) s_bad = 1;
+            }
+            xs[i] = val;
+        }
+        if (!ready) {
+            wait_parity0(&s_bar);
+            ready = true;
+        }
+        __syncthreads();
+        if (s_bad && tid == 0 && rank == 0) raise_dev_err(prm.dev_err, SPL_DEV_ERR_NUMERIC);
+
+        // warp w handles vectors w and w + 4 (warp-uniform guards)
+        const uint32_t va = warp, vb = warp + 4;
+        const float* act = xs;
+        if (mlp) {
+            for (uint32_t jb = 0; jb < hs; jb += 32) {
+                const uint32_t jl = jb + lane;
+                float acc0 = 0.0f, acc1 = 0.0f;
+                if (va < nv) {
+                    for (uint32_t p = 0; p < d; p += 4) {
+                        const float4 xa = *reinterpret_cast<const float4*>(xs + va * d + p);
+                        const float w0 = sw1[(p + 0) * hs + jl], w1v = sw1[(p + 1) * hs + jl];
+                        const float w2v = sw1[(p + 2) * hs + jl], w3 = sw1[(p + 3) * hs + jl];
+                        acc0 = __fmaf_rn(xa.x, w0, acc0);
+                        acc0 = __fmaf_rn(xa.y, w1v, acc0);
+                        acc0 = __fmaf_rn(xa.z, w2v, acc0);
+                        acc0 = __fmaf_rn(xa.w, w3, acc0);
+                        if (vb < nv) {
+                            const float4 xb = *reinterpret_cast<const float4*>(xs + vb * d + p);
+                            acc1 = __fmaf_rn(xb.x, w0, acc1);
+                            acc1 = __fmaf_rn(xb.y, w1v, acc1);
+                            acc1 = __fmaf_rn(xb.z, w2v, acc1);
+                            acc1 = __fmaf_rn(xb.w, w3, acc1);
+                        }
+                    }
+                    const uint32_t j = rank * hs + jl;
+                    const float bj = __ldg(prm.b1 + (size_t)head * h + j);
+                    const float ya = silu_exact(__fadd_rn(acc0, bj));
+#pragma unroll
+                    for (int r = 0; r < kCS; ++r)
+                        asm volatile("st.shared::cluster.f32 [%0], %1;"
+                                     :: "r"(a1_peer[r] + (va * h + j) * 4), "f"(ya) : "memory");
+                    if (vb < nv) {
+                        const float yb = silu_exact(__fadd_rn(acc1, bj));
+#pragma unroll
+                        for (int r = 0; r < kCS; ++r)
+                            asm volatile("st.shared::cluster.f32 [%0], %1;"
+                                         :: "r"(a1_peer[r] + (vb * h + j) * 4), "f"(yb) : "memory");
+                    }
+                }
+            }
+            cluster_sync_all();  // every CTA now holds all h hidden units
+            act = a1;
+        }
+
+        // layer 2: this CTA's Wc words; lane c computes column c*W + w
+        for (uint32_t wl = 0; wl < Wc; ++wl) {
+            const uint32_t w = rank * Wc + wl;
+            const float* sw = sw2 + (size_t)wl * act_dim * 32;
+            float acc0 = 0.0f, acc1 = 0.0f;
+            if (va < nv) {
+                for (uint32_t p = 0; p < act_dim; p += 4) {
+                    const float4 xa = *reinterpret_cast<const float4*>(act + va * act_dim + p);
+                    const float w0 = sw[(p + 0) * 32 + lane], w1v = sw[(p + 1) * 32 + lane];
+                    const float w2v = sw[(p + 2) * 32 + lane], w3 = sw[(p + 3) * 32 + lane];
+                    acc0 = __fmaf_rn(xa.x, w0, acc0);
+                    acc0 = __fmaf_rn(xa.y, w1v, acc0);
+                    acc0 = __fmaf_rn(xa.z, w2v, acc0);
+                    acc0 = __fmaf_rn(xa.w, w3, acc0);
+                    if (vb < nv) {
+                        const float4 xb = *reinterpret_cast<const float4*>(act + vb * act_dim + p);
+                        acc1 = __fmaf_rn(xb.x, w0, acc1);
+                        acc1 = __fmaf_rn(xb.y, w1v, acc1);
+                        acc1 = __fmaf_rn(xb.z, w2v, acc1);
+                        acc1 = __fmaf_rn(xb.w, w3, acc1);
+                    }
+                }
+            }
+            const uint32_t col = lane * W + w;
+#pragma unroll
+            for (int s2 = 0; s2 < 2; ++s2) {
+                const uint32_t v = s2 == 0 ? va : vb;
+                if (v >= nv) continue;  // warp-uniform
+                const float z = s2 == 0 ? acc0 : acc1;
+                const uint32_t vg = v0 + v, b = vg / job.m, mi = vg % job.m;
+                if (job.out_mode == ENC_PRE) {
+                    job.pre[(((uint64_t)b * H + head) * job.m + mi) * L + col] = z;
+                } else {
+                    const uint32_t bits = __ballot_sync(0xffffffffu, z >= 0.0f);
+                    if (lane == 0) {
+                        uint64_t row;
+                        if (job.out_mode == ENC_APPEND)
+                            row = ((uint64_t)b * H + head) * job.cap + (job.pos[b] - job.pos_minus_one);
+                        else
+                            row = ((uint64_t)b * H + head) * job.m + mi;
+                        job.codes[row * W + w] = __brev(bits);
+                    }
+                }
+            }
+        }
+
+        if (rank == 0 && job.out_mode == ENC_APPEND && job.kcache) {
+            for (uint32_t i = tid; i < nv * d; i += kEncThreads) {
+                const uint32_t v = i / d, c = i % d;
+                const uint32_t b = v0 + v;  // m == 1
+                const uint64_t src = ((uint64_t)b * H + head) * d + c;
+                const uint64_t dst =
+                    (((uint64_t)b * H + head) * job.cap + (job.pos[b] - job.pos_minus_one)) * d + c;
+                const float kv = xs[v * d + c];
+                const float vv = job.v_new[src];
+                if (job.kv_dtype == SPL_BF16) {
+                    static_cast<__nv_bfloat16*>(job.kcache)[dst] = __float2bfloat16_rn(kv);
+                    static_cast<__nv_bfloat16*>(job.vcache)[dst] = __float2bfloat16_rn(vv);
+                } else {
+                    static_cast<float*>(job.kcache)[dst] = kv;
+                    static_cast<float*>(job.vcache)[dst] = vv;
+                }
+            }
+        }
+        cluster_sync_relaxed();  // peers finished reading a1 before the next tile rewrites it
+    }
+    if (!ready) wait_parity0(&s_bar);  // no tile: let the bulk copies land first
+}
+
+bool cluster_eligible(const spl_hasher* hs) {
+    const uint32_t W = hs->L / 32;
+    if (!hs->w1_slices || !hs->w2_words || W % kCS != 0 || hs->d % 4 != 0) return false;
+    if (hs->kind == SPL_HASHER_MLP && (hs->h % (32 * kCS) != 0)) return false;
+    return true;
+}
+
+spl_status encode_cluster_launch(spl_ctx* ctx, const spl_hasher* hs, uint32_t B,
+                                 const EncJob* jobs, int njobs, cudaStream_t s) {
+    EncClusterParams prm{};
+    const bool mlp = hs->kind == SPL_HASHER_MLP;
+    prm.w1s = hs->w1_slices;
+    prm.b1 = hs->b1;
+    prm.w2w = hs->w2_words;
+    prm.H = hs->H;
+    prm.d = hs->d;
+    prm.h = hs->h;
+    prm.L = hs->L;
+    prm.W = hs->L / 32;
+    prm.kind = hs->kind;
+    prm.B = B;
+    uint32_t max_m = 0;
+    for (int i = 0; i < njobs; ++i) {
+        prm.job[i] = jobs[i];
+        max_m = jobs[i].m > max_m ? jobs[i].m : max_m;
+    }
+    prm.dev_err = ctx->dev_err;
+    const uint32_t nvec = B * max_m;
+    if (nvec == 0) return SPL_OK;
+    const size_t act_dim = mlp ? hs->h : hs->d;
+    const size_t smem = sizeof(float) * ((mlp ? (size_t)hs->d * (hs->h / kCS) : 0) +
+                                         (size_t)(prm.W / kCS) * act_dim * 32 +
+                                         (size_t)kVT * hs->d + (size_t)kVT * (mlp ? hs->h : 0));
+    if (smem > 200 * 1024) return SPL_E_STATE;
+    SPL_CUDA_TRY(ctx, cudaFuncSetAttribute(k1_encode_cluster,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    const uint32_t ntiles = (nvec + kVT - 1) / kVT;
+    const uint32_t groups = std::max<uint32_t>(
+        1, std::min<uint32_t>(ntiles, (uint32_t)(2 * ctx->num_sms) / (kCS * hs->H)));
+    dim3 grid(groups * kCS, hs->H, njobs);
+    k1_encode_cluster<<<grid, kEncThreads, smem, s>>>(prm);
+    return after_launch(ctx, "k1_encode_cluster");
+}
+
 spl_status encode_exact_launch(spl_ctx* ctx, const spl_hasher* hs, uint32_t B,
                                const EncJob* jobs, int njobs, cudaStream_t s) {
+    if (cluster_eligible(hs)) {
+        const spl_status st = encode_cluster_launch(ctx, hs, B, jobs, njobs, s);
+        if (st != SPL_E_STATE) return st;
+    }
     EncParams prm{};
     const bool mlp = hs->kind == SPL_HASHER_MLP;
     prm.w1 = hs->w1;

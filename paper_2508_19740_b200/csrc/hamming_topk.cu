@@ -17,11 +17,10 @@
 // flushed into a u32 histogram before they can wrap) — a shared-atomic
 // histogram cannot keep up with ~1.5 rows/clk/SM.
 //
-// Fused path (k3_scan<..., FUSED>): when a CTA's scores fit in shared memory
-// (the headline 32 x 512K case), the kernel is launched cooperatively: scores
-// stay on chip, per-segment suffix-cumulative histograms go to global, one
-// grid barrier, then every CTA derives T / tie quota / its output offset and
-// compacts its rows from shared memory. One launch, one HBM pass.
+// Fused path (k3_fused, see below): when the scores fit in shared memory (the
+// headline 32 x 512K case), one cooperative launch streams, histograms,
+// derives T / tie quota / offsets and compacts from shared memory, with
+// per-problem barriers only. One launch, one HBM pass.
 // Two-pass path (k3_scan + k3_select): u8/u16 scores to an L2-resident
 // buffer; the CTA finishing a problem's last segment plans it; k3_select
 // compacts. Used for caches too large for on-chip scores and for the
@@ -31,7 +30,9 @@
 #include <stdint.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <string>
+#include <vector>
 
 #include "spl_launch.cuh"
 #include "spl_plan.cuh"
@@ -77,10 +78,11 @@ struct K3Params {
     uint32_t* dev_err;
     int shard;             // 1: no planning; tot_hist = caller's histogram
     uint32_t score_region; // fused: bytes of shared memory for scores
+    uint64_t* trace;       // optional [G][8] globaltimer stamps (SPL_K3_TRACE)
 };
 
 constexpr int kThreads = 256;
-constexpr int kU = 4;  // 32-byte units per thread per load batch
+constexpr int kU = 2;  // 32-byte units per thread per load batch (x2 double-buffered)
 
 // ------------------------------------------------------------ block scans
 __device__ __forceinline__ uint64_t warp_incl_scan_u64(uint64_t v) {
@@ -466,7 +468,7 @@ __device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
     return v;
 }
 
-template <int W, typename ScoreT, bool PRIV, bool FUSED>
+template <int W, typename ScoreT, bool PRIV>
 __global__ void __launch_bounds__(kThreads) k3_scan(K3Params prm) {
     extern __shared__ __align__(16) uint8_t smem[];
     __shared__ uint64_t s_warp[kThreads / 32 + 1];
@@ -477,14 +479,12 @@ __global__ void __launch_bounds__(kThreads) k3_scan(K3Params prm) {
     const size_t priv_bytes = PRIV ? (((size_t)bins * kThreads + 15) & ~size_t(15)) : 0;
     uint8_t* priv = smem;
     uint32_t* hist32 = reinterpret_cast<uint32_t*>(smem + priv_bytes);  // [bins + 1]
-    uint8_t* sregion = smem + priv_bytes + (((size_t)(bins + 1) * 4 + 15) & ~size_t(15));
     const int tid = threadIdx.x;
     const K3Geom& g = prm.g;
 
     const uint64_t g0 = (uint64_t)blockIdx.x * g.S;
     const uint64_t g1 = min(g0 + g.S, g.total);
     const uint32_t p_first = (uint32_t)(g0 / g.n_max);
-    uint32_t region_off = 0;  // fused: byte offset of the current piece's scores
 
     // zero the counters once (flush_priv re-zeroes them)
     if constexpr (PRIV)
@@ -507,17 +507,8 @@ __global__ void __launch_bounds__(kThreads) k3_scan(K3Params prm) {
         if (r0 < r1) {
             const uint32_t* qp = prm.qcodes + (uint64_t)p * Wr;
             const uint32_t* base = prm.codes + (uint64_t)p * prm.stride_rows * Wr;
-            ScoreT* dst;
-            uint64_t dst_row0;
-            if (FUSED) {
-                dst_row0 = r0 & ~uint64_t(15);
-                dst = reinterpret_cast<ScoreT*>(sregion + region_off);
-                region_off += (uint32_t)((((r1 - dst_row0) * sizeof(ScoreT)) + 15) & ~uint64_t(15));
-            } else {
-                dst_row0 = 0;
-                dst = reinterpret_cast<ScoreT*>(prm.scores) + (uint64_t)p * g.n_pad;
-            }
-            stream_piece<W, ScoreT, PRIV, FUSED>(base, qp, L, r0, r1, dst, dst_row0, priv, hist32, bins);
+            ScoreT* dst = reinterpret_cast<ScoreT*>(prm.scores) + (uint64_t)p * g.n_pad;
+            stream_piece<W, ScoreT, PRIV, false>(base, qp, L, r0, r1, dst, 0, priv, hist32, bins);
         }
         __syncthreads();
         // raw counts -> global per-problem histogram (integer atomics: the
@@ -530,7 +521,7 @@ __global__ void __launch_bounds__(kThreads) k3_scan(K3Params prm) {
         uint32_t* rec = prm.records + (uint64_t)(blockIdx.x + p) * (L + 2);
         for (uint32_t t = tid; t < L + 2; t += kThreads) rec[t] = hist32[t];
 
-        if (!FUSED && !prm.shard) {
+        if (!prm.shard) {
             __threadfence();
             __syncthreads();
             if (tid == 0) {
@@ -554,16 +545,90 @@ __global__ void __launch_bounds__(kThreads) k3_scan(K3Params prm) {
         }
         __syncthreads();
     }
-    if constexpr (!FUSED) return;
+}
+
+// ------------------------------------------------------------ fused
+// Single-launch path for caches whose scores fit on chip (the headline
+// 32 x 512K case). Same contiguous-segment geometry as the two-pass path
+// (G = SMs x 3 CTAs at 80 registers), but scores stay in shared memory:
+// stream -> segment record + per-problem histogram (atomics) -> one grid
+// barrier (cooperative launch) -> each CTA derives T / tie quota from the
+// problem histogram and its output offset from the earlier segments'
+// records, then compacts its rows from shared memory.
+__device__ __forceinline__ uint64_t gtimer() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+#define K3_STAMP(i) \
+    if (prm.trace && threadIdx.x == 0) prm.trace[blockIdx.x * 8 + (i)] = gtimer()
+
+template <int W, typename ScoreT>
+__global__ void __launch_bounds__(kThreads) k3_fused(K3Params prm) {
+    extern __shared__ __align__(16) uint8_t smem[];
+    __shared__ uint64_t s_warp[kThreads / 32 + 1];
+    __shared__ uint32_t s_flag, s_T;
+    const uint32_t L = prm.L;
+    const uint32_t bins = L + 1;
+    const size_t priv_bytes = ((size_t)bins * kThreads + 15) & ~size_t(15);
+    const size_t hist_bytes = (((size_t)(bins + 1) * 4) + 15) & ~size_t(15);
+    uint8_t* priv = smem;
+    uint32_t* hist32 = reinterpret_cast<uint32_t*>(smem + priv_bytes);                // [bins + 1]
+    uint32_t* s_cum = reinterpret_cast<uint32_t*>(smem + priv_bytes + hist_bytes);    // [bins + 1]
+    uint8_t* sregion = smem + priv_bytes + 2 * hist_bytes;
+    const int tid = threadIdx.x;
+    const K3Geom& g = prm.g;
+    K3_STAMP(0);
+
+    const uint64_t g0 = (uint64_t)blockIdx.x * g.S;
+    const uint64_t g1 = min(g0 + g.S, g.total);
+    const uint32_t p_first = (uint32_t)(g0 / g.n_max);
+    uint32_t region_off = 0;  // byte offset of the current piece's scores
+
+    for (uint32_t i = tid; i < priv_bytes / 16; i += kThreads)
+        reinterpret_cast<uint4*>(priv)[i] = make_uint4(0, 0, 0, 0);
+
+    for (uint32_t p = p_first; p < g.P && (uint64_t)p * g.n_max < g1; ++p) {
+        const uint64_t pbase = (uint64_t)p * g.n_max;
+        const uint64_t lo = max(g0, pbase) - pbase;
+        const uint64_t hi = min(g1, pbase + g.n_max) - pbase;
+        uint32_t nv = prm.n_valid[p / prm.nvalid_div];
+        if (nv > g.n_max) {
+            if (tid == 0) raise_dev_err(prm.dev_err, SPL_DEV_ERR_DIMENSION);
+            nv = (uint32_t)g.n_max;
+        }
+        const uint64_t r0 = lo, r1 = min(hi, (uint64_t)nv);
+        for (uint32_t i = tid; i <= bins; i += kThreads) hist32[i] = 0;
+        __syncthreads();
+        if (r0 < r1) {
+            const uint64_t a0 = r0 & ~uint64_t(15);
+            ScoreT* dst = reinterpret_cast<ScoreT*>(sregion + region_off);
+            region_off += (uint32_t)((((r1 - a0) * sizeof(ScoreT)) + 15) & ~uint64_t(15));
+            stream_piece<W, ScoreT, true, true>(prm.codes + (uint64_t)p * prm.stride_rows * W,
+                                                prm.qcodes + (uint64_t)p * W, L, r0, r1, dst, a0,
+                                                priv, hist32, bins);
+        }
+        __syncthreads();
+        uint32_t* tot = prm.tot_hist + (uint64_t)p * prm.tot_stride;
+        for (uint32_t b = tid; b < bins; b += kThreads)
+            if (hist32[b]) atomicAdd(tot + b, hist32[b]);
+        __syncthreads();
+        block_suffix_sum(hist32, bins, s_warp);  // hist32[bins] stays 0
+        uint32_t* rec = prm.records + (uint64_t)(blockIdx.x + p) * (L + 2);
+        for (uint32_t t = tid; t < L + 2; t += kThreads) rec[t] = hist32[t];
+        __syncthreads();
+    }
+    K3_STAMP(1);
 
     // ---------------- grid barrier (cooperative launch: all CTAs resident)
     __threadfence();
     __syncthreads();
     if (tid == 0) {
         atomicAdd(prm.sync, 1u);
-        while (ld_acquire(prm.sync) < gridDim.x) __nanosleep(64);
+        while (ld_acquire(prm.sync) < gridDim.x) __nanosleep(32);
     }
     __syncthreads();
+    K3_STAMP(2);
 
     // ---------------- plan + select from shared memory
     region_off = 0;
@@ -576,8 +641,9 @@ __global__ void __launch_bounds__(kThreads) k3_scan(K3Params prm) {
         const uint64_t r0 = lo, r1 = min(hi, (uint64_t)nv);
         const uint32_t kk = prm.k < nv ? prm.k : nv;
         uint32_t T, quota;
-        problem_threshold(prm.tot_hist + (uint64_t)p * prm.tot_stride, L, kk, hist32, s_warp, &s_T,
-                          T, quota);
+        problem_threshold(prm.tot_hist + (uint64_t)p * prm.tot_stride, L, kk, s_cum, s_warp, &s_T, T,
+                          quota);
+        K3_STAMP(3);
         const uint32_t c0 = seg_first(g, p);
         if (tid == 0 && blockIdx.x == c0) prm.cnt_out[p] = kk;
         if (r0 >= r1) continue;
@@ -585,7 +651,7 @@ __global__ void __launch_bounds__(kThreads) k3_scan(K3Params prm) {
         const ScoreT* sc = reinterpret_cast<const ScoreT*>(sregion + region_off);
         region_off += (uint32_t)((((r1 - a0) * sizeof(ScoreT)) + 15) & ~uint64_t(15));
         if (T == SPL_PLAN_SKIP) continue;
-        // counts of the earlier segments of this problem (their records)
+        // (gt, eq) of the earlier segments of this problem, from their records
         uint64_t gt_before = 0, eq_before = 0;
         for (uint32_t cb = c0; cb < blockIdx.x; cb += kThreads) {
             const uint32_t c = cb + tid;
@@ -596,19 +662,23 @@ __global__ void __launch_bounds__(kThreads) k3_scan(K3Params prm) {
                 gtv = geT1;
                 eqv = geT - geT1;
             }
-            uint64_t tot;
-            block_excl_scan_u64(((uint64_t)eqv << 32) | gtv, s_warp, tot);
-            gt_before += tot & 0xffffffffu;
-            eq_before += tot >> 32;
+            uint64_t totv;
+            block_excl_scan_u64(((uint64_t)eqv << 32) | gtv, s_warp, totv);
+            gt_before += totv & 0xffffffffu;
+            eq_before += totv >> 32;
         }
-        const uint64_t left = quota > eq_before ? quota - eq_before : 0;
+        K3_STAMP(4);
+        // own record: this CTA's last piece record is still in hist32; an
+        // earlier piece's (CTA spans two problems) is re-read from global
         const uint32_t* own = prm.records + (uint64_t)(blockIdx.x + p) * (L + 2);
         const uint64_t eq_mine = (uint64_t)__ldcg(own + T) - __ldcg(own + T + 1);
+        const uint64_t left = quota > eq_before ? quota - eq_before : 0;
         const uint32_t take = (uint32_t)(eq_mine < left ? eq_mine : left);
         const uint64_t off = gt_before + (eq_before < quota ? eq_before : quota);
         select_rows<ScoreT, false>(sc, a0, r0, r1, T, take,
                                    prm.idx_out + (uint64_t)p * prm.idx_stride + off, s_warp);
     }
+    K3_STAMP(5);
 
     // ---------------- completion: the last CTA resets the shared state
     __threadfence();
@@ -696,106 +766,158 @@ namespace {
 
 size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
+// two-pass plan (also the sharded flow)
 struct K3Plan {
     K3Geom g;
     bool vec;
     bool priv;
-    bool fused;
     size_t smem;
     size_t score_bytes;
-    uint32_t score_region;
 };
 
-template <int W, typename ScoreT, bool PRIV, bool FUSED>
+template <int W, typename ScoreT, bool PRIV>
 const void* scan_fn() {
-    return reinterpret_cast<const void*>(&k3_scan<W, ScoreT, PRIV, FUSED>);
+    return reinterpret_cast<const void*>(&k3_scan<W, ScoreT, PRIV>);
 }
-template <typename ScoreT, bool PRIV, bool FUSED>
+template <typename ScoreT, bool PRIV>
 const void* pick_w(uint32_t W) {
     switch (W) {
-        case 1: return scan_fn<1, ScoreT, PRIV, FUSED>();
-        case 2: return scan_fn<2, ScoreT, PRIV, FUSED>();
-        case 4: return scan_fn<4, ScoreT, PRIV, FUSED>();
-        case 8: return scan_fn<8, ScoreT, PRIV, FUSED>();
-        default: return scan_fn<0, ScoreT, PRIV, FUSED>();  // any W, 32-bit loads
+        case 1: return scan_fn<1, ScoreT, PRIV>();
+        case 2: return scan_fn<2, ScoreT, PRIV>();
+        case 4: return scan_fn<4, ScoreT, PRIV>();
+        case 8: return scan_fn<8, ScoreT, PRIV>();
+        default: return scan_fn<0, ScoreT, PRIV>();  // any W, 32-bit loads
     }
-}
-template <typename ScoreT>
-const void* pick_st(uint32_t W, bool priv, bool fused) {
-    if (priv) return fused ? pick_w<ScoreT, true, true>(W) : pick_w<ScoreT, true, false>(W);
-    return fused ? pick_w<ScoreT, false, true>(W) : pick_w<ScoreT, false, false>(W);
 }
 const void* pick_scan(const K3Plan& pl, uint32_t L) {
     const uint32_t W = pl.vec ? L / 32 : 0;
-    return L <= 255 ? pick_st<uint8_t>(W, pl.priv, pl.fused) : pick_st<uint16_t>(W, pl.priv, pl.fused);
+    if (L <= 255) return pl.priv ? pick_w<uint8_t, true>(W) : pick_w<uint8_t, false>(W);
+    return pl.priv ? pick_w<uint16_t, true>(W) : pick_w<uint16_t, false>(W);
 }
 
-size_t base_smem(uint32_t L, bool priv) {
-    const size_t bins = L + 1;
-    return (priv ? align_up(bins * kThreads, 16) : 0) + align_up((bins + 1) * 4, 16);
+bool vec_ok(const void* codes, uint64_t stride_rows, uint32_t W) {
+    return W <= 8 && 8 % W == 0 && (reinterpret_cast<uintptr_t>(codes) % 32) == 0 &&
+           (stride_rows * W * 4) % 32 == 0;
 }
 
-// allow_fused: try the single-launch cooperative path first.
 spl_status make_plan(spl_ctx* ctx, uint32_t P, uint64_t n_max, uint32_t L, const void* codes,
-                     uint64_t stride_rows, bool allow_fused, K3Plan* out) {
+                     uint64_t stride_rows, K3Plan* out) {
     K3Plan pl{};
     const uint32_t W = L / 32;
-    pl.vec = W <= 8 && 8 % W == 0 && (reinterpret_cast<uintptr_t>(codes) % 32) == 0 &&
-             (stride_rows * W * 4) % 32 == 0;
+    pl.vec = vec_ok(codes, stride_rows, W);
     pl.priv = (size_t)(L + 1) * kThreads <= 96 * 1024;
     pl.score_bytes = L <= 255 ? 1 : 2;
     const uint64_t total = (uint64_t)P * n_max;
-    const size_t base = base_smem(L, pl.priv);
-    int dev_max_smem = 0, sm_smem = 0;
-    SPL_CUDA_TRY(ctx, cudaDeviceGetAttribute(&dev_max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin,
-                                             ctx->device));
-    SPL_CUDA_TRY(ctx, cudaDeviceGetAttribute(&sm_smem, cudaDevAttrMaxSharedMemoryPerMultiprocessor,
-                                             ctx->device));
-    auto geom = [&](uint64_t G_target) {
-        K3Geom g{};
-        uint64_t S = (total + G_target - 1) / G_target;
-        S = align_up(std::max<uint64_t>(S, 1024), 256);
-        g.n_max = n_max;
-        g.total = total;
-        g.S = S;
-        g.G = (uint32_t)((total + S - 1) / S);
-        g.P = P;
-        g.n_pad = align_up(n_max, 64);
-        return g;
-    };
-    if (allow_fused) {
-        for (int cps = 3; cps >= 1; --cps) {
-            const K3Geom g = geom((uint64_t)ctx->num_sms * cps);
-            const uint64_t pieces = g.S / n_max + 2;
-            const size_t region =
-                align_up((size_t)(g.S + 16 * pieces) * pl.score_bytes + 16 * pieces, 16);
-            const size_t smem = base + region;
-            if (smem > (size_t)dev_max_smem || (smem + 1024 + 128) * cps > (size_t)sm_smem) continue;
-            K3Plan t = pl;
-            t.fused = true;
-            t.g = g;
-            t.smem = smem;
-            t.score_region = (uint32_t)region;
-            const void* fn = pick_scan(t, L);
-            SPL_CUDA_TRY(ctx, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                   (int)smem));
-            int per_sm = 0;
-            SPL_CUDA_TRY(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kThreads, smem));
-            if ((uint64_t)per_sm * ctx->num_sms < g.G) continue;
-            *out = t;
-            return SPL_OK;
-        }
-    }
-    pl.fused = false;
-    pl.smem = base;
+    pl.smem = (pl.priv ? align_up((size_t)(L + 1) * kThreads, 16) : 0) + align_up((size_t)(L + 2) * 4, 16);
     const void* fn = pick_scan(pl, L);
     SPL_CUDA_TRY(ctx, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            (int)pl.smem));
     int per_sm = 0;
     SPL_CUDA_TRY(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kThreads, pl.smem));
     if (per_sm < 1) per_sm = 1;
-    pl.g = geom((uint64_t)ctx->num_sms * per_sm);
+    const uint64_t G_target = (uint64_t)ctx->num_sms * per_sm;
+    uint64_t S = (total + G_target - 1) / G_target;
+    S = align_up(std::max<uint64_t>(S, 1024), 256);
+    pl.g.n_max = n_max;
+    pl.g.total = total;
+    pl.g.S = S;
+    pl.g.G = (uint32_t)((total + S - 1) / S);
+    pl.g.P = P;
+    pl.g.n_pad = align_up(n_max, 64);
     *out = pl;
+    return SPL_OK;
+}
+
+// fused plan: geometry + launch shape when the scores fit on chip
+struct K3FPlan {
+    K3Plan pl;
+    size_t smem;
+    const void* fn;
+};
+
+template <int W, typename ScoreT>
+const void* fused_fn() {
+    return reinterpret_cast<const void*>(&k3_fused<W, ScoreT>);
+}
+
+spl_status make_fused_plan(spl_ctx* ctx, uint32_t P, uint64_t n_max, uint32_t L, const void* codes,
+                           uint64_t stride_rows, bool* ok, K3FPlan* out) {
+    *ok = false;
+    const uint32_t W = L / 32;
+    if (!vec_ok(codes, stride_rows, W) || (size_t)(L + 1) * kThreads > 96 * 1024) return SPL_OK;
+    const void* fn = nullptr;
+    if (L <= 255) {
+        switch (W) {
+            case 1: fn = fused_fn<1, uint8_t>(); break;
+            case 2: fn = fused_fn<2, uint8_t>(); break;
+            case 4: fn = fused_fn<4, uint8_t>(); break;
+            default: return SPL_OK;
+        }
+    } else if (W == 8) {
+        fn = fused_fn<8, uint16_t>();
+    } else {
+        return SPL_OK;
+    }
+    const size_t sb = L <= 255 ? 1 : 2;
+    const uint64_t total = (uint64_t)P * n_max;
+    const size_t base = align_up((size_t)(L + 1) * kThreads, 16) + 2 * align_up((size_t)(L + 2) * 4, 16);
+    int dev_max_smem = 0, sm_smem = 0;
+    SPL_CUDA_TRY(ctx, cudaDeviceGetAttribute(&dev_max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin,
+                                             ctx->device));
+    SPL_CUDA_TRY(ctx, cudaDeviceGetAttribute(&sm_smem, cudaDevAttrMaxSharedMemoryPerMultiprocessor,
+                                             ctx->device));
+    for (int cps = 3; cps >= 1; --cps) {
+        const uint64_t G_target = (uint64_t)ctx->num_sms * cps;
+        uint64_t S = (total + G_target - 1) / G_target;
+        S = align_up(std::max<uint64_t>(S, 1024), 256);
+        const uint64_t pieces = S / n_max + 2;
+        const size_t region = align_up((size_t)(S + 16 * pieces) * sb + 16 * pieces, 16);
+        const size_t smem = base + region;
+        if (smem > (size_t)dev_max_smem || (smem + 1024 + 256) * cps > (size_t)sm_smem) continue;
+        SPL_CUDA_TRY(ctx, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        int per_sm = 0;
+        SPL_CUDA_TRY(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kThreads, smem));
+        const uint64_t G = (total + S - 1) / S;
+        if ((uint64_t)per_sm * ctx->num_sms < G) continue;
+        K3Plan& pl = out->pl;
+        pl = K3Plan{};
+        pl.vec = true;
+        pl.priv = true;
+        pl.score_bytes = sb;
+        pl.g.n_max = n_max;
+        pl.g.total = total;
+        pl.g.S = S;
+        pl.g.G = (uint32_t)G;
+        pl.g.P = P;
+        pl.g.n_pad = align_up(n_max, 64);
+        out->smem = smem;
+        out->fn = fn;
+        *ok = true;
+        return SPL_OK;
+    }
+    return SPL_OK;
+}
+
+// Persistent zeroed per-problem state (self-resetting after every launch):
+// [2 spare][counters P][tot P x (L+2)][bar P x 4]
+struct K3State {
+    uint32_t* sync;
+    uint32_t* counters;
+    uint32_t* tot;
+    uint32_t* bar;
+};
+
+spl_status k3_state(spl_ctx* ctx, uint32_t P, uint32_t L, cudaStream_t s, K3State* st) {
+    const size_t words = 2 + (size_t)P * (1 + (L + 2) + 4);
+    size_t have = ctx->k3_state_words * 4;
+    spl_status e = ensure_buffer(ctx, reinterpret_cast<void**>(&ctx->k3_state), &have, words * 4,
+                                 true, s, "hamming_topk");
+    if (e) return e;
+    ctx->k3_state_words = have / 4;
+    st->sync = ctx->k3_state;
+    st->counters = ctx->k3_state + 2;
+    st->tot = st->counters + P;
+    st->bar = st->tot + (size_t)P * (L + 2);
     return SPL_OK;
 }
 
@@ -803,31 +925,20 @@ struct K3Ws {
     void* scores;
     uint32_t* records;
     uint4* plans;
-    uint32_t* sync;
-    uint32_t* counters;
-    uint32_t* tot;
 };
 
-spl_status k3_workspace(spl_ctx* ctx, const K3Plan& pl, uint32_t L, cudaStream_t s, K3Ws* ws) {
-    const size_t sc = pl.fused ? 0 : align_up((size_t)pl.g.P * pl.g.n_pad * pl.score_bytes, 256);
+spl_status k3_workspace(spl_ctx* ctx, const K3Plan& pl, uint32_t L, cudaStream_t s, K3Ws* ws,
+                        bool global_scores = true) {
+    const size_t sc = global_scores ? align_up((size_t)pl.g.P * pl.g.n_pad * pl.score_bytes, 256) : 0;
     const size_t rec = align_up((size_t)(pl.g.G + pl.g.P) * (L + 2) * 4, 256);
     const size_t plans = align_up((size_t)(pl.g.G + pl.g.P) * 16, 256);
     spl_status st = ensure_buffer(ctx, &ctx->k3_ws, &ctx->k3_ws_bytes, sc + rec + plans, false, s,
                                   "hamming_topk");
     if (st) return st;
-    const size_t state_words = 2 + (size_t)pl.g.P * (1 + (L + 2));
-    size_t have = ctx->k3_state_words * 4;
-    st = ensure_buffer(ctx, reinterpret_cast<void**>(&ctx->k3_state), &have, state_words * 4, true,
-                       s, "hamming_topk");
-    if (st) return st;
-    ctx->k3_state_words = have / 4;
     uint8_t* b = static_cast<uint8_t*>(ctx->k3_ws);
     ws->scores = b;
     ws->records = reinterpret_cast<uint32_t*>(b + sc);
     ws->plans = reinterpret_cast<uint4*>(b + sc + rec);
-    ws->sync = ctx->k3_state;
-    ws->counters = ctx->k3_state + 2;
-    ws->tot = ctx->k3_state + 2 + pl.g.P;
     return SPL_OK;
 }
 
@@ -848,11 +959,8 @@ spl_status validate_common(spl_ctx* ctx, const char* who, const uint32_t* codes,
 spl_status launch_scan(spl_ctx* ctx, const K3Plan& pl, const K3Params& prm, cudaStream_t s) {
     const void* fn = pick_scan(pl, prm.L);
     void* args[] = {const_cast<K3Params*>(&prm)};
-    if (pl.fused)
-        SPL_CUDA_TRY(ctx, cudaLaunchCooperativeKernel(fn, dim3(pl.g.G), dim3(kThreads), args, pl.smem, s));
-    else
-        SPL_CUDA_TRY(ctx, cudaLaunchKernel(fn, dim3(pl.g.G), dim3(kThreads), args, pl.smem, s));
-    return after_launch(ctx, pl.fused ? "k3_scan(fused)" : "k3_scan");
+    SPL_CUDA_TRY(ctx, cudaLaunchKernel(fn, dim3(pl.g.G), dim3(kThreads), args, pl.smem, s));
+    return after_launch(ctx, "k3_scan");
 }
 
 spl_status launch_select(spl_ctx* ctx, const K3Plan& pl, const K3Params& prm, uint32_t* idx,
@@ -864,9 +972,10 @@ spl_status launch_select(spl_ctx* ctx, const K3Plan& pl, const K3Params& prm, ui
     return after_launch(ctx, "k3_select");
 }
 
-K3Params base_params(spl_ctx* ctx, const K3Plan& pl, const K3Ws& ws, const uint32_t* codes,
-                     uint64_t stride_rows, uint32_t L, const uint32_t* qcodes,
-                     const uint32_t* n_valid, uint32_t nvalid_div, uint32_t k) {
+K3Params base_params(spl_ctx* ctx, const K3Plan& pl, const K3Ws& ws, const K3State& kst,
+                     const uint32_t* codes, uint64_t stride_rows, uint32_t L,
+                     const uint32_t* qcodes, const uint32_t* n_valid, uint32_t nvalid_div,
+                     uint32_t k) {
     K3Params prm{};
     prm.codes = codes;
     prm.stride_rows = stride_rows;
@@ -879,13 +988,12 @@ K3Params base_params(spl_ctx* ctx, const K3Plan& pl, const K3Ws& ws, const uint3
     prm.g = pl.g;
     prm.scores = ws.scores;
     prm.records = ws.records;
-    prm.tot_hist = ws.tot;
+    prm.tot_hist = kst.tot;
     prm.tot_stride = L + 2;
-    prm.counters = ws.counters;
-    prm.sync = ws.sync;
+    prm.counters = kst.counters;
+    prm.sync = kst.sync;
     prm.plans = ws.plans;
     prm.dev_err = ctx->dev_err;
-    prm.score_region = pl.score_region;
     return prm;
 }
 
@@ -911,17 +1019,62 @@ spl_status hamming_topk_impl(spl_ctx* ctx, const uint32_t* codes, uint64_t strid
         return SPL_OK;
     }
     if (n_max > 0xFFFFFFFFull) return fail(ctx, SPL_E_DIMENSION, "hamming_topk: n_max exceeds 2^32 rows");
+    K3State kst;
+    if ((st = k3_state(ctx, P, L, s, &kst))) return st;
+    if (fused_allowed()) {
+        bool ok = false;
+        K3FPlan fp{};
+        if ((st = make_fused_plan(ctx, P, n_max, L, codes, stride_rows, &ok, &fp))) return st;
+        if (ok) {
+            K3Ws ws;
+            if ((st = k3_workspace(ctx, fp.pl, L, s, &ws, false))) return st;
+            K3Params prm =
+                base_params(ctx, fp.pl, ws, kst, codes, stride_rows, L, qcodes, n_valid, nvalid_div, k);
+            prm.cnt_out = cnt;
+            prm.idx_out = idx;
+            prm.idx_stride = k;
+            const uint32_t G = fp.pl.g.G;
+            const char* tr = getenv("SPL_K3_TRACE");
+            uint64_t* dtrace = nullptr;
+            if (tr && *tr && !stream_capturing(s)) SPL_CUDA_TRY(ctx, cudaMalloc(&dtrace, (size_t)G * 8 * 8));
+            prm.trace = dtrace;
+            void* args[] = {&prm};
+            SPL_CUDA_TRY(ctx, cudaLaunchCooperativeKernel(fp.fn, dim3(G), dim3(kThreads), args, fp.smem, s));
+            st = after_launch(ctx, "k3_fused");
+            if (dtrace) {
+                std::vector<uint64_t> h((size_t)G * 8);
+                cudaStreamSynchronize(s);
+                cudaMemcpy(h.data(), dtrace, h.size() * 8, cudaMemcpyDeviceToHost);
+                cudaFree(dtrace);
+                uint64_t t0 = ~0ull;
+                for (uint32_t i = 0; i < G; ++i) t0 = std::min(t0, h[i * 8]);
+                double mx[6] = {0}, mean[6] = {0};
+                for (uint32_t i = 0; i < G; ++i)
+                    for (int j = 0; j < 6; ++j) {
+                        const double v = (double)(h[i * 8 + j] - t0) / 1000.0;
+                        mx[j] = std::max(mx[j], v);
+                        mean[j] += v / G;
+                    }
+                fprintf(stderr, "k3_fused trace G=%u S=%llu [start, stream, barrier, thresh, prefix, select] mean:",
+                        G, (unsigned long long)fp.pl.g.S);
+                for (int j = 0; j < 6; ++j) fprintf(stderr, " %.1f", mean[j]);
+                fprintf(stderr, "  max:");
+                for (int j = 0; j < 6; ++j) fprintf(stderr, " %.1f", mx[j]);
+                fprintf(stderr, " us\n");
+            }
+            return st;
+        }
+    }
     K3Plan pl;
-    if ((st = make_plan(ctx, P, n_max, L, codes, stride_rows, fused_allowed(), &pl))) return st;
+    if ((st = make_plan(ctx, P, n_max, L, codes, stride_rows, &pl))) return st;
     K3Ws ws;
     if ((st = k3_workspace(ctx, pl, L, s, &ws))) return st;
-    K3Params prm = base_params(ctx, pl, ws, codes, stride_rows, L, qcodes, n_valid, nvalid_div, k);
+    K3Params prm = base_params(ctx, pl, ws, kst, codes, stride_rows, L, qcodes, n_valid, nvalid_div, k);
     prm.cnt_out = cnt;
     prm.idx_out = idx;
     prm.idx_stride = k;
     prm.shard = 0;
     if ((st = launch_scan(ctx, pl, prm, s))) return st;
-    if (pl.fused) return SPL_OK;
     return launch_select(ctx, pl, prm, idx, k, s);
 }
 
@@ -941,12 +1094,14 @@ spl_status shard_histogram_impl(spl_ctx* ctx, const uint32_t* codes, uint64_t st
         return SPL_OK;
     }
     K3Plan pl;
-    if ((st = make_plan(ctx, P, n_max, L, codes, stride_rows, false, &pl))) return st;
+    if ((st = make_plan(ctx, P, n_max, L, codes, stride_rows, &pl))) return st;
     K3Ws ws;
     if ((st = k3_workspace(ctx, pl, L, s, &ws))) return st;
+    K3State kst;
+    if ((st = k3_state(ctx, P, L, s, &kst))) return st;
     ctx->shard_G = pl.g.G;
     ctx->shard_S = pl.g.S;
-    K3Params prm = base_params(ctx, pl, ws, codes, stride_rows, L, qcodes, n_valid, nvalid_div, 1);
+    K3Params prm = base_params(ctx, pl, ws, kst, codes, stride_rows, L, qcodes, n_valid, nvalid_div, 1);
     prm.tot_hist = hist;
     prm.tot_stride = L + 1;
     prm.shard = 1;
@@ -978,7 +1133,9 @@ spl_status shard_select_impl(spl_ctx* ctx, const uint32_t* all_hist, uint32_t R,
     pl.score_bytes = L <= 255 ? 1 : 2;
     K3Ws ws;
     if ((st = k3_workspace(ctx, pl, L, s, &ws))) return st;
-    K3Params prm = base_params(ctx, pl, ws, nullptr, 0, L, nullptr, n_valid, nvalid_div, k);
+    K3State kst;
+    if ((st = k3_state(ctx, P, L, s, &kst))) return st;
+    K3Params prm = base_params(ctx, pl, ws, kst, nullptr, 0, L, nullptr, n_valid, nvalid_div, k);
     prm.cnt_out = cnt;
     prm.shard = 1;
     k3_shard_plan<<<P, kThreads, 0, s>>>(prm, all_hist, R, rank, out_offset);

@@ -2,13 +2,22 @@
 //
 // Replaces sparse_attention (attention_eval.cpp:234-264) + attend_subset
 // (:54-78): per problem, softmax(q K_S^T * scale) V_S over S = picked U {own}
-// (the own row n_valid - 1 is always attended, :249-260). Flash-decoding:
-// the row list is split across CTAs (grid = splits x problems); each warp
-// gathers 8 rows at a time (lane owns d/32 contiguous dims, one coalesced
-// 8 B (bf16) / 16 B (f32) load per lane per row), keeps an online-softmax
-// (m, l, o) in fp32 registers (log2 domain: q is pre-scaled by
-// scale*log2(e)), warps merge in shared memory, and the CTA that finishes a
-// problem's last split performs the log-sum-exp combine (K5) — one launch.
+// (the own row n_valid - 1 is always attended, :249-260), fp32 accumulation.
+//
+// Flash-decoding split: a CTA (4 warps) takes 128 consecutive entries of the
+// problem's row list; grid = splits x problems.
+//   * logits, lane-per-row: lane i of a warp gathers its own K row with
+//     16-byte loads (8 in flight) and dots it with q held in shared memory
+//     (q pre-scaled by scale * log2(e): base-2 softmax), 4 partial sums —
+//     no cross-lane reduction per row;
+//   * warp softmax over its 32 rows (max / sum: 5 shuffles each);
+//   * values, lane-per-dims: lane owns d/32 contiguous dims; for each row the
+//     probability and row id are broadcast by shuffle and the V slice is one
+//     coalesced 8 B (bf16) / 16 B (f32) load per lane, 8-16 rows in flight;
+//   * warps merge (m, l, o) in shared memory; the CTA finishing a problem's
+//     last split performs the log-sum-exp combine (K5) — one launch.
+// Tolerance vs the reference (different summation order): max-abs 1e-5 with
+// f32 K/V, 1e-3 with bf16 K/V (tests/test_gpu_parity.py).
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -22,16 +31,55 @@ namespace spl {
 
 constexpr int kAttThreads = 128;
 constexpr int kAttWarps = kAttThreads / 32;
-constexpr int kGroup = 8;  // rows in flight per warp
+constexpr uint32_t kWarpRows = 32;  // one row per lane for the logits
+constexpr uint32_t kInv = 0xFFFFFFFFu;
 
-// Raw (undecoded) row slice of one lane: E elements of a K or V row. Loaded
-// as one coalesced vector per lane (warp = one full row), decoded to fp32 at
-// use, so the double buffer costs E/2 (bf16) or E (f32) registers per row.
+__device__ __forceinline__ float bf16lo(uint32_t w) { return __uint_as_float(w << 16); }
+__device__ __forceinline__ float bf16hi(uint32_t w) { return __uint_as_float(w & 0xffff0000u); }
+
+// dot(q_s, K row) over D values, the row read as 16-byte chunks.
+template <int D, typename KV>
+__device__ __forceinline__ float row_dot(const KV* row, const float* q_s) {
+    constexpr int NPER = 16 / (int)sizeof(KV);  // elements per 16-byte chunk
+    constexpr int NCH = D / NPER;
+    constexpr int BATCH = NCH < 8 ? NCH : 8;
+    float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+    const uint4* p = reinterpret_cast<const uint4*>(row);
+#pragma unroll
+    for (int b0 = 0; b0 < NCH; b0 += BATCH) {
+        uint4 v[BATCH];
+#pragma unroll
+        for (int i = 0; i < BATCH; ++i) v[i] = __ldg(p + b0 + i);
+#pragma unroll
+        for (int i = 0; i < BATCH; ++i) {
+            const int e0 = (b0 + i) * NPER;
+            const float4 qa = *reinterpret_cast<const float4*>(q_s + e0);
+            if constexpr (sizeof(KV) == 2) {
+                const float4 qb = *reinterpret_cast<const float4*>(q_s + e0 + 4);
+                a0 = fmaf(qa.x, bf16lo(v[i].x), a0);
+                a1 = fmaf(qa.y, bf16hi(v[i].x), a1);
+                a2 = fmaf(qa.z, bf16lo(v[i].y), a2);
+                a3 = fmaf(qa.w, bf16hi(v[i].y), a3);
+                a0 = fmaf(qb.x, bf16lo(v[i].z), a0);
+                a1 = fmaf(qb.y, bf16hi(v[i].z), a1);
+                a2 = fmaf(qb.z, bf16lo(v[i].w), a2);
+                a3 = fmaf(qb.w, bf16hi(v[i].w), a3);
+            } else {
+                a0 = fmaf(qa.x, __uint_as_float(v[i].x), a0);
+                a1 = fmaf(qa.y, __uint_as_float(v[i].y), a1);
+                a2 = fmaf(qa.z, __uint_as_float(v[i].z), a2);
+                a3 = fmaf(qa.w, __uint_as_float(v[i].w), a3);
+            }
+        }
+    }
+    return (a0 + a1) + (a2 + a3);
+}
+
+// A lane's E-element slice of a V row.
 template <int E, typename KV>
-struct Raw;
+struct VSlice;
 template <int E>
-struct Raw<E, __nv_bfloat16> {
-    static_assert(E == 1 || E == 2 || E == 4 || E == 8, "E");
+struct VSlice<E, __nv_bfloat16> {
     uint32_t u[(E + 1) / 2];
     __device__ __forceinline__ void load(const __nv_bfloat16* row, int lane) {
         const __nv_bfloat16* p = row + lane * E;
@@ -48,12 +96,11 @@ struct Raw<E, __nv_bfloat16> {
         }
     }
     __device__ __forceinline__ float get(int e) const {
-        const uint32_t w = u[e / 2];
-        return __uint_as_float((e & 1) ? (w & 0xffff0000u) : (w << 16));
+        return (e & 1) ? bf16hi(u[e / 2]) : bf16lo(u[e / 2]);
     }
 };
 template <int E>
-struct Raw<E, float> {
+struct VSlice<E, float> {
     float f[E];
     __device__ __forceinline__ void load(const float* row, int lane) {
         const float* p = row + lane * E;
@@ -73,83 +120,31 @@ struct Raw<E, float> {
     __device__ __forceinline__ float get(int e) const { return f[e]; }
 };
 
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
     return v;
 }
 
-constexpr uint32_t kInv = 0xFFFFFFFFu;
-constexpr uint32_t kWarpRows = 64;  // rows per warp per split (2 indices per lane)
-
-// rows per in-flight group: 8, or 4 when a lane's slice of a row is >= 32 B
-template <int E, typename KV>
-constexpr int group_rows() {
-    return E * (int)sizeof(KV) >= 32 ? 4 : kGroup;
-}
-
-template <int E, typename KV>
-struct Group {
-    static constexpr int G = group_rows<E, KV>();
-    Raw<E, KV> k[G], v[G];
-    uint32_t row[G];
-    __device__ __forceinline__ void issue(uint32_t rid, int sub, const KV* kb, const KV* vb,
-                                          int lane) {
-#pragma unroll
-        for (int r = 0; r < G; ++r) {
-            row[r] = __shfl_sync(0xffffffffu, rid, sub * G + r);
-            if (row[r] != kInv) {
-                k[r].load(kb + (uint64_t)row[r] * (32 * E), lane);
-                v[r].load(vb + (uint64_t)row[r] * (32 * E), lane);
-            }
-        }
-    }
-};
-
-template <int E, typename KV>
-__device__ __forceinline__ void consume(const Group<E, KV>& g, const float* qv, float& m, float& l,
-                                        float* o) {
-    constexpr int G = Group<E, KV>::G;
-    float s[G];
-    float gmax = -INFINITY;
-#pragma unroll
-    for (int r = 0; r < G; ++r) {
-        float part = 0.0f;
-#pragma unroll
-        for (int e = 0; e < E; ++e) part = fmaf(qv[e], g.k[r].get(e), part);
-        part = warp_sum(part);
-        s[r] = g.row[r] != kInv ? part : -INFINITY;
-        gmax = fmaxf(gmax, s[r]);
-    }
-    if (gmax == -INFINITY) return;
-    const float m_new = fmaxf(m, gmax);
-    const float corr = exp2f(m - m_new);  // m = -inf -> 0
-    l *= corr;
-#pragma unroll
-    for (int e = 0; e < E; ++e) o[e] *= corr;
-#pragma unroll
-    for (int r = 0; r < G; ++r) {
-        if (g.row[r] == kInv) continue;  // never touch unloaded registers
-        const float w = exp2f(s[r] - m_new);
-        l += w;
-#pragma unroll
-        for (int e = 0; e < E; ++e) o[e] = fmaf(w, g.v[r].get(e), o[e]);
-    }
-    m = m_new;
-}
-
-// E = d / 32 elements per lane (d in {32, 64, 128, 256}). A split is
-// kAttWarps x kWarpRows rows; each warp prefetches its 64 row ids (2 per
-// lane) once, then streams 8-row groups with the next group's K/V gathers in
-// flight while the current group is reduced.
+// E = d / 32 elements per lane (d in {32, 64, 128, 256}).
 template <int E, typename KV>
 __global__ void __launch_bounds__(kAttThreads) k4_sparse_attend(AttParams prm) {
     constexpr int D = 32 * E;
+    constexpr int VB = sizeof(KV) * E >= 16 ? 8 : 16;  // V rows in flight per lane
+    __shared__ __align__(16) float q_s[D];
     __shared__ float s_m[kAttWarps], s_l[kAttWarps];
     __shared__ float s_o[kAttWarps][D];
+    __shared__ float s_cmb[2][kAttThreads];  // combine: per-split scale, l
     __shared__ uint32_t s_last;
     const uint32_t p = blockIdx.y, split = blockIdx.x;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+
+    for (int i = tid; i < D; i += kAttThreads) q_s[i] = prm.q[(uint64_t)p * D + i] * prm.qscale;
 
     const uint32_t c = prm.cnt[p];
     const uint32_t* list = prm.idx + (uint64_t)p * prm.idx_stride;
@@ -161,37 +156,40 @@ __global__ void __launch_bounds__(kAttThreads) k4_sparse_attend(AttParams prm) {
     const bool has_own = own != kInv;
     const bool own_listed = has_own && c > 0 && __ldg(list + c - 1) == own;
     const uint32_t nrows = c + ((has_own && !own_listed) ? 1u : 0u);
-
     const KV* kbase = static_cast<const KV*>(prm.kc) + (uint64_t)p * prm.stride_rows * D;
     const KV* vbase = static_cast<const KV*>(prm.vc) + (uint64_t)p * prm.stride_rows * D;
 
     const uint32_t wb = split * prm.rows_per_split + warp * kWarpRows;
     const uint32_t we = min(wb + kWarpRows, nrows);
-    auto row_at = [&](uint32_t j) -> uint32_t {
-        return j < we ? (j < c ? __ldg(list + j) : own) : kInv;
-    };
-    const uint32_t rid0 = row_at(wb + lane), rid1 = row_at(wb + 32 + lane);
+    const uint32_t nr = we > wb ? we - wb : 0;  // rows of this warp (warp-uniform)
+    const uint32_t j = wb + lane;
+    const uint32_t rid = j < we ? (j < c ? __ldg(list + j) : own) : kInv;
+    __syncthreads();  // q_s
 
-    float qv[E];
-#pragma unroll
-    for (int e = 0; e < E; ++e) qv[e] = prm.q[(uint64_t)p * D + lane * E + e] * prm.qscale;
     float m = -INFINITY, l = 0.0f, o[E];
 #pragma unroll
     for (int e = 0; e < E; ++e) o[e] = 0.0f;
-
-    if (wb < we) {
-        constexpr int G = Group<E, KV>::G;
-        constexpr int PER_RID = 32 / G;  // groups per 32 prefetched ids
-        const int ngroups = (int)((we - wb + G - 1) / G);
-        Group<E, KV> ga, gb;
-        ga.issue(rid0, 0, kbase, vbase, lane);
-        for (int gi = 0; gi < ngroups; gi += 2) {
-            const int g1 = gi + 1, g2 = gi + 2;
-            if (g1 < ngroups) gb.issue(g1 < PER_RID ? rid0 : rid1, g1 % PER_RID, kbase, vbase, lane);
-            consume(ga, qv, m, l, o);
-            if (g1 >= ngroups) break;
-            if (g2 < ngroups) ga.issue(g2 < PER_RID ? rid0 : rid1, g2 % PER_RID, kbase, vbase, lane);
-            consume(gb, qv, m, l, o);
+    if (nr > 0) {
+        float s = -INFINITY;
+        if (rid != kInv) s = row_dot<D, KV>(kbase + (uint64_t)rid * D, q_s);
+        m = warp_max(s);
+        const float pr = rid != kInv ? exp2f(s - m) : 0.0f;
+        l = warp_sum(pr);
+        for (uint32_t r0 = 0; r0 < nr; r0 += VB) {
+            VSlice<E, KV> vv[VB];
+            float pw[VB];
+#pragma unroll
+            for (int i = 0; i < VB; ++i) {
+                const uint32_t rr = __shfl_sync(0xffffffffu, rid, (r0 + i) & 31);
+                pw[i] = __shfl_sync(0xffffffffu, pr, (r0 + i) & 31);
+                if (r0 + i < nr) vv[i].load(vbase + (uint64_t)rr * D, lane);
+            }
+#pragma unroll
+            for (int i = 0; i < VB; ++i) {
+                if (r0 + i >= nr) break;
+#pragma unroll
+                for (int e = 0; e < E; ++e) o[e] = fmaf(pw[i], vv[i].get(e), o[e]);
+            }
         }
     }
 
@@ -233,25 +231,59 @@ __global__ void __launch_bounds__(kAttThreads) k4_sparse_attend(AttParams prm) {
     __syncthreads();
     if (!s_last) return;
     __threadfence();
+    // Combine in parallel: every (m, l) of the splits is fetched at once into
+    // shared memory (one L2 round trip), the per-split scale factors computed
+    // there, then each thread owns one output dim and streams the splits'
+    // o[dim] with independent loads.
     const float* parts = prm.partials + (uint64_t)p * prm.nsplit * (D + 2);
-    float Mx = -INFINITY;
-    for (uint32_t sidx = 0; sidx < prm.nsplit; ++sidx)
-        Mx = fmaxf(Mx, __ldcg(parts + (uint64_t)sidx * (D + 2)));
-    float Lx = 0.0f;
-    for (uint32_t sidx = 0; sidx < prm.nsplit; ++sidx) {
-        const float ms = __ldcg(parts + (uint64_t)sidx * (D + 2));
-        if (ms != -INFINITY) Lx += __ldcg(parts + (uint64_t)sidx * (D + 2) + 1) * exp2f(ms - Mx);
-    }
-    for (int i = tid; i < D; i += kAttThreads) {
-        float acc = 0.0f;
-        for (uint32_t sidx = 0; sidx < prm.nsplit; ++sidx) {
-            const float ms = __ldcg(parts + (uint64_t)sidx * (D + 2));
-            if (ms != -INFINITY) acc += __ldcg(parts + (uint64_t)sidx * (D + 2) + 2 + i) * exp2f(ms - Mx);
+    float Mx = -INFINITY, Lx = 0.0f;
+    float acc[(D + kAttThreads - 1) / kAttThreads];
+#pragma unroll
+    for (int k = 0; k < (D + kAttThreads - 1) / kAttThreads; ++k) acc[k] = 0.0f;
+    for (uint32_t s0 = 0; s0 < prm.nsplit; s0 += kAttThreads) {
+        const uint32_t ns = min((uint32_t)kAttThreads, prm.nsplit - s0);
+        float* s_scale = s_cmb[0];
+        float* s_lv = s_cmb[1];
+        __syncthreads();
+        if ((uint32_t)tid < ns) {
+            s_scale[tid] = __ldcg(parts + (uint64_t)(s0 + tid) * (D + 2));
+            s_lv[tid] = __ldcg(parts + (uint64_t)(s0 + tid) * (D + 2) + 1);
         }
+        __syncthreads();
+        float Mc = -INFINITY;
+        for (uint32_t i = 0; i < ns; ++i) Mc = fmaxf(Mc, s_scale[i]);
+        const float Mn = fmaxf(Mx, Mc);
+        const float rescale = Mx == -INFINITY ? 0.0f : exp2f(Mx - Mn);
+        Lx *= rescale;
+#pragma unroll
+        for (int k = 0; k < (D + kAttThreads - 1) / kAttThreads; ++k) acc[k] *= rescale;
+        Mx = Mn;
+        __syncthreads();
+        if ((uint32_t)tid < ns) {
+            const float ms = s_scale[tid];
+            s_scale[tid] = ms == -INFINITY ? 0.0f : exp2f(ms - Mx);
+        }
+        __syncthreads();
+        for (uint32_t i = 0; i < ns; ++i) Lx += s_lv[i] * s_scale[i];
+#pragma unroll
+        for (int k = 0; k < (D + kAttThreads - 1) / kAttThreads; ++k) {
+            const int dim = tid + k * kAttThreads;
+            if (dim >= D) break;
+            float a = 0.0f;
+#pragma unroll 8
+            for (uint32_t i = 0; i < ns; ++i)
+                a = fmaf(__ldcg(parts + (uint64_t)(s0 + i) * (D + 2) + 2 + dim), s_scale[i], a);
+            acc[k] += a;
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < (D + kAttThreads - 1) / kAttThreads; ++k) {
+        const int dim = tid + k * kAttThreads;
+        if (dim >= D) break;
         if (prm.partial_mode)
-            prm.out[(uint64_t)p * (D + 2) + 2 + i] = acc;
+            prm.out[(uint64_t)p * (D + 2) + 2 + dim] = acc[k];
         else
-            prm.out[(uint64_t)p * D + i] = acc / Lx;
+            prm.out[(uint64_t)p * D + dim] = acc[k] / Lx;
     }
     if (tid == 0) {
         if (prm.partial_mode) {
@@ -297,6 +329,8 @@ spl_status sparse_attend_launch(spl_ctx* ctx, AttParams prm, uint32_t kmax, int 
                                 cudaStream_t s) {
     const uint32_t d = prm.d;
     const void* fn = nullptr;
+    if (kv_dtype != SPL_F32 && kv_dtype != SPL_BF16)
+        return fail(ctx, SPL_E_DIMENSION, "sparse_attend: unknown kv dtype");
     switch (d) {
         case 32: fn = att_fn<1>(kv_dtype); break;
         case 64: fn = att_fn<2>(kv_dtype); break;

@@ -58,6 +58,30 @@ __global__ void __launch_bounds__(256) rd_ldg_chunk(const uint32_t* __restrict__
     if (acc == 0x12345678u) out[0] = acc;
 }
 
+// K3-fused-v2 pattern: CPP CTAs per problem, tiles of 256 units dealt
+// round-robin, KB tiles per load batch, double buffered
+template <int KB>
+__global__ void __launch_bounds__(256) rd_tiles(const uint32_t* __restrict__ a, uint32_t P, uint32_t CPP,
+                                                uint32_t units_per_p, uint32_t* out) {
+    const uint32_t p = blockIdx.x / CPP, c = blockIdx.x % CPP;
+    const uint32_t ntiles = units_per_p / 256;
+    const uint32_t mt = ntiles > c ? (ntiles - c + CPP - 1) / CPP : 0;
+    const uint32_t* base = a + (uint64_t)p * units_per_p * 8;
+    uint32_t acc = 0;
+    for (uint32_t t0 = 0; t0 < mt; t0 += KB) {
+        uint32_t w[KB][8];
+#pragma unroll
+        for (int i = 0; i < KB; ++i)
+            if (t0 + i < mt) ld256(base + ((uint64_t)(c + (t0 + i) * CPP) * 256 + threadIdx.x) * 8, w[i]);
+            else for (int k = 0; k < 8; ++k) w[i][k] = 0;
+#pragma unroll
+        for (int i = 0; i < KB; ++i)
+#pragma unroll
+            for (int k = 0; k < 8; ++k) acc ^= w[i][k];
+    }
+    if (acc == 0x12345678u) out[0] = acc;
+}
+
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
 template <int S>
@@ -135,6 +159,15 @@ int main() {
         snprintf(n, 64, "ldg256 U8 grid=%dx", occ); timeit(n, [&] { rd_ldg<8><<<sms * occ, 256>>>(a, units, o); });
         snprintf(n, 64, "chunk U4 grid=%dx", occ); timeit(n, [&] { rd_ldg_chunk<4><<<sms * occ, 256>>>(a, units, o); });
         snprintf(n, 64, "chunk U8 grid=%dx", occ); timeit(n, [&] { rd_ldg_chunk<8><<<sms * occ, 256>>>(a, units, o); });
+    }
+    {
+        const uint32_t upp = (uint32_t)(units / 32);
+        timeit("tiles KB4 CPP9 (288)", [&] { rd_tiles<4><<<32 * 9, 256>>>(a, 32, 9, upp, o); });
+        timeit("tiles KB8 CPP9 (288)", [&] { rd_tiles<8><<<32 * 9, 256>>>(a, 32, 9, upp, o); });
+        timeit("tiles KB4 CPP13 (416)", [&] { rd_tiles<4><<<32 * 13, 256>>>(a, 32, 13, upp, o); });
+        timeit("tiles KB2 CPP13 (416)", [&] { rd_tiles<2><<<32 * 13, 256>>>(a, 32, 13, upp, o); });
+        timeit("chunk U4 grid=288", [&] { rd_ldg_chunk<4><<<288, 256>>>(a, units, o); });
+        timeit("ldg256 U4 grid=288", [&] { rd_ldg<4><<<288, 256>>>(a, units, o); });
     }
     for (int occ : {1, 2}) {
         char n[64];
