@@ -4,8 +4,8 @@
  * torch or C++ types. Every entry point names the reference interface it
  * replaces (paths relative to /root/reference/proj). The reference's C++ API
  * (spotlight/bitcodes.hpp, hashers.hpp, attention_eval.hpp) is re-exposed on
- * top of this ABI by the C++ drop-in library (include/spotlight/*.hpp,
- * libspotlight_b200.so), which marshals host<->device and re-throws the
+ * top of this ABI by the C++ drop-in library (the headers under
+ * include/spotlight/, libspotlight_b200.so), which marshals host<->device and re-throws the
  * reference exception types.
  *
  * Conventions

@@ -294,6 +294,53 @@ __global__ void __launch_bounds__(kAttThreads) k4_sparse_attend(AttParams prm) {
     }
 }
 
+// Any head dim (the reference's API accepts every d; the tuned kernel above
+// covers d in {32, 64, 128, 256}). One warp per problem, rows processed one
+// at a time with a warp-reduced dot product; f32 only (the drop-in API feeds
+// f32 K/V). Same log-sum-exp semantics; partial mode supported.
+__global__ void k4_attend_generic(AttParams prm) {
+    const uint32_t p = blockIdx.x;
+    const int lane = threadIdx.x;
+    const uint32_t d = prm.d;
+    const uint32_t c = prm.cnt[p];
+    const uint32_t* list = prm.idx + (uint64_t)p * prm.idx_stride;
+    uint32_t own;
+    if (prm.partial_mode)
+        own = prm.own_row ? prm.own_row[p] : kInv;
+    else
+        own = prm.n_valid[p / prm.nvalid_div] - 1u;
+    const bool has_own = own != kInv;
+    const bool own_listed = has_own && c > 0 && list[c - 1] == own;
+    const uint32_t nrows = c + ((has_own && !own_listed) ? 1u : 0u);
+    const float* K = static_cast<const float*>(prm.kc) + (uint64_t)p * prm.stride_rows * d;
+    const float* V = static_cast<const float*>(prm.vc) + (uint64_t)p * prm.stride_rows * d;
+    const float* q = prm.q + (uint64_t)p * d;
+    float m = -INFINITY, l = 0.0f;
+    float* o = prm.partials + (uint64_t)p * d;  // scratch accumulator [P][d]
+    for (uint32_t i = lane; i < d; i += 32) o[i] = 0.0f;
+    for (uint32_t j = 0; j < nrows; ++j) {
+        const uint32_t r = j < c ? list[j] : own;
+        float part = 0.0f;
+        for (uint32_t i = lane; i < d; i += 32) part = fmaf(q[i] * prm.qscale, K[(uint64_t)r * d + i], part);
+        const float s = warp_sum(part);
+        const float mn = fmaxf(m, s);
+        const float corr = exp2f(m - mn), w = exp2f(s - mn);
+        l = l * corr + w;
+        for (uint32_t i = lane; i < d; i += 32) o[i] = o[i] * corr + w * V[(uint64_t)r * d + i];
+        m = mn;
+    }
+    for (uint32_t i = lane; i < d; i += 32) {
+        if (prm.partial_mode)
+            prm.out[(uint64_t)p * (d + 2) + 2 + i] = o[i];
+        else
+            prm.out[(uint64_t)p * d + i] = o[i] / l;
+    }
+    if (prm.partial_mode && lane == 0) {
+        prm.out[(uint64_t)p * (d + 2)] = m;
+        prm.out[(uint64_t)p * (d + 2) + 1] = l;
+    }
+}
+
 // Merge R partial sets [R][P][d+2] (log2-domain m) -> out [P][d].
 __global__ void k5_combine(const float* partials, uint32_t R, uint32_t P, uint32_t d,
                            float* out) {
@@ -336,10 +383,20 @@ spl_status sparse_attend_launch(spl_ctx* ctx, AttParams prm, uint32_t kmax, int 
         case 64: fn = att_fn<2>(kv_dtype); break;
         case 128: fn = att_fn<4>(kv_dtype); break;
         case 256: fn = att_fn<8>(kv_dtype); break;
-        default:
-            return fail(ctx, SPL_E_DIMENSION,
-                        "sparse_attend: head dim " + std::to_string(d) +
-                            " not supported (32, 64, 128, 256)");
+        default: {
+            if (d == 0) return fail(ctx, SPL_E_DIMENSION, "attention: embedding dimensions differ");
+            if (kv_dtype != SPL_F32)
+                return fail(ctx, SPL_E_DIMENSION,
+                            "sparse_attend: bf16 K/V needs head dim 32, 64, 128 or 256");
+            if (prm.P == 0) return SPL_OK;
+            spl_status st = ensure_buffer(ctx, reinterpret_cast<void**>(&ctx->att_ws),
+                                          &ctx->att_ws_bytes, (size_t)prm.P * d * sizeof(float),
+                                          false, s, "sparse_attend");
+            if (st) return st;
+            prm.partials = ctx->att_ws;
+            k4_attend_generic<<<prm.P, 32, 0, s>>>(prm);
+            return after_launch(ctx, "k4_attend_generic");
+        }
     }
     if (prm.P == 0) return SPL_OK;
     const uint64_t rows_max = (uint64_t)kmax + 1;

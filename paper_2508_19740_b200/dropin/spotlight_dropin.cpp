@@ -1,0 +1,636 @@
+// C++ drop-in of the reference's hot-path API (include/spotlight/*.hpp) on
+// top of the C-ABI (include/spl_c.h). Host-side only: marshals host buffers
+// to the device, calls the sm_100a kernels, copies results back and re-throws
+// the reference's exception types with its wording. Every compute path is a
+// GPU launch; without a Blackwell GPU the calls throw DeviceError.
+//
+// Concurrency: the reference functions are pure and thread-safe
+// (SPEC.md:88-89); here each host thread gets its own spl_ctx (thread_local),
+// which keeps that property.
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <fstream>
+#include <memory>
+#include <random>
+#include <string>
+#include <type_traits>
+#include <vector>
+
+#include "spl_c.h"
+#include "spotlight/attention_eval.hpp"
+#include "spotlight/bitcodes.hpp"
+#include "spotlight/hashers.hpp"
+
+namespace spotlight {
+namespace {
+
+// ------------------------------------------------------------- plumbing
+struct CtxHolder {
+    spl_ctx* c = nullptr;
+    ~CtxHolder() {
+        if (c) spl_ctx_destroy(c);
+    }
+};
+
+spl_ctx* ctx() {
+    thread_local CtxHolder h;
+    if (!h.c) {
+        const char* dev = std::getenv("SPOTLIGHT_DEVICE");
+        const spl_status st = spl_ctx_create(dev ? std::atoi(dev) : 0, &h.c);
+        if (st != SPL_OK) {
+            h.c = nullptr;
+            throw DeviceError("spotlight: no usable sm_100 GPU (spl_ctx_create failed)");
+        }
+    }
+    return h.c;
+}
+
+[[noreturn]] void raise(spl_status st) {
+    const std::string msg = spl_last_error(ctx());
+    switch (st) {
+        case SPL_E_DIMENSION: throw DimensionError(msg);
+        case SPL_E_NUMERIC: throw NumericError(msg);
+        case SPL_E_FORMAT: throw FormatError(msg);
+        case SPL_E_IO: throw IoError(msg);
+        default: throw DeviceError(msg.empty() ? "spotlight: device failure" : msg);
+    }
+}
+
+void check(spl_status st) {
+    if (st != SPL_OK) raise(st);
+}
+
+// Synchronise the (default) stream and surface device-side error words.
+void finish() {
+    check(spl_stream_synchronize(ctx(), nullptr));
+    check(spl_check_device_error(ctx(), nullptr));
+}
+
+class DevBuf {
+public:
+    explicit DevBuf(std::size_t bytes) : n_(bytes) { check(spl_device_alloc(ctx(), bytes ? bytes : 4, &p_)); }
+    DevBuf(const void* host, std::size_t bytes) : DevBuf(bytes) { upload(host, bytes); }
+    ~DevBuf() {
+        if (p_) spl_device_free(ctx(), p_);
+    }
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    void upload(const void* host, std::size_t bytes) {
+        if (bytes) check(spl_memcpy(ctx(), p_, host, bytes, nullptr));
+    }
+    void download(void* host, std::size_t bytes) const {
+        if (bytes) check(spl_memcpy(ctx(), host, p_, bytes, nullptr));
+    }
+    template <typename T>
+    T* as() const {
+        return static_cast<T*>(p_);
+    }
+
+private:
+    void* p_ = nullptr;
+    std::size_t n_ = 0;
+};
+
+// A device hasher bank of one head for the duration of a call.
+class DevHasher {
+public:
+    explicit DevHasher(const MlpHasher& h) {
+        if (h.w2.rows() != h.w1.cols() || h.b1.size() != h.w1.cols())
+            throw DimensionError("mlp_forward: inconsistent hasher shapes");
+        check(spl_hasher_create(ctx(), SPL_HASHER_MLP, 1, h.input_dim(), h.hidden_dim(),
+                                h.code_bits(), h.w1.data(), h.b1.data(), h.w2.data(), &h_));
+    }
+    explicit DevHasher(const LinearHasher& h) {
+        check(spl_hasher_create(ctx(), SPL_HASHER_LINEAR, 1, h.input_dim(), 0, h.code_bits(),
+                                h.projection.data(), nullptr, nullptr, &h_));
+    }
+    ~DevHasher() { spl_hasher_destroy(h_); }
+    DevHasher(const DevHasher&) = delete;
+    DevHasher& operator=(const DevHasher&) = delete;
+    const spl_hasher* get() const { return h_; }
+
+private:
+    spl_hasher* h_ = nullptr;
+};
+
+// Codes of x (m x d) through the GPU exact encoder, as a host CodeMatrix.
+template <typename H>
+CodeMatrix encode_codes(const H& hasher, const Matrix<float>& x, std::uint32_t L) {
+    CodeMatrix out(static_cast<std::uint32_t>(x.rows()), L);
+    if (x.rows() == 0) return out;
+    DevHasher dh(hasher);
+    DevBuf dx(x.data(), x.size() * sizeof(float));
+    DevBuf dc(out.raw().size() * 4);
+    check(spl_encode(ctx(), dh.get(), dx.as<float>(), 1, static_cast<std::uint32_t>(x.rows()),
+                     SPL_ENCODE_EXACT, dc.as<std::uint32_t>(), nullptr));
+    finish();
+    dc.download(out.raw().data(), out.raw().size() * 4);
+    return out;
+}
+
+std::string str(std::size_t v) { return std::to_string(v); }
+
+// ------------------------------------------------------------- little-endian file I/O
+void write_u32(std::ofstream& os, std::uint32_t v) {
+    const unsigned char b[4] = {static_cast<unsigned char>(v), static_cast<unsigned char>(v >> 8),
+                                static_cast<unsigned char>(v >> 16),
+                                static_cast<unsigned char>(v >> 24)};
+    os.write(reinterpret_cast<const char*>(b), 4);
+}
+void write_f32(std::ofstream& os, float f) {
+    std::uint32_t u;
+    std::memcpy(&u, &f, 4);
+    write_u32(os, u);
+}
+template <typename T>
+void write_words(std::ofstream& os, const T* p, std::size_t n) {
+    static_assert(sizeof(T) == 4);
+    for (std::size_t i = 0; i < n; ++i) {
+        std::uint32_t u;
+        std::memcpy(&u, p + i, 4);
+        write_u32(os, u);
+    }
+}
+
+class Reader {
+public:
+    explicit Reader(const std::string& path) : path_(path), is_(path, std::ios::binary) {
+        if (!is_) throw IoError("cannot open for reading: " + path);
+    }
+    void magic(const char* m) {
+        char got[4];
+        if (!is_.read(got, 4)) throw FormatError(path_ + ": truncated while reading magic at offset 0");
+        if (std::memcmp(got, m, 4) != 0)
+            throw FormatError(path_ + ": bad magic at offset 0, expected \"" + std::string(m, 4) +
+                              "\" got \"" + std::string(got, 4) + "\"");
+    }
+    std::uint32_t u32(const char* field) {
+        unsigned char b[4];
+        const auto at = static_cast<long long>(is_.tellg());
+        if (!is_.read(reinterpret_cast<char*>(b), 4))
+            throw FormatError(path_ + ": truncated while reading " + field + " at offset " +
+                              std::to_string(at));
+        return b[0] | (b[1] << 8) | (b[2] << 16) | (static_cast<std::uint32_t>(b[3]) << 24);
+    }
+    std::uint8_t u8(const char* field) {
+        char c;
+        if (!is_.read(&c, 1)) throw FormatError(path_ + ": truncated while reading " + field);
+        return static_cast<std::uint8_t>(c);
+    }
+    float f32(const char* field) {
+        const std::uint32_t u = u32(field);
+        float f;
+        std::memcpy(&f, &u, 4);
+        return f;
+    }
+    template <typename T>
+    void words(T* out, std::size_t n, const char* field) {
+        static_assert(sizeof(T) == 4);
+        std::vector<unsigned char> buf(n * 4);
+        if (n && !is_.read(reinterpret_cast<char*>(buf.data()), static_cast<std::streamsize>(n * 4)))
+            throw FormatError(path_ + ": truncated payload while reading " + field + " (expected " +
+                              str(n * 4) + " bytes)");
+        for (std::size_t i = 0; i < n; ++i) {
+            const std::uint32_t u = buf[4 * i] | (buf[4 * i + 1] << 8) | (buf[4 * i + 2] << 16) |
+                                    (static_cast<std::uint32_t>(buf[4 * i + 3]) << 24);
+            std::memcpy(out + i, &u, 4);
+        }
+    }
+
+private:
+    std::string path_;
+    std::ifstream is_;
+};
+
+std::ofstream open_out(const std::string& path) {
+    std::ofstream os(path, std::ios::binary);
+    if (!os) throw IoError("cannot open for writing: " + path);
+    return os;
+}
+
+}  // namespace
+
+// =================================================================== bitcodes
+CodeMatrix::CodeMatrix(std::uint32_t rows, std::uint32_t length_bits) : n_(rows), L_(length_bits) {
+    if (length_bits == 0 || length_bits % 32 != 0)
+        throw DimensionError("CodeMatrix: length_bits " + str(length_bits) +
+                             " must be a positive multiple of 32");
+    if (length_bits > kMaxBits)
+        throw DimensionError("CodeMatrix: length_bits " + str(length_bits) + " exceeds the " +
+                             str(kMaxBits) + "-bit limit");
+    w_.assign(static_cast<std::size_t>(rows) * (length_bits / 32), 0u);
+}
+
+CodeMatrix pack_bits(const BitMatrix& bits) {
+    const std::size_t d = bits.cols();
+    if (d == 0 || d % 32 != 0)
+        throw DimensionError("pack_bits: column count " + str(d) + " must be a positive multiple of 32");
+    CodeMatrix out(static_cast<std::uint32_t>(bits.rows()), static_cast<std::uint32_t>(d));
+    if (bits.rows() == 0) return out;
+    DevBuf db(bits.data(), bits.rows() * d);
+    DevBuf dc(out.raw().size() * 4);
+    check(spl_pack_bits(ctx(), db.as<std::uint8_t>(), bits.rows(), static_cast<std::uint32_t>(d),
+                        dc.as<std::uint32_t>(), nullptr));
+    finish();
+    dc.download(out.raw().data(), out.raw().size() * 4);
+    return out;
+}
+
+BitMatrix unpack_bits(const CodeMatrix& codes) {
+    BitMatrix out(codes.rows(), codes.length_bits());
+    if (codes.rows() == 0) return out;
+    DevBuf dc(codes.raw().data(), codes.raw().size() * 4);
+    DevBuf db(static_cast<std::size_t>(codes.rows()) * codes.length_bits());
+    check(spl_unpack_bits(ctx(), dc.as<std::uint32_t>(), codes.rows(), codes.length_bits(),
+                          db.as<std::uint8_t>(), nullptr));
+    finish();
+    db.download(out.data(), static_cast<std::size_t>(codes.rows()) * codes.length_bits());
+    return out;
+}
+
+void nxor_scores_into(std::span<const std::uint32_t> query_words, const CodeMatrix& index,
+                      std::uint32_t n_valid, std::int32_t* out) {
+    const std::size_t wpr = index.words_per_row();
+    if (query_words.size() != wpr)
+        throw DimensionError("nxor_scores: query has " + str(query_words.size() * 32) +
+                             " bits, index has " + str(index.length_bits()));
+    if (n_valid == 0) return;
+    n_valid = std::min(n_valid, index.rows());
+    DevBuf dc(index.raw().data(), static_cast<std::size_t>(n_valid) * wpr * 4);
+    DevBuf dq(query_words.data(), wpr * 4);
+    DevBuf dn(&n_valid, 4);
+    DevBuf ds(static_cast<std::size_t>(n_valid) * 4);
+    check(spl_nxor_scores(ctx(), dc.as<std::uint32_t>(), 0, index.length_bits(),
+                          dq.as<std::uint32_t>(), 1, dn.as<std::uint32_t>(), 1, n_valid,
+                          ds.as<std::int32_t>(), n_valid, nullptr));
+    finish();
+    ds.download(out, static_cast<std::size_t>(n_valid) * 4);
+}
+
+ScoreVector nxor_scores(const HashCode& query, const CodeMatrix& index) {
+    if (query.length_bits != index.length_bits())
+        throw DimensionError("nxor_scores: query length " + str(query.length_bits) +
+                             " != index length " + str(index.length_bits()));
+    ScoreVector s(index.rows());
+    nxor_scores_into(std::span<const std::uint32_t>(query.words.data(), query.words.size()), index,
+                     index.rows(), s.data());
+    return s;
+}
+
+template <typename S>
+std::vector<std::uint32_t> top_k_indices(std::span<const S> scores, std::uint32_t k) {
+    const std::size_t n = scores.size();
+    if (k == 0 || k > n)
+        throw DimensionError("top_k_indices: k=" + str(k) + " out of range for n=" + str(n));
+    constexpr int dtype = std::is_same_v<S, std::int32_t> ? 0 : (std::is_same_v<S, float> ? 1 : 2);
+    DevBuf ds(scores.data(), n * sizeof(S));
+    DevBuf di(static_cast<std::size_t>(k) * 4);
+    check(spl_top_k(ctx(), ds.as<void>(), dtype, 1, n, n, k, di.as<std::uint32_t>(), nullptr));
+    finish();
+    std::vector<std::uint32_t> out(k);
+    di.download(out.data(), static_cast<std::size_t>(k) * 4);
+    return out;
+}
+
+template std::vector<std::uint32_t> top_k_indices<std::int32_t>(std::span<const std::int32_t>,
+                                                                std::uint32_t);
+template std::vector<std::uint32_t> top_k_indices<float>(std::span<const float>, std::uint32_t);
+template std::vector<std::uint32_t> top_k_indices<double>(std::span<const double>, std::uint32_t);
+
+void write_code_index(const std::string& path, const CodeMatrix& codes) {
+    auto os = open_out(path);
+    os.write("SPLC", 4);
+    write_u32(os, 1);
+    write_u32(os, codes.rows());
+    write_u32(os, codes.length_bits());
+    write_words(os, codes.raw().data(), codes.raw().size());
+    if (!os) throw IoError("write failed: " + path);
+}
+
+CodeMatrix read_code_index(const std::string& path) {
+    Reader r(path);
+    r.magic("SPLC");
+    const std::uint32_t version = r.u32("version");
+    if (version != 1) throw FormatError(path + ": unsupported SPLC version " + str(version));
+    const std::uint32_t n = r.u32("row count");
+    const std::uint32_t bits = r.u32("code length");
+    CodeMatrix codes(n, bits);
+    r.words(codes.raw().data(), codes.raw().size(), "code words");
+    return codes;
+}
+
+// ==================================================================== hashers
+MlpHasher mlp_gaussian_init(std::uint32_t d, std::uint32_t h, std::uint32_t code_bits,
+                            float gamma, std::uint64_t seed) {
+    if (d < 1 || h < 1 || code_bits < 1)
+        throw DimensionError("mlp_gaussian_init: dimensions must be >= 1");
+    if (gamma <= 0.0f) throw DimensionError("mlp_gaussian_init: gamma must be positive");
+    // The same engine and distribution (mt19937_64, normal_distribution<double>)
+    // in the same draw order: W1 row-major, then W2 row-major.
+    std::mt19937_64 eng(seed);
+    std::normal_distribution<double> gauss(0.0, 1.0);
+    MlpHasher m;
+    m.w1 = Matrix<float>(d, h);
+    const double s1 = 1.0 / std::sqrt(static_cast<double>(d));
+    for (std::size_t i = 0; i < m.w1.size(); ++i) m.w1.data()[i] = static_cast<float>(gauss(eng) * s1);
+    m.b1.assign(h, 0.0f);
+    m.w2 = Matrix<float>(h, code_bits);
+    const double s2 = 1.0 / std::sqrt(static_cast<double>(h));
+    for (std::size_t i = 0; i < m.w2.size(); ++i) m.w2.data()[i] = static_cast<float>(gauss(eng) * s2);
+    m.gamma = gamma;
+    return m;
+}
+
+Matrix<float> mlp_forward(const MlpHasher& h, const Matrix<float>& x) {
+    if (x.cols() != h.w1.rows())
+        throw DimensionError("mlp_forward: input dim " + str(x.cols()) + " != hasher dim " +
+                             str(h.w1.rows()));
+    Matrix<float> pre(x.rows(), h.code_bits());
+    if (x.rows() == 0 || h.code_bits() == 0) return pre;
+    if (h.code_bits() % 32 != 0)
+        throw DimensionError("mlp_forward: the GPU encoder needs code_bits % 32 == 0 (got " +
+                             str(h.code_bits()) + ")");
+    DevHasher dh(h);
+    DevBuf dx(x.data(), x.size() * 4);
+    DevBuf dp(pre.size() * 4);
+    check(spl_mlp_forward(ctx(), dh.get(), dx.as<float>(), 1, static_cast<std::uint32_t>(x.rows()),
+                          dp.as<float>(), nullptr));
+    finish();
+    dp.download(pre.data(), pre.size() * 4);
+    return pre;
+}
+
+CodeMatrix mlp_hash_packed(const MlpHasher& h, const Matrix<float>& x) {
+    if (x.cols() != h.w1.rows())
+        throw DimensionError("mlp_forward: input dim " + str(x.cols()) + " != hasher dim " +
+                             str(h.w1.rows()));
+    return encode_codes(h, x, h.code_bits());
+}
+
+CodeMatrix linear_hash_packed(const LinearHasher& h, const Matrix<float>& x) {
+    if (x.cols() != h.projection.rows())
+        throw DimensionError("linear_hash: input dim " + str(x.cols()) + " != hasher dim " +
+                             str(h.projection.rows()));
+    return encode_codes(h, x, h.code_bits());
+}
+
+BitMatrix mlp_hash(const MlpHasher& h, const Matrix<float>& x) {
+    return unpack_bits(mlp_hash_packed(h, x));
+}
+
+BitMatrix linear_hash(const LinearHasher& h, const Matrix<float>& x) {
+    return unpack_bits(linear_hash_packed(h, x));
+}
+
+void write_hasher(const std::string& path, const AnyHasher& hasher) {
+    auto os = open_out(path);
+    os.write("SPLH", 4);
+    write_u32(os, 1);
+    if (const auto* lin = std::get_if<LinearHasher>(&hasher)) {
+        os.put(0);
+        write_u32(os, lin->input_dim());
+        write_u32(os, 0);
+        write_u32(os, lin->code_bits());
+        write_f32(os, 0.0f);
+        write_words(os, lin->projection.data(), lin->projection.size());
+    } else if (const auto* mlp = std::get_if<MlpHasher>(&hasher)) {
+        os.put(1);
+        write_u32(os, mlp->input_dim());
+        write_u32(os, mlp->hidden_dim());
+        write_u32(os, mlp->code_bits());
+        write_f32(os, mlp->gamma);
+        write_words(os, mlp->w1.data(), mlp->w1.size());
+        write_words(os, mlp->b1.data(), mlp->b1.size());
+        write_words(os, mlp->w2.data(), mlp->w2.size());
+    } else {
+        const auto& dp = std::get<DownProjEstimator>(hasher);
+        os.put(2);
+        write_u32(os, dp.input_dim());
+        write_u32(os, 0);
+        write_u32(os, dp.reduced_dim());
+        write_f32(os, 0.0f);
+        write_words(os, dp.projection.data(), dp.projection.size());
+    }
+    if (!os) throw IoError("write failed: " + path);
+}
+
+AnyHasher read_hasher(const std::string& path) {
+    Reader r(path);
+    r.magic("SPLH");
+    const std::uint32_t version = r.u32("version");
+    if (version != 1) throw FormatError(path + ": unsupported SPLH version " + str(version));
+    const std::uint8_t kind = r.u8("kind");
+    const std::uint32_t d = r.u32("d"), h = r.u32("h"), L = r.u32("L");
+    const float gamma = r.f32("gamma");
+    auto mat = [&](std::size_t rows, std::size_t cols, const char* f) {
+        Matrix<float> m(rows, cols);
+        r.words(m.data(), m.size(), f);
+        return m;
+    };
+    switch (kind) {
+        case 0: return LinearHasher{mat(d, L, "projection")};
+        case 1: {
+            MlpHasher m;
+            m.w1 = mat(d, h, "w1");
+            m.b1.assign(h, 0.0f);
+            r.words(m.b1.data(), m.b1.size(), "b1");
+            m.w2 = mat(h, L, "w2");
+            m.gamma = gamma;
+            if (m.gamma <= 0.0f) throw FormatError(path + ": mlp gamma must be positive");
+            return m;
+        }
+        case 2: return DownProjEstimator{mat(d, L, "projection")};
+        default: throw FormatError(path + ": unknown hasher kind " + str(kind));
+    }
+}
+
+const char* hasher_kind_name(const AnyHasher& hasher) {
+    if (std::holds_alternative<LinearHasher>(hasher)) return "linear";
+    if (std::holds_alternative<MlpHasher>(hasher)) return "mlp";
+    return "downproj";
+}
+
+// ============================================================= attention_eval
+void AttentionInstance::validate() const {
+    const std::size_t n = keys.rows();
+    if (n == 0) throw DimensionError("attention: empty KV cache");
+    if (values.rows() != n) throw DimensionError("attention: key/value row counts differ");
+    if (queries.cols() != keys.cols() || values.cols() != keys.cols())
+        throw DimensionError("attention: embedding dimensions differ");
+    if (!(scale > 0.0f)) throw DimensionError("attention: scale must be positive");
+    if (causal_offsets.size() != queries.rows())
+        throw DimensionError("attention: need one causal offset per query");
+    for (std::uint32_t off : causal_offsets)
+        if (off == 0 || off > n)
+            throw DimensionError("attention: causal offset " + str(off) + " outside [1, " + str(n) + "]");
+}
+
+AttentionInstance make_causal_instance(Matrix<float> queries, Matrix<float> keys,
+                                       Matrix<float> values) {
+    if (queries.rows() != keys.rows())
+        throw DimensionError("make_causal_instance: query count must equal cache size");
+    AttentionInstance inst;
+    inst.scale = 1.0f / std::sqrt(static_cast<float>(keys.cols()));
+    inst.causal_offsets.resize(queries.rows());
+    for (std::size_t i = 0; i < queries.rows(); ++i)
+        inst.causal_offsets[i] = static_cast<std::uint32_t>(i + 1);
+    inst.queries = std::move(queries);
+    inst.keys = std::move(keys);
+    inst.values = std::move(values);
+    inst.validate();
+    return inst;
+}
+
+const char* retrieval_method_name(RetrievalMethod m) {
+    switch (m) {
+        case RetrievalMethod::oracle: return "oracle";
+        case RetrievalMethod::lsh: return "lsh";
+        case RetrievalMethod::mlp: return "mlp";
+        case RetrievalMethod::downproj: return "downproj";
+    }
+    return "?";
+}
+
+RetrievalResult hash_topk(const AttentionInstance& inst, const AnyHasher& hasher,
+                          std::uint32_t k) {
+    inst.validate();
+    if (k == 0) throw DimensionError("hash_topk: k must be >= 1");
+    if (std::holds_alternative<DownProjEstimator>(hasher))
+        throw DimensionError("hash_topk: down-projection estimator is not a hash; use downproj_topk");
+    const bool is_mlp = std::holds_alternative<MlpHasher>(hasher);
+    const std::uint32_t dim = is_mlp ? std::get<MlpHasher>(hasher).input_dim()
+                                     : std::get<LinearHasher>(hasher).input_dim();
+    if (inst.keys.cols() != dim) throw DimensionError("hash_topk: hasher dimension mismatch");
+    // Encode the whole cache and the queries once (K1), then one K3 launch
+    // retrieves for every query against the shared code cache (stride 0),
+    // query r seeing rows [0, causal_offsets[r]).
+    const CodeMatrix key_codes = is_mlp ? mlp_hash_packed(std::get<MlpHasher>(hasher), inst.keys)
+                                        : linear_hash_packed(std::get<LinearHasher>(hasher), inst.keys);
+    const CodeMatrix query_codes = is_mlp
+                                       ? mlp_hash_packed(std::get<MlpHasher>(hasher), inst.queries)
+                                       : linear_hash_packed(std::get<LinearHasher>(hasher), inst.queries);
+    const auto q = static_cast<std::uint32_t>(inst.num_queries());
+    const auto n = static_cast<std::uint32_t>(inst.cache_size());
+    RetrievalResult res;
+    res.method = is_mlp ? RetrievalMethod::mlp : RetrievalMethod::lsh;
+    res.budget = k;
+    res.indices.resize(q);
+    if (q == 0) return res;
+    DevBuf dk(key_codes.raw().data(), key_codes.raw().size() * 4);
+    DevBuf dq(query_codes.raw().data(), query_codes.raw().size() * 4);
+    DevBuf dn(inst.causal_offsets.data(), static_cast<std::size_t>(q) * 4);
+    DevBuf di(static_cast<std::size_t>(q) * k * 4);
+    DevBuf dc(static_cast<std::size_t>(q) * 4);
+    check(spl_hamming_topk(ctx(), dk.as<std::uint32_t>(), 0, key_codes.length_bits(),
+                           dq.as<std::uint32_t>(), q, dn.as<std::uint32_t>(), 1, n, k,
+                           di.as<std::uint32_t>(), dc.as<std::uint32_t>(), nullptr));
+    finish();
+    std::vector<std::uint32_t> idx(static_cast<std::size_t>(q) * k), cnt(q);
+    di.download(idx.data(), idx.size() * 4);
+    dc.download(cnt.data(), cnt.size() * 4);
+    for (std::uint32_t r = 0; r < q; ++r)
+        res.indices[r].assign(idx.begin() + static_cast<std::size_t>(r) * k,
+                              idx.begin() + static_cast<std::size_t>(r) * k + cnt[r]);
+    return res;
+}
+
+namespace {
+// Attention over explicit per-query row lists (own token already inserted):
+// one K4 launch in partial-free mode with own-token insertion disabled.
+Matrix<float> attend_lists(const AttentionInstance& inst,
+                           const std::vector<std::vector<std::uint32_t>>& lists) {
+    const auto q = static_cast<std::uint32_t>(inst.num_queries());
+    const auto d = static_cast<std::uint32_t>(inst.keys.cols());
+    Matrix<float> out(q, d);
+    if (q == 0) return out;
+    std::size_t kmax = 1;
+    for (const auto& l : lists) kmax = std::max(kmax, l.size());
+    std::vector<std::uint32_t> idx(static_cast<std::size_t>(q) * kmax, 0), cnt(q);
+    for (std::uint32_t r = 0; r < q; ++r) {
+        std::copy(lists[r].begin(), lists[r].end(), idx.begin() + static_cast<std::size_t>(r) * kmax);
+        cnt[r] = static_cast<std::uint32_t>(lists[r].size());
+    }
+    // own_row = ~0: attend exactly the given rows (the lists already hold the
+    // own token, inserted on the host exactly as the reference does)
+    const std::vector<std::uint32_t> no_own(q, 0xFFFFFFFFu);
+    DevBuf dq(inst.queries.data(), inst.queries.size() * 4);
+    DevBuf dk(inst.keys.data(), inst.keys.size() * 4);
+    DevBuf dv(inst.values.data(), inst.values.size() * 4);
+    DevBuf di(idx.data(), idx.size() * 4);
+    DevBuf dc(cnt.data(), cnt.size() * 4);
+    DevBuf downr(no_own.data(), no_own.size() * 4);
+    DevBuf dpart(static_cast<std::size_t>(q) * (d + 2) * 4);
+    check(spl_sparse_attend_partial(ctx(), dq.as<float>(), dk.as<void>(), dv.as<void>(), SPL_F32, 0, d,
+                                    q, di.as<std::uint32_t>(), kmax, dc.as<std::uint32_t>(),
+                                    downr.as<std::uint32_t>(), 1, inst.scale, dpart.as<float>(),
+                                    nullptr));
+    DevBuf dout(out.size() * 4);
+    check(spl_attend_combine(ctx(), dpart.as<float>(), 1, q, d, dout.as<float>(), nullptr));
+    finish();
+    dout.download(out.data(), out.size() * 4);
+    return out;
+}
+}  // namespace
+
+Matrix<float> sparse_attention(const AttentionInstance& inst, const RetrievalResult& result) {
+    inst.validate();
+    if (result.indices.size() != inst.num_queries())
+        throw DimensionError("sparse_attention: result has " + str(result.indices.size()) +
+                             " index sets for " + str(inst.num_queries()) + " queries");
+    std::vector<std::vector<std::uint32_t>> lists(inst.num_queries());
+    for (std::size_t row = 0; row < inst.num_queries(); ++row) {
+        const auto& picked = result.indices[row];
+        if (picked.empty())
+            throw DimensionError("sparse_attention: empty index set for query " + str(row));
+        const std::uint32_t valid = inst.causal_offsets[row];
+        const std::uint32_t own = valid - 1;
+        auto& subset = lists[row];
+        subset.assign(picked.begin(), picked.end());
+        for (std::uint32_t i : subset)
+            if (i >= valid)
+                throw DimensionError("sparse_attention: index " + str(i) +
+                                     " outside causal range for query " + str(row));
+        if (!std::binary_search(subset.begin(), subset.end(), own))
+            subset.insert(std::upper_bound(subset.begin(), subset.end(), own), own);
+    }
+    return attend_lists(inst, lists);
+}
+
+Matrix<float> full_attention(const AttentionInstance& inst) {
+    inst.validate();
+    std::vector<std::vector<std::uint32_t>> lists(inst.num_queries());
+    for (std::size_t row = 0; row < inst.num_queries(); ++row) {
+        lists[row].resize(inst.causal_offsets[row]);
+        for (std::uint32_t i = 0; i < inst.causal_offsets[row]; ++i) lists[row][i] = i;
+    }
+    return attend_lists(inst, lists);
+}
+
+double iou(std::span<const std::uint32_t> a, std::span<const std::uint32_t> b) {
+    if (a.empty() && b.empty()) return 1.0;
+    std::size_t i = 0, j = 0, both = 0;
+    while (i < a.size() && j < b.size()) {
+        if (a[i] == b[j]) {
+            ++both;
+            ++i;
+            ++j;
+        } else if (a[i] < b[j]) {
+            ++i;
+        } else {
+            ++j;
+        }
+    }
+    return static_cast<double>(both) / static_cast<double>(a.size() + b.size() - both);
+}
+
+std::uint32_t budget_from_rate(double rate, std::size_t n) {
+    std::uint32_t k = 0;
+    if (spl_budget_from_rate(rate, n, &k) != SPL_OK)
+        throw DimensionError("budget_from_rate: rate must lie in (0, 1]");
+    return k;
+}
+
+}  // namespace spotlight

@@ -1,0 +1,433 @@
+// C++ parity tests of the drop-in spotlight:: API (libspotlight_b200.so, GPU)
+// written like the reference's own doctest suite
+// (proj/tests/test_bitcodes.cpp, test_hashers.cpp, test_attention_eval.cpp),
+// plus bit-exact differential checks against the unmodified reference
+// (oracle/_ref/libspotref.so via its extern "C" shim) when it was built.
+// Run by tests/test_gpu_dropin.py; exit code = number of failed checks.
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <functional>
+#include <numeric>
+#include <random>
+#include <string>
+#include <unistd.h>
+#include <vector>
+
+#include "spotlight/attention_eval.hpp"
+#include "spotlight/bitcodes.hpp"
+#include "spotlight/errors.hpp"
+#include "spotlight/hashers.hpp"
+
+using namespace spotlight;
+
+// ------------------------------------------------------------ mini harness
+static int g_checks = 0, g_failed = 0;
+static const char* g_case = "";
+#define CHECK(cond)                                                                   \
+    do {                                                                              \
+        ++g_checks;                                                                   \
+        if (!(cond)) {                                                                \
+            ++g_failed;                                                               \
+            std::fprintf(stderr, "FAIL [%s] %s:%d: %s\n", g_case, __FILE__, __LINE__, #cond); \
+        }                                                                             \
+    } while (0)
+#define CHECK_THROWS_AS(expr, Exc)                                 \
+    do {                                                           \
+        bool thrown_ = false;                                      \
+        try {                                                      \
+            (void)(expr);                                          \
+        } catch (const Exc&) {                                     \
+            thrown_ = true;                                        \
+        } catch (...) {                                            \
+        }                                                          \
+        CHECK(thrown_ && #Exc);                                    \
+    } while (0)
+#define CHECK_THROWS_WITH(expr, Exc, needle)                                  \
+    do {                                                                      \
+        bool ok_ = false;                                                     \
+        try {                                                                 \
+            (void)(expr);                                                     \
+        } catch (const Exc& e) {                                              \
+            ok_ = std::string(e.what()).find(needle) != std::string::npos;    \
+        } catch (...) {                                                       \
+        }                                                                     \
+        CHECK(ok_ && "exception message");                                    \
+    } while (0)
+
+static std::vector<std::pair<const char*, std::function<void()>>>& registry() {
+    static std::vector<std::pair<const char*, std::function<void()>>> r;
+    return r;
+}
+struct Reg {
+    Reg(const char* n, std::function<void()> f) { registry().push_back({n, std::move(f)}); }
+};
+#define CAT2(a, b) a##b
+#define CAT(a, b) CAT2(a, b)
+#define TEST_CASE(name)                                   \
+    static void CAT(tc_, __LINE__)();                     \
+    static Reg CAT(reg_, __LINE__)(name, CAT(tc_, __LINE__)); \
+    static void CAT(tc_, __LINE__)()
+
+// ------------------------------------------------------------ helpers
+static BitMatrix random_bits(std::size_t n, std::size_t d, std::mt19937_64& eng) {
+    BitMatrix b(n, d);
+    std::bernoulli_distribution coin(0.5);
+    for (std::size_t i = 0; i < n; ++i)
+        for (std::size_t j = 0; j < d; ++j) b.set(i, j, coin(eng));
+    return b;
+}
+static Matrix<float> random_matrix(std::size_t r, std::size_t c, std::mt19937_64& eng, double s = 1.0) {
+    std::normal_distribution<double> g(0.0, s);
+    Matrix<float> m(r, c);
+    for (std::size_t i = 0; i < m.size(); ++i) m.data()[i] = static_cast<float>(g(eng));
+    return m;
+}
+static std::vector<std::uint32_t> full_sort_topk(const std::vector<std::int32_t>& s, std::uint32_t k) {
+    std::vector<std::uint32_t> idx(s.size());
+    std::iota(idx.begin(), idx.end(), 0u);
+    std::sort(idx.begin(), idx.end(), [&](std::uint32_t a, std::uint32_t b) {
+        return s[a] != s[b] ? s[a] > s[b] : a < b;
+    });
+    idx.resize(k);
+    std::sort(idx.begin(), idx.end());
+    return idx;
+}
+static AttentionInstance random_instance(std::size_t q, std::size_t n, std::size_t d,
+                                         std::mt19937_64& eng, bool causal) {
+    AttentionInstance inst;
+    inst.queries = random_matrix(q, d, eng);
+    inst.keys = random_matrix(n, d, eng);
+    inst.values = random_matrix(n, d, eng);
+    inst.scale = 1.0f / std::sqrt(static_cast<float>(d));
+    inst.causal_offsets.resize(q);
+    for (std::size_t i = 0; i < q; ++i)
+        inst.causal_offsets[i] = causal ? static_cast<std::uint32_t>(std::min(i + 1, n))
+                                        : static_cast<std::uint32_t>(n);
+    return inst;
+}
+
+// ------------------------------------------------------------ bitcodes
+TEST_CASE("pack_bits single-word examples") {
+    BitMatrix one(1, 32);
+    one.set(0, 0, true);
+    CHECK(pack_bits(one).row(0)[0] == 0x80000000u);
+    CHECK(pack_bits(BitMatrix(1, 32)).row(0)[0] == 0u);
+    BitMatrix wide(1, 64);
+    wide.set(0, 1, true);
+    const CodeMatrix c = pack_bits(wide);
+    CHECK(c.row(0)[0] == 0u);
+    CHECK(c.row(0)[1] == 0x80000000u);
+}
+
+TEST_CASE("pack_bits rejects widths that are not multiples of 32") {
+    CHECK_THROWS_AS(pack_bits(BitMatrix(1, 33)), DimensionError);
+    CHECK_THROWS_AS(pack_bits(BitMatrix(1, 0)), DimensionError);
+}
+
+TEST_CASE("pack_bits layout oracle and unpack round trip") {
+    std::mt19937_64 eng(7);
+    for (int it = 0; it < 60; ++it) {
+        const std::size_t n = 1 + eng() % 8, d = 32 * (1 + eng() % 8);
+        const BitMatrix bits = random_bits(n, d, eng);
+        const CodeMatrix got = pack_bits(bits);
+        CodeMatrix want(static_cast<std::uint32_t>(n), static_cast<std::uint32_t>(d));
+        const std::size_t cw = d / 32;
+        for (std::size_t i = 0; i < n; ++i)
+            for (std::size_t j = 0; j < d; ++j)
+                if (bits.get(i, j)) want.row(static_cast<std::uint32_t>(i))[j % cw] |= 1u << (31 - j / cw);
+        CHECK(got == want);
+        CHECK(unpack_bits(got) == bits);
+    }
+}
+
+TEST_CASE("nxor_scores counts agreeing bits") {
+    std::mt19937_64 eng(13);
+    const BitMatrix bits = random_bits(8, 128, eng);
+    const CodeMatrix codes = pack_bits(bits);
+    CHECK(nxor_scores(codes.code(3), codes)[3] == 128);
+    BitMatrix flipped = bits;
+    for (std::size_t j = 0; j < 128; ++j) flipped.set(0, j, !bits.get(0, j));
+    CHECK(nxor_scores(pack_bits(flipped).code(0), codes)[0] == 0);
+    const CodeMatrix other(4, 64);
+    CHECK_THROWS_AS(nxor_scores(other.code(0), codes), DimensionError);
+}
+
+TEST_CASE("affine identity 2m - L == signed dot product") {
+    std::mt19937_64 eng(17);
+    for (int it = 0; it < 40; ++it) {
+        const std::size_t d = 32 * (1 + eng() % 8);
+        const BitMatrix bits = random_bits(6, d, eng);
+        const ScoreVector s = nxor_scores(pack_bits(bits).code(0), pack_bits(bits));
+        for (std::size_t r = 0; r < 6; ++r) {
+            int dot = 0;
+            for (std::size_t j = 0; j < d; ++j) dot += (bits.get(0, j) ? 1 : -1) * (bits.get(r, j) ? 1 : -1);
+            CHECK(2 * s[r] - static_cast<int>(d) == dot);
+        }
+    }
+}
+
+TEST_CASE("top_k_indices examples, tie rule and full-sort oracle") {
+    CHECK(top_k_indices(ScoreVector{3, 1, 2}, 1) == std::vector<std::uint32_t>{0});
+    CHECK(top_k_indices(ScoreVector{2, 2, 1}, 1) == std::vector<std::uint32_t>{0});
+    CHECK((top_k_indices(ScoreVector{5, 9, 1, 7}, 4) == std::vector<std::uint32_t>{0, 1, 2, 3}));
+    CHECK_THROWS_WITH(top_k_indices(ScoreVector{3, 1, 2}, 0), DimensionError, "k=0 out of range for n=3");
+    CHECK_THROWS_AS(top_k_indices(ScoreVector{3, 1, 2}, 4), DimensionError);
+    std::mt19937_64 eng(23);
+    for (int it = 0; it < 100; ++it) {
+        const std::size_t n = 1 + eng() % 257;
+        std::uniform_int_distribution<std::int32_t> sc(0, 12);
+        ScoreVector s(n);
+        for (auto& v : s) v = sc(eng);
+        const std::uint32_t k = 1 + eng() % n;
+        CHECK(top_k_indices(s, k) == full_sort_topk(s, k));
+    }
+    std::uniform_int_distribution<std::int32_t> sc(0, 128);
+    ScoreVector s(10000);
+    for (auto& v : s) v = sc(eng);
+    for (std::uint32_t k : {1u, 17u, 200u, 9999u, 10000u}) CHECK(top_k_indices(s, k) == full_sort_topk(s, k));
+    const std::vector<float> f{0.5f, -0.0f, 0.0f, 0.5f, -1.0f};
+    CHECK((top_k_indices<float>(std::span<const float>(f), 3) == std::vector<std::uint32_t>{0, 1, 3}));
+}
+
+TEST_CASE("SPLC round trip and validation") {
+    std::mt19937_64 eng(29);
+    const CodeMatrix codes = pack_bits(random_bits(17, 96, eng));
+    const std::string path = "test_dropin_codes.splc";
+    write_code_index(path, codes);
+    CHECK(read_code_index(path) == codes);
+    {
+        FILE* f = std::fopen(path.c_str(), "r+b");
+        std::fputc('X', f);
+        std::fclose(f);
+        CHECK_THROWS_WITH(read_code_index(path), FormatError, "offset 0");
+    }
+    write_code_index(path, codes);
+    {
+        FILE* f = std::fopen(path.c_str(), "r+b");
+        CHECK(ftruncate(fileno(f), 24) == 0);
+        std::fclose(f);
+        CHECK_THROWS_AS(read_code_index(path), FormatError);
+    }
+    std::remove(path.c_str());
+}
+
+// ------------------------------------------------------------ hashers
+TEST_CASE("mlp_hash sign behaviour") {
+    std::mt19937_64 eng(37);
+    MlpHasher zero;
+    zero.w1 = Matrix<float>(8, 8);
+    zero.b1.assign(8, 0.0f);
+    zero.w2 = Matrix<float>(8, 32);
+    const BitMatrix ones = mlp_hash(zero, random_matrix(2, 8, eng));
+    bool all = true;
+    for (std::size_t i = 0; i < ones.rows(); ++i)
+        for (std::size_t j = 0; j < ones.cols(); ++j) all = all && ones.get(i, j);
+    CHECK(all);
+    const MlpHasher h = mlp_gaussian_init(16, 16, 32, 64.0f, 5);
+    const Matrix<float> x = random_matrix(7, 16, eng, 3.0);
+    const Matrix<float> pre = mlp_forward(h, x);
+    const BitMatrix bits = mlp_hash(h, x);
+    bool same = true;
+    for (std::size_t i = 0; i < pre.rows(); ++i)
+        for (std::size_t j = 0; j < pre.cols(); ++j) same = same && (bits.get(i, j) == (pre(i, j) >= 0.0f));
+    CHECK(same);
+    MlpHasher scaled = mlp_gaussian_init(16, 16, 32, 64.0f, 9);
+    const BitMatrix before = mlp_hash(scaled, x);
+    for (std::size_t i = 0; i < scaled.w2.size(); ++i) scaled.w2.data()[i] *= 7.5f;
+    CHECK(mlp_hash(scaled, x) == before);
+}
+
+TEST_CASE("non-finite input and weights are rejected") {
+    MlpHasher h = mlp_gaussian_init(4, 4, 32, 64.0f, 3);
+    Matrix<float> x(1, 4);
+    x(0, 2) = std::nanf("");
+    CHECK_THROWS_WITH(mlp_forward(h, x), NumericError, "mlp input contains non-finite values");
+    h.w2(0, 0) = INFINITY;
+    CHECK_THROWS_AS(mlp_forward(h, Matrix<float>(1, 4)), NumericError);
+}
+
+TEST_CASE("hamming score equals (signed dot + L) / 2 on MLP codes") {
+    std::mt19937_64 eng(47);
+    const MlpHasher h = mlp_gaussian_init(16, 16, 32, 64.0f, 13);
+    const BitMatrix bits = mlp_hash(h, random_matrix(10, 16, eng, 2.0));
+    const ScoreVector s = nxor_scores(pack_bits(bits).code(0), pack_bits(bits));
+    for (std::size_t r = 0; r < bits.rows(); ++r) {
+        int dot = 0;
+        for (std::size_t j = 0; j < bits.cols(); ++j) dot += (bits.get(0, j) ? 1 : -1) * (bits.get(r, j) ? 1 : -1);
+        CHECK(s[r] == (dot + 32) / 2);
+    }
+}
+
+TEST_CASE("hashing is deterministic across repeated calls") {
+    std::mt19937_64 eng(59);
+    const MlpHasher h = mlp_gaussian_init(32, 32, 32, 64.0f, 17);
+    const Matrix<float> x = random_matrix(64, 32, eng, 2.0);
+    const BitMatrix first = mlp_hash(h, x);
+    for (int i = 0; i < 3; ++i) CHECK(mlp_hash(h, x) == first);
+}
+
+TEST_CASE("SPLH checkpoint round trips") {
+    const std::string path = "test_dropin_hasher.splh";
+    const MlpHasher h = mlp_gaussian_init(8, 12, 32, 48.0f, 23);
+    write_hasher(path, h);
+    const AnyHasher back = read_hasher(path);
+    CHECK(std::holds_alternative<MlpHasher>(back));
+    const auto& m = std::get<MlpHasher>(back);
+    CHECK(m.w1 == h.w1);
+    CHECK(m.b1 == h.b1);
+    CHECK(m.w2 == h.w2);
+    CHECK(m.gamma == h.gamma);
+    CHECK(std::string(hasher_kind_name(back)) == "mlp");
+    std::remove(path.c_str());
+}
+
+// ------------------------------------------------------------ attention_eval
+TEST_CASE("budget_from_rate applies floor and clamp") {
+    CHECK(budget_from_rate(0.02, 2048) == 40);
+    CHECK(budget_from_rate(0.02, 500) == 20);
+    CHECK(budget_from_rate(1.0, 8) == 8);
+    CHECK_THROWS_AS(budget_from_rate(0.0, 10), DimensionError);
+}
+
+TEST_CASE("sparse_attention over the full set reproduces full attention") {
+    std::mt19937_64 eng(11);
+    const AttentionInstance inst = random_instance(6, 32, 16, eng, true);
+    RetrievalResult all;
+    all.indices.resize(6);
+    for (std::size_t r = 0; r < 6; ++r) {
+        all.indices[r].resize(inst.causal_offsets[r]);
+        std::iota(all.indices[r].begin(), all.indices[r].end(), 0u);
+    }
+    const Matrix<float> sp = sparse_attention(inst, all), fu = full_attention(inst);
+    for (std::size_t r = 0; r < 6; ++r) {
+        double d2 = 0, n2 = 0;
+        for (std::size_t p = 0; p < 16; ++p) {
+            d2 += (sp(r, p) - fu(r, p)) * (sp(r, p) - fu(r, p));
+            n2 += fu(r, p) * fu(r, p);
+        }
+        CHECK(std::sqrt(d2) <= 1e-6 * std::sqrt(n2));
+    }
+}
+
+TEST_CASE("own token is always attended; rejections") {
+    std::mt19937_64 eng(11);
+    const AttentionInstance inst = random_instance(4, 4, 8, eng, true);
+    RetrievalResult own;
+    own.indices = {{0}, {1}, {2}, {3}};
+    const Matrix<float> o = sparse_attention(inst, own);
+    for (std::size_t p = 0; p < 8; ++p) CHECK(std::fabs(o(0, p) - inst.values(0, p)) < 1e-6f);
+    RetrievalResult empty;
+    empty.indices = {{0}, {}, {0}, {0}};
+    CHECK_THROWS_AS(sparse_attention(inst, empty), DimensionError);
+    RetrievalResult out_of_range;
+    out_of_range.indices = {{3}, {0}, {0}, {0}};
+    CHECK_THROWS_AS(sparse_attention(inst, out_of_range), DimensionError);
+}
+
+TEST_CASE("hash_topk: duplicated keys keep the lower index; collapsed hasher -> first k") {
+    std::mt19937_64 eng(13);
+    AttentionInstance inst = random_instance(2, 8, 32, eng, false);
+    for (std::size_t p = 0; p < 32; ++p) inst.keys(4, p) = inst.keys(1, p);
+    LinearHasher lin{random_matrix(32, 32, eng)};
+    const RetrievalResult a = hash_topk(inst, lin, 3), b = hash_topk(inst, lin, 3);
+    CHECK(a.indices == b.indices);
+    for (const auto& idx : a.indices)
+        if (std::find(idx.begin(), idx.end(), 4u) != idx.end())
+            CHECK(std::find(idx.begin(), idx.end(), 1u) != idx.end());
+    const AttentionInstance big = random_instance(64, 512, 32, eng, false);
+    MlpHasher collapsed;
+    collapsed.w1 = Matrix<float>(32, 8);
+    collapsed.b1.assign(8, 0.0f);
+    collapsed.w2 = Matrix<float>(8, 32);
+    const RetrievalResult res = hash_topk(big, collapsed, 16);
+    std::vector<std::uint32_t> first(16);
+    std::iota(first.begin(), first.end(), 0u);
+    for (const auto& idx : res.indices) CHECK(idx == first);
+    CHECK_THROWS_AS(hash_topk(big, DownProjEstimator{Matrix<float>(32, 4)}, 16), DimensionError);
+    CHECK_THROWS_AS(hash_topk(big, collapsed, 0), DimensionError);
+}
+
+// ------------------------------------------------------------ vs the reference
+struct Ref {
+    void* h = nullptr;
+    int (*mlp_forward)(const float*, const float*, const float*, std::uint32_t, std::uint32_t,
+                       std::uint32_t, const float*, std::uint32_t, float*) = nullptr;
+    int (*hash_topk)(const float*, const float*, const float*, std::uint32_t, std::uint32_t,
+                     const float*, std::uint32_t, const float*, const float*, std::uint32_t,
+                     std::uint32_t, float, const std::uint32_t*, std::uint32_t, std::uint32_t*,
+                     std::uint32_t*) = nullptr;
+    int (*sparse)(const float*, std::uint32_t, const float*, const float*, std::uint32_t,
+                  std::uint32_t, float, const std::uint32_t*, const std::uint32_t*,
+                  const std::uint64_t*, float*) = nullptr;
+    Ref() {
+        const char* p = std::getenv("SPOTREF_SO");
+        h = dlopen(p ? p : "oracle/_ref/libspotref.so", RTLD_NOW | RTLD_LOCAL);
+        if (!h) return;
+        mlp_forward = reinterpret_cast<decltype(mlp_forward)>(dlsym(h, "spotref_mlp_forward"));
+        hash_topk = reinterpret_cast<decltype(hash_topk)>(dlsym(h, "spotref_hash_topk_mlp"));
+        sparse = reinterpret_cast<decltype(sparse)>(dlsym(h, "spotref_sparse_attention"));
+    }
+};
+
+TEST_CASE("drop-in == reference: mlp_forward, hash_topk, sparse_attention") {
+    static Ref ref;
+    if (!ref.h) {
+        std::fprintf(stderr, "note: oracle/_ref/libspotref.so not present, reference diff skipped\n");
+        return;
+    }
+    std::mt19937_64 eng(2024);
+    const std::uint32_t n = 600, d = 128, L = 128;
+    const MlpHasher h = mlp_gaussian_init(d, d, L, 64.0f, 99);
+    AttentionInstance inst = make_causal_instance(random_matrix(n, d, eng), random_matrix(n, d, eng),
+                                                  random_matrix(n, d, eng));
+    const Matrix<float> pre = mlp_forward(h, inst.keys);
+    std::vector<float> rpre(pre.size());
+    CHECK(ref.mlp_forward(h.w1.data(), h.b1.data(), h.w2.data(), d, d, L, inst.keys.data(), n,
+                          rpre.data()) == 0);
+    CHECK(std::memcmp(rpre.data(), pre.data(), pre.size() * 4) == 0);
+    const std::uint32_t k = 24;
+    const RetrievalResult res = hash_topk(inst, h, k);
+    std::vector<std::uint32_t> ridx(static_cast<std::size_t>(n) * k), rcnt(n);
+    CHECK(ref.hash_topk(h.w1.data(), h.b1.data(), h.w2.data(), d, L, inst.queries.data(), n,
+                        inst.keys.data(), inst.values.data(), n, d, inst.scale,
+                        inst.causal_offsets.data(), k, ridx.data(), rcnt.data()) == 0);
+    bool same = true;
+    for (std::uint32_t r = 0; r < n; ++r) {
+        std::vector<std::uint32_t> want(ridx.begin() + static_cast<std::size_t>(r) * k,
+                                        ridx.begin() + static_cast<std::size_t>(r) * k + rcnt[r]);
+        same = same && (res.indices[r] == want);
+    }
+    CHECK(same);
+    const Matrix<float> sp = sparse_attention(inst, res);
+    std::vector<std::uint32_t> flat;
+    std::vector<std::uint64_t> off(n + 1, 0);
+    for (std::uint32_t r = 0; r < n; ++r) {
+        flat.insert(flat.end(), res.indices[r].begin(), res.indices[r].end());
+        off[r + 1] = flat.size();
+    }
+    std::vector<float> rout(static_cast<std::size_t>(n) * d);
+    CHECK(ref.sparse(inst.queries.data(), n, inst.keys.data(), inst.values.data(), n, d, inst.scale,
+                     inst.causal_offsets.data(), flat.data(), off.data(), rout.data()) == 0);
+    double mx = 0;
+    for (std::size_t i = 0; i < rout.size(); ++i) mx = std::max(mx, (double)std::fabs(rout[i] - sp.data()[i]));
+    std::fprintf(stderr, "sparse_attention max-abs vs reference: %.3g\n", mx);
+    CHECK(mx <= 1e-5);
+}
+
+int main() {
+    for (auto& [name, fn] : registry()) {
+        g_case = name;
+        try {
+            fn();
+        } catch (const std::exception& e) {
+            ++g_failed;
+            std::fprintf(stderr, "FAIL [%s] unexpected exception: %s\n", name, e.what());
+        }
+    }
+    std::printf("%d checks, %d failed, %zu test cases\n", g_checks, g_failed, registry().size());
+    return g_failed ? 1 : 0;
+}
