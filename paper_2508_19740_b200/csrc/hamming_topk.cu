@@ -564,7 +564,7 @@ __device__ __forceinline__ uint64_t gtimer() {
     if (prm.trace && threadIdx.x == 0) prm.trace[blockIdx.x * 8 + (i)] = gtimer()
 
 template <int W, typename ScoreT>
-__global__ void __launch_bounds__(kThreads) k3_fused(K3Params prm) {
+__global__ void __launch_bounds__(kThreads, 3) k3_fused(K3Params prm) {
     extern __shared__ __align__(16) uint8_t smem[];
     __shared__ uint64_t s_warp[kThreads / 32 + 1];
     __shared__ uint32_t s_flag, s_T;
@@ -616,18 +616,12 @@ __global__ void __launch_bounds__(kThreads) k3_fused(K3Params prm) {
         block_suffix_sum(hist32, bins, s_warp);  // hist32[bins] stays 0
         uint32_t* rec = prm.records + (uint64_t)(blockIdx.x + p) * (L + 2);
         for (uint32_t t = tid; t < L + 2; t += kThreads) rec[t] = hist32[t];
+        // publish: this segment of problem p is complete (record + histogram)
+        __threadfence();
         __syncthreads();
+        if (tid == 0) atomicAdd(prm.counters + p, 1u);
     }
     K3_STAMP(1);
-
-    // ---------------- grid barrier (cooperative launch: all CTAs resident)
-    __threadfence();
-    __syncthreads();
-    if (tid == 0) {
-        atomicAdd(prm.sync, 1u);
-        while (ld_acquire(prm.sync) < gridDim.x) __nanosleep(32);
-    }
-    __syncthreads();
     K3_STAMP(2);
 
     // ---------------- plan + select from shared memory
@@ -640,6 +634,13 @@ __global__ void __launch_bounds__(kThreads) k3_fused(K3Params prm) {
         if (nv > g.n_max) nv = (uint32_t)g.n_max;
         const uint64_t r0 = lo, r1 = min(hi, (uint64_t)nv);
         const uint32_t kk = prm.k < nv ? prm.k : nv;
+        // wait only for the segments of THIS problem (cooperative launch: all
+        // of them are resident), not for the whole grid
+        if (tid == 0) {
+            const uint32_t nseg = seg_last(g, p) - seg_first(g, p) + 1;
+            while (ld_acquire(prm.counters + p) < nseg) __nanosleep(32);
+        }
+        __syncthreads();
         uint32_t T, quota;
         problem_threshold(prm.tot_hist + (uint64_t)p * prm.tot_stride, L, kk, s_cum, s_warp, &s_T, T,
                           quota);
@@ -688,6 +689,7 @@ __global__ void __launch_bounds__(kThreads) k3_fused(K3Params prm) {
     if (s_flag) {
         __threadfence();
         for (uint64_t i = tid; i < (uint64_t)g.P * prm.tot_stride; i += kThreads) prm.tot_hist[i] = 0u;
+        for (uint32_t i = tid; i < g.P; i += kThreads) prm.counters[i] = 0u;
         if (tid == 0) {
             prm.sync[0] = 0u;
             prm.sync[1] = 0u;
