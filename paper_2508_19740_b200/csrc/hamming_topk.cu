@@ -40,8 +40,10 @@
 namespace spl {
 
 struct K3Geom {
-    uint64_t n_max;  // rows per problem (virtual)
-    uint64_t total;  // P * n_max
+    uint64_t n_max;    // rows per problem (cache capacity; rows >= n_max are never scored)
+    uint64_t pstride;  // rows per problem in the virtual row space (>= n_max; the fused
+                       // plan pads it to whole segments so no CTA straddles two problems)
+    uint64_t total;    // P * pstride
     uint64_t S;      // rows per CTA
     uint64_t n_pad;  // global score row stride (two-pass)
     uint32_t G;      // CTAs
@@ -49,10 +51,10 @@ struct K3Geom {
 };
 
 __host__ __device__ __forceinline__ uint32_t seg_first(const K3Geom& g, uint32_t p) {
-    return (uint32_t)(((uint64_t)p * g.n_max) / g.S);
+    return (uint32_t)(((uint64_t)p * g.pstride) / g.S);
 }
 __host__ __device__ __forceinline__ uint32_t seg_last(const K3Geom& g, uint32_t p) {
-    return (uint32_t)((((uint64_t)p + 1) * g.n_max - 1) / g.S);
+    return (uint32_t)((((uint64_t)p + 1) * g.pstride - 1) / g.S);
 }
 
 struct K3Params {
@@ -79,10 +81,22 @@ struct K3Params {
     int shard;             // 1: no planning; tot_hist = caller's histogram
     uint32_t score_region; // fused: bytes of shared memory for scores
     uint64_t* trace;       // optional [G][8] globaltimer stamps (SPL_K3_TRACE)
+    uint32_t hist_lo;      // fused: private counters cover scores [hist_lo, L] only
+    uint32_t* counters2;   // fused: [P] low-bin fallback completion
 };
 
 constexpr int kThreads = 256;
-constexpr int kU = 2;  // 32-byte units per thread per load batch (x2 double-buffered)
+// Shared memory per SM the fused plan may use: above this the driver must
+// pick the 228 KB carve-out (L1 ~0), and streaming LDG.256 reads drop from
+// 6.2 to 5.2 TB/s on this B200 (tools/read_bw.cu "sweep": the slowdown is a
+// step at the carve-out switch, not a function of the smem size).
+constexpr size_t kFastCarveBytes = 196 * 1024;
+#ifndef K3_EXP
+#define K3_EXP 0  // timing experiments only (tools/k3_exp.sh); 0 = product
+#endif
+// 32-byte units per thread per load batch (x2 double-buffered): keeps
+// ~128 KB of loads in flight per SM at 512 (4 x 128) or 768 threads/SM
+constexpr int kU = kThreads == 128 ? 4 : 2;
 
 // ------------------------------------------------------------ block scans
 __device__ __forceinline__ uint64_t warp_incl_scan_u64(uint64_t v) {
@@ -131,10 +145,13 @@ __device__ void block_suffix_sum(uint32_t* a, uint32_t n, uint64_t* s_warp) {
 }
 
 // Threshold of one problem from its (global) histogram: s_cum <- suffix
-// sums, returns T (SPL_PLAN_SKIP when kk == 0) and the tie quota.
+// sums, returns T (SPL_PLAN_SKIP when kk == 0, or when fewer than kk rows
+// score >= from) and the tie quota. Bins below `from` are read as 0.
 __device__ void problem_threshold(const uint32_t* tot, uint32_t L, uint32_t kk, uint32_t* s_cum,
-                                  uint64_t* s_warp, uint32_t* s_T, uint32_t& T, uint32_t& quota) {
-    for (uint32_t t = threadIdx.x; t <= L + 1; t += kThreads) s_cum[t] = t <= L ? __ldcg(tot + t) : 0u;
+                                  uint64_t* s_warp, uint32_t* s_T, uint32_t& T, uint32_t& quota,
+                                  uint32_t from = 0) {
+    for (uint32_t t = threadIdx.x; t <= L + 1; t += kThreads)
+        s_cum[t] = (t <= L && t >= from) ? __ldcg(tot + t) : 0u;
     __syncthreads();
     block_suffix_sum(s_cum, L + 1, s_warp);
     if (threadIdx.x == 0) *s_T = SPL_PLAN_SKIP;
@@ -213,23 +230,40 @@ __device__ __forceinline__ void store_scores(ScoreT* dst, const uint32_t* s) {
     }
 }
 
+// Byte slot of thread t inside a 256-byte bin row of the private counters:
+// the 32 lanes of a warp land in 32 distinct banks (lane*4), the 4 bytes of
+// a bank word belong to 4 different warps. (Slot = t would put lanes
+// 4i..4i+3 on one bank with different bins: a 4-way conflict per update.)
+// The flush sums whole bin rows, so it does not depend on the mapping.
+__device__ __forceinline__ uint32_t priv_slot(uint32_t t) {
+    static_assert(kThreads % 128 == 0, "priv_slot maps 4 warps per 128-byte group");
+    return (t & 31u) * 4u + ((t >> 5) & 3u) + (t >> 7) * 128u;
+}
 template <bool PRIV>
 __device__ __forceinline__ void count_score(uint8_t* priv, uint32_t* hist32, uint32_t s) {
     if (PRIV)
-        priv[s * kThreads + threadIdx.x] += 1;
+        priv[s * kThreads + priv_slot(threadIdx.x)] += 1;
     else
         atomicAdd(hist32 + s, 1u);
 }
 
 // Add the private u8 counters [bins][kThreads] into hist32 and clear them.
+static_assert(kThreads == 128 || kThreads == 256, "flush_priv row width");
 __device__ void flush_priv(uint8_t* priv, uint32_t* hist32, uint32_t bins) {
     __syncthreads();
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     for (uint32_t b = warp; b < bins; b += kThreads / 32) {
-        uint2* row = reinterpret_cast<uint2*>(priv + (size_t)b * kThreads);  // 256 B = 32 x 8 B
-        const uint2 x = row[lane];
-        uint32_t sum = __vsadu4(x.x, 0u) + __vsadu4(x.y, 0u);
-        row[lane] = make_uint2(0u, 0u);
+        uint32_t sum = 0;
+        if constexpr (kThreads == 128) {  // 128 B = 32 x 4 B
+            uint32_t* row = reinterpret_cast<uint32_t*>(priv + (size_t)b * kThreads);
+            sum = __vsadu4(row[lane], 0u);
+            row[lane] = 0u;
+        } else {  // 256 B = 32 x 8 B
+            uint2* row = reinterpret_cast<uint2*>(priv + (size_t)b * kThreads);
+            const uint2 x = row[lane];
+            sum = __vsadu4(x.x, 0u) + __vsadu4(x.y, 0u);
+            row[lane] = make_uint2(0u, 0u);
+        }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
         if (lane == 0) hist32[b] += sum;
@@ -254,7 +288,9 @@ __device__ __forceinline__ uint32_t row_score(const uint32_t* row, const uint32_
 template <int W, typename ScoreT, bool PRIV, bool DST_SMEM>
 __device__ void stream_piece(const uint32_t* base, const uint32_t* qp, uint32_t L, uint64_t r0,
                              uint64_t r1, ScoreT* dst, uint64_t dst_row0, uint8_t* priv,
-                             uint32_t* hist32, uint32_t bins) {
+                             uint32_t* hist32, uint32_t bins, uint32_t lo) {
+    // counters (priv rows / hist32 entries) are indexed by score - lo; scores
+    // below lo are stored but not counted (lo = 0: full histogram)
     const int tid = threadIdx.x;
     if constexpr (W > 0) {
         constexpr int R = 8 / W;  // rows per 32-byte unit
@@ -271,7 +307,7 @@ __device__ void stream_piece(const uint32_t* base, const uint32_t* qp, uint32_t 
                 const uint64_t row = (uint32_t)tid < nhead ? r0 + tid : tail_beg + (tid - nhead);
                 const uint32_t sc = row_score<W>(base + row * W, q, L);
                 dst[row - dst_row0] = (ScoreT)sc;
-                count_score<PRIV>(priv, hist32, sc);
+                if (sc >= lo) count_score<PRIV>(priv, hist32, sc - lo);
             }
         }
         if (ut <= uh) {
@@ -284,7 +320,7 @@ __device__ void stream_piece(const uint32_t* base, const uint32_t* qp, uint32_t 
         ScoreT* udst = dst + (uh * R - dst_row0) + (size_t)tid * R;  // its scores
         // private counters through 32-bit shared-window addresses hoisted out
         // of the loop (ld/st.shared.u8; asm volatile keeps their order)
-        const uint32_t priv_s = (uint32_t)__cvta_generic_to_shared(priv) + tid;
+        const uint32_t priv_s = (uint32_t)__cvta_generic_to_shared(priv) + priv_slot(tid);
         const uint32_t dst_s = DST_SMEM ? (uint32_t)__cvta_generic_to_shared(udst) : 0u;
         constexpr uint32_t per_it = (uint32_t)kThreads * kU;
         const uint32_t nit = (nu + per_it - 1) / per_it;
@@ -299,23 +335,31 @@ __device__ void stream_piece(const uint32_t* base, const uint32_t* qp, uint32_t 
                 if (!check || it * per_it + j * kThreads + tid < nu) buf[j].load(p, (uint32_t)j * kThreads);
         };
         auto count = [&](uint32_t sc) {
+            if (sc < lo) return;
             if (PRIV) {
-                const uint32_t addr = priv_s + sc * kThreads;
+                const uint32_t addr = priv_s + (sc - lo) * kThreads;
                 uint32_t v;
                 asm volatile("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(addr));
                 asm volatile("st.shared.u8 [%0], %1;" ::"r"(addr), "r"(v + 1));
             } else {
-                atomicAdd(hist32 + sc, 1u);
+                atomicAdd(hist32 + (sc - lo), 1u);
             }
         };
         auto process_unit = [&](const Unit32& u, uint32_t it, int j) {
             uint32_t sc[R];
 #pragma unroll
             for (int r = 0; r < R; ++r) {
+#if K3_EXP >= 2  // experiment: no popcount
+                uint32_t x = 0;
+#pragma unroll
+                for (int w = 0; w < W; ++w) x ^= u.w[r * W + w] ^ q[w];
+                sc[r] = x & 127u;
+#else
                 uint32_t mism = 0;
 #pragma unroll
                 for (int w = 0; w < W; ++w) mism += __popc(u.w[r * W + w] ^ q[w]);
                 sc[r] = L - mism;
+#endif
             }
             const size_t off = ((size_t)it * per_it + (size_t)j * kThreads) * R;
             if constexpr (DST_SMEM) {
@@ -334,8 +378,10 @@ __device__ void stream_piece(const uint32_t* base, const uint32_t* qp, uint32_t 
             } else {
                 store_scores<ScoreT, R>(udst + off, sc);
             }
+#if K3_EXP == 0
 #pragma unroll
             for (int r = 0; r < R; ++r) count(sc[r]);
+#endif
         };
         auto process_full = [&](const Unit32* buf, uint32_t it) {
 #pragma unroll
@@ -368,7 +414,7 @@ __device__ void stream_piece(const uint32_t* base, const uint32_t* qp, uint32_t 
                 for (uint32_t w = 0; w < Wr; ++w) mism += __popc(__ldg(row + w) ^ __ldg(qp + w));
                 const uint32_t s = L - mism;
                 dst[r - dst_row0] = (ScoreT)s;
-                count_score<PRIV>(priv, hist32, s);
+                if (s >= lo) count_score<PRIV>(priv, hist32, s - lo);
             }
             if (PRIV && ++steps == 255) {
                 flush_priv(priv, hist32, bins);
@@ -484,17 +530,17 @@ __global__ void __launch_bounds__(kThreads) k3_scan(K3Params prm) {
 
     const uint64_t g0 = (uint64_t)blockIdx.x * g.S;
     const uint64_t g1 = min(g0 + g.S, g.total);
-    const uint32_t p_first = (uint32_t)(g0 / g.n_max);
+    const uint32_t p_first = (uint32_t)(g0 / g.pstride);
 
     // zero the counters once (flush_priv re-zeroes them)
     if constexpr (PRIV)
         for (uint32_t i = tid; i < priv_bytes / 16; i += kThreads)
             reinterpret_cast<uint4*>(priv)[i] = make_uint4(0, 0, 0, 0);
 
-    for (uint32_t p = p_first; p < g.P && (uint64_t)p * g.n_max < g1; ++p) {
-        const uint64_t pbase = (uint64_t)p * g.n_max;
+    for (uint32_t p = p_first; p < g.P && (uint64_t)p * g.pstride < g1; ++p) {
+        const uint64_t pbase = (uint64_t)p * g.pstride;
         const uint64_t lo = max(g0, pbase) - pbase;
-        const uint64_t hi = min(g1, pbase + g.n_max) - pbase;
+        const uint64_t hi = min(g1, pbase + g.pstride) - pbase;
         uint32_t nv = prm.n_valid[p / prm.nvalid_div];
         if (nv > g.n_max) {
             if (tid == 0) raise_dev_err(prm.dev_err, SPL_DEV_ERR_DIMENSION);
@@ -508,7 +554,7 @@ __global__ void __launch_bounds__(kThreads) k3_scan(K3Params prm) {
             const uint32_t* qp = prm.qcodes + (uint64_t)p * Wr;
             const uint32_t* base = prm.codes + (uint64_t)p * prm.stride_rows * Wr;
             ScoreT* dst = reinterpret_cast<ScoreT*>(prm.scores) + (uint64_t)p * g.n_pad;
-            stream_piece<W, ScoreT, PRIV, false>(base, qp, L, r0, r1, dst, 0, priv, hist32, bins);
+            stream_piece<W, ScoreT, PRIV, false>(base, qp, L, r0, r1, dst, 0, priv, hist32, bins, 0u);
         }
         __syncthreads();
         // raw counts -> global per-problem histogram (integer atomics: the
@@ -570,7 +616,9 @@ __global__ void __launch_bounds__(kThreads, 3) k3_fused(K3Params prm) {
     __shared__ uint32_t s_flag, s_T;
     const uint32_t L = prm.L;
     const uint32_t bins = L + 1;
-    const size_t priv_bytes = ((size_t)bins * kThreads + 15) & ~size_t(15);
+    const uint32_t lo = prm.hist_lo;        // counted window [lo, L]
+    const uint32_t wbins = bins - lo;
+    const size_t priv_bytes = ((size_t)wbins * kThreads + 15) & ~size_t(15);
     const size_t hist_bytes = (((size_t)(bins + 1) * 4) + 15) & ~size_t(15);
     uint8_t* priv = smem;
     uint32_t* hist32 = reinterpret_cast<uint32_t*>(smem + priv_bytes);                // [bins + 1]
@@ -579,25 +627,30 @@ __global__ void __launch_bounds__(kThreads, 3) k3_fused(K3Params prm) {
     const int tid = threadIdx.x;
     const K3Geom& g = prm.g;
     K3_STAMP(0);
+    if (prm.trace && tid == 0) {
+        uint32_t smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        prm.trace[(uint64_t)blockIdx.x * 8 + 6] = smid;
+    }
 
     const uint64_t g0 = (uint64_t)blockIdx.x * g.S;
     const uint64_t g1 = min(g0 + g.S, g.total);
-    const uint32_t p_first = (uint32_t)(g0 / g.n_max);
+    const uint32_t p_first = (uint32_t)(g0 / g.pstride);
     uint32_t region_off = 0;  // byte offset of the current piece's scores
 
     for (uint32_t i = tid; i < priv_bytes / 16; i += kThreads)
         reinterpret_cast<uint4*>(priv)[i] = make_uint4(0, 0, 0, 0);
 
-    for (uint32_t p = p_first; p < g.P && (uint64_t)p * g.n_max < g1; ++p) {
-        const uint64_t pbase = (uint64_t)p * g.n_max;
-        const uint64_t lo = max(g0, pbase) - pbase;
-        const uint64_t hi = min(g1, pbase + g.n_max) - pbase;
+    for (uint32_t p = p_first; p < g.P && (uint64_t)p * g.pstride < g1; ++p) {
+        const uint64_t pbase = (uint64_t)p * g.pstride;
+        const uint64_t lo_r = max(g0, pbase) - pbase;
+        const uint64_t hi_r = min(g1, pbase + g.pstride) - pbase;
         uint32_t nv = prm.n_valid[p / prm.nvalid_div];
         if (nv > g.n_max) {
             if (tid == 0) raise_dev_err(prm.dev_err, SPL_DEV_ERR_DIMENSION);
             nv = (uint32_t)g.n_max;
         }
-        const uint64_t r0 = lo, r1 = min(hi, (uint64_t)nv);
+        const uint64_t r0 = lo_r, r1 = min(hi_r, (uint64_t)nv);
         for (uint32_t i = tid; i <= bins; i += kThreads) hist32[i] = 0;
         __syncthreads();
         if (r0 < r1) {
@@ -606,13 +659,14 @@ __global__ void __launch_bounds__(kThreads, 3) k3_fused(K3Params prm) {
             region_off += (uint32_t)((((r1 - a0) * sizeof(ScoreT)) + 15) & ~uint64_t(15));
             stream_piece<W, ScoreT, true, true>(prm.codes + (uint64_t)p * prm.stride_rows * W,
                                                 prm.qcodes + (uint64_t)p * W, L, r0, r1, dst, a0,
-                                                priv, hist32, bins);
+                                                priv, hist32 + lo, wbins, lo);
         }
         __syncthreads();
         uint32_t* tot = prm.tot_hist + (uint64_t)p * prm.tot_stride;
-        for (uint32_t b = tid; b < bins; b += kThreads)
+        for (uint32_t b = lo + tid; b < bins; b += kThreads)
             if (hist32[b]) atomicAdd(tot + b, hist32[b]);
         __syncthreads();
+        // suffix-cumulative record; below the window it repeats rec[lo]
         block_suffix_sum(hist32, bins, s_warp);  // hist32[bins] stays 0
         uint32_t* rec = prm.records + (uint64_t)(blockIdx.x + p) * (L + 2);
         for (uint32_t t = tid; t < L + 2; t += kThreads) rec[t] = hist32[t];
@@ -626,31 +680,63 @@ __global__ void __launch_bounds__(kThreads, 3) k3_fused(K3Params prm) {
 
     // ---------------- plan + select from shared memory
     region_off = 0;
-    for (uint32_t p = p_first; p < g.P && (uint64_t)p * g.n_max < g1; ++p) {
-        const uint64_t pbase = (uint64_t)p * g.n_max;
-        const uint64_t lo = max(g0, pbase) - pbase;
-        const uint64_t hi = min(g1, pbase + g.n_max) - pbase;
+    for (uint32_t p = p_first; p < g.P && (uint64_t)p * g.pstride < g1; ++p) {
+        const uint64_t pbase = (uint64_t)p * g.pstride;
+        const uint64_t lo_r = max(g0, pbase) - pbase;
+        const uint64_t hi_r = min(g1, pbase + g.pstride) - pbase;
         uint32_t nv = prm.n_valid[p / prm.nvalid_div];
         if (nv > g.n_max) nv = (uint32_t)g.n_max;
-        const uint64_t r0 = lo, r1 = min(hi, (uint64_t)nv);
+        const uint64_t r0 = lo_r, r1 = min(hi_r, (uint64_t)nv);
         const uint32_t kk = prm.k < nv ? prm.k : nv;
+        const uint32_t nseg = seg_last(g, p) - seg_first(g, p) + 1;
+        const uint64_t a0 = r0 & ~uint64_t(15);
+        const ScoreT* sc = reinterpret_cast<const ScoreT*>(sregion + region_off);
+        if (r0 < r1) region_off += (uint32_t)((((r1 - a0) * sizeof(ScoreT)) + 15) & ~uint64_t(15));
         // wait only for the segments of THIS problem (cooperative launch: all
         // of them are resident), not for the whole grid
-        if (tid == 0) {
-            const uint32_t nseg = seg_last(g, p) - seg_first(g, p) + 1;
+        if (tid == 0)
             while (ld_acquire(prm.counters + p) < nseg) __nanosleep(32);
-        }
         __syncthreads();
+        uint32_t* tot = prm.tot_hist + (uint64_t)p * prm.tot_stride;
+        // window bins only: CTAs that take the fallback below add the low
+        // bins to `tot` while others may still be reading it, and every CTA
+        // of the problem must reach the same decision
         uint32_t T, quota;
-        problem_threshold(prm.tot_hist + (uint64_t)p * prm.tot_stride, L, kk, s_cum, s_warp, &s_T, T,
-                          quota);
+        problem_threshold(tot, L, kk, s_cum, s_warp, &s_T, T, quota, lo);
+        if (kk > 0 && T == SPL_PLAN_SKIP) {
+            // Fewer than kk rows scored >= lo, so T < lo: every CTA of this
+            // problem (the decision is the same for all of them) counts its
+            // rows below the window from shared memory, completes its record
+            // and the problem histogram, then T is taken again. Exact for any
+            // data; only slower for problems whose k-th score is below L/2.
+            for (uint32_t t = tid; t <= bins; t += kThreads) hist32[t] = 0;
+            __syncthreads();
+            if (r0 < r1)
+                for (uint64_t r = r0 + tid; r < r1; r += kThreads) {
+                    const uint32_t v = sc[r - a0];
+                    if (v < lo) atomicAdd(hist32 + v, 1u);
+                }
+            __syncthreads();
+            for (uint32_t b = tid; b < lo; b += kThreads)
+                if (hist32[b]) atomicAdd(tot + b, hist32[b]);
+            __syncthreads();
+            block_suffix_sum(hist32, lo, s_warp);
+            uint32_t* rec = prm.records + (uint64_t)(blockIdx.x + p) * (L + 2);
+            const uint32_t at_lo = __ldcg(rec + lo);
+            for (uint32_t t = tid; t < lo; t += kThreads) rec[t] = at_lo + hist32[t];
+            __threadfence();
+            __syncthreads();
+            if (tid == 0) {
+                atomicAdd(prm.counters2 + p, 1u);
+                while (ld_acquire(prm.counters2 + p) < nseg) __nanosleep(32);
+            }
+            __syncthreads();
+            problem_threshold(tot, L, kk, s_cum, s_warp, &s_T, T, quota);
+        }
         K3_STAMP(3);
         const uint32_t c0 = seg_first(g, p);
         if (tid == 0 && blockIdx.x == c0) prm.cnt_out[p] = kk;
         if (r0 >= r1) continue;
-        const uint64_t a0 = r0 & ~uint64_t(15);
-        const ScoreT* sc = reinterpret_cast<const ScoreT*>(sregion + region_off);
-        region_off += (uint32_t)((((r1 - a0) * sizeof(ScoreT)) + 15) & ~uint64_t(15));
         if (T == SPL_PLAN_SKIP) continue;
         // (gt, eq) of the earlier segments of this problem, from their records
         uint64_t gt_before = 0, eq_before = 0;
@@ -669,8 +755,6 @@ __global__ void __launch_bounds__(kThreads, 3) k3_fused(K3Params prm) {
             eq_before += totv >> 32;
         }
         K3_STAMP(4);
-        // own record: this CTA's last piece record is still in hist32; an
-        // earlier piece's (CTA spans two problems) is re-read from global
         const uint32_t* own = prm.records + (uint64_t)(blockIdx.x + p) * (L + 2);
         const uint64_t eq_mine = (uint64_t)__ldcg(own + T) - __ldcg(own + T + 1);
         const uint64_t left = quota > eq_before ? quota - eq_before : 0;
@@ -689,7 +773,10 @@ __global__ void __launch_bounds__(kThreads, 3) k3_fused(K3Params prm) {
     if (s_flag) {
         __threadfence();
         for (uint64_t i = tid; i < (uint64_t)g.P * prm.tot_stride; i += kThreads) prm.tot_hist[i] = 0u;
-        for (uint32_t i = tid; i < g.P; i += kThreads) prm.counters[i] = 0u;
+        for (uint32_t i = tid; i < g.P; i += kThreads) {
+            prm.counters[i] = 0u;
+            prm.counters2[i] = 0u;
+        }
         if (tid == 0) {
             prm.sync[0] = 0u;
             prm.sync[1] = 0u;
@@ -705,10 +792,10 @@ __global__ void __launch_bounds__(kThreads) k3_select(K3Params prm, uint32_t* id
     const K3Geom& g = prm.g;
     const uint64_t g0 = (uint64_t)blockIdx.x * g.S;
     const uint64_t g1 = min(g0 + g.S, g.total);
-    for (uint32_t p = (uint32_t)(g0 / g.n_max); p < g.P && (uint64_t)p * g.n_max < g1; ++p) {
-        const uint64_t pbase = (uint64_t)p * g.n_max;
+    for (uint32_t p = (uint32_t)(g0 / g.pstride); p < g.P && (uint64_t)p * g.pstride < g1; ++p) {
+        const uint64_t pbase = (uint64_t)p * g.pstride;
         const uint64_t lo = max(g0, pbase) - pbase;
-        const uint64_t hi = min(g1, pbase + g.n_max) - pbase;
+        const uint64_t hi = min(g1, pbase + g.pstride) - pbase;
         uint32_t nv = prm.n_valid[p / prm.nvalid_div];
         if (nv > g.n_max) nv = (uint32_t)g.n_max;
         const uint64_t r0 = lo, r1 = min(hi, (uint64_t)nv);
@@ -775,6 +862,7 @@ struct K3Plan {
     bool priv;
     size_t smem;
     size_t score_bytes;
+    uint32_t hist_lo;  // fused: counted score window [hist_lo, L]
 };
 
 template <int W, typename ScoreT, bool PRIV>
@@ -821,6 +909,7 @@ spl_status make_plan(spl_ctx* ctx, uint32_t P, uint64_t n_max, uint32_t L, const
     uint64_t S = (total + G_target - 1) / G_target;
     S = align_up(std::max<uint64_t>(S, 1024), 256);
     pl.g.n_max = n_max;
+    pl.g.pstride = n_max;
     pl.g.total = total;
     pl.g.S = S;
     pl.g.G = (uint32_t)((total + S - 1) / S);
@@ -846,7 +935,14 @@ spl_status make_fused_plan(spl_ctx* ctx, uint32_t P, uint64_t n_max, uint32_t L,
                            uint64_t stride_rows, bool* ok, K3FPlan* out) {
     *ok = false;
     const uint32_t W = L / 32;
-    if (!vec_ok(codes, stride_rows, W) || (size_t)(L + 1) * kThreads > 96 * 1024) return SPL_OK;
+    // Private counters cover scores [L/2, L] only: the k-th best agreement is
+    // >= L/2 whenever at least k rows agree on half their bits (retrieval
+    // keeps a small fraction of the rows); the kernel completes the lower
+    // bins from its on-chip scores when that does not hold. Halving the
+    // counters is what keeps 3 CTAs/SM under the fast carve-out.
+    const uint32_t lo = L / 2;
+    const size_t wbins = (size_t)L + 1 - lo;
+    if (!vec_ok(codes, stride_rows, W) || wbins * kThreads > 96 * 1024) return SPL_OK;
     const void* fn = nullptr;
     if (L <= 255) {
         switch (W) {
@@ -862,32 +958,49 @@ spl_status make_fused_plan(spl_ctx* ctx, uint32_t P, uint64_t n_max, uint32_t L,
     }
     const size_t sb = L <= 255 ? 1 : 2;
     const uint64_t total = (uint64_t)P * n_max;
-    const size_t base = align_up((size_t)(L + 1) * kThreads, 16) + 2 * align_up((size_t)(L + 2) * 4, 16);
+    const size_t base = align_up(wbins * kThreads, 16) + 2 * align_up((size_t)(L + 2) * 4, 16);
     int dev_max_smem = 0, sm_smem = 0;
     SPL_CUDA_TRY(ctx, cudaDeviceGetAttribute(&dev_max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin,
                                              ctx->device));
     SPL_CUDA_TRY(ctx, cudaDeviceGetAttribute(&sm_smem, cudaDevAttrMaxSharedMemoryPerMultiprocessor,
                                              ctx->device));
+    // first choice: the most CTAs per SM that stay under the fast carve-out;
+    // else the most that fit at all
+    for (int pass = 0; pass < 2; ++pass)
     for (int cps = 3; cps >= 1; --cps) {
         const uint64_t G_target = (uint64_t)ctx->num_sms * cps;
-        uint64_t S = (total + G_target - 1) / G_target;
-        S = align_up(std::max<uint64_t>(S, 1024), 256);
-        const uint64_t pieces = S / n_max + 2;
+        // P <= G_target: a whole number of segments per problem (a CTA whose
+        // segment straddled two problems paid a second pipeline ramp, flush
+        // and record: ~5 us on the slowest CTA); else equal cuts of P x n_max
+        uint64_t S, pstride;
+        if (P <= G_target) {
+            const uint64_t cpp = G_target / P;
+            S = align_up(std::max<uint64_t>((n_max + cpp - 1) / cpp, 1024), 256);
+            pstride = align_up(n_max, S);
+        } else {
+            S = align_up(std::max<uint64_t>((total + G_target - 1) / G_target, 1024), 256);
+            pstride = n_max;
+        }
+        const uint64_t vtotal = (uint64_t)P * pstride;
+        const uint64_t pieces = S / pstride + 2;
         const size_t region = align_up((size_t)(S + 16 * pieces) * sb + 16 * pieces, 16);
         const size_t smem = base + region;
         if (smem > (size_t)dev_max_smem || (smem + 1024 + 256) * cps > (size_t)sm_smem) continue;
+        if (pass == 0 && (smem + 1024) * cps > kFastCarveBytes) continue;
         SPL_CUDA_TRY(ctx, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         int per_sm = 0;
         SPL_CUDA_TRY(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kThreads, smem));
-        const uint64_t G = (total + S - 1) / S;
+        const uint64_t G = (vtotal + S - 1) / S;
         if ((uint64_t)per_sm * ctx->num_sms < G) continue;
         K3Plan& pl = out->pl;
         pl = K3Plan{};
         pl.vec = true;
         pl.priv = true;
         pl.score_bytes = sb;
+        pl.hist_lo = lo;
         pl.g.n_max = n_max;
-        pl.g.total = total;
+        pl.g.pstride = pstride;
+        pl.g.total = vtotal;
         pl.g.S = S;
         pl.g.G = (uint32_t)G;
         pl.g.P = P;
@@ -901,7 +1014,7 @@ spl_status make_fused_plan(spl_ctx* ctx, uint32_t P, uint64_t n_max, uint32_t L,
 }
 
 // Persistent zeroed per-problem state (self-resetting after every launch):
-// [2 spare][counters P][tot P x (L+2)][bar P x 4]
+// [2 sync][counters P][tot P x (L+2)][bar P x 4: fused low-bin fallback counters]
 struct K3State {
     uint32_t* sync;
     uint32_t* counters;
@@ -1035,6 +1148,8 @@ spl_status hamming_topk_impl(spl_ctx* ctx, const uint32_t* codes, uint64_t strid
             prm.cnt_out = cnt;
             prm.idx_out = idx;
             prm.idx_stride = k;
+            prm.hist_lo = fp.pl.hist_lo;
+            prm.counters2 = kst.bar;
             const uint32_t G = fp.pl.g.G;
             const char* tr = getenv("SPL_K3_TRACE");
             uint64_t* dtrace = nullptr;
@@ -1063,6 +1178,18 @@ spl_status hamming_topk_impl(spl_ctx* ctx, const uint32_t* codes, uint64_t strid
                 fprintf(stderr, "  max:");
                 for (int j = 0; j < 6; ++j) fprintf(stderr, " %.1f", mx[j]);
                 fprintf(stderr, " us\n");
+                if (*tr == '2') {  // per-CTA dump: cta, smid, stamps (us)
+                    FILE* f = fopen("gpurun_out/k3_trace.csv", "w");
+                    if (f) {
+                        fprintf(f, "cta,smid,start,stream,barrier,thresh,prefix,select\n");
+                        for (uint32_t i = 0; i < G; ++i) {
+                            fprintf(f, "%u,%llu", i, (unsigned long long)h[i * 8 + 6]);
+                            for (int j = 0; j < 6; ++j) fprintf(f, ",%.3f", (double)(h[i * 8 + j] - t0) / 1000.0);
+                            fprintf(f, "\n");
+                        }
+                        fclose(f);
+                    }
+                }
             }
             return st;
         }
@@ -1127,6 +1254,7 @@ spl_status shard_select_impl(spl_ctx* ctx, const uint32_t* all_hist, uint32_t R,
     K3Plan pl{};
     spl_status st;
     pl.g.n_max = n_max;
+    pl.g.pstride = n_max;
     pl.g.total = (uint64_t)P * n_max;
     pl.g.S = ctx->shard_S;
     pl.g.G = ctx->shard_G;

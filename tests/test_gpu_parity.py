@@ -98,6 +98,32 @@ def test_topk_edge_cases(ctx, k3_path, oracle):
             assert np.array_equal(got[p], want[p, :kk])
 
 
+@pytest.mark.parametrize("L", [64, 128, 256])
+def test_topk_low_threshold_fallback(ctx, k3_path, oracle, L):
+    """The fused kernel counts only scores >= L/2 on its first pass; problems
+    whose k-th score is lower take the in-kernel fallback (low bins recounted
+    from the on-chip scores). Mixed batch: problems 0 and 2 are anti-correlated
+    with their query (all scores ~0.2 L), problem 1 is a normal random cache,
+    problem 3 has k = 0.9 n."""
+    rng = np.random.default_rng(100 + L)
+    P, n, W = 4, 30000, L // 32
+    q = rng.integers(0, 2**32, (P, W), dtype=np.uint64).astype(np.uint32)
+    codes = rng.integers(0, 2**32, (P, n, W), dtype=np.uint64).astype(np.uint32)
+    for p in (0, 2):
+        keep = np.zeros((n, W), np.uint32)  # ~20% of bits agree with q
+        for _ in range(3):
+            keep |= rng.integers(0, 2**32, (n, W), dtype=np.uint64).astype(np.uint32)
+        keep = ~keep  # P(bit) = 1/8
+        codes[p] = (~q[p])[None, :] ^ (keep & rng.integers(0, 2**32, (n, W), dtype=np.uint64).astype(np.uint32))
+    nv = np.array([n, n, n - 5, n], np.uint32)
+    for k in (10, 3000, 27000):
+        got = run_topk(ctx, codes, q, nv, k)
+        want = oracle.retrieve_batch(codes, q, nv, k)
+        for p in range(P):
+            kk = min(k, int(nv[p]))
+            assert np.array_equal(got[p], want[p, :kk]), (L, k, p)
+
+
 def test_topk_k_zero_rejected(ctx):
     codes = np.zeros((1, 10, 4), np.uint32)
     with pytest.raises(capi.DimensionError):

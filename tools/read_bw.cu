@@ -58,6 +58,85 @@ __global__ void __launch_bounds__(256) rd_ldg_chunk(const uint32_t* __restrict__
     if (acc == 0x12345678u) out[0] = acc;
 }
 
+// contiguous chunks with NT threads per CTA and double-buffered U-unit batches
+// (the K3-fused stream loop shape)
+template <int U, int NT>
+__global__ void __launch_bounds__(NT) rd_chunk_db(const uint32_t* __restrict__ a, uint64_t units, uint32_t* out) {
+    const uint64_t per = (units + gridDim.x - 1) / gridDim.x;
+    const uint64_t u0 = blockIdx.x * per, u1 = min(units, u0 + per);
+    uint32_t acc = 0;
+    uint32_t wa[U][8], wb[U][8];
+    auto load = [&](uint32_t (*w)[8], uint64_t base) {
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const uint64_t i = base + u * NT + threadIdx.x;
+            if (i < u1) ld256(a + i * 8, w[u]); else for (int k = 0; k < 8; ++k) w[u][k] = 0;
+        }
+    };
+    auto use = [&](uint32_t (*w)[8]) {
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+#pragma unroll
+            for (int k = 0; k < 8; ++k) acc += __popc(w[u][k]);
+    };
+    const uint64_t step = (uint64_t)U * NT;
+    load(wa, u0);
+    for (uint64_t base = u0; base < u1; base += 2 * step) {
+        if (base + step < u1) load(wb, base + step);
+        use(wa);
+        if (base + step < u1) {
+            if (base + 2 * step < u1) load(wa, base + 2 * step);
+            use(wb);
+        }
+    }
+    if (acc == 0x12345678u) out[0] = acc;
+}
+
+// single-buffered chunk loop, NT threads, optional popcount use
+template <int U, int NT, bool POPC>
+__global__ void __launch_bounds__(NT) rd_chunk_sb(const uint32_t* __restrict__ a, uint64_t units, uint32_t* out) {
+    const uint64_t per = (units + gridDim.x - 1) / gridDim.x;
+    const uint64_t u0 = blockIdx.x * per, u1 = min(units, u0 + per);
+    uint32_t acc = 0;
+    for (uint64_t base = u0; base < u1; base += (uint64_t)U * NT) {
+        uint32_t w[U][8];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const uint64_t i = base + u * NT + threadIdx.x;
+            if (i < u1) ld256(a + i * 8, w[u]); else for (int k = 0; k < 8; ++k) w[u][k] = 0;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+#pragma unroll
+            for (int k = 0; k < 8; ++k) acc = POPC ? acc + __popc(w[u][k]) : acc ^ w[u][k];
+    }
+    if (acc == 0x12345678u) out[0] = acc;
+}
+
+// chunk read + one u16 score write per 32-byte unit (K3 two-pass shape):
+// scores go to a global array that stays L2-resident (16.7 MB)
+template <int U>
+__global__ void __launch_bounds__(256) rd_chunk_wr(const uint32_t* __restrict__ a, uint64_t units, uint16_t* sc) {
+    const uint64_t per = (units + gridDim.x - 1) / gridDim.x;
+    const uint64_t u0 = blockIdx.x * per, u1 = min(units, u0 + per);
+    for (uint64_t base = u0; base < u1; base += (uint64_t)U * 256) {
+        uint32_t w[U][8];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const uint64_t i = base + u * 256 + threadIdx.x;
+            if (i < u1) ld256(a + i * 8, w[u]); else for (int k = 0; k < 8; ++k) w[u][k] = 0;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const uint64_t i = base + u * 256 + threadIdx.x;
+            uint32_t m0 = 0, m1 = 0;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) { m0 += __popc(w[u][k]); m1 += __popc(w[u][k + 4]); }
+            if (i < u1) sc[i] = (uint16_t)(m0 | (m1 << 8));
+        }
+    }
+}
+
 // K3-fused-v2 pattern: CPP CTAs per problem, tiles of 256 units dealt
 // round-robin, KB tiles per load batch, double buffered
 template <int KB>
@@ -84,9 +163,8 @@ __global__ void __launch_bounds__(256) rd_tiles(const uint32_t* __restrict__ a, 
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
-template <int S>
-__global__ void __launch_bounds__(256) rd_tma(const uint8_t* __restrict__ a, uint64_t bytes, uint32_t* out) {
-    constexpr uint32_t CH = 16384;
+template <int S, uint32_t CH = 16384>
+__global__ void __launch_bounds__(512) rd_tma(const uint8_t* __restrict__ a, uint64_t bytes, uint32_t* out) {
     extern __shared__ __align__(128) uint8_t sm[];
     __shared__ __align__(8) uint64_t full[S], empty[S];
     const uint64_t nch = bytes / CH;
@@ -96,7 +174,7 @@ __global__ void __launch_bounds__(256) rd_tma(const uint8_t* __restrict__ a, uin
     if (tid == 0) {
         for (int s = 0; s < S; ++s) {
             asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"(smem_u32(&full[s])));
-            asm volatile("mbarrier.init.shared::cta.b64 [%0], 256;" :: "r"(smem_u32(&empty[s])));
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(smem_u32(&empty[s])), "r"(blockDim.x));
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -119,8 +197,8 @@ __global__ void __launch_bounds__(256) rd_tma(const uint8_t* __restrict__ a, uin
                          : "=r"(done) : "r"(smem_u32(&full[s])), "r"(ph) : "memory");
         const uint4* v = reinterpret_cast<const uint4*>(sm + s * CH);
 #pragma unroll
-        for (int k = 0; k < (int)(CH / 16 / 256); ++k) {
-            const uint4 x = v[k * 256 + tid];
+        for (uint32_t k = tid; k < CH / 16; k += blockDim.x) {
+            const uint4 x = v[k];
             acc ^= x.x ^ x.y ^ x.z ^ x.w;
         }
         asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"(smem_u32(&empty[s])) : "memory");
@@ -139,6 +217,7 @@ int main() {
     const uint64_t bytes = 268435456ull;
     uint32_t* a; uint32_t* o;
     cudaMalloc(&a, bytes); cudaMalloc(&o, 4);
+    uint32_t* a2; cudaMalloc(&a2, bytes / 16);
     cudaMemset(a, 1, bytes);
     int sms; cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
     cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
@@ -161,6 +240,73 @@ int main() {
         snprintf(n, 64, "chunk U8 grid=%dx", occ); timeit(n, [&] { rd_ldg_chunk<8><<<sms * occ, 256>>>(a, units, o); });
     }
     {
+        // same patterns with K3-fused's shared-memory carve-out (72 KB/CTA,
+        // 3 CTAs/SM): does the tiny L1 left over throttle the loads?
+        const int pad = 72 * 1024;
+        cudaFuncSetAttribute(rd_ldg_chunk<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, pad);
+        cudaFuncSetAttribute(rd_ldg_chunk<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, pad);
+        cudaFuncSetAttribute(rd_ldg<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, pad);
+        cudaFuncSetAttribute(rd_ldg<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, pad);
+        timeit("chunk U2 3x smem72K", [&] { rd_ldg_chunk<2><<<sms * 3, 256, pad>>>(a, units, o); });
+        timeit("chunk U4 3x smem72K", [&] { rd_ldg_chunk<4><<<sms * 3, 256, pad>>>(a, units, o); });
+        timeit("ldg256 U2 3x smem72K", [&] { rd_ldg<2><<<sms * 3, 256, pad>>>(a, units, o); });
+        timeit("ldg256 U4 3x smem72K", [&] { rd_ldg<4><<<sms * 3, 256, pad>>>(a, units, o); });
+        for (int kb : {20, 24, 28, 30, 32, 33, 36, 40, 44, 52, 56, 60, 64, 68, 70, 72}) {
+            const int pd = kb * 1024;
+            char n[64];
+            cudaFuncSetAttribute(rd_ldg_chunk<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, pd);
+            int occ = 0;
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, rd_ldg_chunk<2>, 256, pd);
+            snprintf(n, 64, "sweep chunk U2 3x smem%dK occ%d", kb, occ); timeit(n, [&] { rd_ldg_chunk<2><<<sms * 3, 256, pd>>>(a, units, o); });
+        }
+        {
+            auto run = [&](const char* name, auto k, int grid, int nt, int kb) {
+                cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, kb * 1024);
+                int occ = 0;
+                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, nt, kb * 1024);
+                char n[80];
+                snprintf(n, 80, "%s g%d smem%dK occ%d", name, grid, kb, occ);
+                timeit(n, [&] { k<<<grid, nt, kb * 1024>>>(a, units, o); });
+            };
+            run("db U4 NT128", rd_chunk_db<4, 128>, 576, 128, 47);
+            run("db U4 NT128", rd_chunk_db<4, 128>, 592, 128, 47);
+            run("db U2 NT128", rd_chunk_db<2, 128>, 576, 128, 47);
+            run("db U2 NT256", rd_chunk_db<2, 256>, 444, 256, 60);
+            run("db U1 NT256", rd_chunk_db<1, 256>, 444, 256, 60);
+            run("db U4 NT128", rd_chunk_db<4, 128>, 576, 128, 0);
+            run("db U2 NT256", rd_chunk_db<2, 256>, 444, 256, 0);
+            run("db U8 NT128", rd_chunk_db<8, 128>, 576, 128, 47);
+            run("sb U4 NT128 xor", rd_chunk_sb<4, 128, false>, 576, 128, 47);
+            run("sb U4 NT128 popc", rd_chunk_sb<4, 128, true>, 576, 128, 47);
+            run("sb U8 NT128 popc", rd_chunk_sb<8, 128, true>, 576, 128, 47);
+            run("sb U2 NT256 xor", rd_chunk_sb<2, 256, false>, 444, 256, 60);
+            run("sb U2 NT256 popc", rd_chunk_sb<2, 256, true>, 444, 256, 60);
+            run("sb U4 NT256 popc", rd_chunk_sb<4, 256, true>, 444, 256, 60);
+            run("sb U4 NT128 popc", rd_chunk_sb<4, 128, true>, 592, 128, 47);
+            run("sb U6 NT128 popc", rd_chunk_sb<6, 128, true>, 576, 128, 47);
+        }
+        for (int co : {50, 75, 100}) {
+            const int pd = 33 * 1024;
+            char n[64];
+            cudaFuncSetAttribute(rd_ldg_chunk<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, pd);
+            cudaFuncSetAttribute(rd_ldg_chunk<2>, cudaFuncAttributePreferredSharedMemoryCarveout, co);
+            snprintf(n, 64, "sweep chunk U2 3x smem33K carve%d", co); timeit(n, [&] { rd_ldg_chunk<2><<<sms * 3, 256, pd>>>(a, units, o); });
+        }
+        cudaFuncSetAttribute(rd_ldg_chunk<2>, cudaFuncAttributePreferredSharedMemoryCarveout, -1);
+        for (int kb : {0, 16, 33, 48}) {
+            const int pd = kb * 1024;
+            char n[64];
+            cudaFuncSetAttribute(rd_ldg_chunk<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, pd);
+            cudaFuncSetAttribute(rd_chunk_wr<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, pd);
+            cudaFuncSetAttribute(rd_chunk_wr<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, pd);
+            snprintf(n, 64, "chunk U2 3x smem%dK", kb); timeit(n, [&] { rd_ldg_chunk<2><<<sms * 3, 256, pd>>>(a, units, o); });
+            snprintf(n, 64, "chunk+wr U2 3x smem%dK", kb); timeit(n, [&] { rd_chunk_wr<2><<<sms * 3, 256, pd>>>(a, units, (uint16_t*)(a2)); });
+            snprintf(n, 64, "chunk+wr U4 2x smem%dK", kb); timeit(n, [&] { rd_chunk_wr<4><<<sms * 2, 256, pd>>>(a, units, (uint16_t*)(a2)); });
+        }
+        timeit("chunk U2 443 smem72K", [&] { rd_ldg_chunk<2><<<443, 256, pad>>>(a, units, o); });
+        timeit("chunk U2 3x", [&] { rd_ldg_chunk<2><<<sms * 3, 256>>>(a, units, o); });
+    }
+    {
         const uint32_t upp = (uint32_t)(units / 32);
         timeit("tiles KB4 CPP9 (288)", [&] { rd_tiles<4><<<32 * 9, 256>>>(a, 32, 9, upp, o); });
         timeit("tiles KB8 CPP9 (288)", [&] { rd_tiles<8><<<32 * 9, 256>>>(a, 32, 9, upp, o); });
@@ -168,6 +314,20 @@ int main() {
         timeit("tiles KB2 CPP13 (416)", [&] { rd_tiles<2><<<32 * 13, 256>>>(a, 32, 13, upp, o); });
         timeit("chunk U4 grid=288", [&] { rd_ldg_chunk<4><<<288, 256>>>(a, units, o); });
         timeit("ldg256 U4 grid=288", [&] { rd_ldg<4><<<288, 256>>>(a, units, o); });
+    }
+    {
+        // TMA ring at the fused kernel's budget: 1 CTA/SM, 512 threads,
+        // ~176 KB of the CTA's shared memory taken by counters + scores
+        auto run = [&](const char* name, auto k, int ring, int thr) {
+            const int dyn = ring + 176 * 1024;
+            cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
+            timeit(name, [&] { k<<<sms, thr, dyn>>>((const uint8_t*)a, bytes, o); });
+        };
+        run("tma S3x16K 1x512 +176K", rd_tma<3, 16384>, 3 * 16384, 512);
+        run("tma S4x12K 1x512 +176K", rd_tma<4, 12288>, 4 * 12288, 512);
+        run("tma S6x8K 1x512 +176K", rd_tma<6, 8192>, 6 * 8192, 512);
+        run("tma S3x16K 1x256 +176K", rd_tma<3, 16384>, 3 * 16384, 256);
+        run("tma S2x16K 1x512 +176K", rd_tma<2, 16384>, 2 * 16384, 512);
     }
     for (int occ : {1, 2}) {
         char n[64];
