@@ -124,6 +124,10 @@ spl_status spl_check_device_error(spl_ctx* ctx, void* stream) {
         return fail(ctx, SPL_E_NUMERIC, "mlp input contains non-finite values");
     if (flags & SPL_DEV_ERR_DIMENSION)
         return fail(ctx, SPL_E_DIMENSION, "attention: causal offset outside the cache");
+    if (flags & SPL_DEV_ERR_STALL)
+        return fail(ctx, SPL_E_CUDA,
+                    "hamming_topk: fused kernel CTAs were not co-resident (watchdog); "
+                    "set SPL_K3_COOP=1 or SPL_K3_PATH=twopass");
     return SPL_OK;
 }
 

@@ -18,9 +18,9 @@
 // histogram cannot keep up with ~1.5 rows/clk/SM.
 //
 // Fused path (k3_fused, see below): when the scores fit in shared memory (the
-// headline 32 x 512K case), one cooperative launch streams, histograms,
+// headline 32 x 512K case), one plain launch streams, histograms,
 // derives T / tie quota / offsets and compacts from shared memory, with
-// per-problem barriers only. One launch, one HBM pass.
+// per-problem readiness waits only. One launch, one HBM pass.
 // Two-pass path (k3_scan + k3_select): u8/u16 scores to an L2-resident
 // buffer; the CTA finishing a problem's last segment plans it; k3_select
 // compacts. Used for caches too large for on-chip scores and for the
@@ -33,6 +33,7 @@
 #include <cstdio>
 #include <string>
 #include <vector>
+#include <cstring>
 
 #include "spl_launch.cuh"
 #include "spl_plan.cuh"
@@ -513,6 +514,25 @@ __device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
     asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
     return v;
 }
+__device__ __forceinline__ uint64_t gtimer() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+// Spin (one thread) until *p >= need. A wait that outlives 2 s means some
+// CTA of the problem was never scheduled: flag SPL_DEV_ERR_STALL and give up
+// rather than hang the stream (results of that launch are then invalid).
+__device__ void wait_count(const uint32_t* p, uint32_t need, uint32_t* dev_err) {
+    if (ld_acquire(p) >= need) return;
+    const uint64_t t0 = gtimer();
+    while (ld_acquire(p) < need) {
+        __nanosleep(64);
+        if (gtimer() - t0 > 2000000000ull) {
+            raise_dev_err(dev_err, SPL_DEV_ERR_STALL);
+            return;
+        }
+    }
+}
 
 template <int W, typename ScoreT, bool PRIV>
 __global__ void __launch_bounds__(kThreads) k3_scan(K3Params prm) {
@@ -595,17 +615,14 @@ __global__ void __launch_bounds__(kThreads) k3_scan(K3Params prm) {
 
 // ------------------------------------------------------------ fused
 // Single-launch path for caches whose scores fit on chip (the headline
-// 32 x 512K case). Same contiguous-segment geometry as the two-pass path
-// (G = SMs x 3 CTAs at 80 registers), but scores stay in shared memory:
-// stream -> segment record + per-problem histogram (atomics) -> one grid
-// barrier (cooperative launch) -> each CTA derives T / tie quota from the
-// problem histogram and its output offset from the earlier segments'
-// records, then compacts its rows from shared memory.
-__device__ __forceinline__ uint64_t gtimer() {
-    uint64_t t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    return t;
-}
+// 32 x 512K case). Contiguous segments, a whole number per problem (G <= SMs
+// x 3 CTAs at 80 registers), scores kept in shared memory:
+// stream -> segment record + per-problem histogram of the window [L/2, L]
+// (atomics) -> wait for the problem's other segments -> T / tie quota from
+// the problem histogram (low-bin fallback when T < L/2), output offset from
+// the earlier segments' records -> compact the rows from shared memory.
+// Shared memory stays <= 196 KB/SM: above that the driver must choose the
+// 228 KB carve-out and LDG streaming loses ~16% (tools/read_bw.cu).
 #define K3_STAMP(i) \
     if (prm.trace && threadIdx.x == 0) prm.trace[blockIdx.x * 8 + (i)] = gtimer()
 
@@ -632,14 +649,21 @@ __global__ void __launch_bounds__(kThreads, 3) k3_fused(K3Params prm) {
         asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
         prm.trace[(uint64_t)blockIdx.x * 8 + 6] = smid;
     }
+    // The readiness waits below need every CTA of a problem resident: the
+    // plan keeps G <= SMs x CTAs/SM (occupancy API) and the launch is a plain
+    // one (a cooperative launch costs ~3 us more per graph replay; opt in
+    // with SPL_K3_COOP=1 where other work may hold SMs, e.g. MPS caps). If
+    // that ever fails, the watchdog in wait_count turns the hang into a
+    // device error. (Arrival tickets would remove the requirement but their
+    // single-address atomic delays the last CTAs' start by ~2 us.)
+    const uint32_t seg = blockIdx.x;
+    for (uint32_t i = tid; i < priv_bytes / 16; i += kThreads)
+        reinterpret_cast<uint4*>(priv)[i] = make_uint4(0, 0, 0, 0);
 
-    const uint64_t g0 = (uint64_t)blockIdx.x * g.S;
+    const uint64_t g0 = (uint64_t)seg * g.S;
     const uint64_t g1 = min(g0 + g.S, g.total);
     const uint32_t p_first = (uint32_t)(g0 / g.pstride);
     uint32_t region_off = 0;  // byte offset of the current piece's scores
-
-    for (uint32_t i = tid; i < priv_bytes / 16; i += kThreads)
-        reinterpret_cast<uint4*>(priv)[i] = make_uint4(0, 0, 0, 0);
 
     for (uint32_t p = p_first; p < g.P && (uint64_t)p * g.pstride < g1; ++p) {
         const uint64_t pbase = (uint64_t)p * g.pstride;
@@ -668,7 +692,7 @@ __global__ void __launch_bounds__(kThreads, 3) k3_fused(K3Params prm) {
         __syncthreads();
         // suffix-cumulative record; below the window it repeats rec[lo]
         block_suffix_sum(hist32, bins, s_warp);  // hist32[bins] stays 0
-        uint32_t* rec = prm.records + (uint64_t)(blockIdx.x + p) * (L + 2);
+        uint32_t* rec = prm.records + (uint64_t)(seg + p) * (L + 2);
         for (uint32_t t = tid; t < L + 2; t += kThreads) rec[t] = hist32[t];
         // publish: this segment of problem p is complete (record + histogram)
         __threadfence();
@@ -692,10 +716,9 @@ __global__ void __launch_bounds__(kThreads, 3) k3_fused(K3Params prm) {
         const uint64_t a0 = r0 & ~uint64_t(15);
         const ScoreT* sc = reinterpret_cast<const ScoreT*>(sregion + region_off);
         if (r0 < r1) region_off += (uint32_t)((((r1 - a0) * sizeof(ScoreT)) + 15) & ~uint64_t(15));
-        // wait only for the segments of THIS problem (cooperative launch: all
-        // of them are resident), not for the whole grid
-        if (tid == 0)
-            while (ld_acquire(prm.counters + p) < nseg) __nanosleep(32);
+        // wait only for the segments of THIS problem (all resident: see the
+        // ticket note above), not for the whole grid
+        if (tid == 0) wait_count(prm.counters + p, nseg, prm.dev_err);
         __syncthreads();
         uint32_t* tot = prm.tot_hist + (uint64_t)p * prm.tot_stride;
         // window bins only: CTAs that take the fallback below add the low
@@ -721,29 +744,29 @@ __global__ void __launch_bounds__(kThreads, 3) k3_fused(K3Params prm) {
                 if (hist32[b]) atomicAdd(tot + b, hist32[b]);
             __syncthreads();
             block_suffix_sum(hist32, lo, s_warp);
-            uint32_t* rec = prm.records + (uint64_t)(blockIdx.x + p) * (L + 2);
+            uint32_t* rec = prm.records + (uint64_t)(seg + p) * (L + 2);
             const uint32_t at_lo = __ldcg(rec + lo);
             for (uint32_t t = tid; t < lo; t += kThreads) rec[t] = at_lo + hist32[t];
             __threadfence();
             __syncthreads();
             if (tid == 0) {
                 atomicAdd(prm.counters2 + p, 1u);
-                while (ld_acquire(prm.counters2 + p) < nseg) __nanosleep(32);
+                wait_count(prm.counters2 + p, nseg, prm.dev_err);
             }
             __syncthreads();
             problem_threshold(tot, L, kk, s_cum, s_warp, &s_T, T, quota);
         }
         K3_STAMP(3);
         const uint32_t c0 = seg_first(g, p);
-        if (tid == 0 && blockIdx.x == c0) prm.cnt_out[p] = kk;
+        if (tid == 0 && seg == c0) prm.cnt_out[p] = kk;
         if (r0 >= r1) continue;
         if (T == SPL_PLAN_SKIP) continue;
         // (gt, eq) of the earlier segments of this problem, from their records
         uint64_t gt_before = 0, eq_before = 0;
-        for (uint32_t cb = c0; cb < blockIdx.x; cb += kThreads) {
+        for (uint32_t cb = c0; cb < seg; cb += kThreads) {
             const uint32_t c = cb + tid;
             uint32_t gtv = 0, eqv = 0;
-            if (c < blockIdx.x) {
+            if (c < seg) {
                 const uint32_t* r = prm.records + (uint64_t)(c + p) * (L + 2);
                 const uint32_t geT = __ldcg(r + T), geT1 = __ldcg(r + T + 1);
                 gtv = geT1;
@@ -755,7 +778,7 @@ __global__ void __launch_bounds__(kThreads, 3) k3_fused(K3Params prm) {
             eq_before += totv >> 32;
         }
         K3_STAMP(4);
-        const uint32_t* own = prm.records + (uint64_t)(blockIdx.x + p) * (L + 2);
+        const uint32_t* own = prm.records + (uint64_t)(seg + p) * (L + 2);
         const uint64_t eq_mine = (uint64_t)__ldcg(own + T) - __ldcg(own + T + 1);
         const uint64_t left = quota > eq_before ? quota - eq_before : 0;
         const uint32_t take = (uint32_t)(eq_mine < left ? eq_mine : left);
@@ -1156,7 +1179,11 @@ spl_status hamming_topk_impl(spl_ctx* ctx, const uint32_t* codes, uint64_t strid
             if (tr && *tr && !stream_capturing(s)) SPL_CUDA_TRY(ctx, cudaMalloc(&dtrace, (size_t)G * 8 * 8));
             prm.trace = dtrace;
             void* args[] = {&prm};
-            SPL_CUDA_TRY(ctx, cudaLaunchCooperativeKernel(fp.fn, dim3(G), dim3(kThreads), args, fp.smem, s));
+            const char* coop = getenv("SPL_K3_COOP");
+            if (coop && *coop == '1')
+                SPL_CUDA_TRY(ctx, cudaLaunchCooperativeKernel(fp.fn, dim3(G), dim3(kThreads), args, fp.smem, s));
+            else
+                SPL_CUDA_TRY(ctx, cudaLaunchKernel(fp.fn, dim3(G), dim3(kThreads), args, fp.smem, s));
             st = after_launch(ctx, "k3_fused");
             if (dtrace) {
                 std::vector<uint64_t> h((size_t)G * 8);
@@ -1181,9 +1208,10 @@ spl_status hamming_topk_impl(spl_ctx* ctx, const uint32_t* codes, uint64_t strid
                 if (*tr == '2') {  // per-CTA dump: cta, smid, stamps (us)
                     FILE* f = fopen("gpurun_out/k3_trace.csv", "w");
                     if (f) {
-                        fprintf(f, "cta,smid,start,stream,barrier,thresh,prefix,select\n");
+                        fprintf(f, "cta,smid,seg,start,stream,barrier,thresh,prefix,select\n");
                         for (uint32_t i = 0; i < G; ++i) {
-                            fprintf(f, "%u,%llu", i, (unsigned long long)h[i * 8 + 6]);
+                            fprintf(f, "%u,%llu,%llu", i, (unsigned long long)h[i * 8 + 6],
+                                    (unsigned long long)h[i * 8 + 7]);
                             for (int j = 0; j < 6; ++j) fprintf(f, ",%.3f", (double)(h[i * 8 + j] - t0) / 1000.0);
                             fprintf(f, "\n");
                         }

@@ -10,6 +10,7 @@
 
 #define SPL_DEV_ERR_NUMERIC 1u
 #define SPL_DEV_ERR_DIMENSION 2u
+#define SPL_DEV_ERR_STALL 4u  // K3-fused watchdog: a problem's CTAs were not co-resident
 
 // One context per caller (see spl_c.h). Owns the workspace and the device
 // error word. Workspace regions are sized by spl_reserve or lazily (never

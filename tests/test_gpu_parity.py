@@ -124,6 +124,24 @@ def test_topk_low_threshold_fallback(ctx, k3_path, oracle, L):
             assert np.array_equal(got[p], want[p, :kk]), (L, k, p)
 
 
+def test_topk_fused_cooperative_optin(ctx, oracle, monkeypatch):
+    """SPL_K3_COOP=1 launches the fused kernel cooperatively (co-residency
+    guaranteed by the driver); results are the same as the plain launch."""
+    rng = np.random.default_rng(77)
+    P, n, W = 5, 40000, 4
+    codes = rng.integers(0, 2**32, (P, n, W), dtype=np.uint64).astype(np.uint32)
+    q = rng.integers(0, 2**32, (P, W), dtype=np.uint64).astype(np.uint32)
+    nv = np.array([n, n - 1, 3000, 1, n], np.uint32)
+    want = oracle.retrieve_batch(codes, q, nv, 800)
+    plain = run_topk(ctx, codes, q, nv, 800)
+    monkeypatch.setenv("SPL_K3_COOP", "1")
+    coop = run_topk(ctx, codes, q, nv, 800)
+    for p in range(P):
+        kk = min(800, int(nv[p]))
+        assert np.array_equal(plain[p], want[p, :kk])
+        assert np.array_equal(coop[p], want[p, :kk])
+
+
 def test_topk_k_zero_rejected(ctx):
     codes = np.zeros((1, 10, 4), np.uint32)
     with pytest.raises(capi.DimensionError):
