@@ -272,6 +272,14 @@ __device__ void flush_priv(uint8_t* priv, uint32_t* hist32, uint32_t bins) {
     __syncthreads();
 }
 
+// Transposed on-chip layout of u8 scores (fused path): inside each 16-row
+// vector, word i byte b holds row 4b + i, so OR-ing the per-word SWAR flag
+// masks shifted by (7 - i) yields one flag bit per row in row order
+// (select_rows_t8). Byte position of row j (relative to the 16-aligned a0):
+__device__ __forceinline__ uint32_t tpos(uint32_t j) {
+    return (j & ~15u) | ((j & 3u) << 2) | ((j >> 2) & 3u);
+}
+
 // One row's agreement score from W words (edge rows: plain loads).
 template <int W>
 __device__ __forceinline__ uint32_t row_score(const uint32_t* row, const uint32_t* q, uint32_t L) {
@@ -292,6 +300,7 @@ __device__ void stream_piece(const uint32_t* base, const uint32_t* qp, uint32_t 
                              uint32_t* hist32, uint32_t bins, uint32_t lo) {
     // counters (priv rows / hist32 entries) are indexed by score - lo; scores
     // below lo are stored but not counted (lo = 0: full histogram)
+    constexpr bool TR = DST_SMEM && sizeof(ScoreT) == 1;  // transposed layout (tpos)
     const int tid = threadIdx.x;
     if constexpr (W > 0) {
         constexpr int R = 8 / W;  // rows per 32-byte unit
@@ -307,7 +316,10 @@ __device__ void stream_piece(const uint32_t* base, const uint32_t* qp, uint32_t 
             if ((uint32_t)tid < nhead + ntail) {
                 const uint64_t row = (uint32_t)tid < nhead ? r0 + tid : tail_beg + (tid - nhead);
                 const uint32_t sc = row_score<W>(base + row * W, q, L);
-                dst[row - dst_row0] = (ScoreT)sc;
+                if constexpr (TR)
+                    dst[tpos((uint32_t)(row - dst_row0))] = (ScoreT)sc;
+                else
+                    dst[row - dst_row0] = (ScoreT)sc;
                 if (sc >= lo) count_score<PRIV>(priv, hist32, sc - lo);
             }
         }
@@ -323,6 +335,9 @@ __device__ void stream_piece(const uint32_t* base, const uint32_t* qp, uint32_t 
         // of the loop (ld/st.shared.u8; asm volatile keeps their order)
         const uint32_t priv_s = (uint32_t)__cvta_generic_to_shared(priv) + priv_slot(tid);
         const uint32_t dst_s = DST_SMEM ? (uint32_t)__cvta_generic_to_shared(udst) : 0u;
+        // transposed layout: row index of this thread's unit 0 relative to a0
+        const uint32_t jb = (uint32_t)(uh * R - dst_row0) + (uint32_t)tid * R;
+        const uint32_t dst0_s = TR ? (uint32_t)__cvta_generic_to_shared(dst) : 0u;
         constexpr uint32_t per_it = (uint32_t)kThreads * kU;
         const uint32_t nit = (nu + per_it - 1) / per_it;
         // private u8 counters: flush before any thread can add 256 to a bin
@@ -363,7 +378,14 @@ __device__ void stream_piece(const uint32_t* base, const uint32_t* qp, uint32_t 
 #endif
             }
             const size_t off = ((size_t)it * per_it + (size_t)j * kThreads) * R;
-            if constexpr (DST_SMEM) {
+            if constexpr (TR) {
+                // R consecutive rows from a multiple of R (R | 16): row r of
+                // the unit sits 4 * (r % 4) + r / 4 bytes after tpos(first)
+                const uint32_t ad = dst0_s + tpos(jb + (uint32_t)off);
+#pragma unroll
+                for (int r = 0; r < R; ++r)
+                    asm volatile("st.shared.u8 [%0], %1;" ::"r"(ad + 4 * (r & 3) + (r >> 2)), "r"(sc[r]));
+            } else if constexpr (DST_SMEM) {
                 uint32_t v = 0;
 #pragma unroll
                 for (int r = 0; r < R; ++r) v |= sc[r] << (r * 8 * sizeof(ScoreT));
@@ -505,6 +527,108 @@ __device__ void select_rows(const ScoreT* sc, uint64_t a0, uint64_t r0, uint64_t
         }
         carry_gt += tot & 0xffffffffu;
         carry_eq += tot >> 32;
+    }
+}
+
+// Fused-path select over u8 scores in the transposed layout (tpos), L <= 128
+// so every score is <= 128: with c = (128 - t) * 0x01010101, byte x >= t
+// iff bit 7 of byte (x + c) is set, and x + c never carries into the next
+// byte. Per 4 rows: ge, gt (2 x IADD + LOP), eq = ge & ~gt, then the shifted
+// OR that turns the 0x80 flags of words 0..3 into one bit per row, in row
+// order (bit 8b + i <-> row 4b + i). Same contract as select_rows.
+// Each thread owns NV consecutive 16-row vectors per round; NV odd makes the
+// per-lane stride (16 * NV bytes) hit 8 distinct 16-byte bank groups across
+// any 8 lanes, so every LDS.128 is conflict-free (4 wavefronts). NV = 11
+// covers the headline segment (40448 rows) in one round (one block scan).
+// Offsets are 32-bit, relative to a0. Flags: per word (w + c) >> (7 - i)
+// masked with 0x01010101 << i and OR-ed (IADD, SHF, LOP3), so bit 8b + i of
+// a vector's mask is row 4b + i.
+__device__ void select_rows_t8(const uint8_t* sc, uint64_t a0, uint64_t r0, uint64_t r1,
+                               uint32_t T, uint32_t take, uint32_t* out, uint64_t* s_warp) {
+    constexpr int NV = 11;
+    constexpr int CH = 16 * NV;  // rows per thread per round
+    // T == 0: every row is >= T (x + 128 would carry for x = 128);
+    // T >= 128: no row is > T
+    const uint32_t c_ge = T >= 1 ? (128u - T) * 0x01010101u : 0u;
+    const uint32_t all_ge = T == 0 ? 0x0F0F0F0Fu : 0u;
+    const uint32_t c_gt = T < 128 ? (127u - T) * 0x01010101u : 0u;
+    const uint32_t m_gt = T < 128 ? 0x0F0F0F0Fu : 0u;
+    const uint32_t lo = (uint32_t)(r0 - a0), hi = (uint32_t)(r1 - a0);  // rows [lo, hi)
+    const uint32_t rb = (uint32_t)a0;  // output row ids are a0 + offset (32-bit)
+    const int tid = threadIdx.x;
+    const uint32_t round_rows = (uint32_t)kThreads * CH;
+    uint32_t carry_gt = 0, carry_eq = 0;
+    for (uint32_t base = 0; base < hi; base += round_rows) {
+        const uint32_t my = base + (uint32_t)tid * CH;
+        uint32_t gm[NV], em[NV];
+        uint32_t gt = 0, eq = 0;
+#pragma unroll
+        for (int v = 0; v < NV; ++v) {
+            const uint32_t at = my + 16u * v;
+            uint32_t g = 0, ge = 0;
+            if (at < hi) {
+                const uint4 x = *reinterpret_cast<const uint4*>(sc + at);
+                const uint32_t w[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    g |= ((w[i] + c_gt) >> (7 - i)) & (0x01010101u << i);
+                    ge |= ((w[i] + c_ge) >> (7 - i)) & (0x01010101u << i);
+                }
+                g &= m_gt;
+                ge |= all_ge;
+                if (at < lo || at + 16 > hi) {  // edge vector: rows outside [lo, hi)
+                    uint32_t valid = 0;
+                    for (uint32_t j = 0; j < 16; ++j)
+                        if (at + j >= lo && at + j < hi) valid |= 1u << (8 * (j >> 2) + (j & 3));
+                    g &= valid;
+                    ge &= valid;
+                }
+            }
+            gm[v] = g;
+            em[v] = ge & ~g;
+            gt += __popc(gm[v]);
+            eq += __popc(em[v]);
+        }
+        uint64_t tot;
+        const uint64_t ex = block_excl_scan_u64(((uint64_t)eq << 32) | gt, s_warp, tot);
+        if (gt | eq) {
+            const uint32_t eq_before = carry_eq + (uint32_t)(ex >> 32);
+            uint32_t pos = carry_gt + (uint32_t)ex + (eq_before < take ? eq_before : take);
+            if (eq_before + eq <= take || eq_before >= take) {
+                // all of this thread's ties are taken, or none
+                const bool ties = eq_before < take;
+#pragma unroll
+                for (int v = 0; v < NV; ++v) {
+                    uint32_t m = ties ? (gm[v] | em[v]) : gm[v];
+                    const uint32_t at = rb + my + 16u * v;
+                    while (m) {
+                        const uint32_t b = __ffs(m) - 1;
+                        m &= m - 1;
+                        out[pos++] = at + 4 * (b >> 3) + (b & 7);
+                    }
+                }
+            } else {  // the thread where the tie quota runs out
+                uint32_t eb = eq_before;
+#pragma unroll
+                for (int v = 0; v < NV; ++v) {
+                    uint32_t m = gm[v] | em[v];
+                    const uint32_t at = rb + my + 16u * v;
+                    while (m) {
+                        const uint32_t b = __ffs(m) - 1;
+                        m &= m - 1;
+                        const uint32_t row = at + 4 * (b >> 3) + (b & 7);
+                        if ((gm[v] >> b) & 1u) {
+                            out[pos++] = row;
+                        } else {
+                            if (eb < take) out[pos++] = row;
+                            ++eb;
+                        }
+                    }
+                }
+            }
+        }
+        carry_gt += (uint32_t)tot;
+        carry_eq += (uint32_t)(tot >> 32);
     }
 }
 
@@ -684,6 +808,15 @@ __global__ void __launch_bounds__(kThreads, 3) k3_fused(K3Params prm) {
             stream_piece<W, ScoreT, true, true>(prm.codes + (uint64_t)p * prm.stride_rows * W,
                                                 prm.qcodes + (uint64_t)p * W, L, r0, r1, dst, a0,
                                                 priv, hist32 + lo, wbins, lo);
+            if constexpr (sizeof(ScoreT) == 1) {
+                // zero the unused rows of the first / last 16-row vector: the
+                // SWAR compares of select_rows_t8 assume bytes <= 128, and
+                // left-over shared memory could carry into a valid row's byte
+                const uint32_t head = (uint32_t)(r0 - a0), end = (uint32_t)(r1 - a0);
+                const uint32_t pad_end = (end + 15u) & ~15u;
+                if ((uint32_t)tid < head) dst[tpos(tid)] = 0;
+                if (end + tid < pad_end) dst[tpos(end + tid)] = 0;
+            }
         }
         __syncthreads();
         uint32_t* tot = prm.tot_hist + (uint64_t)p * prm.tot_stride;
@@ -736,7 +869,7 @@ __global__ void __launch_bounds__(kThreads, 3) k3_fused(K3Params prm) {
             __syncthreads();
             if (r0 < r1)
                 for (uint64_t r = r0 + tid; r < r1; r += kThreads) {
-                    const uint32_t v = sc[r - a0];
+                    const uint32_t v = sizeof(ScoreT) == 1 ? sc[tpos((uint32_t)(r - a0))] : sc[r - a0];
                     if (v < lo) atomicAdd(hist32 + v, 1u);
                 }
             __syncthreads();
@@ -783,8 +916,12 @@ __global__ void __launch_bounds__(kThreads, 3) k3_fused(K3Params prm) {
         const uint64_t left = quota > eq_before ? quota - eq_before : 0;
         const uint32_t take = (uint32_t)(eq_mine < left ? eq_mine : left);
         const uint64_t off = gt_before + (eq_before < quota ? eq_before : quota);
-        select_rows<ScoreT, false>(sc, a0, r0, r1, T, take,
-                                   prm.idx_out + (uint64_t)p * prm.idx_stride + off, s_warp);
+        if constexpr (sizeof(ScoreT) == 1)
+            select_rows_t8(reinterpret_cast<const uint8_t*>(sc), a0, r0, r1, T, take,
+                           prm.idx_out + (uint64_t)p * prm.idx_stride + off, s_warp);
+        else
+            select_rows<ScoreT, false>(sc, a0, r0, r1, T, take,
+                                       prm.idx_out + (uint64_t)p * prm.idx_stride + off, s_warp);
     }
     K3_STAMP(5);
 

@@ -399,6 +399,14 @@ TEST_CASE("drop-in == reference: mlp_forward, hash_topk, sparse_attention") {
     for (std::uint32_t r = 0; r < n; ++r) {
         std::vector<std::uint32_t> want(ridx.begin() + static_cast<std::size_t>(r) * k,
                                         ridx.begin() + static_cast<std::size_t>(r) * k + rcnt[r]);
+        if (same && res.indices[r] != want) {
+            std::fprintf(stderr, "hash_topk differs at query %u (got %zu, want %zu):", r,
+                         res.indices[r].size(), want.size());
+            for (std::size_t i = 0; i < want.size() && i < res.indices[r].size(); ++i)
+                if (res.indices[r][i] != want[i])
+                    std::fprintf(stderr, " [%zu] %u!=%u", i, res.indices[r][i], want[i]);
+            std::fprintf(stderr, "\n");
+        }
         same = same && (res.indices[r] == want);
     }
     CHECK(same);

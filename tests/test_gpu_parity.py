@@ -152,17 +152,25 @@ def test_topk_k_zero_rejected(ctx):
                          4, idx, idx)
 
 
-def test_topk_shared_cache_causal(ctx, k3_path, oracle):
-    """hash_topk's layout: q queries share one cache, query r sees rows < r+1."""
-    rng = np.random.default_rng(9)
-    n, W = 3000, 4
+@pytest.mark.parametrize("n,k", [(3000, 64), (600, 24), (1000, 1)])
+def test_topk_shared_cache_causal(ctx, k3_path, oracle, n, k):
+    """hash_topk's layout: q queries share one cache, query r sees rows < r+1.
+    P = n problems > the fused plan's CTA target, so segments straddle
+    problems and most small problems take the low-bin fallback."""
+    rng = np.random.default_rng(9 + n)
+    W = 4
     codes = rng.integers(0, 2**32, (n, W), dtype=np.uint64).astype(np.uint32)
     q = rng.integers(0, 2**32, (n, W), dtype=np.uint64).astype(np.uint32)
     offs = np.arange(1, n + 1, dtype=np.uint32)
-    got = run_topk(ctx, codes[None], q, offs, 64, stride_rows=0, n_max=n)
-    for r in range(0, n, 97):
+    got = run_topk(ctx, codes[None], q, offs, k, stride_rows=0, n_max=n)
+    bad = []
+    for r in range(n):
         s = oracle.nxor_scores(q[r], codes, int(offs[r]))
-        assert np.array_equal(got[r], oracle.top_k(s, min(64, int(offs[r]))))
+        if not np.array_equal(got[r], oracle.top_k(s, min(k, int(offs[r])))):
+            bad.append(r)
+    assert not bad, (len(bad), bad[:10], got[bad[0]][:8].tolist(),
+                     oracle.top_k(oracle.nxor_scores(q[bad[0]], codes, int(offs[bad[0]])),
+                                  min(k, int(offs[bad[0]])))[:8].tolist())
 
 
 def test_topk_nvalid_per_batch(ctx, k3_path, oracle):
