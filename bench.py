@@ -365,7 +365,7 @@ def main():
                    "heads": H, "tokens_per_gpu": n_local, "tokens_total": n_total, "code_bits": L,
                    "k": k, "l2": "inputs (268 MB codes) larger than the 126 MB L2; no flush"},
         "roofline": {"bound": "hbm",
-                     "kernel": ("one retrieval = k3_fused (single cooperative launch)" if world == 1
+                     "kernel": ("one retrieval = k3_fused (single launch)" if world == 1
                                 else "k3_scan + NCCL all-gather + k3_shard_plan + k3_select"),
                      "achieved": round(achieved, 1), "peak": hbm, "peak_kind": peak_kind,
                      "unit": "GB/s", "frac": round(achieved / hbm, 4),
