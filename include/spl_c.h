@@ -165,6 +165,15 @@ spl_status spl_mlp_forward(spl_ctx* ctx, const spl_hasher* hasher, const float* 
  * the bf16 error band). Non-finite input raises the device error word. */
 spl_status spl_encode(spl_ctx* ctx, const spl_hasher* hasher, const float* x, uint32_t B,
                       uint32_t m, int mode, uint32_t* codes, void* stream);
+/* Bulk / prefill encode on the tcgen05 tensor cores (K2, the SPL_ENCODE_TC
+ * mode of spl_encode with a choice of input dtype): x [B][H][m][d] f32 or
+ * bf16 (x_dtype SPL_F32 / SPL_BF16) -> codes [B][H][m][W]; bf16 operands,
+ * fp32 accumulation. Needs d = 128 (MLP: h = 128) and L in {32, 64, 128,
+ * 256}, else SPL_E_DIMENSION. pre (nullable) receives the f32
+ * pre-activations [B][H][m][L] (numerics tests). Replaces the same
+ * mlp_hash / linear_hash + pack_bits as spl_encode (hashers.hpp:70-79). */
+spl_status spl_encode_tc(spl_ctx* ctx, const spl_hasher* hasher, const void* x, int x_dtype,
+                         uint32_t B, uint32_t m, uint32_t* codes, float* pre, void* stream);
 /* Decode-time append (new capability): for every (b, head),
  * encode k_new[b][head] (exact mode) into codes[b][head][pos[b]] and copy
  * k_new / v_new into the K/V caches at the same slot (kv_dtype storage,

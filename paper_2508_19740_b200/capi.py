@@ -91,6 +91,7 @@ _SIGS = {
     "spl_hasher_destroy": [vp],
     "spl_mlp_forward": [vp, vp, vp, u32, u32, vp, vp],
     "spl_encode": [vp, vp, vp, u32, u32, i32, vp, vp],
+    "spl_encode_tc": [vp, vp, vp, i32, u32, u32, vp, vp, vp],
     "spl_encode_append": [vp, vp, vp, vp, u32, vp, vp, vp, i32, u64, vp, vp],
     "spl_sparse_attend": [vp, vp, vp, vp, i32, u64, u32, u32, vp, u64, vp, vp, u32, f32, vp, vp],
     "spl_sparse_attend_partial": [vp, vp, vp, vp, i32, u64, u32, u32, vp, u64, vp, vp, u32, f32,
@@ -319,6 +320,12 @@ class Hasher:
     def encode(self, x, B, m, codes, mode=SPL_ENCODE_EXACT, stream=None):
         self.ctx.check(self.ctx.lib.spl_encode(self.ctx.h, self.h, _ptr(x), B, m, mode, _ptr(codes),
                                                _stream(stream)))
+
+    def encode_tc(self, x, x_dtype, B, m, codes, pre=None, stream=None):
+        """tcgen05 bulk encoder (K2): x [B][H][m][d] f32 / bf16 -> codes; pre
+        (optional f32 [B][H][m][L]) receives the pre-activations."""
+        self.ctx.check(self.ctx.lib.spl_encode_tc(self.ctx.h, self.h, _ptr(x), x_dtype, B, m,
+                                                  _ptr(codes), _ptr(pre), _stream(stream)))
 
     def encode_append(self, k_new, v_new, B, codes, kcache, vcache, kv_dtype, cap, pos,
                       stream=None):

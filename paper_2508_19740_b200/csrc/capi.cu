@@ -8,8 +8,10 @@
 #include <cmath>
 #include <string>
 #include <vector>
+#include <cstring>
 
 #include "spl_launch.cuh"
+#include "spl_tc.cuh"
 
 
 using namespace spl;
@@ -294,6 +296,36 @@ spl_status spl_hasher_create(spl_ctx* ctx, int kind, uint32_t H, uint32_t d, uin
         spl_hasher_destroy(hs);
         return fail(ctx, SPL_E_CUDA, "hasher: device allocation failed");
     }
+    // tcgen05 bulk encoder operands (encode_tc.cu / spl_tc.cuh): per head, B
+    // operands K-major bf16 swizzled: W1^T [N1 = h (linear: L)][K = d] and
+    // W2^T [L][K = h]
+    if (encode_tc_eligible(kind, d, h, L)) {
+        const uint32_t N1 = kind == SPL_HASHER_MLP ? h : L, cols1 = N1;
+        const size_t ob1 = tc_operand_bytes(N1), ob2 = tc_operand_bytes(L);
+        std::vector<uint8_t> t1((size_t)H * ob1), t2(kind == SPL_HASHER_MLP ? (size_t)H * ob2 : 0);
+        for (uint32_t hd = 0; hd < H; ++hd)
+            for (uint32_t n = 0; n < N1; ++n)
+                for (uint32_t k = 0; k < d; ++k) {
+                    const uint16_t b = tc_bf16_bits(h1[((size_t)hd * d + k) * cols1 + n]);
+                    std::memcpy(&t1[hd * ob1 + tc_sw_off(n, k, N1)], &b, 2);
+                }
+        if (kind == SPL_HASHER_MLP)
+            for (uint32_t hd = 0; hd < H; ++hd)
+                for (uint32_t n = 0; n < L; ++n)
+                    for (uint32_t k = 0; k < h; ++k) {
+                        const uint16_t b = tc_bf16_bits(h2[((size_t)hd * h + k) * L + n]);
+                        std::memcpy(&t2[hd * ob2 + tc_sw_off(n, k, L)], &b, 2);
+                    }
+        auto upb = [&](void** dst, const std::vector<uint8_t>& src) -> bool {
+            if (src.empty()) return true;
+            if (cudaMalloc(dst, src.size()) != cudaSuccess) return false;
+            return cudaMemcpy(*dst, src.data(), src.size(), cudaMemcpyHostToDevice) == cudaSuccess;
+        };
+        if (!upb(&hs->w1_tc, t1) || !upb(&hs->w2_tc, t2)) {
+            spl_hasher_destroy(hs);
+            return fail(ctx, SPL_E_CUDA, "hasher: device allocation failed");
+        }
+    }
     *out = hs;
     return SPL_OK;
 }
@@ -325,7 +357,8 @@ spl_status spl_mlp_forward(spl_ctx* ctx, const spl_hasher* hs, const float* x, u
 spl_status spl_encode(spl_ctx* ctx, const spl_hasher* hs, const float* x, uint32_t B, uint32_t m,
                       int mode, uint32_t* codes, void* stream) {
     if (!ctx || !hs) return SPL_E_STATE;
-    if (mode == SPL_ENCODE_TC) return encode_tc_launch(ctx, hs, x, B, m, codes, S(stream));
+    if (mode == SPL_ENCODE_TC)
+        return encode_tc_launch(ctx, hs, x, SPL_F32, B, m, codes, nullptr, S(stream));
     if (mode != SPL_ENCODE_EXACT) return fail(ctx, SPL_E_DIMENSION, "encode: unknown mode");
     EncJob j{};
     j.x = x;
@@ -333,6 +366,12 @@ spl_status spl_encode(spl_ctx* ctx, const spl_hasher* hs, const float* x, uint32
     j.out_mode = ENC_CODES;
     j.codes = codes;
     return encode_exact_launch(ctx, hs, B, &j, 1, S(stream));
+}
+
+spl_status spl_encode_tc(spl_ctx* ctx, const spl_hasher* hs, const void* x, int x_dtype,
+                         uint32_t B, uint32_t m, uint32_t* codes, float* pre, void* stream) {
+    if (!ctx || !hs) return SPL_E_STATE;
+    return encode_tc_launch(ctx, hs, x, x_dtype, B, m, codes, pre, S(stream));
 }
 
 spl_status spl_encode_append(spl_ctx* ctx, const spl_hasher* hs, const float* k_new,

@@ -66,8 +66,9 @@ spl_status top_k_launch(spl_ctx*, const void*, int, uint32_t, uint64_t, uint64_t
 spl_status encode_exact_launch(spl_ctx*, const spl_hasher*, uint32_t, const EncJob*, int,
                                cudaStream_t);
 // encode_tc.cu
-spl_status encode_tc_launch(spl_ctx*, const spl_hasher*, const float*, uint32_t, uint32_t,
-                            uint32_t*, cudaStream_t);
+spl_status encode_tc_launch(spl_ctx*, const spl_hasher*, const void* x, int x_dtype, uint32_t B,
+                            uint32_t m, uint32_t* codes, float* pre, cudaStream_t);
+bool encode_tc_eligible(uint32_t kind, uint32_t d, uint32_t h, uint32_t L);
 // sparse_attend.cu
 spl_status sparse_attend_launch(spl_ctx*, AttParams, uint32_t, int, cudaStream_t);
 spl_status attend_combine_launch(spl_ctx*, const float*, uint32_t, uint32_t, uint32_t, float*,
