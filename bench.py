@@ -49,6 +49,15 @@ def peaks():
         return 6650.0, "fallback"
 
 
+def tensor_peak():
+    """(burst, sustained) dense bf16 TF/s from MEASURED_PEAKS.json."""
+    try:
+        p = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
+        return float(p["bf16_tflops"]), float(p["bf16_tflops_sustained"]), "measured"
+    except Exception:
+        return 2250.0, 2250.0, "fallback (nominal dense)"
+
+
 # ---------------------------------------------------------------- clocks
 class ClockSampler:
     FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
@@ -194,6 +203,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-decode", action="store_true")
+    ap.add_argument("--no-prefill", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
@@ -294,6 +304,7 @@ def main():
     rng = np.random.default_rng(7)
     e2e = None
     decode = None
+    prefill = None
     if world == 1:
         w1 = (rng.standard_normal((H, D, D)) / np.sqrt(D)).astype(np.float32)
         b1 = np.zeros((H, D), np.float32)
@@ -323,6 +334,8 @@ def main():
                "encode_us": round(enc_ms * 1000, 2)}
         if not args.no_decode:
             decode = bench_decode(torch, capi, ctx, dev, stream, args, hasher)
+        if not args.no_prefill:
+            prefill = bench_prefill(torch, capi, ctx, dev, stream, args)
     clk = clocks.stop()
 
     # CPU baseline (rank 0, N = 1): the reference on this host's cores
@@ -382,11 +395,60 @@ def main():
     }
     if decode:
         line["sparse_decode"] = decode
+    if prefill:
+        line["prefill_encode"] = prefill
     if rank == 0:
         print(json.dumps(line), flush=True)
     ctx.close()
     if dist:
         dist.destroy_process_group()
+
+
+def bench_prefill(torch, capi, ctx, dev, stream, args):
+    """Config 4 prefill: K2 (tcgen05) encodes B=16 x 32 heads x 131072 bf16
+    keys (17.2 GB) into 256-bit codes, one spl_encode_tc call per step.
+    98,304 FLOP per key (2dh + 2hL)."""
+    B, n, L4 = 16, 131072, 256
+    rng = np.random.default_rng(4)
+    w1 = (rng.standard_normal((H, D, D)) / np.sqrt(D)).astype(np.float32)
+    b1 = np.zeros((H, D), np.float32)
+    w2 = (rng.standard_normal((H, D, L4)) / np.sqrt(D)).astype(np.float32)
+    hs = ctx.hasher(w1, b1, w2)
+    g = torch.Generator(device=dev)
+    g.manual_seed(44)
+    x = torch.empty((B, H, n, D), device=dev, dtype=torch.bfloat16)
+    for b in range(B):  # fill in slices (keeps the f32 temporary small)
+        x[b].copy_(torch.randn((H, n, D), generator=g, device=dev, dtype=torch.float32))
+    codes = torch.empty((B, H, n, L4 // 32), device=dev, dtype=torch.int32)
+
+    def step():
+        hs.encode_tc(x, capi.SPL_BF16, B, n, codes, None, stream)
+
+    for _ in range(args.warmup):
+        step()
+    steps = min(args.steps, 10)
+    l0 = ctx.launches()
+    ms = event_timer(torch, step, steps, stream)
+    launches = (ctx.launches() - l0) / steps
+    keys = B * H * n
+    flops = keys * (2 * D * D + 2 * D * L4)
+    nbytes = keys * D * 2 + keys * (L4 // 32) * 4 + H * (D * D + D * L4) * 2
+    burst, sustained, kind = tensor_peak()
+    hbm, _ = peaks()
+    tf = flops / (ms * 1e-3) / 1e12
+    gbs = nbytes / (ms * 1e-3) / 1e9
+    del x, codes
+    hs.close() if hasattr(hs, "close") else None
+    return {"workload": "config4 prefill: 16 x 32 heads x 131072 bf16 keys, d = h = 128, L = 256 "
+                        "(K2 tcgen05, bf16 operands, fp32 TMEM accumulation)",
+            "ms_per_step": round(ms, 3), "keys_per_s": round(keys / (ms * 1e-3) / 1e9, 3),
+            "unit_keys": "G keys/s", "gpu_launches_per_step": launches,
+            "roofline": {"tensor": {"achieved": round(tf, 1), "unit": "TFLOP/s", "peak": burst,
+                                    "peak_kind": f"{kind} burst", "frac": round(tf / burst, 4),
+                                    "frac_of_sustained": round(tf / sustained, 4),
+                                    "flops": flops},
+                         "hbm": {"achieved": round(gbs, 1), "unit": "GB/s", "peak": hbm,
+                                 "frac": round(gbs / hbm, 4), "algorithmic_bytes": nbytes}}}
 
 
 def bench_decode(torch, capi, ctx, dev, stream, args, hasher_c3):

@@ -24,7 +24,12 @@
 // Roofline (SURVEY §8 d, config 4 prefill): 98,304 FLOP per key (2dh + 2hL,
 // d = h = L = 128: 65,536; L = 256: 98,304) against 256 B (bf16) or 512 B
 // (f32) of input per key: bf16 input at L = 256 is at/above the ridge.
+#include <cuda.h>
 #include <cuda_bf16.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <cstring>
 
 #include "spl_launch.cuh"
 #include "spl_tc.cuh"
@@ -104,18 +109,6 @@ __device__ __forceinline__ void fence_after() {
 __device__ __forceinline__ void fence_async_smem() {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
-__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
-    uint32_t r[16];
-    asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
-          "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
-          "=r"(r[14]), "=r"(r[15])
-        : "r"(taddr));
-    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-    for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
-}
 __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
     const __nv_bfloat162 t = __floats2bfloat162_rn(a, b);
     return *reinterpret_cast<const uint32_t*>(&t);
@@ -151,25 +144,119 @@ __device__ __forceinline__ void stage_x(const TcParams& prm, uint64_t bh, uint32
     if (bad) raise_dev_err(prm.dev_err, SPL_DEV_ERR_NUMERIC);
 }
 
-__global__ void __launch_bounds__(kTcThreads, 1) k2_encode_tc(TcParams prm) {
+// SiLU with one MUFU op: z * sigmoid(z) = 0.5 z (1 + tanh(z / 2))
+__device__ __forceinline__ float silu_fast(float z) {
+    float t;
+    asm("tanh.approx.f32 %0, %1;" : "=f"(t) : "f"(0.5f * z));
+    return 0.5f * z * (1.0f + t);
+}
+
+__device__ __forceinline__ void tma_x(const CUtensorMap* tmap, uint8_t* dst, uint64_t* bar,
+                                      uint64_t row) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(tc_operand_bytes(kTcTileM))
+                 : "memory");
+#pragma unroll
+    for (uint32_t kb = 0; kb < 2; ++kb)
+        asm volatile(
+            "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::
+                "r"(smem_u32(dst + kb * kTcTileM * 128u)),
+            "l"(reinterpret_cast<uint64_t>(tmap)), "r"(kb * 64u), "r"((uint32_t)row), "r"(smem_u32(bar))
+            : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld16_nowait(uint32_t taddr, uint32_t (&r)[16]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+          "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+          "=r"(r[14]), "=r"(r[15])
+        : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
+// Epilogue 2 for one column half: code bit of column j = (z_j >= 0) goes to
+// word j % W, bit 31 - j / W (Appendix A.7). Collects NEGATIVE flags (sign
+// bits after z + 0, which maps -0 to +0) with compile-time shifts: per column
+// FADD, SHF, LOP3; the word is the complement. `sum` accumulates the values
+// (non-finite check). Two TMEM loads in flight per wait.
+template <uint32_t W, uint32_t HALF>
+__device__ __forceinline__ void sign_half(uint32_t tz, uint32_t (&neg)[W], float& sum) {
+    constexpr uint32_t L = 32 * W, NCH = W;  // W chunks of 16 columns per half
+#pragma unroll
+    for (uint32_t cp = 0; cp < NCH; cp += 2) {
+        uint32_t r[2][16];
+        tmem_ld16_nowait(tz + HALF * (L / 2) + 16 * cp, r[0]);
+        if (cp + 1 < NCH) tmem_ld16_nowait(tz + HALF * (L / 2) + 16 * (cp + 1), r[1]);
+        tmem_wait_ld();
+#pragma unroll
+        for (uint32_t q = 0; q < 2; ++q) {
+            if (cp + q >= NCH) break;
+            const uint32_t c0 = HALF * (L / 2) + 16 * (cp + q);
+#pragma unroll
+            for (uint32_t i = 0; i < 16; ++i) {
+                const float z = __uint_as_float(r[q][i]);
+                sum += z;
+                const uint32_t u = __float_as_uint(z + 0.0f);
+                const uint32_t sh = (c0 + i) / W;
+                neg[(c0 + i) % W] |= (u >> sh) & (0x80000000u >> sh);
+            }
+        }
+    }
+}
+
+// TMA_X: bf16 input through a 2-D tensor map (128-byte swizzle = the UMMA
+// operand layout) into a 2-slot ring, issued two tiles ahead; otherwise (f32
+// input) all threads convert and stage the tile two ahead once its slot is free.
+template <bool TMA_X, uint32_t W>
+__global__ void __launch_bounds__(kTcThreads, 1)
+    k2_encode_tc(const __grid_constant__ CUtensorMap tmap, TcParams prm) {
     extern __shared__ uint8_t smem_raw[];
-    __shared__ __align__(8) uint64_t s_bar[2];
+    __shared__ __align__(8) uint64_t s_bar[4];  // [0,1] X slot full, [2] GEMM1 done, [3] GEMM2 done
     __shared__ uint32_t s_tmem;
     __shared__ float s_b1[kTcK];
+    constexpr uint32_t L = 32 * W;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const uint32_t L = prm.L, W = prm.W;
     const uint32_t N1 = prm.linear ? L : kTcK;
-    // 1024-aligned operand regions: sX, sA1 (128 rows), sW1 (N1 rows), sW2 (L rows), s_code
     const uint32_t base_s = (smem_u32(smem_raw) + 1023u) & ~1023u;
     uint8_t* base = smem_raw + (base_s - smem_u32(smem_raw));
-    uint8_t* sX = base;
-    uint8_t* sA1 = sX + tc_operand_bytes(kTcTileM);
+    uint8_t* sX0 = base;  // 2 slots
+    uint8_t* sA1 = sX0 + 2 * tc_operand_bytes(kTcTileM);
     uint8_t* sW1 = sA1 + tc_operand_bytes(kTcTileM);
     uint8_t* sW2 = sW1 + tc_operand_bytes(N1);
     uint32_t* s_code = reinterpret_cast<uint32_t*>(sW2 + (prm.linear ? 0u : tc_operand_bytes(L)));
+    auto sX = [&](uint64_t t) { return sX0 + (t & 1) * tc_operand_bytes(kTcTileM); };
 
     const uint64_t T = prm.total_tiles;
+    const uint32_t tpp = prm.tiles_per_problem;
     const uint64_t t0 = T * blockIdx.x / gridDim.x, t1 = T * (blockIdx.x + 1) / gridDim.x;
+    // tile t <-> (problem bh, tile-in-problem mb), head = bh % H; walked incrementally
+    struct Pos {
+        uint64_t bh;
+        uint32_t mb, head;
+    };
+    auto pos_of = [&](uint64_t t) {
+        Pos p;
+        p.bh = t / tpp;
+        p.mb = (uint32_t)(t - p.bh * tpp);
+        p.head = (uint32_t)(p.bh % prm.H);
+        return p;
+    };
+    auto next = [&](Pos p) {
+        if (++p.mb == tpp) {
+            p.mb = 0;
+            ++p.bh;
+            if (++p.head == prm.H) p.head = 0;
+        }
+        return p;
+    };
+    auto stage = [&](uint64_t t, Pos p) {  // bring tile t's keys into its slot
+        if (TMA_X) {
+            if (tid == 0) tma_x(&tmap, sX(t), &s_bar[t & 1], p.bh * prm.m + (uint64_t)p.mb * kTcTileM);
+        } else {
+            stage_x(prm, p.bh, p.mb * kTcTileM, sX(t));
+        }
+    };
     if (warp == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
                          smem_u32(&s_tmem))
@@ -177,9 +264,10 @@ __global__ void __launch_bounds__(kTcThreads, 1) k2_encode_tc(TcParams prm) {
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
     }
     if (tid == 0) {
-        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&s_bar[0])));
-        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&s_bar[1])));
+        for (int i = 0; i < 4; ++i)
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&s_bar[i])));
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        if (TMA_X) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap)) : "memory");
     }
     fence_before();
     __syncthreads();
@@ -190,119 +278,148 @@ __global__ void __launch_bounds__(kTcThreads, 1) k2_encode_tc(TcParams prm) {
     const uint32_t row = quarter * 32 + lane;  // this thread's TMEM lane = tile row
     const uint32_t lane_addr = (quarter * 32) << 16;
 
-    uint32_t phase = 0;
-    uint64_t cur_head = ~0ull;
-    if (t0 < t1) {
-        const uint64_t bh0 = t0 / prm.tiles_per_problem;
-        stage_x(prm, bh0, (uint32_t)(t0 % prm.tiles_per_problem) * kTcTileM, sX);
-    }
-    for (uint64_t t = t0; t < t1; ++t) {
-        const uint64_t bh = t / prm.tiles_per_problem;
-        const uint32_t row0 = (uint32_t)(t % prm.tiles_per_problem) * kTcTileM;
-        const uint64_t head = bh % prm.H;
-        if (head != cur_head) {  // previous MMAs are complete (waited below)
-            const uint4* g1 = reinterpret_cast<const uint4*>(prm.w1_tc + head * tc_operand_bytes(N1));
-            for (uint32_t i = tid; i < tc_operand_bytes(N1) / 16; i += kTcThreads)
-                reinterpret_cast<uint4*>(sW1)[i] = __ldg(g1 + i);
-            if (!prm.linear) {
-                const uint4* g2 = reinterpret_cast<const uint4*>(prm.w2_tc + head * tc_operand_bytes(L));
-                for (uint32_t i = tid; i < tc_operand_bytes(L) / 16; i += kTcThreads)
-                    reinterpret_cast<uint4*>(sW2)[i] = __ldg(g2 + i);
-                for (uint32_t i = tid; i < kTcK; i += kTcThreads) s_b1[i] = prm.b1[head * kTcK + i];
-            }
-            cur_head = head;
-        }
-        fence_async_smem();
-        fence_before();
-        __syncthreads();
-        // ---- GEMM1
-        if (tid == 0) {
-            fence_after();
-            gemm_k128(tD1, smem_u32(sX), smem_u32(sW1), N1);
-            umma_commit(&s_bar[0]);
-        }
-        mbar_wait(&s_bar[0], phase);
-        fence_after();
-        uint32_t tZ = tD1;
+    uint32_t xph = 0, g1ph = 0, g2ph = 0;  // xph bit s: parity of X slot s
+    uint32_t cur_head = ~0u;
+    bool g1_issued = false;  // GEMM1 of the current tile already in flight
+    Pos pc = pos_of(t0 < t1 ? t0 : 0);
+    if (t0 < t1) stage(t0, pc);
+    Pos pn = next(pc), pnn = next(pn);
+    if (t0 + 1 < t1) stage(t0 + 1, pn);
+    auto load_weights = [&](uint32_t head) {
+        const uint4* g1 = reinterpret_cast<const uint4*>(prm.w1_tc + (uint64_t)head * tc_operand_bytes(N1));
+        for (uint32_t i = tid; i < tc_operand_bytes(N1) / 16; i += kTcThreads)
+            reinterpret_cast<uint4*>(sW1)[i] = __ldg(g1 + i);
         if (!prm.linear) {
-            // ---- epilogue 1: +b1, SiLU -> bf16 A1 (columns [64 half, +64))
-#pragma unroll 1
-            for (uint32_t c0 = half * 64; c0 < half * 64 + 64; c0 += 16) {
-                float v[16];
-                tmem_ld16(tD1 + lane_addr + c0, v);
-                uint32_t p[8];
-#pragma unroll
-                for (int i = 0; i < 16; i += 2) {
-                    const float z0 = v[i] + s_b1[c0 + i], z1 = v[i + 1] + s_b1[c0 + i + 1];
-                    p[i / 2] = pack_bf16(__fdividef(z0, 1.0f + __expf(-z0)),
-                                         __fdividef(z1, 1.0f + __expf(-z1)));
-                }
-                *reinterpret_cast<uint4*>(sA1 + tc_sw_off(row, c0, kTcTileM)) =
-                    make_uint4(p[0], p[1], p[2], p[3]);
-                *reinterpret_cast<uint4*>(sA1 + tc_sw_off(row, c0 + 8, kTcTileM)) =
-                    make_uint4(p[4], p[5], p[6], p[7]);
+            const uint4* g2 = reinterpret_cast<const uint4*>(prm.w2_tc + (uint64_t)head * tc_operand_bytes(L));
+            for (uint32_t i = tid; i < tc_operand_bytes(L) / 16; i += kTcThreads)
+                reinterpret_cast<uint4*>(sW2)[i] = __ldg(g2 + i);
+            for (uint32_t i = tid; i < kTcK; i += kTcThreads) s_b1[i] = prm.b1[(uint64_t)head * kTcK + i];
+        }
+    };
+    auto issue_g1 = [&](uint64_t t) {  // thread 0 only
+        if (TMA_X) mbar_wait(&s_bar[t & 1], (xph >> (t & 1)) & 1u);
+        fence_after();
+        gemm_k128(tD1, smem_u32(sX(t)), smem_u32(sW1), N1);
+        umma_commit(&s_bar[2]);
+    };
+    for (uint64_t t = t0; t < t1; ++t) {
+        if (!g1_issued) {
+            if (pc.head != cur_head) {  // all earlier MMAs are complete here
+                load_weights(pc.head);
+                cur_head = pc.head;
             }
             fence_async_smem();
             fence_before();
             __syncthreads();
-            // ---- GEMM2
+            if (tid == 0) issue_g1(t);
+        }
+        xph ^= 1u << (t & 1);
+        // ---- GEMM1(t) done: its X slot is free for tile t + 2
+        mbar_wait(&s_bar[2], g1ph);
+        g1ph ^= 1u;
+        fence_after();
+        if (t + 2 < t1) stage(t + 2, pnn);
+        uint32_t tZ = tD1;
+        // GEMM1(t + 1) runs under epilogue 2 of tile t when its weights (head)
+        // are already loaded and D1 is not the final accumulator (MLP)
+        const bool early = !prm.linear && t + 1 < t1 && pn.head == pc.head;
+        if (!prm.linear) {
+            // ---- epilogue 1: +b1, SiLU -> bf16 A1 (columns [64 half, +64))
+#pragma unroll
+            for (uint32_t cc = 0; cc < 64; cc += 32) {
+                const uint32_t c0 = half * 64 + cc;
+                uint32_t r[2][16];
+                tmem_ld16_nowait(tD1 + lane_addr + c0, r[0]);
+                tmem_ld16_nowait(tD1 + lane_addr + c0 + 16, r[1]);
+                tmem_wait_ld();
+#pragma unroll
+                for (uint32_t q = 0; q < 2; ++q) {
+                    uint32_t p[8];
+#pragma unroll
+                    for (int i = 0; i < 16; i += 2)
+                        p[i / 2] = pack_bf16(silu_fast(__uint_as_float(r[q][i]) + s_b1[c0 + 16 * q + i]),
+                                             silu_fast(__uint_as_float(r[q][i + 1]) + s_b1[c0 + 16 * q + i + 1]));
+                    *reinterpret_cast<uint4*>(sA1 + tc_sw_off(row, c0 + 16 * q, kTcTileM)) =
+                        make_uint4(p[0], p[1], p[2], p[3]);
+                    *reinterpret_cast<uint4*>(sA1 + tc_sw_off(row, c0 + 16 * q + 8, kTcTileM)) =
+                        make_uint4(p[4], p[5], p[6], p[7]);
+                }
+            }
+            fence_async_smem();
+            fence_before();
+            __syncthreads();
+            // ---- GEMM2(t), then GEMM1(t + 1) (D1 has been drained)
             if (tid == 0) {
                 fence_after();
                 gemm_k128(tD2, smem_u32(sA1), smem_u32(sW2), L);
-                umma_commit(&s_bar[1]);
+                umma_commit(&s_bar[3]);
+                if (early) issue_g1(t + 1);
             }
             tZ = tD2;
-        }
-        // sX is free (GEMM1 has completed): stage the next tile's keys while
-        // GEMM2 runs
-        if (t + 1 < t1) {
-            const uint64_t nbh = (t + 1) / prm.tiles_per_problem;
-            stage_x(prm, nbh, (uint32_t)((t + 1) % prm.tiles_per_problem) * kTcTileM, sX);
-        }
-        if (!prm.linear) {
-            mbar_wait(&s_bar[1], phase);
+            mbar_wait(&s_bar[3], g2ph);
+            g2ph ^= 1u;
             fence_after();
         }
-        // ---- epilogue 2: sign bits of columns [half L/2, +L/2) -> partial words
-        uint32_t wd[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-        const uint32_t grow = row0 + row;
-#pragma unroll 1
-        for (uint32_t c0 = half * (L / 2); c0 < (half + 1) * (L / 2); c0 += 16) {
-            float v[16];
-            tmem_ld16(tZ + lane_addr + c0, v);
+        g1_issued = early;
+        // ---- epilogue 2: this half's columns -> negative flags -> code words
+        uint32_t neg[W];
 #pragma unroll
-            for (int i = 0; i < 16; ++i) {
-                const uint32_t j = c0 + i;  // W divides 16: word j % W = i % W
-                const uint32_t bit = v[i] >= 0.0f ? 1u : 0u;
-                if (W == 1) wd[0] |= bit << (31 - j);
-                else if (W == 2) wd[i & 1] |= bit << (31 - (j >> 1));
-                else if (W == 4) wd[i & 3] |= bit << (31 - (j >> 2));
-                else wd[i & 7] |= bit << (31 - (j >> 3));
+        for (uint32_t w = 0; w < W; ++w) neg[w] = 0u;
+        float sum = 0.0f;
+        if (half == 0) sign_half<W, 0>(tZ + lane_addr, neg, sum);
+        else sign_half<W, 1>(tZ + lane_addr, neg, sum);
+        const uint32_t grow = pc.mb * kTcTileM + row;
+        if (TMA_X && !isfinite(sum) && grow < prm.m) raise_dev_err(prm.dev_err, SPL_DEV_ERR_NUMERIC);
+        if (prm.pre) {  // tests: the f32 pre-activations of this half (tcgen05.ld
+                        // is warp-collective: load on every lane, store if valid)
+            float* dst = prm.pre + ((pc.bh * prm.m) + grow) * L + half * (L / 2);
+            for (uint32_t c = 0; c < L / 2; c += 16) {
+                uint32_t r[16];
+                tmem_ld16_nowait(tZ + lane_addr + half * (L / 2) + c, r);
+                tmem_wait_ld();
+                if (grow < prm.m)
+                    for (int i = 0; i < 16; ++i) dst[c + i] = __uint_as_float(r[i]);
             }
-            if (prm.pre && grow < prm.m)
-                for (int i = 0; i < 16; ++i) prm.pre[((bh * prm.m) + grow) * L + c0 + i] = v[i];
         }
-        if (half == 1)
-            for (uint32_t w = 0; w < W; ++w) s_code[row * 8 + w] = wd[w];
+        if (half == 1) {
+#pragma unroll
+            for (uint32_t w = 0; w < W; ++w) s_code[row * 8 + w] = neg[w];
+        }
         fence_before();
         __syncthreads();
         if (half == 0 && grow < prm.m) {
-            uint32_t* dst = prm.codes + ((bh * prm.m) + grow) * W;
-            if (W == 4) {
-                *reinterpret_cast<uint4*>(dst) =
-                    make_uint4(wd[0] | s_code[row * 8 + 0], wd[1] | s_code[row * 8 + 1],
-                               wd[2] | s_code[row * 8 + 2], wd[3] | s_code[row * 8 + 3]);
+            uint32_t wd[W];
+#pragma unroll
+            for (uint32_t w = 0; w < W; ++w) wd[w] = ~(neg[w] | s_code[row * 8 + w]);
+            uint32_t* dst = prm.codes + ((pc.bh * prm.m) + grow) * W;
+            if constexpr (W >= 4) {
+#pragma unroll
+                for (uint32_t w = 0; w < W; w += 4)
+                    *reinterpret_cast<uint4*>(dst + w) = make_uint4(wd[w], wd[w + 1], wd[w + 2], wd[w + 3]);
             } else {
-                for (uint32_t w = 0; w < W; ++w) dst[w] = wd[w] | s_code[row * 8 + w];
+#pragma unroll
+                for (uint32_t w = 0; w < W; ++w) dst[w] = wd[w];
             }
         }
-        phase ^= 1u;
+        pc = pn;
+        pn = pnn;
+        pnn = next(pnn);
     }
     fence_before();
     __syncthreads();
     fence_after();
     if (warp == 0)
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
+}
+
+template <bool TMA_X>
+const void* k2_fn(uint32_t W) {
+    switch (W) {
+        case 1: return reinterpret_cast<const void*>(&k2_encode_tc<TMA_X, 1>);
+        case 2: return reinterpret_cast<const void*>(&k2_encode_tc<TMA_X, 2>);
+        case 4: return reinterpret_cast<const void*>(&k2_encode_tc<TMA_X, 4>);
+        default: return reinterpret_cast<const void*>(&k2_encode_tc<TMA_X, 8>);
+    }
 }
 
 }  // namespace
@@ -338,12 +455,40 @@ spl_status encode_tc_launch(spl_ctx* ctx, const spl_hasher* hs, const void* x, i
     prm.total_tiles = (uint64_t)B * hs->H * prm.tiles_per_problem;
     prm.dev_err = ctx->dev_err;
     const uint32_t N1 = prm.linear ? prm.L : kTcK;
-    const size_t smem = 1024 + 2 * (size_t)tc_operand_bytes(kTcTileM) + tc_operand_bytes(N1) +
+    const size_t smem = 1024 + 3 * (size_t)tc_operand_bytes(kTcTileM) + tc_operand_bytes(N1) +
                         (prm.linear ? 0 : tc_operand_bytes(prm.L)) + kTcTileM * 8 * 4;
-    SPL_CUDA_TRY(ctx, cudaFuncSetAttribute(k2_encode_tc, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           (int)smem));
     const uint64_t G = std::min<uint64_t>(prm.total_tiles, (uint64_t)ctx->num_sms);
-    k2_encode_tc<<<(uint32_t)G, kTcThreads, smem, s>>>(prm);
+    CUtensorMap tmap;
+    std::memset(&tmap, 0, sizeof(tmap));
+    if (prm.x_bf16) {
+        // [B*H*m rows][128] bf16, box 64 x 128 (one K block of one tile),
+        // 128-byte swizzle; rows past the end are zero-filled
+        static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+        if (!encode) {
+            void* fn = nullptr;
+            cudaDriverEntryPointQueryResult q;
+            if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) !=
+                    cudaSuccess ||
+                q != cudaDriverEntryPointSuccess || !fn)
+                return fail(ctx, SPL_E_CUDA, "encode: cuTensorMapEncodeTiled unavailable");
+            encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+        }
+        const cuuint64_t dims[2] = {kTcK, (cuuint64_t)B * hs->H * m};
+        const cuuint64_t strides[1] = {kTcK * 2};
+        const cuuint32_t box[2] = {64, kTcTileM};
+        const cuuint32_t estr[2] = {1, 1};
+        if (reinterpret_cast<uintptr_t>(x) % 16 != 0)
+            return fail(ctx, SPL_E_DIMENSION, "encode: bf16 input must be 16-byte aligned");
+        const CUresult r = encode(&tmap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(x),
+                                  dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                  CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) return fail(ctx, SPL_E_CUDA, "encode: cuTensorMapEncodeTiled failed");
+    }
+    const void* fn = prm.x_bf16 ? k2_fn<true>(prm.W) : k2_fn<false>(prm.W);
+    SPL_CUDA_TRY(ctx, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    void* args[] = {&tmap, &prm};
+    SPL_CUDA_TRY(ctx, cudaLaunchKernel(fn, dim3((uint32_t)G), dim3(kTcThreads), args, smem, s));
     return after_launch(ctx, "k2_encode_tc");
 }
 

@@ -151,3 +151,16 @@ def test_encode_tc_non_finite_raises(ctx):
     torch.cuda.synchronize()
     with pytest.raises(capi.NumericError):
         ctx.check_device_error()
+
+
+def test_encode_tc_non_finite_bf16_raises(ctx):
+    rng = np.random.default_rng(7)
+    w1, b1, w2 = mlp_weights(rng, 1, 128, 128, 128)
+    hs = ctx.hasher(w1, b1, w2)
+    x = torch.zeros((1, 1, 130, 128), dtype=torch.bfloat16, device=DEV)
+    x[0, 0, 3, 5] = float("nan")
+    codes = torch.zeros((1, 1, 130, 4), dtype=torch.int32, device=DEV)
+    hs.encode_tc(x, capi.SPL_BF16, 1, 130, codes)
+    torch.cuda.synchronize()
+    with pytest.raises(capi.NumericError):
+        ctx.check_device_error()
