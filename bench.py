@@ -304,6 +304,7 @@ def main():
     rng = np.random.default_rng(7)
     e2e = None
     decode = None
+    decode4 = None
     prefill = None
     if world == 1:
         w1 = (rng.standard_normal((H, D, D)) / np.sqrt(D)).astype(np.float32)
@@ -336,6 +337,8 @@ def main():
             decode = bench_decode(torch, capi, ctx, dev, stream, args, hasher)
         if not args.no_prefill:
             prefill = bench_prefill(torch, capi, ctx, dev, stream, args)
+        if not args.no_decode:
+            decode4 = bench_decode4(torch, capi, ctx, dev, stream, args)
     clk = clocks.stop()
 
     # CPU baseline (rank 0, N = 1): the reference on this host's cores
@@ -397,6 +400,8 @@ def main():
         line["sparse_decode"] = decode
     if prefill:
         line["prefill_encode"] = prefill
+    if decode4:
+        line["batched_decode"] = decode4
     if rank == 0:
         print(json.dumps(line), flush=True)
     ctx.close()
@@ -449,6 +454,66 @@ def bench_prefill(torch, capi, ctx, dev, stream, args):
                                     "flops": flops},
                          "hbm": {"achieved": round(gbs, 1), "unit": "GB/s", "peak": hbm,
                                  "frac": round(gbs / hbm, 4), "algorithmic_bytes": nbytes}}}
+
+
+def bench_decode4(torch, capi, ctx, dev, stream, args):
+    """Config 4: B=16 sequences x 32 heads, 131072-token bf16 K/V caches,
+    256-bit codes, k = 2% = 2621: one batched decode step (append each new
+    key + value and its code, encode the queries, retrieve, sparse attend)."""
+    B, n, L4 = 16, 131072, 256
+    k = budget(n)
+    P = B * H
+    W4 = L4 // 32
+    cap = n
+    rng = np.random.default_rng(40)
+    w1 = (rng.standard_normal((H, D, D)) / np.sqrt(D)).astype(np.float32)
+    b1 = np.zeros((H, D), np.float32)
+    w2 = (rng.standard_normal((H, D, L4)) / np.sqrt(D)).astype(np.float32)
+    hs = ctx.hasher(w1, b1, w2)
+    codes = random_codes(torch, P, cap, W4, seed=56, dev=dev)
+    g = torch.Generator(device=dev)
+    g.manual_seed(6)
+    kc = torch.empty((B, H, cap, D), device=dev, dtype=torch.bfloat16)
+    vc = torch.empty((B, H, cap, D), device=dev, dtype=torch.bfloat16)
+    for b in range(B):
+        kc[b].copy_(torch.randn((H, cap, D), generator=g, device=dev))
+        vc[b].copy_(torch.randn((H, cap, D), generator=g, device=dev))
+    q = torch.randn((B, H, D), generator=g, device=dev)
+    kn = torch.randn((B, H, D), generator=g, device=dev)
+    vn = torch.randn((B, H, D), generator=g, device=dev)
+    nvalid = torch.full((B,), n, dtype=torch.int32, device=dev)
+    idx = torch.zeros((P, k), dtype=torch.int32, device=dev)
+    cnt = torch.zeros(P, dtype=torch.int32, device=dev)
+    out = torch.zeros((B, H, D), dtype=torch.float32, device=dev)
+    scale = float(1 / np.sqrt(D))
+
+    def step():
+        hs.decode_step(q, kn, vn, B, codes, kc, vc, capi.SPL_BF16, cap, nvalid, n, k, scale,
+                       idx, cnt, out, stream)
+
+    for _ in range(args.warmup):
+        step()
+    steps = min(args.steps, 20)
+    l0 = ctx.launches()
+    ms = event_timer(torch, step, steps, stream)
+    launches = (ctx.launches() - l0) / steps
+
+    qz = torch.randint(-2**31, 2**31 - 1, (P, W4), generator=g, device=dev, dtype=torch.int32)
+
+    def retr():
+        ctx.hamming_topk(codes, cap, L4, qz, P, nvalid, H, n, k, idx, cnt, stream)
+    r_ms = event_timer(torch, retr, steps, stream)
+    hbm, _ = peaks()
+    alg = P * n * W4 * 4 + P * (k + 1) * D * 2 * 2 + H * (D * D + D + D * L4) * 4 + P * k * 4
+    del kc, vc, codes
+    return {"workload": "config4: B=16 x 32 heads, 131072-token bf16 K/V caches, 256-bit codes, "
+                        "k=2621; append + encode + retrieve + attend",
+            "us_per_step": round(ms * 1000, 2), "tok_per_s": round(B / (ms * 1e-3), 1),
+            "unit": "tok/s (one 32-head layer, 16 sequences)", "gpu_launches_per_step": launches,
+            "retrieval_us": round(r_ms * 1000, 2),
+            "roofline": {"bound": "hbm", "algorithmic_bytes": alg,
+                         "achieved": round(alg / (ms * 1e-3) / 1e9, 1), "peak": hbm,
+                         "frac": round(alg / (ms * 1e-3) / 1e9 / hbm, 4)}}
 
 
 def bench_decode(torch, capi, ctx, dev, stream, args, hasher_c3):
