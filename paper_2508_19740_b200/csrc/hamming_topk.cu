@@ -591,6 +591,10 @@ __device__ void select_rows_t8(const uint8_t* sc, uint64_t a0, uint64_t r0, uint
         }
         uint64_t tot;
         const uint64_t ex = block_excl_scan_u64(((uint64_t)eq << 32) | gt, s_warp, tot);
+#if defined(K3_SEL_EXP) && K3_SEL_EXP == 2
+        if (ex == 0x123456789ull) out[0] = gm[0] ^ em[NV - 1];
+        return;
+#endif
         if (gt | eq) {
             const uint32_t eq_before = carry_eq + (uint32_t)(ex >> 32);
             uint32_t pos = carry_gt + (uint32_t)ex + (eq_before < take ? eq_before : take);
@@ -604,7 +608,12 @@ __device__ void select_rows_t8(const uint8_t* sc, uint64_t a0, uint64_t r0, uint
                     while (m) {
                         const uint32_t b = __ffs(m) - 1;
                         m &= m - 1;
+#if defined(K3_SEL_EXP) && K3_SEL_EXP == 1
+                        if (b == 77) out[pos] = at;
+                        pos++;
+#else
                         out[pos++] = at + 4 * (b >> 3) + (b & 7);
+#endif
                     }
                 }
             } else {  // the thread where the tie quota runs out

@@ -312,6 +312,21 @@ int main() {
         timeit("tiles KB8 CPP9 (288)", [&] { rd_tiles<8><<<32 * 9, 256>>>(a, 32, 9, upp, o); });
         timeit("tiles KB4 CPP13 (416)", [&] { rd_tiles<4><<<32 * 13, 256>>>(a, 32, 13, upp, o); });
         timeit("tiles KB2 CPP13 (416)", [&] { rd_tiles<2><<<32 * 13, 256>>>(a, 32, 13, upp, o); });
+        for (int kb : {0, 58}) {
+            cudaFuncSetAttribute(rd_tiles<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kb * 1024);
+            cudaFuncSetAttribute(rd_tiles<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, kb * 1024);
+            char n[64];
+            snprintf(n, 64, "tiles KB2 CPP13 (416) smem%dK", kb);
+            timeit(n, [&] { rd_tiles<2><<<32 * 13, 256, kb * 1024>>>(a, 32, 13, upp, o); });
+            snprintf(n, 64, "tiles KB4 CPP13 (416) smem%dK", kb);
+            timeit(n, [&] { rd_tiles<4><<<32 * 13, 256, kb * 1024>>>(a, 32, 13, upp, o); });
+            cudaFuncSetAttribute(rd_ldg_chunk<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kb * 1024);
+            snprintf(n, 64, "chunk U2 grid=416 smem%dK", kb);
+            timeit(n, [&] { rd_ldg_chunk<2><<<416, 256, kb * 1024>>>(a, units, o); });
+            cudaFuncSetAttribute(rd_ldg<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kb * 1024);
+            snprintf(n, 64, "ldg256 U2 grid=416 smem%dK", kb);
+            timeit(n, [&] { rd_ldg<2><<<416, 256, kb * 1024>>>(a, units, o); });
+        }
         timeit("chunk U4 grid=288", [&] { rd_ldg_chunk<4><<<288, 256>>>(a, units, o); });
         timeit("ldg256 U4 grid=288", [&] { rd_ldg<4><<<288, 256>>>(a, units, o); });
     }
