@@ -87,7 +87,7 @@ spl_status spl_reserve(spl_ctx* ctx, uint32_t P, uint64_t n_max, uint32_t L, uin
     if (!ctx) return SPL_E_STATE;
     // Run each path once on a dummy problem set sized like the real one is
     // not possible without data; size the buffers from the same formulas.
-    const size_t score_bytes = L <= 255 ? 1 : 2;
+    const size_t score_bytes = L <= 256 ? 1 : 2;
     const size_t n_pad = (n_max + 63) / 64 * 64;
     const size_t G = (size_t)ctx->num_sms * 8 + 1;
     const size_t sc = ((size_t)P * n_pad * score_bytes + 255) / 256 * 256;

@@ -84,6 +84,7 @@ struct K3Params {
     uint64_t* trace;       // optional [G][8] globaltimer stamps (SPL_K3_TRACE)
     uint32_t hist_lo;      // fused: private counters cover scores [hist_lo, L] only
     uint32_t* counters2;   // fused: [P] low-bin fallback completion
+    int clamp8;            // two-pass L = 256: u8 scores hold min(score, 255)
 };
 
 constexpr int kThreads = 256;
@@ -92,6 +93,9 @@ constexpr int kThreads = 256;
 // 6.2 to 5.2 TB/s on this B200 (tools/read_bw.cu "sweep": the slowdown is a
 // step at the carve-out switch, not a function of the smem size).
 constexpr size_t kFastCarveBytes = 196 * 1024;
+// two-pass scan segments per CTA: 1 measured best at config 4 (each segment
+// boundary costs a pipeline drain + flush; 2/4/8 per CTA: +1/+4/+11%)
+constexpr uint64_t kSegsPerCta = 1;
 #ifndef K3_EXP
 #define K3_EXP 0  // timing experiments only (tools/k3_exp.sh); 0 = product
 #endif
@@ -166,6 +170,12 @@ __device__ void problem_threshold(const uint32_t* tot, uint32_t L, uint32_t kk, 
     __syncthreads();
 }
 
+// plan.w = 1: the stored u8 scores cannot decide this threshold (clamped
+// L = 256 scores and T >= 255), k3_select recomputes them from the codes.
+__device__ __forceinline__ uint32_t exact_flag(const K3Params& prm, uint32_t T) {
+    return (prm.clamp8 && T != SPL_PLAN_SKIP && T >= 255u) ? 1u : 0u;
+}
+
 // Two-pass: plan every segment of problem p given (T, quota).
 __device__ void plan_segments(const K3Params& prm, uint32_t p, uint32_t T, uint32_t quota,
                               uint64_t* s_warp) {
@@ -189,6 +199,39 @@ __device__ void plan_segments(const K3Params& prm, uint32_t p, uint32_t T, uint3
             const uint64_t left = quota > eq_before ? quota - eq_before : 0;
             const uint32_t take = (uint32_t)(eq < left ? eq : left);
             const uint32_t off = (uint32_t)(gt_before + (eq_before < quota ? eq_before : quota));
+            prm.plans[c + p] = make_uint4(T, off, take, exact_flag(prm, T));
+        }
+        carry_gt += tot & 0xffffffffu;
+        carry_eq += tot >> 32;
+    }
+}
+
+// Two-pass low-threshold fallback: plan the segments of problem p by
+// counting score > T / == T over each segment's stored scores (T < 255).
+template <typename ScoreT>
+__device__ void plan_segments_recount(const K3Params& prm, uint32_t p, uint32_t nv, uint32_t T,
+                                      uint32_t quota, uint64_t* s_warp) {
+    const K3Geom& g = prm.g;
+    const ScoreT* srow = reinterpret_cast<const ScoreT*>(prm.scores) + (uint64_t)p * g.n_pad;
+    const uint64_t pbase = (uint64_t)p * g.pstride;
+    uint64_t carry_gt = 0, carry_eq = 0;
+    for (uint32_t c = seg_first(g, p); c <= seg_last(g, p); ++c) {
+        const uint64_t lo_r = max((uint64_t)c * g.S, pbase) - pbase;
+        const uint64_t hi_r = min(min(((uint64_t)c + 1) * g.S, pbase + g.pstride) - pbase, (uint64_t)nv);
+        uint32_t gt = 0, eq = 0;
+        if (T != SPL_PLAN_SKIP)
+            for (uint64_t r = lo_r + threadIdx.x; r < hi_r; r += kThreads) {
+                const uint32_t v = srow[r];
+                gt += v > T;
+                eq += v == T;
+            }
+        uint64_t tot;
+        block_excl_scan_u64(((uint64_t)eq << 32) | gt, s_warp, tot);
+        if (threadIdx.x == 0) {
+            const uint64_t eeq = tot >> 32;
+            const uint64_t left = quota > carry_eq ? quota - carry_eq : 0;
+            const uint32_t take = (uint32_t)(eeq < left ? eeq : left);
+            const uint32_t off = (uint32_t)(carry_gt + (carry_eq < quota ? carry_eq : quota));
             prm.plans[c + p] = make_uint4(T, off, take, 0u);
         }
         carry_gt += tot & 0xffffffffu;
@@ -304,6 +347,7 @@ __device__ void stream_piece(const uint32_t* base, const uint32_t* qp, uint32_t 
     const int tid = threadIdx.x;
     if constexpr (W > 0) {
         constexpr int R = 8 / W;  // rows per 32-byte unit
+        constexpr bool kClamp = sizeof(ScoreT) == 1 && W == 8;
         uint32_t q[W];
 #pragma unroll
         for (int w = 0; w < W; ++w) q[w] = __ldg(qp + w);
@@ -316,10 +360,11 @@ __device__ void stream_piece(const uint32_t* base, const uint32_t* qp, uint32_t 
             if ((uint32_t)tid < nhead + ntail) {
                 const uint64_t row = (uint32_t)tid < nhead ? r0 + tid : tail_beg + (tid - nhead);
                 const uint32_t sc = row_score<W>(base + row * W, q, L);
+                const uint32_t sv = kClamp ? min(sc, 255u) : sc;
                 if constexpr (TR)
-                    dst[tpos((uint32_t)(row - dst_row0))] = (ScoreT)sc;
+                    dst[tpos((uint32_t)(row - dst_row0))] = (ScoreT)sv;
                 else
-                    dst[row - dst_row0] = (ScoreT)sc;
+                    dst[row - dst_row0] = (ScoreT)sv;
                 if (sc >= lo) count_score<PRIV>(priv, hist32, sc - lo);
             }
         }
@@ -377,6 +422,11 @@ __device__ void stream_piece(const uint32_t* base, const uint32_t* qp, uint32_t 
                 sc[r] = L - mism;
 #endif
             }
+            // u8 scores at L = 256: stored as min(score, 255) (exact for
+            // every threshold <= 254; the counters below see the true score)
+            uint32_t st[R];
+#pragma unroll
+            for (int r = 0; r < R; ++r) st[r] = kClamp ? min(sc[r], 255u) : sc[r];
             const size_t off = ((size_t)it * per_it + (size_t)j * kThreads) * R;
             if constexpr (TR) {
                 // R consecutive rows from a multiple of R (R | 16): row r of
@@ -384,11 +434,11 @@ __device__ void stream_piece(const uint32_t* base, const uint32_t* qp, uint32_t 
                 const uint32_t ad = dst0_s + tpos(jb + (uint32_t)off);
 #pragma unroll
                 for (int r = 0; r < R; ++r)
-                    asm volatile("st.shared.u8 [%0], %1;" ::"r"(ad + 4 * (r & 3) + (r >> 2)), "r"(sc[r]));
+                    asm volatile("st.shared.u8 [%0], %1;" ::"r"(ad + 4 * (r & 3) + (r >> 2)), "r"(st[r]));
             } else if constexpr (DST_SMEM) {
                 uint32_t v = 0;
 #pragma unroll
-                for (int r = 0; r < R; ++r) v |= sc[r] << (r * 8 * sizeof(ScoreT));
+                for (int r = 0; r < R; ++r) v |= st[r] << (r * 8 * sizeof(ScoreT));
                 const uint32_t ad = dst_s + (uint32_t)(off * sizeof(ScoreT));
                 if constexpr (sizeof(ScoreT) * R == 1)
                     asm volatile("st.shared.u8 [%0], %1;" ::"r"(ad), "r"(v));
@@ -397,9 +447,9 @@ __device__ void stream_piece(const uint32_t* base, const uint32_t* qp, uint32_t 
                 else if constexpr (sizeof(ScoreT) * R == 4)
                     asm volatile("st.shared.u32 [%0], %1;" ::"r"(ad), "r"(v));
                 else
-                    store_scores<ScoreT, R>(udst + off, sc);
+                    store_scores<ScoreT, R>(udst + off, st);
             } else {
-                store_scores<ScoreT, R>(udst + off, sc);
+                store_scores<ScoreT, R>(udst + off, st);
             }
 #if K3_EXP == 0
 #pragma unroll
@@ -436,7 +486,7 @@ __device__ void stream_piece(const uint32_t* base, const uint32_t* qp, uint32_t 
                 uint32_t mism = 0;
                 for (uint32_t w = 0; w < Wr; ++w) mism += __popc(__ldg(row + w) ^ __ldg(qp + w));
                 const uint32_t s = L - mism;
-                dst[r - dst_row0] = (ScoreT)s;
+                dst[r - dst_row0] = (ScoreT)(sizeof(ScoreT) == 1 ? min(s, 255u) : s);
                 if (s >= lo) count_score<PRIV>(priv, hist32, s - lo);
             }
             if (PRIV && ++steps == 255) {
@@ -467,12 +517,17 @@ __device__ __forceinline__ void word_flags(uint32_t w, uint32_t Tw, uint32_t& gt
 // Ordered compaction of rows [r0, r1) whose scores sit at sc[row - a0]
 // (a0 = r0 rounded down to 16 rows; sc 16-byte aligned): keep score > T and
 // the first `take` score == T rows, writing ascending row ids to out[0..).
+// Each thread owns NG consecutive groups of 64 rows per round, all loads of
+// a round issued before any is used (GLOBAL: the two-pass k3_select reads
+// L2/DRAM, so a round is one memory latency; NG = 4 cuts the rounds of a
+// 150 K-row segment from 10 to 3).
 template <typename ScoreT, bool GLOBAL>
 __device__ void select_rows(const ScoreT* sc, uint64_t a0, uint64_t r0, uint64_t r1, uint32_t T,
                             uint32_t take, uint32_t* out, uint64_t* s_warp) {
     constexpr int PER = 16 / sizeof(ScoreT);  // scores per 16-byte vector
-    constexpr int NV = 4;
-    constexpr int CH = PER * NV;              // <= 64 rows per thread per round
+    constexpr int NVG = 64 / PER;             // vectors per 64-row group
+    constexpr int NG = 1;  // groups per thread per round (4: k3_select 43 -> 48 us at config 4)
+    constexpr int CH = 64 * NG;               // rows per thread per round
     constexpr int SPW = 4 / sizeof(ScoreT);   // scores per word
     const uint32_t Tw = sizeof(ScoreT) == 1 ? T * 0x01010101u : T * 0x00010001u;
     const int tid = threadIdx.x;
@@ -480,48 +535,63 @@ __device__ void select_rows(const ScoreT* sc, uint64_t a0, uint64_t r0, uint64_t
     uint64_t carry_gt = 0, carry_eq = 0;
     for (uint64_t base = a0; base < r1; base += round_rows) {
         const uint64_t my = base + (uint64_t)tid * CH;
-        uint64_t gtm = 0, eqm = 0;
-        if (my < r1) {
+        uint4 x[NG * NVG];
 #pragma unroll
-            for (int v = 0; v < NV; ++v) {
-                const uint64_t at = my + (uint64_t)v * PER;
-                uint4 x = make_uint4(0, 0, 0, 0);
-                if (at < r1) {
-                    const uint4* ptr = reinterpret_cast<const uint4*>(sc + (at - a0));
-                    x = GLOBAL ? __ldcg(ptr) : *ptr;
-                }
-                const uint32_t ws[4] = {x.x, x.y, x.z, x.w};
+        for (int v = 0; v < NG * NVG; ++v) {
+            const uint64_t at = my + (uint64_t)v * PER;
+            x[v] = make_uint4(0, 0, 0, 0);
+            if (at < r1) {
+                const uint4* ptr = reinterpret_cast<const uint4*>(sc + (at - a0));
+                x[v] = GLOBAL ? __ldcg(ptr) : *ptr;
+            }
+        }
+        uint64_t gtm[NG], eqm[NG];
+        uint32_t gt = 0, eq = 0;
+#pragma unroll
+        for (int gi = 0; gi < NG; ++gi) {
+            gtm[gi] = 0;
+            eqm[gi] = 0;
+#pragma unroll
+            for (int v = 0; v < NVG; ++v) {
+                const uint4 xv = x[gi * NVG + v];
+                const uint32_t ws[4] = {xv.x, xv.y, xv.z, xv.w};
 #pragma unroll
                 for (int i = 0; i < 4; ++i) {
                     uint32_t g, e;
                     word_flags<ScoreT>(ws[i], Tw, g, e);
-                    gtm |= (uint64_t)g << (v * PER + i * SPW);
-                    eqm |= (uint64_t)e << (v * PER + i * SPW);
+                    gtm[gi] |= (uint64_t)g << (v * PER + i * SPW);
+                    eqm[gi] |= (uint64_t)e << (v * PER + i * SPW);
                 }
             }
             // rows outside [r0, r1)
-            const uint64_t lo = r0 > my ? r0 - my : 0;
-            const uint64_t hi = r1 - my < (uint64_t)CH ? r1 - my : (uint64_t)CH;
+            const uint64_t g0 = my + 64 * gi;
+            const uint64_t lo = r0 > g0 ? r0 - g0 : 0;
+            const uint64_t hi = r1 > g0 ? (r1 - g0 < 64 ? r1 - g0 : 64) : 0;
             uint64_t valid = hi >= 64 ? ~0ull : ((1ull << hi) - 1);
             valid &= lo >= 64 ? 0ull : ~((1ull << lo) - 1);
-            gtm &= valid;
-            eqm &= valid;
+            gtm[gi] &= valid;
+            eqm[gi] &= valid;
+            gt += __popcll(gtm[gi]);
+            eq += __popcll(eqm[gi]);
         }
-        const uint32_t gt = __popcll(gtm), eq = __popcll(eqm);
         uint64_t tot;
         const uint64_t ex = block_excl_scan_u64(((uint64_t)eq << 32) | gt, s_warp, tot);
-        uint64_t m = gtm | eqm;
-        if (m) {
+        if (gt | eq) {
             uint64_t eq_before = carry_eq + (ex >> 32);
             uint64_t pos = carry_gt + (ex & 0xffffffffu) + (eq_before < take ? eq_before : take);
-            while (m) {
-                const int i = __ffsll((long long)m) - 1;
-                m &= m - 1;
-                if ((gtm >> i) & 1u) {
-                    out[pos++] = (uint32_t)(my + i);
-                } else {
-                    if (eq_before < take) out[pos++] = (uint32_t)(my + i);
-                    ++eq_before;
+#pragma unroll
+            for (int gi = 0; gi < NG; ++gi) {
+                uint64_t m = gtm[gi] | eqm[gi];
+                const uint32_t rowb = (uint32_t)(my + 64 * gi);
+                while (m) {
+                    const int i = __ffsll((long long)m) - 1;
+                    m &= m - 1;
+                    if ((gtm[gi] >> i) & 1u) {
+                        out[pos++] = rowb + i;
+                    } else {
+                        if (eq_before < take) out[pos++] = rowb + i;
+                        ++eq_before;
+                    }
                 }
             }
         }
@@ -667,29 +737,63 @@ __device__ void wait_count(const uint32_t* p, uint32_t need, uint32_t* dev_err) 
     }
 }
 
+// Ordered compaction with scores recomputed from the codes (plan.w = 1: the
+// stored u8 scores are clamped and T >= 255). Same contract as select_rows.
+__device__ void select_rows_exact(const K3Params& prm, uint32_t p, uint64_t r0, uint64_t r1,
+                                  uint32_t T, uint32_t take, uint32_t* out, uint64_t* s_warp) {
+    const uint32_t W = prm.W;
+    const uint32_t* q = prm.qcodes + (uint64_t)p * W;
+    const uint32_t* base = prm.codes + (uint64_t)p * prm.stride_rows * W;
+    uint64_t carry_gt = 0, carry_eq = 0;
+    for (uint64_t b = r0; b < r1; b += kThreads) {
+        const uint64_t r = b + threadIdx.x;
+        uint32_t gt = 0, eq = 0;
+        if (r < r1) {
+            uint32_t mism = 0;
+            for (uint32_t w = 0; w < W; ++w) mism += __popc(__ldg(base + r * W + w) ^ __ldg(q + w));
+            const uint32_t sc = prm.L - mism;
+            gt = sc > T;
+            eq = sc == T;
+        }
+        uint64_t tot;
+        const uint64_t ex = block_excl_scan_u64(((uint64_t)eq << 32) | gt, s_warp, tot);
+        const uint64_t eq_before = carry_eq + (ex >> 32);
+        const uint64_t pos = carry_gt + (ex & 0xffffffffu) + (eq_before < take ? eq_before : take);
+        if (gt || (eq && eq_before < take)) out[pos] = (uint32_t)r;
+        carry_gt += tot & 0xffffffffu;
+        carry_eq += tot >> 32;
+    }
+}
+
+// Two-pass scan: CTAs walk the segments grid-stride (segment = S rows of the
+// virtual row space; several per CTA, so all CTAs sweep the problems in order
+// and problems complete progressively); per segment: stream, private counts
+// -> record + problem histogram; the CTA completing a problem plans it.
 template <int W, typename ScoreT, bool PRIV>
-__global__ void __launch_bounds__(kThreads) k3_scan(K3Params prm) {
+__global__ void __launch_bounds__(kThreads, 3) k3_scan(K3Params prm) {
     extern __shared__ __align__(16) uint8_t smem[];
     __shared__ uint64_t s_warp[kThreads / 32 + 1];
     __shared__ uint32_t s_flag, s_T;
     const uint32_t L = prm.L;
     const uint32_t bins = L + 1;
+    const uint32_t hlo = prm.hist_lo;  // counted window [hlo, L] (0: every bin)
+    const uint32_t wbins = bins - hlo;
     const uint32_t Wr = (W > 0) ? (uint32_t)W : prm.W;
-    const size_t priv_bytes = PRIV ? (((size_t)bins * kThreads + 15) & ~size_t(15)) : 0;
+    const size_t priv_bytes = PRIV ? (((size_t)wbins * kThreads + 15) & ~size_t(15)) : 0;
     uint8_t* priv = smem;
     uint32_t* hist32 = reinterpret_cast<uint32_t*>(smem + priv_bytes);  // [bins + 1]
     const int tid = threadIdx.x;
     const K3Geom& g = prm.g;
-
-    const uint64_t g0 = (uint64_t)blockIdx.x * g.S;
-    const uint64_t g1 = min(g0 + g.S, g.total);
-    const uint32_t p_first = (uint32_t)(g0 / g.pstride);
 
     // zero the counters once (flush_priv re-zeroes them)
     if constexpr (PRIV)
         for (uint32_t i = tid; i < priv_bytes / 16; i += kThreads)
             reinterpret_cast<uint4*>(priv)[i] = make_uint4(0, 0, 0, 0);
 
+    for (uint32_t seg = blockIdx.x; seg < g.G; seg += gridDim.x) {
+    const uint64_t g0 = (uint64_t)seg * g.S;
+    const uint64_t g1 = min(g0 + g.S, g.total);
+    const uint32_t p_first = (uint32_t)(g0 / g.pstride);
     for (uint32_t p = p_first; p < g.P && (uint64_t)p * g.pstride < g1; ++p) {
         const uint64_t pbase = (uint64_t)p * g.pstride;
         const uint64_t lo = max(g0, pbase) - pbase;
@@ -707,17 +811,18 @@ __global__ void __launch_bounds__(kThreads) k3_scan(K3Params prm) {
             const uint32_t* qp = prm.qcodes + (uint64_t)p * Wr;
             const uint32_t* base = prm.codes + (uint64_t)p * prm.stride_rows * Wr;
             ScoreT* dst = reinterpret_cast<ScoreT*>(prm.scores) + (uint64_t)p * g.n_pad;
-            stream_piece<W, ScoreT, PRIV, false>(base, qp, L, r0, r1, dst, 0, priv, hist32, bins, 0u);
+            stream_piece<W, ScoreT, PRIV, false>(base, qp, L, r0, r1, dst, 0, priv, hist32 + hlo,
+                                                 wbins, hlo);
         }
         __syncthreads();
         // raw counts -> global per-problem histogram (integer atomics: the
         // sums are order-independent, so results stay deterministic)
         uint32_t* tot = prm.tot_hist + (uint64_t)p * prm.tot_stride;
-        for (uint32_t b = tid; b < bins; b += kThreads)
+        for (uint32_t b = hlo + tid; b < bins; b += kThreads)
             if (hist32[b]) atomicAdd(tot + b, hist32[b]);
         __syncthreads();
         block_suffix_sum(hist32, bins, s_warp);  // hist32[bins] stays 0
-        uint32_t* rec = prm.records + (uint64_t)(blockIdx.x + p) * (L + 2);
+        uint32_t* rec = prm.records + (uint64_t)(seg + p) * (L + 2);
         for (uint32_t t = tid; t < L + 2; t += kThreads) rec[t] = hist32[t];
 
         if (!prm.shard) {
@@ -733,9 +838,31 @@ __global__ void __launch_bounds__(kThreads) k3_scan(K3Params prm) {
                 __threadfence();
                 const uint32_t kk = prm.k < nv ? prm.k : nv;
                 uint32_t T, quota;
-                problem_threshold(tot, L, kk, hist32, s_warp, &s_T, T, quota);
+                problem_threshold(tot, L, kk, hist32, s_warp, &s_T, T, quota, hlo);
+                const bool low = kk > 0 && T == SPL_PLAN_SKIP && hlo > 0;
+                if (low) {
+                    // Fewer than kk rows scored >= lo: count the bins below
+                    // the window from the stored scores (exact below 255),
+                    // take T again and plan the segments by recounting.
+                    // Exact for any data; slow only for such problems.
+                    const ScoreT* srow = reinterpret_cast<const ScoreT*>(prm.scores) + (uint64_t)p * g.n_pad;
+                    for (uint32_t t = tid; t < hlo; t += kThreads) hist32[t] = 0u;
+                    __syncthreads();
+                    for (uint32_t r = tid; r < nv; r += kThreads) {
+                        const uint32_t v = srow[r];
+                        if (v < hlo) atomicAdd(hist32 + v, 1u);
+                    }
+                    __syncthreads();
+                    for (uint32_t t = tid; t < hlo; t += kThreads) tot[t] = hist32[t];
+                    __threadfence();
+                    __syncthreads();
+                    problem_threshold(tot, L, kk, hist32, s_warp, &s_T, T, quota);
+                }
                 for (uint32_t t = tid; t <= L; t += kThreads) tot[t] = 0u;  // self-reset
-                plan_segments(prm, p, T, quota, s_warp);
+                if (low)
+                    plan_segments_recount<ScoreT>(prm, p, nv, T, quota, s_warp);
+                else
+                    plan_segments(prm, p, T, quota, s_warp);
                 if (tid == 0) {
                     prm.cnt_out[p] = kk;
                     prm.counters[p] = 0u;
@@ -743,6 +870,7 @@ __global__ void __launch_bounds__(kThreads) k3_scan(K3Params prm) {
             }
         }
         __syncthreads();
+    }
     }
 }
 
@@ -955,7 +1083,7 @@ __global__ void __launch_bounds__(kThreads, 3) k3_fused(K3Params prm) {
 
 // ---------------------------------------------------------------- select
 template <typename ScoreT>
-__global__ void __launch_bounds__(kThreads) k3_select(K3Params prm, uint32_t* idx,
+__global__ void __launch_bounds__(kThreads, 3) k3_select(K3Params prm, uint32_t* idx,
                                                       uint64_t idx_stride) {
     __shared__ uint64_t s_warp[kThreads / 32 + 1];
     const K3Geom& g = prm.g;
@@ -970,6 +1098,11 @@ __global__ void __launch_bounds__(kThreads) k3_select(K3Params prm, uint32_t* id
         const uint64_t r0 = lo, r1 = min(hi, (uint64_t)nv);
         const uint4 plan = prm.plans[blockIdx.x + p];
         if (plan.x == SPL_PLAN_SKIP || r0 >= r1) continue;  // uniform across the block
+        if (plan.w) {
+            select_rows_exact(prm, p, r0, r1, plan.x, plan.z, idx + (uint64_t)p * idx_stride + plan.y,
+                              s_warp);
+            continue;
+        }
         const ScoreT* srow = reinterpret_cast<const ScoreT*>(prm.scores) + (uint64_t)p * g.n_pad;
         const uint64_t a0 = r0 & ~uint64_t(15);
         select_rows<ScoreT, true>(srow + a0, a0, r0, r1, plan.x, plan.z,
@@ -1031,7 +1164,9 @@ struct K3Plan {
     bool priv;
     size_t smem;
     size_t score_bytes;
-    uint32_t hist_lo;  // fused: counted score window [hist_lo, L]
+    uint32_t hist_lo;  // counted score window [hist_lo, L]
+    bool clamp8;       // two-pass u8 scores at L = 256 hold min(score, 255)
+    uint32_t grid;     // two-pass scan CTAs (<= g.G segments, grid-stride)
 };
 
 template <int W, typename ScoreT, bool PRIV>
@@ -1050,7 +1185,7 @@ const void* pick_w(uint32_t W) {
 }
 const void* pick_scan(const K3Plan& pl, uint32_t L) {
     const uint32_t W = pl.vec ? L / 32 : 0;
-    if (L <= 255) return pl.priv ? pick_w<uint8_t, true>(W) : pick_w<uint8_t, false>(W);
+    if (pl.score_bytes == 1) return pl.priv ? pick_w<uint8_t, true>(W) : pick_w<uint8_t, false>(W);
     return pl.priv ? pick_w<uint16_t, true>(W) : pick_w<uint16_t, false>(W);
 }
 
@@ -1059,29 +1194,50 @@ bool vec_ok(const void* codes, uint64_t stride_rows, uint32_t W) {
            (stride_rows * W * 4) % 32 == 0;
 }
 
+// Two-pass geometry. `single` (one-GPU retrieval, planned in-kernel):
+//  - private counters over the window [L/2, L] only when the full range
+//    would not fit 3 CTAs/SM under the fast carve-out (the planner counts
+//    the low bins from the stored scores if T < L/2, see k3_scan);
+//  - u8 scores up to L = 256, clamped to 255 at L = 256 (half the score
+//    traffic of u16; thresholds >= 255 re-read the codes, see exact_flag).
+// The sharded flow keeps full histograms (they are all-gathered) and u16
+// scores above L = 255.
 spl_status make_plan(spl_ctx* ctx, uint32_t P, uint64_t n_max, uint32_t L, const void* codes,
-                     uint64_t stride_rows, K3Plan* out) {
+                     uint64_t stride_rows, K3Plan* out, bool single = false) {
     K3Plan pl{};
     const uint32_t W = L / 32;
     pl.vec = vec_ok(codes, stride_rows, W);
-    pl.priv = (size_t)(L + 1) * kThreads <= 96 * 1024;
-    pl.score_bytes = L <= 255 ? 1 : 2;
+    pl.score_bytes = (L <= 255 || (single && L == 256)) ? 1 : 2;
+    pl.clamp8 = single && L == 256;
+    const size_t hist_b = align_up((size_t)(L + 2) * 4, 16);
+    if (single && (align_up((size_t)(L + 1) * kThreads, 16) + hist_b + 1024) * 3 > kFastCarveBytes)
+        pl.hist_lo = L / 2;
+    pl.priv = (size_t)(L + 1 - pl.hist_lo) * kThreads <= 96 * 1024;
     const uint64_t total = (uint64_t)P * n_max;
-    pl.smem = (pl.priv ? align_up((size_t)(L + 1) * kThreads, 16) : 0) + align_up((size_t)(L + 2) * 4, 16);
+    pl.smem = (pl.priv ? align_up((size_t)(L + 1 - pl.hist_lo) * kThreads, 16) : 0) + hist_b;
     const void* fn = pick_scan(pl, L);
     SPL_CUDA_TRY(ctx, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            (int)pl.smem));
+    // keep the SM's shared memory under the fast carve-out: streaming reads
+    // lose ~16% with the 228 KB one (tools/read_bw.cu "sweep")
+    SPL_CUDA_TRY(ctx, cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                           (int)(kFastCarveBytes * 100 / (228 * 1024))));
     int per_sm = 0;
     SPL_CUDA_TRY(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kThreads, pl.smem));
     if (per_sm < 1) per_sm = 1;
     const uint64_t G_target = (uint64_t)ctx->num_sms * per_sm;
-    uint64_t S = (total + G_target - 1) / G_target;
+    // kSegsPerCta segments per CTA, walked grid-stride (SPL_K3_SEGS overrides
+    // it for experiments)
+    uint64_t spc = kSegsPerCta;
+    if (const char* e = getenv("SPL_K3_SEGS")) spc = std::max(1, atoi(e));  // experiments
+    uint64_t S = (total + G_target * spc - 1) / (G_target * spc);
     S = align_up(std::max<uint64_t>(S, 1024), 256);
     pl.g.n_max = n_max;
     pl.g.pstride = n_max;
     pl.g.total = total;
     pl.g.S = S;
     pl.g.G = (uint32_t)((total + S - 1) / S);
+    pl.grid = (uint32_t)std::min<uint64_t>(pl.g.G, G_target);
     pl.g.P = P;
     pl.g.n_pad = align_up(n_max, 64);
     *out = pl;
@@ -1243,7 +1399,7 @@ spl_status validate_common(spl_ctx* ctx, const char* who, const uint32_t* codes,
 spl_status launch_scan(spl_ctx* ctx, const K3Plan& pl, const K3Params& prm, cudaStream_t s) {
     const void* fn = pick_scan(pl, prm.L);
     void* args[] = {const_cast<K3Params*>(&prm)};
-    SPL_CUDA_TRY(ctx, cudaLaunchKernel(fn, dim3(pl.g.G), dim3(kThreads), args, pl.smem, s));
+    SPL_CUDA_TRY(ctx, cudaLaunchKernel(fn, dim3(pl.grid), dim3(kThreads), args, pl.smem, s));
     return after_launch(ctx, "k3_scan");
 }
 
@@ -1369,7 +1525,7 @@ spl_status hamming_topk_impl(spl_ctx* ctx, const uint32_t* codes, uint64_t strid
         }
     }
     K3Plan pl;
-    if ((st = make_plan(ctx, P, n_max, L, codes, stride_rows, &pl))) return st;
+    if ((st = make_plan(ctx, P, n_max, L, codes, stride_rows, &pl, true))) return st;
     K3Ws ws;
     if ((st = k3_workspace(ctx, pl, L, s, &ws))) return st;
     K3Params prm = base_params(ctx, pl, ws, kst, codes, stride_rows, L, qcodes, n_valid, nvalid_div, k);
@@ -1377,6 +1533,8 @@ spl_status hamming_topk_impl(spl_ctx* ctx, const uint32_t* codes, uint64_t strid
     prm.idx_out = idx;
     prm.idx_stride = k;
     prm.shard = 0;
+    prm.hist_lo = pl.hist_lo;
+    prm.clamp8 = pl.clamp8 ? 1 : 0;
     if ((st = launch_scan(ctx, pl, prm, s))) return st;
     return launch_select(ctx, pl, prm, idx, k, s);
 }

@@ -124,6 +124,32 @@ def test_topk_low_threshold_fallback(ctx, k3_path, oracle, L):
             assert np.array_equal(got[p], want[p, :kk]), (L, k, p)
 
 
+@pytest.mark.parametrize("L", [256, 512])
+def test_topk_near_duplicates_top_bins(ctx, k3_path, oracle, L):
+    """Thresholds in the top two bins. The two-pass path stores L = 256
+    scores as u8 clamped to 255, so T >= 255 must take the exact re-read of
+    the codes: rows equal to the query (score L), rows one bit away (L - 1),
+    the rest random, with k landing on each bin and its ties."""
+    rng = np.random.default_rng(200 + L)
+    P, n, W = 3, 20000, L // 32
+    codes = rng.integers(0, 2**32, (P, n, W), dtype=np.uint64).astype(np.uint32)
+    q = rng.integers(0, 2**32, (P, W), dtype=np.uint64).astype(np.uint32)
+    for p in range(P):
+        dup = rng.choice(n, 1200, replace=False)
+        codes[p, dup[:500]] = q[p]
+        near = np.repeat(q[p][None], 700, axis=0)
+        word = rng.integers(0, W, 700)
+        near[np.arange(700), word] ^= (np.uint32(1) << rng.integers(0, 32, 700).astype(np.uint32))
+        codes[p, dup[500:]] = near
+    nv = np.array([n, n - 7, 15000], np.uint32)
+    for k in (1, 300, 500, 800, 1200, 1500):
+        got = run_topk(ctx, codes, q, nv, k)
+        want = oracle.retrieve_batch(codes, q, nv, k)
+        for p in range(P):
+            kk = min(k, int(nv[p]))
+            assert np.array_equal(got[p], want[p, :kk]), (L, k, p)
+
+
 def test_topk_fused_cooperative_optin(ctx, oracle, monkeypatch):
     """SPL_K3_COOP=1 launches the fused kernel cooperatively (co-residency
     guaranteed by the driver); results are the same as the plain launch."""
@@ -200,7 +226,8 @@ def test_topk_config3_shape(ctx, k3_path, oracle):
 
 
 def test_topk_config4_shape_l256(ctx, oracle):
-    """Config-4-shaped: batched problems, 256-bit codes (u16 score path)."""
+    """Config-4-shaped: batched problems, 256-bit codes (two-pass path, u8
+    scores clamped at 255, windowed counters)."""
     rng = np.random.default_rng(4)
     B, H, n, W = 2, 32, 131072, 8
     codes = rng.integers(0, 2**32, (B * H, n, W), dtype=np.uint64).astype(np.uint32)
