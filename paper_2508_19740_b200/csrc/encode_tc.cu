@@ -29,6 +29,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 
 #include "spl_launch.cuh"
@@ -412,6 +413,288 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
 }
 
+// ---------------------------------------------------------------------------
+// Warp-specialised MLP encoder (bf16 keys via TMA, no pre-activation dump):
+// the production prefill path. The single-CTA-team kernel above runs GEMM1 ->
+// epilogue 1 -> GEMM2 -> epilogue 2 as one chain per tile, so the tensor pipe
+// idles while the CUDA cores work (~42% of peak). Here every stage has its
+// own warps and its own buffers, handshaking through mbarriers, so GEMM1 of
+// tile i+1 and GEMM2 of tile i-1 run under epilogue 1 of tile i and
+// epilogue 2 of tile i-1:
+//   warp 0 (lane 0)  MMA issuer: GEMM1(i) -> D1[i&1], GEMM2(i-1) -> D2
+//   warp 1 (lane 0)  producer: X tiles (TMA, 2 slots), per-head W1/W2 (bulk copy)
+//   warps 2-5        epilogue 1: D1 -> +b1, SiLU -> bf16 A1[i&1] (smem)
+//   warps 6-9        epilogue 2: D2 -> sign bits -> Appendix A.7 code words
+// TMEM: D1[0] cols [0,128), D1[1] [128,256), D2 [256, 256+L) (512 allocated).
+// Shared: X 2 x 32 KB, A1 2 x 32 KB, W1 32 KB, W2 L x 256 B (<= 224 KB).
+// A warp may only touch the TMEM lane quarter warp % 4, so each epilogue
+// group is 4 consecutive warps covering the 4 quarters; thread = tile row.
+constexpr int kWsThreads = 320;
+// tile t <-> (problem bh, tile-in-problem mb, head = bh % H), advanced one
+// tile at a time (a 64-bit divide per tile per role cost ~17% of the samples)
+struct TilePos {
+    uint64_t bh;
+    uint32_t mb, head, tpp, H;
+    __device__ TilePos(uint64_t t, uint32_t tpp_, uint32_t H_) : tpp(tpp_), H(H_) {
+        bh = t / tpp;
+        mb = (uint32_t)(t - bh * tpp);
+        head = (uint32_t)(bh % H);
+    }
+    __device__ __forceinline__ void advance() {
+        if (++mb == tpp) {
+            mb = 0;
+            ++bh;
+            if (++head == H) head = 0;
+        }
+    }
+    __device__ __forceinline__ bool last_of_head() const { return mb + 1 == tpp; }
+};
+enum WsBar {
+    kXFull = 0,      // [2] producer -> MMA (TMA tx)
+    kXEmpty = 2,     // [2] GEMM1 done reading X
+    kD1Full = 4,     // [2] GEMM1 done -> epilogue 1
+    kD1Empty = 6,    // [2] epilogue 1 drained D1 (128 arrivals)
+    kA1Full = 8,     // [2] epilogue 1 wrote A1 (128 arrivals)
+    kA1Empty = 10,   // [2] GEMM2 done reading A1
+    kD2Full = 12,    // GEMM2 done -> epilogue 2
+    kD2Empty = 13,   // epilogue 2 drained D2 (128 arrivals)
+    kWFull = 14,     // head weights landed (bulk tx)
+    kWEmpty = 15,    // last GEMM2 of a head done: weights may be replaced
+    kWsBars = 16
+};
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+
+template <uint32_t W>
+__global__ void __launch_bounds__(kWsThreads, 1)
+    k2_encode_ws(const __grid_constant__ CUtensorMap tmap, TcParams prm) {
+    extern __shared__ uint8_t smem_raw[];
+    __shared__ __align__(8) uint64_t bar[kWsBars];
+    __shared__ uint32_t s_tmem;
+    __shared__ __align__(16) float s_b1[kTcK];  // epilogue 1's bias of the current head
+    constexpr uint32_t L = 32 * W;
+    constexpr uint32_t XB = kTcTileM * 256u;  // one 128 x 128 bf16 operand
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint32_t base_s = (smem_u32(smem_raw) + 1023u) & ~1023u;
+    uint8_t* base = smem_raw + (base_s - smem_u32(smem_raw));
+    uint8_t* sX = base;             // 2 slots
+    uint8_t* sA1 = sX + 2 * XB;     // 2 slots
+    uint8_t* sW1 = sA1 + 2 * XB;
+    uint8_t* sW2 = sW1 + XB;
+
+    const uint64_t T = prm.total_tiles;
+    const uint32_t tpp = prm.tiles_per_problem;
+    const uint64_t t0 = T * blockIdx.x / gridDim.x, t1 = T * (blockIdx.x + 1) / gridDim.x;
+    const uint32_t n = (uint32_t)(t1 - t0);
+
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+                         smem_u32(&s_tmem))
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    if (tid == 32) {
+        for (int i = 0; i < kWsBars; ++i) {
+            const bool many = (i >= kD1Empty && i < kD1Empty + 2) || (i >= kA1Full && i < kA1Full + 2) ||
+                              i == kD2Empty;
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&bar[i])),
+                         "r"(many ? 128u : 1u));
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap)) : "memory");
+    }
+    fence_before();
+    __syncthreads();
+    fence_after();
+    const uint32_t tmem = s_tmem;
+
+    if (warp == 0) {
+        // ------------------------------------------------ MMA issuer
+        if (lane == 0 && n > 0) {
+            uint32_t nw = 0;
+            // a head's weights are last used by GEMM2 of a tile that ends its
+            // problem (consecutive problems have consecutive heads; H = 1
+            // reloads the same head, harmless)
+            auto g2 = [&](uint32_t j, bool ends_head) {
+                mbar_wait(&bar[kA1Full + (j & 1)], (j >> 1) & 1u);
+                if (j >= 1) mbar_wait(&bar[kD2Empty], (j - 1) & 1u);
+                fence_after();
+                gemm_k128(tmem + 256u, smem_u32(sA1 + (j & 1) * XB), smem_u32(sW2), L);
+                umma_commit(&bar[kA1Empty + (j & 1)]);
+                umma_commit(&bar[kD2Full]);
+                if (j + 1 < n && ends_head) umma_commit(&bar[kWEmpty]);
+            };
+            TilePos pos(t0, tpp, prm.H);
+            bool prev_ends = false;
+            for (uint32_t i = 0; i < n; ++i) {
+                const bool newhead = i == 0 || prev_ends;
+                if (newhead) {
+                    // the previous head's last GEMM2 goes first: the producer
+                    // may only replace W1/W2 once it has completed
+                    if (i >= 1) g2(i - 1, true);
+                    mbar_wait(&bar[kWFull], nw & 1u);
+                    ++nw;
+                }
+                mbar_wait(&bar[kXFull + (i & 1)], (i >> 1) & 1u);
+                if (i >= 2) mbar_wait(&bar[kD1Empty + (i & 1)], ((i - 2) >> 1) & 1u);
+                fence_after();
+                gemm_k128(tmem + (i & 1) * 128u, smem_u32(sX + (i & 1) * XB), smem_u32(sW1), kTcK);
+                umma_commit(&bar[kXEmpty + (i & 1)]);
+                umma_commit(&bar[kD1Full + (i & 1)]);
+                if (i >= 1 && !newhead) g2(i - 1, false);
+                prev_ends = pos.last_of_head();
+                pos.advance();
+            }
+            g2(n - 1, false);
+        }
+    } else if (warp == 1) {
+        // ------------------------------------------------ producer
+        if (lane == 0) {
+            uint32_t nw = 0;
+            TilePos pos(t0, tpp, prm.H);
+            bool prev_ends = false;
+            for (uint32_t i = 0; i < n; ++i) {
+                const uint32_t h = pos.head;
+                if (i == 0 || prev_ends) {
+                    if (nw > 0) mbar_wait(&bar[kWEmpty], (nw - 1) & 1u);
+                    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
+                                     smem_u32(&bar[kWFull])),
+                                 "r"(XB + L * 256u)
+                                 : "memory");
+                    bulk_g2s(sW1, prm.w1_tc + (uint64_t)h * XB, XB, &bar[kWFull]);
+                    bulk_g2s(sW2, prm.w2_tc + (uint64_t)h * L * 256u, L * 256u, &bar[kWFull]);
+                    ++nw;
+                }
+                if (i >= 2) mbar_wait(&bar[kXEmpty + (i & 1)], ((i - 2) >> 1) & 1u);
+                tma_x(&tmap, sX + (i & 1) * XB, &bar[kXFull + (i & 1)],
+                      pos.bh * prm.m + (uint64_t)pos.mb * kTcTileM);
+                prev_ends = pos.last_of_head();
+                pos.advance();
+            }
+        }
+    } else if (warp < 6) {
+        // ------------------------------------------------ epilogue 1
+        const uint32_t q = (uint32_t)(warp & 3), row = q * 32 + lane;
+        const uint32_t lane_addr = (q * 32) << 16;
+        const int et = tid - 64;  // 0..127 within the group
+        TilePos pos(t0, tpp, prm.H);
+        uint32_t cur_head = ~0u;
+        for (uint32_t i = 0; i < n; ++i, pos.advance()) {
+            if (pos.head != cur_head) {  // the group's own copy of b1 (named barrier 1)
+                asm volatile("bar.sync 1, 128;" ::: "memory");
+                s_b1[et] = __ldg(prm.b1 + (uint64_t)pos.head * kTcK + et);
+                asm volatile("bar.sync 1, 128;" ::: "memory");
+                cur_head = pos.head;
+            }
+            mbar_wait(&bar[kD1Full + (i & 1)], (i >> 1) & 1u);
+            if (i >= 2) mbar_wait(&bar[kA1Empty + (i & 1)], ((i - 2) >> 1) & 1u);
+            fence_after();
+            uint8_t* a1 = sA1 + (i & 1) * XB;
+            const uint32_t tD = tmem + (i & 1) * 128u + lane_addr;
+#pragma unroll 1
+            for (uint32_t c0 = 0; c0 < kTcK; c0 += 32) {
+                uint32_t r[2][16];
+                tmem_ld16_nowait(tD + c0, r[0]);
+                tmem_ld16_nowait(tD + c0 + 16, r[1]);
+                tmem_wait_ld();
+#pragma unroll
+                for (uint32_t hh = 0; hh < 2; ++hh) {
+                    const float4* bp = reinterpret_cast<const float4*>(s_b1 + c0 + 16 * hh);
+                    float bb[16];
+#pragma unroll
+                    for (int v = 0; v < 4; ++v) {
+                        const float4 x = bp[v];
+                        bb[4 * v] = x.x; bb[4 * v + 1] = x.y; bb[4 * v + 2] = x.z; bb[4 * v + 3] = x.w;
+                    }
+                    uint32_t pk[8];
+#pragma unroll
+                    for (int e = 0; e < 16; e += 2)
+                        pk[e / 2] = pack_bf16(silu_fast(__uint_as_float(r[hh][e]) + bb[e]),
+                                              silu_fast(__uint_as_float(r[hh][e + 1]) + bb[e + 1]));
+                    const uint32_t c = c0 + 16 * hh;
+                    *reinterpret_cast<uint4*>(a1 + tc_sw_off(row, c, kTcTileM)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+                    *reinterpret_cast<uint4*>(a1 + tc_sw_off(row, c + 8, kTcTileM)) = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+                }
+            }
+            fence_before();
+            mbar_arrive(&bar[kD1Empty + (i & 1)]);
+            fence_async_smem();
+            mbar_arrive(&bar[kA1Full + (i & 1)]);
+        }
+    } else {
+        // ------------------------------------------------ epilogue 2
+        const uint32_t q = (uint32_t)(warp & 3), row = q * 32 + lane;
+        const uint32_t tD = tmem + 256u + ((q * 32) << 16);
+        TilePos pos(t0, tpp, prm.H);
+        for (uint32_t i = 0; i < n; ++i, pos.advance()) {
+            const uint64_t bh = pos.bh;
+            const uint32_t grow = pos.mb * kTcTileM + row;
+            mbar_wait(&bar[kD2Full], i & 1u);
+            fence_after();
+            // column j -> word j % W, bit 31 - j / W: feeding the sign bits of
+            // columns w, w + W, w + 2W, ... into word w with a funnel shift
+            // puts column w + W*b at bit 31 - b. Sign after z + 0 (-0 -> +0).
+            uint32_t neg[W];
+#pragma unroll
+            for (uint32_t w = 0; w < W; ++w) neg[w] = 0u;
+            float sum4[4] = {0.0f, 0.0f, 0.0f, 0.0f};  // non-finite check, 4 chains
+#pragma unroll
+            for (uint32_t c0 = 0; c0 < L; c0 += 32) {
+                uint32_t r[2][16];
+                tmem_ld16_nowait(tD + c0, r[0]);
+                tmem_ld16_nowait(tD + c0 + 16, r[1]);
+                tmem_wait_ld();
+#pragma unroll
+                for (uint32_t e = 0; e < 32; ++e) {
+                    const float z = __uint_as_float(r[e >> 4][e & 15]);
+                    sum4[e & 3] += z;
+                    const uint32_t u = __float_as_uint(z + 0.0f);
+                    neg[(c0 + e) % W] = __funnelshift_l(u, neg[(c0 + e) % W], 1);
+                }
+            }
+            fence_before();
+            mbar_arrive(&bar[kD2Empty]);
+            if (grow < prm.m) {
+                if (!isfinite((sum4[0] + sum4[1]) + (sum4[2] + sum4[3])))
+                    raise_dev_err(prm.dev_err, SPL_DEV_ERR_NUMERIC);
+                uint32_t* dst = prm.codes + ((bh * prm.m) + grow) * W;
+                if constexpr (W >= 4) {
+#pragma unroll
+                    for (uint32_t w = 0; w < W; w += 4)
+                        *reinterpret_cast<uint4*>(dst + w) =
+                            make_uint4(~neg[w], ~neg[w + 1], ~neg[w + 2], ~neg[w + 3]);
+                } else {
+#pragma unroll
+                    for (uint32_t w = 0; w < W; ++w) dst[w] = ~neg[w];
+                }
+            }
+        }
+    }
+    fence_before();
+    __syncthreads();
+    fence_after();
+    if (warp == 0)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
+}
+
+const void* k2_ws_fn(uint32_t W) {
+    switch (W) {
+        case 1: return reinterpret_cast<const void*>(&k2_encode_ws<1>);
+        case 2: return reinterpret_cast<const void*>(&k2_encode_ws<2>);
+        case 4: return reinterpret_cast<const void*>(&k2_encode_ws<4>);
+        default: return reinterpret_cast<const void*>(&k2_encode_ws<8>);
+    }
+}
+
 template <bool TMA_X>
 const void* k2_fn(uint32_t W) {
     switch (W) {
@@ -484,6 +767,17 @@ spl_status encode_tc_launch(spl_ctx* ctx, const spl_hasher* hs, const void* x, i
                                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
         if (r != CUDA_SUCCESS) return fail(ctx, SPL_E_CUDA, "encode: cuTensorMapEncodeTiled failed");
+    }
+    // production path: MLP, bf16 keys, no pre-activation dump -> the
+    // warp-specialised kernel (SPL_K2_WS=0 forces the single-team kernel)
+    const char* ws_env = getenv("SPL_K2_WS");
+    if (prm.x_bf16 && !prm.linear && !pre && !(ws_env && *ws_env == '0')) {
+        const size_t wsmem = 1024 + 5 * (size_t)tc_operand_bytes(kTcTileM) + (size_t)prm.L * 256u;
+        const void* wfn = k2_ws_fn(prm.W);
+        SPL_CUDA_TRY(ctx, cudaFuncSetAttribute(wfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wsmem));
+        void* wargs[] = {&tmap, &prm};
+        SPL_CUDA_TRY(ctx, cudaLaunchKernel(wfn, dim3((uint32_t)G), dim3(kWsThreads), wargs, wsmem, s));
+        return after_launch(ctx, "k2_encode_ws");
     }
     const void* fn = prm.x_bf16 ? k2_fn<true>(prm.W) : k2_fn<false>(prm.W);
     SPL_CUDA_TRY(ctx, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));

@@ -115,6 +115,50 @@ def test_encode_tc_bf16_input(ctx):
     assert np.array_equal(p32, p16)
 
 
+@pytest.mark.parametrize("L", [256, 128, 64, 32])
+@pytest.mark.parametrize("shape", [(2, 3, 300), (1, 5, 1000), (3, 2, 128)])
+def test_encode_tc_warp_specialised_matches(ctx, L, shape, monkeypatch):
+    """The production prefill kernel (warp-specialised, bf16 keys through TMA,
+    no pre-activation dump) performs the same bf16 UMMAs, SiLU and sign
+    packing as the single-team kernel, so the codes must be bit-identical;
+    shapes cover partial tiles, several heads per CTA (weight reloads) and
+    more tiles than SMs' worth of work per CTA boundary."""
+    B, H, m = shape
+    rng = np.random.default_rng(7 * L + m)
+    w1, b1, w2 = mlp_weights(rng, H, 128, 128, L)
+    x = torch.from_numpy(rng.standard_normal((B, H, m, 128)).astype(np.float32)).to(DEV).bfloat16()
+    hs = ctx.hasher(w1, b1, w2)
+    ws = torch.zeros((B, H, m, L // 32), dtype=torch.int32, device=DEV)
+    hs.encode_tc(x, capi.SPL_BF16, B, m, ws)
+    torch.cuda.synchronize()
+    ctx.check_device_error()
+    monkeypatch.setenv("SPL_K2_WS", "0")
+    one = torch.zeros_like(ws)
+    hs.encode_tc(x, capi.SPL_BF16, B, m, one)
+    torch.cuda.synchronize()
+    assert torch.equal(ws, one)
+
+
+def test_encode_tc_warp_specialised_large(ctx, monkeypatch):
+    """Many tiles per CTA (long mbarrier phase sequences) at config-4 width."""
+    B, H, m, L = 2, 32, 8192, 256
+    rng = np.random.default_rng(99)
+    w1, b1, w2 = mlp_weights(rng, H, 128, 128, L)
+    g = torch.Generator(device=DEV)
+    g.manual_seed(5)
+    x = torch.randn((B, H, m, 128), generator=g, device=DEV).bfloat16()
+    hs = ctx.hasher(w1, b1, w2)
+    ws = torch.zeros((B, H, m, L // 32), dtype=torch.int32, device=DEV)
+    hs.encode_tc(x, capi.SPL_BF16, B, m, ws)
+    torch.cuda.synchronize()
+    ctx.check_device_error()
+    monkeypatch.setenv("SPL_K2_WS", "0")
+    one = torch.zeros_like(ws)
+    hs.encode_tc(x, capi.SPL_BF16, B, m, one)
+    torch.cuda.synchronize()
+    assert torch.equal(ws, one)
+
+
 @pytest.mark.parametrize("L", [128, 256])
 def test_encode_tc_linear(ctx, L):
     rng = np.random.default_rng(40 + L)
