@@ -145,11 +145,14 @@ __device__ __forceinline__ void stage_x(const TcParams& prm, uint64_t bh, uint32
     if (bad) raise_dev_err(prm.dev_err, SPL_DEV_ERR_NUMERIC);
 }
 
-// SiLU with one MUFU op: z * sigmoid(z) = 0.5 z (1 + tanh(z / 2))
+// SiLU with one MUFU op: z * sigmoid(z) = h (1 + tanh h), h = z / 2, as
+// fma(h, tanh h, h) (the warp-specialised kernel computes the same h as
+// fma(acc, 1/2, b1/2), so both kernels round identically)
 __device__ __forceinline__ float silu_fast(float z) {
+    const float h = 0.5f * z;
     float t;
-    asm("tanh.approx.f32 %0, %1;" : "=f"(t) : "f"(0.5f * z));
-    return 0.5f * z * (1.0f + t);
+    asm("tanh.approx.f32 %0, %1;" : "=f"(t) : "f"(h));
+    return fmaf(h, t, h);
 }
 
 __device__ __forceinline__ void tma_x(const CUtensorMap* tmap, uint8_t* dst, uint64_t* bar,
@@ -423,13 +426,17 @@ __global__ void __launch_bounds__(kTcThreads, 1)
 // epilogue 2 of tile i-1:
 //   warp 0 (lane 0)  MMA issuer: GEMM1(i) -> D1[i&1], GEMM2(i-1) -> D2
 //   warp 1 (lane 0)  producer: X tiles (TMA, 2 slots), per-head W1/W2 (bulk copy)
-//   warps 2-5        epilogue 1: D1 -> +b1, SiLU -> bf16 A1[i&1] (smem)
-//   warps 6-9        epilogue 2: D2 -> sign bits -> Appendix A.7 code words
+//   warps 2-9        epilogue 1: D1 -> +b1, SiLU -> bf16 A1[i&1] (smem); two
+//                    warps per lane quarter (column halves): it is the
+//                    busiest stage (MUFU tanh + packing), one warp per SMSP
+//                    could not hide its latencies
+//   warps 10-13      epilogue 2: D2 -> sign bits -> Appendix A.7 code words
 // TMEM: D1[0] cols [0,128), D1[1] [128,256), D2 [256, 256+L) (512 allocated).
 // Shared: X 2 x 32 KB, A1 2 x 32 KB, W1 32 KB, W2 L x 256 B (<= 224 KB).
 // A warp may only touch the TMEM lane quarter warp % 4, so each epilogue
 // group is 4 consecutive warps covering the 4 quarters; thread = tile row.
-constexpr int kWsThreads = 320;
+constexpr int kWsThreads = 448;
+constexpr uint32_t kEpi1Threads = 256;
 // tile t <-> (problem bh, tile-in-problem mb, head = bh % H), advanced one
 // tile at a time (a 64-bit divide per tile per role cost ~17% of the samples)
 struct TilePos {
@@ -453,8 +460,8 @@ enum WsBar {
     kXFull = 0,      // [2] producer -> MMA (TMA tx)
     kXEmpty = 2,     // [2] GEMM1 done reading X
     kD1Full = 4,     // [2] GEMM1 done -> epilogue 1
-    kD1Empty = 6,    // [2] epilogue 1 drained D1 (128 arrivals)
-    kA1Full = 8,     // [2] epilogue 1 wrote A1 (128 arrivals)
+    kD1Empty = 6,    // [2] epilogue 1 drained D1 (256 arrivals)
+    kA1Full = 8,     // [2] epilogue 1 wrote A1 (256 arrivals)
     kA1Empty = 10,   // [2] GEMM2 done reading A1
     kD2Full = 12,    // GEMM2 done -> epilogue 2
     kD2Empty = 13,   // epilogue 2 drained D2 (128 arrivals)
@@ -504,10 +511,9 @@ __global__ void __launch_bounds__(kWsThreads, 1)
     }
     if (tid == 32) {
         for (int i = 0; i < kWsBars; ++i) {
-            const bool many = (i >= kD1Empty && i < kD1Empty + 2) || (i >= kA1Full && i < kA1Full + 2) ||
-                              i == kD2Empty;
+            const bool e1 = (i >= kD1Empty && i < kD1Empty + 2) || (i >= kA1Full && i < kA1Full + 2);
             asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&bar[i])),
-                         "r"(many ? 128u : 1u));
+                         "r"(e1 ? kEpi1Threads : i == kD2Empty ? 128u : 1u));
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap)) : "memory");
@@ -581,48 +587,61 @@ __global__ void __launch_bounds__(kWsThreads, 1)
                 pos.advance();
             }
         }
-    } else if (warp < 6) {
+    } else if (warp < 10) {
         // ------------------------------------------------ epilogue 1
         const uint32_t q = (uint32_t)(warp & 3), row = q * 32 + lane;
+        const uint32_t ch = (uint32_t)(warp - 2) >> 2;  // column half
         const uint32_t lane_addr = (q * 32) << 16;
-        const int et = tid - 64;  // 0..127 within the group
+        const int et = tid - 64;  // 0..255 within the group
+        const uint32_t r7 = row & 7u;
         TilePos pos(t0, tpp, prm.H);
         uint32_t cur_head = ~0u;
         for (uint32_t i = 0; i < n; ++i, pos.advance()) {
-            if (pos.head != cur_head) {  // the group's own copy of b1 (named barrier 1)
-                asm volatile("bar.sync 1, 128;" ::: "memory");
-                s_b1[et] = __ldg(prm.b1 + (uint64_t)pos.head * kTcK + et);
-                asm volatile("bar.sync 1, 128;" ::: "memory");
+            if (pos.head != cur_head) {  // the group's own copy of b1 / 2 (named barrier 1)
+                asm volatile("bar.sync 1, 256;" ::: "memory");
+                if (et < (int)kTcK) s_b1[et] = 0.5f * __ldg(prm.b1 + (uint64_t)pos.head * kTcK + et);
+                asm volatile("bar.sync 1, 256;" ::: "memory");
                 cur_head = pos.head;
             }
             mbar_wait(&bar[kD1Full + (i & 1)], (i >> 1) & 1u);
             if (i >= 2) mbar_wait(&bar[kA1Empty + (i & 1)], ((i - 2) >> 1) & 1u);
             fence_after();
-            uint8_t* a1 = sA1 + (i & 1) * XB;
-            const uint32_t tD = tmem + (i & 1) * 128u + lane_addr;
-#pragma unroll 1
-            for (uint32_t c0 = 0; c0 < kTcK; c0 += 32) {
+            // this thread's half row of A1: K block ch (64 columns), row `row`;
+            // 16-byte chunk j of the row sits at chunk j ^ (row % 8)
+            uint8_t* a1row = sA1 + (i & 1) * XB + ch * (kTcTileM * 128u) + row * 128u;
+            const uint32_t tD = tmem + (i & 1) * 128u + lane_addr + ch * 64u;
+#pragma unroll
+            for (uint32_t c0 = 0; c0 < 64; c0 += 32) {
                 uint32_t r[2][16];
                 tmem_ld16_nowait(tD + c0, r[0]);
                 tmem_ld16_nowait(tD + c0 + 16, r[1]);
                 tmem_wait_ld();
 #pragma unroll
                 for (uint32_t hh = 0; hh < 2; ++hh) {
-                    const float4* bp = reinterpret_cast<const float4*>(s_b1 + c0 + 16 * hh);
-                    float bb[16];
+                    const float4* bp = reinterpret_cast<const float4*>(s_b1 + ch * 64u + c0 + 16 * hh);
+                    float hb[16];  // b1 / 2
 #pragma unroll
                     for (int v = 0; v < 4; ++v) {
                         const float4 x = bp[v];
-                        bb[4 * v] = x.x; bb[4 * v + 1] = x.y; bb[4 * v + 2] = x.z; bb[4 * v + 3] = x.w;
+                        hb[4 * v] = x.x; hb[4 * v + 1] = x.y; hb[4 * v + 2] = x.z; hb[4 * v + 3] = x.w;
                     }
                     uint32_t pk[8];
 #pragma unroll
-                    for (int e = 0; e < 16; e += 2)
-                        pk[e / 2] = pack_bf16(silu_fast(__uint_as_float(r[hh][e]) + bb[e]),
-                                              silu_fast(__uint_as_float(r[hh][e + 1]) + bb[e + 1]));
-                    const uint32_t c = c0 + 16 * hh;
-                    *reinterpret_cast<uint4*>(a1 + tc_sw_off(row, c, kTcTileM)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
-                    *reinterpret_cast<uint4*>(a1 + tc_sw_off(row, c + 8, kTcTileM)) = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+                    for (int e = 0; e < 16; e += 2) {
+                        // SiLU(z) = h (1 + tanh h), h = z / 2 = acc / 2 + b1 / 2
+                        float a[2];
+#pragma unroll
+                        for (int u = 0; u < 2; ++u) {
+                            const float hv = fmaf(__uint_as_float(r[hh][e + u]), 0.5f, hb[e + u]);
+                            float t;
+                            asm("tanh.approx.f32 %0, %1;" : "=f"(t) : "f"(hv));
+                            a[u] = fmaf(hv, t, hv);
+                        }
+                        pk[e / 2] = pack_bf16(a[0], a[1]);
+                    }
+                    const uint32_t j = (c0 + 16 * hh) >> 3;  // chunk index in the K block
+                    *reinterpret_cast<uint4*>(a1row + (((j) ^ r7) << 4)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+                    *reinterpret_cast<uint4*>(a1row + (((j + 1) ^ r7) << 4)) = make_uint4(pk[4], pk[5], pk[6], pk[7]);
                 }
             }
             fence_before();
