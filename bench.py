@@ -301,38 +301,52 @@ def main():
 
     # e2e through the C-ABI with host buffers: H2D of the step's query vectors
     # (encoded on device, exact mode), retrieval, D2H of the indices + counts.
+    # (N > 1: every rank encodes the step's queries, runs the sharded flow and
+    # reads back its share of the indices + their global offsets)
     rng = np.random.default_rng(7)
-    e2e = None
     decode = None
     decode4 = None
     prefill = None
+    w1 = (rng.standard_normal((H, D, D)) / np.sqrt(D)).astype(np.float32)
+    b1 = np.zeros((H, D), np.float32)
+    w2 = (rng.standard_normal((H, D, L)) / np.sqrt(D)).astype(np.float32)
+    hasher = ctx.hasher(w1, b1, w2)
+    q_host = torch.from_numpy(rng.standard_normal((1, H, D)).astype(np.float32)).pin_memory()
+    idx_host = torch.empty((P, k), dtype=torch.int32).pin_memory()
+    cnt_host = torch.empty(P, dtype=torch.int32).pin_memory()
+    off_host = torch.empty(P, dtype=torch.int32).pin_memory()
+    q_dev = torch.empty((1, H, D), dtype=torch.float32, device=dev)
+
+    def e2e_step():
+        q_dev.copy_(q_host, non_blocking=True)
+        hasher.encode(q_dev, 1, 1, qcodes, capi.SPL_ENCODE_EXACT, stream)
+        retrieval()
+        idx_host.copy_(idx, non_blocking=True)
+        cnt_host.copy_(cnt, non_blocking=True)
+        if world > 1:
+            off_host.copy_(off, non_blocking=True)
+
+    for _ in range(args.warmup):
+        e2e_step()
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    e2e_ms = event_timer(torch, e2e_step, args.steps, stream)
+    enc_ms = event_timer(torch, lambda: hasher.encode(q_dev, 1, 1, qcodes, capi.SPL_ENCODE_EXACT, stream),
+                         args.steps, stream)
+    if dist:
+        t = torch.tensor([e2e_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+    d2h = idx_host.numel() * 4 + cnt_host.numel() * 4 + (off_host.numel() * 4 if world > 1 else 0)
+    e2e = {"value": round(e2e_ms * 1000, 2), "unit": "µs",
+           "h2d_bytes_per_step": int(q_host.numel() * 4),
+           "d2h_bytes_per_step": int(d2h),
+           "path": ("spl_encode(query, exact) + spl_hamming_topk, pinned host buffers" if world == 1
+                    else "spl_encode(query, exact) + spl_shard_histogram + NCCL all-gather + "
+                         "spl_shard_select, pinned host buffers (max over ranks)"),
+           "encode_us": round(enc_ms * 1000, 2)}
     if world == 1:
-        w1 = (rng.standard_normal((H, D, D)) / np.sqrt(D)).astype(np.float32)
-        b1 = np.zeros((H, D), np.float32)
-        w2 = (rng.standard_normal((H, D, L)) / np.sqrt(D)).astype(np.float32)
-        hasher = ctx.hasher(w1, b1, w2)
-        q_host = torch.from_numpy(rng.standard_normal((1, H, D)).astype(np.float32)).pin_memory()
-        idx_host = torch.empty((P, k), dtype=torch.int32).pin_memory()
-        cnt_host = torch.empty(P, dtype=torch.int32).pin_memory()
-        q_dev = torch.empty((1, H, D), dtype=torch.float32, device=dev)
-
-        def e2e_step():
-            q_dev.copy_(q_host, non_blocking=True)
-            hasher.encode(q_dev, 1, 1, qcodes, capi.SPL_ENCODE_EXACT, stream)
-            ctx.hamming_topk(codes, n_local, L, qcodes, P, nvalid, 1, n_local, k, idx, cnt, stream)
-            idx_host.copy_(idx, non_blocking=True)
-            cnt_host.copy_(cnt, non_blocking=True)
-
-        for _ in range(args.warmup):
-            e2e_step()
-        e2e_ms = event_timer(torch, e2e_step, args.steps, stream)
-        enc_ms = event_timer(torch, lambda: hasher.encode(q_dev, 1, 1, qcodes, capi.SPL_ENCODE_EXACT, stream),
-                             args.steps, stream)
-        e2e = {"value": round(e2e_ms * 1000, 2), "unit": "µs",
-               "h2d_bytes_per_step": int(q_host.numel() * 4),
-               "d2h_bytes_per_step": int(idx_host.numel() * 4 + cnt_host.numel() * 4),
-               "path": "spl_encode(query, exact) + spl_hamming_topk, pinned host buffers",
-               "encode_us": round(enc_ms * 1000, 2)}
         if not args.no_decode:
             decode = bench_decode(torch, capi, ctx, dev, stream, args, hasher)
         if not args.no_prefill:

@@ -235,6 +235,32 @@ int spotref_full_attention(const float* queries, std::uint32_t q, const float* k
     });
 }
 
+// oracle_topk (attention_eval.cpp:121-135); out[q][k], counts[q].
+int spotref_oracle_topk(const float* queries, std::uint32_t q, const float* keys, std::uint32_t n,
+                        std::uint32_t d, float scale, const std::uint32_t* offsets, std::uint32_t k,
+                        std::uint32_t* out, std::uint32_t* counts) {
+    return guard([&] {
+        AttentionInstance inst;
+        inst.queries = mat(queries, q, d);
+        inst.keys = mat(keys, n, d);
+        inst.values = mat(keys, n, d);
+        inst.scale = scale;
+        inst.causal_offsets.assign(offsets, offsets + q);
+        const RetrievalResult r = oracle_topk(inst, k);
+        for (std::uint32_t i = 0; i < q; ++i) {
+            counts[i] = static_cast<std::uint32_t>(r.indices[i].size());
+            std::memcpy(out + std::size_t(i) * k, r.indices[i].data(),
+                        sizeof(std::uint32_t) * r.indices[i].size());
+        }
+    });
+}
+
+// iou (attention_eval.cpp:216-232) of two ascending index lists.
+double spotref_iou(const std::uint32_t* a, std::uint32_t na, const std::uint32_t* b,
+                   std::uint32_t nb) {
+    return iou({a, na}, {b, nb});
+}
+
 // hash_topk (attention_eval.cpp:137-181) with an MLP hasher; out[q][k]
 // (each row holds min(k, offset) indices; the rest untouched).
 int spotref_hash_topk_mlp(const float* w1, const float* b1, const float* w2, std::uint32_t h,

@@ -230,6 +230,36 @@ static float ref_dot(const float* q, const float* k, uint32_t d) {
     return acc;
 }
 
+/* causal_logits (attention_eval.cpp:80-91): the same `acc += q[p] * k[p]`
+ * loop as attend_subset, compiled the same way (ref_dot), times scale.
+ * oracle_topk (attention_eval.cpp:121-135): per query, top_k_indices<float>
+ * over its causal logits with k clamped to the causal range. out[i][k]
+ * holds min(k, offsets[i]) ascending indices; counts[i] that number. */
+int orc_oracle_topk(const float* queries, uint32_t q, const float* keys, uint32_t n, uint32_t d,
+                    float scale, const uint32_t* offsets, uint32_t k, uint32_t* out,
+                    uint32_t* counts) {
+    if (k == 0) return 1;
+    float* logits = (float*)malloc(sizeof(float) * (n ? n : 1));
+    if (!logits) return 1;
+    for (uint32_t i = 0; i < q; ++i) {
+        const uint32_t valid = offsets[i];
+        if (valid == 0 || valid > n) {
+            free(logits);
+            return 1;
+        }
+        for (uint32_t j = 0; j < valid; ++j)
+            logits[j] = ref_dot(queries + (size_t)i * d, keys + (size_t)j * d, d) * scale;
+        const uint32_t kk = k < valid ? k : valid;
+        counts[i] = kk;
+        if (orc_top_k_f32(logits, valid, kk, out + (size_t)i * k)) {
+            free(logits);
+            return 1;
+        }
+    }
+    free(logits);
+    return 0;
+}
+
 /* attend_subset, attention_eval.cpp:54-78. */
 static void attend_subset(const float* q, const float* keys, const float* values, uint32_t d,
                           float scale, const uint32_t* idx, size_t cnt, float* out) {

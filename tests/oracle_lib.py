@@ -80,6 +80,8 @@ class Oracle(_Base):
                                            C.c_uint32, C.c_float, u32p, u32p, u64p, f32p]
         L.orc_retrieve_batch.argtypes = [u32p, C.c_uint32, C.c_uint64, C.c_uint32, u32p, u32p,
                                          C.c_uint32, u32p, C.c_int]
+        L.orc_oracle_topk.argtypes = [f32p, C.c_uint32, f32p, C.c_uint32, C.c_uint32, C.c_float,
+                                      u32p, C.c_uint32, u32p, u32p]
 
     # -- bitcodes
     def pack_bits(self, bits):
@@ -163,6 +165,16 @@ class Oracle(_Base):
                                                 po, out))
         return out
 
+    def oracle_topk(self, queries, keys, scale, offsets, k):
+        """-> (indices [q][k] uint32, counts [q])"""
+        queries, keys = _c(queries, np.float32), _c(keys, np.float32)
+        q, d = queries.shape
+        out = np.zeros((q, k), np.uint32)
+        cnt = np.zeros(q, np.uint32)
+        self._chk(self.lib.orc_oracle_topk(queries, q, keys, keys.shape[0], d, C.c_float(scale),
+                                           _c(offsets, np.uint32), k, out, cnt))
+        return out, cnt
+
     def retrieve_batch(self, codes, qcodes, n_valid, k, threads=None):
         """codes [P][cap][W], qcodes [P][W], n_valid [P] -> out [P][k] (0-padded)."""
         codes = _c(codes, np.uint32)
@@ -208,6 +220,10 @@ class RefLib(_Base):
                                                C.c_uint32, C.c_float, u32p, u32p, u64p, f32p]
         L.spotref_full_attention.argtypes = [f32p, C.c_uint32, f32p, f32p, C.c_uint32,
                                              C.c_uint32, C.c_float, u32p, f32p]
+        L.spotref_oracle_topk.argtypes = [f32p, C.c_uint32, f32p, C.c_uint32, C.c_uint32,
+                                          C.c_float, u32p, C.c_uint32, u32p, u32p]
+        L.spotref_iou.argtypes = [u32p, C.c_uint32, u32p, C.c_uint32]
+        L.spotref_iou.restype = C.c_double
         L.spotref_hash_topk_mlp.argtypes = [f32p, f32p, f32p, C.c_uint32, C.c_uint32, f32p,
                                             C.c_uint32, f32p, f32p, C.c_uint32, C.c_uint32,
                                             C.c_float, u32p, C.c_uint32, u32p, u32p]
@@ -318,6 +334,20 @@ class RefLib(_Base):
         self._chk(self.lib.spotref_full_attention(queries, q, keys, values, keys.shape[0], d, scale,
                                                   _c(offsets, np.uint32), out))
         return out
+
+    def oracle_topk(self, queries, keys, scale, offsets, k):
+        queries, keys = _c(queries, np.float32), _c(keys, np.float32)
+        q, d = queries.shape
+        out = np.zeros((q, k), np.uint32)
+        cnt = np.zeros(q, np.uint32)
+        self._chk(self.lib.spotref_oracle_topk(queries, q, keys, keys.shape[0], d, C.c_float(scale),
+                                               _c(offsets, np.uint32), k, out, cnt))
+        return out, cnt
+
+    def iou(self, a, b):
+        a, b = _c(a, np.uint32), _c(b, np.uint32)
+        return float(self.lib.spotref_iou(a if a.size else np.zeros(1, np.uint32), a.size,
+                                          b if b.size else np.zeros(1, np.uint32), b.size))
 
     def hash_topk_mlp(self, w1, b1, w2, queries, keys, values, scale, offsets, k):
         w1, b1, w2 = _c(w1, np.float32), _c(b1, np.float32), _c(w2, np.float32)

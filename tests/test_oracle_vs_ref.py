@@ -65,3 +65,29 @@ def test_retrieve_batch_config_shape_vs_reference(oracle, ref):
         ref.index_destroy(h)
     b = oracle.retrieve_batch(codes, q, nv, k)
     assert np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("d", [128, 64, 100, 36])
+def test_oracle_topk_vs_reference(oracle, ref, d):
+    """oracle_topk (attention_eval.cpp:121-135): the C restatement's causal
+    logits (products rounded, summed in order, FMA tail) give the reference's
+    indices, including near-ties from duplicated keys."""
+    rng = np.random.default_rng(d)
+    n, q = 3000, 6
+    keys = rng.standard_normal((n, d)).astype(np.float32)
+    keys[100:140] = keys[7]  # exact logit ties
+    queries = rng.standard_normal((q, d)).astype(np.float32)
+    offsets = np.array([n, n - 1, 2000, 141, 1, 500], np.uint32)
+    scale = np.float32(1.0 / np.sqrt(d))
+    for k in (1, 64, 300, 3000):
+        a, ca = oracle.oracle_topk(queries, keys, scale, offsets, k)
+        b, cb = ref.oracle_topk(queries, keys, scale, offsets, k)
+        assert np.array_equal(ca, cb)
+        for i in range(q):
+            assert np.array_equal(a[i, :ca[i]], b[i, :cb[i]]), (d, k, i)
+
+
+def test_iou_reference_examples(ref):
+    assert ref.iou([], []) == 1.0
+    assert ref.iou([1, 2, 3], [2, 3, 4]) == 0.5
+    assert ref.iou([0, 5], [1, 6]) == 0.0
