@@ -307,6 +307,7 @@ def main():
     decode = None
     decode4 = None
     prefill = None
+    accuracy = None
     w1 = (rng.standard_normal((H, D, D)) / np.sqrt(D)).astype(np.float32)
     b1 = np.zeros((H, D), np.float32)
     w2 = (rng.standard_normal((H, D, L)) / np.sqrt(D)).astype(np.float32)
@@ -353,6 +354,8 @@ def main():
             prefill = bench_prefill(torch, capi, ctx, dev, stream, args)
         if not args.no_decode:
             decode4 = bench_decode4(torch, capi, ctx, dev, stream, args)
+        if not args.no_decode:
+            accuracy = bench_accuracy(torch, capi, ctx, dev, stream, args)
     clk = clocks.stop()
 
     # CPU baseline (rank 0, N = 1): the reference on this host's cores
@@ -416,6 +419,8 @@ def main():
         line["prefill_encode"] = prefill
     if decode4:
         line["batched_decode"] = decode4
+    if accuracy:
+        line["retrieval_accuracy"] = accuracy
     if rank == 0:
         print(json.dumps(line), flush=True)
     ctx.close()
@@ -528,6 +533,53 @@ def bench_decode4(torch, capi, ctx, dev, stream, args):
             "roofline": {"bound": "hbm", "algorithmic_bytes": alg,
                          "achieved": round(alg / (ms * 1e-3) / 1e9, 1), "peak": hbm,
                          "frac": round(alg / (ms * 1e-3) / 1e9 / hbm, 4)}}
+
+
+def bench_accuracy(torch, capi, ctx, dev, stream, args):
+    """Retrieval accuracy (the paper's Table-1 metric) at the
+    config-2 shape: IoU of the MLP-hash top-k (exact codes of the actual
+    keys, K3) with the exact dense top-k (spl_oracle_topk), per head, plus
+    the dense oracle's own time. Random-init hasher on Gaussian keys, so the
+    IoU is the untrained baseline; trained SPLH checkpoints raise it."""
+    Hh, n, d, L2 = 32, 131072, 128, 128
+    k = budget(n)
+    rng = np.random.default_rng(21)
+    w1 = (rng.standard_normal((Hh, d, d)) / np.sqrt(d)).astype(np.float32)
+    b1 = np.zeros((Hh, d), np.float32)
+    w2 = (rng.standard_normal((Hh, d, L2)) / np.sqrt(d)).astype(np.float32)
+    hs = ctx.hasher(w1, b1, w2)
+    g = torch.Generator(device=dev)
+    g.manual_seed(21)
+    keys = torch.randn((1, Hh, n, d), generator=g, device=dev, dtype=torch.float32)
+    q = torch.randn((1, Hh, d), generator=g, device=dev, dtype=torch.float32)
+    codes = torch.empty((1, Hh, n, L2 // 32), device=dev, dtype=torch.int32)
+    hs.encode(keys, 1, n, codes, capi.SPL_ENCODE_EXACT, stream)
+    qc = torch.empty((1, Hh, L2 // 32), device=dev, dtype=torch.int32)
+    hs.encode(q, 1, 1, qc, capi.SPL_ENCODE_EXACT, stream)
+    nv = torch.full((1,), n, dtype=torch.int32, device=dev)
+    hidx = torch.zeros((Hh, k), dtype=torch.int32, device=dev)
+    hcnt = torch.zeros(Hh, dtype=torch.int32, device=dev)
+    ctx.hamming_topk(codes, n, L2, qc, Hh, nv, Hh, n, k, hidx, hcnt, stream)
+    oidx = torch.zeros((Hh, k), dtype=torch.int32, device=dev)
+    ocnt = torch.zeros(Hh, dtype=torch.int32, device=dev)
+    scale = float(1 / np.sqrt(d))
+
+    def oracle():
+        ctx.oracle_topk(q[0], keys, capi.SPL_F32, n, d, Hh, nv, Hh, n, scale, k, oidx, ocnt,
+                        None, stream)
+    oracle()
+    o_ms = event_timer(torch, oracle, 5, stream)
+    out = torch.zeros(Hh, dtype=torch.float64, device=dev)
+    ctx.iou(hidx, hcnt, k, oidx, ocnt, k, Hh, out, stream)
+    torch.cuda.synchronize()
+    ious = out.cpu().numpy()
+    del keys, codes
+    return {"workload": "config2 shape: 32 heads x 131072 f32 keys, d=128, 128-bit exact MLP codes, "
+                        "k=2621; IoU(hash top-k, exact dense top-k) per head",
+            "mean_iou": round(float(ious.mean()), 4), "min_iou": round(float(ious.min()), 4),
+            "max_iou": round(float(ious.max()), 4),
+            "oracle_topk_us": round(o_ms * 1000, 1),
+            "data": "synthetic Gaussian keys/queries, random-init hasher (untrained baseline)"}
 
 
 def bench_decode(torch, capi, ctx, dev, stream, args, hasher_c3):

@@ -102,6 +102,29 @@ spl_status spl_nxor_scores(spl_ctx* ctx, const uint32_t* codes, uint64_t problem
 spl_status spl_top_k(spl_ctx* ctx, const void* scores, int dtype, uint32_t P, uint64_t n,
                      uint64_t scores_stride, uint32_t k, uint32_t* idx, void* stream);
 
+/* ------------------------------------------- dense retrieval */
+/* oracle_topk (attention_eval.hpp:47, attention_eval.cpp:121-135): for every
+ * problem p (one query q[p][d] against rows [0, n_valid) of keys + p * cap * d,
+ * an f32/bf16 [.][cap][d] cache; cap = 0: every problem reads the same
+ * rows, as the queries of one AttentionInstance do), the exact float
+ * logits of causal_logits
+ * (attention_eval.cpp:80-91: products rounded, summed in index order, FMA
+ * for the < 4-element tail, times scale) and top_k_indices<float> of
+ * min(k, n_valid) of them (score desc, index asc; -0 == +0), ascending in
+ * idx[p][0..cnt[p]) (row stride k). Bit-identical with the reference.
+ * logits (nullable, [P][n_max] f32) receives the logits; NULL uses the
+ * context workspace. k == 0 -> SPL_E_DIMENSION ("oracle_topk: k must be >= 1"). */
+spl_status spl_oracle_topk(spl_ctx* ctx, const float* q, const void* keys, int kv_dtype,
+                           uint64_t cap, uint32_t d, uint32_t P, const uint32_t* n_valid,
+                           uint32_t nvalid_div, uint64_t n_max, float scale, uint32_t k,
+                           uint32_t* idx, uint32_t* cnt, float* logits, void* stream);
+/* iou (attention_eval.hpp:63, attention_eval.cpp:216-232) per problem of two
+ * ascending index lists a[p][0..cnt_a[p]) and b[p][0..cnt_b[p]) (row strides
+ * a_stride, b_stride): |a ∩ b| / |a ∪ b| as double, 1.0 when both are empty. */
+spl_status spl_iou(spl_ctx* ctx, const uint32_t* a, const uint32_t* cnt_a, uint64_t a_stride,
+                   const uint32_t* b, const uint32_t* cnt_b, uint64_t b_stride, uint32_t P,
+                   double* out, void* stream);
+
 /* --------------------------------------------------- hamming top-k (K3) */
 /* The fused retrieval (hash_topk's hot loop, attention_eval.cpp:172-179:
  * nxor_scores_into(valid) + top_k_indices(min(k, valid))): for every

@@ -100,6 +100,8 @@ _SIGS = {
     "spl_decode_step": [vp, vp, vp, vp, vp, u32, vp, vp, vp, i32, u64, vp, u64, u32, f32, vp, vp,
                         vp, vp],
     "spl_budget_from_rate": [dbl, u64, u32p],
+    "spl_oracle_topk": [vp, vp, vp, i32, u64, u32, u32, vp, u32, u64, f32, u32, vp, vp, vp, vp],
+    "spl_iou": [vp, vp, vp, u64, vp, vp, u64, u32, vp, vp],
 }
 _RESTYPE = {"spl_version": C.c_char_p, "spl_last_error": C.c_char_p, "spl_ctx_destroy": None,
             "spl_hasher_destroy": None, "spl_launch_count": C.c_uint64}
@@ -234,6 +236,17 @@ class Context:
                                       _stream(stream)))
 
     # -- K3
+    def oracle_topk(self, q, keys, kv_dtype, cap, d, P, n_valid, nvalid_div, n_max, scale, k, idx,
+                    cnt, logits=None, stream=None):
+        """Exact dense top-k (the reference's oracle_topk) on the GPU."""
+        self.check(self.lib.spl_oracle_topk(self.h, _ptr(q), _ptr(keys), kv_dtype, cap, d, P,
+                                            _ptr(n_valid), nvalid_div, n_max, scale, k, _ptr(idx),
+                                            _ptr(cnt), _ptr(logits), _stream(stream)))
+
+    def iou(self, a, cnt_a, a_stride, b, cnt_b, b_stride, P, out, stream=None):
+        self.check(self.lib.spl_iou(self.h, _ptr(a), _ptr(cnt_a), a_stride, _ptr(b), _ptr(cnt_b),
+                                    b_stride, P, _ptr(out), _stream(stream)))
+
     def hamming_topk(self, codes, stride_rows, L, qcodes, P, n_valid, nvalid_div, n_max, k, idx,
                      cnt, stream=None):
         self.check(self.lib.spl_hamming_topk(self.h, _ptr(codes), stride_rows, L, _ptr(qcodes), P,

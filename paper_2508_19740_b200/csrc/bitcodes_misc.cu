@@ -79,15 +79,23 @@ __device__ __forceinline__ uint64_t score_key(const void* s, uint64_t i) {
 
 constexpr int kTopkThreads = 1024;
 
+// n_valid (nullable): row p ranks only its first min(n, n_valid[p / div])
+// scores and keeps min(k, that) of them (oracle_topk's causal clamp,
+// attention_eval.cpp:131); cnt (nullable) receives that count.
 template <int DT>
-__global__ void __launch_bounds__(kTopkThreads) k_topk_radix(const void* scores, uint64_t n,
-                                                             uint64_t stride, uint32_t k,
-                                                             uint32_t* idx) {
+__global__ void __launch_bounds__(kTopkThreads) k_topk_radix(const void* scores, uint64_t n_all,
+                                                             uint64_t stride, uint32_t k_all,
+                                                             uint32_t* idx, const uint32_t* n_valid,
+                                                             uint32_t nvalid_div, uint32_t* cnt) {
     __shared__ uint32_t hist[256];
     __shared__ uint64_t s_prefix, s_mask;
     __shared__ uint32_t s_need;
     __shared__ uint32_t s_warp[kTopkThreads / 32 + 1];
     const uint32_t p = blockIdx.x;
+    const uint64_t n = n_valid ? min(n_all, (uint64_t)n_valid[p / nvalid_div]) : n_all;
+    const uint32_t k = (uint32_t)min((uint64_t)k_all, n);
+    if (cnt && threadIdx.x == 0) cnt[p] = k;
+    if (k == 0) return;
     const size_t esz = DT == 0 ? 4 : (DT == 1 ? 4 : 8);
     const void* row = static_cast<const uint8_t*>(scores) + (uint64_t)p * stride * esz;
     const int key_bits = DT == 2 ? 64 : 32;
@@ -154,7 +162,7 @@ __global__ void __launch_bounds__(kTopkThreads) k_topk_radix(const void* scores,
             sel_tile += s_warp[w];
         }
         if (sel)
-            idx[(uint64_t)p * k + carry_sel + sel_before_warp +
+            idx[(uint64_t)p * k_all + carry_sel + sel_before_warp +
                 __popc(sel_ball & ((1u << lane) - 1u))] = (uint32_t)i;
         carry_sel += sel_tile;
         carry_eq += eq_tile;
@@ -191,12 +199,13 @@ spl_status nxor_scores_launch(spl_ctx* ctx, const uint32_t* codes, uint64_t stri
 }
 
 spl_status top_k_launch(spl_ctx* ctx, const void* scores, int dtype, uint32_t P, uint64_t n,
-                        uint64_t stride, uint32_t k, uint32_t* idx, cudaStream_t s) {
+                        uint64_t stride, uint32_t k, uint32_t* idx, cudaStream_t s,
+                        const uint32_t* n_valid, uint32_t nvalid_div, uint32_t* cnt) {
     if (P == 0) return SPL_OK;
     switch (dtype) {
-        case 0: k_topk_radix<0><<<P, kTopkThreads, 0, s>>>(scores, n, stride, k, idx); break;
-        case 1: k_topk_radix<1><<<P, kTopkThreads, 0, s>>>(scores, n, stride, k, idx); break;
-        case 2: k_topk_radix<2><<<P, kTopkThreads, 0, s>>>(scores, n, stride, k, idx); break;
+        case 0: k_topk_radix<0><<<P, kTopkThreads, 0, s>>>(scores, n, stride, k, idx, n_valid, nvalid_div, cnt); break;
+        case 1: k_topk_radix<1><<<P, kTopkThreads, 0, s>>>(scores, n, stride, k, idx, n_valid, nvalid_div, cnt); break;
+        case 2: k_topk_radix<2><<<P, kTopkThreads, 0, s>>>(scores, n, stride, k, idx, n_valid, nvalid_div, cnt); break;
         default: return fail(ctx, SPL_E_DIMENSION, "top_k_indices: unknown score dtype");
     }
     return after_launch(ctx, "k_topk_radix");

@@ -75,6 +75,7 @@ void spl_ctx_destroy(spl_ctx* ctx) {
     cudaFree(ctx->att_ws);
     cudaFree(ctx->att_counters);
     cudaFree(ctx->scratch);
+    cudaFree(ctx->dense_ws);
     delete ctx;
 }
 
@@ -195,6 +196,42 @@ spl_status spl_top_k(spl_ctx* ctx, const void* scores, int dtype, uint32_t P, ui
                     "top_k_indices: k=" + std::to_string(k) + " out of range for n=" +
                         std::to_string(n));
     return top_k_launch(ctx, scores, dtype, P, n, scores_stride, k, idx, S(stream));
+}
+
+// ------------------------------------------------ dense retrieval (§8 f2)
+spl_status spl_oracle_topk(spl_ctx* ctx, const float* q, const void* keys, int kv_dtype,
+                           uint64_t cap, uint32_t d, uint32_t P, const uint32_t* n_valid,
+                           uint32_t nvalid_div, uint64_t n_max, float scale, uint32_t k,
+                           uint32_t* idx, uint32_t* cnt, float* logits, void* stream) {
+    if (!ctx) return SPL_E_STATE;
+    if (k == 0) return fail(ctx, SPL_E_DIMENSION, "oracle_topk: k must be >= 1");
+    if (kv_dtype != SPL_F32 && kv_dtype != SPL_BF16)
+        return fail(ctx, SPL_E_DIMENSION, "oracle_topk: unknown key dtype");
+    if (nvalid_div == 0) return fail(ctx, SPL_E_DIMENSION, "oracle_topk: nvalid_div == 0");
+    if (P == 0 || n_max == 0) return SPL_OK;
+    if (!q || !keys || !n_valid || !idx || !cnt)
+        return fail(ctx, SPL_E_STATE, "oracle_topk: null device pointer");
+    if (!logits) {
+        spl_status st = ensure_buffer(ctx, &ctx->dense_ws, &ctx->dense_ws_bytes,
+                                      (size_t)P * n_max * sizeof(float), false, S(stream),
+                                      "oracle_topk");
+        if (st) return st;
+        logits = static_cast<float*>(ctx->dense_ws);
+    }
+    spl_status st = causal_logits_launch(ctx, q, keys, kv_dtype, cap, d, P, n_valid, nvalid_div,
+                                         n_max, scale, logits, S(stream));
+    if (st) return st;
+    return top_k_launch(ctx, logits, 1, P, n_max, n_max, k, idx, S(stream), n_valid, nvalid_div,
+                        cnt);
+}
+
+spl_status spl_iou(spl_ctx* ctx, const uint32_t* a, const uint32_t* cnt_a, uint64_t a_stride,
+                   const uint32_t* b, const uint32_t* cnt_b, uint64_t b_stride, uint32_t P,
+                   double* out, void* stream) {
+    if (!ctx) return SPL_E_STATE;
+    if (P == 0) return SPL_OK;
+    if (!a || !cnt_a || !b || !cnt_b || !out) return fail(ctx, SPL_E_STATE, "iou: null device pointer");
+    return iou_launch(ctx, a, cnt_a, a_stride, b, cnt_b, b_stride, P, out, S(stream));
 }
 
 // ------------------------------------------------------------ K3

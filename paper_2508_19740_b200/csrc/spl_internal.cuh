@@ -37,6 +37,10 @@ struct spl_ctx {
     uint32_t* att_counters = nullptr;
     size_t att_counters_n = 0;
 
+    // dense retrieval (oracle_topk) logits [P][n_max] when the caller passes none.
+    void* dense_ws = nullptr;
+    size_t dense_ws_bytes = 0;
+
     // generic scratch for encoders / top_k keys.
     void* scratch = nullptr;
     size_t scratch_bytes = 0;

@@ -61,7 +61,16 @@ spl_status nxor_scores_launch(spl_ctx*, const uint32_t*, uint64_t, uint32_t, con
                               uint32_t, const uint32_t*, uint32_t, uint64_t, int32_t*, uint64_t,
                               cudaStream_t);
 spl_status top_k_launch(spl_ctx*, const void*, int, uint32_t, uint64_t, uint64_t, uint32_t,
-                        uint32_t*, cudaStream_t);
+                        uint32_t*, cudaStream_t, const uint32_t* n_valid = nullptr,
+                        uint32_t nvalid_div = 1, uint32_t* cnt = nullptr);
+// dense_retrieval.cu
+spl_status causal_logits_launch(spl_ctx*, const float* q, const void* keys, int kv_dtype,
+                                uint64_t cap, uint32_t d, uint32_t P, const uint32_t* n_valid,
+                                uint32_t nvalid_div, uint64_t n_max, float scale, float* logits,
+                                cudaStream_t);
+spl_status iou_launch(spl_ctx*, const uint32_t* a, const uint32_t* cnt_a, uint64_t a_stride,
+                      const uint32_t* b, const uint32_t* cnt_b, uint64_t b_stride, uint32_t P,
+                      double* out, cudaStream_t);
 // encode_exact.cu
 spl_status encode_exact_launch(spl_ctx*, const spl_hasher*, uint32_t, const EncJob*, int,
                                cudaStream_t);

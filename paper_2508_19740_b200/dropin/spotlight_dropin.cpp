@@ -537,6 +537,37 @@ RetrievalResult hash_topk(const AttentionInstance& inst, const AnyHasher& hasher
     return res;
 }
 
+// oracle_topk (attention_eval.cpp:121-135): exact dense logits + float top-k
+// on the GPU (spl_oracle_topk), every query against the shared key matrix.
+RetrievalResult oracle_topk(const AttentionInstance& inst, std::uint32_t k) {
+    inst.validate();
+    if (k == 0) throw DimensionError("oracle_topk: k must be >= 1");
+    const auto q = static_cast<std::uint32_t>(inst.num_queries());
+    const auto n = static_cast<std::uint32_t>(inst.cache_size());
+    const auto d = static_cast<std::uint32_t>(inst.keys.cols());
+    RetrievalResult res;
+    res.method = RetrievalMethod::oracle;
+    res.budget = k;
+    res.indices.resize(q);
+    if (q == 0) return res;
+    DevBuf dqv(inst.queries.data(), inst.queries.size() * 4);
+    DevBuf dkv(inst.keys.data(), inst.keys.size() * 4);
+    DevBuf dn(inst.causal_offsets.data(), static_cast<std::size_t>(q) * 4);
+    DevBuf di(static_cast<std::size_t>(q) * k * 4);
+    DevBuf dc(static_cast<std::size_t>(q) * 4);
+    check(spl_oracle_topk(ctx(), dqv.as<float>(), dkv.as<float>(), SPL_F32, 0, d, q,
+                          dn.as<std::uint32_t>(), 1, n, inst.scale, k, di.as<std::uint32_t>(),
+                          dc.as<std::uint32_t>(), nullptr, nullptr));
+    finish();
+    std::vector<std::uint32_t> idx(static_cast<std::size_t>(q) * k), cnt(q);
+    di.download(idx.data(), idx.size() * 4);
+    dc.download(cnt.data(), cnt.size() * 4);
+    for (std::uint32_t r = 0; r < q; ++r)
+        res.indices[r].assign(idx.begin() + static_cast<std::size_t>(r) * k,
+                              idx.begin() + static_cast<std::size_t>(r) * k + cnt[r]);
+    return res;
+}
+
 namespace {
 // Attention over explicit per-query row lists (own token already inserted):
 // one K4 launch in partial-free mode with own-token insertion disabled.

@@ -363,6 +363,8 @@ struct Ref {
     int (*sparse)(const float*, std::uint32_t, const float*, const float*, std::uint32_t,
                   std::uint32_t, float, const std::uint32_t*, const std::uint32_t*,
                   const std::uint64_t*, float*) = nullptr;
+    int (*oracle)(const float*, std::uint32_t, const float*, std::uint32_t, std::uint32_t, float,
+                  const std::uint32_t*, std::uint32_t, std::uint32_t*, std::uint32_t*) = nullptr;
     Ref() {
         const char* p = std::getenv("SPOTREF_SO");
         h = dlopen(p ? p : "oracle/_ref/libspotref.so", RTLD_NOW | RTLD_LOCAL);
@@ -370,8 +372,38 @@ struct Ref {
         mlp_forward = reinterpret_cast<decltype(mlp_forward)>(dlsym(h, "spotref_mlp_forward"));
         hash_topk = reinterpret_cast<decltype(hash_topk)>(dlsym(h, "spotref_hash_topk_mlp"));
         sparse = reinterpret_cast<decltype(sparse)>(dlsym(h, "spotref_sparse_attention"));
+        oracle = reinterpret_cast<decltype(oracle)>(dlsym(h, "spotref_oracle_topk"));
     }
 };
+
+TEST_CASE("oracle_topk: exact logits top-k, causal clamp, rejection; iou vs hash_topk") {
+    std::mt19937_64 eng(77);
+    const std::uint32_t n = 500, d = 64;
+    AttentionInstance inst = make_causal_instance(random_matrix(n, d, eng), random_matrix(n, d, eng),
+                                                  random_matrix(n, d, eng));
+    const RetrievalResult o = oracle_topk(inst, 32);
+    CHECK(o.method == RetrievalMethod::oracle);
+    CHECK(o.indices[0].size() == 1 && o.indices[0][0] == 0);  // query 0 sees one row
+    CHECK(o.indices[n - 1].size() == 32);
+    CHECK(std::is_sorted(o.indices[n - 1].begin(), o.indices[n - 1].end()));
+    CHECK_THROWS_AS(oracle_topk(inst, 0), DimensionError);
+    const MlpHasher h = mlp_gaussian_init(d, d, 128, 64.0f, 5);
+    const RetrievalResult r = hash_topk(inst, h, 32);
+    for (std::uint32_t q = 0; q < n; q += 50) {
+        const double v = iou(r.indices[q], o.indices[q]);
+        CHECK(v >= 0.0 && v <= 1.0);
+    }
+    static Ref ref;
+    if (!ref.h || !ref.oracle) return;
+    std::vector<std::uint32_t> ridx(static_cast<std::size_t>(n) * 32), rcnt(n);
+    CHECK(ref.oracle(inst.queries.data(), n, inst.keys.data(), n, d, inst.scale,
+                     inst.causal_offsets.data(), 32, ridx.data(), rcnt.data()) == 0);
+    bool same = true;
+    for (std::uint32_t q = 0; q < n; ++q)
+        same = same && o.indices[q] == std::vector<std::uint32_t>(ridx.begin() + q * 32,
+                                                                  ridx.begin() + q * 32 + rcnt[q]);
+    CHECK(same);
+}
 
 TEST_CASE("drop-in == reference: mlp_forward, hash_topk, sparse_attention") {
     static Ref ref;
