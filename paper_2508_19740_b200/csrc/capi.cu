@@ -16,6 +16,33 @@
 
 using namespace spl;
 
+namespace spl {
+bool pdl_enabled() {
+    // off by default: measured on B200 it cost more than it hid (config-3
+    // retrieval 59.2 -> 61.9 us, config-2 decode step 58.1 -> 59.5 us;
+    // config-4 step 689 -> 684 us). SPL_PDL=1 turns it on.
+    static const bool on = [] {
+        const char* e = getenv("SPL_PDL");
+        return e && *e == '1';
+    }();
+    return on;
+}
+cudaError_t launch_pdl(const void* fn, dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                       void** args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    return cudaLaunchKernelExC(&cfg, fn, args);
+}
+}  // namespace spl
+
 namespace {
 inline cudaStream_t S(void* s) { return static_cast<cudaStream_t>(s); }
 constexpr float kLog2e = 1.4426950408889634f;

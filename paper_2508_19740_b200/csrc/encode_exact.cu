@@ -287,6 +287,7 @@ __global__ void __cluster_dims__(kCS, 1, 1) __launch_bounds__(kEncThreads)
     float* xs = sw2 + (size_t)Wc * act_dim * 32;
     float* a1 = xs + (size_t)kVT * d;
 
+    pdl_trigger();
     if (tid == 0) {
         asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"(smem_u32(&s_bar)));
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -297,6 +298,9 @@ __global__ void __cluster_dims__(kCS, 1, 1) __launch_bounds__(kEncThreads)
             bulk_g2s(sw1, prm.w1s + ((size_t)head * kCS + rank) * d * hs, b1n, &s_bar);
         bulk_g2s(sw2, prm.w2w + ((size_t)head * W + rank * Wc) * act_dim * 32, b2n, &s_bar);
     }
+    // the weights stream in while the previous kernel of the stream finishes;
+    // inputs, caches and code rows are touched only after it has completed
+    pdl_wait();
     cluster_sync_relaxed();  // peers' shared memory is live before any DSMEM store
     uint32_t a1_peer[kCS];
 #pragma unroll
@@ -479,7 +483,9 @@ spl_status encode_cluster_launch(spl_ctx* ctx, const spl_hasher* hs, uint32_t B,
     const uint32_t groups = std::max<uint32_t>(
         1, std::min<uint32_t>(ntiles, (uint32_t)(2 * ctx->num_sms) / (kCS * hs->H)));
     dim3 grid(groups * kCS, hs->H, njobs);
-    k1_encode_cluster<<<grid, kEncThreads, smem, s>>>(prm);
+    void* args[] = {&prm};
+    SPL_CUDA_TRY(ctx, launch_pdl(reinterpret_cast<const void*>(&k1_encode_cluster), grid,
+                                 dim3(kEncThreads), smem, s, args));
     return after_launch(ctx, "k1_encode_cluster");
 }
 

@@ -103,6 +103,12 @@ constexpr uint64_t kSegsPerCta = 1;
 // ~128 KB of loads in flight per SM at 512 (4 x 128) or 768 threads/SM
 constexpr int kU = kThreads == 128 ? 4 : 2;
 
+__device__ __forceinline__ uint64_t gtimer() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
 // ------------------------------------------------------------ block scans
 __device__ __forceinline__ uint64_t warp_incl_scan_u64(uint64_t v) {
     const int lane = threadIdx.x & 31;
@@ -614,7 +620,8 @@ __device__ void select_rows(const ScoreT* sc, uint64_t a0, uint64_t r0, uint64_t
 // masked with 0x01010101 << i and OR-ed (IADD, SHF, LOP3), so bit 8b + i of
 // a vector's mask is row 4b + i.
 __device__ void select_rows_t8(const uint8_t* sc, uint64_t a0, uint64_t r0, uint64_t r1,
-                               uint32_t T, uint32_t take, uint32_t* out, uint64_t* s_warp) {
+                               uint32_t T, uint32_t take, uint32_t* out, uint64_t* s_warp,
+                               uint64_t* tr = nullptr) {
     constexpr int NV = 11;
     constexpr int CH = 16 * NV;  // rows per thread per round
     // T == 0: every row is >= T (x + 128 would carry for x = 128);
@@ -659,8 +666,10 @@ __device__ void select_rows_t8(const uint8_t* sc, uint64_t a0, uint64_t r0, uint
             gt += __popc(gm[v]);
             eq += __popc(em[v]);
         }
+        if (tr && threadIdx.x == 0) { tr[9] = gtimer(); tr[13] = clock64(); }
         uint64_t tot;
         const uint64_t ex = block_excl_scan_u64(((uint64_t)eq << 32) | gt, s_warp, tot);
+        if (tr && threadIdx.x == 0) { tr[10] = gtimer(); tr[14] = clock64(); }
 #if defined(K3_SEL_EXP) && K3_SEL_EXP == 2
         if (ex == 0x123456789ull) out[0] = gm[0] ^ em[NV - 1];
         return;
@@ -709,6 +718,7 @@ __device__ void select_rows_t8(const uint8_t* sc, uint64_t a0, uint64_t r0, uint
         carry_gt += (uint32_t)tot;
         carry_eq += (uint32_t)(tot >> 32);
     }
+    if (tr && threadIdx.x == 0) { tr[11] = gtimer(); tr[15] = clock64(); }
 }
 
 // ------------------------------------------------------------------ scan
@@ -716,11 +726,6 @@ __device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
     uint32_t v;
     asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
     return v;
-}
-__device__ __forceinline__ uint64_t gtimer() {
-    uint64_t t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    return t;
 }
 // Spin (one thread) until *p >= need. A wait that outlives 2 s means some
 // CTA of the problem was never scheduled: flag SPL_DEV_ERR_STALL and give up
@@ -786,9 +791,11 @@ __global__ void __launch_bounds__(kThreads, 3) k3_scan(K3Params prm) {
     const K3Geom& g = prm.g;
 
     // zero the counters once (flush_priv re-zeroes them)
+    pdl_trigger();
     if constexpr (PRIV)
         for (uint32_t i = tid; i < priv_bytes / 16; i += kThreads)
             reinterpret_cast<uint4*>(priv)[i] = make_uint4(0, 0, 0, 0);
+    pdl_wait();
 
     for (uint32_t seg = blockIdx.x; seg < g.G; seg += gridDim.x) {
     const uint64_t g0 = (uint64_t)seg * g.S;
@@ -885,7 +892,7 @@ __global__ void __launch_bounds__(kThreads, 3) k3_scan(K3Params prm) {
 // Shared memory stays <= 196 KB/SM: above that the driver must choose the
 // 228 KB carve-out and LDG streaming loses ~16% (tools/read_bw.cu).
 #define K3_STAMP(i) \
-    if (prm.trace && threadIdx.x == 0) prm.trace[blockIdx.x * 8 + (i)] = gtimer()
+    if (prm.trace && threadIdx.x == 0) prm.trace[blockIdx.x * 16 + (i)] = gtimer()
 
 template <int W, typename ScoreT>
 __global__ void __launch_bounds__(kThreads, 3) k3_fused(K3Params prm) {
@@ -908,7 +915,7 @@ __global__ void __launch_bounds__(kThreads, 3) k3_fused(K3Params prm) {
     if (prm.trace && tid == 0) {
         uint32_t smid;
         asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
-        prm.trace[(uint64_t)blockIdx.x * 8 + 6] = smid;
+        prm.trace[(uint64_t)blockIdx.x * 16 + 6] = smid;
     }
     // The readiness waits below need every CTA of a problem resident: the
     // plan keeps G <= SMs x CTAs/SM (occupancy API) and the launch is a plain
@@ -918,8 +925,10 @@ __global__ void __launch_bounds__(kThreads, 3) k3_fused(K3Params prm) {
     // device error. (Arrival tickets would remove the requirement but their
     // single-address atomic delays the last CTAs' start by ~2 us.)
     const uint32_t seg = blockIdx.x;
+    pdl_trigger();
     for (uint32_t i = tid; i < priv_bytes / 16; i += kThreads)
         reinterpret_cast<uint4*>(priv)[i] = make_uint4(0, 0, 0, 0);
+    pdl_wait();  // query codes / appended code rows come from the previous kernel
 
     const uint64_t g0 = (uint64_t)seg * g.S;
     const uint64_t g1 = min(g0 + g.S, g.total);
@@ -1053,9 +1062,12 @@ __global__ void __launch_bounds__(kThreads, 3) k3_fused(K3Params prm) {
         const uint64_t left = quota > eq_before ? quota - eq_before : 0;
         const uint32_t take = (uint32_t)(eq_mine < left ? eq_mine : left);
         const uint64_t off = gt_before + (eq_before < quota ? eq_before : quota);
+        K3_STAMP(8);
+        if (prm.trace && threadIdx.x == 0) prm.trace[blockIdx.x * 16 + 12] = clock64();
         if constexpr (sizeof(ScoreT) == 1)
             select_rows_t8(reinterpret_cast<const uint8_t*>(sc), a0, r0, r1, T, take,
-                           prm.idx_out + (uint64_t)p * prm.idx_stride + off, s_warp);
+                           prm.idx_out + (uint64_t)p * prm.idx_stride + off, s_warp,
+                           prm.trace ? prm.trace + (uint64_t)blockIdx.x * 16 : nullptr);
         else
             select_rows<ScoreT, false>(sc, a0, r0, r1, T, take,
                                        prm.idx_out + (uint64_t)p * prm.idx_stride + off, s_warp);
@@ -1087,6 +1099,8 @@ __global__ void __launch_bounds__(kThreads, 3) k3_select(K3Params prm, uint32_t*
                                                       uint64_t idx_stride) {
     __shared__ uint64_t s_warp[kThreads / 32 + 1];
     const K3Geom& g = prm.g;
+    pdl_trigger();
+    pdl_wait();
     const uint64_t g0 = (uint64_t)blockIdx.x * g.S;
     const uint64_t g1 = min(g0 + g.S, g.total);
     for (uint32_t p = (uint32_t)(g0 / g.pstride); p < g.P && (uint64_t)p * g.pstride < g1; ++p) {
@@ -1399,16 +1413,17 @@ spl_status validate_common(spl_ctx* ctx, const char* who, const uint32_t* codes,
 spl_status launch_scan(spl_ctx* ctx, const K3Plan& pl, const K3Params& prm, cudaStream_t s) {
     const void* fn = pick_scan(pl, prm.L);
     void* args[] = {const_cast<K3Params*>(&prm)};
-    SPL_CUDA_TRY(ctx, cudaLaunchKernel(fn, dim3(pl.grid), dim3(kThreads), args, pl.smem, s));
+    SPL_CUDA_TRY(ctx, launch_pdl(fn, dim3(pl.grid), dim3(kThreads), pl.smem, s, args));
     return after_launch(ctx, "k3_scan");
 }
 
 spl_status launch_select(spl_ctx* ctx, const K3Plan& pl, const K3Params& prm, uint32_t* idx,
                          uint64_t idx_stride, cudaStream_t s) {
-    if (pl.score_bytes == 1)
-        k3_select<uint8_t><<<pl.g.G, kThreads, 0, s>>>(prm, idx, idx_stride);
-    else
-        k3_select<uint16_t><<<pl.g.G, kThreads, 0, s>>>(prm, idx, idx_stride);
+    const void* fn = pl.score_bytes == 1 ? reinterpret_cast<const void*>(&k3_select<uint8_t>)
+                                         : reinterpret_cast<const void*>(&k3_select<uint16_t>);
+    K3Params p2 = prm;
+    void* args[] = {&p2, &idx, &idx_stride};
+    SPL_CUDA_TRY(ctx, launch_pdl(fn, dim3(pl.g.G), dim3(kThreads), 0, s, args));
     return after_launch(ctx, "k3_select");
 }
 
@@ -1478,43 +1493,61 @@ spl_status hamming_topk_impl(spl_ctx* ctx, const uint32_t* codes, uint64_t strid
             const uint32_t G = fp.pl.g.G;
             const char* tr = getenv("SPL_K3_TRACE");
             uint64_t* dtrace = nullptr;
-            if (tr && *tr && !stream_capturing(s)) SPL_CUDA_TRY(ctx, cudaMalloc(&dtrace, (size_t)G * 8 * 8));
+            if (tr && *tr && !stream_capturing(s)) {
+                SPL_CUDA_TRY(ctx, cudaMalloc(&dtrace, (size_t)G * 16 * 8));
+                SPL_CUDA_TRY(ctx, cudaMemsetAsync(dtrace, 0, (size_t)G * 16 * 8, s));
+            }
             prm.trace = dtrace;
             void* args[] = {&prm};
             const char* coop = getenv("SPL_K3_COOP");
             if (coop && *coop == '1')
                 SPL_CUDA_TRY(ctx, cudaLaunchCooperativeKernel(fp.fn, dim3(G), dim3(kThreads), args, fp.smem, s));
             else
-                SPL_CUDA_TRY(ctx, cudaLaunchKernel(fp.fn, dim3(G), dim3(kThreads), args, fp.smem, s));
+                SPL_CUDA_TRY(ctx, launch_pdl(fp.fn, dim3(G), dim3(kThreads), fp.smem, s, args));
             st = after_launch(ctx, "k3_fused");
             if (dtrace) {
-                std::vector<uint64_t> h((size_t)G * 8);
+                // stamps per CTA (16 slots): 0 start, 1 stream end, 2 (= 1), 3 T known,
+                // 4 prefix, 5 select end, 6 smid, 8 own record read, 9 select counts,
+                // 10 select scan, 11 select emitted
+                constexpr int kSlots = 16;
+                const int cols[] = {0, 1, 3, 4, 8, 9, 10, 11, 5};
+                const char* names = "start stream thresh prefix rec counts scan emit end";
+                std::vector<uint64_t> h((size_t)G * kSlots);
                 cudaStreamSynchronize(s);
                 cudaMemcpy(h.data(), dtrace, h.size() * 8, cudaMemcpyDeviceToHost);
                 cudaFree(dtrace);
                 uint64_t t0 = ~0ull;
-                for (uint32_t i = 0; i < G; ++i) t0 = std::min(t0, h[i * 8]);
-                double mx[6] = {0}, mean[6] = {0};
+                for (uint32_t i = 0; i < G; ++i) t0 = std::min(t0, h[i * kSlots]);
+                double mx[9] = {0}, mean[9] = {0};
                 for (uint32_t i = 0; i < G; ++i)
-                    for (int j = 0; j < 6; ++j) {
-                        const double v = (double)(h[i * 8 + j] - t0) / 1000.0;
+                    for (int j = 0; j < 9; ++j) {
+                        const uint64_t raw = h[i * kSlots + cols[j]];
+                        const double v = raw ? (double)(raw - t0) / 1000.0 : 0.0;
                         mx[j] = std::max(mx[j], v);
                         mean[j] += v / G;
                     }
-                fprintf(stderr, "k3_fused trace G=%u S=%llu [start, stream, barrier, thresh, prefix, select] mean:",
-                        G, (unsigned long long)fp.pl.g.S);
-                for (int j = 0; j < 6; ++j) fprintf(stderr, " %.1f", mean[j]);
+                fprintf(stderr, "k3_fused trace G=%u S=%llu [%s] mean:", G,
+                        (unsigned long long)fp.pl.g.S, names);
+                for (int j = 0; j < 9; ++j) fprintf(stderr, " %.1f", mean[j]);
                 fprintf(stderr, "  max:");
-                for (int j = 0; j < 6; ++j) fprintf(stderr, " %.1f", mx[j]);
-                fprintf(stderr, " us\n");
+                for (int j = 0; j < 9; ++j) fprintf(stderr, " %.1f", mx[j]);
+                fprintf(stderr, " us");
+                double cyc[3] = {0, 0, 0};
+                for (uint32_t i = 0; i < G; ++i)
+                    for (int j = 0; j < 3; ++j)
+                        cyc[j] += (double)(int64_t)(h[i * kSlots + 13 + j] - h[i * kSlots + 12 + j]) / G;
+                fprintf(stderr, "  select thread-0 cycles: counts %.0f scan %.0f emit %.0f\n", cyc[0], cyc[1],
+                        cyc[2]);
                 if (*tr == '2') {  // per-CTA dump: cta, smid, stamps (us)
                     FILE* f = fopen("gpurun_out/k3_trace.csv", "w");
                     if (f) {
-                        fprintf(f, "cta,smid,seg,start,stream,barrier,thresh,prefix,select\n");
+                        fprintf(f, "cta,smid,start,stream,thresh,prefix,rec,counts,scan,emit,end\n");
                         for (uint32_t i = 0; i < G; ++i) {
-                            fprintf(f, "%u,%llu,%llu", i, (unsigned long long)h[i * 8 + 6],
-                                    (unsigned long long)h[i * 8 + 7]);
-                            for (int j = 0; j < 6; ++j) fprintf(f, ",%.3f", (double)(h[i * 8 + j] - t0) / 1000.0);
+                            fprintf(f, "%u,%llu", i, (unsigned long long)h[i * kSlots + 6]);
+                            for (int j = 0; j < 9; ++j) {
+                                const uint64_t raw = h[i * kSlots + cols[j]];
+                                fprintf(f, ",%.3f", raw ? (double)(raw - t0) / 1000.0 : 0.0);
+                            }
                             fprintf(f, "\n");
                         }
                         fclose(f);

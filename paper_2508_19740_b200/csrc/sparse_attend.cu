@@ -143,6 +143,8 @@ __global__ void __launch_bounds__(kAttThreads) k4_sparse_attend(AttParams prm) {
     __shared__ uint32_t s_last;
     const uint32_t p = blockIdx.y, split = blockIdx.x;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    pdl_trigger();
+    pdl_wait();  // the row lists (and the appended own row) come from the previous kernels
 
     for (int i = tid; i < D; i += kAttThreads) q_s[i] = prm.q[(uint64_t)p * D + i] * prm.qscale;
 
@@ -416,7 +418,7 @@ spl_status sparse_attend_launch(spl_ctx* ctx, AttParams prm, uint32_t kmax, int 
     prm.partials = ctx->att_ws;
     prm.counters = ctx->att_counters;
     void* args[] = {&prm};
-    SPL_CUDA_TRY(ctx, cudaLaunchKernel(fn, dim3(nsplit, prm.P), dim3(kAttThreads), args, 0, s));
+    SPL_CUDA_TRY(ctx, launch_pdl(fn, dim3(nsplit, prm.P), dim3(kAttThreads), 0, s, args));
     return after_launch(ctx, "k4_sparse_attend");
 }
 

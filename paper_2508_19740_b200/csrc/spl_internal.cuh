@@ -90,6 +90,24 @@ inline spl_status after_launch(spl_ctx* ctx, const char* name) {
     return SPL_OK;
 }
 
+// Programmatic dependent launch (PDL) along the decode chain K1 -> K3 -> K4
+// -> K1 ...: each kernel lets its dependent launch as soon as all of its own
+// CTAs are running (pdl_trigger at entry — the dependent is released only
+// when every CTA of this grid has triggered, so co-residency assumptions of
+// this grid are never undercut), and waits for its predecessor's completion
+// and memory (pdl_wait) right before it first reads or writes shared data.
+// Prologues (weight TMA, counter zeroing) overlap the predecessor's tail.
+// Without the launch attribute both are no-ops. Opt-in (SPL_PDL=1): see
+// pdl_enabled() for the measurement that keeps it off by default.
+__device__ __forceinline__ void pdl_trigger() {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+bool pdl_enabled();
+cudaError_t launch_pdl(const void* fn, dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                       void** args);
+
 inline bool stream_capturing(cudaStream_t s) {
     cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
     if (cudaStreamIsCapturing(s, &st) != cudaSuccess) return false;
