@@ -100,6 +100,20 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
             : "r"(smem_u32(bar)), "r"(parity)
             : "memory");
 }
+// Same with a suspend-time hint: the waiting warp sleeps until the phase
+// completes (or ~hint ns pass) instead of re-issuing try_wait. In the
+// warp-specialised kernel the spinning of the MMA / producer / epilogue
+// waits was ~20 % of all issued instructions, taking issue slots from the
+// epilogue warps on the same SMSP.
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+    uint32_t done = 0;
+    while (!done)
+        asm volatile(
+            "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3; selp.u32 %0, 1, 0, p; }"
+            : "=r"(done)
+            : "r"(smem_u32(bar)), "r"(parity), "r"(1000000u)
+            : "memory");
+}
 __device__ __forceinline__ void fence_before() {
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
 }
@@ -531,8 +545,8 @@ __global__ void __launch_bounds__(kWsThreads, 1)
             // problem (consecutive problems have consecutive heads; H = 1
             // reloads the same head, harmless)
             auto g2 = [&](uint32_t j, bool ends_head) {
-                mbar_wait(&bar[kA1Full + (j & 1)], (j >> 1) & 1u);
-                if (j >= 1) mbar_wait(&bar[kD2Empty], (j - 1) & 1u);
+                mbar_wait_sleep(&bar[kA1Full + (j & 1)], (j >> 1) & 1u);
+                if (j >= 1) mbar_wait_sleep(&bar[kD2Empty], (j - 1) & 1u);
                 fence_after();
                 gemm_k128(tmem + 256u, smem_u32(sA1 + (j & 1) * XB), smem_u32(sW2), L);
                 umma_commit(&bar[kA1Empty + (j & 1)]);
@@ -547,11 +561,11 @@ __global__ void __launch_bounds__(kWsThreads, 1)
                     // the previous head's last GEMM2 goes first: the producer
                     // may only replace W1/W2 once it has completed
                     if (i >= 1) g2(i - 1, true);
-                    mbar_wait(&bar[kWFull], nw & 1u);
+                    mbar_wait_sleep(&bar[kWFull], nw & 1u);
                     ++nw;
                 }
-                mbar_wait(&bar[kXFull + (i & 1)], (i >> 1) & 1u);
-                if (i >= 2) mbar_wait(&bar[kD1Empty + (i & 1)], ((i - 2) >> 1) & 1u);
+                mbar_wait_sleep(&bar[kXFull + (i & 1)], (i >> 1) & 1u);
+                if (i >= 2) mbar_wait_sleep(&bar[kD1Empty + (i & 1)], ((i - 2) >> 1) & 1u);
                 fence_after();
                 gemm_k128(tmem + (i & 1) * 128u, smem_u32(sX + (i & 1) * XB), smem_u32(sW1), kTcK);
                 umma_commit(&bar[kXEmpty + (i & 1)]);
@@ -571,7 +585,7 @@ __global__ void __launch_bounds__(kWsThreads, 1)
             for (uint32_t i = 0; i < n; ++i) {
                 const uint32_t h = pos.head;
                 if (i == 0 || prev_ends) {
-                    if (nw > 0) mbar_wait(&bar[kWEmpty], (nw - 1) & 1u);
+                    if (nw > 0) mbar_wait_sleep(&bar[kWEmpty], (nw - 1) & 1u);
                     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
                                      smem_u32(&bar[kWFull])),
                                  "r"(XB + L * 256u)
@@ -580,7 +594,7 @@ __global__ void __launch_bounds__(kWsThreads, 1)
                     bulk_g2s(sW2, prm.w2_tc + (uint64_t)h * L * 256u, L * 256u, &bar[kWFull]);
                     ++nw;
                 }
-                if (i >= 2) mbar_wait(&bar[kXEmpty + (i & 1)], ((i - 2) >> 1) & 1u);
+                if (i >= 2) mbar_wait_sleep(&bar[kXEmpty + (i & 1)], ((i - 2) >> 1) & 1u);
                 tma_x(&tmap, sX + (i & 1) * XB, &bar[kXFull + (i & 1)],
                       pos.bh * prm.m + (uint64_t)pos.mb * kTcTileM);
                 prev_ends = pos.last_of_head();
@@ -603,8 +617,8 @@ __global__ void __launch_bounds__(kWsThreads, 1)
                 asm volatile("bar.sync 1, 256;" ::: "memory");
                 cur_head = pos.head;
             }
-            mbar_wait(&bar[kD1Full + (i & 1)], (i >> 1) & 1u);
-            if (i >= 2) mbar_wait(&bar[kA1Empty + (i & 1)], ((i - 2) >> 1) & 1u);
+            mbar_wait_sleep(&bar[kD1Full + (i & 1)], (i >> 1) & 1u);
+            if (i >= 2) mbar_wait_sleep(&bar[kA1Empty + (i & 1)], ((i - 2) >> 1) & 1u);
             fence_after();
             // this thread's half row of A1: K block ch (64 columns), row `row`;
             // 16-byte chunk j of the row sits at chunk j ^ (row % 8)
@@ -657,7 +671,7 @@ __global__ void __launch_bounds__(kWsThreads, 1)
         for (uint32_t i = 0; i < n; ++i, pos.advance()) {
             const uint64_t bh = pos.bh;
             const uint32_t grow = pos.mb * kTcTileM + row;
-            mbar_wait(&bar[kD2Full], i & 1u);
+            mbar_wait_sleep(&bar[kD2Full], i & 1u);
             fence_after();
             // column j -> word j % W, bit 31 - j / W: feeding the sign bits of
             // columns w, w + W, w + 2W, ... into word w with a funnel shift
@@ -665,7 +679,10 @@ __global__ void __launch_bounds__(kWsThreads, 1)
             uint32_t neg[W];
 #pragma unroll
             for (uint32_t w = 0; w < W; ++w) neg[w] = 0u;
-            float sum4[4] = {0.0f, 0.0f, 0.0f, 0.0f};  // non-finite check, 4 chains
+            // non-finite input: any NaN / Inf in a key row reaches every z1
+            // column (x * w, NaN * 0 = NaN), every a1 and every z2 column, so
+            // column 0 of D2 decides the row (one check instead of L)
+            float z0 = 0.0f;
 #pragma unroll
             for (uint32_t c0 = 0; c0 < L; c0 += 32) {
                 uint32_t r[2][16];
@@ -675,7 +692,7 @@ __global__ void __launch_bounds__(kWsThreads, 1)
 #pragma unroll
                 for (uint32_t e = 0; e < 32; ++e) {
                     const float z = __uint_as_float(r[e >> 4][e & 15]);
-                    sum4[e & 3] += z;
+                    if (c0 == 0 && e == 0) z0 = z;
                     const uint32_t u = __float_as_uint(z + 0.0f);
                     neg[(c0 + e) % W] = __funnelshift_l(u, neg[(c0 + e) % W], 1);
                 }
@@ -683,8 +700,7 @@ __global__ void __launch_bounds__(kWsThreads, 1)
             fence_before();
             mbar_arrive(&bar[kD2Empty]);
             if (grow < prm.m) {
-                if (!isfinite((sum4[0] + sum4[1]) + (sum4[2] + sum4[3])))
-                    raise_dev_err(prm.dev_err, SPL_DEV_ERR_NUMERIC);
+                if (!isfinite(z0)) raise_dev_err(prm.dev_err, SPL_DEV_ERR_NUMERIC);
                 uint32_t* dst = prm.codes + ((bh * prm.m) + grow) * W;
                 if constexpr (W >= 4) {
 #pragma unroll

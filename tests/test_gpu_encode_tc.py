@@ -197,13 +197,18 @@ def test_encode_tc_non_finite_raises(ctx):
         ctx.check_device_error()
 
 
-def test_encode_tc_non_finite_bf16_raises(ctx):
+@pytest.mark.parametrize("bad", [float("nan"), float("inf"), float("-inf")])
+@pytest.mark.parametrize("L", [128, 256])
+def test_encode_tc_non_finite_bf16_raises(ctx, bad, L):
+    """The warp-specialised kernel checks one z2 column per row: a NaN / Inf
+    key element reaches every column (also through a zero weight row)."""
     rng = np.random.default_rng(7)
-    w1, b1, w2 = mlp_weights(rng, 1, 128, 128, 128)
+    w1, b1, w2 = mlp_weights(rng, 1, 128, 128, L)
+    w1[0, 5, :] = 0.0  # the bad feature meets a zero weight row
     hs = ctx.hasher(w1, b1, w2)
     x = torch.zeros((1, 1, 130, 128), dtype=torch.bfloat16, device=DEV)
-    x[0, 0, 3, 5] = float("nan")
-    codes = torch.zeros((1, 1, 130, 4), dtype=torch.int32, device=DEV)
+    x[0, 0, 129, 5] = bad
+    codes = torch.zeros((1, 1, 130, L // 32), dtype=torch.int32, device=DEV)
     hs.encode_tc(x, capi.SPL_BF16, 1, 130, codes)
     torch.cuda.synchronize()
     with pytest.raises(capi.NumericError):
