@@ -545,8 +545,8 @@ __global__ void __launch_bounds__(kWsThreads, 1)
             // problem (consecutive problems have consecutive heads; H = 1
             // reloads the same head, harmless)
             auto g2 = [&](uint32_t j, bool ends_head) {
-                mbar_wait_sleep(&bar[kA1Full + (j & 1)], (j >> 1) & 1u);
-                if (j >= 1) mbar_wait_sleep(&bar[kD2Empty], (j - 1) & 1u);
+                mbar_wait(&bar[kA1Full + (j & 1)], (j >> 1) & 1u);
+                if (j >= 1) mbar_wait(&bar[kD2Empty], (j - 1) & 1u);
                 fence_after();
                 gemm_k128(tmem + 256u, smem_u32(sA1 + (j & 1) * XB), smem_u32(sW2), L);
                 umma_commit(&bar[kA1Empty + (j & 1)]);
@@ -561,11 +561,11 @@ __global__ void __launch_bounds__(kWsThreads, 1)
                     // the previous head's last GEMM2 goes first: the producer
                     // may only replace W1/W2 once it has completed
                     if (i >= 1) g2(i - 1, true);
-                    mbar_wait_sleep(&bar[kWFull], nw & 1u);
+                    mbar_wait(&bar[kWFull], nw & 1u);
                     ++nw;
                 }
-                mbar_wait_sleep(&bar[kXFull + (i & 1)], (i >> 1) & 1u);
-                if (i >= 2) mbar_wait_sleep(&bar[kD1Empty + (i & 1)], ((i - 2) >> 1) & 1u);
+                mbar_wait(&bar[kXFull + (i & 1)], (i >> 1) & 1u);
+                if (i >= 2) mbar_wait(&bar[kD1Empty + (i & 1)], ((i - 2) >> 1) & 1u);
                 fence_after();
                 gemm_k128(tmem + (i & 1) * 128u, smem_u32(sX + (i & 1) * XB), smem_u32(sW1), kTcK);
                 umma_commit(&bar[kXEmpty + (i & 1)]);
