@@ -96,6 +96,7 @@ constexpr size_t kFastCarveBytes = 196 * 1024;
 // two-pass scan segments per CTA: 1 measured best at config 4 (each segment
 // boundary costs a pipeline drain + flush; 2/4/8 per CTA: +1/+4/+11%)
 constexpr uint64_t kSegsPerCta = 1;
+#define K3_SEL_SCRATCH_BYTES ((size_t)kThreads * 11 * 4)  // select_rows_t8 masks
 #ifndef K3_EXP
 #define K3_EXP 0  // timing experiments only (tools/k3_exp.sh); 0 = product
 #endif
@@ -619,9 +620,11 @@ __device__ void select_rows(const ScoreT* sc, uint64_t a0, uint64_t r0, uint64_t
 // Offsets are 32-bit, relative to a0. Flags: per word (w + c) >> (7 - i)
 // masked with 0x01010101 << i and OR-ed (IADD, SHF, LOP3), so bit 8b + i of
 // a vector's mask is row 4b + i.
+// scratch: kThreads x NV words of shared memory (the private counters,
+// free once the stream is over).
 __device__ void select_rows_t8(const uint8_t* sc, uint64_t a0, uint64_t r0, uint64_t r1,
                                uint32_t T, uint32_t take, uint32_t* out, uint64_t* s_warp,
-                               uint64_t* tr = nullptr) {
+                               uint32_t* scratch, uint64_t* tr = nullptr) {
     constexpr int NV = 11;
     constexpr int CH = 16 * NV;  // rows per thread per round
     // T == 0: every row is >= T (x + 128 would carry for x = 128);
@@ -675,44 +678,44 @@ __device__ void select_rows_t8(const uint8_t* sc, uint64_t a0, uint64_t r0, uint
         return;
 #endif
         if (gt | eq) {
-            const uint32_t eq_before = carry_eq + (uint32_t)(ex >> 32);
-            uint32_t pos = carry_gt + (uint32_t)ex + (eq_before < take ? eq_before : take);
-            if (eq_before + eq <= take || eq_before >= take) {
-                // all of this thread's ties are taken, or none
-                const bool ties = eq_before < take;
+            uint32_t eb = carry_eq + (uint32_t)(ex >> 32);  // ties before this thread's rows
+            uint32_t pos = carry_gt + (uint32_t)ex + (eb < take ? eb : take);
+            // final per-vector masks (ties trimmed where the quota runs out)
+            // go to this thread's scratch row; one flat loop then walks the
+            // set bits of the non-empty vectors only — small code (the
+            // unrolled per-vector loops missed the instruction cache) and
+            // fewer divergent iterations per warp
+            uint32_t nz = 0;
 #pragma unroll
-                for (int v = 0; v < NV; ++v) {
-                    uint32_t m = ties ? (gm[v] | em[v]) : gm[v];
-                    const uint32_t at = rb + my + 16u * v;
-                    while (m) {
-                        const uint32_t b = __ffs(m) - 1;
-                        m &= m - 1;
+            for (int v = 0; v < NV; ++v) {
+                uint32_t e = em[v];
+                const uint32_t ne = __popc(e);
+                if (eb >= take) {
+                    e = 0;
+                } else if (eb + ne > take) {
+                    for (uint32_t drop = eb + ne - take; drop; --drop) e &= ~(0x80000000u >> __clz(e));
+                }
+                eb += ne;
+                const uint32_t m = gm[v] | e;
+                scratch[(uint32_t)tid * NV + v] = m;
+                nz |= (m != 0u ? 1u : 0u) << v;
+            }
+            const uint32_t rowb = rb + my;
+            uint32_t v = 0, m = 0;
+            while (nz | m) {
+                if (m == 0u) {
+                    v = __ffs(nz) - 1;
+                    nz &= nz - 1;
+                    m = scratch[(uint32_t)tid * NV + v];
+                }
+                const uint32_t bb = __ffs(m) - 1;
+                m &= m - 1;
 #if defined(K3_SEL_EXP) && K3_SEL_EXP == 1
-                        if (b == 77) out[pos] = at;
-                        pos++;
+                if (bb == 77) out[pos] = rowb;
+                pos++;
 #else
-                        out[pos++] = at + 4 * (b >> 3) + (b & 7);
+                out[pos++] = rowb + 16u * v + 4 * (bb >> 3) + (bb & 7);
 #endif
-                    }
-                }
-            } else {  // the thread where the tie quota runs out
-                uint32_t eb = eq_before;
-#pragma unroll
-                for (int v = 0; v < NV; ++v) {
-                    uint32_t m = gm[v] | em[v];
-                    const uint32_t at = rb + my + 16u * v;
-                    while (m) {
-                        const uint32_t b = __ffs(m) - 1;
-                        m &= m - 1;
-                        const uint32_t row = at + 4 * (b >> 3) + (b & 7);
-                        if ((gm[v] >> b) & 1u) {
-                            out[pos++] = row;
-                        } else {
-                            if (eb < take) out[pos++] = row;
-                            ++eb;
-                        }
-                    }
-                }
             }
         }
         carry_gt += (uint32_t)tot;
@@ -903,7 +906,10 @@ __global__ void __launch_bounds__(kThreads, 3) k3_fused(K3Params prm) {
     const uint32_t bins = L + 1;
     const uint32_t lo = prm.hist_lo;        // counted window [lo, L]
     const uint32_t wbins = bins - lo;
-    const size_t priv_bytes = ((size_t)wbins * kThreads + 15) & ~size_t(15);
+    // the private counters double as select_rows_t8's scratch afterwards
+    const size_t priv_counters = ((size_t)wbins * kThreads + 15) & ~size_t(15);
+    const size_t priv_bytes =
+        priv_counters > K3_SEL_SCRATCH_BYTES ? priv_counters : K3_SEL_SCRATCH_BYTES;
     const size_t hist_bytes = (((size_t)(bins + 1) * 4) + 15) & ~size_t(15);
     uint8_t* priv = smem;
     uint32_t* hist32 = reinterpret_cast<uint32_t*>(smem + priv_bytes);                // [bins + 1]
@@ -1000,6 +1006,7 @@ __global__ void __launch_bounds__(kThreads, 3) k3_fused(K3Params prm) {
         if (tid == 0) wait_count(prm.counters + p, nseg, prm.dev_err);
         __syncthreads();
         uint32_t* tot = prm.tot_hist + (uint64_t)p * prm.tot_stride;
+        const uint32_t c0 = seg_first(g, p);
         // window bins only: CTAs that take the fallback below add the low
         // bins to `tot` while others may still be reading it, and every CTA
         // of the problem must reach the same decision
@@ -1036,7 +1043,6 @@ __global__ void __launch_bounds__(kThreads, 3) k3_fused(K3Params prm) {
             problem_threshold(tot, L, kk, s_cum, s_warp, &s_T, T, quota);
         }
         K3_STAMP(3);
-        const uint32_t c0 = seg_first(g, p);
         if (tid == 0 && seg == c0) prm.cnt_out[p] = kk;
         if (r0 >= r1) continue;
         if (T == SPL_PLAN_SKIP) continue;
@@ -1067,6 +1073,7 @@ __global__ void __launch_bounds__(kThreads, 3) k3_fused(K3Params prm) {
         if constexpr (sizeof(ScoreT) == 1)
             select_rows_t8(reinterpret_cast<const uint8_t*>(sc), a0, r0, r1, T, take,
                            prm.idx_out + (uint64_t)p * prm.idx_stride + off, s_warp,
+                           reinterpret_cast<uint32_t*>(priv),
                            prm.trace ? prm.trace + (uint64_t)blockIdx.x * 16 : nullptr);
         else
             select_rows<ScoreT, false>(sc, a0, r0, r1, T, take,
@@ -1297,7 +1304,8 @@ spl_status make_fused_plan(spl_ctx* ctx, uint32_t P, uint64_t n_max, uint32_t L,
     }
     const size_t sb = L <= 255 ? 1 : 2;
     const uint64_t total = (uint64_t)P * n_max;
-    const size_t base = align_up(wbins * kThreads, 16) + 2 * align_up((size_t)(L + 2) * 4, 16);
+    const size_t base = std::max<size_t>(align_up(wbins * kThreads, 16), K3_SEL_SCRATCH_BYTES) +
+                        2 * align_up((size_t)(L + 2) * 4, 16);
     int dev_max_smem = 0, sm_smem = 0;
     SPL_CUDA_TRY(ctx, cudaDeviceGetAttribute(&dev_max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin,
                                              ctx->device));
