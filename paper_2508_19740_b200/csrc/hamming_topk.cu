@@ -1131,25 +1131,74 @@ __global__ void __launch_bounds__(kThreads, 3) k3_select(K3Params prm, uint32_t*
     }
 }
 
-// Shard planning: one CTA per problem, from all ranks' histograms.
+// Shard planning: one CTA per problem, from all ranks' histograms. The same
+// integer arithmetic as spl_plan_shard (spl_plan.cuh, the host form the CPU
+// tests check), spread over the block: thread t owns score bin t (summing it
+// over ranks), a block suffix sum finds T, and block reductions give this
+// rank's tie share and output offset. (Run by one thread it walked
+// R x (L + 1) global counters serially: 52 us at R = 8.)
 __global__ void __launch_bounds__(kThreads) k3_shard_plan(K3Params prm, const uint32_t* all_hist,
                                                           uint32_t R, uint32_t rank,
                                                           uint32_t* out_offset) {
     __shared__ uint64_t s_warp[kThreads / 32 + 1];
-    __shared__ spl_shard_plan s_plan;
+    extern __shared__ uint32_t s_G[];            // [L + 2] global count per bin, then suffix sums
+    __shared__ unsigned long long s_red[4];       // n, gt_before, gt_mine, (unused)
+    __shared__ uint32_t s_T, s_eqb, s_eqm;
     const uint32_t p = blockIdx.x;
     const uint32_t L = prm.L;
-    if (threadIdx.x == 0) {
-        // O(R * L) integer arithmetic, identical to the host form.
-        s_plan = spl_plan_shard(all_hist + (uint64_t)p * (L + 1), (uint64_t)prm.g.P * (L + 1), R,
-                                rank, L, prm.k);
-    }
+    const uint64_t rstride = (uint64_t)prm.g.P * (L + 1);
+    const uint32_t* h = all_hist + (uint64_t)p * (L + 1);
+    if (threadIdx.x < 4) s_red[threadIdx.x] = 0;
+    if (threadIdx.x == 0) s_T = SPL_PLAN_SKIP;
+    for (uint32_t t = threadIdx.x; t <= L + 1; t += kThreads) s_G[t] = 0;
     __syncthreads();
-    const spl_shard_plan pl = s_plan;
-    plan_segments(prm, p, pl.T, pl.take_eq, s_warp);
+    uint64_t n_loc = 0;
+    for (uint32_t t = threadIdx.x; t <= L; t += kThreads) {
+        uint32_t G = 0;
+        for (uint32_t r = 0; r < R; ++r) G += __ldg(h + r * rstride + t);
+        s_G[t] = G;
+        n_loc += G;
+    }
+    if (n_loc) atomicAdd(&s_red[0], (unsigned long long)n_loc);
+    __syncthreads();
+    const uint64_t n = s_red[0];
+    const uint32_t kk = (uint32_t)(prm.k < n ? prm.k : n);
+    if (kk > 0) {
+        block_suffix_sum(s_G, L + 1, s_warp);  // s_G[t] = #(score >= t), s_G[L+1] = 0
+        for (uint32_t t = threadIdx.x; t <= L; t += kThreads)
+            if (s_G[t] >= kk && s_G[t + 1] < kk) s_T = t;
+        __syncthreads();
+    }
+    const uint32_t T = s_T;
+    uint32_t take = 0, count = 0, off = 0;
+    if (T != SPL_PLAN_SKIP) {
+        const uint64_t quota = kk - s_G[T + 1];
+        uint64_t gtb = 0, gtm = 0;
+        for (uint32_t t = threadIdx.x; t <= L; t += kThreads) {
+            uint32_t before = 0;
+            for (uint32_t r = 0; r < rank; ++r) before += __ldg(h + r * rstride + t);
+            const uint32_t mine = __ldg(h + (uint64_t)rank * rstride + t);
+            if (t > T) {
+                gtb += before;
+                gtm += mine;
+            } else if (t == T) {
+                s_eqb = before;
+                s_eqm = mine;
+            }
+        }
+        if (gtb) atomicAdd(&s_red[1], (unsigned long long)gtb);
+        if (gtm) atomicAdd(&s_red[2], (unsigned long long)gtm);
+        __syncthreads();
+        const uint64_t eq_before = s_eqb, eq_mine = s_eqm;
+        const uint64_t left = quota > eq_before ? quota - eq_before : 0;
+        take = (uint32_t)(eq_mine < left ? eq_mine : left);
+        count = (uint32_t)(s_red[2] + take);
+        off = (uint32_t)(s_red[1] + (eq_before < quota ? eq_before : quota));
+    }
+    plan_segments(prm, p, T, take, s_warp);
     if (threadIdx.x == 0) {
-        prm.cnt_out[p] = pl.T == SPL_PLAN_SKIP ? 0u : pl.count;
-        if (out_offset) out_offset[p] = pl.offset;
+        prm.cnt_out[p] = T == SPL_PLAN_SKIP ? 0u : count;
+        if (out_offset) out_offset[p] = off;
     }
 }
 
@@ -1641,7 +1690,11 @@ spl_status shard_select_impl(spl_ctx* ctx, const uint32_t* all_hist, uint32_t R,
     K3Params prm = base_params(ctx, pl, ws, kst, nullptr, 0, L, nullptr, n_valid, nvalid_div, k);
     prm.cnt_out = cnt;
     prm.shard = 1;
-    k3_shard_plan<<<P, kThreads, 0, s>>>(prm, all_hist, R, rank, out_offset);
+    const size_t plan_smem = (size_t)(L + 2) * 4;
+    if (plan_smem > 48 * 1024)
+        SPL_CUDA_TRY(ctx, cudaFuncSetAttribute(k3_shard_plan, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               (int)plan_smem));
+    k3_shard_plan<<<P, kThreads, plan_smem, s>>>(prm, all_hist, R, rank, out_offset);
     if ((st = after_launch(ctx, "k3_shard_plan"))) return st;
     return launch_select(ctx, pl, prm, idx, k, s);
 }

@@ -454,17 +454,17 @@ def test_decode_step_vs_oracle(ctx, oracle, ref, kv):
 
 
 # ------------------------------------------------------------ sharded (virtual ranks on one GPU)
-@pytest.mark.parametrize("R", [2, 3, 8])
-def test_sharded_select_equals_reference(oracle, R):
+@pytest.mark.parametrize("R,P,N,W,k", [(2, 4, 40000, 4, 1234), (3, 4, 40000, 4, 1234),
+                                         (8, 4, 40000, 4, 1234), (3, 2, 60, 4, 1000),
+                                         (5, 3, 9000, 8, 4000), (8, 32, 16384, 4, 2621)])
+def test_sharded_select_equals_reference(oracle, R, P, N, W, k):
     """Sequence sharding: R contiguous shards, each with its own
     context; histograms 'all-gathered' by a device concat; the rank-order
     concatenation must equal the single-GPU reference list."""
-    rng = np.random.default_rng(R)
-    P, N, W = 4, 40000, 4
+    rng = np.random.default_rng(R * 1000 + N)
     codes = rng.integers(0, 2**32, (P, N, W), dtype=np.uint64).astype(np.uint32)
     codes[1] = codes[1][rng.integers(0, 4, N)]  # heavy ties crossing shards
     q = codes[:, 7].copy()
-    k = 1234
     bounds = np.linspace(0, N, R + 1).astype(np.int64)
     ctxs = [capi.Context(0) for _ in range(R)]
     hists = []
@@ -498,7 +498,7 @@ def test_sharded_select_equals_reference(oracle, R):
     want = oracle.retrieve_batch(codes, q, np.full(P, N, np.uint32), k)
     for p in range(P):
         cat = np.concatenate(got[p]).astype(np.uint32)
-        assert np.array_equal(cat, want[p])
+        assert np.array_equal(cat, want[p, :min(k, N)])
     for c in ctxs:
         c.close()
 
