@@ -167,6 +167,35 @@ spl_status spl_plan_shard_host(const uint32_t* all_hist, uint32_t R, uint32_t ra
                                uint32_t k, uint32_t* T, uint32_t* quota, uint32_t* take_eq,
                                uint32_t* count, uint32_t* offset);
 
+/* Fused sequence-sharded retrieval: ONE kernel per rank, the histogram
+ * exchange done inside it over peer memory (NVLink P2P stores into every
+ * rank's exchange area + release/acquire flags) instead of a host-issued
+ * collective between two kernels. Same results as spl_shard_histogram ->
+ * all-gather -> spl_shard_select: idx[p][0..cnt[p]) are this rank's local
+ * row ids, out_offset[p] their position in the global ascending list, k the
+ * GLOBAL budget. Every rank of the group must make the same sequence of
+ * calls (they rendezvous inside the kernel; a missing rank turns into
+ * SPL_E_CUDA from spl_check_device_error after a 2 s watchdog, not a hang).
+ * Setup: spl_peer_create on every rank; exchange the 64-byte handles of
+ * spl_peer_ipc_handle (e.g. an all-gather on the host), spl_peer_open with
+ * all R handles in rank order. spl_peer_connect_local wires R peers living in
+ * ONE process (tests, or several ranks per GPU). L <= 255 (u8 scores) and
+ * caches whose scores fit on chip (the fused single-GPU geometry); otherwise
+ * SPL_E_STATE and the caller uses the two-kernel flow above. */
+typedef struct spl_peer spl_peer;
+spl_status spl_peer_create(spl_ctx* ctx, uint32_t R, uint32_t rank, uint32_t P_max,
+                           uint32_t L_max, spl_peer** out);
+spl_status spl_peer_ipc_handle(spl_ctx* ctx, const spl_peer* peer, void* handle /* host, 64 B */);
+spl_status spl_peer_open(spl_ctx* ctx, spl_peer* peer, const void* handles /* host, R x 64 B */);
+spl_status spl_peer_connect_local(spl_ctx* ctx, spl_peer* const* peers, uint32_t R);
+void spl_peer_destroy(spl_peer* peer);
+spl_status spl_hamming_topk_sharded(spl_ctx* ctx, spl_peer* peer, const uint32_t* codes,
+                                    uint64_t problem_stride_rows, uint32_t L,
+                                    const uint32_t* qcodes, uint32_t P, const uint32_t* n_valid,
+                                    uint32_t nvalid_div, uint64_t n_max, uint32_t k,
+                                    uint32_t* idx, uint32_t* cnt, uint32_t* out_offset,
+                                    void* stream);
+
 /* ------------------------------------------------------ encoders (K1/K2) */
 /* A per-head hasher bank (one independent hasher per head).
  * MLP (hashers.hpp:24-34): w1 [H][d][h], b1 [H][h], w2 [H][h][L], row-major

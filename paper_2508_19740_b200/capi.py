@@ -102,8 +102,15 @@ _SIGS = {
     "spl_budget_from_rate": [dbl, u64, u32p],
     "spl_oracle_topk": [vp, vp, vp, i32, u64, u32, u32, vp, u32, u64, f32, u32, vp, vp, vp, vp],
     "spl_iou": [vp, vp, vp, u64, vp, vp, u64, u32, vp, vp],
+    "spl_peer_create": [vp, u32, u32, u32, u32, C.POINTER(vp)],
+    "spl_peer_ipc_handle": [vp, vp, vp],
+    "spl_peer_open": [vp, vp, vp],
+    "spl_peer_connect_local": [vp, C.POINTER(vp), u32],
+    "spl_peer_destroy": [vp],
+    "spl_hamming_topk_sharded": [vp, vp, vp, u64, u32, vp, u32, vp, u32, u64, u32, vp, vp, vp, vp],
 }
 _RESTYPE = {"spl_version": C.c_char_p, "spl_last_error": C.c_char_p, "spl_ctx_destroy": None,
+            "spl_peer_destroy": None,
             "spl_hasher_destroy": None, "spl_launch_count": C.c_uint64}
 
 
@@ -269,6 +276,17 @@ class Context:
     def hasher(self, w1, b1=None, w2=None, kind=SPL_HASHER_MLP) -> "Hasher":
         return Hasher(self, w1, b1, w2, kind)
 
+    def peer(self, R, rank, P_max, L_max) -> "Peer":
+        return Peer(self, R, rank, P_max, L_max)
+
+    def hamming_topk_sharded(self, peer, codes, stride_rows, L, qcodes, P, n_valid, nvalid_div,
+                             n_max, k, idx, cnt, out_offset, stream=None):
+        """Fused sequence-sharded retrieval (in-kernel exchange over peer memory)."""
+        self.check(self.lib.spl_hamming_topk_sharded(self.h, peer.h, _ptr(codes), stride_rows, L,
+                                                     _ptr(qcodes), P, _ptr(n_valid), nvalid_div,
+                                                     n_max, k, _ptr(idx), _ptr(cnt),
+                                                     _ptr(out_offset), _stream(stream)))
+
     # -- attention
     def sparse_attend(self, q, kcache, vcache, kv_dtype, stride_rows, d, P, idx, idx_stride, cnt,
                       n_valid, nvalid_div, scale, out, stream=None):
@@ -288,6 +306,39 @@ class Context:
     def attend_combine(self, partials, R, P, d, out, stream=None):
         self.check(self.lib.spl_attend_combine(self.h, _ptr(partials), R, P, d, _ptr(out),
                                                _stream(stream)))
+
+
+class Peer:
+    """spl_peer: this rank's member of a fused-sharding peer group."""
+
+    def __init__(self, ctx: Context, R, rank, P_max, L_max):
+        self.ctx = ctx
+        h = vp()
+        ctx.check(ctx.lib.spl_peer_create(ctx.h, R, rank, P_max, L_max, C.byref(h)))
+        self.h = h
+        self.R, self.rank = R, rank
+
+    def ipc_handle(self) -> bytes:
+        buf = C.create_string_buffer(64)
+        self.ctx.check(self.ctx.lib.spl_peer_ipc_handle(self.ctx.h, self.h, buf))
+        return buf.raw
+
+    def open(self, handles):
+        """handles: the R 64-byte handles in rank order (e.g. all-gathered)."""
+        blob = b"".join(handles)
+        assert len(blob) == 64 * self.R
+        buf = C.create_string_buffer(blob, len(blob))
+        self.ctx.check(self.ctx.lib.spl_peer_open(self.ctx.h, self.h, buf))
+
+    @staticmethod
+    def connect_local(ctx: Context, peers):
+        arr = (vp * len(peers))(*[p.h for p in peers])
+        ctx.check(ctx.lib.spl_peer_connect_local(ctx.h, arr, len(peers)))
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.ctx.lib.spl_peer_destroy(self.h)
+            self.h = None
 
 
 class Hasher:

@@ -225,6 +225,96 @@ spl_status spl_top_k(spl_ctx* ctx, const void* scores, int dtype, uint32_t P, ui
     return top_k_launch(ctx, scores, dtype, P, n, scores_stride, k, idx, S(stream));
 }
 
+// ------------------------------------------------ peer group (fused sharding)
+spl_status spl_peer_create(spl_ctx* ctx, uint32_t R, uint32_t rank, uint32_t P_max,
+                           uint32_t L_max, spl_peer** out) {
+    if (!ctx || !out) return SPL_E_STATE;
+    *out = nullptr;
+    if (R == 0 || rank >= R || P_max == 0 || L_max == 0 || L_max % 32 != 0 || L_max > (1u << 15))
+        return fail(ctx, SPL_E_DIMENSION, "peer_create: need 0 <= rank < R, P_max >= 1, L_max % 32 == 0");
+    auto* pe = new spl_peer;
+    pe->R = R;
+    pe->rank = rank;
+    pe->Pmax = P_max;
+    pe->Lmax = L_max;
+    pe->device = ctx->device;
+    pe->bytes = peer_area_words(R, P_max, L_max) * 4;
+    cudaError_t e = cudaMalloc(&pe->buf, pe->bytes);
+    if (e == cudaSuccess) e = cudaMemset(pe->buf, 0, pe->bytes);
+    if (e == cudaSuccess) e = cudaMalloc(&pe->d_table, sizeof(uint32_t*) * R);
+    if (e != cudaSuccess) {
+        cudaFree(pe->buf);
+        delete pe;
+        return cuda_fail(ctx, e, "peer_create");
+    }
+    *out = pe;
+    return SPL_OK;
+}
+
+spl_status spl_peer_ipc_handle(spl_ctx* ctx, const spl_peer* peer, void* handle) {
+    if (!ctx || !peer || !handle) return SPL_E_STATE;
+    cudaIpcMemHandle_t h;
+    SPL_CUDA_TRY(ctx, cudaIpcGetMemHandle(&h, peer->buf));
+    std::memcpy(handle, &h, sizeof(h));
+    return SPL_OK;
+}
+
+spl_status spl_peer_open(spl_ctx* ctx, spl_peer* peer, const void* handles) {
+    if (!ctx || !peer || !handles) return SPL_E_STATE;
+    std::vector<uint32_t*> table(peer->R, nullptr);
+    for (uint32_t r = 0; r < peer->R; ++r) {
+        if (r == peer->rank) {
+            table[r] = peer->buf;
+            continue;
+        }
+        cudaIpcMemHandle_t h;
+        std::memcpy(&h, static_cast<const uint8_t*>(handles) + (size_t)r * sizeof(h), sizeof(h));
+        void* ptr = nullptr;
+        SPL_CUDA_TRY(ctx, cudaIpcOpenMemHandle(&ptr, h, cudaIpcMemLazyEnablePeerAccess));
+        peer->opened.push_back(ptr);
+        table[r] = static_cast<uint32_t*>(ptr);
+    }
+    SPL_CUDA_TRY(ctx, cudaMemcpy(peer->d_table, table.data(), sizeof(uint32_t*) * peer->R,
+                                 cudaMemcpyHostToDevice));
+    peer->connected = true;
+    return SPL_OK;
+}
+
+spl_status spl_peer_connect_local(spl_ctx* ctx, spl_peer* const* peers, uint32_t R) {
+    if (!ctx || !peers || R == 0) return SPL_E_STATE;
+    std::vector<uint32_t*> table(R);
+    for (uint32_t r = 0; r < R; ++r) {
+        if (!peers[r] || peers[r]->R != R || peers[r]->rank != r)
+            return fail(ctx, SPL_E_DIMENSION, "peer_connect_local: peers must be ranks 0..R-1 of one group");
+        table[r] = peers[r]->buf;
+    }
+    for (uint32_t r = 0; r < R; ++r) {
+        SPL_CUDA_TRY(ctx, cudaMemcpy(peers[r]->d_table, table.data(), sizeof(uint32_t*) * R,
+                                     cudaMemcpyHostToDevice));
+        peers[r]->connected = true;
+    }
+    return SPL_OK;
+}
+
+void spl_peer_destroy(spl_peer* peer) {
+    if (!peer) return;
+    cudaDeviceSynchronize();
+    for (void* p : peer->opened) cudaIpcCloseMemHandle(p);
+    cudaFree(peer->d_table);
+    cudaFree(peer->buf);
+    delete peer;
+}
+
+spl_status spl_hamming_topk_sharded(spl_ctx* ctx, spl_peer* peer, const uint32_t* codes,
+                                    uint64_t problem_stride_rows, uint32_t L,
+                                    const uint32_t* qcodes, uint32_t P, const uint32_t* n_valid,
+                                    uint32_t nvalid_div, uint64_t n_max, uint32_t k,
+                                    uint32_t* idx, uint32_t* cnt, uint32_t* out_offset,
+                                    void* stream) {
+    return hamming_topk_sharded_impl(ctx, peer, codes, problem_stride_rows, L, qcodes, P, n_valid,
+                                     nvalid_div, n_max, k, idx, cnt, out_offset, S(stream));
+}
+
 // ------------------------------------------------ dense retrieval (§8 f2)
 spl_status spl_oracle_topk(spl_ctx* ctx, const float* q, const void* keys, int kv_dtype,
                            uint64_t cap, uint32_t d, uint32_t P, const uint32_t* n_valid,

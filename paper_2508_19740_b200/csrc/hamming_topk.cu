@@ -85,6 +85,13 @@ struct K3Params {
     uint32_t hist_lo;      // fused: private counters cover scores [hist_lo, L] only
     uint32_t* counters2;   // fused: [P] low-bin fallback completion
     int clamp8;            // two-pass L = 256: u8 scores hold min(score, 255)
+    // fused sequence-sharded path (k3_fused<.., SHARD = true>): per-problem
+    // histograms are exchanged with the other ranks inside the kernel through
+    // their exchange areas (IPC-mapped peer memory over NVLink)
+    uint32_t** peer_bufs;  // [R] exchange area of every rank (own included)
+    uint32_t* own_buf;     // this rank's exchange area
+    uint32_t R, rank, epoch, Pmax;
+    uint32_t* out_offset;  // [P] position of this rank's first index in the global list
 };
 
 constexpr int kThreads = 256;
@@ -884,6 +891,131 @@ __global__ void __launch_bounds__(kThreads, 3) k3_scan(K3Params prm) {
     }
 }
 
+// ------------------------------------------------------------ peer exchange
+// Exchange area of one rank (u32 words; S = L + 2 slots per (rank, problem),
+// slot L + 1 = the sender's valid row count), double-buffered by epoch parity
+// (a rank can run at most one call ahead of a peer: it cannot finish call
+// i + 1 before that peer has pushed its call-(i + 1) histograms, which it does
+// only after finishing call i):
+//   recv   [2][R][Pmax][S]
+//   flags1 [2][R][Pmax]   window histogram [lo, L] + valid count delivered
+//   flags2 [2][R][Pmax]   low bins [0, lo) delivered (fallback round)
+// A flag holds the epoch of the call whose data sits in the slot.
+__host__ __device__ __forceinline__ uint64_t xslot(uint32_t R, uint32_t Pmax, uint32_t S,
+                                                   uint32_t par, uint32_t r, uint32_t p) {
+    return (((uint64_t)par * R + r) * Pmax + p) * S;
+}
+__host__ __device__ __forceinline__ uint64_t xflag(uint32_t R, uint32_t Pmax, uint32_t S,
+                                                   int set, uint32_t par, uint32_t r, uint32_t p) {
+    return 2ull * R * Pmax * S + (uint64_t)(set - 1) * 2 * R * Pmax + ((uint64_t)par * R + r) * Pmax + p;
+}
+__host__ __device__ __forceinline__ uint64_t xwords(uint32_t R, uint32_t Pmax, uint32_t S) {
+    return 2ull * R * Pmax * S + 4ull * R * Pmax;
+}
+__device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
+    asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+// One thread: spin until *p == v (a peer's release store); 2 s watchdog.
+__device__ void wait_flag_eq(const uint32_t* p, uint32_t v, uint32_t* dev_err) {
+    if (ld_acquire_sys(p) == v) return;
+    const uint64_t t0 = gtimer();
+    while (ld_acquire_sys(p) != v) {
+        __nanosleep(64);
+        if (gtimer() - t0 > 2000000000ull) {
+            raise_dev_err(dev_err, SPL_DEV_ERR_STALL);
+            return;
+        }
+    }
+}
+// Block: push bins [b0, b1) of this rank's problem histogram (tot, complete)
+// into slot (rank, p) of every rank's exchange area, then release flag `set`.
+__device__ void shard_push(const K3Params& prm, const uint32_t* tot, uint32_t p, uint32_t b0,
+                           uint32_t b1, int set, uint32_t nv_local) {
+    const uint32_t S = prm.L + 2, par = prm.epoch & 1u;
+    __threadfence();
+    for (uint32_t r = 0; r < prm.R; ++r) {
+        uint32_t* dst = prm.peer_bufs[r] + xslot(prm.R, prm.Pmax, S, par, prm.rank, p);
+        for (uint32_t t = b0 + threadIdx.x; t < b1; t += kThreads) dst[t] = __ldcg(tot + t);
+        if (set == 1 && threadIdx.x == 0) dst[prm.L + 1] = nv_local;
+    }
+    __threadfence_system();
+    __syncthreads();
+    for (uint32_t r = threadIdx.x; r < prm.R; r += kThreads)
+        st_release_sys(prm.peer_bufs[r] + xflag(prm.R, prm.Pmax, S, set, par, prm.rank, p), prm.epoch);
+}
+// Block: wait until every rank delivered flag `set` of problem p.
+__device__ void shard_wait(const K3Params& prm, uint32_t p, int set) {
+    const uint32_t S = prm.L + 2, par = prm.epoch & 1u;
+    for (uint32_t r = threadIdx.x; r < prm.R; r += kThreads)
+        wait_flag_eq(prm.own_buf + xflag(prm.R, prm.Pmax, S, set, par, r, p), prm.epoch, prm.dev_err);
+    __syncthreads();
+}
+// Block: the global plan of problem p from all ranks' delivered histograms
+// (bins >= from; the same integer arithmetic as spl_plan_shard). Outputs are
+// uniform across the block. T = SPL_PLAN_SKIP: kk == 0, or fewer than kk rows
+// score >= from (the caller then runs the low-bin round).
+struct ShardPlanOut {
+    uint32_t T, take, count, off, kk;
+};
+__device__ ShardPlanOut shard_global_plan(const K3Params& prm, uint32_t p, uint32_t from,
+                                          uint32_t* s_cum, uint64_t* s_warp,
+                                          unsigned long long* s_red, uint32_t* s_aux) {
+    const uint32_t L = prm.L, S = L + 2, par = prm.epoch & 1u;
+    const uint32_t* base = prm.own_buf + xslot(prm.R, prm.Pmax, S, par, 0, p);
+    const uint64_t rs = (uint64_t)prm.Pmax * S;  // rank stride inside the recv array
+    if (threadIdx.x < 4) s_red[threadIdx.x] = 0;
+    if (threadIdx.x == 0) s_aux[0] = SPL_PLAN_SKIP;
+    __syncthreads();
+    uint64_t nloc = 0;
+    for (uint32_t r = threadIdx.x; r < prm.R; r += kThreads) nloc += __ldcg(base + r * rs + L + 1);
+    if (nloc) atomicAdd(&s_red[0], (unsigned long long)nloc);
+    for (uint32_t t = threadIdx.x; t <= L + 1; t += kThreads) {
+        uint32_t G = 0;
+        if (t >= from && t <= L)
+            for (uint32_t r = 0; r < prm.R; ++r) G += __ldcg(base + r * rs + t);
+        s_cum[t] = G;
+    }
+    __syncthreads();
+    const uint64_t n = s_red[0];
+    ShardPlanOut o{SPL_PLAN_SKIP, 0, 0, 0, (uint32_t)(prm.k < n ? prm.k : n)};
+    if (o.kk == 0) return o;
+    block_suffix_sum(s_cum, L + 1, s_warp);  // s_cum[t] = #(score >= t) over bins >= from
+    for (uint32_t t = threadIdx.x; t <= L; t += kThreads)
+        if (s_cum[t] >= o.kk && s_cum[t + 1] < o.kk) s_aux[0] = t;
+    __syncthreads();
+    o.T = s_aux[0];
+    if (o.T == SPL_PLAN_SKIP) return o;
+    const uint64_t quota = o.kk - s_cum[o.T + 1];
+    uint64_t gtb = 0, gtm = 0;
+    for (uint32_t t = o.T + threadIdx.x; t <= L; t += kThreads) {
+        uint32_t before = 0;
+        for (uint32_t r = 0; r < prm.rank; ++r) before += __ldcg(base + r * rs + t);
+        const uint32_t mine = __ldcg(base + (uint64_t)prm.rank * rs + t);
+        if (t > o.T) {
+            gtb += before;
+            gtm += mine;
+        } else {
+            s_aux[1] = before;
+            s_aux[2] = mine;
+        }
+    }
+    if (gtb) atomicAdd(&s_red[1], (unsigned long long)gtb);
+    if (gtm) atomicAdd(&s_red[2], (unsigned long long)gtm);
+    __syncthreads();
+    const uint64_t eq_before = s_aux[1], eq_mine = s_aux[2];
+    const uint64_t left = quota > eq_before ? quota - eq_before : 0;
+    o.take = (uint32_t)(eq_mine < left ? eq_mine : left);
+    o.count = (uint32_t)(s_red[2] + o.take);
+    o.off = (uint32_t)(s_red[1] + (eq_before < quota ? eq_before : quota));
+    __syncthreads();
+    return o;
+}
+
 // ------------------------------------------------------------ fused
 // Single-launch path for caches whose scores fit on chip (the headline
 // 32 x 512K case). Contiguous segments, a whole number per problem (G <= SMs
@@ -897,11 +1029,20 @@ __global__ void __launch_bounds__(kThreads, 3) k3_scan(K3Params prm) {
 #define K3_STAMP(i) \
     if (prm.trace && threadIdx.x == 0) prm.trace[blockIdx.x * 16 + (i)] = gtimer()
 
-template <int W, typename ScoreT>
+// SHARD: one rank of a sequence-sharded cache. The CTA completing a
+// problem's local histogram pushes it to every rank's exchange area (peer
+// memory over NVLink), every CTA of the problem waits for all ranks' pushes,
+// takes the global threshold / tie quota / this rank's share and offset
+// (shard_global_plan) and compacts its rows as usual — one launch, no
+// host-side collective. Local positions, plus out_offset[p] into the global
+// list (rank order = index order, as in spl_shard_select).
+template <int W, typename ScoreT, bool SHARD = false>
 __global__ void __launch_bounds__(kThreads, 3) k3_fused(K3Params prm) {
     extern __shared__ __align__(16) uint8_t smem[];
     __shared__ uint64_t s_warp[kThreads / 32 + 1];
     __shared__ uint32_t s_flag, s_T;
+    __shared__ unsigned long long s_red[4];
+    __shared__ uint32_t s_aux[4];
     const uint32_t L = prm.L;
     const uint32_t bins = L + 1;
     const uint32_t lo = prm.hist_lo;        // counted window [lo, L]
@@ -982,7 +1123,14 @@ __global__ void __launch_bounds__(kThreads, 3) k3_fused(K3Params prm) {
         // publish: this segment of problem p is complete (record + histogram)
         __threadfence();
         __syncthreads();
-        if (tid == 0) atomicAdd(prm.counters + p, 1u);
+        if (tid == 0) {
+            const uint32_t prev = atomicAdd(prm.counters + p, 1u);
+            s_flag = prev + 1 == seg_last(g, p) - seg_first(g, p) + 1 ? 1u : 0u;
+        }
+        if constexpr (SHARD) {
+            __syncthreads();
+            if (s_flag) shard_push(prm, tot, p, lo, bins, 1, nv);  // the local histogram is complete
+        }
     }
     K3_STAMP(1);
     K3_STAMP(2);
@@ -1011,8 +1159,16 @@ __global__ void __launch_bounds__(kThreads, 3) k3_fused(K3Params prm) {
         // bins to `tot` while others may still be reading it, and every CTA
         // of the problem must reach the same decision
         uint32_t T, quota;
-        problem_threshold(tot, L, kk, s_cum, s_warp, &s_T, T, quota, lo);
-        if (kk > 0 && T == SPL_PLAN_SKIP) {
+        ShardPlanOut sp{};
+        if constexpr (SHARD) {
+            shard_wait(prm, p, 1);
+            sp = shard_global_plan(prm, p, lo, s_cum, s_warp, s_red, s_aux);
+            T = sp.T;
+            quota = sp.take;  // this rank's ties
+        } else {
+            problem_threshold(tot, L, kk, s_cum, s_warp, &s_T, T, quota, lo);
+        }
+        if ((SHARD ? sp.kk : kk) > 0 && T == SPL_PLAN_SKIP) {
             // Fewer than kk rows scored >= lo, so T < lo: every CTA of this
             // problem (the decision is the same for all of them) counts its
             // rows below the window from shared memory, completes its record
@@ -1036,14 +1192,33 @@ __global__ void __launch_bounds__(kThreads, 3) k3_fused(K3Params prm) {
             __threadfence();
             __syncthreads();
             if (tid == 0) {
-                atomicAdd(prm.counters2 + p, 1u);
-                wait_count(prm.counters2 + p, nseg, prm.dev_err);
+                const uint32_t prev = atomicAdd(prm.counters2 + p, 1u);
+                s_flag = prev + 1 == nseg ? 1u : 0u;
             }
             __syncthreads();
-            problem_threshold(tot, L, kk, s_cum, s_warp, &s_T, T, quota);
+            if constexpr (SHARD) {
+                if (s_flag) shard_push(prm, tot, p, 0, lo, 2, 0);  // low bins of all local segments
+            }
+            if (tid == 0) wait_count(prm.counters2 + p, nseg, prm.dev_err);
+            __syncthreads();
+            if constexpr (SHARD) {
+                shard_wait(prm, p, 2);
+                sp = shard_global_plan(prm, p, 0, s_cum, s_warp, s_red, s_aux);
+                T = sp.T;
+                quota = sp.take;
+            } else {
+                problem_threshold(tot, L, kk, s_cum, s_warp, &s_T, T, quota);
+            }
         }
         K3_STAMP(3);
-        if (tid == 0 && seg == c0) prm.cnt_out[p] = kk;
+        if (tid == 0 && seg == c0) {
+            if constexpr (SHARD) {
+                prm.cnt_out[p] = T == SPL_PLAN_SKIP ? 0u : sp.count;
+                prm.out_offset[p] = sp.off;
+            } else {
+                prm.cnt_out[p] = kk;
+            }
+        }
         if (r0 >= r1) continue;
         if (T == SPL_PLAN_SKIP) continue;
         // (gt, eq) of the earlier segments of this problem, from their records
@@ -1321,13 +1496,13 @@ struct K3FPlan {
     const void* fn;
 };
 
-template <int W, typename ScoreT>
+template <int W, typename ScoreT, bool SHARD = false>
 const void* fused_fn() {
-    return reinterpret_cast<const void*>(&k3_fused<W, ScoreT>);
+    return reinterpret_cast<const void*>(&k3_fused<W, ScoreT, SHARD>);
 }
 
 spl_status make_fused_plan(spl_ctx* ctx, uint32_t P, uint64_t n_max, uint32_t L, const void* codes,
-                           uint64_t stride_rows, bool* ok, K3FPlan* out) {
+                           uint64_t stride_rows, bool* ok, K3FPlan* out, bool shard = false) {
     *ok = false;
     const uint32_t W = L / 32;
     // Private counters cover scores [L/2, L] only: the k-th best agreement is
@@ -1341,11 +1516,13 @@ spl_status make_fused_plan(spl_ctx* ctx, uint32_t P, uint64_t n_max, uint32_t L,
     const void* fn = nullptr;
     if (L <= 255) {
         switch (W) {
-            case 1: fn = fused_fn<1, uint8_t>(); break;
-            case 2: fn = fused_fn<2, uint8_t>(); break;
-            case 4: fn = fused_fn<4, uint8_t>(); break;
+            case 1: fn = shard ? fused_fn<1, uint8_t, true>() : fused_fn<1, uint8_t>(); break;
+            case 2: fn = shard ? fused_fn<2, uint8_t, true>() : fused_fn<2, uint8_t>(); break;
+            case 4: fn = shard ? fused_fn<4, uint8_t, true>() : fused_fn<4, uint8_t>(); break;
             default: return SPL_OK;
         }
+    } else if (shard) {
+        return SPL_OK;  // the fused sharded path keeps u8 scores (L <= 255)
     } else if (W == 8) {
         fn = fused_fn<8, uint16_t>();
     } else {
@@ -1697,6 +1874,58 @@ spl_status shard_select_impl(spl_ctx* ctx, const uint32_t* all_hist, uint32_t R,
     k3_shard_plan<<<P, kThreads, plan_smem, s>>>(prm, all_hist, R, rank, out_offset);
     if ((st = after_launch(ctx, "k3_shard_plan"))) return st;
     return launch_select(ctx, pl, prm, idx, k, s);
+}
+
+uint64_t peer_area_words(uint32_t R, uint32_t Pmax, uint32_t Lmax) {
+    return xwords(R, Pmax, Lmax + 2);
+}
+
+// ------------------------------------------------ fused sharded retrieval
+spl_status hamming_topk_sharded_impl(spl_ctx* ctx, spl_peer* peer, const uint32_t* codes,
+                                     uint64_t stride_rows, uint32_t L, const uint32_t* qcodes,
+                                     uint32_t P, const uint32_t* n_valid, uint32_t nvalid_div,
+                                     uint64_t n_max, uint32_t k, uint32_t* idx, uint32_t* cnt,
+                                     uint32_t* out_offset, cudaStream_t s) {
+    spl_status st = validate_common(ctx, "hamming_topk_sharded", codes, qcodes, n_valid, L, nvalid_div);
+    if (st) return st;
+    if (!peer || !peer->connected) return fail(ctx, SPL_E_STATE, "hamming_topk_sharded: peer group not connected");
+    if (k == 0) return fail(ctx, SPL_E_DIMENSION, "hash_topk: k must be >= 1");
+    if (!idx || !cnt || !out_offset) return fail(ctx, SPL_E_STATE, "hamming_topk_sharded: null output pointer");
+    if (P > peer->Pmax || L > peer->Lmax)
+        return fail(ctx, SPL_E_DIMENSION, "hamming_topk_sharded: P or L exceeds the peer group's capacity");
+    if (P == 0) return SPL_OK;
+    if (n_max == 0 || n_max > 0xFFFFFFFFull)
+        return fail(ctx, SPL_E_DIMENSION, "hamming_topk_sharded: every rank must own 1 .. 2^32 rows");
+    K3State kst;
+    if ((st = k3_state(ctx, P, L, s, &kst))) return st;
+    bool ok = false;
+    K3FPlan fp{};
+    if ((st = make_fused_plan(ctx, P, n_max, L, codes, stride_rows, &ok, &fp, true))) return st;
+    if (!ok)
+        return fail(ctx, SPL_E_STATE,
+                    "hamming_topk_sharded: the local cache does not fit the fused path; use "
+                    "spl_shard_histogram + collective + spl_shard_select");
+    K3Ws ws;
+    if ((st = k3_workspace(ctx, fp.pl, L, s, &ws, false))) return st;
+    K3Params prm = base_params(ctx, fp.pl, ws, kst, codes, stride_rows, L, qcodes, n_valid, nvalid_div, k);
+    prm.cnt_out = cnt;
+    prm.idx_out = idx;
+    prm.idx_stride = k;
+    prm.hist_lo = fp.pl.hist_lo;
+    prm.counters2 = kst.bar;
+    prm.peer_bufs = peer->d_table;
+    prm.own_buf = peer->buf;
+    prm.R = peer->R;
+    prm.rank = peer->rank;
+    prm.Pmax = peer->Pmax;
+    prm.epoch = ++peer->epoch;
+    if (prm.epoch == 0) prm.epoch = ++peer->epoch;  // 0 = never written
+    prm.out_offset = out_offset;
+    // the exchange layout is sized for Lmax: slots are (Lmax + 2) words
+    prm.L = L;
+    void* args[] = {&prm};
+    SPL_CUDA_TRY(ctx, cudaLaunchKernel(fp.fn, dim3(fp.pl.g.G), dim3(kThreads), args, fp.smem, s));
+    return after_launch(ctx, "k3_fused_shard");
 }
 
 }  // namespace spl

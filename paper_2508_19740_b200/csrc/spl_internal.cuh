@@ -5,6 +5,7 @@
 #include <stdint.h>
 
 #include <string>
+#include <vector>
 
 #include "../../include/spl_c.h"
 
@@ -49,6 +50,20 @@ struct spl_ctx {
     uint64_t shard_n_max = 0;
     uint32_t shard_P = 0, shard_L = 0, shard_G = 0;
     uint64_t shard_S = 0;
+};
+
+// A sequence-sharding peer group member (fused in-kernel exchange, see
+// hamming_topk.cu "peer exchange"): this rank's exchange area, the table of
+// every rank's area as mapped into this process, and the call epoch.
+struct spl_peer {
+    uint32_t R = 0, rank = 0, Pmax = 0, Lmax = 0;
+    uint32_t* buf = nullptr;        // own exchange area (zeroed at creation)
+    size_t bytes = 0;
+    uint32_t** d_table = nullptr;   // [R] device pointers (own included)
+    std::vector<void*> opened;      // IPC mappings to close
+    uint32_t epoch = 0;
+    bool connected = false;
+    int device = 0;
 };
 
 struct spl_hasher {

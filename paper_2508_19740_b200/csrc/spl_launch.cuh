@@ -53,6 +53,11 @@ spl_status shard_histogram_impl(spl_ctx*, const uint32_t*, uint64_t, uint32_t, c
 spl_status shard_select_impl(spl_ctx*, const uint32_t*, uint32_t, uint32_t, uint32_t, uint32_t,
                              const uint32_t*, uint32_t, uint64_t, uint32_t, uint32_t*, uint32_t*,
                              uint32_t*, cudaStream_t);
+spl_status hamming_topk_sharded_impl(spl_ctx*, spl_peer*, const uint32_t*, uint64_t, uint32_t,
+                                     const uint32_t*, uint32_t, const uint32_t*, uint32_t,
+                                     uint64_t, uint32_t, uint32_t*, uint32_t*, uint32_t*,
+                                     cudaStream_t);
+uint64_t peer_area_words(uint32_t R, uint32_t Pmax, uint32_t Lmax);
 // bitcodes_misc.cu
 spl_status pack_bits_launch(spl_ctx*, const uint8_t*, uint64_t, uint32_t, uint32_t*, cudaStream_t);
 spl_status unpack_bits_launch(spl_ctx*, const uint32_t*, uint64_t, uint32_t, uint8_t*,

@@ -533,3 +533,77 @@ def test_sharded_attention_combine(ctx, oracle):
         want = oracle.sparse_attention(Q[p:p + 1], K[p], V[p], np.float32(1 / np.sqrt(d)),
                                        np.array([n], np.uint32), [picks[p]])
         assert np.abs(out[p].cpu().numpy() - want[0]).max() <= 1e-5
+
+
+def _run_fused_sharded(oracle, R, P, N, W, k, codes, q, trials=2):
+    """R virtual ranks in one process (own contexts, peer group wired with
+    spl_peer_connect_local, one stream each so the R kernels run at once)."""
+    L = W * 32
+    bounds = np.linspace(0, N, R + 1).astype(np.int64)
+    ctxs = [capi.Context(0) for _ in range(R)]
+    peers = [ctxs[r].peer(R, r, P, L) for r in range(R)]
+    capi.Peer.connect_local(ctxs[0], peers)
+    streams = [torch.cuda.Stream() for _ in range(R)]
+    parts, outs = [], []
+    for r in range(R):
+        part = np.ascontiguousarray(codes[:, bounds[r]:bounds[r + 1]])
+        n_r = part.shape[1]
+        parts.append((T(part), n_r, T(np.full(P, n_r, np.uint32))))
+        outs.append((torch.zeros((P, k), dtype=torch.int32, device=DEV),
+                     torch.zeros(P, dtype=torch.int32, device=DEV),
+                     torch.zeros(P, dtype=torch.int32, device=DEV)))
+    qt = T(q)
+    want = oracle.retrieve_batch(codes, q, np.full(P, N, np.uint32), k)
+    torch.cuda.synchronize()
+    for _ in range(trials):  # epochs advance, both parity buffers get used
+        for r in range(R):
+            cp, n_r, nv = parts[r]
+            idx, cnt, off = outs[r]
+            idx.fill_(-1)
+            ctxs[r].hamming_topk_sharded(peers[r], cp, n_r, L, qt, P, nv, 1, n_r, k, idx, cnt, off,
+                                         streams[r].cuda_stream)
+        torch.cuda.synchronize()
+        for c in ctxs:
+            c.check_device_error()
+        for p in range(P):
+            cat = np.zeros(min(k, N), np.uint32)
+            filled = 0
+            for r in range(R):
+                idx, cnt, off = (U(t) for t in outs[r])
+                c, o = int(cnt[p]), int(off[p])
+                cat[o:o + c] = idx[p, :c] + bounds[r]
+                filled += c
+            assert filled == min(k, N)
+            assert np.array_equal(cat, want[p, :min(k, N)]), (R, p)
+    for pe in peers:
+        pe.close()
+    for c in ctxs:
+        c.close()
+
+
+@pytest.mark.parametrize("R", [1, 2, 3])
+def test_fused_sharded_equals_reference(oracle, R):
+    """spl_hamming_topk_sharded: one kernel per rank, histograms exchanged in
+    kernel through peer memory; the ranks' lists placed at their offsets
+    equal the single-GPU reference list (heavy ties crossing ranks)."""
+    rng = np.random.default_rng(70 + R)
+    P, N, W, k = 4, 30000, 4, 1500
+    codes = rng.integers(0, 2**32, (P, N, W), dtype=np.uint64).astype(np.uint32)
+    codes[1] = codes[1][rng.integers(0, 5, N)]
+    q = codes[:, 11].copy()
+    _run_fused_sharded(oracle, R, P, N, W, k, codes, q)
+
+
+def test_fused_sharded_low_threshold_round(oracle):
+    """Global k-th score below the counted window [L/2, L] on every rank: the
+    second (low-bin) exchange round runs; k close to N too."""
+    rng = np.random.default_rng(81)
+    P, N, W = 2, 24000, 4
+    q = rng.integers(0, 2**32, (P, W), dtype=np.uint64).astype(np.uint32)
+    codes = rng.integers(0, 2**32, (P, N, W), dtype=np.uint64).astype(np.uint32)
+    keep = np.zeros((N, W), np.uint32)
+    for _ in range(3):
+        keep |= rng.integers(0, 2**32, (N, W), dtype=np.uint64).astype(np.uint32)
+    codes[0] = (~q[0])[None, :] ^ (~keep & rng.integers(0, 2**32, (N, W), dtype=np.uint64).astype(np.uint32))
+    for k in (50, 23000):
+        _run_fused_sharded(oracle, 3, P, N, W, k, codes, q, trials=1)
