@@ -892,99 +892,98 @@ __global__ void __launch_bounds__(kThreads, 3) k3_scan(K3Params prm) {
 }
 
 // ------------------------------------------------------------ peer exchange
-// Exchange area of one rank (u32 words; S = L + 2 slots per (rank, problem),
-// slot L + 1 = the sender's valid row count), double-buffered by epoch parity
-// (a rank can run at most one call ahead of a peer: it cannot finish call
-// i + 1 before that peer has pushed its call-(i + 1) histograms, which it does
-// only after finishing call i):
-//   recv   [2][R][Pmax][S]
-//   flags1 [2][R][Pmax]   window histogram [lo, L] + valid count delivered
-//   flags2 [2][R][Pmax]   low bins [0, lo) delivered (fallback round)
-// A flag holds the epoch of the call whose data sits in the slot.
+// Exchange area of one rank: u64 entries {value, epoch} (NCCL "LL"-style:
+// the epoch tag travels in the same aligned 8-byte store as the value, so a
+// reader that sees the current epoch sees the value, and no system-scope
+// fence is needed on either side — a MEMBAR.SYS under the streaming load cost
+// ~13 us). S = L + 2 entries per (rank, problem): bins 0..L and, at L + 1,
+// the sender's valid row count. Double-buffered by epoch parity (a rank can
+// run at most one call ahead of a peer: it cannot finish call i + 1 before
+// that peer pushed its call-(i + 1) histograms, which it does only after
+// finishing call i):  recv [2][R][Pmax][S] x u64.
 __host__ __device__ __forceinline__ uint64_t xslot(uint32_t R, uint32_t Pmax, uint32_t S,
                                                    uint32_t par, uint32_t r, uint32_t p) {
     return (((uint64_t)par * R + r) * Pmax + p) * S;
 }
-__host__ __device__ __forceinline__ uint64_t xflag(uint32_t R, uint32_t Pmax, uint32_t S,
-                                                   int set, uint32_t par, uint32_t r, uint32_t p) {
-    return 2ull * R * Pmax * S + (uint64_t)(set - 1) * 2 * R * Pmax + ((uint64_t)par * R + r) * Pmax + p;
-}
 __host__ __device__ __forceinline__ uint64_t xwords(uint32_t R, uint32_t Pmax, uint32_t S) {
-    return 2ull * R * Pmax * S + 4ull * R * Pmax;
+    return 2ull * 2ull * R * Pmax * S;  // u32 words
 }
-__device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
-    asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+__device__ __forceinline__ void st_tagged(uint32_t* p, uint32_t v, uint32_t tag) {
+    asm volatile("st.volatile.global.v2.u32 [%0], {%1, %2};" ::"l"(p), "r"(v), "r"(tag) : "memory");
 }
-__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
-    uint32_t v;
-    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-    return v;
+__device__ __forceinline__ uint2 ld_tagged(const uint32_t* p) {
+    uint2 r;
+    asm volatile("ld.volatile.global.v2.u32 {%0, %1}, [%2];" : "=r"(r.x), "=r"(r.y) : "l"(p) : "memory");
+    return r;
 }
-// One thread: spin until *p == v (a peer's release store); 2 s watchdog.
-__device__ void wait_flag_eq(const uint32_t* p, uint32_t v, uint32_t* dev_err) {
-    if (ld_acquire_sys(p) == v) return;
+// One thread: spin until entry p carries `tag`; returns its value. 2 s watchdog.
+__device__ uint32_t wait_tagged(const uint32_t* p, uint32_t tag, uint32_t* dev_err) {
+    uint2 e = ld_tagged(p);
+    if (e.y == tag) return e.x;
     const uint64_t t0 = gtimer();
-    while (ld_acquire_sys(p) != v) {
-        __nanosleep(64);
+    while ((e = ld_tagged(p)).y != tag) {
+        __nanosleep(32);
         if (gtimer() - t0 > 2000000000ull) {
             raise_dev_err(dev_err, SPL_DEV_ERR_STALL);
-            return;
+            return 0;
         }
     }
+    return e.x;
 }
-// Block: push bins [b0, b1) of this rank's problem histogram (tot, complete)
-// into slot (rank, p) of every rank's exchange area, then release flag `set`.
+// Block: push bins [b0, b1) of this rank's problem histogram (tot, complete
+// at GPU scope) into slot (rank, p) of every rank's exchange area.
 __device__ void shard_push(const K3Params& prm, const uint32_t* tot, uint32_t p, uint32_t b0,
-                           uint32_t b1, int set, uint32_t nv_local) {
+                           uint32_t b1, bool with_count, uint32_t nv_local) {
     const uint32_t S = prm.L + 2, par = prm.epoch & 1u;
     __threadfence();
     for (uint32_t r = 0; r < prm.R; ++r) {
-        uint32_t* dst = prm.peer_bufs[r] + xslot(prm.R, prm.Pmax, S, par, prm.rank, p);
-        for (uint32_t t = b0 + threadIdx.x; t < b1; t += kThreads) dst[t] = __ldcg(tot + t);
-        if (set == 1 && threadIdx.x == 0) dst[prm.L + 1] = nv_local;
+        uint32_t* dst = prm.peer_bufs[r] + 2 * xslot(prm.R, prm.Pmax, S, par, prm.rank, p);
+        for (uint32_t t = b0 + threadIdx.x; t < b1; t += kThreads)
+            st_tagged(dst + 2 * t, __ldcg(tot + t), prm.epoch);
+        if (with_count && threadIdx.x == 0) st_tagged(dst + 2 * (prm.L + 1), nv_local, prm.epoch);
     }
-    __threadfence_system();
-    __syncthreads();
-    for (uint32_t r = threadIdx.x; r < prm.R; r += kThreads)
-        st_release_sys(prm.peer_bufs[r] + xflag(prm.R, prm.Pmax, S, set, par, prm.rank, p), prm.epoch);
-}
-// Block: wait until every rank delivered flag `set` of problem p.
-__device__ void shard_wait(const K3Params& prm, uint32_t p, int set) {
-    const uint32_t S = prm.L + 2, par = prm.epoch & 1u;
-    for (uint32_t r = threadIdx.x; r < prm.R; r += kThreads)
-        wait_flag_eq(prm.own_buf + xflag(prm.R, prm.Pmax, S, set, par, r, p), prm.epoch, prm.dev_err);
-    __syncthreads();
 }
 // Block: the global plan of problem p from all ranks' delivered histograms
-// (bins >= from; the same integer arithmetic as spl_plan_shard). Outputs are
-// uniform across the block. T = SPL_PLAN_SKIP: kk == 0, or fewer than kk rows
-// score >= from (the caller then runs the low-bin round).
+// (bins >= from; the same integer arithmetic as spl_plan_shard). Collects
+// the R x (bins [from, L] + count) entries into `mat` (shared, R x (L + 2)
+// words; entries below `from` keep what an earlier round stored), waiting
+// on each entry's epoch tag. Outputs are uniform across the block.
+// T = SPL_PLAN_SKIP: kk == 0, or fewer than kk rows score >= from (the
+// caller then runs the low-bin round).
 struct ShardPlanOut {
     uint32_t T, take, count, off, kk;
 };
 __device__ ShardPlanOut shard_global_plan(const K3Params& prm, uint32_t p, uint32_t from,
-                                          uint32_t* s_cum, uint64_t* s_warp,
-                                          unsigned long long* s_red, uint32_t* s_aux) {
+                                          uint32_t to, uint32_t* mat, uint32_t* s_cum,
+                                          uint64_t* s_warp, unsigned long long* s_red,
+                                          uint32_t* s_aux) {
     const uint32_t L = prm.L, S = L + 2, par = prm.epoch & 1u;
-    const uint32_t* base = prm.own_buf + xslot(prm.R, prm.Pmax, S, par, 0, p);
-    const uint64_t rs = (uint64_t)prm.Pmax * S;  // rank stride inside the recv array
+    const uint32_t* base = prm.own_buf + 2 * xslot(prm.R, prm.Pmax, S, par, 0, p);
+    const uint64_t rs = 2ull * prm.Pmax * S;  // rank stride (u32 words)
+    // entries [from, to) of every rank (+ the count at L + 1 when to == L + 2)
+    const uint32_t span = to - from;
+    for (uint32_t i = threadIdx.x; i < prm.R * span; i += kThreads) {
+        const uint32_t r = i / span, t = from + i % span;
+        mat[r * S + t] = wait_tagged(base + r * rs + 2 * t, prm.epoch, prm.dev_err);
+    }
     if (threadIdx.x < 4) s_red[threadIdx.x] = 0;
     if (threadIdx.x == 0) s_aux[0] = SPL_PLAN_SKIP;
     __syncthreads();
     uint64_t nloc = 0;
-    for (uint32_t r = threadIdx.x; r < prm.R; r += kThreads) nloc += __ldcg(base + r * rs + L + 1);
+    for (uint32_t r = threadIdx.x; r < prm.R; r += kThreads) nloc += mat[r * S + L + 1];
     if (nloc) atomicAdd(&s_red[0], (unsigned long long)nloc);
+    const uint32_t lo = (to == L + 2) ? from : 0;  // bins counted so far: [lo, L]
     for (uint32_t t = threadIdx.x; t <= L + 1; t += kThreads) {
         uint32_t G = 0;
-        if (t >= from && t <= L)
-            for (uint32_t r = 0; r < prm.R; ++r) G += __ldcg(base + r * rs + t);
+        if (t >= lo && t <= L)
+            for (uint32_t r = 0; r < prm.R; ++r) G += mat[r * S + t];
         s_cum[t] = G;
     }
     __syncthreads();
     const uint64_t n = s_red[0];
     ShardPlanOut o{SPL_PLAN_SKIP, 0, 0, 0, (uint32_t)(prm.k < n ? prm.k : n)};
     if (o.kk == 0) return o;
-    block_suffix_sum(s_cum, L + 1, s_warp);  // s_cum[t] = #(score >= t) over bins >= from
+    block_suffix_sum(s_cum, L + 1, s_warp);  // s_cum[t] = #(score >= t) over bins >= lo
     for (uint32_t t = threadIdx.x; t <= L; t += kThreads)
         if (s_cum[t] >= o.kk && s_cum[t + 1] < o.kk) s_aux[0] = t;
     __syncthreads();
@@ -994,8 +993,8 @@ __device__ ShardPlanOut shard_global_plan(const K3Params& prm, uint32_t p, uint3
     uint64_t gtb = 0, gtm = 0;
     for (uint32_t t = o.T + threadIdx.x; t <= L; t += kThreads) {
         uint32_t before = 0;
-        for (uint32_t r = 0; r < prm.rank; ++r) before += __ldcg(base + r * rs + t);
-        const uint32_t mine = __ldcg(base + (uint64_t)prm.rank * rs + t);
+        for (uint32_t r = 0; r < prm.rank; ++r) before += mat[r * S + t];
+        const uint32_t mine = mat[prm.rank * S + t];
         if (t > o.T) {
             gtb += before;
             gtm += mine;
@@ -1129,7 +1128,7 @@ __global__ void __launch_bounds__(kThreads, 3) k3_fused(K3Params prm) {
         }
         if constexpr (SHARD) {
             __syncthreads();
-            if (s_flag) shard_push(prm, tot, p, lo, bins, 1, nv);  // the local histogram is complete
+            if (s_flag) shard_push(prm, tot, p, lo, bins, true, nv);  // the local histogram is complete
         }
     }
     K3_STAMP(1);
@@ -1160,9 +1159,11 @@ __global__ void __launch_bounds__(kThreads, 3) k3_fused(K3Params prm) {
         // of the problem must reach the same decision
         uint32_t T, quota;
         ShardPlanOut sp{};
+        // SHARD: all ranks' histograms land in the private-counter region (free
+        // now; the plan checked R x (L + 2) words fit)
+        uint32_t* mat = reinterpret_cast<uint32_t*>(priv);
         if constexpr (SHARD) {
-            shard_wait(prm, p, 1);
-            sp = shard_global_plan(prm, p, lo, s_cum, s_warp, s_red, s_aux);
+            sp = shard_global_plan(prm, p, lo, L + 2, mat, s_cum, s_warp, s_red, s_aux);
             T = sp.T;
             quota = sp.take;  // this rank's ties
         } else {
@@ -1197,13 +1198,12 @@ __global__ void __launch_bounds__(kThreads, 3) k3_fused(K3Params prm) {
             }
             __syncthreads();
             if constexpr (SHARD) {
-                if (s_flag) shard_push(prm, tot, p, 0, lo, 2, 0);  // low bins of all local segments
+                if (s_flag) shard_push(prm, tot, p, 0, lo, false, 0);  // low bins of all local segments
             }
             if (tid == 0) wait_count(prm.counters2 + p, nseg, prm.dev_err);
             __syncthreads();
             if constexpr (SHARD) {
-                shard_wait(prm, p, 2);
-                sp = shard_global_plan(prm, p, 0, s_cum, s_warp, s_red, s_aux);
+                sp = shard_global_plan(prm, p, 0, lo, mat, s_cum, s_warp, s_red, s_aux);
                 T = sp.T;
                 quota = sp.take;
             } else {
@@ -1686,6 +1686,59 @@ K3Params base_params(spl_ctx* ctx, const K3Plan& pl, const K3Ws& ws, const K3Sta
     return prm;
 }
 
+void k3_trace_report(uint64_t* dtrace, uint32_t G, uint64_t S, cudaStream_t s) {
+    const char* tr = getenv("SPL_K3_TRACE");
+    {
+                // stamps per CTA (16 slots): 0 start, 1 stream end, 2 (= 1), 3 T known,
+                // 4 prefix, 5 select end, 6 smid, 8 own record read, 9 select counts,
+                // 10 select scan, 11 select emitted
+                constexpr int kSlots = 16;
+                const int cols[] = {0, 1, 3, 4, 8, 9, 10, 11, 5};
+                const char* names = "start stream thresh prefix rec counts scan emit end";
+                std::vector<uint64_t> h((size_t)G * kSlots);
+                cudaStreamSynchronize(s);
+                cudaMemcpy(h.data(), dtrace, h.size() * 8, cudaMemcpyDeviceToHost);
+                cudaFree(dtrace);
+                uint64_t t0 = ~0ull;
+                for (uint32_t i = 0; i < G; ++i) t0 = std::min(t0, h[i * kSlots]);
+                double mx[9] = {0}, mean[9] = {0};
+                for (uint32_t i = 0; i < G; ++i)
+                    for (int j = 0; j < 9; ++j) {
+                        const uint64_t raw = h[i * kSlots + cols[j]];
+                        const double v = raw ? (double)(raw - t0) / 1000.0 : 0.0;
+                        mx[j] = std::max(mx[j], v);
+                        mean[j] += v / G;
+                    }
+                fprintf(stderr, "k3_fused trace G=%u S=%llu [%s] mean:", G,
+                        (unsigned long long)S, names);
+                for (int j = 0; j < 9; ++j) fprintf(stderr, " %.1f", mean[j]);
+                fprintf(stderr, "  max:");
+                for (int j = 0; j < 9; ++j) fprintf(stderr, " %.1f", mx[j]);
+                fprintf(stderr, " us");
+                double cyc[3] = {0, 0, 0};
+                for (uint32_t i = 0; i < G; ++i)
+                    for (int j = 0; j < 3; ++j)
+                        cyc[j] += (double)(int64_t)(h[i * kSlots + 13 + j] - h[i * kSlots + 12 + j]) / G;
+                fprintf(stderr, "  select thread-0 cycles: counts %.0f scan %.0f emit %.0f\n", cyc[0], cyc[1],
+                        cyc[2]);
+                if (*tr == '2') {  // per-CTA dump: cta, smid, stamps (us)
+                    FILE* f = fopen("gpurun_out/k3_trace.csv", "w");
+                    if (f) {
+                        fprintf(f, "cta,smid,start,stream,thresh,prefix,rec,counts,scan,emit,end\n");
+                        for (uint32_t i = 0; i < G; ++i) {
+                            fprintf(f, "%u,%llu", i, (unsigned long long)h[i * kSlots + 6]);
+                            for (int j = 0; j < 9; ++j) {
+                                const uint64_t raw = h[i * kSlots + cols[j]];
+                                fprintf(f, ",%.3f", raw ? (double)(raw - t0) / 1000.0 : 0.0);
+                            }
+                            fprintf(f, "\n");
+                        }
+                        fclose(f);
+                    }
+                }
+            }
+}
+
 // SPL_K3_PATH=twopass forces the two-kernel path (A/B measurement, tests).
 bool fused_allowed() {
     const char* e = getenv("SPL_K3_PATH");
@@ -1739,55 +1792,7 @@ spl_status hamming_topk_impl(spl_ctx* ctx, const uint32_t* codes, uint64_t strid
             else
                 SPL_CUDA_TRY(ctx, launch_pdl(fp.fn, dim3(G), dim3(kThreads), fp.smem, s, args));
             st = after_launch(ctx, "k3_fused");
-            if (dtrace) {
-                // stamps per CTA (16 slots): 0 start, 1 stream end, 2 (= 1), 3 T known,
-                // 4 prefix, 5 select end, 6 smid, 8 own record read, 9 select counts,
-                // 10 select scan, 11 select emitted
-                constexpr int kSlots = 16;
-                const int cols[] = {0, 1, 3, 4, 8, 9, 10, 11, 5};
-                const char* names = "start stream thresh prefix rec counts scan emit end";
-                std::vector<uint64_t> h((size_t)G * kSlots);
-                cudaStreamSynchronize(s);
-                cudaMemcpy(h.data(), dtrace, h.size() * 8, cudaMemcpyDeviceToHost);
-                cudaFree(dtrace);
-                uint64_t t0 = ~0ull;
-                for (uint32_t i = 0; i < G; ++i) t0 = std::min(t0, h[i * kSlots]);
-                double mx[9] = {0}, mean[9] = {0};
-                for (uint32_t i = 0; i < G; ++i)
-                    for (int j = 0; j < 9; ++j) {
-                        const uint64_t raw = h[i * kSlots + cols[j]];
-                        const double v = raw ? (double)(raw - t0) / 1000.0 : 0.0;
-                        mx[j] = std::max(mx[j], v);
-                        mean[j] += v / G;
-                    }
-                fprintf(stderr, "k3_fused trace G=%u S=%llu [%s] mean:", G,
-                        (unsigned long long)fp.pl.g.S, names);
-                for (int j = 0; j < 9; ++j) fprintf(stderr, " %.1f", mean[j]);
-                fprintf(stderr, "  max:");
-                for (int j = 0; j < 9; ++j) fprintf(stderr, " %.1f", mx[j]);
-                fprintf(stderr, " us");
-                double cyc[3] = {0, 0, 0};
-                for (uint32_t i = 0; i < G; ++i)
-                    for (int j = 0; j < 3; ++j)
-                        cyc[j] += (double)(int64_t)(h[i * kSlots + 13 + j] - h[i * kSlots + 12 + j]) / G;
-                fprintf(stderr, "  select thread-0 cycles: counts %.0f scan %.0f emit %.0f\n", cyc[0], cyc[1],
-                        cyc[2]);
-                if (*tr == '2') {  // per-CTA dump: cta, smid, stamps (us)
-                    FILE* f = fopen("gpurun_out/k3_trace.csv", "w");
-                    if (f) {
-                        fprintf(f, "cta,smid,start,stream,thresh,prefix,rec,counts,scan,emit,end\n");
-                        for (uint32_t i = 0; i < G; ++i) {
-                            fprintf(f, "%u,%llu", i, (unsigned long long)h[i * kSlots + 6]);
-                            for (int j = 0; j < 9; ++j) {
-                                const uint64_t raw = h[i * kSlots + cols[j]];
-                                fprintf(f, ",%.3f", raw ? (double)(raw - t0) / 1000.0 : 0.0);
-                            }
-                            fprintf(f, "\n");
-                        }
-                        fclose(f);
-                    }
-                }
-            }
+            if (dtrace) k3_trace_report(dtrace, G, fp.pl.g.S, s);
             return st;
         }
     }
@@ -1901,10 +1906,10 @@ spl_status hamming_topk_sharded_impl(spl_ctx* ctx, spl_peer* peer, const uint32_
     bool ok = false;
     K3FPlan fp{};
     if ((st = make_fused_plan(ctx, P, n_max, L, codes, stride_rows, &ok, &fp, true))) return st;
-    if (!ok)
+    if (!ok || (size_t)peer->R * (L + 2) * 4 > K3_SEL_SCRATCH_BYTES)
         return fail(ctx, SPL_E_STATE,
-                    "hamming_topk_sharded: the local cache does not fit the fused path; use "
-                    "spl_shard_histogram + collective + spl_shard_select");
+                    "hamming_topk_sharded: the local cache (or R x (L + 2) histogram words) does not "
+                    "fit the fused path; use spl_shard_histogram + collective + spl_shard_select");
     K3Ws ws;
     if ((st = k3_workspace(ctx, fp.pl, L, s, &ws, false))) return st;
     K3Params prm = base_params(ctx, fp.pl, ws, kst, codes, stride_rows, L, qcodes, n_valid, nvalid_div, k);
@@ -1921,11 +1926,18 @@ spl_status hamming_topk_sharded_impl(spl_ctx* ctx, spl_peer* peer, const uint32_
     prm.epoch = ++peer->epoch;
     if (prm.epoch == 0) prm.epoch = ++peer->epoch;  // 0 = never written
     prm.out_offset = out_offset;
-    // the exchange layout is sized for Lmax: slots are (Lmax + 2) words
-    prm.L = L;
+    const char* tr = getenv("SPL_K3_TRACE");
+    uint64_t* dtrace = nullptr;
+    if (tr && *tr && !stream_capturing(s)) {
+        SPL_CUDA_TRY(ctx, cudaMalloc(&dtrace, (size_t)fp.pl.g.G * 16 * 8));
+        SPL_CUDA_TRY(ctx, cudaMemsetAsync(dtrace, 0, (size_t)fp.pl.g.G * 16 * 8, s));
+    }
+    prm.trace = dtrace;
     void* args[] = {&prm};
     SPL_CUDA_TRY(ctx, cudaLaunchKernel(fp.fn, dim3(fp.pl.g.G), dim3(kThreads), args, fp.smem, s));
-    return after_launch(ctx, "k3_fused_shard");
+    st = after_launch(ctx, "k3_fused_shard");
+    if (dtrace) k3_trace_report(dtrace, fp.pl.g.G, fp.pl.g.S, s);
+    return st;
 }
 
 }  // namespace spl

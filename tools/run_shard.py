@@ -54,4 +54,14 @@ def timeit(fn, reps=30):
 th = timeit(hist_phase)
 ts = timeit(lambda: (hist_phase(), select_phase()))
 print(f"R={R}: shard_histogram {th:.1f} us, histogram + select (incl. copy) {ts:.1f} us")
+# fused in-kernel exchange, a single-rank group (exchange with itself)
+peer = ctx.peer(1, 0, P, L)
+capi.Peer.connect_local(ctx, [peer])
+k1 = int(0.02 * n)
+idx1 = torch.zeros((P, k1), dtype=torch.int32, device=dev)
+tf = timeit(lambda: ctx.hamming_topk_sharded(peer, codes, n, L, q, P, nv, 1, n, k1, idx1, cnt, off,
+                                             s.cuda_stream))
+tu = timeit(lambda: ctx.hamming_topk(codes, n, L, q, P, nv, 1, n, k1, idx1, cnt, s.cuda_stream))
+print(f"fused sharded (R=1 group) {tf:.1f} us vs single-GPU fused {tu:.1f} us (eager)")
+peer.close()
 ctx.close()
