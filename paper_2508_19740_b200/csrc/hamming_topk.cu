@@ -628,11 +628,13 @@ __device__ void select_rows(const ScoreT* sc, uint64_t a0, uint64_t r0, uint64_t
 // masked with 0x01010101 << i and OR-ed (IADD, SHF, LOP3), so bit 8b + i of
 // a vector's mask is row 4b + i.
 // scratch: kThreads x NV words of shared memory (the private counters,
-// free once the stream is over).
+// free once the stream is over). NV = 3 for short segments (<= 12 K rows,
+// e.g. the config-2 decode shape): the per-thread work is unrolled over NV
+// vectors whether they hold rows or not.
+template <int NV>
 __device__ void select_rows_t8(const uint8_t* sc, uint64_t a0, uint64_t r0, uint64_t r1,
                                uint32_t T, uint32_t take, uint32_t* out, uint64_t* s_warp,
                                uint32_t* scratch, uint64_t* tr = nullptr) {
-    constexpr int NV = 11;
     constexpr int CH = 16 * NV;  // rows per thread per round
     // T == 0: every row is >= T (x + 128 would carry for x = 128);
     // T >= 128: no row is > T
@@ -1245,11 +1247,16 @@ __global__ void __launch_bounds__(kThreads, 3) k3_fused(K3Params prm) {
         const uint64_t off = gt_before + (eq_before < quota ? eq_before : quota);
         K3_STAMP(8);
         if (prm.trace && threadIdx.x == 0) prm.trace[blockIdx.x * 16 + 12] = clock64();
-        if constexpr (sizeof(ScoreT) == 1)
-            select_rows_t8(reinterpret_cast<const uint8_t*>(sc), a0, r0, r1, T, take,
-                           prm.idx_out + (uint64_t)p * prm.idx_stride + off, s_warp,
-                           reinterpret_cast<uint32_t*>(priv),
-                           prm.trace ? prm.trace + (uint64_t)blockIdx.x * 16 : nullptr);
+        if constexpr (sizeof(ScoreT) == 1) {
+            uint32_t* o = prm.idx_out + (uint64_t)p * prm.idx_stride + off;
+            uint64_t* trp = prm.trace ? prm.trace + (uint64_t)blockIdx.x * 16 : nullptr;
+            if (r1 - a0 <= (uint64_t)kThreads * 16 * 3)  // uniform
+                select_rows_t8<3>(reinterpret_cast<const uint8_t*>(sc), a0, r0, r1, T, take, o,
+                                  s_warp, reinterpret_cast<uint32_t*>(priv), trp);
+            else
+                select_rows_t8<11>(reinterpret_cast<const uint8_t*>(sc), a0, r0, r1, T, take, o,
+                                   s_warp, reinterpret_cast<uint32_t*>(priv), trp);
+        }
         else
             select_rows<ScoreT, false>(sc, a0, r0, r1, T, take,
                                        prm.idx_out + (uint64_t)p * prm.idx_stride + off, s_warp);
