@@ -118,6 +118,12 @@ spl_status spl_oracle_topk(spl_ctx* ctx, const float* q, const void* keys, int k
                            uint64_t cap, uint32_t d, uint32_t P, const uint32_t* n_valid,
                            uint32_t nvalid_div, uint64_t n_max, float scale, uint32_t k,
                            uint32_t* idx, uint32_t* cnt, float* logits, void* stream);
+/* matmul (matrix.hpp:81-99) with the reference build's arithmetic (per
+ * output, fma over the inner index in order): c[m][n] = a[m][k] . b[k][n],
+ * row-major f32. downproj_topk (attention_eval.cpp:183-206) = this for keys
+ * and queries, then spl_oracle_topk on the projections with scale 1. */
+spl_status spl_project(spl_ctx* ctx, const float* a, uint64_t m, uint32_t k, const float* b,
+                       uint32_t n, float* c, void* stream);
 /* iou (attention_eval.hpp:63, attention_eval.cpp:216-232) per problem of two
  * ascending index lists a[p][0..cnt_a[p]) and b[p][0..cnt_b[p]) (row strides
  * a_stride, b_stride): |a ∩ b| / |a ∪ b| as double, 1.0 when both are empty. */

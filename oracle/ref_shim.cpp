@@ -255,6 +255,71 @@ int spotref_oracle_topk(const float* queries, std::uint32_t q, const float* keys
     });
 }
 
+// downproj_topk (attention_eval.cpp:183-206); proj d x r.
+int spotref_downproj_topk(const float* queries, std::uint32_t q, const float* keys,
+                          std::uint32_t n, std::uint32_t d, const float* proj, std::uint32_t r,
+                          const std::uint32_t* offsets, std::uint32_t k, std::uint32_t* out,
+                          std::uint32_t* counts) {
+    return guard([&] {
+        AttentionInstance inst;
+        inst.queries = mat(queries, q, d);
+        inst.keys = mat(keys, n, d);
+        inst.values = mat(keys, n, d);
+        inst.scale = 1.0f;
+        inst.causal_offsets.assign(offsets, offsets + q);
+        DownProjEstimator est;
+        est.projection = mat(proj, d, r);
+        const RetrievalResult res = downproj_topk(inst, est, k);
+        for (std::uint32_t i = 0; i < q; ++i) {
+            counts[i] = static_cast<std::uint32_t>(res.indices[i].size());
+            std::memcpy(out + std::size_t(i) * k, res.indices[i].data(),
+                        sizeof(std::uint32_t) * res.indices[i].size());
+        }
+    });
+}
+
+// evaluate (attention_eval.cpp:285-353) over four methods in this order:
+// oracle, mlp (w1 b1 w2), downproj (proj d x r), frozen. stats[4][6] =
+// mean_iou, p10, p50, p90, mean_rel_err, max_rel_err; *budget = k.
+int spotref_evaluate(const float* queries, std::uint32_t q, const float* keys, const float* values,
+                     std::uint32_t n, std::uint32_t d, float scale, const std::uint32_t* offsets,
+                     double rate, const float* w1, const float* b1, const float* w2,
+                     std::uint32_t h, std::uint32_t L, const float* proj, std::uint32_t r,
+                     double* stats, std::uint32_t* budget) {
+    return guard([&] {
+        AttentionInstance inst;
+        inst.queries = mat(queries, q, d);
+        inst.keys = mat(keys, n, d);
+        inst.values = mat(values, n, d);
+        inst.scale = scale;
+        inst.causal_offsets.assign(offsets, offsets + q);
+        const AnyHasher mlp = make_mlp(w1, b1, w2, d, h, L);
+        DownProjEstimator est;
+        est.projection = mat(proj, d, r);
+        const AnyHasher dp = est;
+        std::vector<EvalMethodSpec> ms(4);
+        ms[0].name = "oracle";
+        ms[0].kind = RetrievalMethod::oracle;
+        ms[1].name = "mlp";
+        ms[1].kind = RetrievalMethod::mlp;
+        ms[1].hasher = &mlp;
+        ms[2].name = "downproj";
+        ms[2].kind = RetrievalMethod::downproj;
+        ms[2].hasher = &dp;
+        ms[3].name = "full";
+        ms[3].kind = RetrievalMethod::oracle;
+        ms[3].frozen = true;
+        const EvalReport rep = evaluate(inst, ms, rate);
+        *budget = rep.budget;
+        for (int i = 0; i < 4; ++i) {
+            const MethodReport& m = rep.methods[i];
+            const double v[6] = {m.mean_iou, m.p10_iou, m.p50_iou, m.p90_iou, m.mean_rel_err,
+                                 m.max_rel_err};
+            for (int j = 0; j < 6; ++j) stats[i * 6 + j] = v[j];
+        }
+    });
+}
+
 // iou (attention_eval.cpp:216-232) of two ascending index lists.
 double spotref_iou(const std::uint32_t* a, std::uint32_t na, const std::uint32_t* b,
                    std::uint32_t nb) {

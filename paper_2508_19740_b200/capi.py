@@ -102,6 +102,7 @@ _SIGS = {
     "spl_budget_from_rate": [dbl, u64, u32p],
     "spl_oracle_topk": [vp, vp, vp, i32, u64, u32, u32, vp, u32, u64, f32, u32, vp, vp, vp, vp],
     "spl_iou": [vp, vp, vp, u64, vp, vp, u64, u32, vp, vp],
+    "spl_project": [vp, vp, u64, u32, vp, u32, vp, vp],
     "spl_peer_create": [vp, u32, u32, u32, u32, C.POINTER(vp)],
     "spl_peer_ipc_handle": [vp, vp, vp],
     "spl_peer_open": [vp, vp, vp],
@@ -249,6 +250,10 @@ class Context:
         self.check(self.lib.spl_oracle_topk(self.h, _ptr(q), _ptr(keys), kv_dtype, cap, d, P,
                                             _ptr(n_valid), nvalid_div, n_max, scale, k, _ptr(idx),
                                             _ptr(cnt), _ptr(logits), _stream(stream)))
+
+    def project(self, a, m, k, b, n, c, stream=None):
+        """c[m][n] = a[m][k] . b[k][n] with the reference matmul's FMA order."""
+        self.check(self.lib.spl_project(self.h, _ptr(a), m, k, _ptr(b), n, _ptr(c), _stream(stream)))
 
     def iou(self, a, cnt_a, a_stride, b, cnt_b, b_stride, P, out, stream=None):
         self.check(self.lib.spl_iou(self.h, _ptr(a), _ptr(cnt_a), a_stride, _ptr(b), _ptr(cnt_b),

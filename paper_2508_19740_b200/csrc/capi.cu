@@ -342,6 +342,14 @@ spl_status spl_oracle_topk(spl_ctx* ctx, const float* q, const void* keys, int k
                         cnt);
 }
 
+spl_status spl_project(spl_ctx* ctx, const float* a, uint64_t m, uint32_t k, const float* b,
+                       uint32_t n, float* c, void* stream) {
+    if (!ctx) return SPL_E_STATE;
+    if (k == 0) return fail(ctx, SPL_E_DIMENSION, "matmul: inner dimension must be >= 1");
+    if (m && n && (!a || !b || !c)) return fail(ctx, SPL_E_STATE, "matmul: null device pointer");
+    return project_launch(ctx, a, m, k, b, n, c, S(stream));
+}
+
 spl_status spl_iou(spl_ctx* ctx, const uint32_t* a, const uint32_t* cnt_a, uint64_t a_stride,
                    const uint32_t* b, const uint32_t* cnt_b, uint64_t b_stride, uint32_t P,
                    double* out, void* stream) {

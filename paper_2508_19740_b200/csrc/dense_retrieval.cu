@@ -107,7 +107,31 @@ __global__ void __launch_bounds__(256) k_iou(const uint32_t* a, const uint32_t* 
     }
 }
 
+// matmul (matrix.hpp:81-99) as the reference build computes it: every
+// output c[i][j] starts at 0 and takes fma(a[i][p], b[p][j], c) for p = 0..k-1
+// in order. One thread per output; b (k x n, row-major) is read coalesced.
+__global__ void __launch_bounds__(256) k_project(const float* __restrict__ a, uint64_t m,
+                                                 uint32_t k, const float* __restrict__ b,
+                                                 uint32_t n, float* __restrict__ c) {
+    const uint64_t i = blockIdx.y;
+    const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= m || j >= n) return;
+    const float* ar = a + i * k;
+    float acc = 0.0f;
+    for (uint32_t p = 0; p < k; ++p) acc = __fmaf_rn(__ldg(ar + p), __ldg(b + (uint64_t)p * n + j), acc);
+    c[i * n + j] = acc;
+}
+
 }  // namespace
+
+spl_status project_launch(spl_ctx* ctx, const float* a, uint64_t m, uint32_t k, const float* b,
+                          uint32_t n, float* c, cudaStream_t s) {
+    if (m == 0 || n == 0) return SPL_OK;
+    if (m > 0xFFFFFFFFull / 2) return fail(ctx, SPL_E_DIMENSION, "matmul: too many rows");
+    const dim3 grid((n + 255) / 256, (unsigned)m);
+    k_project<<<grid, 256, 0, s>>>(a, m, k, b, n, c);
+    return after_launch(ctx, "k_project");
+}
 
 spl_status causal_logits_launch(spl_ctx* ctx, const float* q, const void* keys, int kv_dtype,
                                 uint64_t cap, uint32_t d, uint32_t P, const uint32_t* n_valid,

@@ -73,6 +73,8 @@ spl_status causal_logits_launch(spl_ctx*, const float* q, const void* keys, int 
                                 uint64_t cap, uint32_t d, uint32_t P, const uint32_t* n_valid,
                                 uint32_t nvalid_div, uint64_t n_max, float scale, float* logits,
                                 cudaStream_t);
+spl_status project_launch(spl_ctx*, const float* a, uint64_t m, uint32_t k, const float* b,
+                          uint32_t n, float* c, cudaStream_t);
 spl_status iou_launch(spl_ctx*, const uint32_t* a, const uint32_t* cnt_a, uint64_t a_stride,
                       const uint32_t* b, const uint32_t* cnt_b, uint64_t b_stride, uint32_t P,
                       double* out, cudaStream_t);

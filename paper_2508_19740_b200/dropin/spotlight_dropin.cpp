@@ -12,6 +12,8 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <numeric>
+#include <sstream>
 #include <fstream>
 #include <memory>
 #include <random>
@@ -537,35 +539,86 @@ RetrievalResult hash_topk(const AttentionInstance& inst, const AnyHasher& hasher
     return res;
 }
 
-// oracle_topk (attention_eval.cpp:121-135): exact dense logits + float top-k
-// on the GPU (spl_oracle_topk), every query against the shared key matrix.
-RetrievalResult oracle_topk(const AttentionInstance& inst, std::uint32_t k) {
-    inst.validate();
-    if (k == 0) throw DimensionError("oracle_topk: k must be >= 1");
-    const auto q = static_cast<std::uint32_t>(inst.num_queries());
-    const auto n = static_cast<std::uint32_t>(inst.cache_size());
-    const auto d = static_cast<std::uint32_t>(inst.keys.cols());
-    RetrievalResult res;
-    res.method = RetrievalMethod::oracle;
-    res.budget = k;
-    res.indices.resize(q);
-    if (q == 0) return res;
-    DevBuf dqv(inst.queries.data(), inst.queries.size() * 4);
-    DevBuf dkv(inst.keys.data(), inst.keys.size() * 4);
-    DevBuf dn(inst.causal_offsets.data(), static_cast<std::size_t>(q) * 4);
+namespace {
+// Exact dense top-k of q x d queries against n x d keys (shared by all
+// queries, causal offsets per query) on the GPU: spl_oracle_topk.
+std::vector<std::vector<std::uint32_t>> dense_topk(const float* queries, std::uint32_t q,
+                                                   const float* keys, std::uint32_t n,
+                                                   std::uint32_t d, const std::uint32_t* offsets,
+                                                   float scale, std::uint32_t k) {
+    std::vector<std::vector<std::uint32_t>> out(q);
+    if (q == 0) return out;
+    DevBuf dqv(queries, static_cast<std::size_t>(q) * d * 4);
+    DevBuf dkv(keys, static_cast<std::size_t>(n) * d * 4);
+    DevBuf dn(offsets, static_cast<std::size_t>(q) * 4);
     DevBuf di(static_cast<std::size_t>(q) * k * 4);
     DevBuf dc(static_cast<std::size_t>(q) * 4);
     check(spl_oracle_topk(ctx(), dqv.as<float>(), dkv.as<float>(), SPL_F32, 0, d, q,
-                          dn.as<std::uint32_t>(), 1, n, inst.scale, k, di.as<std::uint32_t>(),
+                          dn.as<std::uint32_t>(), 1, n, scale, k, di.as<std::uint32_t>(),
                           dc.as<std::uint32_t>(), nullptr, nullptr));
     finish();
     std::vector<std::uint32_t> idx(static_cast<std::size_t>(q) * k), cnt(q);
     di.download(idx.data(), idx.size() * 4);
     dc.download(cnt.data(), cnt.size() * 4);
     for (std::uint32_t r = 0; r < q; ++r)
-        res.indices[r].assign(idx.begin() + static_cast<std::size_t>(r) * k,
-                              idx.begin() + static_cast<std::size_t>(r) * k + cnt[r]);
+        out[r].assign(idx.begin() + static_cast<std::size_t>(r) * k,
+                      idx.begin() + static_cast<std::size_t>(r) * k + cnt[r]);
+    return out;
+}
+
+// matmul (matrix.hpp:81-99) on the GPU with the reference's FMA order.
+Matrix<float> project(const Matrix<float>& a, const Matrix<float>& b) {
+    const auto m = a.rows(), k = a.cols(), n = b.cols();
+    Matrix<float> c(m, n);
+    if (m == 0 || n == 0) return c;
+    DevBuf da(a.data(), a.size() * 4), db(b.data(), b.size() * 4), dc(c.size() * 4);
+    check(spl_project(ctx(), da.as<float>(), m, static_cast<std::uint32_t>(k), db.as<float>(),
+                      static_cast<std::uint32_t>(n), dc.as<float>(), nullptr));
+    finish();
+    dc.download(c.data(), c.size() * 4);
+    return c;
+}
+}  // namespace
+
+// oracle_topk (attention_eval.cpp:121-135): exact dense logits + float top-k
+// on the GPU (spl_oracle_topk), every query against the shared key matrix.
+RetrievalResult oracle_topk(const AttentionInstance& inst, std::uint32_t k) {
+    inst.validate();
+    if (k == 0) throw DimensionError("oracle_topk: k must be >= 1");
+    RetrievalResult res;
+    res.method = RetrievalMethod::oracle;
+    res.budget = k;
+    res.indices = dense_topk(inst.queries.data(), static_cast<std::uint32_t>(inst.num_queries()),
+                             inst.keys.data(), static_cast<std::uint32_t>(inst.cache_size()),
+                             static_cast<std::uint32_t>(inst.keys.cols()),
+                             inst.causal_offsets.data(), inst.scale, k);
     return res;
+}
+
+// downproj_topk (attention_eval.cpp:183-206): keys and queries projected by
+// the estimator (the reference matmul, GPU), scores = dot of the projections
+// (the causal_logits arithmetic with scale 1, exact), float top-k.
+RetrievalResult downproj_topk(const AttentionInstance& inst, const DownProjEstimator& est,
+                              std::uint32_t k) {
+    inst.validate();
+    if (k == 0) throw DimensionError("downproj_topk: k must be >= 1");
+    if (inst.keys.cols() != est.input_dim())
+        throw DimensionError("downproj_topk: estimator dimension mismatch");
+    const Matrix<float> kp = project(inst.keys, est.projection);
+    const Matrix<float> qp = project(inst.queries, est.projection);
+    RetrievalResult res;
+    res.method = RetrievalMethod::downproj;
+    res.budget = k;
+    res.indices = dense_topk(qp.data(), static_cast<std::uint32_t>(qp.rows()), kp.data(),
+                             static_cast<std::uint32_t>(kp.rows()), est.reduced_dim(),
+                             inst.causal_offsets.data(), 1.0f, k);
+    return res;
+}
+
+RetrievalResult retrieval_topk(const AttentionInstance& inst, const AnyHasher& hasher,
+                               std::uint32_t k) {
+    if (const auto* dp = std::get_if<DownProjEstimator>(&hasher)) return downproj_topk(inst, *dp, k);
+    return hash_topk(inst, hasher, k);
 }
 
 namespace {
@@ -662,6 +715,130 @@ std::uint32_t budget_from_rate(double rate, std::size_t n) {
     if (spl_budget_from_rate(rate, n, &k) != SPL_OK)
         throw DimensionError("budget_from_rate: rate must lie in (0, 1]");
     return k;
+}
+
+namespace {
+// percentile over ascending values (attention_eval.cpp:276-281): nearest rank
+// round(p (size - 1)).
+double percentile_sorted(const std::vector<double>& v, double p) {
+    if (v.empty()) return 0.0;
+    const auto rank = static_cast<std::size_t>(p * static_cast<double>(v.size() - 1) + 0.5);
+    return v[std::min(rank, v.size() - 1)];
+}
+// norm2<float> (matrix.hpp:152-155): sqrt of the float dot, in order.
+double norm2f(std::span<const float> a) {
+    float acc = 0.0f;
+    for (float x : a) acc += x * x;
+    return static_cast<double>(std::sqrt(acc));
+}
+}  // namespace
+
+// evaluate (attention_eval.cpp:285-353): every method at the rate-derived
+// budget; per-query IoU against the oracle top-k, output error against full
+// attention. Retrieval, attention and the oracle run on the GPU; the
+// statistics are host arithmetic over their results.
+EvalReport evaluate(const AttentionInstance& inst, std::span<const EvalMethodSpec> methods,
+                    double budget_rate) {
+    inst.validate();
+    const std::uint32_t k = budget_from_rate(budget_rate, inst.cache_size());
+    const RetrievalResult oracle = oracle_topk(inst, k);
+    const Matrix<float> full = full_attention(inst);
+    const std::size_t nq = inst.num_queries();
+    std::vector<double> full_norms(nq);
+    for (std::size_t r = 0; r < nq; ++r) full_norms[r] = norm2f(full.row(r));
+    EvalReport report;
+    report.budget = k;
+    report.budget_rate = budget_rate;
+    for (const EvalMethodSpec& spec : methods) {
+        RetrievalResult res;
+        if (spec.frozen) {  // every valid row
+            res.method = spec.kind;
+            res.budget = k;
+            res.indices.resize(nq);
+            for (std::size_t r = 0; r < nq; ++r) {
+                res.indices[r].resize(inst.causal_offsets[r]);
+                std::iota(res.indices[r].begin(), res.indices[r].end(), 0u);
+            }
+        } else if (spec.kind == RetrievalMethod::oracle) {
+            res = oracle;
+        } else {
+            if (!spec.hasher)
+                throw DimensionError("evaluate: method \"" + spec.name + "\" needs a hasher");
+            res = retrieval_topk(inst, *spec.hasher, k);
+        }
+        MethodReport mr;
+        mr.name = spec.name;
+        mr.kind = spec.kind;
+        mr.budget = k;
+        mr.frozen = spec.frozen;
+        mr.per_query_iou.resize(nq);
+        const Matrix<float> sparse = sparse_attention(inst, res);
+        double iou_sum = 0.0, err_sum = 0.0, err_max = 0.0;
+        for (std::size_t r = 0; r < nq; ++r) {
+            mr.per_query_iou[r] = iou(res.indices[r], oracle.indices[r]);
+            iou_sum += mr.per_query_iou[r];
+            double d2 = 0.0;
+            for (std::size_t c = 0; c < full.cols(); ++c) {
+                const double dl = static_cast<double>(sparse(r, c)) - static_cast<double>(full(r, c));
+                d2 += dl * dl;
+            }
+            const double rel = full_norms[r] > 0.0 ? std::sqrt(d2) / full_norms[r] : std::sqrt(d2);
+            err_sum += rel;
+            err_max = std::max(err_max, rel);
+        }
+        mr.mean_iou = iou_sum / static_cast<double>(nq);
+        mr.mean_rel_err = err_sum / static_cast<double>(nq);
+        mr.max_rel_err = err_max;
+        std::vector<double> sorted = mr.per_query_iou;
+        std::sort(sorted.begin(), sorted.end());
+        mr.p10_iou = percentile_sorted(sorted, 0.10);
+        mr.p50_iou = percentile_sorted(sorted, 0.50);
+        mr.p90_iou = percentile_sorted(sorted, 0.90);
+        report.methods.push_back(std::move(mr));
+    }
+    return report;
+}
+
+// format_eval_report (attention_eval.cpp:355-373): provenance lines, budget,
+// one record per method — same fields and number formats.
+std::string format_eval_report(const EvalReport& report, std::span<const std::string> header_lines) {
+    std::string out;
+    for (const std::string& h : header_lines) out += "# " + h + "\n";
+    char buf[320];
+    std::snprintf(buf, sizeof(buf), "budget %u\n", report.budget);
+    out += buf;
+    {
+        std::ostringstream os;
+        os << report.budget_rate;  // default stream formatting, as the reference prints it
+        out += "budget_rate " + os.str() + "\n";
+    }
+    for (const MethodReport& m : report.methods) {
+        std::snprintf(buf, sizeof(buf),
+                      "method %s kind=%s budget=%u frozen=%d mean_iou=%.6f p10=%.6f p50=%.6f "
+                      "p90=%.6f mean_rel_err=%.6e max_rel_err=%.6e\n",
+                      m.name.c_str(), retrieval_method_name(m.kind), m.budget, m.frozen ? 1 : 0,
+                      m.mean_iou, m.p10_iou, m.p50_iou, m.p90_iou, m.mean_rel_err, m.max_rel_err);
+        out += buf;
+    }
+    return out;
+}
+
+// eval_report_csv (attention_eval.cpp:375-391): per-query IoU, one column per method.
+std::string eval_report_csv(const EvalReport& report) {
+    std::string out = "query";
+    for (const MethodReport& m : report.methods) out += "," + m.name;
+    out += "\n";
+    if (report.methods.empty()) return out;
+    char buf[32];
+    for (std::size_t r = 0; r < report.methods.front().per_query_iou.size(); ++r) {
+        out += std::to_string(r);
+        for (const MethodReport& m : report.methods) {
+            std::snprintf(buf, sizeof(buf), ",%.6f", m.per_query_iou[r]);
+            out += buf;
+        }
+        out += "\n";
+    }
+    return out;
 }
 
 }  // namespace spotlight

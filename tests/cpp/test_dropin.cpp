@@ -365,6 +365,13 @@ struct Ref {
                   const std::uint64_t*, float*) = nullptr;
     int (*oracle)(const float*, std::uint32_t, const float*, std::uint32_t, std::uint32_t, float,
                   const std::uint32_t*, std::uint32_t, std::uint32_t*, std::uint32_t*) = nullptr;
+    int (*downproj)(const float*, std::uint32_t, const float*, std::uint32_t, std::uint32_t,
+                    const float*, std::uint32_t, const std::uint32_t*, std::uint32_t,
+                    std::uint32_t*, std::uint32_t*) = nullptr;
+    int (*evaluate)(const float*, std::uint32_t, const float*, const float*, std::uint32_t,
+                    std::uint32_t, float, const std::uint32_t*, double, const float*,
+                    const float*, const float*, std::uint32_t, std::uint32_t, const float*,
+                    std::uint32_t, double*, std::uint32_t*) = nullptr;
     Ref() {
         const char* p = std::getenv("SPOTREF_SO");
         h = dlopen(p ? p : "oracle/_ref/libspotref.so", RTLD_NOW | RTLD_LOCAL);
@@ -373,8 +380,71 @@ struct Ref {
         hash_topk = reinterpret_cast<decltype(hash_topk)>(dlsym(h, "spotref_hash_topk_mlp"));
         sparse = reinterpret_cast<decltype(sparse)>(dlsym(h, "spotref_sparse_attention"));
         oracle = reinterpret_cast<decltype(oracle)>(dlsym(h, "spotref_oracle_topk"));
+        downproj = reinterpret_cast<decltype(downproj)>(dlsym(h, "spotref_downproj_topk"));
+        evaluate = reinterpret_cast<decltype(evaluate)>(dlsym(h, "spotref_evaluate"));
     }
 };
+
+TEST_CASE("downproj_topk and evaluate: exact retrieval, report statistics, formatting") {
+    std::mt19937_64 eng(91);
+    const std::uint32_t n = 700, d = 64, r = 16, L = 128;
+    AttentionInstance inst = make_causal_instance(random_matrix(n, d, eng), random_matrix(n, d, eng),
+                                                  random_matrix(n, d, eng));
+    DownProjEstimator est{random_matrix(d, r, eng)};
+    const RetrievalResult dp = downproj_topk(inst, est, 40);
+    CHECK(dp.method == RetrievalMethod::downproj);
+    CHECK(dp.indices[n - 1].size() == 40);
+    CHECK_THROWS_AS(downproj_topk(inst, est, 0), DimensionError);
+    CHECK_THROWS_AS(downproj_topk(inst, DownProjEstimator{random_matrix(d + 1, r, eng)}, 4),
+                    DimensionError);
+    const MlpHasher mh = mlp_gaussian_init(d, d, L, 64.0f, 12);
+    const AnyHasher mlp = mh, dph = est;
+    std::vector<EvalMethodSpec> ms(4);
+    ms[0].name = "oracle";
+    ms[1].name = "mlp";
+    ms[1].kind = RetrievalMethod::mlp;
+    ms[1].hasher = &mlp;
+    ms[2].name = "downproj";
+    ms[2].kind = RetrievalMethod::downproj;
+    ms[2].hasher = &dph;
+    ms[3].name = "full";
+    ms[3].frozen = true;
+    const EvalReport rep = evaluate(inst, ms, 0.05);
+    CHECK(rep.budget == budget_from_rate(0.05, n));
+    CHECK(rep.methods.size() == 4);
+    CHECK(rep.methods[0].mean_iou == 1.0);            // the oracle against itself
+    CHECK(rep.methods[3].max_rel_err < 1e-5);         // every row attended == full attention
+    const std::vector<std::string> hdr = {"provenance line"};
+    const std::string txt = format_eval_report(rep, hdr);
+    CHECK(txt.rfind("# provenance line\nbudget ", 0) == 0);
+    CHECK(txt.find("method mlp kind=mlp budget=") != std::string::npos);
+    CHECK(eval_report_csv(rep).rfind("query,oracle,mlp,downproj,full\n0,", 0) == 0);
+    static Ref ref;
+    if (!ref.h || !ref.downproj || !ref.evaluate) return;
+    std::vector<std::uint32_t> ridx(static_cast<std::size_t>(n) * 40), rcnt(n);
+    CHECK(ref.downproj(inst.queries.data(), n, inst.keys.data(), n, d, est.projection.data(), r,
+                       inst.causal_offsets.data(), 40, ridx.data(), rcnt.data()) == 0);
+    bool same = true;
+    for (std::uint32_t q = 0; q < n; ++q)
+        same = same && dp.indices[q] == std::vector<std::uint32_t>(ridx.begin() + q * 40,
+                                                                   ridx.begin() + q * 40 + rcnt[q]);
+    CHECK(same);
+    double st[24];
+    std::uint32_t kb = 0;
+    CHECK(ref.evaluate(inst.queries.data(), n, inst.keys.data(), inst.values.data(), n, d,
+                       inst.scale, inst.causal_offsets.data(), 0.05, mh.w1.data(), mh.b1.data(),
+                       mh.w2.data(), d, L, est.projection.data(), r, st, &kb) == 0);
+    CHECK(kb == rep.budget);
+    for (int i = 0; i < 4; ++i) {
+        const MethodReport& m = rep.methods[i];
+        // IoU statistics are exact (bit-identical index sets); the output
+        // errors follow the attention tolerance (fp32, <= 1e-5 max-abs)
+        CHECK(m.mean_iou == st[i * 6] && m.p10_iou == st[i * 6 + 1] && m.p50_iou == st[i * 6 + 2] &&
+              m.p90_iou == st[i * 6 + 3]);
+        CHECK(std::fabs(m.mean_rel_err - st[i * 6 + 4]) <= 1e-5 + 1e-3 * st[i * 6 + 4]);
+        CHECK(std::fabs(m.max_rel_err - st[i * 6 + 5]) <= 1e-5 + 1e-3 * st[i * 6 + 5]);
+    }
+}
 
 TEST_CASE("oracle_topk: exact logits top-k, causal clamp, rejection; iou vs hash_topk") {
     std::mt19937_64 eng(77);
