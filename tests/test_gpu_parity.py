@@ -607,3 +607,71 @@ def test_fused_sharded_low_threshold_round(oracle):
     codes[0] = (~q[0])[None, :] ^ (~keep & rng.integers(0, 2**32, (N, W), dtype=np.uint64).astype(np.uint32))
     for k in (50, 23000):
         _run_fused_sharded(oracle, 3, P, N, W, k, codes, q, trials=1)
+
+
+def test_topk_config4_full_batch(ctx, oracle):
+    """Config 4 at full size: B = 16 x 32 heads x 131072 rows x 256-bit codes,
+    k = 2621 (two-pass path: u8 scores clamped at 255, windowed counters),
+    every one of the 512 problems bit-exact against the oracle."""
+    B, H, n, W = 16, 32, 131072, 8
+    P = B * H
+    k = oracle.budget_from_rate(0.02, n)
+    g = torch.Generator(device=DEV)
+    g.manual_seed(404)
+    codes = torch.randint(-2**31, 2**31 - 1, (P, n, W), generator=g, device=DEV, dtype=torch.int32)
+    q = torch.randint(-2**31, 2**31 - 1, (P, W), generator=g, device=DEV, dtype=torch.int32)
+    nvb = np.array([n - 37 * b for b in range(B)], np.uint32)  # ragged per sequence
+    idx = torch.full((P, k), -1, dtype=torch.int32, device=DEV)
+    cnt = torch.zeros(P, dtype=torch.int32, device=DEV)
+    ctx.hamming_topk(codes, n, W * 32, q, P, T(nvb), H, n, k, idx, cnt)
+    torch.cuda.synchronize()
+    ctx.check_device_error()
+    want = oracle.retrieve_batch(U(codes), U(q), np.repeat(nvb, H), k)
+    got = U(idx)
+    assert np.array_equal(U(cnt), np.full(P, k, np.uint32))
+    assert np.array_equal(got, want)
+
+
+def test_sharded_config5_full(oracle):
+    """Config 5 at full size: a 4M-token cache of 32 heads x 128-bit codes
+    split over 8 ranks (the two-kernel flow, ranks run one after another on
+    this GPU; the all-gather is a device stack), k = 2% of 4M = 83886. The
+    rank-order concatenation equals the single-GPU reference list."""
+    R, P, N, W = 8, 32, 4194304, 4
+    L = W * 32
+    k = oracle.budget_from_rate(0.02, N)
+    g = torch.Generator(device=DEV)
+    g.manual_seed(505)
+    codes = torch.randint(-2**31, 2**31 - 1, (P, N, W), generator=g, device=DEV, dtype=torch.int32)
+    q = torch.randint(-2**31, 2**31 - 1, (P, W), generator=g, device=DEV, dtype=torch.int32)
+    n_r = N // R
+    ctx = capi.Context(0)
+    hists = []
+    for r in range(R):
+        part = codes[:, r * n_r:(r + 1) * n_r].contiguous()
+        h = torch.zeros((P, L + 1), dtype=torch.int32, device=DEV)
+        ctx.shard_histogram(part, n_r, L, q, P, T(np.full(P, n_r, np.uint32)), 1, n_r, h)
+        hists.append(h)
+        del part
+    all_hist = torch.stack(hists)
+    got = [[] for _ in range(P)]
+    for r in range(R):
+        part = codes[:, r * n_r:(r + 1) * n_r].contiguous()
+        ctx.shard_histogram(part, n_r, L, q, P, T(np.full(P, n_r, np.uint32)), 1, n_r, hists[r])
+        idx = torch.zeros((P, k), dtype=torch.int32, device=DEV)
+        cnt = torch.zeros(P, dtype=torch.int32, device=DEV)
+        off = torch.zeros(P, dtype=torch.int32, device=DEV)
+        ctx.shard_select(all_hist, R, r, L, P, T(np.full(P, n_r, np.uint32)), 1, n_r, k, idx, cnt, off)
+        torch.cuda.synchronize()
+        ia, ca, oa = U(idx), U(cnt), U(off)
+        for p in range(P):
+            got[p].append((int(oa[p]), ia[p, :ca[p]].astype(np.int64) + r * n_r))
+        del part
+    ctx.check_device_error()
+    ctx.close()
+    want = oracle.retrieve_batch(U(codes), U(q), np.full(P, N, np.uint32), k)
+    for p in range(P):
+        parts = sorted(got[p])
+        cat = np.concatenate([x for _, x in parts]).astype(np.uint32)
+        assert [o for o, _ in parts] == list(np.cumsum([0] + [len(x) for _, x in parts[:-1]]))
+        assert np.array_equal(cat, want[p]), p
