@@ -385,6 +385,65 @@ struct Ref {
     }
 };
 
+// softmax weights of one query over its causal range (f64; monotone in the logits)
+static std::vector<double> soft_weights(const AttentionInstance& inst, std::size_t row) {
+    const std::size_t d = inst.keys.cols(), n = inst.causal_offsets[row];
+    std::vector<double> lg(n);
+    double mx = -1e300;
+    for (std::size_t j = 0; j < n; ++j) {
+        double a = 0.0;
+        for (std::size_t p = 0; p < d; ++p) a += double(inst.queries(row, p)) * inst.keys(j, p);
+        lg[j] = a * inst.scale;
+        mx = std::max(mx, lg[j]);
+    }
+    double s = 0.0;
+    for (double& v : lg) s += (v = std::exp(v - mx));
+    for (double& v : lg) v /= s;
+    return lg;
+}
+
+TEST_CASE("oracle_topk agrees with an exhaustive sort; one dropped key obeys the leak-mass relation") {
+    std::mt19937_64 eng(4242);
+    for (int iter = 0; iter < 30; ++iter) {
+        const std::size_t n = 5 + eng() % 60;
+        const AttentionInstance inst = random_instance(4, n, 8, eng, iter % 2 == 0);
+        const std::uint32_t k = 1 + eng() % 5;
+        const RetrievalResult res = oracle_topk(inst, k);
+        for (std::size_t row = 0; row < 4; ++row) {
+            const auto w = soft_weights(inst, row);
+            std::vector<std::uint32_t> order(w.size());
+            std::iota(order.begin(), order.end(), 0u);
+            std::sort(order.begin(), order.end(), [&](std::uint32_t a, std::uint32_t b) {
+                return w[a] != w[b] ? w[a] > w[b] : a < b;
+            });
+            order.resize(std::min<std::size_t>(k, w.size()));
+            std::sort(order.begin(), order.end());
+            CHECK(res.indices[row] == order);
+        }
+    }
+    for (int iter = 0; iter < 30; ++iter) {
+        const std::size_t n = 8 + eng() % 24;
+        const AttentionInstance inst = random_instance(1, n, 8, eng, false);
+        const RetrievalResult res = oracle_topk(inst, static_cast<std::uint32_t>(n - 1));
+        const auto w = soft_weights(inst, 0);
+        std::vector<char> kept(n, 0);
+        for (auto i : res.indices[0]) kept[i] = 1;
+        std::size_t drop = 0;
+        for (std::size_t j = 0; j < n; ++j)
+            if (!kept[j]) drop = j;
+        if (drop == n - 1) continue;  // the own row is always attended: nothing dropped
+        const Matrix<float> sp = sparse_attention(inst, res), full = full_attention(inst);
+        double diff2 = 0.0, gap2 = 0.0;
+        for (std::size_t p = 0; p < 8; ++p) {
+            const double dl = double(sp(0, p)) - full(0, p), g = double(inst.values(drop, p)) - sp(0, p);
+            diff2 += dl * dl;
+            gap2 += g * g;
+        }
+        // one dropped key: full - sparse == w_drop * (v_drop - sparse)
+        CHECK(std::fabs(std::sqrt(diff2) - w[drop] * std::sqrt(gap2)) <= 1e-3 * w[drop] * std::sqrt(gap2) + 1e-6);
+    }
+}
+
 TEST_CASE("downproj_topk and evaluate: exact retrieval, report statistics, formatting") {
     std::mt19937_64 eng(91);
     const std::uint32_t n = 700, d = 64, r = 16, L = 128;
