@@ -130,6 +130,23 @@ def event_timer(torch, fn, steps, stream):
     return start.elapsed_time(end) / steps  # ms per step
 
 
+def graph_timer(torch, fn, steps, warmup):
+    """Capture one call of fn (our kernels on a side stream) in a CUDA graph
+    and time `steps` replays; None if capture is not possible."""
+    try:
+        gs = torch.cuda.Stream()
+        gs.wait_stream(torch.cuda.current_stream())
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, stream=gs, capture_error_mode="relaxed"):
+            fn(gs)
+        for _ in range(warmup):
+            graph.replay()
+        torch.cuda.synchronize()
+        return event_timer(torch, graph.replay, steps, torch.cuda.current_stream())
+    except Exception:
+        return None
+
+
 # ---------------------------------------------------------------- CPU legs
 def cpu_reference_retrieval(codes_np, q_np, k, threads, reps, warmup):
     """The reference's retrieval (per head nxor_scores_into + top_k_indices,
@@ -541,16 +558,19 @@ def bench_decode4(torch, capi, ctx, dev, stream, args):
     out = torch.zeros((B, H, D), dtype=torch.float32, device=dev)
     scale = float(1 / np.sqrt(D))
 
-    def step():
+    def step(st=None):
         hs.decode_step(q, kn, vn, B, codes, kc, vc, capi.SPL_BF16, cap, nvalid, n, k, scale,
-                       idx, cnt, out, stream)
+                       idx, cnt, out, st if st is not None else stream)
 
     for _ in range(args.warmup):
         step()
     steps = min(args.steps, 20)
     l0 = ctx.launches()
-    ms = event_timer(torch, step, steps, stream)
+    eager_ms = event_timer(torch, step, steps, stream)
     launches = (ctx.launches() - l0) / steps
+    ctx.reserve(P, cap, L4, k, D)
+    g_ms = graph_timer(torch, lambda st: step(st), steps, args.warmup)
+    ms = g_ms if g_ms is not None else eager_ms
 
     qz = torch.randint(-2**31, 2**31 - 1, (P, W4), generator=g, device=dev, dtype=torch.int32)
 
@@ -563,6 +583,8 @@ def bench_decode4(torch, capi, ctx, dev, stream, args):
     return {"workload": "config4: B=16 x 32 heads, 131072-token bf16 K/V caches, 256-bit codes, "
                         "k=2621; append + encode + retrieve + attend",
             "us_per_step": round(ms * 1000, 2), "tok_per_s": round(B / (ms * 1e-3), 1),
+            "timing": "CUDA graph replay of one decode step" if g_ms is not None else "eager",
+            "eager_us_per_step": round(eager_ms * 1000, 2),
             "unit": "tok/s (one 32-head layer, 16 sequences)", "gpu_launches_per_step": launches,
             "retrieval_us": round(r_ms * 1000, 2),
             "roofline": {"bound": "hbm", "algorithmic_bytes": alg,
@@ -639,15 +661,18 @@ def bench_decode(torch, capi, ctx, dev, stream, args, hasher_c3):
     out = torch.zeros((B, H, D), dtype=torch.float32, device=dev)
     scale = float(1 / np.sqrt(D))
 
-    def step():
+    def step(st=None):
         hasher_c3.decode_step(q, kn, vn, B, codes, kc, vc, capi.SPL_BF16, cap, nvalid, n, k, scale,
-                              idx, cnt, out, stream)
+                              idx, cnt, out, st if st is not None else stream)
 
     for _ in range(args.warmup):
         step()
     l0 = ctx.launches()
-    ms = event_timer(torch, step, args.steps, stream)
+    eager_ms = event_timer(torch, step, args.steps, stream)
     launches = ctx.launches() - l0
+    ctx.reserve(P, cap, L, k, D)
+    g_ms = graph_timer(torch, lambda st: step(st), args.steps, args.warmup)
+    ms = g_ms if g_ms is not None else eager_ms
     # attention alone (same indices)
     def att():
         ctx.sparse_attend(q, kc, vc, capi.SPL_BF16, cap, D, P, idx, k, cnt, nvalid, H, scale, out, stream)
@@ -656,6 +681,8 @@ def bench_decode(torch, capi, ctx, dev, stream, args, hasher_c3):
     alg = P * n * W * 4 + P * (k + 1) * D * 2 * 2 + H * (D * D + D + D * L) * 4 + P * k * 4
     return {"workload": "config2: B=1, 32 heads, 131072-token bf16 K/V cache, 128-bit codes, k=2621",
             "us_per_step": round(ms * 1000, 2), "tok_per_s": round(B / (ms * 1e-3), 1),
+            "timing": "CUDA graph replay of one decode step" if g_ms is not None else "eager",
+            "eager_us_per_step": round(eager_ms * 1000, 2),
             "unit": "tok/s (one 32-head layer)", "gpu_launches_per_step": launches / args.steps,
             "attend_us": round(att_ms * 1000, 2),
             "roofline": {"bound": "hbm", "algorithmic_bytes": alg,
