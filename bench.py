@@ -425,6 +425,10 @@ def main():
                "kind": kind, "sample": f"3 full config-3 retrievals ({H} heads x {n_local} rows, "
                                        f"k={k}) after 1 warm-up; heads over {threads} threads",
                "gpu_indices_equal_reference": parity}
+        # "as shipped": the reference's own loop is single-threaded for scan +
+        # top-k (it only threads matmul); one full retrieval on one core
+        t1, _, _ = cpu_reference_retrieval(codes_np, q_np, k, 1, reps=1, warmup=0)
+        cpu["as_shipped_one_core"] = {"value": round(t1[0], 1), "unit": "µs", "cores": 1}
         del hamming_topk_np
 
     hbm, peak_kind = peaks()
