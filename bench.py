@@ -186,21 +186,28 @@ def run_reference_arm(args):
     if rank != 0:
         return
     threads = os.cpu_count() or 1
+    # the same workload as our arm: N x 512K tokens per head at N GPUs
+    # (config 5 when N > 1), k = 2% of the whole cache
+    world = max(args.gpus, int(os.environ.get("WORLD_SIZE", "1")))
+    n_tot = N_TOK * world
     rng = np.random.default_rng(0)
-    codes = rng.integers(0, 2**32, (H, N_TOK, L // 32), dtype=np.uint64).astype(np.uint32)
-    q = rng.integers(0, 2**32, (H, L // 32), dtype=np.uint64).astype(np.uint32)
-    k = budget(N_TOK)
-    times, kind, _ = cpu_reference_retrieval(codes, q, k, threads, args.steps, args.warmup)
+    codes = rng.integers(0, 2**32, (H, n_tot, L // 32), dtype=np.uint32)
+    q = rng.integers(0, 2**32, (H, L // 32), dtype=np.uint32)
+    k = budget(n_tot)
+    steps = args.steps if world == 1 else min(args.steps, 10)  # bounded sample
+    times, kind, _ = cpu_reference_retrieval(codes, q, k, threads, steps, args.warmup)
     v = statistics.mean(times)
     line = {"metric": METRIC, "value": round(v, 2), "unit": "µs", "impl": "reference",
-            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "n_gpus": world, "steps": steps, "warmup": args.warmup,
             "ms_per_step": round(v / 1000, 4), "higher_is_better": False, "scaling": "weak",
             "vs_baseline": None, "dtype": "u32", "data": "synthetic",
-            "config": {"workload": "config3: 32 heads x 524288 tokens x 128-bit codes, k=10485 "
-                                   "(per head nxor_scores_into + top_k_indices)", "heads": H,
-                       "tokens": N_TOK, "code_bits": L, "k": k},
+            "config": {"workload": (f"config3: 32 heads x 524288 tokens x 128-bit codes, k={k} "
+                                    if world == 1 else
+                                    f"config5: 32 heads x {n_tot} tokens x 128-bit codes, k={k} ")
+                                   + "(per head nxor_scores_into + top_k_indices)", "heads": H,
+                       "tokens": n_tot, "code_bits": L, "k": k},
             "cpu_baseline": {"value": round(v, 2), "unit": "µs", "cores": threads, "kind": kind,
-                             "sample": f"full config-3 workload per step ({H} heads x {N_TOK} rows), "
+                             "sample": f"full workload per step ({H} heads x {n_tot} rows), "
                                        f"heads spread over {threads} OpenMP threads"},
             "e2e": {"value": round(v, 2), "unit": "µs", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
