@@ -514,15 +514,61 @@ __device__ void stream_piece(const uint32_t* base, const uint32_t* qp, uint32_t 
 }
 
 // ------------------------------------------------------------ ordered select
-// 4/2 packed scores per word -> per-row flags via SIMD byte/half compares.
-template <typename ScoreT>
-__device__ __forceinline__ void word_flags(uint32_t w, uint32_t Tw, uint32_t& gt, uint32_t& eq) {
-    if constexpr (sizeof(ScoreT) == 1) {
-        const uint32_t g = __vcmpgtu4(w, Tw) & 0x01010101u, e = __vcmpeq4(w, Tw) & 0x01010101u;
-        gt = (g * 0x01020408u) >> 24;
-        eq = (e * 0x01020408u) >> 24;
+// Per-row flags of 4 packed u8 / 2 packed u16 scores against a threshold.
+// u8 (any byte value, incl. the clamped L = 256 scores): carry-free SWAR.
+// With xl = w & 0x7f.., xh = w & 0x80..: for s <= 127, byte >= s iff bit 7 of
+// (xl + 128 - s) | xh; for s >= 128, iff bit 7 of (xl + 256 - s) & xh (xl <=
+// 127 keeps every byte sum below 256). The __vcmp*4 intrinsics are emulated
+// on sm_100 and made the select issue-bound.
+struct U8Cmp {
+    uint32_t add, hi_or, hi_and;  // per-byte addend; xh OR-mask (s <= 127) / AND-mask (s >= 128)
+    uint32_t never;               // s > 255: no byte qualifies
+};
+__device__ __forceinline__ U8Cmp u8cmp_ge(uint32_t s) {
+    U8Cmp c;
+    c.never = s > 255 ? 1u : 0u;
+    if (s <= 127) {
+        c.add = (128u - s) * 0x01010101u;
+        c.hi_or = 0xFFFFFFFFu;
+        c.hi_and = 0xFFFFFFFFu;
     } else {
-        const uint32_t g = __vcmpgtu2(w, Tw), e = __vcmpeq2(w, Tw);
+        c.add = (256u - (s > 255 ? 255u : s)) * 0x01010101u;
+        c.hi_or = 0u;
+        c.hi_and = 0u;
+    }
+    return c;
+}
+// bit 7 of each byte = (byte >= s)
+__device__ __forceinline__ uint32_t u8_ge(uint32_t xl, uint32_t xh, const U8Cmp& c) {
+    const uint32_t t = xl + c.add;
+    // s <= 127: t | xh ; s >= 128: t & xh
+    const uint32_t r = c.hi_or ? (t | xh) : (t & xh);
+    return c.never ? 0u : (r & 0x80808080u);
+}
+template <typename ScoreT>
+struct WordCmp {
+    U8Cmp ge, gt;   // u8
+    uint32_t Tw;    // u16
+};
+template <typename ScoreT>
+__device__ __forceinline__ WordCmp<ScoreT> make_wordcmp(uint32_t T) {
+    WordCmp<ScoreT> c;
+    c.ge = u8cmp_ge(T);
+    c.gt = u8cmp_ge(T + 1);
+    c.Tw = T * 0x00010001u;
+    return c;
+}
+template <typename ScoreT>
+__device__ __forceinline__ void word_flags(uint32_t w, const WordCmp<ScoreT>& c, uint32_t& gt,
+                                           uint32_t& eq) {
+    if constexpr (sizeof(ScoreT) == 1) {
+        const uint32_t xl = w & 0x7F7F7F7Fu, xh = w & 0x80808080u;
+        const uint32_t ge = u8_ge(xl, xh, c.ge), g = u8_ge(xl, xh, c.gt);
+        // 0x80 flags of bytes 0..3 -> bits 0..3
+        gt = ((g >> 7) * 0x01020408u) >> 24;
+        eq = (((ge & ~g) >> 7) * 0x01020408u) >> 24;
+    } else {
+        const uint32_t g = __vcmpgtu2(w, c.Tw), e = __vcmpeq2(w, c.Tw);
         gt = (g & 1u) | ((g >> 15) & 2u);
         eq = (e & 1u) | ((e >> 15) & 2u);
     }
@@ -543,7 +589,7 @@ __device__ void select_rows(const ScoreT* sc, uint64_t a0, uint64_t r0, uint64_t
     constexpr int NG = 1;  // groups per thread per round (4: k3_select 43 -> 48 us at config 4)
     constexpr int CH = 64 * NG;               // rows per thread per round
     constexpr int SPW = 4 / sizeof(ScoreT);   // scores per word
-    const uint32_t Tw = sizeof(ScoreT) == 1 ? T * 0x01010101u : T * 0x00010001u;
+    const WordCmp<ScoreT> Tw = make_wordcmp<ScoreT>(T);
     const int tid = threadIdx.x;
     const uint64_t round_rows = (uint64_t)kThreads * CH;
     uint64_t carry_gt = 0, carry_eq = 0;
