@@ -241,6 +241,12 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # SPL_BENCH_SAME_GPU=1: every rank on GPU 0 with gloo collectives (host
+    # staged) — exercises the N > 1 code paths on a one-GPU box (timings are
+    # then meaningless: the ranks time-share the GPU)
+    same_gpu = os.environ.get("SPL_BENCH_SAME_GPU") == "1"
+    if same_gpu:
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     dist = None
@@ -248,7 +254,26 @@ def main():
         import torch.distributed as dist_mod
 
         dist = dist_mod
-        dist.init_process_group("nccl", device_id=dev)
+        if same_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
+
+    def all_gather_dev(out, inp):
+        if not same_gpu:
+            dist.all_gather_into_tensor(out, inp)
+            return
+        parts = [torch.empty_like(inp, device="cpu") for _ in range(world)]
+        dist.all_gather(parts, inp.cpu())
+        out.copy_(torch.stack(parts).to(dev))
+
+    def all_reduce_dev(t, op):
+        if not same_gpu:
+            dist.all_reduce(t, op=op)
+            return
+        c = t.cpu()
+        dist.all_reduce(c, op=op)
+        t.copy_(c.to(dev))
     ctx = capi.Context(local)
     stream = torch.cuda.current_stream()
     W = L // 32
@@ -275,7 +300,7 @@ def main():
     else:
         def retrieval_nccl():
             ctx.shard_histogram(codes, n_local, L, qcodes, P, nvalid, 1, n_local, hist, stream)
-            dist.all_gather_into_tensor(all_hist, hist)
+            all_gather_dev(all_hist, hist)
             ctx.shard_select(all_hist, world, rank, L, P, nvalid, 1, n_local, k, idx, cnt, off, stream)
 
         # Fused path: one kernel per rank, the histogram exchange inside it over
@@ -303,7 +328,7 @@ def main():
             ctx.check_device_error()
             same = all(torch.equal(a, b) for a, b in zip(ref, (idx, cnt, off)))
             ok = torch.tensor([1 if same else 0], device=dev)
-            dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+            all_reduce_dev(ok, dist.ReduceOp.MIN)
             if int(ok.item()) == 1:
                 retrieval = retrieval_fused
                 shard_path = "fused (one k3_fused<SHARD> per rank, in-kernel exchange over NVLink peer memory)"
@@ -347,7 +372,7 @@ def main():
             graph_note = f"eager (graph capture failed: {str(e)[:80]})"
     if dist:
         t = torch.tensor([ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        all_reduce_dev(t, dist.ReduceOp.MAX)
         ms = float(t.item())
     us = ms * 1000.0
 
@@ -396,7 +421,7 @@ def main():
                          args.steps, stream)
     if dist:
         t = torch.tensor([e2e_ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        all_reduce_dev(t, dist.ReduceOp.MAX)
         e2e_ms = float(t.item())
     d2h = idx_host.numel() * 4 + cnt_host.numel() * 4 + (off_host.numel() * 4 if world > 1 else 0)
     e2e = {"value": round(e2e_ms * 1000, 2), "unit": "µs",
@@ -457,7 +482,7 @@ def main():
         "config": {"workload": ("config3: 32 heads x 524288 tokens x 128-bit codes, k=10485"
                                 if world == 1 else
                                 f"config5: sequence-sharded {n_total} tokens x 32 heads x 128-bit, "
-                                f"k={k}, NCCL all-gather of per-head histograms"),
+                                f"k={k}, per-head histograms exchanged across ranks"),
                    "heads": H, "tokens_per_gpu": n_local, "tokens_total": n_total, "code_bits": L,
                    "k": k, "l2": "inputs (268 MB codes) larger than the 126 MB L2; no flush"},
         "roofline": {"bound": "hbm",
