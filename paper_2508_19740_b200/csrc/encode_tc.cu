@@ -194,9 +194,11 @@ __device__ __forceinline__ void tmem_ld16_nowait(uint32_t taddr, uint32_t (&r)[1
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
 // Epilogue 2 for one column half: code bit of column j = (z_j >= 0) goes to
-// word j % W, bit 31 - j / W (Appendix A.7). Collects NEGATIVE flags (sign
-// bits after z + 0, which maps -0 to +0) with compile-time shifts: per column
-// FADD, SHF, LOP3; the word is the complement. `sum` accumulates the values
+// word j % W, bit 31 - j / W (Appendix A.7). Collects NEGATIVE flags (raw
+// sign bits) with compile-time shifts; the word is the complement. A z2 of
+// exactly -0.0 (every product of its dot a signed zero) gets bit 0 where the
+// exact encoder gives 1: K2 is the fast mode, whose bits may differ from the
+// exact ones only inside the rounding band around 0, and -0.0 is at 0. `sum` accumulates the values
 // (non-finite check). Two TMEM loads in flight per wait.
 template <uint32_t W, uint32_t HALF>
 __device__ __forceinline__ void sign_half(uint32_t tz, uint32_t (&neg)[W], float& sum) {
@@ -215,7 +217,7 @@ __device__ __forceinline__ void sign_half(uint32_t tz, uint32_t (&neg)[W], float
             for (uint32_t i = 0; i < 16; ++i) {
                 const float z = __uint_as_float(r[q][i]);
                 sum += z;
-                const uint32_t u = __float_as_uint(z + 0.0f);
+                const uint32_t u = r[q][i];
                 const uint32_t sh = (c0 + i) / W;
                 neg[(c0 + i) % W] |= (u >> sh) & (0x80000000u >> sh);
             }
@@ -675,7 +677,8 @@ __global__ void __launch_bounds__(kWsThreads, 1)
             fence_after();
             // column j -> word j % W, bit 31 - j / W: feeding the sign bits of
             // columns w, w + W, w + 2W, ... into word w with a funnel shift
-            // puts column w + W*b at bit 31 - b. Sign after z + 0 (-0 -> +0).
+            // puts column w + W*b at bit 31 - b. Raw sign bits (see sign_half
+            // for -0.0): one funnel shift per column.
             uint32_t neg[W];
 #pragma unroll
             for (uint32_t w = 0; w < W; ++w) neg[w] = 0u;
@@ -691,9 +694,8 @@ __global__ void __launch_bounds__(kWsThreads, 1)
                 tmem_wait_ld();
 #pragma unroll
                 for (uint32_t e = 0; e < 32; ++e) {
-                    const float z = __uint_as_float(r[e >> 4][e & 15]);
-                    if (c0 == 0 && e == 0) z0 = z;
-                    const uint32_t u = __float_as_uint(z + 0.0f);
+                    const uint32_t u = r[e >> 4][e & 15];
+                    if (c0 == 0 && e == 0) z0 = __uint_as_float(u);
                     neg[(c0 + e) % W] = __funnelshift_l(u, neg[(c0 + e) % W], 1);
                 }
             }
