@@ -242,6 +242,8 @@ spl_status spl_peer_create(spl_ctx* ctx, uint32_t R, uint32_t rank, uint32_t P_m
     cudaError_t e = cudaMalloc(&pe->buf, pe->bytes);
     if (e == cudaSuccess) e = cudaMemset(pe->buf, 0, pe->bytes);
     if (e == cudaSuccess) e = cudaMalloc(&pe->d_table, sizeof(uint32_t*) * R);
+    if (e == cudaSuccess) e = cudaMalloc(&pe->d_epoch, sizeof(uint32_t));
+    if (e == cudaSuccess) e = cudaMemset(pe->d_epoch, 0, sizeof(uint32_t));
     if (e != cudaSuccess) {
         cudaFree(pe->buf);
         delete pe;
@@ -301,6 +303,7 @@ void spl_peer_destroy(spl_peer* peer) {
     cudaDeviceSynchronize();
     for (void* p : peer->opened) cudaIpcCloseMemHandle(p);
     cudaFree(peer->d_table);
+    cudaFree(peer->d_epoch);
     cudaFree(peer->buf);
     delete peer;
 }

@@ -90,7 +90,8 @@ struct K3Params {
     // their exchange areas (IPC-mapped peer memory over NVLink)
     uint32_t** peer_bufs;  // [R] exchange area of every rank (own included)
     uint32_t* own_buf;     // this rank's exchange area
-    uint32_t R, rank, epoch, Pmax;
+    uint32_t R, rank, Pmax;
+    uint32_t* epoch_ptr;   // the group's call counter (device; advanced by the last CTA)
     uint32_t* out_offset;  // [P] position of this rank's first index in the global list
 };
 
@@ -980,15 +981,15 @@ __device__ uint32_t wait_tagged(const uint32_t* p, uint32_t tag, uint32_t* dev_e
 }
 // Block: push bins [b0, b1) of this rank's problem histogram (tot, complete
 // at GPU scope) into slot (rank, p) of every rank's exchange area.
-__device__ void shard_push(const K3Params& prm, const uint32_t* tot, uint32_t p, uint32_t b0,
-                           uint32_t b1, bool with_count, uint32_t nv_local) {
-    const uint32_t S = prm.L + 2, par = prm.epoch & 1u;
+__device__ void shard_push(const K3Params& prm, uint32_t epoch, const uint32_t* tot, uint32_t p,
+                           uint32_t b0, uint32_t b1, bool with_count, uint32_t nv_local) {
+    const uint32_t S = prm.L + 2, par = epoch & 1u;
     __threadfence();
     for (uint32_t r = 0; r < prm.R; ++r) {
         uint32_t* dst = prm.peer_bufs[r] + 2 * xslot(prm.R, prm.Pmax, S, par, prm.rank, p);
         for (uint32_t t = b0 + threadIdx.x; t < b1; t += kThreads)
-            st_tagged(dst + 2 * t, __ldcg(tot + t), prm.epoch);
-        if (with_count && threadIdx.x == 0) st_tagged(dst + 2 * (prm.L + 1), nv_local, prm.epoch);
+            st_tagged(dst + 2 * t, __ldcg(tot + t), epoch);
+        if (with_count && threadIdx.x == 0) st_tagged(dst + 2 * (prm.L + 1), nv_local, epoch);
     }
 }
 // Block: the global plan of problem p from all ranks' delivered histograms
@@ -1001,18 +1002,18 @@ __device__ void shard_push(const K3Params& prm, const uint32_t* tot, uint32_t p,
 struct ShardPlanOut {
     uint32_t T, take, count, off, kk;
 };
-__device__ ShardPlanOut shard_global_plan(const K3Params& prm, uint32_t p, uint32_t from,
-                                          uint32_t to, uint32_t* mat, uint32_t* s_cum,
-                                          uint64_t* s_warp, unsigned long long* s_red,
-                                          uint32_t* s_aux) {
-    const uint32_t L = prm.L, S = L + 2, par = prm.epoch & 1u;
+__device__ ShardPlanOut shard_global_plan(const K3Params& prm, uint32_t epoch, uint32_t p,
+                                          uint32_t from, uint32_t to, uint32_t* mat,
+                                          uint32_t* s_cum, uint64_t* s_warp,
+                                          unsigned long long* s_red, uint32_t* s_aux) {
+    const uint32_t L = prm.L, S = L + 2, par = epoch & 1u;
     const uint32_t* base = prm.own_buf + 2 * xslot(prm.R, prm.Pmax, S, par, 0, p);
     const uint64_t rs = 2ull * prm.Pmax * S;  // rank stride (u32 words)
     // entries [from, to) of every rank (+ the count at L + 1 when to == L + 2)
     const uint32_t span = to - from;
     for (uint32_t i = threadIdx.x; i < prm.R * span; i += kThreads) {
         const uint32_t r = i / span, t = from + i % span;
-        mat[r * S + t] = wait_tagged(base + r * rs + 2 * t, prm.epoch, prm.dev_err);
+        mat[r * S + t] = wait_tagged(base + r * rs + 2 * t, epoch, prm.dev_err);
     }
     if (threadIdx.x < 4) s_red[threadIdx.x] = 0;
     if (threadIdx.x == 0) s_aux[0] = SPL_PLAN_SKIP;
@@ -1123,6 +1124,13 @@ __global__ void __launch_bounds__(kThreads, 3) k3_fused(K3Params prm) {
     for (uint32_t i = tid; i < priv_bytes / 16; i += kThreads)
         reinterpret_cast<uint4*>(priv)[i] = make_uint4(0, 0, 0, 0);
     pdl_wait();  // query codes / appended code rows come from the previous kernel
+    // SHARD: this call's epoch = the group's device-side counter + 1 (the
+    // last CTA stores it back), so CUDA-graph replays advance it too
+    uint32_t epoch = 0;
+    if constexpr (SHARD) {
+        epoch = __ldcg(prm.epoch_ptr) + 1u;
+        if (epoch == 0) epoch = 1;  // 0 marks never-written entries
+    }
 
     const uint64_t g0 = (uint64_t)seg * g.S;
     const uint64_t g1 = min(g0 + g.S, g.total);
@@ -1176,7 +1184,7 @@ __global__ void __launch_bounds__(kThreads, 3) k3_fused(K3Params prm) {
         }
         if constexpr (SHARD) {
             __syncthreads();
-            if (s_flag) shard_push(prm, tot, p, lo, bins, true, nv);  // the local histogram is complete
+            if (s_flag) shard_push(prm, epoch, tot, p, lo, bins, true, nv);  // the local histogram is complete
         }
     }
     K3_STAMP(1);
@@ -1211,7 +1219,7 @@ __global__ void __launch_bounds__(kThreads, 3) k3_fused(K3Params prm) {
         // now; the plan checked R x (L + 2) words fit)
         uint32_t* mat = reinterpret_cast<uint32_t*>(priv);
         if constexpr (SHARD) {
-            sp = shard_global_plan(prm, p, lo, L + 2, mat, s_cum, s_warp, s_red, s_aux);
+            sp = shard_global_plan(prm, epoch, p, lo, L + 2, mat, s_cum, s_warp, s_red, s_aux);
             T = sp.T;
             quota = sp.take;  // this rank's ties
         } else {
@@ -1246,12 +1254,12 @@ __global__ void __launch_bounds__(kThreads, 3) k3_fused(K3Params prm) {
             }
             __syncthreads();
             if constexpr (SHARD) {
-                if (s_flag) shard_push(prm, tot, p, 0, lo, false, 0);  // low bins of all local segments
+                if (s_flag) shard_push(prm, epoch, tot, p, 0, lo, false, 0);  // low bins of all local segments
             }
             if (tid == 0) wait_count(prm.counters2 + p, nseg, prm.dev_err);
             __syncthreads();
             if constexpr (SHARD) {
-                sp = shard_global_plan(prm, p, 0, lo, mat, s_cum, s_warp, s_red, s_aux);
+                sp = shard_global_plan(prm, epoch, p, 0, lo, mat, s_cum, s_warp, s_red, s_aux);
                 T = sp.T;
                 quota = sp.take;
             } else {
@@ -1324,6 +1332,7 @@ __global__ void __launch_bounds__(kThreads, 3) k3_fused(K3Params prm) {
         if (tid == 0) {
             prm.sync[0] = 0u;
             prm.sync[1] = 0u;
+            if constexpr (SHARD) *prm.epoch_ptr = epoch;
         }
     }
 }
@@ -1976,8 +1985,7 @@ spl_status hamming_topk_sharded_impl(spl_ctx* ctx, spl_peer* peer, const uint32_
     prm.R = peer->R;
     prm.rank = peer->rank;
     prm.Pmax = peer->Pmax;
-    prm.epoch = ++peer->epoch;
-    if (prm.epoch == 0) prm.epoch = ++peer->epoch;  // 0 = never written
+    prm.epoch_ptr = peer->d_epoch;
     prm.out_offset = out_offset;
     const char* tr = getenv("SPL_K3_TRACE");
     uint64_t* dtrace = nullptr;

@@ -61,7 +61,7 @@ struct spl_peer {
     size_t bytes = 0;
     uint32_t** d_table = nullptr;   // [R] device pointers (own included)
     std::vector<void*> opened;      // IPC mappings to close
-    uint32_t epoch = 0;
+    uint32_t* d_epoch = nullptr;    // call counter (device, so graph replays advance it)
     bool connected = false;
     int device = 0;
 };
