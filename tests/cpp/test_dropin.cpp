@@ -15,6 +15,7 @@
 #include <random>
 #include <string>
 #include <unistd.h>
+#include <thread>
 #include <vector>
 
 #include "spotlight/attention_eval.hpp"
@@ -441,6 +442,35 @@ TEST_CASE("oracle_topk agrees with an exhaustive sort; one dropped key obeys the
         }
         // one dropped key: full - sparse == w_drop * (v_drop - sparse)
         CHECK(std::fabs(std::sqrt(diff2) - w[drop] * std::sqrt(gap2)) <= 1e-3 * w[drop] * std::sqrt(gap2) + 1e-6);
+    }
+}
+
+TEST_CASE("concurrent callers: each host thread gets its own context (SPEC.md:88-89)") {
+    std::mt19937_64 eng(555);
+    const std::uint32_t n = 400, d = 64;
+    std::vector<AttentionInstance> insts;
+    for (int t = 0; t < 4; ++t)
+        insts.push_back(make_causal_instance(random_matrix(n, d, eng), random_matrix(n, d, eng),
+                                             random_matrix(n, d, eng)));
+    const MlpHasher h = mlp_gaussian_init(d, d, 128, 64.0f, 8);
+    std::vector<RetrievalResult> seq(4), par(4);
+    std::vector<Matrix<float>> seq_out, par_out(4);
+    for (int t = 0; t < 4; ++t) {
+        seq[t] = hash_topk(insts[t], h, 24);
+        seq_out.push_back(sparse_attention(insts[t], seq[t]));
+    }
+    std::vector<std::thread> th;
+    for (int t = 0; t < 4; ++t)
+        th.emplace_back([&, t] {
+            for (int rep = 0; rep < 3; ++rep) {
+                par[t] = hash_topk(insts[t], h, 24);
+                par_out[t] = sparse_attention(insts[t], par[t]);
+            }
+        });
+    for (auto& x : th) x.join();
+    for (int t = 0; t < 4; ++t) {
+        CHECK(par[t].indices == seq[t].indices);
+        CHECK(std::memcmp(par_out[t].data(), seq_out[t].data(), seq_out[t].size() * 4) == 0);
     }
 }
 
