@@ -10,6 +10,8 @@
 #include <vector>
 #include <cstring>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "spl_launch.cuh"
 #include "spl_tc.cuh"
 
@@ -45,6 +47,11 @@ cudaError_t launch_pdl(const void* fn, dim3 grid, dim3 block, size_t smem, cudaS
 
 namespace {
 inline cudaStream_t S(void* s) { return static_cast<cudaStream_t>(s); }
+// NVTX range around each compute entry point (no cost without a profiler)
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+};
 constexpr float kLog2e = 1.4426950408889634f;
 
 
@@ -314,6 +321,7 @@ spl_status spl_hamming_topk_sharded(spl_ctx* ctx, spl_peer* peer, const uint32_t
                                     uint32_t nvalid_div, uint64_t n_max, uint32_t k,
                                     uint32_t* idx, uint32_t* cnt, uint32_t* out_offset,
                                     void* stream) {
+    NvtxRange nvtx_("spl_hamming_topk_sharded");
     return hamming_topk_sharded_impl(ctx, peer, codes, problem_stride_rows, L, qcodes, P, n_valid,
                                      nvalid_div, n_max, k, idx, cnt, out_offset, S(stream));
 }
@@ -323,6 +331,7 @@ spl_status spl_oracle_topk(spl_ctx* ctx, const float* q, const void* keys, int k
                            uint64_t cap, uint32_t d, uint32_t P, const uint32_t* n_valid,
                            uint32_t nvalid_div, uint64_t n_max, float scale, uint32_t k,
                            uint32_t* idx, uint32_t* cnt, float* logits, void* stream) {
+    NvtxRange nvtx_("spl_oracle_topk");
     if (!ctx) return SPL_E_STATE;
     if (k == 0) return fail(ctx, SPL_E_DIMENSION, "oracle_topk: k must be >= 1");
     if (kv_dtype != SPL_F32 && kv_dtype != SPL_BF16)
@@ -367,6 +376,7 @@ spl_status spl_hamming_topk(spl_ctx* ctx, const uint32_t* codes, uint64_t proble
                             uint32_t L, const uint32_t* qcodes, uint32_t P,
                             const uint32_t* n_valid, uint32_t nvalid_div, uint64_t n_max,
                             uint32_t k, uint32_t* idx, uint32_t* cnt, void* stream) {
+    NvtxRange nvtx_("spl_hamming_topk");
     return hamming_topk_impl(ctx, codes, problem_stride_rows, L, qcodes, P, n_valid, nvalid_div,
                              n_max, k, idx, cnt, S(stream));
 }
@@ -376,6 +386,7 @@ spl_status spl_shard_histogram(spl_ctx* ctx, const uint32_t* codes,
                                const uint32_t* qcodes, uint32_t P, const uint32_t* n_valid,
                                uint32_t nvalid_div, uint64_t n_max, uint32_t* hist,
                                void* stream) {
+    NvtxRange nvtx_("spl_shard_histogram");
     return shard_histogram_impl(ctx, codes, problem_stride_rows, L, qcodes, P, n_valid,
                                 nvalid_div, n_max, hist, S(stream));
 }
@@ -384,6 +395,7 @@ spl_status spl_shard_select(spl_ctx* ctx, const uint32_t* all_hist, uint32_t R, 
                             uint32_t L, uint32_t P, const uint32_t* n_valid,
                             uint32_t nvalid_div, uint64_t n_max, uint32_t k, uint32_t* idx,
                             uint32_t* cnt, uint32_t* out_offset, void* stream) {
+    NvtxRange nvtx_("spl_shard_select");
     return shard_select_impl(ctx, all_hist, R, rank, L, P, n_valid, nvalid_div, n_max, k, idx,
                              cnt, out_offset, S(stream));
 }
@@ -521,6 +533,7 @@ spl_status spl_mlp_forward(spl_ctx* ctx, const spl_hasher* hs, const float* x, u
 
 spl_status spl_encode(spl_ctx* ctx, const spl_hasher* hs, const float* x, uint32_t B, uint32_t m,
                       int mode, uint32_t* codes, void* stream) {
+    NvtxRange nvtx_("spl_encode");
     if (!ctx || !hs) return SPL_E_STATE;
     if (mode == SPL_ENCODE_TC)
         return encode_tc_launch(ctx, hs, x, SPL_F32, B, m, codes, nullptr, S(stream));
@@ -535,6 +548,7 @@ spl_status spl_encode(spl_ctx* ctx, const spl_hasher* hs, const float* x, uint32
 
 spl_status spl_encode_tc(spl_ctx* ctx, const spl_hasher* hs, const void* x, int x_dtype,
                          uint32_t B, uint32_t m, uint32_t* codes, float* pre, void* stream) {
+    NvtxRange nvtx_("spl_encode_tc");
     if (!ctx || !hs) return SPL_E_STATE;
     return encode_tc_launch(ctx, hs, x, x_dtype, B, m, codes, pre, S(stream));
 }
@@ -543,6 +557,7 @@ spl_status spl_encode_append(spl_ctx* ctx, const spl_hasher* hs, const float* k_
                              const float* v_new, uint32_t B, uint32_t* codes, void* kcache,
                              void* vcache, int kv_dtype, uint64_t cap, const uint32_t* pos,
                              void* stream) {
+    NvtxRange nvtx_("spl_encode_append");
     if (!ctx || !hs) return SPL_E_STATE;
     if (kv_dtype != SPL_F32 && kv_dtype != SPL_BF16)
         return fail(ctx, SPL_E_DIMENSION, "encode_append: unknown kv dtype");
@@ -566,6 +581,7 @@ spl_status spl_sparse_attend(spl_ctx* ctx, const float* q, const void* kcache,
                              uint32_t d, uint32_t P, const uint32_t* idx, uint64_t idx_stride,
                              const uint32_t* cnt, const uint32_t* n_valid, uint32_t nvalid_div,
                              float scale, float* out, void* stream) {
+    NvtxRange nvtx_("spl_sparse_attend");
     if (!ctx) return SPL_E_STATE;
     if (!(scale > 0.0f)) return fail(ctx, SPL_E_DIMENSION, "attention: scale must be positive");
     if (nvalid_div == 0) return fail(ctx, SPL_E_DIMENSION, "sparse_attend: nvalid_div == 0");
@@ -626,6 +642,7 @@ spl_status spl_decode_step(spl_ctx* ctx, const spl_hasher* hs, const float* q,
                            uint32_t* codes, void* kcache, void* vcache, int kv_dtype,
                            uint64_t cap, const uint32_t* n_valid, uint64_t n_max, uint32_t k,
                            float scale, uint32_t* idx, uint32_t* cnt, float* out, void* stream) {
+    NvtxRange nvtx_("spl_decode_step");
     if (!ctx || !hs) return SPL_E_STATE;
     const uint32_t H = hs->H, W = hs->L / 32, P = B * H;
     // query codes live in the context scratch
