@@ -1869,8 +1869,28 @@ spl_status hamming_topk_impl(spl_ctx* ctx, const uint32_t* codes, uint64_t strid
     prm.shard = 0;
     prm.hist_lo = pl.hist_lo;
     prm.clamp8 = pl.clamp8 ? 1 : 0;
+    // SPL_K3_TIME=1: print the two-pass kernels' device times (diagnostics)
+    const char* tm = getenv("SPL_K3_TIME");
+    cudaEvent_t ev[3];
+    const bool timed = tm && *tm == '1' && !stream_capturing(s);
+    if (timed) {
+        for (auto& e : ev) cudaEventCreate(&e);
+        cudaEventRecord(ev[0], s);
+    }
     if ((st = launch_scan(ctx, pl, prm, s))) return st;
-    return launch_select(ctx, pl, prm, idx, k, s);
+    if (timed) cudaEventRecord(ev[1], s);
+    st = launch_select(ctx, pl, prm, idx, k, s);
+    if (timed) {
+        cudaEventRecord(ev[2], s);
+        cudaEventSynchronize(ev[2]);
+        float a = 0, b = 0;
+        cudaEventElapsedTime(&a, ev[0], ev[1]);
+        cudaEventElapsedTime(&b, ev[1], ev[2]);
+        fprintf(stderr, "k3 two-pass: scan %.1f us (G=%u grid=%u S=%llu), select %.1f us\n", a * 1e3,
+                pl.g.G, pl.grid, (unsigned long long)pl.g.S, b * 1e3);
+        for (auto& e : ev) cudaEventDestroy(e);
+    }
+    return st;
 }
 
 spl_status shard_histogram_impl(spl_ctx* ctx, const uint32_t* codes, uint64_t stride_rows,
