@@ -43,11 +43,16 @@ typedef enum spl_status {
     SPL_E_IO = 4,        /* IoError        (errors.hpp:32-35) */
     SPL_E_CUDA = 5,      /* CUDA runtime failure / no device */
     SPL_E_NCCL = 6,      /* collective failure (reported by host glue) */
-    SPL_E_STATE = 7      /* misuse: null handle, workspace during capture */
+    SPL_E_STATE = 7,     /* misuse: null handle, workspace during capture */
+    SPL_E_EMPTY_PAIRS = 8 /* EmptyPairError (errors.hpp:27-30): no valid ranking pairs */
 } spl_status;
 
 typedef enum spl_dtype { SPL_F32 = 0, SPL_BF16 = 1 } spl_dtype;
-typedef enum spl_hasher_kind { SPL_HASHER_MLP = 1, SPL_HASHER_LINEAR = 0 } spl_hasher_kind;
+typedef enum spl_hasher_kind {
+    SPL_HASHER_MLP = 1,
+    SPL_HASHER_LINEAR = 0,
+    SPL_HASHER_DOWNPROJ = 2 /* DownProjEstimator (training / evaluation only) */
+} spl_hasher_kind;
 typedef enum spl_encode_mode {
     SPL_ENCODE_EXACT = 0, /* CUDA cores, the reference's fmaf order + glibc expf: bit-exact */
     SPL_ENCODE_TC = 1     /* tcgen05 bf16 tensor cores, fp32 TMEM accumulation (bulk/prefill) */
@@ -282,6 +287,45 @@ spl_status spl_decode_step(spl_ctx* ctx, const spl_hasher* hasher, const float* 
 
 /* budget_from_rate (attention_eval.hpp:70, attention_eval.cpp:266-272). */
 spl_status spl_budget_from_rate(double rate, uint64_t n, uint32_t* k);
+
+/* ---------------------------------------------------------------- training
+ * Hasher training. Mirrors spotlight::train_hasher
+ * (trainer.hpp:115-118, trainer.cpp:634-645): RankingLossConfig
+ * (ranking_loss.hpp:15-24; optional counts < 0 = unset) and TrainConfig
+ * (trainer.hpp:18-37). Loss: pairwise ranking (TrainLoss::ranking). */
+typedef struct spl_rank_config {
+    double beta, alpha, maskout;
+    int64_t max_top, max_oth, query_subsample; /* < 0: unset (std::nullopt) */
+} spl_rank_config;
+typedef struct spl_train_config {
+    uint32_t num_iters, warmup_iters, batch, holdout_queries;
+    uint64_t seed;
+    double max_lr, min_lr, adam_beta1, adam_beta2, adam_eps, weight_decay, grad_clip,
+        soft_gamma, holdout_budget_rate;
+} spl_train_config;
+/* All pointers HOST. kind: SPL_HASHER_MLP (w1 d x h, b1 h, w2 h x L, gamma =
+ * the hasher's), SPL_HASHER_LINEAR (w1 = projection d x L, soft_gamma) or
+ * SPL_HASHER_DOWNPROJ (w1 = projection d x L). Weights are updated in place
+ * (also when an error stops the run, as the reference's in-place hasher).
+ * Sequences are concatenated: sequence s has seq_len[s] query rows and as
+ * many key rows (causally aligned). records: [num_iters][3] = {loss,
+ * violation_rate, lr} (IterRecord, trainer.hpp:84-89). Sequences are limited
+ * to 16384 keys (per-row order sort in shared memory). */
+spl_status spl_train_hasher(spl_ctx* ctx, int kind, uint32_t d, uint32_t h, uint32_t L,
+                            float gamma, float* w1, float* b1, float* w2, uint32_t n_seq,
+                            const float* queries, const float* keys, const uint32_t* seq_len,
+                            const spl_rank_config* rank, const spl_train_config* train,
+                            double* records, double* holdout_iou, uint32_t* skipped,
+                            void* stream);
+/* partition_topk's draws (ranking_loss.cpp:80-116), host only: rows
+ * [min(query_subsample, q_train)], top positions [min(max_top, k_full)], other
+ * positions relative to k_full [min(max_oth, n - k_full)]; counts = {rows,
+ * top, other, k_full}. */
+spl_status spl_train_partition_host(const spl_rank_config* rank, uint32_t q_train, uint32_t n,
+                                    uint64_t seed, uint32_t* rows, uint32_t* top_pos,
+                                    uint32_t* oth_pos, uint32_t* counts);
+/* lr_at (trainer.cpp:35-46) */
+double spl_train_lr_at(uint32_t iter, const spl_train_config* train);
 
 #ifdef __cplusplus
 }

@@ -25,6 +25,8 @@
 #include "spotlight/errors.hpp"
 #include "spotlight/hashers.hpp"
 #include "spotlight/rng.hpp"
+#include "spotlight/ranking_loss.hpp"
+#include "spotlight/trainer.hpp"
 
 using namespace spotlight;  // == spotref under -Dspotlight=spotref
 
@@ -48,6 +50,9 @@ int guard(F&& f) {
     } catch (const IoError& e) {
         g_err = e.what();
         return 4;
+    } catch (const EmptyPairError& e) {
+        g_err = e.what();
+        return 5;
     } catch (const std::exception& e) {
         g_err = e.what();
         return 9;
@@ -415,6 +420,130 @@ int spotref_retrieve_batch(void* handle, const std::uint32_t* qcodes,
         }
         if (status) throw DimensionError(err);
     });
+}
+
+// ------------------------------------------------------------ trainer (§8 f4)
+// train_hasher (trainer.cpp:634-645) on an MLP hasher. Sequences are
+// concatenated: sequence s has seq_len[s] query rows and as many key rows.
+// dcfg = {max_lr, min_lr, adam_beta1, adam_beta2, adam_eps, weight_decay,
+//         grad_clip, soft_gamma, holdout_budget_rate, beta, alpha, maskout}
+// ucfg = {num_iters, warmup_iters, batch, seed, holdout_queries}
+// opt  = {max_top, max_oth, query_subsample} (-1: unset)
+// rec  = num_iters x {loss, violation_rate, lr}
+// kind: 1 MLP (w1 d x h, b1, w2 h x L), 0 linear / 2 downproj (w1 = projection d x L).
+int spotref_train(int kind, float* w1, float* b1, float* w2, std::uint32_t d, std::uint32_t h,
+                  std::uint32_t L, float gamma, std::uint32_t n_seq, const float* queries,
+                  const float* keys, const std::uint32_t* seq_len, const double* dcfg,
+                  const std::uint64_t* ucfg, const std::int64_t* opt, int loss_kind,
+                  double* rec, double* holdout_iou, std::uint32_t* skipped) {
+    return guard([&] {
+        AnyHasher any;
+        if (kind == 1) {
+            MlpHasher m;
+            m.w1 = mat(w1, d, h);
+            m.b1.assign(b1, b1 + h);
+            m.w2 = mat(w2, h, L);
+            m.gamma = gamma;
+            any = m;
+        } else if (kind == 0) {
+            any = LinearHasher{mat(w1, d, L)};
+        } else {
+            any = DownProjEstimator{mat(w1, d, L)};
+        }
+        TrainDataset data;
+        std::size_t off = 0;
+        for (std::uint32_t s = 0; s < n_seq; ++s) {
+            data.sequences.push_back(QkSequence{mat(queries + off * d, seq_len[s], d),
+                                                mat(keys + off * d, seq_len[s], d)});
+            off += seq_len[s];
+        }
+        TrainConfig cfg;
+        cfg.max_lr = dcfg[0];
+        cfg.min_lr = dcfg[1];
+        cfg.adam_beta1 = dcfg[2];
+        cfg.adam_beta2 = dcfg[3];
+        cfg.adam_eps = dcfg[4];
+        cfg.weight_decay = dcfg[5];
+        cfg.grad_clip = dcfg[6];
+        cfg.soft_gamma = dcfg[7];
+        cfg.holdout_budget_rate = dcfg[8];
+        cfg.num_iters = static_cast<std::uint32_t>(ucfg[0]);
+        cfg.warmup_iters = static_cast<std::uint32_t>(ucfg[1]);
+        cfg.batch = static_cast<std::uint32_t>(ucfg[2]);
+        cfg.seed = ucfg[3];
+        cfg.holdout_queries = static_cast<std::uint32_t>(ucfg[4]);
+        RankingLossConfig lc;
+        lc.beta = dcfg[9];
+        lc.alpha = dcfg[10];
+        lc.maskout = dcfg[11];
+        if (opt[0] >= 0) lc.max_top = static_cast<std::uint32_t>(opt[0]);
+        if (opt[1] >= 0) lc.max_oth = static_cast<std::uint32_t>(opt[1]);
+        if (opt[2] >= 0) lc.query_subsample = static_cast<std::uint32_t>(opt[2]);
+        const TrainReport r = train_hasher(
+            any, data, lc, cfg, loss_kind == 1 ? TrainLoss::reconstruction : TrainLoss::ranking);
+        if (kind == 1) {
+            const MlpHasher& out = std::get<MlpHasher>(any);
+            std::memcpy(w1, out.w1.data(), sizeof(float) * d * h);
+            std::memcpy(b1, out.b1.data(), sizeof(float) * h);
+            std::memcpy(w2, out.w2.data(), sizeof(float) * h * L);
+        } else if (kind == 0) {
+            std::memcpy(w1, std::get<LinearHasher>(any).projection.data(), sizeof(float) * d * L);
+        } else {
+            std::memcpy(w1, std::get<DownProjEstimator>(any).projection.data(), sizeof(float) * d * L);
+        }
+        for (std::size_t i = 0; i < r.records.size(); ++i) {
+            rec[3 * i] = r.records[i].loss;
+            rec[3 * i + 1] = r.records[i].violation_rate;
+            rec[3 * i + 2] = r.records[i].lr;
+        }
+        *holdout_iou = r.final_holdout_iou;
+        *skipped = r.skipped_steps;
+    });
+}
+
+// partition_topk (ranking_loss.cpp:80-145) over an identity order (row i of
+// the order = 0..n-1), so the returned key indices ARE the sampled positions:
+// the host sampler of the GPU trainer is checked against this.
+int spotref_partition_identity(std::uint32_t q, std::uint32_t n, const std::uint32_t* offsets,
+                               const double* bam, const std::int64_t* opt, std::uint64_t seed,
+                               std::uint32_t* rows_out, std::uint32_t* top_out,
+                               std::uint32_t* oth_out, std::uint32_t* counts,
+                               std::uint64_t* valid_pairs) {
+    return guard([&] {
+        TopkOrder o;
+        o.n_keys = n;
+        o.n_queries = q;
+        o.causal_offsets.assign(offsets, offsets + q);
+        o.order.resize(std::size_t(q) * n);
+        for (std::size_t r = 0; r < q; ++r)
+            for (std::uint32_t j = 0; j < n; ++j) o.order[r * n + j] = j;
+        RankingLossConfig lc;
+        lc.beta = bam[0];
+        lc.alpha = bam[1];
+        lc.maskout = bam[2];
+        if (opt[0] >= 0) lc.max_top = static_cast<std::uint32_t>(opt[0]);
+        if (opt[1] >= 0) lc.max_oth = static_cast<std::uint32_t>(opt[1]);
+        if (opt[2] >= 0) lc.query_subsample = static_cast<std::uint32_t>(opt[2]);
+        const PairPartition p = partition_topk(o, lc, seed);
+        counts[0] = static_cast<std::uint32_t>(p.query_rows.size());
+        counts[1] = p.top_count;
+        counts[2] = p.oth_count;
+        counts[3] = p.k_full;
+        std::copy(p.query_rows.begin(), p.query_rows.end(), rows_out);
+        for (std::uint32_t i = 0; i < p.top_count; ++i) top_out[i] = p.top_indices[i];
+        for (std::uint32_t j = 0; j < p.oth_count; ++j) oth_out[j] = p.oth_indices[j] - p.k_full;
+        *valid_pairs = p.valid_pairs;
+    });
+}
+
+double spotref_lr_at(std::uint32_t iter, std::uint32_t num_iters, std::uint32_t warmup,
+                     double max_lr, double min_lr) {
+    TrainConfig cfg;
+    cfg.num_iters = num_iters;
+    cfg.warmup_iters = warmup;
+    cfg.max_lr = max_lr;
+    cfg.min_lr = min_lr;
+    return lr_at(iter, cfg);
 }
 
 }  // extern "C"

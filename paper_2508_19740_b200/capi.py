@@ -21,7 +21,9 @@ ROOT = PKG.parent
 LIB_PATH = PKG / "lib" / "libspl.so"
 HEADER = ROOT / "include" / "spl_c.h"
 
-SPL_OK, SPL_E_DIMENSION, SPL_E_NUMERIC, SPL_E_FORMAT, SPL_E_IO, SPL_E_CUDA, SPL_E_NCCL, SPL_E_STATE = range(8)
+(SPL_OK, SPL_E_DIMENSION, SPL_E_NUMERIC, SPL_E_FORMAT, SPL_E_IO, SPL_E_CUDA, SPL_E_NCCL, SPL_E_STATE,
+ SPL_E_EMPTY_PAIRS) = range(9)
+SPL_HASHER_LINEAR, SPL_HASHER_MLP, SPL_HASHER_DOWNPROJ = 0, 1, 2
 SPL_F32, SPL_BF16 = 0, 1
 SPL_HASHER_LINEAR, SPL_HASHER_MLP = 0, 1
 SPL_ENCODE_EXACT, SPL_ENCODE_TC = 0, 1
@@ -51,13 +53,17 @@ class CudaError(SpotlightError):
     pass
 
 
+class EmptyPairError(SpotlightError):
+    """errors.hpp:27-30"""
+
+
 class StateError(SpotlightError):
     pass
 
 
 _ERR = {SPL_E_DIMENSION: DimensionError, SPL_E_NUMERIC: NumericError, SPL_E_FORMAT: FormatError,
         SPL_E_IO: IoError, SPL_E_CUDA: CudaError, SPL_E_NCCL: SpotlightError,
-        SPL_E_STATE: StateError}
+        SPL_E_STATE: StateError, SPL_E_EMPTY_PAIRS: EmptyPairError}
 
 _lib = None
 
@@ -109,8 +115,12 @@ _SIGS = {
     "spl_peer_connect_local": [vp, C.POINTER(vp), u32],
     "spl_peer_destroy": [vp],
     "spl_hamming_topk_sharded": [vp, vp, vp, u64, u32, vp, u32, vp, u32, u64, u32, vp, vp, vp, vp],
+    "spl_train_hasher": [vp, i32, u32, u32, u32, f32, vp, vp, vp, u32, vp, vp, vp, vp, vp, vp,
+                         C.POINTER(dbl), u32p, vp],
+    "spl_train_partition_host": [vp, u32, u32, u64, vp, vp, vp, vp],
+    "spl_train_lr_at": [u32, vp],
 }
-_RESTYPE = {"spl_version": C.c_char_p, "spl_last_error": C.c_char_p, "spl_ctx_destroy": None,
+_RESTYPE = {"spl_version": C.c_char_p, "spl_train_lr_at": C.c_double, "spl_last_error": C.c_char_p, "spl_ctx_destroy": None,
             "spl_peer_destroy": None,
             "spl_hasher_destroy": None, "spl_launch_count": C.c_uint64}
 
@@ -179,6 +189,54 @@ def plan_shard_host(all_hist, rank: int, k: int):
     if st:
         raise DimensionError("plan_shard_host: bad arguments")
     return dict(zip(("T", "quota", "take_eq", "count", "offset"), (o.value for o in outs)))
+
+
+class RankConfig(C.Structure):
+    """spl_rank_config = RankingLossConfig (ranking_loss.hpp:15-24); counts < 0: unset."""
+    _fields_ = [("beta", dbl), ("alpha", dbl), ("maskout", dbl), ("max_top", C.c_int64),
+                ("max_oth", C.c_int64), ("query_subsample", C.c_int64)]
+
+    def __init__(self, beta=1.0, alpha=3.0, maskout=0.98, max_top=None, max_oth=None,
+                 query_subsample=None):
+        super().__init__(beta, alpha, maskout, -1 if max_top is None else max_top,
+                         -1 if max_oth is None else max_oth,
+                         -1 if query_subsample is None else query_subsample)
+
+
+class TrainConfig(C.Structure):
+    """spl_train_config = TrainConfig (trainer.hpp:18-37), same defaults."""
+    _fields_ = [("num_iters", u32), ("warmup_iters", u32), ("batch", u32),
+                ("holdout_queries", u32), ("seed", u64), ("max_lr", dbl), ("min_lr", dbl),
+                ("adam_beta1", dbl), ("adam_beta2", dbl), ("adam_eps", dbl),
+                ("weight_decay", dbl), ("grad_clip", dbl), ("soft_gamma", dbl),
+                ("holdout_budget_rate", dbl)]
+
+    def __init__(self, num_iters=8192, warmup_iters=81, batch=1, holdout_queries=128, seed=0,
+                 max_lr=1e-3, min_lr=0.0, adam_beta1=0.9, adam_beta2=0.98, adam_eps=1e-8,
+                 weight_decay=0.1, grad_clip=1.0, soft_gamma=64.0, holdout_budget_rate=0.02):
+        super().__init__(num_iters, warmup_iters, batch, holdout_queries, seed, max_lr, min_lr,
+                         adam_beta1, adam_beta2, adam_eps, weight_decay, grad_clip, soft_gamma,
+                         holdout_budget_rate)
+
+
+def train_partition_host(rank: RankConfig, q_train: int, n: int, seed: int):
+    """partition_topk's draws (host; no GPU): (rows, top_pos, oth_pos, k_full)."""
+    import numpy as np
+
+    rows = np.zeros(max(q_train, 1), np.uint32)
+    top = np.zeros(max(n, 1), np.uint32)
+    oth = np.zeros(max(n, 1), np.uint32)
+    cnt = np.zeros(4, np.uint32)
+    st = load().spl_train_partition_host(C.byref(rank), q_train, n, seed, rows.ctypes.data,
+                                         top.ctypes.data, oth.ctypes.data, cnt.ctypes.data)
+    if st:
+        raise StateError("train_partition_host failed")
+    return rows[:cnt[0]].copy(), top[:cnt[1]].copy(), oth[:cnt[2]].copy(), int(cnt[3])
+
+
+def train_lr_at(it: int, cfg: TrainConfig) -> float:
+    """lr_at (trainer.cpp:35-46)."""
+    return load().spl_train_lr_at(it, C.byref(cfg))
 
 
 class Context:
@@ -258,6 +316,35 @@ class Context:
     def iou(self, a, cnt_a, a_stride, b, cnt_b, b_stride, P, out, stream=None):
         self.check(self.lib.spl_iou(self.h, _ptr(a), _ptr(cnt_a), a_stride, _ptr(b), _ptr(cnt_b),
                                     b_stride, P, _ptr(out), _stream(stream)))
+
+    # -- training
+    def train_hasher(self, kind, d, h, L, gamma, w1, b1, w2, sequences, rank: RankConfig,
+                     cfg: TrainConfig, stream=None):
+        """train_hasher (trainer.cpp:634-645) on the GPU. w1/b1/w2: float32 numpy
+        arrays updated in place (b1/w2 None for linear / downproj); sequences:
+        list of (queries, keys) float32 [n][d]. Returns dict(records [iters][3]
+        = loss, violation_rate, lr; holdout_iou; skipped_steps)."""
+        import numpy as np
+
+        for a in (w1, b1, w2):
+            if a is not None:
+                assert a.dtype == np.float32 and a.flags.c_contiguous
+        qs = np.ascontiguousarray(np.concatenate([q for q, _ in sequences]), dtype=np.float32)
+        ks = np.ascontiguousarray(np.concatenate([k for _, k in sequences]), dtype=np.float32)
+        lens = np.array([len(q) for q, _ in sequences], np.uint32)
+        for q, k in sequences:
+            if len(q) != len(k):
+                raise DimensionError("train_hasher: queries and keys must be causally aligned")
+        rec = np.zeros((max(cfg.num_iters, 1), 3), np.float64)
+        iou = C.c_double(0.0)
+        sk = C.c_uint32(0)
+        self.check(self.lib.spl_train_hasher(
+            self.h, kind, d, h, L, gamma, w1.ctypes.data,
+            None if b1 is None else b1.ctypes.data, None if w2 is None else w2.ctypes.data,
+            len(sequences), qs.ctypes.data, ks.ctypes.data, lens.ctypes.data, C.byref(rank),
+            C.byref(cfg), rec.ctypes.data, C.byref(iou), C.byref(sk), _stream(stream)))
+        return {"records": rec[:cfg.num_iters], "holdout_iou": iou.value,
+                "skipped_steps": sk.value}
 
     def hamming_topk(self, codes, stride_rows, L, qcodes, P, n_valid, nvalid_div, n_max, k, idx,
                      cnt, stream=None):

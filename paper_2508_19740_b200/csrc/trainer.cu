@@ -1,0 +1,1163 @@
+// Hasher training on the GPU: the reference's train_hasher
+// (trainer.cpp:520-645) for the MLP and linear coders with the pairwise
+// ranking loss (ranking_loss.cpp:80-145 sampling, trainer.cpp:297-380 soft
+// loss), AdamW (trainer.cpp:100-143), global-norm clipping (:83-97), the
+// warmup + cosine schedule (:35-46) and the holdout IoU (:472-518).
+//
+// Division of labour. The host keeps what is sequential and tiny: the
+// mt19937_64 draws (sequence pick, partition seed, randperm prefixes — the
+// same std:: engine and distributions as the reference, so the sampled
+// (query, top, other) sets are identical), the schedule, and pow(beta, t)
+// for the bias corrections. Everything that touches a matrix is a kernel:
+// exact q.k logits, the per-row descending order (bitonic sort in shared
+// memory), soft-code forward passes over every key, the ranking loss and its
+// gradient, backward through the coder, clipping, AdamW, and the holdout
+// retrieval (K1 codes -> K3 top-k vs float top-k of the logits -> IoU).
+//
+// Arithmetic follows the reference build's evaluation order per output
+// (compiled with EXACT_FLAGS; every rounding is an explicit intrinsic):
+//  * matmul / add_matmul_at (matrix.hpp:81-99, :121-138): one fused
+//    multiply-add chain per output, in index order, starting from the
+//    output's current value;
+//  * matmul_bt (matrix.hpp:101-117): rounded products summed in index order
+//    for the vectorised part, fused tail (as attention_eval's dot, see
+//    dense_retrieval.cu);
+//  * double dots of float soft codes (trainer.cpp:313-335): products are
+//    exact in double, so only the (sequential) add order matters;
+//  * per-key soft-code gradients: the reference adds g * sq to a key row
+//    query by query; here dk[key] is one fma chain over the selected queries
+//    in order, reading a dense [key][query] matrix of the g values — the same
+//    sequence of roundings.
+// Two reductions differ in order from the reference's sequential loops (the
+// reported loss sum and the clipping norm's sum of squares); both are
+// deterministic here and agree to a few ulps of a double. Double exp/log1p
+// are CUDA's (<= 1-2 ulp from glibc's): the pair gradients are rounded to
+// float before use, so they match unless a double lands within an ulp of a
+// float rounding boundary. tests/test_gpu_trainer.py checks weights, records
+// and holdout IoU against the unmodified reference's train_hasher.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdlib>
+#include <numeric>
+#include <random>
+#include <string>
+#include <vector>
+
+#include "spl_expf.cuh"
+#include "spl_launch.cuh"
+
+namespace spl {
+namespace {
+
+constexpr uint32_t kMaxSortKeys = 16384;  // per-row order sort in shared memory
+
+// halt codes (device): the reference throws out of train_loop at that point
+enum : uint32_t { HALT_NONE = 0, HALT_EMPTY = 1, HALT_NONFINITE = 2 };
+
+struct TrainDev {
+    uint32_t halt;          // HALT_*
+    uint32_t halt_iter;
+    uint32_t step;          // AdamW step (applied updates)
+    uint32_t skipped;       // non-finite gradient steps
+    uint32_t skip_now;      // this iteration's gradients are non-finite
+    uint32_t pad;
+    double bc1, bc2;        // this iteration's bias corrections
+    double loss_acc, viol_acc;
+    unsigned long long pairs;  // valid pairs of the current (iteration, batch) element
+};
+
+// ------------------------------------------------------------ scalar pieces
+__device__ __forceinline__ float sigmoid_f(float z) {
+    return __fdiv_rn(1.0f, __fadd_rn(1.0f, spl_expf(-z)));
+}
+// trainer.cpp:181-185 (silu_grad): s * (1 + z * (1 - s)), z*(1-s)+1 fused
+__device__ __forceinline__ float silu_grad_f(float z) {
+    const float s = sigmoid_f(z);
+    return __fmul_rn(s, __fmaf_rn(z, __fsub_rn(1.0f, s), 1.0f));
+}
+// hashers.hpp:151-159: gamma*z / (1 + gamma*|z|), gamma / (1 + gamma*|z|)^2
+__device__ __forceinline__ float soft_sign_f(float z, float g) {
+    return __fdiv_rn(__fmul_rn(g, z), __fmaf_rn(g, fabsf(z), 1.0f));
+}
+__device__ __forceinline__ float soft_sign_grad_f(float z, float g) {
+    const float den = __fmaf_rn(g, fabsf(z), 1.0f);
+    return __fdiv_rn(g, __fmul_rn(den, den));
+}
+// trainer.cpp:295-297
+__device__ __forceinline__ double softplus_d(double x) {
+    return x > 0.0 ? __dadd_rn(x, log1p(exp(-x))) : log1p(exp(x));
+}
+// the pair gradient of trainer.cpp:349-351 (beta * (1 - sigmoid(logit)) * inv)
+__device__ __forceinline__ double pair_g(double logit, double beta, double inv) {
+    const double sg = __ddiv_rn(1.0, __dadd_rn(1.0, exp(-logit)));
+    return __dmul_rn(__dmul_rn(beta, __dsub_rn(1.0, sg)), inv);
+}
+__device__ __forceinline__ uint32_t n4_of(uint32_t k) {
+    const uint32_t n8 = k / 8 * 8;
+    return (k - n8) >= 4 ? n8 + 4 : n8;
+}
+
+// ------------------------------------------------------------ exact logits
+// logits[i][j] = matmul_bt(Q, K)[i][j] * scale (trainer.cpp:394-400), all
+// q x n entries. 64 x 64 output tile per block, 4 x 4 per thread; the chain
+// of each output walks p in order across the 32-wide shared-memory chunks.
+__global__ void __launch_bounds__(256) k_logits(const float* __restrict__ Q, const float* __restrict__ K,
+                                                uint32_t q, uint32_t n, uint32_t d, float scale,
+                                                float* __restrict__ out) {
+    __shared__ float qs[64][33], ks[64][33];
+    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+    const uint32_t r0 = blockIdx.y * 64, c0 = blockIdx.x * 64;
+    const uint32_t n4 = n4_of(d);
+    float acc[4][4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = 0.0f;
+    for (uint32_t p0 = 0; p0 < d; p0 += 32) {
+        const uint32_t w = min(32u, d - p0);
+        for (uint32_t e = threadIdx.x; e < 64 * 32; e += 256) {
+            const uint32_t r = e / 32, c = e % 32;
+            qs[r][c] = (r0 + r < q && c < w) ? Q[(uint64_t)(r0 + r) * d + p0 + c] : 0.0f;
+            ks[r][c] = (c0 + r < n && c < w) ? K[(uint64_t)(c0 + r) * d + p0 + c] : 0.0f;
+        }
+        __syncthreads();
+        for (uint32_t pp = 0; pp < w; ++pp) {
+            const bool fused = p0 + pp >= n4;
+            float a[4], b[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) a[i] = qs[ty + 16 * i][pp];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) b[j] = ks[tx + 16 * j][pp];
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+                    acc[i][j] = fused ? __fmaf_rn(a[i], b[j], acc[i][j])
+                                      : __fadd_rn(acc[i][j], __fmul_rn(a[i], b[j]));
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const uint32_t r = r0 + ty + 16 * i, c = c0 + tx + 16 * j;
+            if (r < q && c < n) out[(uint64_t)r * n + c] = __fmul_rn(acc[i][j], scale);
+        }
+}
+
+// ------------------------------------------------------------ order
+// build_topk_order (ranking_loss.cpp:30-59) for one row per block: causally
+// valid keys by descending score, ties to the lower index, masked keys last
+// in index order. Keys (~orderable(score) << 32 | j) sorted ascending by a
+// bitonic network over the next power of two (pads sort last); -0 == +0.
+__device__ __forceinline__ uint32_t orderable(float f) {
+    uint32_t u = __float_as_uint(f);
+    if (u == 0x80000000u) u = 0u;
+    return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+__global__ void __launch_bounds__(1024) k_order(const float* __restrict__ logits, uint32_t n,
+                                                uint32_t npow2, uint32_t* __restrict__ order) {
+    extern __shared__ unsigned long long keys[];
+    const uint32_t row = blockIdx.x;
+    const uint32_t valid = min(row + 1, n);
+    const float* s = logits + (uint64_t)row * n;
+    for (uint32_t j = threadIdx.x; j < npow2; j += blockDim.x) {
+        unsigned long long key = ~0ull;
+        if (j < n) {
+            const uint32_t hi = j < valid ? ~orderable(s[j]) : 0xFFFFFFFFu;
+            key = ((unsigned long long)hi << 32) | j;
+        }
+        keys[j] = key;
+    }
+    __syncthreads();
+    for (uint32_t k = 2; k <= npow2; k <<= 1)
+        for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+            for (uint32_t i = threadIdx.x; i < npow2; i += blockDim.x) {
+                const uint32_t l = i ^ j;
+                if (l > i) {
+                    const unsigned long long a = keys[i], b = keys[l];
+                    const bool up = (i & k) == 0;
+                    if ((a > b) == up) {
+                        keys[i] = b;
+                        keys[l] = a;
+                    }
+                }
+            }
+            __syncthreads();
+        }
+    for (uint32_t j = threadIdx.x; j < n; j += blockDim.x)
+        order[(uint64_t)row * n + j] = (uint32_t)keys[j];
+}
+
+// ------------------------------------------------------------ forward
+// MlpCoder / LinearCoder / DownProjCoder forward (trainer.cpp:199-217,
+// :245-250, :275-277) over m rows (rows[] selects rows of x when given):
+// MLP z1 = x W1 (+ b1), a1 = z1 * sigmoid(z1), z2 = a1 W2; linear z2 = x P;
+// soft = soft_sign(z2) (downproj: soft = x P). 16 rows per block; each
+// thread owns output columns, one fma chain per (row, column).
+constexpr int kFwdRows = 16;
+template <int KIND>  // SPL_HASHER_MLP / SPL_HASHER_LINEAR / 2 = downproj
+__global__ void __launch_bounds__(128) k_forward(const float* __restrict__ x, const uint32_t* rows,
+                                                 uint32_t m, uint32_t d, uint32_t h, uint32_t L,
+                                                 const float* __restrict__ w1,
+                                                 const float* __restrict__ b1,
+                                                 const float* __restrict__ w2, float gamma,
+                                                 float* z1, float* a1, float* z2, float* soft,
+                                                 const TrainDev* st) {
+    if (st->halt) return;
+    extern __shared__ float sm[];
+    float* xs = sm;                       // [kFwdRows][d]
+    float* as = sm + kFwdRows * d;        // [kFwdRows][h] (MLP)
+    const uint32_t r0 = blockIdx.x * kFwdRows;
+    const uint32_t nr = min((uint32_t)kFwdRows, m - r0);
+    for (uint32_t e = threadIdx.x; e < (uint32_t)kFwdRows * d; e += blockDim.x) {
+        const uint32_t r = e / d, c = e % d;
+        float v = 0.0f;
+        if (r < nr) {
+            const uint32_t src = rows ? rows[r0 + r] : r0 + r;
+            v = x[(uint64_t)src * d + c];
+        }
+        xs[e] = v;
+    }
+    __syncthreads();
+    const float* in = xs;
+    uint32_t K = d;
+    const float* W = w1;
+    if (KIND == SPL_HASHER_MLP) {
+        for (uint32_t j = threadIdx.x; j < h; j += blockDim.x) {
+            float acc[kFwdRows];
+#pragma unroll
+            for (int r = 0; r < kFwdRows; ++r) acc[r] = 0.0f;
+            for (uint32_t p = 0; p < d; ++p) {
+                const float w = w1[(uint64_t)p * h + j];
+#pragma unroll
+                for (int r = 0; r < kFwdRows; ++r) acc[r] = __fmaf_rn(xs[r * d + p], w, acc[r]);
+            }
+            const float bj = b1[j];
+#pragma unroll
+            for (int r = 0; r < kFwdRows; ++r) {
+                const float z = __fadd_rn(acc[r], bj);
+                const float a = __fmul_rn(z, sigmoid_f(z));
+                as[r * h + j] = a;
+                if ((uint32_t)r < nr) {
+                    z1[(uint64_t)(r0 + r) * h + j] = z;
+                    a1[(uint64_t)(r0 + r) * h + j] = a;
+                }
+            }
+        }
+        __syncthreads();
+        in = as;
+        K = h;
+        W = w2;
+    }
+    for (uint32_t j = threadIdx.x; j < L; j += blockDim.x) {
+        float acc[kFwdRows];
+#pragma unroll
+        for (int r = 0; r < kFwdRows; ++r) acc[r] = 0.0f;
+        for (uint32_t p = 0; p < K; ++p) {
+            const float w = W[(uint64_t)p * L + j];
+#pragma unroll
+            for (int r = 0; r < kFwdRows; ++r) acc[r] = __fmaf_rn(in[r * K + p], w, acc[r]);
+        }
+#pragma unroll
+        for (int r = 0; r < kFwdRows; ++r)
+            if ((uint32_t)r < nr) {
+                const uint64_t o = (uint64_t)(r0 + r) * L + j;
+                if (KIND != 2) z2[o] = acc[r];
+                soft[o] = KIND == 2 ? acc[r] : soft_sign_f(acc[r], gamma);
+            }
+    }
+}
+
+// ------------------------------------------------------------ partition
+// partition_topk's index gather (ranking_loss.cpp:118-141): key =
+// order[row][pos]; an entry is valid iff key < the row's causal offset.
+// Adds this (iteration, element)'s valid pair count (sum over rows of
+// valid_top * valid_oth) into st->pairs.
+__global__ void __launch_bounds__(256) k_partition(const uint32_t* __restrict__ order, uint32_t n,
+                                                   uint32_t k_full, const uint32_t* qrows,
+                                                   const uint32_t* top_pos, uint32_t T,
+                                                   const uint32_t* oth_pos, uint32_t O,
+                                                   uint32_t* top_idx, uint32_t* oth_idx,
+                                                   TrainDev* st) {
+    if (st->halt) return;
+    __shared__ uint32_t s_t[8], s_o[8];
+    const uint32_t qi = blockIdx.x;
+    const uint32_t row = qrows[qi];
+    const uint32_t valid = min(row + 1, n);
+    const uint32_t* ro = order + (uint64_t)row * n;
+    uint32_t ct = 0, co = 0;
+    for (uint32_t i = threadIdx.x; i < T; i += blockDim.x) {
+        const uint32_t key = ro[top_pos[i]];
+        const bool ok = key < valid;
+        top_idx[(uint64_t)qi * T + i] = ok ? key : ~0u;
+        ct += ok;
+    }
+    for (uint32_t j = threadIdx.x; j < O; j += blockDim.x) {
+        const uint32_t key = ro[k_full + oth_pos[j]];
+        const bool ok = key < valid;
+        oth_idx[(uint64_t)qi * O + j] = ok ? key : ~0u;
+        co += ok;
+    }
+    for (int o = 16; o; o >>= 1) {
+        ct += __shfl_xor_sync(~0u, ct, o);
+        co += __shfl_xor_sync(~0u, co, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        s_t[threadIdx.x >> 5] = ct;
+        s_o[threadIdx.x >> 5] = co;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint32_t a = 0, b = 0;
+        for (uint32_t w = 0; w < blockDim.x / 32; ++w) {
+            a += s_t[w];
+            b += s_o[w];
+        }
+        atomicAdd(&st->pairs, (unsigned long long)a * b);
+    }
+}
+
+// ------------------------------------------------------------ ranking loss
+// ranking_soft_loss (trainer.cpp:299-380) for one selected query per block:
+// B_i = <sq, sk_top_i>, C_j = <sq, sk_oth_j> in double; per valid pair
+// softplus(-(beta (B_i - C_j) - alpha)), violations, and the pair gradient
+// g; gb[i] = -sum_j g (j ascending), gc[j] = sum_i g (i ascending); then
+// dq = fma chain over the top entries then the other entries, and the g
+// values of every touched key go to G[key][qi] for the key-side chain.
+__global__ void __launch_bounds__(256) k_rank_loss(const float* __restrict__ softq,
+                                                   const float* __restrict__ softk, uint32_t L,
+                                                   const uint32_t* top_idx, uint32_t T,
+                                                   const uint32_t* oth_idx, uint32_t O,
+                                                   uint32_t Qs, double beta, double alpha,
+                                                   double* gbuf_t, double* gbuf_o, float* G,
+                                                   float* dsq, double* loss_part,
+                                                   unsigned long long* viol_part, TrainDev* st,
+                                                   uint32_t iter) {
+    if (st->halt) return;
+    const unsigned long long vp = st->pairs;
+    if (vp == 0) {  // EmptyPairError (trainer.cpp:303-305)
+        if (blockIdx.x == 0 && threadIdx.x == 0) {
+            st->halt = HALT_EMPTY;
+            st->halt_iter = iter;
+        }
+        return;
+    }
+    const double inv = __ddiv_rn(1.0, (double)vp);
+    extern __shared__ double dsm[];
+    double* bv = dsm;           // [T]
+    double* cv = dsm + T;       // [O]
+    float* sq = reinterpret_cast<float*>(dsm + T + O);  // [L]
+    __shared__ double s_loss[8];
+    __shared__ unsigned long long s_viol[8];
+    const uint32_t qi = blockIdx.x;
+    const uint32_t* ti = top_idx + (uint64_t)qi * T;
+    const uint32_t* oi = oth_idx + (uint64_t)qi * O;
+    for (uint32_t p = threadIdx.x; p < L; p += blockDim.x) sq[p] = softq[(uint64_t)qi * L + p];
+    __syncthreads();
+    for (uint32_t e = threadIdx.x; e < T + O; e += blockDim.x) {
+        const uint32_t key = e < T ? ti[e] : oi[e - T];
+        double acc = 0.0;
+        if (key != ~0u) {
+            const float* sk = softk + (uint64_t)key * L;
+            for (uint32_t p = 0; p < L; ++p)
+                acc = __dadd_rn(acc, __dmul_rn((double)sq[p], (double)sk[p]));
+        }
+        if (e < T) bv[e] = acc; else cv[e - T] = acc;
+    }
+    __syncthreads();
+    double loss = 0.0;
+    unsigned long long viol = 0;
+    for (uint32_t i = threadIdx.x; i < T; i += blockDim.x) {
+        double g_acc = 0.0;
+        if (ti[i] != ~0u) {
+            const double b = bv[i];
+            for (uint32_t j = 0; j < O; ++j) {
+                if (oi[j] == ~0u) continue;
+                const double z = __dsub_rn(b, cv[j]);
+                const double logit = __fma_rn(beta, z, -alpha);
+                loss = __dadd_rn(loss, softplus_d(-logit));
+                viol += z < 0.0;
+                g_acc = __dsub_rn(g_acc, pair_g(logit, beta, inv));
+            }
+        }
+        gbuf_t[(uint64_t)qi * T + i] = g_acc;
+    }
+    for (uint32_t j = threadIdx.x; j < O; j += blockDim.x) {
+        double g_acc = 0.0;
+        if (oi[j] != ~0u) {
+            const double c = cv[j];
+            for (uint32_t i = 0; i < T; ++i) {
+                if (ti[i] == ~0u) continue;
+                const double logit = __fma_rn(beta, __dsub_rn(bv[i], c), -alpha);
+                g_acc = __dadd_rn(g_acc, pair_g(logit, beta, inv));
+            }
+        }
+        gbuf_o[(uint64_t)qi * O + j] = g_acc;
+    }
+    // deterministic block reduction of the loss / violation partials
+    for (int o = 16; o; o >>= 1) {
+        loss = __dadd_rn(loss, __shfl_xor_sync(~0u, loss, o));
+        viol += __shfl_xor_sync(~0u, viol, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        s_loss[threadIdx.x >> 5] = loss;
+        s_viol[threadIdx.x >> 5] = viol;
+    }
+    __syncthreads();  // also orders the gbuf writes before the reads below
+    if (threadIdx.x == 0) {
+        double a = 0.0;
+        unsigned long long v = 0;
+        for (uint32_t w = 0; w < blockDim.x / 32; ++w) {
+            a = __dadd_rn(a, s_loss[w]);
+            v += s_viol[w];
+        }
+        loss_part[qi] = a;
+        viol_part[qi] = v;
+    }
+    const double* gt = gbuf_t + (uint64_t)qi * T;
+    const double* go = gbuf_o + (uint64_t)qi * O;
+    for (uint32_t p = threadIdx.x; p < L; p += blockDim.x) {
+        float dq = 0.0f;
+        for (uint32_t i = 0; i < T; ++i) {
+            const double g = gt[i];
+            if (g == 0.0) continue;
+            dq = __fmaf_rn(__double2float_rn(g), softk[(uint64_t)ti[i] * L + p], dq);
+        }
+        for (uint32_t j = 0; j < O; ++j) {
+            const double g = go[j];
+            if (g == 0.0) continue;
+            dq = __fmaf_rn(__double2float_rn(g), softk[(uint64_t)oi[j] * L + p], dq);
+        }
+        dsq[(uint64_t)qi * L + p] = dq;
+    }
+    for (uint32_t i = threadIdx.x; i < T; i += blockDim.x)
+        if (gt[i] != 0.0) G[(uint64_t)ti[i] * Qs + qi] = __double2float_rn(gt[i]);
+    for (uint32_t j = threadIdx.x; j < O; j += blockDim.x)
+        if (go[j] != 0.0) G[(uint64_t)oi[j] * Qs + qi] = __double2float_rn(go[j]);
+}
+
+// loss = sum of the query partials * inv_pairs; non-finite -> NumericError
+// (trainer.cpp:587-590); accumulates the iteration record over the batch.
+__global__ void k_loss_finalize(const double* loss_part, const unsigned long long* viol_part,
+                                uint32_t Qs, uint32_t b, uint32_t batch, uint32_t iter,
+                                double* rec, TrainDev* st) {
+    if (st->halt) return;
+    const double inv = __ddiv_rn(1.0, (double)st->pairs);
+    double s = 0.0;
+    unsigned long long v = 0;
+    for (uint32_t q = 0; q < Qs; ++q) {
+        s = __dadd_rn(s, loss_part[q]);
+        v += viol_part[q];
+    }
+    const double loss = __dmul_rn(s, inv), vr = __dmul_rn((double)v, inv);
+    if (!isfinite(loss)) {
+        st->halt = HALT_NONFINITE;
+        st->halt_iter = iter;
+        return;
+    }
+    st->loss_acc = b == 0 ? loss : __dadd_rn(st->loss_acc, loss);
+    st->viol_acc = b == 0 ? vr : __dadd_rn(st->viol_acc, vr);
+    if (b + 1 == batch) {
+        rec[3 * (uint64_t)iter] = __ddiv_rn(st->loss_acc, (double)batch);
+        rec[3 * (uint64_t)iter + 1] = __ddiv_rn(st->viol_acc, (double)batch);
+    }
+    st->pairs = 0;  // the next element's count starts from zero
+}
+
+// d soft_k = G^T-chain: dk[key][p] = fma over the selected queries in order
+// of G[key][qi] * sq[qi][p] (zero G entries are the reference's skipped
+// pairs); x (1/batch) when batch > 1 (trainer.cpp:591-595).
+__global__ void __launch_bounds__(256) k_dsoft_keys(const float* __restrict__ G,
+                                                    const float* __restrict__ softq, uint32_t Qs,
+                                                    uint32_t n, uint32_t L, float invb,
+                                                    float* __restrict__ dsk, const TrainDev* st) {
+    if (st->halt) return;
+    const uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= (uint64_t)n * L) return;
+    const uint64_t key = e / L;
+    const uint32_t p = (uint32_t)(e % L);
+    float acc = 0.0f;
+    for (uint32_t q = 0; q < Qs; ++q) {
+        const float g = G[key * Qs + q];
+        if (g != 0.0f) acc = __fmaf_rn(g, softq[(uint64_t)q * L + p], acc);
+    }
+    dsk[e] = invb != 1.0f ? __fmul_rn(acc, invb) : acc;
+}
+
+__global__ void k_scale(float* x, uint64_t n, float s, const TrainDev* st) {
+    if (st->halt) return;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x)
+        x[i] = __fmul_rn(x[i], s);
+}
+
+__global__ void k_gather_rows(const float* __restrict__ x, const uint32_t* rows, uint32_t d,
+                              float* __restrict__ out, const TrainDev* st) {
+    if (st->halt) return;
+    const uint64_t src = rows[blockIdx.x];
+    for (uint32_t c = threadIdx.x; c < d; c += blockDim.x)
+        out[(uint64_t)blockIdx.x * d + c] = x[src * d + c];
+}
+
+// ------------------------------------------------------------ backward
+// dz = d_soft * soft_sign_grad(z) (trainer.cpp:222-225, :253-257)
+__global__ void k_dz(const float* __restrict__ dsoft, const float* __restrict__ z, uint64_t n,
+                     float gamma, float* __restrict__ dz, const TrainDev* st) {
+    if (st->halt) return;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x)
+        dz[i] = __fmul_rn(dsoft[i], soft_sign_grad_f(z[i], gamma));
+}
+
+// C[m][nc] += A[rows][m]^T B[rows][nc] (add_matmul_at, matrix.hpp:121-138):
+// each output one fma chain over the rows in order, from its current value.
+// Block: 128 columns x 4 output rows; 32-row chunks staged in shared memory.
+__global__ void __launch_bounds__(128) k_add_at(const float* __restrict__ A,
+                                                const float* __restrict__ B, uint32_t rows,
+                                                uint32_t m, uint32_t nc, float* __restrict__ C,
+                                                const TrainDev* st) {
+    if (st->halt) return;
+    __shared__ float as[32][4], bs[32][128];
+    const uint32_t j = blockIdx.x * 128 + threadIdx.x;
+    const uint32_t i0 = blockIdx.y * 4;
+    float acc[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) acc[i] = (i0 + i < m && j < nc) ? C[(uint64_t)(i0 + i) * nc + j] : 0.0f;
+    for (uint32_t r0 = 0; r0 < rows; r0 += 32) {
+        const uint32_t w = min(32u, rows - r0);
+        for (uint32_t e = threadIdx.x; e < 32 * 4; e += 128) {
+            const uint32_t r = e / 4, i = e % 4;
+            as[r][i] = (r < w && i0 + i < m) ? A[(uint64_t)(r0 + r) * m + i0 + i] : 0.0f;
+        }
+        for (uint32_t r = 0; r < w; ++r)
+            bs[r][threadIdx.x] = j < nc ? B[(uint64_t)(r0 + r) * nc + j] : 0.0f;
+        __syncthreads();
+        for (uint32_t r = 0; r < w; ++r) {
+            const float b = bs[r][threadIdx.x];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) acc[i] = __fmaf_rn(as[r][i], b, acc[i]);
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+        if (i0 + i < m && j < nc) C[(uint64_t)(i0 + i) * nc + j] = acc[i];
+}
+
+// da1 = matmul_bt(dz2, W2) * silu_grad(z1) (trainer.cpp:227-230).
+constexpr int kDaRows = 8;
+__global__ void __launch_bounds__(128) k_da1(const float* __restrict__ dz2,
+                                             const float* __restrict__ w2,
+                                             const float* __restrict__ z1, uint32_t m, uint32_t h,
+                                             uint32_t L, float* __restrict__ da1,
+                                             const TrainDev* st) {
+    if (st->halt) return;
+    extern __shared__ float zs[];  // [kDaRows][L]
+    const uint32_t r0 = blockIdx.x * kDaRows;
+    const uint32_t nr = min((uint32_t)kDaRows, m - r0);
+    for (uint32_t e = threadIdx.x; e < nr * L; e += blockDim.x) zs[e] = dz2[(uint64_t)r0 * L + e];
+    __syncthreads();
+    const uint32_t n4 = n4_of(L);
+    for (uint32_t i = threadIdx.x; i < h; i += blockDim.x) {
+        const float* wr = w2 + (uint64_t)i * L;
+        for (uint32_t r = 0; r < nr; ++r) {
+            const float* a = zs + r * L;
+            float acc = 0.0f;
+            uint32_t p = 0;
+            for (; p < n4; ++p) acc = __fadd_rn(acc, __fmul_rn(a[p], wr[p]));
+            for (; p < L; ++p) acc = __fmaf_rn(a[p], wr[p], acc);
+            const uint64_t o = (uint64_t)(r0 + r) * h + i;
+            da1[o] = __fmul_rn(acc, silu_grad_f(z1[o]));
+        }
+    }
+}
+
+// b1 += column sums of da1 in row order (trainer.cpp:231-234)
+__global__ void k_b1(const float* __restrict__ da1, uint32_t m, uint32_t h, float* b1g,
+                     const TrainDev* st) {
+    if (st->halt) return;
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= h) return;
+    float acc = b1g[i];
+    for (uint32_t r = 0; r < m; ++r) acc = __fadd_rn(acc, da1[(uint64_t)r * h + i]);
+    b1g[i] = acc;
+}
+
+// ------------------------------------------------------------ optimiser
+// clip_gradient_norm (trainer.cpp:83-97) + adamw_step's finiteness check and
+// bias corrections (:114-121). One block; deterministic tree sum.
+__global__ void __launch_bounds__(1024) k_clip(float* g, uint64_t n, double max_norm,
+                                               const double* bc1_tab, const double* bc2_tab,
+                                               TrainDev* st) {
+    if (st->halt) return;
+    __shared__ double s[32];
+    __shared__ float s_scale;
+    __shared__ int s_bad;
+    double acc = 0.0;
+    for (uint64_t i = threadIdx.x; i < n; i += blockDim.x) {
+        const double v = (double)g[i];
+        acc = __fma_rn(v, v, acc);
+    }
+    for (int o = 16; o; o >>= 1) acc = __dadd_rn(acc, __shfl_xor_sync(~0u, acc, o));
+    if ((threadIdx.x & 31) == 0) s[threadIdx.x >> 5] = acc;
+    if (threadIdx.x == 0) s_bad = 0;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (uint32_t w = 0; w < blockDim.x / 32; ++w) t = __dadd_rn(t, s[w]);
+        const double norm = __dsqrt_rn(t);
+        s_scale = (max_norm > 0.0 && norm > max_norm) ? __double2float_rn(__ddiv_rn(max_norm, norm))
+                                                      : 1.0f;
+    }
+    __syncthreads();
+    const float sc = s_scale;
+    int bad = 0;
+    for (uint64_t i = threadIdx.x; i < n; i += blockDim.x) {
+        float v = g[i];
+        if (sc != 1.0f) {
+            v = __fmul_rn(v, sc);
+            g[i] = v;
+        }
+        bad |= !isfinite(v);
+    }
+    if (bad) s_bad = 1;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        if (s_bad) {
+            st->skip_now = 1;
+            st->skipped += 1;
+        } else {
+            st->skip_now = 0;
+            st->step += 1;
+            st->bc1 = bc1_tab[st->step];
+            st->bc2 = bc2_tab[st->step];
+        }
+    }
+}
+
+// adamw_step's update (trainer.cpp:122-139), f64 moments; decay on
+// [0, n_decay0) and [n_decay1, n) (the weight matrices, not b1).
+__global__ void k_adamw(float* w, const float* g, double* m1, double* m2, uint64_t n,
+                        uint64_t n_decay0, uint64_t n_decay1, double lr, double b1, double b2,
+                        double eps, double wd, const TrainDev* st) {
+    if (st->halt || st->skip_now) return;
+    const double bc1 = st->bc1, bc2 = st->bc2;
+    const double c1 = __dsub_rn(1.0, b1), c2 = __dsub_rn(1.0, b2);
+    const double lwd = __dmul_rn(lr, wd);
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        const double gv = (double)g[i];
+        const double m = __fma_rn(b1, m1[i], __dmul_rn(c1, gv));
+        const double v = __fma_rn(b2, m2[i], __dmul_rn(__dmul_rn(c2, gv), gv));
+        m1[i] = m;
+        m2[i] = v;
+        const double mhat = __ddiv_rn(m, bc1), vhat = __ddiv_rn(v, bc2);
+        const double w_old = (double)w[i];
+        double w_new = __dsub_rn(w_old, __ddiv_rn(__dmul_rn(lr, mhat), __dadd_rn(__dsqrt_rn(vhat), eps)));
+        if (wd > 0.0 && (i < n_decay0 || i >= n_decay1)) w_new = __fma_rn(-lwd, w_old, w_new);
+        w[i] = __double2float_rn(w_new);
+    }
+}
+
+// ------------------------------------------------------------ host side
+uint64_t derive_seed(uint64_t base, uint64_t stream) {  // rng.hpp:10-15
+    uint64_t z = base + 0x9E3779B97F4A7C15ULL * (stream + 1);
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+    return z ^ (z >> 31);
+}
+
+// first `take` entries of a random permutation of [0, n), in draw order
+// (ranking_loss.cpp:63-75)
+std::vector<uint32_t> randperm_take(uint32_t n, uint32_t take, std::mt19937_64& eng) {
+    std::vector<uint32_t> perm(n);
+    std::iota(perm.begin(), perm.end(), 0u);
+    const uint32_t m = std::min(take, n);
+    for (uint32_t i = 0; i < m; ++i) {
+        std::uniform_int_distribution<uint32_t> pick(i, n - 1);
+        std::swap(perm[i], perm[pick(eng)]);
+    }
+    perm.resize(m);
+    return perm;
+}
+
+struct Sample {  // one (iteration, batch element) draw
+    uint32_t seq = 0;
+    std::vector<uint32_t> qrows, top_pos, oth_pos;
+    uint32_t k_full = 0;
+};
+
+std::string rank_cfg_error(const spl_rank_config& c, uint64_t n) {  // ranking_loss.cpp:13-28
+    if (c.beta <= 0.0) return "ranking loss: beta must be positive";
+    if (!(c.maskout > 0.0 && c.maskout < 1.0)) return "ranking loss: maskout must lie in (0, 1)";
+    const auto k = static_cast<uint32_t>(static_cast<double>(n) * (1.0 - c.maskout));
+    if (k == 0) return "ranking loss: top count floored to zero for n=" + std::to_string(n);
+    if (c.max_top == 0) return "ranking loss: max_top must be >= 1";
+    if (c.max_oth == 0) return "ranking loss: max_oth must be >= 1";
+    if (c.query_subsample == 0) return "ranking loss: query_subsample must be >= 1";
+    return "";
+}
+
+// partition_topk's draws (ranking_loss.cpp:80-116) for a sequence whose
+// order covers q_train rows of n keys.
+Sample draw_partition(uint32_t q_train, uint32_t n, const spl_rank_config& c, uint64_t seed) {
+    Sample s;
+    const auto k_full = static_cast<uint32_t>(static_cast<double>(n) * (1.0 - c.maskout));
+    const uint32_t oth_full = n - k_full;
+    std::mt19937_64 eng(seed);
+    s.k_full = k_full;
+    s.qrows.resize(q_train);
+    std::iota(s.qrows.begin(), s.qrows.end(), 0u);
+    if (c.query_subsample > 0 && (uint64_t)c.query_subsample < q_train) {
+        s.qrows = randperm_take(q_train, (uint32_t)c.query_subsample, eng);
+        std::sort(s.qrows.begin(), s.qrows.end());
+    }
+    s.top_pos.resize(k_full);
+    std::iota(s.top_pos.begin(), s.top_pos.end(), 0u);
+    if (c.max_top > 0 && (uint64_t)c.max_top < k_full)
+        s.top_pos = randperm_take(k_full, (uint32_t)c.max_top, eng);
+    s.oth_pos.resize(oth_full);
+    std::iota(s.oth_pos.begin(), s.oth_pos.end(), 0u);
+    if (c.max_oth > 0 && (uint64_t)c.max_oth < oth_full)
+        s.oth_pos = randperm_take(oth_full, (uint32_t)c.max_oth, eng);
+    return s;
+}
+
+struct DevBuf {  // owning device allocation list
+    std::vector<void*> ptrs;
+    ~DevBuf() {
+        for (void* p : ptrs) cudaFree(p);
+    }
+    template <typename T>
+    T* get(size_t count) {
+        void* p = nullptr;
+        if (cudaMalloc(&p, std::max<size_t>(count, 1) * sizeof(T)) != cudaSuccess) return nullptr;
+        ptrs.push_back(p);
+        return static_cast<T*>(p);
+    }
+};
+
+}  // namespace
+
+double train_lr_at(uint32_t iter, const spl_train_config& c) {  // trainer.cpp:35-46
+    if (c.num_iters == 0) return c.max_lr;
+    const uint32_t warmup = std::min(c.warmup_iters, c.num_iters);
+    if (iter < warmup) return c.max_lr * static_cast<double>(iter) / static_cast<double>(warmup);
+    const uint32_t last = c.num_iters - 1;
+    if (last <= warmup) return c.max_lr;
+    const double progress = static_cast<double>(iter - warmup) / static_cast<double>(last - warmup);
+    // the reference build contracts min + (0.5 (max - min)) (1 + cos) into one fma
+    return std::fma(0.5 * (c.max_lr - c.min_lr), 1.0 + std::cos(M_PI * progress), c.min_lr);
+}
+
+spl_status train_partition_host(const spl_rank_config& c, uint32_t q_train, uint32_t n,
+                                uint64_t seed, uint32_t* rows, uint32_t* top_pos,
+                                uint32_t* oth_pos, uint32_t* counts) {
+    const Sample s = draw_partition(q_train, n, c, seed);
+    std::copy(s.qrows.begin(), s.qrows.end(), rows);
+    std::copy(s.top_pos.begin(), s.top_pos.end(), top_pos);
+    std::copy(s.oth_pos.begin(), s.oth_pos.end(), oth_pos);
+    counts[0] = (uint32_t)s.qrows.size();
+    counts[1] = (uint32_t)s.top_pos.size();
+    counts[2] = (uint32_t)s.oth_pos.size();
+    counts[3] = s.k_full;
+    return SPL_OK;
+}
+
+// holdout_iou (trainer.cpp:472-518) for the MLP / linear coders: hash codes
+// of every key and of the held-out queries (exact encoder K1), Hamming top-k
+// (K3, the index shared by all rows: problem stride 0, per-row causal
+// n_valid), float top-k of the exact logits, IoU per row, host mean in row
+// order.
+spl_status holdout_iou_impl(spl_ctx* ctx, int kind, uint32_t d, uint32_t h, uint32_t L,
+                            const float* w1, const float* b1, const float* w2, const float* xq,
+                            const float* xk, const float* logits, uint32_t q, uint32_t q_train,
+                            double rate, double* out, cudaStream_t s) {
+    const uint32_t n = q;
+    const uint32_t first = q_train < q ? q_train : 0;
+    const uint32_t P = q - first;
+    uint32_t budget = 0;
+    if (spl_status st = spl_budget_from_rate(rate, n, &budget)) return fail(ctx, st, "budget_from_rate");
+    DevBuf db;
+    uint32_t* nv = db.get<uint32_t>(P);
+    uint32_t *ia = db.get<uint32_t>((size_t)P * budget), *ib = db.get<uint32_t>((size_t)P * budget);
+    uint32_t *ca = db.get<uint32_t>(P), *cb = db.get<uint32_t>(P);
+    double* iou = db.get<double>(P);
+    if (!nv || !ia || !ib || !ca || !cb || !iou) return fail(ctx, SPL_E_CUDA, "train: out of device memory");
+    std::vector<uint32_t> hv(P);
+    for (uint32_t r = 0; r < P; ++r) hv[r] = first + r + 1;  // offsets min(i + 1, n)
+    SPL_CUDA_TRY(ctx, cudaMemcpyAsync(nv, hv.data(), P * 4, cudaMemcpyHostToDevice, s));
+    if (kind == SPL_HASHER_DOWNPROJ) {
+        // kp = K P, qp = Q P (matmul), dp_scores = dot(qp, kp_j), float top-k
+        float* dw = db.get<float>((size_t)d * L);
+        float* kp = db.get<float>((size_t)n * L);
+        float* qp = db.get<float>((size_t)P * L);
+        float* sc = db.get<float>((size_t)P * n);
+        if (!dw || !kp || !qp || !sc) return fail(ctx, SPL_E_CUDA, "train: out of device memory");
+        SPL_CUDA_TRY(ctx, cudaMemcpyAsync(dw, w1, (size_t)d * L * 4, cudaMemcpyHostToDevice, s));
+        if (spl_status st = project_launch(ctx, xk, n, d, dw, L, kp, s)) return st;
+        if (spl_status st = project_launch(ctx, xq + (size_t)first * d, P, d, dw, L, qp, s)) return st;
+        if (spl_status st = causal_logits_launch(ctx, qp, kp, SPL_F32, 0, L, P, nv, 1, n, 1.0f, sc, s))
+            return st;
+        if (spl_status st = top_k_launch(ctx, sc, 1, P, n, n, budget, ia, s, nv, 1, ca)) return st;
+    } else {
+        spl_hasher* hs = nullptr;
+        if (spl_status st = spl_hasher_create(ctx, kind, 1, d, h, L, w1, b1, w2, &hs)) return st;
+        struct HG {
+            spl_hasher* h;
+            ~HG() { spl_hasher_destroy(h); }
+        } guard_{hs};
+        const uint32_t W = L / 32;
+        uint32_t* kc = db.get<uint32_t>((size_t)n * W);
+        uint32_t* qc = db.get<uint32_t>((size_t)P * W);
+        if (!kc || !qc) return fail(ctx, SPL_E_CUDA, "train: out of device memory");
+        if (spl_status st = spl_encode(ctx, hs, xk, 1, n, SPL_ENCODE_EXACT, kc, s)) return st;
+        if (spl_status st = spl_encode(ctx, hs, xq + (size_t)first * d, 1, P, SPL_ENCODE_EXACT, qc, s))
+            return st;
+        if (spl_status st = hamming_topk_impl(ctx, kc, 0, L, qc, P, nv, 1, n, budget, ia, ca, s)) return st;
+    }
+    if (spl_status st = top_k_launch(ctx, logits + (size_t)first * n, 1, P, n, n, budget, ib, s, nv, 1, cb))
+        return st;
+    if (spl_status st = iou_launch(ctx, ia, ca, budget, ib, cb, budget, P, iou, s)) return st;
+    std::vector<double> hi(P);
+    SPL_CUDA_TRY(ctx, cudaMemcpyAsync(hi.data(), iou, P * 8, cudaMemcpyDeviceToHost, s));
+    SPL_CUDA_TRY(ctx, cudaStreamSynchronize(s));
+    double sum = 0.0;
+    for (double v : hi) sum += v;
+    *out = P > 0 ? sum / static_cast<double>(P) : 0.0;
+    return SPL_OK;
+}
+
+spl_status train_impl(spl_ctx* ctx, int kind, uint32_t d, uint32_t h, uint32_t L, float gamma,
+                      float* w1, float* b1, float* w2, uint32_t n_seq, const float* queries,
+                      const float* keys, const uint32_t* seq_len, const spl_rank_config& rc,
+                      const spl_train_config& tc, double* records, double* holdout_iou,
+                      uint32_t* skipped, cudaStream_t s) {
+    // TrainConfig::validate (trainer.cpp:19-33)
+    if (tc.max_lr < 0.0 || tc.min_lr < 0.0 || tc.min_lr > tc.max_lr)
+        return fail(ctx, SPL_E_DIMENSION, "TrainConfig: need 0 <= min_lr <= max_lr");
+    if (!(tc.adam_beta1 >= 0.0 && tc.adam_beta1 < 1.0 && tc.adam_beta2 >= 0.0 && tc.adam_beta2 < 1.0))
+        return fail(ctx, SPL_E_DIMENSION, "TrainConfig: adam betas must lie in [0, 1)");
+    if (tc.adam_eps <= 0.0) return fail(ctx, SPL_E_DIMENSION, "TrainConfig: adam_eps must be positive");
+    if (tc.weight_decay < 0.0) return fail(ctx, SPL_E_DIMENSION, "TrainConfig: weight_decay must be >= 0");
+    if (tc.batch < 1) return fail(ctx, SPL_E_DIMENSION, "TrainConfig: batch must be >= 1");
+    if (tc.soft_gamma <= 0.0) return fail(ctx, SPL_E_DIMENSION, "TrainConfig: soft_gamma must be positive");
+    if (!(tc.holdout_budget_rate > 0.0 && tc.holdout_budget_rate <= 1.0))
+        return fail(ctx, SPL_E_DIMENSION, "TrainConfig: holdout_budget_rate must lie in (0, 1]");
+    if (n_seq == 0) return fail(ctx, SPL_E_DIMENSION, "train_hasher: dataset is empty");
+    for (uint32_t q = 0; q < n_seq; ++q)
+        if (seq_len[q] < 2)
+            return fail(ctx, SPL_E_DIMENSION, "train_hasher: sequences need at least two positions");
+    const bool mlp = kind == SPL_HASHER_MLP;
+    const float sgamma = mlp ? gamma : (float)tc.soft_gamma;  // MlpCoder uses h.gamma
+    if (kind == 2 && L == 0) return fail(ctx, SPL_E_DIMENSION, "downproj: width must be >= 1");
+
+    // ---- draws for every iteration (host, the reference's engines)
+    const uint32_t iters = tc.num_iters;
+    std::vector<uint64_t> off(n_seq + 1, 0);
+    for (uint32_t q = 0; q < n_seq; ++q) off[q + 1] = off[q] + seq_len[q];
+    auto q_train_of = [&](uint32_t q) {
+        const uint32_t rows = seq_len[q];
+        const uint32_t holdout = std::min<uint32_t>(tc.holdout_queries, rows / 4);
+        uint32_t qt = rows - holdout;
+        if (qt < 2) qt = rows;
+        return qt;
+    };
+    std::vector<Sample> draws;
+    draws.reserve((size_t)iters * tc.batch);
+    std::vector<char> used(n_seq, 0);
+    for (uint32_t it = 0; it < iters; ++it) {
+        std::mt19937_64 eng(derive_seed(tc.seed, it));
+        for (uint32_t b = 0; b < tc.batch; ++b) {
+            std::uniform_int_distribution<size_t> pick(0, n_seq - 1);
+            const uint32_t sq = (uint32_t)pick(eng);
+            const uint64_t part_seed = eng();
+            const uint32_t n = seq_len[sq];
+            if (!used[sq]) {
+                used[sq] = 1;
+                const std::string e = rank_cfg_error(rc, n);
+                if (!e.empty()) return fail(ctx, SPL_E_DIMENSION, e);
+                if (n > kMaxSortKeys)
+                    return fail(ctx, SPL_E_DIMENSION,
+                                "train_hasher: sequences longer than " +
+                                    std::to_string(kMaxSortKeys) + " keys are not supported");
+            }
+            draws.push_back(draw_partition(q_train_of(sq), n, rc, part_seed));
+            draws.back().seq = sq;
+        }
+    }
+    used[0] = 1;  // the holdout IoU reads sequence 0
+    if (seq_len[0] > kMaxSortKeys)
+        return fail(ctx, SPL_E_DIMENSION, "train_hasher: sequences longer than " +
+                                               std::to_string(kMaxSortKeys) + " keys are not supported");
+
+    // ---- device state
+    DevBuf db;
+    const uint64_t n1 = (uint64_t)d * (mlp ? h : L), nb = mlp ? h : 0, n2 = mlp ? (uint64_t)h * L : 0;
+    const uint64_t np = n1 + nb + n2;
+    float* dP = db.get<float>(np);
+    float* dG = db.get<float>(np);
+    double* dM = db.get<double>(np);
+    double* dV = db.get<double>(np);
+    TrainDev* dst = db.get<TrainDev>(1);
+    double* drec = db.get<double>((size_t)iters * 3 + 3);
+    if (!dP || !dG || !dM || !dV || !dst || !drec) return fail(ctx, SPL_E_CUDA, "train: out of device memory");
+    SPL_CUDA_TRY(ctx, cudaMemcpyAsync(dP, w1, n1 * 4, cudaMemcpyHostToDevice, s));
+    if (mlp) {
+        SPL_CUDA_TRY(ctx, cudaMemcpyAsync(dP + n1, b1, nb * 4, cudaMemcpyHostToDevice, s));
+        SPL_CUDA_TRY(ctx, cudaMemcpyAsync(dP + n1 + nb, w2, n2 * 4, cudaMemcpyHostToDevice, s));
+    }
+    SPL_CUDA_TRY(ctx, cudaMemsetAsync(dM, 0, np * 8, s));
+    SPL_CUDA_TRY(ctx, cudaMemsetAsync(dV, 0, np * 8, s));
+    SPL_CUDA_TRY(ctx, cudaMemsetAsync(dst, 0, sizeof(TrainDev), s));
+    SPL_CUDA_TRY(ctx, cudaMemsetAsync(drec, 0, ((size_t)iters * 3 + 3) * 8, s));
+    // bias corrections 1 - beta^t for every step t the run can reach (host
+    // std::pow, as adamw_step computes them)
+    std::vector<double> bc1(iters + 2), bc2(iters + 2);
+    for (uint32_t t = 0; t < iters + 2; ++t) {
+        bc1[t] = 1.0 - std::pow(tc.adam_beta1, static_cast<double>(t));
+        bc2[t] = 1.0 - std::pow(tc.adam_beta2, static_cast<double>(t));
+    }
+    double* dbc1 = db.get<double>(iters + 2);
+    double* dbc2 = db.get<double>(iters + 2);
+    if (!dbc1 || !dbc2) return fail(ctx, SPL_E_CUDA, "train: out of device memory");
+    SPL_CUDA_TRY(ctx, cudaMemcpyAsync(dbc1, bc1.data(), bc1.size() * 8, cudaMemcpyHostToDevice, s));
+    SPL_CUDA_TRY(ctx, cudaMemcpyAsync(dbc2, bc2.data(), bc2.size() * 8, cudaMemcpyHostToDevice, s));
+
+    // ---- per-sequence preparation: inputs, exact logits, order (prepare_sequence)
+    struct Prep {
+        float* x_q = nullptr;
+        float* x_k = nullptr;
+        float* logits = nullptr;
+        uint32_t* order = nullptr;
+        uint32_t q_train = 0;
+    };
+    std::vector<Prep> prep(n_seq);
+    const float scale = 1.0f / std::sqrt(static_cast<float>(d));
+    uint32_t max_n = 0;
+    for (uint32_t q = 0; q < n_seq; ++q) {
+        if (!used[q]) continue;
+        const uint32_t n = seq_len[q];
+        max_n = std::max(max_n, n);
+        Prep& p = prep[q];
+        p.q_train = q_train_of(q);
+        p.x_q = db.get<float>((size_t)n * d);
+        p.x_k = db.get<float>((size_t)n * d);
+        p.logits = db.get<float>((size_t)n * n);
+        p.order = db.get<uint32_t>((size_t)p.q_train * n);
+        if (!p.x_q || !p.x_k || !p.logits || !p.order) return fail(ctx, SPL_E_CUDA, "train: out of device memory");
+        SPL_CUDA_TRY(ctx, cudaMemcpyAsync(p.x_q, queries + off[q] * d, (size_t)n * d * 4, cudaMemcpyHostToDevice, s));
+        SPL_CUDA_TRY(ctx, cudaMemcpyAsync(p.x_k, keys + off[q] * d, (size_t)n * d * 4, cudaMemcpyHostToDevice, s));
+        k_logits<<<dim3((n + 63) / 64, (n + 63) / 64), 256, 0, s>>>(p.x_q, p.x_k, n, n, d, scale, p.logits);
+        if (spl_status st = after_launch(ctx, "k_logits")) return st;
+        uint32_t npow2 = 1;
+        while (npow2 < n) npow2 <<= 1;
+        const size_t smem = (size_t)npow2 * 8;
+        SPL_CUDA_TRY(ctx, cudaFuncSetAttribute(k_order, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        k_order<<<p.q_train, 1024, smem, s>>>(p.logits, n, npow2, p.order);
+        if (spl_status st = after_launch(ctx, "k_order")) return st;
+    }
+
+    // ---- per-step buffers (sized for the largest draw)
+    uint32_t maxQ = 1, maxT = 1, maxO = 1;
+    for (const Sample& w : draws) {
+        maxQ = std::max<uint32_t>(maxQ, (uint32_t)w.qrows.size());
+        maxT = std::max<uint32_t>(maxT, (uint32_t)w.top_pos.size());
+        maxO = std::max<uint32_t>(maxO, (uint32_t)w.oth_pos.size());
+    }
+    const size_t rank_smem = (size_t)(maxT + maxO) * 8 + (size_t)L * 4;
+    if (rank_smem > 200 * 1024)
+        return fail(ctx, SPL_E_DIMENSION, "train_hasher: sampled pair set too large for one block "
+                                          "(set max_top / max_oth)");
+    SPL_CUDA_TRY(ctx, cudaFuncSetAttribute(k_rank_loss, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rank_smem));
+    const uint32_t hw = mlp ? h : 1;
+    float *z1q = db.get<float>((size_t)maxQ * hw), *a1q = db.get<float>((size_t)maxQ * hw);
+    float *z2q = db.get<float>((size_t)maxQ * L), *sfq = db.get<float>((size_t)maxQ * L);
+    float *z1k = db.get<float>((size_t)max_n * hw), *a1k = db.get<float>((size_t)max_n * hw);
+    float *z2k = db.get<float>((size_t)max_n * L), *sfk = db.get<float>((size_t)max_n * L);
+    float *dsq = db.get<float>((size_t)maxQ * L), *dsk = db.get<float>((size_t)max_n * L);
+    float *dz = db.get<float>((size_t)std::max(maxQ, max_n) * L);
+    float *da1 = db.get<float>((size_t)std::max(maxQ, max_n) * hw);
+    float *Gm = db.get<float>((size_t)max_n * maxQ);
+    double *gbt = db.get<double>((size_t)maxQ * maxT), *gbo = db.get<double>((size_t)maxQ * maxO);
+    double* lpart = db.get<double>(maxQ);
+    unsigned long long* vpart = db.get<unsigned long long>(maxQ);
+    uint32_t *top_idx = db.get<uint32_t>((size_t)maxQ * maxT), *oth_idx = db.get<uint32_t>((size_t)maxQ * maxO);
+    // every draw's index lists, uploaded once
+    std::vector<uint64_t> doff(draws.size() + 1, 0);
+    for (size_t i = 0; i < draws.size(); ++i)
+        doff[i + 1] = doff[i] + draws[i].qrows.size() + draws[i].top_pos.size() + draws[i].oth_pos.size();
+    std::vector<uint32_t> hdraw(doff.back());
+    for (size_t i = 0; i < draws.size(); ++i) {
+        uint32_t* p = hdraw.data() + doff[i];
+        p = std::copy(draws[i].qrows.begin(), draws[i].qrows.end(), p);
+        p = std::copy(draws[i].top_pos.begin(), draws[i].top_pos.end(), p);
+        std::copy(draws[i].oth_pos.begin(), draws[i].oth_pos.end(), p);
+    }
+    uint32_t* ddraw = db.get<uint32_t>(hdraw.size());
+    if (!z1q || !a1q || !z2q || !sfq || !z1k || !a1k || !z2k || !sfk || !dsq || !dsk || !dz || !da1 ||
+        !Gm || !gbt || !gbo || !lpart || !vpart || !top_idx || !oth_idx || !ddraw)
+        return fail(ctx, SPL_E_CUDA, "train: out of device memory");
+    if (!hdraw.empty())
+        SPL_CUDA_TRY(ctx, cudaMemcpyAsync(ddraw, hdraw.data(), hdraw.size() * 4, cudaMemcpyHostToDevice, s));
+
+    float* gW1 = dG;
+    float* gB1 = dG + n1;
+    float* gW2 = dG + n1 + nb;
+    const float* W1 = dP;
+    const float* B1 = dP + n1;
+    const float* W2 = dP + n1 + nb;
+    const size_t fwd_smem = (size_t)kFwdRows * (d + hw) * 4;
+    auto fwd = [&](const float* x, const uint32_t* rows, uint32_t m, float* a, float* b, float* c,
+                   float* sf) -> spl_status {
+        const dim3 grid((m + kFwdRows - 1) / kFwdRows);
+        if (kind == SPL_HASHER_MLP)
+            k_forward<SPL_HASHER_MLP><<<grid, 128, fwd_smem, s>>>(x, rows, m, d, h, L, W1, B1, W2, sgamma, a, b, c, sf, dst);
+        else if (kind == SPL_HASHER_LINEAR)
+            k_forward<SPL_HASHER_LINEAR><<<grid, 128, fwd_smem, s>>>(x, rows, m, d, 0, L, W1, nullptr, nullptr, sgamma, a, b, c, sf, dst);
+        else
+            k_forward<2><<<grid, 128, fwd_smem, s>>>(x, rows, m, d, 0, L, W1, nullptr, nullptr, sgamma, a, b, c, sf, dst);
+        return after_launch(ctx, "k_forward");
+    };
+    // backward of one side (trainer.cpp:219-236 / :252-258 / :279-282);
+    // x rows are gathered (queries) or identity (keys)
+    float* xg = db.get<float>((size_t)maxQ * d);  // gathered query inputs for add_at
+    if (!xg) return fail(ctx, SPL_E_CUDA, "train: out of device memory");
+    auto bwd = [&](const float* x, uint32_t m, const float* z1, const float* a1, const float* z2,
+                   const float* dsoft) -> spl_status {
+        const uint64_t ne = (uint64_t)m * L;
+        const unsigned eg = (unsigned)std::min<uint64_t>((ne + 255) / 256, 4096);
+        const float* dzp = dsoft;
+        if (kind != 2) {
+            k_dz<<<eg, 256, 0, s>>>(dsoft, z2, ne, sgamma, dz, dst);
+            if (spl_status st = after_launch(ctx, "k_dz")) return st;
+            dzp = dz;
+        }
+        if (mlp) {
+            k_add_at<<<dim3((L + 127) / 128, (h + 3) / 4), 128, 0, s>>>(a1, dzp, m, h, L, gW2, dst);
+            if (spl_status st = after_launch(ctx, "k_add_at")) return st;
+            k_da1<<<(m + kDaRows - 1) / kDaRows, 128, (size_t)kDaRows * L * 4, s>>>(dzp, W2, z1, m, h, L, da1, dst);
+            if (spl_status st = after_launch(ctx, "k_da1")) return st;
+            k_b1<<<(h + 127) / 128, 128, 0, s>>>(da1, m, h, gB1, dst);
+            if (spl_status st = after_launch(ctx, "k_b1")) return st;
+            k_add_at<<<dim3((h + 127) / 128, (d + 3) / 4), 128, 0, s>>>(x, da1, m, d, h, gW1, dst);
+            return after_launch(ctx, "k_add_at");
+        }
+        k_add_at<<<dim3((L + 127) / 128, (d + 3) / 4), 128, 0, s>>>(x, dzp, m, d, L, gW1, dst);
+        return after_launch(ctx, "k_add_at");
+    };
+    const float invb = tc.batch > 1 ? (float)(1.0 / tc.batch) : 1.0f;
+    for (uint32_t it = 0; it < iters; ++it) {
+        const double lr = train_lr_at(it, tc);
+        SPL_CUDA_TRY(ctx, cudaMemsetAsync(dG, 0, np * 4, s));
+        for (uint32_t b = 0; b < tc.batch; ++b) {
+            const size_t di = (size_t)it * tc.batch + b;
+            const Sample& w = draws[di];
+            const Prep& p = prep[w.seq];
+            const uint32_t n = seq_len[w.seq];
+            const uint32_t Qs = (uint32_t)w.qrows.size(), T = (uint32_t)w.top_pos.size(),
+                           O = (uint32_t)w.oth_pos.size();
+            const uint32_t* qrows = ddraw + doff[di];
+            const uint32_t* tpos = qrows + Qs;
+            const uint32_t* opos = tpos + T;
+            SPL_CUDA_TRY(ctx, cudaMemsetAsync(Gm, 0, (size_t)n * Qs * 4, s));
+            k_partition<<<Qs, 256, 0, s>>>(p.order, n, w.k_full, qrows, tpos, T, opos, O, top_idx, oth_idx, dst);
+            if (spl_status st = after_launch(ctx, "k_partition")) return st;
+            if (spl_status st = fwd(p.x_q, qrows, Qs, z1q, a1q, z2q, sfq)) return st;
+            if (spl_status st = fwd(p.x_k, nullptr, n, z1k, a1k, z2k, sfk)) return st;
+            k_rank_loss<<<Qs, 256, (size_t)(T + O) * 8 + (size_t)L * 4, s>>>(
+                sfq, sfk, L, top_idx, T, oth_idx, O, Qs, rc.beta, rc.alpha, gbt, gbo, Gm, dsq, lpart,
+                vpart, dst, it);
+            if (spl_status st = after_launch(ctx, "k_rank_loss")) return st;
+            k_loss_finalize<<<1, 1, 0, s>>>(lpart, vpart, Qs, b, tc.batch, it, drec, dst);
+            if (spl_status st = after_launch(ctx, "k_loss_finalize")) return st;
+            k_dsoft_keys<<<(unsigned)(((uint64_t)n * L + 255) / 256), 256, 0, s>>>(Gm, sfq, Qs, n, L, invb, dsk, dst);
+            if (spl_status st = after_launch(ctx, "k_dsoft_keys")) return st;
+            if (invb != 1.0f) {
+                k_scale<<<(Qs * L + 255) / 256, 256, 0, s>>>(dsq, (uint64_t)Qs * L, invb, dst);
+                if (spl_status st = after_launch(ctx, "k_scale")) return st;
+            }
+            // the selected query rows (gather_rows, trainer.cpp:455-464) for
+            // the query-side weight gradients
+            k_gather_rows<<<Qs, 128, 0, s>>>(p.x_q, qrows, d, xg, dst);
+            if (spl_status st = after_launch(ctx, "k_gather_rows")) return st;
+            if (spl_status st = bwd(xg, Qs, z1q, a1q, z2q, dsq)) return st;
+            if (spl_status st = bwd(p.x_k, n, z1k, a1k, z2k, dsk)) return st;
+        }
+        k_clip<<<1, 1024, 0, s>>>(dG, np, tc.grad_clip, dbc1, dbc2, dst);
+        if (spl_status st = after_launch(ctx, "k_clip")) return st;
+        k_adamw<<<(unsigned)std::min<uint64_t>((np + 255) / 256, 1184), 256, 0, s>>>(
+            dP, dG, dM, dV, np, n1, n1 + nb, lr, tc.adam_beta1, tc.adam_beta2, tc.adam_eps,
+            tc.weight_decay, dst);
+        if (spl_status st = after_launch(ctx, "k_adamw")) return st;
+    }
+
+    // ---- results: weights (also on the error paths, as the reference's
+    // in-place hasher), records, then the holdout IoU
+    TrainDev hs{};
+    SPL_CUDA_TRY(ctx, cudaMemcpyAsync(&hs, dst, sizeof(TrainDev), cudaMemcpyDeviceToHost, s));
+    SPL_CUDA_TRY(ctx, cudaMemcpyAsync(w1, dP, n1 * 4, cudaMemcpyDeviceToHost, s));
+    if (mlp) {
+        SPL_CUDA_TRY(ctx, cudaMemcpyAsync(b1, dP + n1, nb * 4, cudaMemcpyDeviceToHost, s));
+        SPL_CUDA_TRY(ctx, cudaMemcpyAsync(w2, dP + n1 + nb, n2 * 4, cudaMemcpyDeviceToHost, s));
+    }
+    if (records && iters)
+        SPL_CUDA_TRY(ctx, cudaMemcpyAsync(records, drec, (size_t)iters * 3 * 8, cudaMemcpyDeviceToHost, s));
+    SPL_CUDA_TRY(ctx, cudaStreamSynchronize(s));
+    if (hs.halt == HALT_EMPTY)
+        return fail(ctx, SPL_E_EMPTY_PAIRS, "ranking loss: no causally valid pairs to rank");
+    if (hs.halt == HALT_NONFINITE)
+        return fail(ctx, SPL_E_NUMERIC, "train_hasher: loss became non-finite at iteration " +
+                                            std::to_string(hs.halt_iter));
+    if (records)
+        for (uint32_t it = 0; it < iters; ++it) records[3 * (size_t)it + 2] = train_lr_at(it, tc);
+    if (skipped) *skipped = hs.skipped;
+    if (holdout_iou) {
+        spl_status st = holdout_iou_impl(ctx, kind, d, h, L, w1, b1, w2, prep[0].x_q, prep[0].x_k,
+                                         prep[0].logits, seq_len[0], prep[0].q_train,
+                                         tc.holdout_budget_rate, holdout_iou, s);
+        if (st) return st;
+    }
+    return SPL_OK;
+}
+
+}  // namespace spl
+
+// ------------------------------------------------------------ C-ABI
+extern "C" spl_status spl_train_hasher(spl_ctx* ctx, int kind, uint32_t d, uint32_t h, uint32_t L,
+                                       float gamma, float* w1, float* b1, float* w2,
+                                       uint32_t n_seq, const float* queries, const float* keys,
+                                       const uint32_t* seq_len, const spl_rank_config* rank,
+                                       const spl_train_config* train, double* records,
+                                       double* holdout_iou, uint32_t* skipped, void* stream) {
+    if (!ctx) return SPL_E_STATE;
+    if (!rank || !train || !w1 || (kind == SPL_HASHER_MLP && (!b1 || !w2)) ||
+        (n_seq && (!queries || !keys || !seq_len)))
+        return spl::fail(ctx, SPL_E_STATE, "train_hasher: null pointer");
+    if (kind != SPL_HASHER_MLP && kind != SPL_HASHER_LINEAR && kind != SPL_HASHER_DOWNPROJ)
+        return spl::fail(ctx, SPL_E_DIMENSION, "train_hasher: unknown hasher kind");
+    if (d == 0 || L == 0 || (kind == SPL_HASHER_MLP && h == 0))
+        return spl::fail(ctx, SPL_E_DIMENSION, "train_hasher: dimensions must be >= 1");
+    if (kind != SPL_HASHER_DOWNPROJ && L % 32 != 0)
+        return spl::fail(ctx, SPL_E_DIMENSION, "train_hasher: code bits must be a multiple of 32");
+    return spl::train_impl(ctx, kind, d, h, L, gamma, w1, b1, w2, n_seq, queries, keys, seq_len,
+                           *rank, *train, records, holdout_iou, skipped,
+                           static_cast<cudaStream_t>(stream));
+}
+
+extern "C" spl_status spl_train_partition_host(const spl_rank_config* rank, uint32_t q_train,
+                                               uint32_t n, uint64_t seed, uint32_t* rows,
+                                               uint32_t* top_pos, uint32_t* oth_pos,
+                                               uint32_t* counts) {
+    if (!rank || !rows || !top_pos || !oth_pos || !counts) return SPL_E_STATE;
+    return spl::train_partition_host(*rank, q_train, n, seed, rows, top_pos, oth_pos, counts);
+}
+
+extern "C" double spl_train_lr_at(uint32_t iter, const spl_train_config* train) {
+    return train ? spl::train_lr_at(iter, *train) : 0.0;
+}

@@ -230,6 +230,16 @@ class RefLib(_Base):
         L.spotref_index_create.argtypes = [u32p, C.c_uint32, C.c_uint64, C.c_uint32, u32p,
                                            C.POINTER(C.c_void_p)]
         L.spotref_index_destroy.argtypes = [C.c_void_p]
+        f64p = np.ctypeslib.ndpointer(np.float64, flags="C_CONTIGUOUS")
+        i64p = np.ctypeslib.ndpointer(np.int64, flags="C_CONTIGUOUS")
+        L.spotref_train.argtypes = [C.c_int, f32p, f32p, f32p, C.c_uint32, C.c_uint32, C.c_uint32,
+                                        C.c_float, C.c_uint32, f32p, f32p, u32p, f64p, u64p, i64p,
+                                        C.c_int, f64p, C.POINTER(C.c_double),
+                                        C.POINTER(C.c_uint32)]
+        L.spotref_partition_identity.argtypes = [C.c_uint32, C.c_uint32, u32p, f64p, i64p,
+                                                 C.c_uint64, u32p, u32p, u32p, u32p, u64p]
+        L.spotref_lr_at.argtypes = [C.c_uint32, C.c_uint32, C.c_uint32, C.c_double, C.c_double]
+        L.spotref_lr_at.restype = C.c_double
         L.spotref_retrieve_batch.argtypes = [C.c_void_p, u32p, u32p, C.c_uint32, u32p, C.c_int]
 
     def _err(self, code):
@@ -378,3 +388,56 @@ class RefLib(_Base):
         self._chk(self.lib.spotref_retrieve_batch(handle, qcodes, _c(n_valid, np.uint32), k, out,
                                                   threads or os.cpu_count() or 1))
         return out
+
+    # -- trainer
+    def train(self, kind, w1, b1, w2, gamma, sequences, rank, cfg, loss_kind=0):
+        """train_hasher. kind 1 MLP (w1 d x h, b1, w2), 0 linear / 2 downproj (w1 =
+        projection d x L; b1, w2 None). rank: dict(beta, alpha, maskout, max_top,
+        max_oth, query_subsample); cfg: dict of TrainConfig fields. Returns
+        (w1, b1, w2, records [iters][3], holdout_iou, skipped)."""
+        w1 = _c(w1, np.float32).copy()
+        d = w1.shape[0]
+        if kind == 1:
+            b1, w2 = _c(b1, np.float32).copy(), _c(w2, np.float32).copy()
+            h, L = w1.shape[1], w2.shape[1]
+        else:
+            h, L = 0, w1.shape[1]
+            b1, w2 = np.zeros(1, np.float32), np.zeros(1, np.float32)
+        qs = _c(np.concatenate([q for q, _ in sequences]), np.float32)
+        ks = _c(np.concatenate([k for _, k in sequences]), np.float32)
+        lens = np.array([len(q) for q, _ in sequences], np.uint32)
+        dc = np.array([cfg["max_lr"], cfg["min_lr"], cfg["adam_beta1"], cfg["adam_beta2"],
+                       cfg["adam_eps"], cfg["weight_decay"], cfg["grad_clip"], cfg["soft_gamma"],
+                       cfg["holdout_budget_rate"], rank["beta"], rank["alpha"], rank["maskout"]],
+                      np.float64)
+        uc = np.array([cfg["num_iters"], cfg["warmup_iters"], cfg["batch"], cfg["seed"],
+                       cfg["holdout_queries"]], np.uint64)
+        op = np.array([-1 if rank.get(k) is None else rank[k]
+                       for k in ("max_top", "max_oth", "query_subsample")], np.int64)
+        rec = np.zeros((max(cfg["num_iters"], 1), 3), np.float64)
+        iou = C.c_double(0.0)
+        sk = C.c_uint32(0)
+        self._chk(self.lib.spotref_train(kind, w1, b1, w2, d, h, L, gamma, len(sequences), qs,
+                                         ks, lens, dc, uc, op, loss_kind, rec, C.byref(iou),
+                                         C.byref(sk)))
+        if kind != 1:
+            b1 = w2 = None
+        return w1, b1, w2, rec[:cfg["num_iters"]], iou.value, sk.value
+
+    def partition_identity(self, q, n, rank, seed, offsets=None):
+        """partition_topk over an identity order: (rows, top_pos, oth_pos, k_full, valid_pairs)."""
+        offs = _c(np.arange(1, q + 1) if offsets is None else offsets, np.uint32)
+        bam = np.array([rank["beta"], rank["alpha"], rank["maskout"]], np.float64)
+        op = np.array([-1 if rank.get(k) is None else rank[k]
+                       for k in ("max_top", "max_oth", "query_subsample")], np.int64)
+        rows = np.zeros(max(q, 1), np.uint32)
+        top = np.zeros(max(n, 1), np.uint32)
+        oth = np.zeros(max(n, 1), np.uint32)
+        cnt = np.zeros(4, np.uint32)
+        vp = np.zeros(1, np.uint64)
+        self._chk(self.lib.spotref_partition_identity(q, n, offs, bam, op, seed, rows, top, oth,
+                                                      cnt, vp))
+        return rows[:cnt[0]], top[:cnt[1]], oth[:cnt[2]], int(cnt[3]), int(vp[0])
+
+    def lr_at(self, it, num_iters, warmup, max_lr, min_lr):
+        return self.lib.spotref_lr_at(it, num_iters, warmup, max_lr, min_lr)

@@ -1,0 +1,153 @@
+"""GPU hasher training against the unmodified reference's
+train_hasher (trainer.cpp:634-645), same hasher, data, configs and seeds.
+
+What is compared, and how tightly:
+  * learning rates: exact;
+  * per-iteration loss: rel 1e-10 (the reference sums pair losses
+    sequentially, the GPU per query then in query order);
+  * violation rates: exact while the weights agree;
+  * weights after training: max abs difference reported; bound 1e-6 x the
+    weight scale (every per-output arithmetic chain follows the reference's
+    order; the only sources of difference are CUDA vs glibc double exp /
+    log1p (<= 2 ulp, rounded to float before use) and the clipping norm's
+    summation order);
+  * holdout IoU: exact when the final weights are bit-identical.
+"""
+import numpy as np
+import pytest
+
+from oracle_lib import RefLib
+from paper_2508_19740_b200 import capi
+
+pytestmark = [pytest.mark.gpu,
+              pytest.mark.skipif(not RefLib.available(), reason="oracle/_ref not built")]
+
+CFG = dict(num_iters=6, warmup_iters=2, batch=1, seed=7, holdout_queries=32, max_lr=1e-3,
+           min_lr=0.0, adam_beta1=0.9, adam_beta2=0.98, adam_eps=1e-8, weight_decay=0.1,
+           grad_clip=1.0, soft_gamma=64.0, holdout_budget_rate=0.02)
+RANK = dict(beta=1.0, alpha=3.0, maskout=0.98, max_top=None, max_oth=256, query_subsample=64)
+
+
+def seqs(seed, lens, d):
+    rng = np.random.default_rng(seed)
+    return [(rng.standard_normal((n, d)).astype(np.float32),
+             rng.standard_normal((n, d)).astype(np.float32)) for n in lens]
+
+
+def run_pair(ctx, kind, weights, data, rank, cfg, gamma=64.0):
+    ref = RefLib()
+    w1, b1, w2 = weights
+    r = ref.train(kind, w1, b1, w2, gamma, data, rank, cfg)
+    g1 = w1.copy()
+    gb = None if b1 is None else b1.copy()
+    g2 = None if w2 is None else w2.copy()
+    d = w1.shape[0]
+    h = w1.shape[1] if kind == 1 else 0
+    L = w2.shape[1] if kind == 1 else w1.shape[1]
+    out = ctx.train_hasher(kind, d, h, L, gamma, g1, gb, g2, data,
+                           capi.RankConfig(**rank), capi.TrainConfig(**cfg))
+    return r, (g1, gb, g2, out)
+
+
+def compare(r, g, tag):
+    rw1, rb1, rw2, rrec, riou, rsk = r
+    g1, gb, g2, out = g
+    rec = out["records"]
+    np.testing.assert_array_equal(rec[:, 2], rrec[:, 2])
+    np.testing.assert_allclose(rec[:, 0], rrec[:, 0], rtol=1e-10, atol=0)
+    ident = True
+    worst = 0.0
+    for a, b in ((g1, rw1), (gb, rb1), (g2, rw2)):
+        if a is None:
+            continue
+        ident &= bool(np.array_equal(a, b))
+        worst = max(worst, float(np.max(np.abs(a.astype(np.float64) - b))))
+        scale = float(np.max(np.abs(b))) + 1e-30
+        assert worst <= 1e-6 * scale, f"{tag}: weights differ by {worst} (scale {scale})"
+    if ident:
+        np.testing.assert_array_equal(rec[:, 1], rrec[:, 1])
+        assert out["holdout_iou"] == riou
+    assert out["skipped_steps"] == rsk
+    print(f"{tag}: weights bit-identical={ident} max|dw|={worst:.3g} "
+          f"loss0={rec[0, 0]:.9g} iou={out['holdout_iou']:.4f} (ref {riou:.4f})")
+    return ident
+
+
+def test_train_mlp_matches_reference(ctx):
+    ref = RefLib()
+    w = ref.mlp_gaussian_init(128, 128, 128, 64.0, ref.derive_seed(0, 100))
+    data = seqs(1, [384], 128)
+    r, g = run_pair(ctx, 1, w, data, RANK, CFG)
+    compare(r, g, "mlp 384")
+
+
+def test_train_mlp_batch_multi_sequence(ctx):
+    ref = RefLib()
+    w = ref.mlp_gaussian_init(64, 96, 64, 64.0, 5)
+    data = seqs(2, [200, 301, 150], 64)
+    cfg = dict(CFG, batch=3, num_iters=4, seed=11)
+    rank = dict(RANK, max_top=4, max_oth=40, query_subsample=17)
+    r, g = run_pair(ctx, 1, w, data, rank, cfg)
+    compare(r, g, "mlp batch3")
+
+
+def test_train_linear_and_downproj(ctx):
+    rng = np.random.default_rng(3)
+    data = seqs(4, [256], 64)
+    p = (rng.standard_normal((64, 64)) / 8).astype(np.float32)
+    r, g = run_pair(ctx, 0, (p, None, None), data, RANK, CFG)
+    compare(r, g, "linear")
+    p2 = (rng.standard_normal((64, 8)) / 8).astype(np.float32)
+    r, g = run_pair(ctx, 2, (p2, None, None), data, dict(RANK, max_oth=None), CFG)
+    compare(r, g, "downproj")
+
+
+def test_zero_lr_leaves_weights_identical(ctx):
+    ref = RefLib()
+    w = ref.mlp_gaussian_init(32, 32, 32, 64.0, 9)
+    data = seqs(5, [100], 32)
+    cfg = dict(CFG, max_lr=0.0, num_iters=3)
+    r, g = run_pair(ctx, 1, w, data, RANK, cfg)
+    for a, b in zip(g[:3], w):
+        np.testing.assert_array_equal(a, b)
+    compare(r, g, "zero lr")
+
+
+def test_empty_pair_set_is_rejected(ctx):
+    # two positions, maskout 0.5: row 0 has one valid key (no pair), row 1 one
+    # pair; a draw of query row 0 alone is the reference's EmptyPairError.
+    # Find a seed whose first draw is row 0 by asking the reference itself.
+    from oracle_lib import CheckerError
+
+    rank = dict(RANK, maskout=0.5, max_oth=None, query_subsample=1)
+    ref = RefLib()
+    w = ref.mlp_gaussian_init(32, 32, 32, 64.0, 1)
+    data = seqs(6, [2], 32)
+    seed = None
+    for sd in range(64):
+        cfg = dict(CFG, seed=sd, num_iters=1, holdout_queries=0)
+        try:
+            ref.train(1, *w, 64.0, data, rank, cfg)
+        except CheckerError as e:
+            assert e.code == 5
+            seed = sd
+            break
+    assert seed is not None
+    cfg = dict(CFG, seed=seed, num_iters=1, holdout_queries=0)
+    with pytest.raises(capi.EmptyPairError):
+        ctx.train_hasher(1, 32, 32, 32, 64.0, *(a.copy() for a in w), data,
+                         capi.RankConfig(**rank), capi.TrainConfig(**cfg))
+    # a seed whose draw has a pair trains normally on both sides
+    ok = next(sd for sd in range(64) if sd != seed and _ref_ok(ref, w, data, rank, sd))
+    r, g = run_pair(ctx, 1, w, data, rank, dict(CFG, seed=ok, num_iters=1, holdout_queries=0))
+    compare(r, g, "two positions")
+
+
+def _ref_ok(ref, w, data, rank, sd):
+    from oracle_lib import CheckerError
+
+    try:
+        ref.train(1, *w, 64.0, data, rank, dict(CFG, seed=sd, num_iters=1, holdout_queries=0))
+        return True
+    except CheckerError:
+        return False
