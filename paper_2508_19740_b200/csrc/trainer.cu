@@ -39,6 +39,8 @@
 #include <stdint.h>
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
 #include <cmath>
 #include <cstdlib>
 #include <numeric>
@@ -232,7 +234,17 @@ __global__ void __launch_bounds__(128) k_forward(const float* __restrict__ x, co
             float acc[kFwdRows];
 #pragma unroll
             for (int r = 0; r < kFwdRows; ++r) acc[r] = 0.0f;
-            for (uint32_t p = 0; p < d; ++p) {
+            uint32_t p = 0;
+            for (; p + 8 <= d; p += 8) {  // loads of 8 weights ahead of their chains
+                float w[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) w[u] = __ldg(w1 + (uint64_t)(p + u) * h + j);
+#pragma unroll
+                for (int u = 0; u < 8; ++u)
+#pragma unroll
+                    for (int r = 0; r < kFwdRows; ++r) acc[r] = __fmaf_rn(xs[r * d + p + u], w[u], acc[r]);
+            }
+            for (; p < d; ++p) {
                 const float w = w1[(uint64_t)p * h + j];
 #pragma unroll
                 for (int r = 0; r < kFwdRows; ++r) acc[r] = __fmaf_rn(xs[r * d + p], w, acc[r]);
@@ -258,7 +270,17 @@ __global__ void __launch_bounds__(128) k_forward(const float* __restrict__ x, co
         float acc[kFwdRows];
 #pragma unroll
         for (int r = 0; r < kFwdRows; ++r) acc[r] = 0.0f;
-        for (uint32_t p = 0; p < K; ++p) {
+        uint32_t p = 0;
+        for (; p + 8 <= K; p += 8) {
+            float w[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) w[u] = __ldg(W + (uint64_t)(p + u) * L + j);
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+#pragma unroll
+                for (int r = 0; r < kFwdRows; ++r) acc[r] = __fmaf_rn(in[r * K + p + u], w[u], acc[r]);
+        }
+        for (; p < K; ++p) {
             const float w = W[(uint64_t)p * L + j];
 #pragma unroll
             for (int r = 0; r < kFwdRows; ++r) acc[r] = __fmaf_rn(in[r * K + p], w, acc[r]);
@@ -323,83 +345,85 @@ __global__ void __launch_bounds__(256) k_partition(const uint32_t* __restrict__ 
 }
 
 // ------------------------------------------------------------ ranking loss
-// ranking_soft_loss (trainer.cpp:299-380) for one selected query per block:
-// B_i = <sq, sk_top_i>, C_j = <sq, sk_oth_j> in double; per valid pair
-// softplus(-(beta (B_i - C_j) - alpha)), violations, and the pair gradient
-// g; gb[i] = -sum_j g (j ascending), gc[j] = sum_i g (i ascending); then
-// dq = fma chain over the top entries then the other entries, and the g
-// values of every touched key go to G[key][qi] for the key-side chain.
-__global__ void __launch_bounds__(256) k_rank_loss(const float* __restrict__ softq,
+// ranking_soft_loss (trainer.cpp:299-380), three kernels:
+//  k_rank_dots   B_i = <sq, sk_top_i>, C_j = <sq, sk_oth_j> in double, one
+//                thread per entry (products of floats are exact in double:
+//                only the sequential add order matters);
+//  k_rank_pairs  one thread per (i, j) pair: softplus(-(beta (B_i - C_j) -
+//                alpha)), the violation flag and the pair gradient g, stored
+//                as gp[qi][i][j] (invalid pairs: 0); loss / violation partial
+//                per block;
+//  k_rank_grad   gb[i] = -sum_j g (j ascending), gc[j] = sum_i g (i
+//                ascending) — the reference's accumulation orders — then dq
+//                = one fma chain over the non-zero entries (top first, then
+//                other), and the g values of the touched keys into G[key][qi]
+//                for the key-side chain.
+__global__ void __launch_bounds__(128) k_rank_dots(const float* __restrict__ softq,
                                                    const float* __restrict__ softk, uint32_t L,
                                                    const uint32_t* top_idx, uint32_t T,
                                                    const uint32_t* oth_idx, uint32_t O,
-                                                   uint32_t Qs, double beta, double alpha,
-                                                   double* gbuf_t, double* gbuf_o, float* G,
-                                                   float* dsq, double* loss_part,
-                                                   unsigned long long* viol_part, TrainDev* st,
-                                                   uint32_t iter) {
+                                                   double* bc, TrainDev* st, uint32_t iter) {
     if (st->halt) return;
-    const unsigned long long vp = st->pairs;
-    if (vp == 0) {  // EmptyPairError (trainer.cpp:303-305)
-        if (blockIdx.x == 0 && threadIdx.x == 0) {
+    if (st->pairs == 0) {  // EmptyPairError (trainer.cpp:303-305)
+        if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) {
             st->halt = HALT_EMPTY;
             st->halt_iter = iter;
         }
         return;
     }
-    const double inv = __ddiv_rn(1.0, (double)vp);
-    extern __shared__ double dsm[];
-    double* bv = dsm;           // [T]
-    double* cv = dsm + T;       // [O]
-    float* sq = reinterpret_cast<float*>(dsm + T + O);  // [L]
-    __shared__ double s_loss[8];
-    __shared__ unsigned long long s_viol[8];
+    extern __shared__ float sq[];  // [L]
     const uint32_t qi = blockIdx.x;
-    const uint32_t* ti = top_idx + (uint64_t)qi * T;
-    const uint32_t* oi = oth_idx + (uint64_t)qi * O;
     for (uint32_t p = threadIdx.x; p < L; p += blockDim.x) sq[p] = softq[(uint64_t)qi * L + p];
     __syncthreads();
-    for (uint32_t e = threadIdx.x; e < T + O; e += blockDim.x) {
-        const uint32_t key = e < T ? ti[e] : oi[e - T];
-        double acc = 0.0;
-        if (key != ~0u) {
-            const float* sk = softk + (uint64_t)key * L;
-            for (uint32_t p = 0; p < L; ++p)
-                acc = __dadd_rn(acc, __dmul_rn((double)sq[p], (double)sk[p]));
+    const uint32_t e = blockIdx.y * blockDim.x + threadIdx.x;
+    if (e >= T + O) return;
+    const uint32_t key = e < T ? top_idx[(uint64_t)qi * T + e] : oth_idx[(uint64_t)qi * O + e - T];
+    double acc = 0.0;
+    if (key != ~0u) {
+        const float* sk = softk + (uint64_t)key * L;
+        uint32_t p = 0;
+        for (; p + 8 <= L; p += 8) {
+            float v[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) v[u] = __ldg(sk + p + u);
+#pragma unroll
+            for (int u = 0; u < 8; ++u) acc = __dadd_rn(acc, __dmul_rn((double)sq[p + u], (double)v[u]));
         }
-        if (e < T) bv[e] = acc; else cv[e - T] = acc;
+        for (; p < L; ++p) acc = __dadd_rn(acc, __dmul_rn((double)sq[p], (double)sk[p]));
     }
-    __syncthreads();
+    bc[(uint64_t)qi * (T + O) + e] = acc;
+}
+
+constexpr int kPairThreads = 256;
+__global__ void __launch_bounds__(kPairThreads) k_rank_pairs(const double* __restrict__ bc,
+                                                             const uint32_t* top_idx, uint32_t T,
+                                                             const uint32_t* oth_idx, uint32_t O,
+                                                             double beta, double alpha,
+                                                             double* __restrict__ gp,
+                                                             double* loss_part,
+                                                             unsigned long long* viol_part,
+                                                             const TrainDev* st) {
+    if (st->halt) return;
+    __shared__ double s_loss[kPairThreads / 32];
+    __shared__ unsigned long long s_viol[kPairThreads / 32];
+    const uint32_t qi = blockIdx.x;
+    const double inv = __ddiv_rn(1.0, (double)st->pairs);
+    const uint64_t e = (uint64_t)blockIdx.y * kPairThreads + threadIdx.x;
     double loss = 0.0;
     unsigned long long viol = 0;
-    for (uint32_t i = threadIdx.x; i < T; i += blockDim.x) {
-        double g_acc = 0.0;
-        if (ti[i] != ~0u) {
-            const double b = bv[i];
-            for (uint32_t j = 0; j < O; ++j) {
-                if (oi[j] == ~0u) continue;
-                const double z = __dsub_rn(b, cv[j]);
-                const double logit = __fma_rn(beta, z, -alpha);
-                loss = __dadd_rn(loss, softplus_d(-logit));
-                viol += z < 0.0;
-                g_acc = __dsub_rn(g_acc, pair_g(logit, beta, inv));
-            }
+    if (e < (uint64_t)T * O) {
+        const uint32_t i = (uint32_t)(e / O), j = (uint32_t)(e % O);
+        double g = 0.0;
+        if (top_idx[(uint64_t)qi * T + i] != ~0u && oth_idx[(uint64_t)qi * O + j] != ~0u) {
+            const double* row = bc + (uint64_t)qi * (T + O);
+            const double z = __dsub_rn(row[i], row[T + j]);
+            const double logit = __fma_rn(beta, z, -alpha);
+            loss = softplus_d(-logit);
+            viol = z < 0.0;
+            g = pair_g(logit, beta, inv);
         }
-        gbuf_t[(uint64_t)qi * T + i] = g_acc;
+        gp[(uint64_t)qi * T * O + e] = g;
     }
-    for (uint32_t j = threadIdx.x; j < O; j += blockDim.x) {
-        double g_acc = 0.0;
-        if (oi[j] != ~0u) {
-            const double c = cv[j];
-            for (uint32_t i = 0; i < T; ++i) {
-                if (ti[i] == ~0u) continue;
-                const double logit = __fma_rn(beta, __dsub_rn(bv[i], c), -alpha);
-                g_acc = __dadd_rn(g_acc, pair_g(logit, beta, inv));
-            }
-        }
-        gbuf_o[(uint64_t)qi * O + j] = g_acc;
-    }
-    // deterministic block reduction of the loss / violation partials
     for (int o = 16; o; o >>= 1) {
         loss = __dadd_rn(loss, __shfl_xor_sync(~0u, loss, o));
         viol += __shfl_xor_sync(~0u, viol, o);
@@ -408,52 +432,144 @@ __global__ void __launch_bounds__(256) k_rank_loss(const float* __restrict__ sof
         s_loss[threadIdx.x >> 5] = loss;
         s_viol[threadIdx.x >> 5] = viol;
     }
-    __syncthreads();  // also orders the gbuf writes before the reads below
+    __syncthreads();
     if (threadIdx.x == 0) {
         double a = 0.0;
         unsigned long long v = 0;
-        for (uint32_t w = 0; w < blockDim.x / 32; ++w) {
+        for (int w = 0; w < kPairThreads / 32; ++w) {
             a = __dadd_rn(a, s_loss[w]);
             v += s_viol[w];
         }
-        loss_part[qi] = a;
-        viol_part[qi] = v;
+        loss_part[(uint64_t)qi * gridDim.y + blockIdx.y] = a;
+        viol_part[(uint64_t)qi * gridDim.y + blockIdx.y] = v;
     }
-    const double* gt = gbuf_t + (uint64_t)qi * T;
-    const double* go = gbuf_o + (uint64_t)qi * O;
-    for (uint32_t p = threadIdx.x; p < L; p += blockDim.x) {
-        float dq = 0.0f;
-        for (uint32_t i = 0; i < T; ++i) {
-            const double g = gt[i];
-            if (g == 0.0) continue;
-            dq = __fmaf_rn(__double2float_rn(g), softk[(uint64_t)ti[i] * L + p], dq);
+}
+
+__global__ void __launch_bounds__(256) k_rank_grad(const float* __restrict__ softk, uint32_t L,
+                                                   const uint32_t* top_idx, uint32_t T,
+                                                   const uint32_t* oth_idx, uint32_t O,
+                                                   uint32_t Qs, const double* __restrict__ gp,
+                                                   float* G, float* dsq, const TrainDev* st) {
+    if (st->halt) return;
+    extern __shared__ double dsm[];
+    double* gsum = dsm;  // [T + O]: gb then gc
+    const uint32_t qi = blockIdx.x;
+    const uint32_t* ti = top_idx + (uint64_t)qi * T;
+    const uint32_t* oi = oth_idx + (uint64_t)qi * O;
+    const double* g = gp + (uint64_t)qi * T * O;
+    // invalid pairs hold g = +0: acc - 0 and acc + 0 leave acc unchanged
+    // (acc starts at +0 and the pair gradients are >= 0), so the chains run
+    // over every slot. gb: 32-column tiles of g staged through shared memory
+    // (coalesced), each thread continuing its row's chain across tiles.
+    double* tile = gsum + T + O + (size_t)(T + O);  // after eg/ek: [T][33]
+    for (uint32_t i = threadIdx.x; i < T; i += blockDim.x) gsum[i] = 0.0;  // running chains
+    for (uint32_t j0 = 0; j0 < O; j0 += 32) {
+        const uint32_t w = min(32u, O - j0);
+        for (uint32_t e = threadIdx.x; e < T * 32; e += blockDim.x) {
+            const uint32_t i = e >> 5, jj = e & 31;
+            tile[i * 33 + jj] = jj < w ? g[(uint64_t)i * O + j0 + jj] : 0.0;
         }
-        for (uint32_t j = 0; j < O; ++j) {
-            const double g = go[j];
-            if (g == 0.0) continue;
-            dq = __fmaf_rn(__double2float_rn(g), softk[(uint64_t)oi[j] * L + p], dq);
+        __syncthreads();
+        for (uint32_t i = threadIdx.x; i < T; i += blockDim.x) {
+            double acc = gsum[i];
+            for (uint32_t jj = 0; jj < w; ++jj) acc = __dsub_rn(acc, tile[i * 33 + jj]);
+            gsum[i] = acc;
         }
-        dsq[(uint64_t)qi * L + p] = dq;
+        __syncthreads();
     }
     for (uint32_t i = threadIdx.x; i < T; i += blockDim.x)
-        if (gt[i] != 0.0) G[(uint64_t)ti[i] * Qs + qi] = __double2float_rn(gt[i]);
-    for (uint32_t j = threadIdx.x; j < O; j += blockDim.x)
-        if (go[j] != 0.0) G[(uint64_t)oi[j] * Qs + qi] = __double2float_rn(go[j]);
+        if (ti[i] == ~0u) gsum[i] = 0.0;
+    for (uint32_t j = threadIdx.x; j < O; j += blockDim.x) {
+        double acc = 0.0;
+        if (oi[j] != ~0u) {
+            uint32_t i = 0;
+            for (; i + 8 <= T; i += 8) {
+                double v[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) v[u] = g[(uint64_t)(i + u) * O + j];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) acc = __dadd_rn(acc, v[u]);
+            }
+            for (; i < T; ++i) acc = __dadd_rn(acc, g[(uint64_t)i * O + j]);
+        }
+        gsum[T + j] = acc;
+    }
+    __syncthreads();
+    // compact the non-zero entries (top first, then other, each in order):
+    // per-warp ballots, one running offset per 256-entry round
+    float* eg = reinterpret_cast<float*>(gsum + T + O);   // [T + O]
+    uint32_t* ek = reinterpret_cast<uint32_t*>(eg + T + O);  // [T + O]
+    __shared__ uint32_t s_ne, s_wc[8];
+    if (threadIdx.x == 0) s_ne = 0;
+    __syncthreads();
+    const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    for (uint32_t e0 = 0; e0 < T + O; e0 += blockDim.x) {
+        const uint32_t e = e0 + threadIdx.x;
+        const double v = e < T + O ? gsum[e] : 0.0;
+        const bool nz = v != 0.0;
+        const uint32_t bal = __ballot_sync(~0u, nz);
+        if (lane == 0) s_wc[wid] = __popc(bal);
+        __syncthreads();
+        uint32_t base = s_ne;
+        for (uint32_t w = 0; w < wid; ++w) base += s_wc[w];
+        if (nz) {
+            const uint32_t pos = base + __popc(bal & ((1u << lane) - 1u));
+            eg[pos] = __double2float_rn(v);
+            ek[pos] = e < T ? ti[e] : oi[e - T];
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            uint32_t t = 0;
+            for (uint32_t w = 0; w < blockDim.x / 32; ++w) t += s_wc[w];
+            s_ne += t;
+        }
+        __syncthreads();
+    }
+    const uint32_t ne = s_ne;
+    for (uint32_t p = threadIdx.x; p < L; p += blockDim.x) {
+        float dq = 0.0f;
+        uint32_t e = 0;
+        for (; e + 8 <= ne; e += 8) {
+            float v[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) v[u] = __ldg(softk + (uint64_t)ek[e + u] * L + p);
+#pragma unroll
+            for (int u = 0; u < 8; ++u) dq = __fmaf_rn(eg[e + u], v[u], dq);
+        }
+        for (; e < ne; ++e) dq = __fmaf_rn(eg[e], softk[(uint64_t)ek[e] * L + p], dq);
+        dsq[(uint64_t)qi * L + p] = dq;
+    }
+    for (uint32_t e = threadIdx.x; e < ne; e += blockDim.x) G[(uint64_t)ek[e] * Qs + qi] = eg[e];
 }
 
 // loss = sum of the query partials * inv_pairs; non-finite -> NumericError
 // (trainer.cpp:587-590); accumulates the iteration record over the batch.
 __global__ void k_loss_finalize(const double* loss_part, const unsigned long long* viol_part,
-                                uint32_t Qs, uint32_t b, uint32_t batch, uint32_t iter,
+                                uint32_t nparts, uint32_t b, uint32_t batch, uint32_t iter,
                                 double* rec, TrainDev* st) {
     if (st->halt) return;
+    __shared__ double s_l[256];
+    __shared__ unsigned long long s_v[256];
     const double inv = __ddiv_rn(1.0, (double)st->pairs);
-    double s = 0.0;
-    unsigned long long v = 0;
-    for (uint32_t q = 0; q < Qs; ++q) {
-        s = __dadd_rn(s, loss_part[q]);
-        v += viol_part[q];
+    double a = 0.0;
+    unsigned long long c = 0;
+    for (uint32_t q = threadIdx.x; q < nparts; q += blockDim.x) {  // fixed order per thread
+        a = __dadd_rn(a, loss_part[q]);
+        c += viol_part[q];
     }
+    s_l[threadIdx.x] = a;
+    s_v[threadIdx.x] = c;
+    __syncthreads();
+    for (uint32_t o = blockDim.x / 2; o; o >>= 1) {
+        if (threadIdx.x < o) {
+            s_l[threadIdx.x] = __dadd_rn(s_l[threadIdx.x], s_l[threadIdx.x + o]);
+            s_v[threadIdx.x] += s_v[threadIdx.x + o];
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x) return;
+    const double s = s_l[0];
+    const unsigned long long v = s_v[0];
     const double loss = __dmul_rn(s, inv), vr = __dmul_rn((double)v, inv);
     if (!isfinite(loss)) {
         st->halt = HALT_NONFINITE;
@@ -515,77 +631,155 @@ __global__ void k_dz(const float* __restrict__ dsoft, const float* __restrict__ 
 }
 
 // C[m][nc] += A[rows][m]^T B[rows][nc] (add_matmul_at, matrix.hpp:121-138):
-// each output one fma chain over the rows in order, from its current value.
-// Block: 128 columns x 4 output rows; 32-row chunks staged in shared memory.
+// each output is one fma chain over the rows in order, from its current
+// value; with b1 != null the column sums of B are chained too (b1[j] +=
+// B[r][j] in row order, trainer.cpp:231-234). The chains are inherently
+// sequential (the reference's rounding order), so the kernel is built for
+// latency: one chain per thread, 128 threads = 4 output rows x 32 columns
+// (every output gets its own thread), 64-row chunks of A and B double-
+// buffered in shared memory with cp.async so the loads of chunk c + 1 run
+// under the chains of chunk c.
+constexpr int kAtRows = 128;   // rows per stage
+constexpr int kAtStages = 4;   // cp.async ring depth (3 stages in flight)
+constexpr size_t kAtSmem = (size_t)kAtStages * kAtRows * 36 * 4;
 __global__ void __launch_bounds__(128) k_add_at(const float* __restrict__ A,
                                                 const float* __restrict__ B, uint32_t rows,
                                                 uint32_t m, uint32_t nc, float* __restrict__ C,
-                                                const TrainDev* st) {
+                                                float* __restrict__ b1, const TrainDev* st) {
     if (st->halt) return;
-    __shared__ float as[32][4], bs[32][128];
-    const uint32_t j = blockIdx.x * 128 + threadIdx.x;
-    const uint32_t i0 = blockIdx.y * 4;
-    float acc[4];
+    extern __shared__ float at_sm[];  // [stage][kAtRows][4] A, then [stage][kAtRows][32] B
+    float* as = at_sm;
+    float* bs = at_sm + kAtStages * kAtRows * 4;
+    const uint32_t ii = threadIdx.x >> 5, jj = threadIdx.x & 31;
+    const uint32_t i = blockIdx.y * 4 + ii, j = blockIdx.x * 32 + jj;
+    const bool own = i < m && j < nc;
+    const bool bsum = b1 != nullptr && blockIdx.y == 0 && ii == 0 && j < nc;
+    float acc = own ? C[(uint64_t)i * nc + j] : 0.0f;
+    float bacc = bsum ? b1[j] : 0.0f;
+    const uint32_t nch = (rows + kAtRows - 1) / kAtRows;
+    // zero-filling 4-byte cp.async (src-size 0 outside the matrices)
+    auto cp4 = [](float* dst, const float* src, bool ok) {
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(
+                         (uint32_t)__cvta_generic_to_shared(dst)),
+                     "l"(src), "r"(ok ? 4 : 0)
+                     : "memory");
+    };
+    const uint32_t bj = blockIdx.x * 32 + (threadIdx.x & 31);
+    const uint32_t ai = blockIdx.y * 4 + (threadIdx.x & 3);
+    auto stage = [&](uint32_t c) {  // always commits a group (possibly empty)
+        if (c < nch) {
+            const uint32_t r0 = c * kAtRows, buf = c % kAtStages;
+            float* bsb = bs + (size_t)buf * kAtRows * 32;
+            float* asb = as + (size_t)buf * kAtRows * 4;
+#pragma unroll 8
+            for (uint32_t k = 0; k < kAtRows / 4; ++k) {  // B: rows x 32 columns
+                const uint32_t r = (threadIdx.x >> 5) + 4 * k;
+                const bool ok = r0 + r < rows && bj < nc;
+                cp4(bsb + r * 32 + (threadIdx.x & 31), ok ? B + (uint64_t)(r0 + r) * nc + bj : B, ok);
+            }
 #pragma unroll
-    for (int i = 0; i < 4; ++i) acc[i] = (i0 + i < m && j < nc) ? C[(uint64_t)(i0 + i) * nc + j] : 0.0f;
-    for (uint32_t r0 = 0; r0 < rows; r0 += 32) {
-        const uint32_t w = min(32u, rows - r0);
-        for (uint32_t e = threadIdx.x; e < 32 * 4; e += 128) {
-            const uint32_t r = e / 4, i = e % 4;
-            as[r][i] = (r < w && i0 + i < m) ? A[(uint64_t)(r0 + r) * m + i0 + i] : 0.0f;
+            for (uint32_t k = 0; k < kAtRows / 32; ++k) {  // A: rows x 4 output rows
+                const uint32_t r = (threadIdx.x >> 2) + 32 * k;
+                const bool ok = r0 + r < rows && ai < m;
+                cp4(asb + r * 4 + (threadIdx.x & 3), ok ? A + (uint64_t)(r0 + r) * m + ai : A, ok);
+            }
         }
-        for (uint32_t r = 0; r < w; ++r)
-            bs[r][threadIdx.x] = j < nc ? B[(uint64_t)(r0 + r) * nc + j] : 0.0f;
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    for (int c = 0; c < kAtStages - 1; ++c) stage(c);
+    for (uint32_t c = 0; c < nch; ++c) {
+        asm volatile("cp.async.wait_group %0;" ::"n"(kAtStages - 2) : "memory");
         __syncthreads();
-        for (uint32_t r = 0; r < w; ++r) {
-            const float b = bs[r][threadIdx.x];
-#pragma unroll
-            for (int i = 0; i < 4; ++i) acc[i] = __fmaf_rn(as[r][i], b, acc[i]);
+        stage(c + kAtStages - 1);  // refills the slot consumed at c - 1
+        const uint32_t buf = c % kAtStages;
+        const float* bsb = bs + (size_t)buf * kAtRows * 32 + jj;
+        const float* asb = as + (size_t)buf * kAtRows * 4 + ii;
+        const uint32_t w = min((uint32_t)kAtRows, rows - c * kAtRows);
+        if (w == kAtRows) {
+#pragma unroll 16
+            for (uint32_t r = 0; r < kAtRows; ++r) {
+                const float bv = bsb[r * 32];
+                acc = __fmaf_rn(asb[r * 4], bv, acc);
+                if (bsum) bacc = __fadd_rn(bacc, bv);
+            }
+        } else {
+            for (uint32_t r = 0; r < w; ++r) {
+                const float bv = bsb[r * 32];
+                acc = __fmaf_rn(asb[r * 4], bv, acc);
+                if (bsum) bacc = __fadd_rn(bacc, bv);
+            }
         }
-        __syncthreads();
     }
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-        if (i0 + i < m && j < nc) C[(uint64_t)(i0 + i) * nc + j] = acc[i];
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+    if (own) C[(uint64_t)i * nc + j] = acc;
+    if (bsum) b1[j] = bacc;
 }
 
-// da1 = matmul_bt(dz2, W2) * silu_grad(z1) (trainer.cpp:227-230).
-constexpr int kDaRows = 8;
+// da1 = matmul_bt(dz2, W2) * silu_grad(z1) (trainer.cpp:227-230). W2 staged
+// in shared memory with a padded row stride (L + 1: the per-thread rows are
+// conflict-free), 32 rows of dz2 per block; thread i keeps the 32 chains of
+// its hidden unit (rounded products summed in order, fused tail).
+constexpr int kDaRows = 16;
 __global__ void __launch_bounds__(128) k_da1(const float* __restrict__ dz2,
                                              const float* __restrict__ w2,
                                              const float* __restrict__ z1, uint32_t m, uint32_t h,
                                              uint32_t L, float* __restrict__ da1,
                                              const TrainDev* st) {
     if (st->halt) return;
-    extern __shared__ float zs[];  // [kDaRows][L]
+    extern __shared__ float sm[];
+    float* ws = sm;                       // [h][L + 1]
+    float* zs = sm + (size_t)h * (L + 1); // [kDaRows][L]
     const uint32_t r0 = blockIdx.x * kDaRows;
     const uint32_t nr = min((uint32_t)kDaRows, m - r0);
-    for (uint32_t e = threadIdx.x; e < nr * L; e += blockDim.x) zs[e] = dz2[(uint64_t)r0 * L + e];
+    for (uint32_t i = 0; i < h; ++i)  // row i of W2 -> padded row of ws (async, 4-byte)
+        for (uint32_t p = threadIdx.x; p < L; p += blockDim.x)
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(
+                             (uint32_t)__cvta_generic_to_shared(ws + (size_t)i * (L + 1) + p)),
+                         "l"(w2 + (uint64_t)i * L + p)
+                         : "memory");
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    for (uint32_t r = 0; r < kDaRows; ++r)  // p-major: zs[p][r] (zero rows past m)
+        for (uint32_t p = threadIdx.x; p < L; p += blockDim.x)
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(
+                             (uint32_t)__cvta_generic_to_shared(zs + p * kDaRows + r)),
+                         "l"(r < nr ? dz2 + (uint64_t)(r0 + r) * L + p : dz2), "r"(r < nr ? 4 : 0)
+                         : "memory");
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
     __syncthreads();
     const uint32_t n4 = n4_of(L);
     for (uint32_t i = threadIdx.x; i < h; i += blockDim.x) {
-        const float* wr = w2 + (uint64_t)i * L;
-        for (uint32_t r = 0; r < nr; ++r) {
-            const float* a = zs + r * L;
-            float acc = 0.0f;
-            uint32_t p = 0;
-            for (; p < n4; ++p) acc = __fadd_rn(acc, __fmul_rn(a[p], wr[p]));
-            for (; p < L; ++p) acc = __fmaf_rn(a[p], wr[p], acc);
-            const uint64_t o = (uint64_t)(r0 + r) * h + i;
-            da1[o] = __fmul_rn(acc, silu_grad_f(z1[o]));
+        const float* wr = ws + (size_t)i * (L + 1);
+        float acc[kDaRows];
+#pragma unroll
+        for (int r = 0; r < kDaRows; ++r) acc[r] = 0.0f;
+        for (uint32_t p = 0; p < L; ++p) {
+            const float wv = wr[p];
+            const float4* zp = reinterpret_cast<const float4*>(zs + p * kDaRows);
+            float z[kDaRows];
+#pragma unroll
+            for (int q = 0; q < kDaRows / 4; ++q) {
+                const float4 t = zp[q];
+                z[4 * q] = t.x;
+                z[4 * q + 1] = t.y;
+                z[4 * q + 2] = t.z;
+                z[4 * q + 3] = t.w;
+            }
+            if (p < n4) {
+#pragma unroll
+                for (int r = 0; r < kDaRows; ++r) acc[r] = __fadd_rn(acc[r], __fmul_rn(z[r], wv));
+            } else {
+#pragma unroll
+                for (int r = 0; r < kDaRows; ++r) acc[r] = __fmaf_rn(z[r], wv, acc[r]);
+            }
         }
+#pragma unroll
+        for (int r = 0; r < kDaRows; ++r)
+            if ((uint32_t)r < nr) {
+                const uint64_t o = (uint64_t)(r0 + r) * h + i;
+                da1[o] = __fmul_rn(acc[r], silu_grad_f(z1[o]));
+            }
     }
-}
-
-// b1 += column sums of da1 in row order (trainer.cpp:231-234)
-__global__ void k_b1(const float* __restrict__ da1, uint32_t m, uint32_t h, float* b1g,
-                     const TrainDev* st) {
-    if (st->halt) return;
-    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= h) return;
-    float acc = b1g[i];
-    for (uint32_t r = 0; r < m; ++r) acc = __fadd_rn(acc, da1[(uint64_t)r * h + i]);
-    b1g[i] = acc;
 }
 
 // ------------------------------------------------------------ optimiser
@@ -970,11 +1164,12 @@ spl_status train_impl(spl_ctx* ctx, int kind, uint32_t d, uint32_t h, uint32_t L
         maxT = std::max<uint32_t>(maxT, (uint32_t)w.top_pos.size());
         maxO = std::max<uint32_t>(maxO, (uint32_t)w.oth_pos.size());
     }
-    const size_t rank_smem = (size_t)(maxT + maxO) * 8 + (size_t)L * 4;
-    if (rank_smem > 200 * 1024)
+    const size_t grad_smem = (size_t)(maxT + maxO) * 16 + (size_t)maxT * 33 * 8;
+    if (grad_smem > 200 * 1024)
         return fail(ctx, SPL_E_DIMENSION, "train_hasher: sampled pair set too large for one block "
                                           "(set max_top / max_oth)");
-    SPL_CUDA_TRY(ctx, cudaFuncSetAttribute(k_rank_loss, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rank_smem));
+    SPL_CUDA_TRY(ctx, cudaFuncSetAttribute(k_rank_grad, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)grad_smem));
+    const uint64_t pair_blocks = ((uint64_t)maxT * maxO + kPairThreads - 1) / kPairThreads;
     const uint32_t hw = mlp ? h : 1;
     float *z1q = db.get<float>((size_t)maxQ * hw), *a1q = db.get<float>((size_t)maxQ * hw);
     float *z2q = db.get<float>((size_t)maxQ * L), *sfq = db.get<float>((size_t)maxQ * L);
@@ -984,9 +1179,10 @@ spl_status train_impl(spl_ctx* ctx, int kind, uint32_t d, uint32_t h, uint32_t L
     float *dz = db.get<float>((size_t)std::max(maxQ, max_n) * L);
     float *da1 = db.get<float>((size_t)std::max(maxQ, max_n) * hw);
     float *Gm = db.get<float>((size_t)max_n * maxQ);
-    double *gbt = db.get<double>((size_t)maxQ * maxT), *gbo = db.get<double>((size_t)maxQ * maxO);
-    double* lpart = db.get<double>(maxQ);
-    unsigned long long* vpart = db.get<unsigned long long>(maxQ);
+    double* bcv = db.get<double>((size_t)maxQ * (maxT + maxO));
+    double* gpair = db.get<double>((size_t)maxQ * maxT * maxO);
+    double* lpart = db.get<double>((size_t)maxQ * pair_blocks);
+    unsigned long long* vpart = db.get<unsigned long long>((size_t)maxQ * pair_blocks);
     uint32_t *top_idx = db.get<uint32_t>((size_t)maxQ * maxT), *oth_idx = db.get<uint32_t>((size_t)maxQ * maxO);
     // every draw's index lists, uploaded once
     std::vector<uint64_t> doff(draws.size() + 1, 0);
@@ -1001,7 +1197,7 @@ spl_status train_impl(spl_ctx* ctx, int kind, uint32_t d, uint32_t h, uint32_t L
     }
     uint32_t* ddraw = db.get<uint32_t>(hdraw.size());
     if (!z1q || !a1q || !z2q || !sfq || !z1k || !a1k || !z2k || !sfk || !dsq || !dsk || !dz || !da1 ||
-        !Gm || !gbt || !gbo || !lpart || !vpart || !top_idx || !oth_idx || !ddraw)
+        !Gm || !bcv || !gpair || !lpart || !vpart || !top_idx || !oth_idx || !ddraw)
         return fail(ctx, SPL_E_CUDA, "train: out of device memory");
     if (!hdraw.empty())
         SPL_CUDA_TRY(ctx, cudaMemcpyAsync(ddraw, hdraw.data(), hdraw.size() * 4, cudaMemcpyHostToDevice, s));
@@ -1028,6 +1224,12 @@ spl_status train_impl(spl_ctx* ctx, int kind, uint32_t d, uint32_t h, uint32_t L
     // x rows are gathered (queries) or identity (keys)
     float* xg = db.get<float>((size_t)maxQ * d);  // gathered query inputs for add_at
     if (!xg) return fail(ctx, SPL_E_CUDA, "train: out of device memory");
+    SPL_CUDA_TRY(ctx, cudaFuncSetAttribute(k_add_at, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kAtSmem));
+    const size_t da1_smem = mlp ? ((size_t)h * (L + 1) + (size_t)kDaRows * L) * 4 : 0;
+    if (da1_smem > 220 * 1024)
+        return fail(ctx, SPL_E_DIMENSION, "train_hasher: hidden x code width too large for the GPU trainer");
+    if (mlp)
+        SPL_CUDA_TRY(ctx, cudaFuncSetAttribute(k_da1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)da1_smem));
     auto bwd = [&](const float* x, uint32_t m, const float* z1, const float* a1, const float* z2,
                    const float* dsoft) -> spl_status {
         const uint64_t ne = (uint64_t)m * L;
@@ -1039,19 +1241,27 @@ spl_status train_impl(spl_ctx* ctx, int kind, uint32_t d, uint32_t h, uint32_t L
             dzp = dz;
         }
         if (mlp) {
-            k_add_at<<<dim3((L + 127) / 128, (h + 3) / 4), 128, 0, s>>>(a1, dzp, m, h, L, gW2, dst);
+            k_add_at<<<dim3((L + 31) / 32, (h + 3) / 4), 128, kAtSmem, s>>>(a1, dzp, m, h, L, gW2, nullptr, dst);
             if (spl_status st = after_launch(ctx, "k_add_at")) return st;
-            k_da1<<<(m + kDaRows - 1) / kDaRows, 128, (size_t)kDaRows * L * 4, s>>>(dzp, W2, z1, m, h, L, da1, dst);
+            k_da1<<<(m + kDaRows - 1) / kDaRows, 128, da1_smem, s>>>(dzp, W2, z1, m, h, L, da1, dst);
             if (spl_status st = after_launch(ctx, "k_da1")) return st;
-            k_b1<<<(h + 127) / 128, 128, 0, s>>>(da1, m, h, gB1, dst);
-            if (spl_status st = after_launch(ctx, "k_b1")) return st;
-            k_add_at<<<dim3((h + 127) / 128, (d + 3) / 4), 128, 0, s>>>(x, da1, m, d, h, gW1, dst);
+            k_add_at<<<dim3((h + 31) / 32, (d + 3) / 4), 128, kAtSmem, s>>>(x, da1, m, d, h, gW1, gB1, dst);
             return after_launch(ctx, "k_add_at");
         }
-        k_add_at<<<dim3((L + 127) / 128, (d + 3) / 4), 128, 0, s>>>(x, dzp, m, d, L, gW1, dst);
+        k_add_at<<<dim3((L + 31) / 32, (d + 3) / 4), 128, kAtSmem, s>>>(x, dzp, m, d, L, gW1, nullptr, dst);
         return after_launch(ctx, "k_add_at");
     };
     const float invb = tc.batch > 1 ? (float)(1.0 / tc.batch) : 1.0f;
+    // SPL_TRAIN_PROFILE=1: host vs device time of the training loop (stderr)
+    const char* prof = getenv("SPL_TRAIN_PROFILE");
+    cudaEvent_t pe[2];
+    std::chrono::steady_clock::time_point pt0;
+    if (prof && *prof == '1') {
+        cudaEventCreate(&pe[0]);
+        cudaEventCreate(&pe[1]);
+        cudaEventRecord(pe[0], s);
+        pt0 = std::chrono::steady_clock::now();
+    }
     for (uint32_t it = 0; it < iters; ++it) {
         const double lr = train_lr_at(it, tc);
         SPL_CUDA_TRY(ctx, cudaMemsetAsync(dG, 0, np * 4, s));
@@ -1070,11 +1280,17 @@ spl_status train_impl(spl_ctx* ctx, int kind, uint32_t d, uint32_t h, uint32_t L
             if (spl_status st = after_launch(ctx, "k_partition")) return st;
             if (spl_status st = fwd(p.x_q, qrows, Qs, z1q, a1q, z2q, sfq)) return st;
             if (spl_status st = fwd(p.x_k, nullptr, n, z1k, a1k, z2k, sfk)) return st;
-            k_rank_loss<<<Qs, 256, (size_t)(T + O) * 8 + (size_t)L * 4, s>>>(
-                sfq, sfk, L, top_idx, T, oth_idx, O, Qs, rc.beta, rc.alpha, gbt, gbo, Gm, dsq, lpart,
-                vpart, dst, it);
-            if (spl_status st = after_launch(ctx, "k_rank_loss")) return st;
-            k_loss_finalize<<<1, 1, 0, s>>>(lpart, vpart, Qs, b, tc.batch, it, drec, dst);
+            k_rank_dots<<<dim3(Qs, (T + O + 127) / 128), 128, (size_t)L * 4, s>>>(
+                sfq, sfk, L, top_idx, T, oth_idx, O, bcv, dst, it);
+            if (spl_status st = after_launch(ctx, "k_rank_dots")) return st;
+            const uint32_t pb = (uint32_t)(((uint64_t)T * O + kPairThreads - 1) / kPairThreads);
+            k_rank_pairs<<<dim3(Qs, pb), kPairThreads, 0, s>>>(bcv, top_idx, T, oth_idx, O, rc.beta,
+                                                                rc.alpha, gpair, lpart, vpart, dst);
+            if (spl_status st = after_launch(ctx, "k_rank_pairs")) return st;
+            k_rank_grad<<<Qs, 256, (size_t)(T + O) * 16 + (size_t)T * 33 * 8, s>>>(sfk, L, top_idx, T, oth_idx, O, Qs,
+                                                               gpair, Gm, dsq, dst);
+            if (spl_status st = after_launch(ctx, "k_rank_grad")) return st;
+            k_loss_finalize<<<1, 256, 0, s>>>(lpart, vpart, Qs * pb, b, tc.batch, it, drec, dst);
             if (spl_status st = after_launch(ctx, "k_loss_finalize")) return st;
             k_dsoft_keys<<<(unsigned)(((uint64_t)n * L + 255) / 256), 256, 0, s>>>(Gm, sfq, Qs, n, L, invb, dsk, dst);
             if (spl_status st = after_launch(ctx, "k_dsoft_keys")) return st;
@@ -1097,6 +1313,18 @@ spl_status train_impl(spl_ctx* ctx, int kind, uint32_t d, uint32_t h, uint32_t L
         if (spl_status st = after_launch(ctx, "k_adamw")) return st;
     }
 
+    if (prof && *prof == '1') {
+        const double host_ms =
+            std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - pt0).count();
+        cudaEventRecord(pe[1], s);
+        cudaEventSynchronize(pe[1]);
+        float dev_ms = 0;
+        cudaEventElapsedTime(&dev_ms, pe[0], pe[1]);
+        fprintf(stderr, "train loop: %u iters, host enqueue %.3f ms, device %.3f ms (%.3f ms/iter)\n",
+                iters, host_ms, dev_ms, iters ? dev_ms / iters : 0.0);
+        cudaEventDestroy(pe[0]);
+        cudaEventDestroy(pe[1]);
+    }
     // ---- results: weights (also on the error paths, as the reference's
     // in-place hasher), records, then the holdout IoU
     TrainDev hs{};
