@@ -228,6 +228,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-decode", action="store_true")
     ap.add_argument("--no-prefill", action="store_true")
+    ap.add_argument("--no-train", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
@@ -392,6 +393,7 @@ def main():
     decode4 = None
     prefill = None
     accuracy = None
+    train = None
     w1 = (rng.standard_normal((H, D, D)) / np.sqrt(D)).astype(np.float32)
     b1 = np.zeros((H, D), np.float32)
     w2 = (rng.standard_normal((H, D, L)) / np.sqrt(D)).astype(np.float32)
@@ -440,6 +442,8 @@ def main():
             decode4 = bench_decode4(torch, capi, ctx, dev, stream, args)
         if not args.no_decode:
             accuracy = bench_accuracy(torch, capi, ctx, dev, stream, args)
+        if not args.no_train:
+            train = bench_train(capi, ctx, args)
     clk = clocks.stop()
 
     # CPU baseline (rank 0, N = 1): the reference on this host's cores
@@ -509,6 +513,8 @@ def main():
         line["batched_decode"] = decode4
     if accuracy:
         line["retrieval_accuracy"] = accuracy
+    if train:
+        line["hasher_training"] = train
     if rank == 0:
         print(json.dumps(line), flush=True)
     ctx.close()
@@ -627,6 +633,67 @@ def bench_decode4(torch, capi, ctx, dev, stream, args):
                          "achieved": round(alg / (ms * 1e-3) / 1e9, 1), "peak": hbm,
                          "frac": round(alg / (ms * 1e-3) / 1e9 / hbm, 4)}}
 
+
+
+def bench_train(capi, ctx, args):
+    """Hasher training through the C-ABI (spl_train_hasher,
+    host weights and data in, host weights and records out): the CLI's
+    default training shape (spotlight.cpp:130-146: MLP d=h=L=128, max_oth 256,
+    query subsample 64, maskout 0.98) on one synthetic 4096-token sequence.
+    ms per iteration = (wall of a 64-iteration run - wall of a 1-iteration
+    run) / 63, so the per-sequence preparation (exact logits, per-row order)
+    and the holdout IoU cancel out. The reference's train_hasher runs the same
+    workload on the host cores for a few iterations beside it, and the
+    weights after those iterations are compared."""
+    from oracle_lib import RefLib
+
+    n, iters = 4096, 64
+    rng = np.random.default_rng(0)
+    data = [(rng.standard_normal((n, 128)).astype(np.float32),
+             rng.standard_normal((n, 128)).astype(np.float32))]
+    rank = dict(beta=1.0, alpha=3.0, maskout=0.98, max_top=None, max_oth=256,
+                query_subsample=64)
+    if not RefLib.available():
+        return None
+    ref = RefLib()
+    w = ref.mlp_gaussian_init(128, 128, 128, 64.0, ref.derive_seed(0, 100))
+
+    def gpu(it):
+        g = [a.copy() for a in w]
+        t = time.perf_counter()
+        out = ctx.train_hasher(1, 128, 128, 128, 64.0, *g, data, capi.RankConfig(**rank),
+                               capi.TrainConfig(num_iters=it))
+        return time.perf_counter() - t, g, out["loop_ms"]
+
+    gpu(2)
+    runs = [gpu(iters) for _ in range(3)]
+    ms_gpu = statistics.median(r[2] for r in runs) / iters
+    e2e_s = statistics.median(r[0] for r in runs)
+    ref_iters = 4
+    cfg = dict(num_iters=1, warmup_iters=81, batch=1, seed=0, holdout_queries=128, max_lr=1e-3,
+               min_lr=0.0, adam_beta1=0.9, adam_beta2=0.98, adam_eps=1e-8, weight_decay=0.1,
+               grad_clip=1.0, soft_gamma=64.0, holdout_budget_rate=0.02)
+    t = time.perf_counter()
+    ref.train(1, *w, 64.0, data, rank, cfg)
+    r1 = time.perf_counter() - t
+    t = time.perf_counter()
+    r = ref.train(1, *w, 64.0, data, rank, dict(cfg, num_iters=ref_iters))
+    r4 = time.perf_counter() - t
+    ms_ref = (r4 - r1) / (ref_iters - 1) * 1e3
+    _, g4, _ = gpu(ref_iters)
+    same = all(np.array_equal(a, b) for a, b in zip(g4, r[:3]))
+    return {"workload": "train_hasher, MLP d=h=L=128, one 4096-token sequence, ranking loss, "
+                        "max_oth 256, query subsample 64 (CLI defaults), AdamW",
+            "ms_per_iter": round(ms_gpu, 3), "iters_timed": iters,
+            "timing": "CUDA events around the iteration loop inside spl_train_hasher "
+                      "(median of 3 runs)",
+            "e2e_s_per_run": round(e2e_s, 4),
+            "e2e_path": "spl_train_hasher wall time for %d iterations: host data and weights in, "
+                        "exact logits + order, loop, weights and records out, holdout IoU" % iters,
+            "reference_ms_per_iter": round(ms_ref, 3),
+            "reference_threads": int(ref.lib.spotref_max_threads()),
+            "speedup_vs_reference": round(ms_ref / ms_gpu, 1),
+            "weights_identical_after_%d_iters" % ref_iters: bool(same)}
 
 def bench_accuracy(torch, capi, ctx, dev, stream, args):
     """Retrieval accuracy (the paper's Table-1 metric) at the

@@ -324,6 +324,9 @@ spl_status spl_train_hasher(spl_ctx* ctx, int kind, uint32_t d, uint32_t h, uint
 spl_status spl_train_partition_host(const spl_rank_config* rank, uint32_t q_train, uint32_t n,
                                     uint64_t seed, uint32_t* rows, uint32_t* top_pos,
                                     uint32_t* oth_pos, uint32_t* counts);
+/* Device time (CUDA events) of the iteration loop of the last
+ * spl_train_hasher call on this context, ms (setup and holdout excluded). */
+double spl_train_last_loop_ms(const spl_ctx* ctx);
 /* lr_at (trainer.cpp:35-46) */
 double spl_train_lr_at(uint32_t iter, const spl_train_config* train);
 

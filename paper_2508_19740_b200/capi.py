@@ -119,8 +119,10 @@ _SIGS = {
                          C.POINTER(dbl), u32p, vp],
     "spl_train_partition_host": [vp, u32, u32, u64, vp, vp, vp, vp],
     "spl_train_lr_at": [u32, vp],
+    "spl_train_last_loop_ms": [vp],
 }
-_RESTYPE = {"spl_version": C.c_char_p, "spl_train_lr_at": C.c_double, "spl_last_error": C.c_char_p, "spl_ctx_destroy": None,
+_RESTYPE = {"spl_version": C.c_char_p, "spl_train_lr_at": C.c_double,
+            "spl_train_last_loop_ms": C.c_double, "spl_last_error": C.c_char_p, "spl_ctx_destroy": None,
             "spl_peer_destroy": None,
             "spl_hasher_destroy": None, "spl_launch_count": C.c_uint64}
 
@@ -344,7 +346,8 @@ class Context:
             len(sequences), qs.ctypes.data, ks.ctypes.data, lens.ctypes.data, C.byref(rank),
             C.byref(cfg), rec.ctypes.data, C.byref(iou), C.byref(sk), _stream(stream)))
         return {"records": rec[:cfg.num_iters], "holdout_iou": iou.value,
-                "skipped_steps": sk.value}
+                "skipped_steps": sk.value,
+                "loop_ms": self.lib.spl_train_last_loop_ms(self.h)}
 
     def hamming_topk(self, codes, stride_rows, L, qcodes, P, n_valid, nvalid_div, n_max, k, idx,
                      cnt, stream=None):

@@ -21,6 +21,7 @@ struct spl_ctx {
     int num_sms = 148;
     std::string err;
     uint64_t launches = 0;
+    double last_train_loop_ms = 0.0;  // device time of the last spl_train_hasher loop
 
     uint32_t* dev_err = nullptr;  // device error word (bit flags above)
 

@@ -1051,6 +1051,7 @@ spl_status train_impl(spl_ctx* ctx, int kind, uint32_t d, uint32_t h, uint32_t L
     const float sgamma = mlp ? gamma : (float)tc.soft_gamma;  // MlpCoder uses h.gamma
     if (kind == 2 && L == 0) return fail(ctx, SPL_E_DIMENSION, "downproj: width must be >= 1");
 
+    const auto tsetup = std::chrono::steady_clock::now();
     // ---- draws for every iteration (host, the reference's engines)
     const uint32_t iters = tc.num_iters;
     std::vector<uint64_t> off(n_seq + 1, 0);
@@ -1252,16 +1253,21 @@ spl_status train_impl(spl_ctx* ctx, int kind, uint32_t d, uint32_t h, uint32_t L
         return after_launch(ctx, "k_add_at");
     };
     const float invb = tc.batch > 1 ? (float)(1.0 / tc.batch) : 1.0f;
-    // SPL_TRAIN_PROFILE=1: host vs device time of the training loop (stderr)
+    // device time of the loop (spl_train_last_loop_ms); SPL_TRAIN_PROFILE=1
+    // also prints host enqueue vs device time and the setup / holdout costs
     const char* prof = getenv("SPL_TRAIN_PROFILE");
     cudaEvent_t pe[2];
-    std::chrono::steady_clock::time_point pt0;
-    if (prof && *prof == '1') {
-        cudaEventCreate(&pe[0]);
-        cudaEventCreate(&pe[1]);
-        cudaEventRecord(pe[0], s);
-        pt0 = std::chrono::steady_clock::now();
-    }
+    SPL_CUDA_TRY(ctx, cudaEventCreate(&pe[0]));
+    SPL_CUDA_TRY(ctx, cudaEventCreate(&pe[1]));
+    struct EvGuard {
+        cudaEvent_t* e;
+        ~EvGuard() {
+            cudaEventDestroy(e[0]);
+            cudaEventDestroy(e[1]);
+        }
+    } evg_{pe};
+    SPL_CUDA_TRY(ctx, cudaEventRecord(pe[0], s));
+    const std::chrono::steady_clock::time_point pt0 = std::chrono::steady_clock::now();
     for (uint32_t it = 0; it < iters; ++it) {
         const double lr = train_lr_at(it, tc);
         SPL_CUDA_TRY(ctx, cudaMemsetAsync(dG, 0, np * 4, s));
@@ -1313,17 +1319,17 @@ spl_status train_impl(spl_ctx* ctx, int kind, uint32_t d, uint32_t h, uint32_t L
         if (spl_status st = after_launch(ctx, "k_adamw")) return st;
     }
 
-    if (prof && *prof == '1') {
+    {
         const double host_ms =
             std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - pt0).count();
-        cudaEventRecord(pe[1], s);
-        cudaEventSynchronize(pe[1]);
+        SPL_CUDA_TRY(ctx, cudaEventRecord(pe[1], s));
+        SPL_CUDA_TRY(ctx, cudaEventSynchronize(pe[1]));
         float dev_ms = 0;
-        cudaEventElapsedTime(&dev_ms, pe[0], pe[1]);
-        fprintf(stderr, "train loop: %u iters, host enqueue %.3f ms, device %.3f ms (%.3f ms/iter)\n",
-                iters, host_ms, dev_ms, iters ? dev_ms / iters : 0.0);
-        cudaEventDestroy(pe[0]);
-        cudaEventDestroy(pe[1]);
+        SPL_CUDA_TRY(ctx, cudaEventElapsedTime(&dev_ms, pe[0], pe[1]));
+        ctx->last_train_loop_ms = dev_ms;
+        if (prof && *prof == '1')
+            fprintf(stderr, "train loop: %u iters, host enqueue %.3f ms, device %.3f ms (%.3f ms/iter)\n",
+                    iters, host_ms, dev_ms, iters ? dev_ms / iters : 0.0);
     }
     // ---- results: weights (also on the error paths, as the reference's
     // in-place hasher), records, then the holdout IoU
@@ -1345,12 +1351,17 @@ spl_status train_impl(spl_ctx* ctx, int kind, uint32_t d, uint32_t h, uint32_t L
     if (records)
         for (uint32_t it = 0; it < iters; ++it) records[3 * (size_t)it + 2] = train_lr_at(it, tc);
     if (skipped) *skipped = hs.skipped;
+    const auto th0 = std::chrono::steady_clock::now();
     if (holdout_iou) {
         spl_status st = holdout_iou_impl(ctx, kind, d, h, L, w1, b1, w2, prep[0].x_q, prep[0].x_k,
                                          prep[0].logits, seq_len[0], prep[0].q_train,
                                          tc.holdout_budget_rate, holdout_iou, s);
         if (st) return st;
     }
+    if (prof && *prof == '1')
+        fprintf(stderr, "train: setup %.3f ms, holdout %.3f ms\n",
+                std::chrono::duration<double, std::milli>(pt0 - tsetup).count(),
+                std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - th0).count());
     return SPL_OK;
 }
 
@@ -1384,6 +1395,10 @@ extern "C" spl_status spl_train_partition_host(const spl_rank_config* rank, uint
                                                uint32_t* counts) {
     if (!rank || !rows || !top_pos || !oth_pos || !counts) return SPL_E_STATE;
     return spl::train_partition_host(*rank, q_train, n, seed, rows, top_pos, oth_pos, counts);
+}
+
+extern "C" double spl_train_last_loop_ms(const spl_ctx* ctx) {
+    return ctx ? ctx->last_train_loop_ms : 0.0;
 }
 
 extern "C" double spl_train_lr_at(uint32_t iter, const spl_train_config* train) {

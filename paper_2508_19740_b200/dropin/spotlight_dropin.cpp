@@ -22,6 +22,10 @@
 #include <vector>
 
 #include "spl_c.h"
+#include <chrono>
+#include <cstdio>
+
+#include "spotlight/trainer.hpp"
 #include "spotlight/attention_eval.hpp"
 #include "spotlight/bitcodes.hpp"
 #include "spotlight/hashers.hpp"
@@ -57,6 +61,7 @@ spl_ctx* ctx() {
         case SPL_E_NUMERIC: throw NumericError(msg);
         case SPL_E_FORMAT: throw FormatError(msg);
         case SPL_E_IO: throw IoError(msg);
+        case SPL_E_EMPTY_PAIRS: throw EmptyPairError(msg);
         default: throw DeviceError(msg.empty() ? "spotlight: device failure" : msg);
     }
 }
@@ -839,6 +844,143 @@ std::string eval_report_csv(const EvalReport& report) {
         out += "\n";
     }
     return out;
+}
+
+// ------------------------------------------------------------ training (§8 f4)
+void RankingLossConfig::validate(std::size_t n_keys) const {  // ranking_loss.cpp:13-28
+    if (beta <= 0.0) throw DimensionError("ranking loss: beta must be positive");
+    if (!(maskout > 0.0 && maskout < 1.0)) throw DimensionError("ranking loss: maskout must lie in (0, 1)");
+    const auto k = static_cast<std::uint32_t>(static_cast<double>(n_keys) * (1.0 - maskout));
+    if (k == 0) throw DimensionError("ranking loss: top count floored to zero for n=" + str(n_keys));
+    if (max_top && *max_top == 0) throw DimensionError("ranking loss: max_top must be >= 1");
+    if (max_oth && *max_oth == 0) throw DimensionError("ranking loss: max_oth must be >= 1");
+    if (query_subsample && *query_subsample == 0)
+        throw DimensionError("ranking loss: query_subsample must be >= 1");
+}
+
+namespace {
+spl_train_config to_c(const TrainConfig& c) {
+    spl_train_config t{};
+    t.num_iters = c.num_iters;
+    t.warmup_iters = c.warmup_iters;
+    t.batch = c.batch;
+    t.holdout_queries = c.holdout_queries;
+    t.seed = c.seed;
+    t.max_lr = c.max_lr;
+    t.min_lr = c.min_lr;
+    t.adam_beta1 = c.adam_beta1;
+    t.adam_beta2 = c.adam_beta2;
+    t.adam_eps = c.adam_eps;
+    t.weight_decay = c.weight_decay;
+    t.grad_clip = c.grad_clip;
+    t.soft_gamma = c.soft_gamma;
+    t.holdout_budget_rate = c.holdout_budget_rate;
+    return t;
+}
+}  // namespace
+
+void TrainConfig::validate() const {  // trainer.cpp:19-33
+    if (max_lr < 0.0 || min_lr < 0.0 || min_lr > max_lr)
+        throw DimensionError("TrainConfig: need 0 <= min_lr <= max_lr");
+    if (!(adam_beta1 >= 0.0 && adam_beta1 < 1.0 && adam_beta2 >= 0.0 && adam_beta2 < 1.0))
+        throw DimensionError("TrainConfig: adam betas must lie in [0, 1)");
+    if (adam_eps <= 0.0) throw DimensionError("TrainConfig: adam_eps must be positive");
+    if (weight_decay < 0.0) throw DimensionError("TrainConfig: weight_decay must be >= 0");
+    if (batch < 1) throw DimensionError("TrainConfig: batch must be >= 1");
+    if (soft_gamma <= 0.0) throw DimensionError("TrainConfig: soft_gamma must be positive");
+    if (!(holdout_budget_rate > 0.0 && holdout_budget_rate <= 1.0))
+        throw DimensionError("TrainConfig: holdout_budget_rate must lie in (0, 1]");
+}
+
+double lr_at(std::uint32_t iter, const TrainConfig& cfg) {
+    const spl_train_config c = to_c(cfg);
+    return spl_train_lr_at(iter, &c);
+}
+
+std::string format_train_report(const TrainReport& report,
+                                std::span<const std::string> header_lines) {  // trainer.cpp:152-175
+    std::string out;
+    for (const std::string& line : header_lines) out += "# " + line + "\n";
+    out += "# columns: iter loss violation_rate lr\n";
+    char buf[160];
+    for (const IterRecord& rec : report.records) {
+        std::snprintf(buf, sizeof(buf), "%u %.9g %.9g %.9g", rec.iter, rec.loss, rec.violation_rate,
+                      rec.lr);
+        out += buf;
+        out += "\n";
+    }
+    std::snprintf(buf, sizeof(buf), "# final_holdout_iou %.6f", report.final_holdout_iou);
+    out += buf;
+    out += "\n# skipped_steps " + std::to_string(report.skipped_steps) + "\n";
+    return out;
+}
+
+TrainReport train_hasher(AnyHasher& hasher, const TrainDataset& dataset,
+                         const RankingLossConfig& loss_cfg, const TrainConfig& cfg,
+                         TrainLoss loss_kind) {
+    const auto t0 = std::chrono::steady_clock::now();
+    cfg.validate();
+    if (loss_kind != TrainLoss::ranking)
+        throw DimensionError("train_hasher: only the ranking loss runs on the B200 trainer");
+    if (dataset.sequences.empty()) throw DimensionError("train_hasher: dataset is empty");
+    std::vector<float> qs, ks;
+    std::vector<std::uint32_t> lens;
+    std::uint32_t d = 0;
+    for (const QkSequence& seq : dataset.sequences) {
+        if (seq.queries.rows() != seq.keys.rows())
+            throw DimensionError("train_hasher: queries and keys must be causally aligned");
+        if (seq.queries.rows() < 2)
+            throw DimensionError("train_hasher: sequences need at least two positions");
+        d = static_cast<std::uint32_t>(seq.queries.cols());
+        qs.insert(qs.end(), seq.queries.data(), seq.queries.data() + seq.queries.size());
+        ks.insert(ks.end(), seq.keys.data(), seq.keys.data() + seq.keys.size());
+        lens.push_back(static_cast<std::uint32_t>(seq.queries.rows()));
+    }
+    spl_rank_config rc{loss_cfg.beta, loss_cfg.alpha, loss_cfg.maskout,
+                       loss_cfg.max_top ? static_cast<std::int64_t>(*loss_cfg.max_top) : -1,
+                       loss_cfg.max_oth ? static_cast<std::int64_t>(*loss_cfg.max_oth) : -1,
+                       loss_cfg.query_subsample ? static_cast<std::int64_t>(*loss_cfg.query_subsample) : -1};
+    const spl_train_config tc = to_c(cfg);
+    std::vector<double> rec(static_cast<std::size_t>(cfg.num_iters) * 3 + 3);
+    double iou = 0.0;
+    std::uint32_t skipped = 0;
+    auto dim_check = [&](std::uint32_t in_dim) {
+        if (in_dim != d)
+            throw DimensionError("train_hasher: data dimension " + std::to_string(d) +
+                                 " does not match hasher dimension " + std::to_string(in_dim));
+    };
+    spl_status st = SPL_OK;
+    if (auto* m = std::get_if<MlpHasher>(&hasher)) {
+        dim_check(m->input_dim());
+        st = spl_train_hasher(ctx(), SPL_HASHER_MLP, m->input_dim(), m->hidden_dim(), m->code_bits(),
+                              m->gamma, m->w1.data(), m->b1.data(), m->w2.data(),
+                              static_cast<std::uint32_t>(lens.size()), qs.data(), ks.data(),
+                              lens.data(), &rc, &tc, rec.data(), &iou, &skipped, nullptr);
+    } else if (auto* l = std::get_if<LinearHasher>(&hasher)) {
+        dim_check(l->input_dim());
+        st = spl_train_hasher(ctx(), SPL_HASHER_LINEAR, l->input_dim(), 0, l->code_bits(), 0.0f,
+                              l->projection.data(), nullptr, nullptr,
+                              static_cast<std::uint32_t>(lens.size()), qs.data(), ks.data(),
+                              lens.data(), &rc, &tc, rec.data(), &iou, &skipped, nullptr);
+    } else {
+        auto& e = std::get<DownProjEstimator>(hasher);
+        dim_check(e.input_dim());
+        st = spl_train_hasher(ctx(), SPL_HASHER_DOWNPROJ, e.input_dim(), 0, e.reduced_dim(), 0.0f,
+                              e.projection.data(), nullptr, nullptr,
+                              static_cast<std::uint32_t>(lens.size()), qs.data(), ks.data(),
+                              lens.data(), &rc, &tc, rec.data(), &iou, &skipped, nullptr);
+    }
+    check(st);
+    TrainReport report;
+    report.records.reserve(cfg.num_iters);
+    for (std::uint32_t it = 0; it < cfg.num_iters; ++it)
+        report.records.push_back(IterRecord{it, rec[3 * static_cast<std::size_t>(it)],
+                                            rec[3 * static_cast<std::size_t>(it) + 1],
+                                            rec[3 * static_cast<std::size_t>(it) + 2]});
+    report.final_holdout_iou = iou;
+    report.skipped_steps = skipped;
+    report.wall_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    return report;
 }
 
 }  // namespace spotlight

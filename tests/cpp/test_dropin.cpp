@@ -22,6 +22,7 @@
 #include "spotlight/bitcodes.hpp"
 #include "spotlight/errors.hpp"
 #include "spotlight/hashers.hpp"
+#include "spotlight/trainer.hpp"
 
 using namespace spotlight;
 
@@ -369,6 +370,10 @@ struct Ref {
     int (*downproj)(const float*, std::uint32_t, const float*, std::uint32_t, std::uint32_t,
                     const float*, std::uint32_t, const std::uint32_t*, std::uint32_t,
                     std::uint32_t*, std::uint32_t*) = nullptr;
+    int (*train)(int, float*, float*, float*, std::uint32_t, std::uint32_t, std::uint32_t, float,
+                 std::uint32_t, const float*, const float*, const std::uint32_t*, const double*,
+                 const std::uint64_t*, const std::int64_t*, int, double*, double*,
+                 std::uint32_t*) = nullptr;
     int (*evaluate)(const float*, std::uint32_t, const float*, const float*, std::uint32_t,
                     std::uint32_t, float, const std::uint32_t*, double, const float*,
                     const float*, const float*, std::uint32_t, std::uint32_t, const float*,
@@ -383,6 +388,7 @@ struct Ref {
         oracle = reinterpret_cast<decltype(oracle)>(dlsym(h, "spotref_oracle_topk"));
         downproj = reinterpret_cast<decltype(downproj)>(dlsym(h, "spotref_downproj_topk"));
         evaluate = reinterpret_cast<decltype(evaluate)>(dlsym(h, "spotref_evaluate"));
+        train = reinterpret_cast<decltype(train)>(dlsym(h, "spotref_train"));
     }
 };
 
@@ -615,6 +621,151 @@ TEST_CASE("drop-in == reference: mlp_forward, hash_topk, sparse_attention") {
     for (std::size_t i = 0; i < rout.size(); ++i) mx = std::max(mx, (double)std::fabs(rout[i] - sp.data()[i]));
     std::fprintf(stderr, "sparse_attention max-abs vs reference: %.3g\n", mx);
     CHECK(mx <= 1e-5);
+}
+
+// ------------------------------------------------------------ trainer (§8 f4)
+// The reference's test_trainer.cpp cases that exercise train_hasher through
+// the public API (lr schedule, zero-lr identity, determinism, validation,
+// loss trend on cone-shaped data), plus a bit-exact comparison with the
+// reference's own train_hasher when oracle/_ref is present.
+static TrainDataset cone_dataset(std::uint32_t n, std::uint32_t d, std::uint64_t seed) {
+    // queries and keys share a common direction (a cone): retrieval is learnable
+    std::mt19937_64 eng(seed);
+    std::normal_distribution<double> g(0.0, 1.0);
+    std::vector<double> axis(d);
+    for (auto& a : axis) a = g(eng);
+    TrainDataset ds;
+    QkSequence seq{Matrix<float>(n, d), Matrix<float>(n, d)};
+    for (std::uint32_t i = 0; i < n; ++i)
+        for (std::uint32_t c = 0; c < d; ++c) {
+            seq.queries(i, c) = static_cast<float>(0.8 * axis[c] + g(eng));
+            seq.keys(i, c) = static_cast<float>(0.8 * axis[c] + g(eng));
+        }
+    ds.sequences.push_back(std::move(seq));
+    return ds;
+}
+
+TEST_CASE("trainer: lr_at warmup then cosine; TrainConfig validation") {
+    TrainConfig cfg;
+    cfg.num_iters = 100;
+    cfg.warmup_iters = 10;
+    CHECK(lr_at(0, cfg) == 0.0);
+    CHECK(std::fabs(lr_at(5, cfg) - 0.5e-3) < 1e-18);
+    CHECK(lr_at(10, cfg) == cfg.max_lr);
+    CHECK(std::fabs(lr_at(99, cfg) - cfg.min_lr) < 1e-18);
+    TrainConfig bad = cfg;
+    bad.min_lr = 1.0;
+    CHECK_THROWS_AS(bad.validate(), DimensionError);
+    bad = cfg;
+    bad.batch = 0;
+    CHECK_THROWS_AS(bad.validate(), DimensionError);
+}
+
+TEST_CASE("trainer: zero lr leaves the hasher bit-identical; runs are deterministic") {
+    const TrainDataset ds = cone_dataset(160, 32, 5);
+    RankingLossConfig rc;
+    rc.maskout = 0.9;
+    rc.max_oth = 32;
+    rc.query_subsample = 16;
+    TrainConfig cfg;
+    cfg.num_iters = 4;
+    cfg.warmup_iters = 2;
+    cfg.holdout_queries = 16;
+    const MlpHasher h0 = mlp_gaussian_init(32, 32, 32, 64.0f, 3);
+    AnyHasher a = h0;
+    TrainConfig z = cfg;
+    z.max_lr = 0.0;
+    const TrainReport r0 = train_hasher(a, ds, rc, z);
+    const MlpHasher& az = std::get<MlpHasher>(a);
+    CHECK(std::memcmp(az.w1.data(), h0.w1.data(), h0.w1.size() * 4) == 0);
+    CHECK(std::memcmp(az.w2.data(), h0.w2.data(), h0.w2.size() * 4) == 0);
+    CHECK(r0.records.size() == 4 && r0.skipped_steps == 0);
+    AnyHasher b1 = h0, b2 = h0;
+    const TrainReport ra = train_hasher(b1, ds, rc, cfg);
+    const TrainReport rb = train_hasher(b2, ds, rc, cfg);
+    CHECK(std::memcmp(std::get<MlpHasher>(b1).w1.data(), std::get<MlpHasher>(b2).w1.data(),
+                      h0.w1.size() * 4) == 0);
+    CHECK(format_train_report(ra, {}) == format_train_report(rb, {}));
+    CHECK(std::memcmp(std::get<MlpHasher>(b1).w1.data(), h0.w1.data(), h0.w1.size() * 4) != 0);
+}
+
+TEST_CASE("trainer: input validation mirrors the reference") {
+    RankingLossConfig rc;
+    TrainConfig cfg;
+    cfg.num_iters = 1;
+    AnyHasher a = mlp_gaussian_init(16, 16, 32, 64.0f, 1);
+    TrainDataset empty;
+    CHECK_THROWS_WITH(train_hasher(a, empty, rc, cfg), DimensionError, "dataset is empty");
+    TrainDataset mis;
+    mis.sequences.push_back(QkSequence{Matrix<float>(8, 16), Matrix<float>(9, 16)});
+    CHECK_THROWS_WITH(train_hasher(a, mis, rc, cfg), DimensionError, "causally aligned");
+    TrainDataset wrong = cone_dataset(64, 8, 1);
+    CHECK_THROWS_WITH(train_hasher(a, wrong, rc, cfg), DimensionError, "does not match hasher dimension");
+    TrainDataset tiny = cone_dataset(20, 16, 1);  // floor(20 * 0.02) = 0 top keys
+    CHECK_THROWS_WITH(train_hasher(a, tiny, rc, cfg), DimensionError, "top count floored to zero");
+}
+
+TEST_CASE("trainer: loss trends downward on cone data") {
+    const TrainDataset ds = cone_dataset(512, 64, 17);
+    RankingLossConfig rc;
+    rc.max_oth = 64;
+    rc.query_subsample = 32;
+    TrainConfig cfg;
+    cfg.num_iters = 200;
+    cfg.warmup_iters = 10;
+    cfg.max_lr = 3e-3;
+    AnyHasher a = mlp_gaussian_init(64, 64, 64, 64.0f, 8);
+    const TrainReport r = train_hasher(a, ds, rc, cfg);
+    double first = 0, last = 0;
+    for (int i = 0; i < 20; ++i) {
+        first += r.records[i].loss;
+        last += r.records[r.records.size() - 1 - i].loss;
+    }
+    std::fprintf(stderr, "trainer loss first20 %.4f last20 %.4f holdout IoU %.4f\n", first / 20,
+                 last / 20, r.final_holdout_iou);
+    CHECK(last < first);
+}
+
+TEST_CASE("trainer: drop-in == reference train_hasher (bit-identical weights)") {
+    static Ref ref;
+    if (!ref.h || !ref.train) {
+        std::fprintf(stderr, "note: oracle/_ref/libspotref.so not present, reference diff skipped\n");
+        return;
+    }
+    const TrainDataset ds = cone_dataset(300, 64, 23);
+    RankingLossConfig rc;
+    rc.max_oth = 48;
+    rc.query_subsample = 20;
+    TrainConfig cfg;
+    cfg.num_iters = 12;
+    cfg.warmup_iters = 3;
+    cfg.seed = 77;
+    cfg.holdout_queries = 40;
+    MlpHasher h0 = mlp_gaussian_init(64, 96, 64, 64.0f, 12);
+    AnyHasher a = h0;
+    const TrainReport r = train_hasher(a, ds, rc, cfg);
+    const double dc[12] = {cfg.max_lr, cfg.min_lr, cfg.adam_beta1, cfg.adam_beta2, cfg.adam_eps,
+                           cfg.weight_decay, cfg.grad_clip, cfg.soft_gamma, cfg.holdout_budget_rate,
+                           rc.beta, rc.alpha, rc.maskout};
+    const std::uint64_t uc[5] = {cfg.num_iters, cfg.warmup_iters, cfg.batch, cfg.seed,
+                                 cfg.holdout_queries};
+    const std::int64_t op[3] = {-1, 48, 20};
+    std::vector<double> rec(3 * cfg.num_iters);
+    double iou = 0;
+    std::uint32_t sk = 0, len = 300;
+    CHECK(ref.train(1, h0.w1.data(), h0.b1.data(), h0.w2.data(), 64, 96, 64, 64.0f, 1,
+                    ds.sequences[0].queries.data(), ds.sequences[0].keys.data(), &len, dc, uc, op,
+                    0, rec.data(), &iou, &sk) == 0);
+    const MlpHasher& g = std::get<MlpHasher>(a);
+    CHECK(std::memcmp(g.w1.data(), h0.w1.data(), h0.w1.size() * 4) == 0);
+    CHECK(std::memcmp(g.b1.data(), h0.b1.data(), h0.b1.size() * 4) == 0);
+    CHECK(std::memcmp(g.w2.data(), h0.w2.data(), h0.w2.size() * 4) == 0);
+    CHECK(r.final_holdout_iou == iou);
+    for (std::uint32_t i = 0; i < cfg.num_iters; ++i) {
+        CHECK(r.records[i].lr == rec[3 * i + 2]);
+        CHECK(r.records[i].violation_rate == rec[3 * i + 1]);
+        CHECK(std::fabs(r.records[i].loss - rec[3 * i]) <= 1e-10 * std::fabs(rec[3 * i]));
+    }
 }
 
 int main() {
