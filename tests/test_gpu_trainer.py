@@ -151,3 +151,26 @@ def _ref_ok(ref, w, data, rank, sd):
         return True
     except CheckerError:
         return False
+
+
+@pytest.mark.parametrize("clip,wd,min_lr", [(1e-4, 0.1, 0.0), (0.0, 0.0, 2e-4), (0.05, 0.3, 1e-4)])
+def test_train_clip_decay_schedule_variants(ctx, clip, wd, min_lr):
+    """Clipping active on every step (tiny bound), clipping disabled, no weight
+    decay, a non-zero final lr: the optimiser paths of trainer.cpp:83-143."""
+    ref = RefLib()
+    w = ref.mlp_gaussian_init(64, 64, 64, 64.0, 21)
+    data = seqs(8, [256], 64)
+    cfg = dict(CFG, grad_clip=clip, weight_decay=wd, min_lr=min_lr, num_iters=10, warmup_iters=3)
+    r, g = run_pair(ctx, 1, w, data, RANK, cfg)
+    compare(r, g, f"clip={clip} wd={wd} min_lr={min_lr}")
+
+
+def test_train_longer_run_stays_identical(ctx):
+    """60 iterations at the CLI's pair-set sizes: the double exp / log1p and
+    the reduction-order differences never reach the float weights."""
+    ref = RefLib()
+    w = ref.mlp_gaussian_init(128, 128, 128, 64.0, ref.derive_seed(3, 100))
+    data = seqs(9, [1024], 128)
+    cfg = dict(CFG, num_iters=60, warmup_iters=6, seed=5)
+    r, g = run_pair(ctx, 1, w, data, RANK, cfg)
+    assert compare(r, g, "60 iters n=1024")
