@@ -65,7 +65,7 @@ struct TrainDev {
     uint32_t step;          // AdamW step (applied updates)
     uint32_t skipped;       // non-finite gradient steps
     uint32_t skip_now;      // this iteration's gradients are non-finite
-    uint32_t pad;
+    float scale;            // this iteration's clipping factor
     double bc1, bc2;        // this iteration's bias corrections
     double loss_acc, viol_acc;
     unsigned long long pairs;  // valid pairs of the current (iteration, batch) element
@@ -465,10 +465,16 @@ __global__ void __launch_bounds__(256) k_rank_grad(const float* __restrict__ sof
     for (uint32_t i = threadIdx.x; i < T; i += blockDim.x) gsum[i] = 0.0;  // running chains
     for (uint32_t j0 = 0; j0 < O; j0 += 32) {
         const uint32_t w = min(32u, O - j0);
-        for (uint32_t e = threadIdx.x; e < T * 32; e += blockDim.x) {
+        for (uint32_t e = threadIdx.x; e < T * 32; e += blockDim.x) {  // async, zero-filled
             const uint32_t i = e >> 5, jj = e & 31;
-            tile[i * 33 + jj] = jj < w ? g[(uint64_t)i * O + j0 + jj] : 0.0;
+            const bool ok = jj < w;
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(
+                             (uint32_t)__cvta_generic_to_shared(tile + i * 33 + jj)),
+                         "l"(ok ? g + (uint64_t)i * O + j0 + jj : g), "r"(ok ? 8 : 0)
+                         : "memory");
         }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+        asm volatile("cp.async.wait_group 0;" ::: "memory");
         __syncthreads();
         for (uint32_t i = threadIdx.x; i < T; i += blockDim.x) {
             double acc = gsum[i];
@@ -529,12 +535,12 @@ __global__ void __launch_bounds__(256) k_rank_grad(const float* __restrict__ sof
     for (uint32_t p = threadIdx.x; p < L; p += blockDim.x) {
         float dq = 0.0f;
         uint32_t e = 0;
-        for (; e + 8 <= ne; e += 8) {
-            float v[8];
+        for (; e + 32 <= ne; e += 32) {  // 32 row loads in flight ahead of the chain
+            float v[32];
 #pragma unroll
-            for (int u = 0; u < 8; ++u) v[u] = __ldg(softk + (uint64_t)ek[e + u] * L + p);
+            for (int u = 0; u < 32; ++u) v[u] = __ldg(softk + (uint64_t)ek[e + u] * L + p);
 #pragma unroll
-            for (int u = 0; u < 8; ++u) dq = __fmaf_rn(eg[e + u], v[u], dq);
+            for (int u = 0; u < 32; ++u) dq = __fmaf_rn(eg[e + u], v[u], dq);
         }
         for (; e < ne; ++e) dq = __fmaf_rn(eg[e], softk[(uint64_t)ek[e] * L + p], dq);
         dsq[(uint64_t)qi * L + p] = dq;
@@ -642,11 +648,25 @@ __global__ void k_dz(const float* __restrict__ dsoft, const float* __restrict__ 
 constexpr int kAtRows = 128;   // rows per stage
 constexpr int kAtStages = 4;   // cp.async ring depth (3 stages in flight)
 constexpr size_t kAtSmem = (size_t)kAtStages * kAtRows * 36 * 4;
-__global__ void __launch_bounds__(128) k_add_at(const float* __restrict__ A,
-                                                const float* __restrict__ B, uint32_t rows,
-                                                uint32_t m, uint32_t nc, float* __restrict__ C,
-                                                float* __restrict__ b1, const TrainDev* st) {
+struct AtJob {
+    const float* A;
+    const float* B;
+    float* C;
+    float* b1;  // optional column sums of B
+    uint32_t m, nc;
+};
+// blockIdx.z selects one of two independent products over the same rows (the
+// W2 and W1 gradients of one backward pass run side by side)
+__global__ void __launch_bounds__(128) k_add_at(AtJob j0, AtJob j1, uint32_t rows,
+                                                const TrainDev* st) {
     if (st->halt) return;
+    const AtJob& jb = blockIdx.z ? j1 : j0;
+    const float* __restrict__ A = jb.A;
+    const float* __restrict__ B = jb.B;
+    float* __restrict__ C = jb.C;
+    float* __restrict__ b1 = jb.b1;
+    const uint32_t m = jb.m, nc = jb.nc;
+    if (blockIdx.x * 32 >= nc || blockIdx.y * 4 >= m) return;
     extern __shared__ float at_sm[];  // [stage][kAtRows][4] A, then [stage][kAtRows][32] B
     float* as = at_sm;
     float* bs = at_sm + kAtStages * kAtRows * 4;
@@ -784,53 +804,60 @@ __global__ void __launch_bounds__(128) k_da1(const float* __restrict__ dz2,
 
 // ------------------------------------------------------------ optimiser
 // clip_gradient_norm (trainer.cpp:83-97) + adamw_step's finiteness check and
-// bias corrections (:114-121). One block; deterministic tree sum.
-__global__ void __launch_bounds__(1024) k_clip(float* g, uint64_t n, double max_norm,
-                                               const double* bc1_tab, const double* bc2_tab,
-                                               TrainDev* st) {
+// bias corrections (:114-121): per-block partial sums of squares (fixed
+// order) and non-finite flags, then one small block combines them in order.
+// Non-finite after clipping <=> non-finite before (scale <= 1; an infinite
+// norm scales finite entries to 0 and infinite ones to NaN), so the flag is
+// taken on the raw gradients; k_adamw applies the scale (g * scale, float, as
+// the reference's in-place multiply).
+constexpr int kNormBlocks = 64;
+__global__ void __launch_bounds__(256) k_norm_partial(const float* g, uint64_t n, double* part,
+                                                      int* bad, const TrainDev* st) {
     if (st->halt) return;
-    __shared__ double s[32];
-    __shared__ float s_scale;
+    __shared__ double s[8];
     __shared__ int s_bad;
+    if (threadIdx.x == 0) s_bad = 0;
+    __syncthreads();
     double acc = 0.0;
-    for (uint64_t i = threadIdx.x; i < n; i += blockDim.x) {
-        const double v = (double)g[i];
+    int b = 0;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        const float f = g[i];
+        const double v = (double)f;
         acc = __fma_rn(v, v, acc);
+        b |= !isfinite(f);
     }
     for (int o = 16; o; o >>= 1) acc = __dadd_rn(acc, __shfl_xor_sync(~0u, acc, o));
     if ((threadIdx.x & 31) == 0) s[threadIdx.x >> 5] = acc;
-    if (threadIdx.x == 0) s_bad = 0;
+    if (b) s_bad = 1;
     __syncthreads();
     if (threadIdx.x == 0) {
         double t = 0.0;
-        for (uint32_t w = 0; w < blockDim.x / 32; ++w) t = __dadd_rn(t, s[w]);
-        const double norm = __dsqrt_rn(t);
-        s_scale = (max_norm > 0.0 && norm > max_norm) ? __double2float_rn(__ddiv_rn(max_norm, norm))
-                                                      : 1.0f;
+        for (int w = 0; w < 8; ++w) t = __dadd_rn(t, s[w]);
+        part[blockIdx.x] = t;
+        bad[blockIdx.x] = s_bad;
     }
-    __syncthreads();
-    const float sc = s_scale;
-    int bad = 0;
-    for (uint64_t i = threadIdx.x; i < n; i += blockDim.x) {
-        float v = g[i];
-        if (sc != 1.0f) {
-            v = __fmul_rn(v, sc);
-            g[i] = v;
-        }
-        bad |= !isfinite(v);
+}
+
+__global__ void k_clip(const double* part, const int* bad, double max_norm, const double* bc1_tab,
+                       const double* bc2_tab, TrainDev* st) {
+    if (st->halt) return;
+    double t = 0.0;
+    int b = 0;
+    for (int i = 0; i < kNormBlocks; ++i) {
+        t = __dadd_rn(t, part[i]);
+        b |= bad[i];
     }
-    if (bad) s_bad = 1;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        if (s_bad) {
-            st->skip_now = 1;
-            st->skipped += 1;
-        } else {
-            st->skip_now = 0;
-            st->step += 1;
-            st->bc1 = bc1_tab[st->step];
-            st->bc2 = bc2_tab[st->step];
-        }
+    const double norm = __dsqrt_rn(t);
+    st->scale = (max_norm > 0.0 && norm > max_norm) ? __double2float_rn(__ddiv_rn(max_norm, norm)) : 1.0f;
+    if (b) {
+        st->skip_now = 1;
+        st->skipped += 1;
+    } else {
+        st->skip_now = 0;
+        st->step += 1;
+        st->bc1 = bc1_tab[st->step];
+        st->bc2 = bc2_tab[st->step];
     }
 }
 
@@ -843,9 +870,10 @@ __global__ void k_adamw(float* w, const float* g, double* m1, double* m2, uint64
     const double bc1 = st->bc1, bc2 = st->bc2;
     const double c1 = __dsub_rn(1.0, b1), c2 = __dsub_rn(1.0, b2);
     const double lwd = __dmul_rn(lr, wd);
+    const float sc = st->scale;
     for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
          i += (uint64_t)gridDim.x * blockDim.x) {
-        const double gv = (double)g[i];
+        const double gv = (double)(sc != 1.0f ? __fmul_rn(g[i], sc) : g[i]);
         const double m = __fma_rn(b1, m1[i], __dmul_rn(c1, gv));
         const double v = __fma_rn(b2, m2[i], __dmul_rn(__dmul_rn(c2, gv), gv));
         m1[i] = m;
@@ -1120,7 +1148,9 @@ spl_status train_impl(spl_ctx* ctx, int kind, uint32_t d, uint32_t h, uint32_t L
     }
     double* dbc1 = db.get<double>(iters + 2);
     double* dbc2 = db.get<double>(iters + 2);
-    if (!dbc1 || !dbc2) return fail(ctx, SPL_E_CUDA, "train: out of device memory");
+    double* npart = db.get<double>(kNormBlocks);
+    int* nbad = db.get<int>(kNormBlocks);
+    if (!dbc1 || !dbc2 || !npart || !nbad) return fail(ctx, SPL_E_CUDA, "train: out of device memory");
     SPL_CUDA_TRY(ctx, cudaMemcpyAsync(dbc1, bc1.data(), bc1.size() * 8, cudaMemcpyHostToDevice, s));
     SPL_CUDA_TRY(ctx, cudaMemcpyAsync(dbc2, bc2.data(), bc2.size() * 8, cudaMemcpyHostToDevice, s));
 
@@ -1242,14 +1272,17 @@ spl_status train_impl(spl_ctx* ctx, int kind, uint32_t d, uint32_t h, uint32_t L
             dzp = dz;
         }
         if (mlp) {
-            k_add_at<<<dim3((L + 31) / 32, (h + 3) / 4), 128, kAtSmem, s>>>(a1, dzp, m, h, L, gW2, nullptr, dst);
-            if (spl_status st = after_launch(ctx, "k_add_at")) return st;
+            // da1 first, then W2 += a1^T dz2 and W1 += x^T da1 (+ b1) in one
+            // launch: independent accumulators, so the order between them is free
             k_da1<<<(m + kDaRows - 1) / kDaRows, 128, da1_smem, s>>>(dzp, W2, z1, m, h, L, da1, dst);
             if (spl_status st = after_launch(ctx, "k_da1")) return st;
-            k_add_at<<<dim3((h + 31) / 32, (d + 3) / 4), 128, kAtSmem, s>>>(x, da1, m, d, h, gW1, gB1, dst);
+            const AtJob jw2{a1, dzp, gW2, nullptr, h, L}, jw1{x, da1, gW1, gB1, d, h};
+            const dim3 grid((std::max(L, h) + 31) / 32, (std::max(h, d) + 3) / 4, 2);
+            k_add_at<<<grid, 128, kAtSmem, s>>>(jw2, jw1, m, dst);
             return after_launch(ctx, "k_add_at");
         }
-        k_add_at<<<dim3((L + 31) / 32, (d + 3) / 4), 128, kAtSmem, s>>>(x, dzp, m, d, L, gW1, nullptr, dst);
+        const AtJob jp{x, dzp, gW1, nullptr, d, L};
+        k_add_at<<<dim3((L + 31) / 32, (d + 3) / 4, 1), 128, kAtSmem, s>>>(jp, jp, m, dst);
         return after_launch(ctx, "k_add_at");
     };
     const float invb = tc.batch > 1 ? (float)(1.0 / tc.batch) : 1.0f;
@@ -1311,7 +1344,9 @@ spl_status train_impl(spl_ctx* ctx, int kind, uint32_t d, uint32_t h, uint32_t L
             if (spl_status st = bwd(xg, Qs, z1q, a1q, z2q, dsq)) return st;
             if (spl_status st = bwd(p.x_k, n, z1k, a1k, z2k, dsk)) return st;
         }
-        k_clip<<<1, 1024, 0, s>>>(dG, np, tc.grad_clip, dbc1, dbc2, dst);
+        k_norm_partial<<<kNormBlocks, 256, 0, s>>>(dG, np, npart, nbad, dst);
+        if (spl_status st = after_launch(ctx, "k_norm_partial")) return st;
+        k_clip<<<1, 1, 0, s>>>(npart, nbad, tc.grad_clip, dbc1, dbc2, dst);
         if (spl_status st = after_launch(ctx, "k_clip")) return st;
         k_adamw<<<(unsigned)std::min<uint64_t>((np + 255) / 256, 1184), 256, 0, s>>>(
             dP, dG, dM, dV, np, n1, n1 + nb, lr, tc.adam_beta1, tc.adam_beta2, tc.adam_eps,
