@@ -292,7 +292,7 @@ spl_status spl_budget_from_rate(double rate, uint64_t n, uint32_t* k);
  * Hasher training. Mirrors spotlight::train_hasher
  * (trainer.hpp:115-118, trainer.cpp:634-645): RankingLossConfig
  * (ranking_loss.hpp:15-24; optional counts < 0 = unset) and TrainConfig
- * (trainer.hpp:18-37). Loss: pairwise ranking (TrainLoss::ranking). */
+ * (trainer.hpp:18-37); loss_kind = TrainLoss (trainer.hpp:82). */
 typedef struct spl_rank_config {
     double beta, alpha, maskout;
     int64_t max_top, max_oth, query_subsample; /* < 0: unset (std::nullopt) */
@@ -311,12 +311,16 @@ typedef struct spl_train_config {
  * many key rows (causally aligned). records: [num_iters][3] = {loss,
  * violation_rate, lr} (IterRecord, trainer.hpp:84-89). Sequences are limited
  * to 16384 keys (per-row order sort in shared memory). */
+typedef enum spl_train_loss {
+    SPL_TRAIN_LOSS_RANKING = 0,        /* TrainLoss::ranking */
+    SPL_TRAIN_LOSS_RECONSTRUCTION = 1  /* TrainLoss::reconstruction (MSE ablation) */
+} spl_train_loss;
 spl_status spl_train_hasher(spl_ctx* ctx, int kind, uint32_t d, uint32_t h, uint32_t L,
                             float gamma, float* w1, float* b1, float* w2, uint32_t n_seq,
                             const float* queries, const float* keys, const uint32_t* seq_len,
                             const spl_rank_config* rank, const spl_train_config* train,
-                            double* records, double* holdout_iou, uint32_t* skipped,
-                            void* stream);
+                            int loss_kind, double* records, double* holdout_iou,
+                            uint32_t* skipped, void* stream);
 /* partition_topk's draws (ranking_loss.cpp:80-116), host only: rows
  * [min(query_subsample, q_train)], top positions [min(max_top, k_full)], other
  * positions relative to k_full [min(max_oth, n - k_full)]; counts = {rows,

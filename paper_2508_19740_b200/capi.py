@@ -115,8 +115,8 @@ _SIGS = {
     "spl_peer_connect_local": [vp, C.POINTER(vp), u32],
     "spl_peer_destroy": [vp],
     "spl_hamming_topk_sharded": [vp, vp, vp, u64, u32, vp, u32, vp, u32, u64, u32, vp, vp, vp, vp],
-    "spl_train_hasher": [vp, i32, u32, u32, u32, f32, vp, vp, vp, u32, vp, vp, vp, vp, vp, vp,
-                         C.POINTER(dbl), u32p, vp],
+    "spl_train_hasher": [vp, i32, u32, u32, u32, f32, vp, vp, vp, u32, vp, vp, vp, vp, vp, i32,
+                         vp, C.POINTER(dbl), u32p, vp],
     "spl_train_partition_host": [vp, u32, u32, u64, vp, vp, vp, vp],
     "spl_train_lr_at": [u32, vp],
     "spl_train_last_loop_ms": [vp],
@@ -321,7 +321,7 @@ class Context:
 
     # -- training
     def train_hasher(self, kind, d, h, L, gamma, w1, b1, w2, sequences, rank: RankConfig,
-                     cfg: TrainConfig, stream=None):
+                     cfg: TrainConfig, loss_kind: int = 0, stream=None):
         """train_hasher (trainer.cpp:634-645) on the GPU. w1/b1/w2: float32 numpy
         arrays updated in place (b1/w2 None for linear / downproj); sequences:
         list of (queries, keys) float32 [n][d]. Returns dict(records [iters][3]
@@ -344,7 +344,7 @@ class Context:
             self.h, kind, d, h, L, gamma, w1.ctypes.data,
             None if b1 is None else b1.ctypes.data, None if w2 is None else w2.ctypes.data,
             len(sequences), qs.ctypes.data, ks.ctypes.data, lens.ctypes.data, C.byref(rank),
-            C.byref(cfg), rec.ctypes.data, C.byref(iou), C.byref(sk), _stream(stream)))
+            C.byref(cfg), loss_kind, rec.ctypes.data, C.byref(iou), C.byref(sk), _stream(stream)))
         return {"records": rec[:cfg.num_iters], "holdout_iou": iou.value,
                 "skipped_steps": sk.value,
                 "loop_ms": self.lib.spl_train_last_loop_ms(self.h)}

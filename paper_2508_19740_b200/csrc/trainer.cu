@@ -548,15 +548,86 @@ __global__ void __launch_bounds__(256) k_rank_grad(const float* __restrict__ sof
     for (uint32_t e = threadIdx.x; e < ne; e += blockDim.x) G[(uint64_t)ek[e] * Qs + qi] = eg[e];
 }
 
+// ------------------------------------------------------------ reconstruction loss
+// recon_soft_loss (trainer.cpp:383-419): draft = matmul_bt(soft_q, soft_k)
+// (rounded products in order, fused tail), diff = draft - true logit over
+// the causal range, loss = sum diff^2 / count, g = float(2 / count * diff);
+// d soft_q = matmul(g, soft_k) (one fma chain over the keys), d soft_k +=
+// g^T soft_q (k_dsoft_keys over G[key][qi] = g[qi][key]).
+__global__ void __launch_bounds__(256) k_recon(const float* __restrict__ softq,
+                                               const float* __restrict__ softk, uint32_t L,
+                                               const float* __restrict__ logits, uint32_t n,
+                                               const uint32_t* qrows, uint32_t Qs, double scale,
+                                               float* G, double* loss_part, const TrainDev* st) {
+    if (st->halt) return;
+    extern __shared__ float sq[];  // [L]
+    __shared__ double s_l[8];
+    const uint32_t qi = blockIdx.x;
+    const uint32_t row = qrows[qi];
+    const uint32_t valid = min(row + 1, n);
+    for (uint32_t p = threadIdx.x; p < L; p += blockDim.x) sq[p] = softq[(uint64_t)qi * L + p];
+    __syncthreads();
+    const uint32_t n4 = n4_of(L);
+    double loss = 0.0;
+    for (uint32_t j = blockIdx.y * blockDim.x + threadIdx.x; j < valid; j += gridDim.y * blockDim.x) {
+        const float* sk = softk + (uint64_t)j * L;
+        float acc = 0.0f;
+        uint32_t p = 0;
+        for (; p < n4; ++p) acc = __fadd_rn(acc, __fmul_rn(sq[p], __ldg(sk + p)));
+        for (; p < L; ++p) acc = __fmaf_rn(sq[p], __ldg(sk + p), acc);
+        const double diff = __dsub_rn((double)acc, (double)logits[(uint64_t)row * n + j]);
+        loss = __fma_rn(diff, diff, loss);
+        G[(uint64_t)j * Qs + qi] = __double2float_rn(__dmul_rn(scale, diff));
+    }
+    for (int o = 16; o; o >>= 1) loss = __dadd_rn(loss, __shfl_xor_sync(~0u, loss, o));
+    if ((threadIdx.x & 31) == 0) s_l[threadIdx.x >> 5] = loss;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double a = 0.0;
+        for (int w = 0; w < 8; ++w) a = __dadd_rn(a, s_l[w]);
+        loss_part[(uint64_t)qi * gridDim.y + blockIdx.y] = a;
+    }
+}
+
+__global__ void __launch_bounds__(128) k_recon_dq(const float* __restrict__ G,
+                                                  const float* __restrict__ softk, uint32_t L,
+                                                  uint32_t n, const uint32_t* qrows, uint32_t Qs,
+                                                  float invb, float* __restrict__ dsq,
+                                                  const TrainDev* st) {
+    if (st->halt) return;
+    const uint32_t qi = blockIdx.x;
+    const uint32_t valid = min(qrows[qi] + 1, n);
+    for (uint32_t p = threadIdx.x; p < L; p += blockDim.x) {
+        float dq = 0.0f;
+        uint32_t j = 0;
+        for (; j + 16 <= valid; j += 16) {
+            float gv[16], kv[16];
+#pragma unroll
+            for (int u = 0; u < 16; ++u) {
+                gv[u] = G[(uint64_t)(j + u) * Qs + qi];
+                kv[u] = __ldg(softk + (uint64_t)(j + u) * L + p);
+            }
+#pragma unroll
+            for (int u = 0; u < 16; ++u)
+                if (gv[u] != 0.0f) dq = __fmaf_rn(gv[u], kv[u], dq);
+        }
+        for (; j < valid; ++j) {
+            const float g = G[(uint64_t)j * Qs + qi];
+            if (g != 0.0f) dq = __fmaf_rn(g, softk[(uint64_t)j * L + p], dq);
+        }
+        dsq[(uint64_t)qi * L + p] = invb != 1.0f ? __fmul_rn(dq, invb) : dq;
+    }
+}
+
 // loss = sum of the query partials * inv_pairs; non-finite -> NumericError
 // (trainer.cpp:587-590); accumulates the iteration record over the batch.
 __global__ void k_loss_finalize(const double* loss_part, const unsigned long long* viol_part,
                                 uint32_t nparts, uint32_t b, uint32_t batch, uint32_t iter,
-                                double* rec, TrainDev* st) {
+                                double* rec, TrainDev* st, double recon_count) {
     if (st->halt) return;
     __shared__ double s_l[256];
     __shared__ unsigned long long s_v[256];
-    const double inv = __ddiv_rn(1.0, (double)st->pairs);
+    const double inv = st->pairs ? __ddiv_rn(1.0, (double)st->pairs) : 0.0;
     double a = 0.0;
     unsigned long long c = 0;
     for (uint32_t q = threadIdx.x; q < nparts; q += blockDim.x) {  // fixed order per thread
@@ -576,7 +647,10 @@ __global__ void k_loss_finalize(const double* loss_part, const unsigned long lon
     if (threadIdx.x) return;
     const double s = s_l[0];
     const unsigned long long v = s_v[0];
-    const double loss = __dmul_rn(s, inv), vr = __dmul_rn((double)v, inv);
+    // ranking: sums x (1 / valid pairs) (trainer.cpp:377-379); reconstruction:
+    // MSE = sum / count, no violation rate (trainer.cpp:383-419, :571-586)
+    const double loss = recon_count > 0.0 ? __ddiv_rn(s, recon_count) : __dmul_rn(s, inv);
+    const double vr = recon_count > 0.0 ? 0.0 : __dmul_rn((double)v, inv);
     if (!isfinite(loss)) {
         st->halt = HALT_NONFINITE;
         st->halt_iter = iter;
@@ -1058,8 +1132,8 @@ spl_status holdout_iou_impl(spl_ctx* ctx, int kind, uint32_t d, uint32_t h, uint
 spl_status train_impl(spl_ctx* ctx, int kind, uint32_t d, uint32_t h, uint32_t L, float gamma,
                       float* w1, float* b1, float* w2, uint32_t n_seq, const float* queries,
                       const float* keys, const uint32_t* seq_len, const spl_rank_config& rc,
-                      const spl_train_config& tc, double* records, double* holdout_iou,
-                      uint32_t* skipped, cudaStream_t s) {
+                      const spl_train_config& tc, bool recon, double* records,
+                      double* holdout_iou, uint32_t* skipped, cudaStream_t s) {
     // TrainConfig::validate (trainer.cpp:19-33)
     if (tc.max_lr < 0.0 || tc.min_lr < 0.0 || tc.min_lr > tc.max_lr)
         return fail(ctx, SPL_E_DIMENSION, "TrainConfig: need 0 <= min_lr <= max_lr");
@@ -1319,21 +1393,36 @@ spl_status train_impl(spl_ctx* ctx, int kind, uint32_t d, uint32_t h, uint32_t L
             if (spl_status st = after_launch(ctx, "k_partition")) return st;
             if (spl_status st = fwd(p.x_q, qrows, Qs, z1q, a1q, z2q, sfq)) return st;
             if (spl_status st = fwd(p.x_k, nullptr, n, z1k, a1k, z2k, sfk)) return st;
-            k_rank_dots<<<dim3(Qs, (T + O + 127) / 128), 128, (size_t)L * 4, s>>>(
-                sfq, sfk, L, top_idx, T, oth_idx, O, bcv, dst, it);
-            if (spl_status st = after_launch(ctx, "k_rank_dots")) return st;
-            const uint32_t pb = (uint32_t)(((uint64_t)T * O + kPairThreads - 1) / kPairThreads);
-            k_rank_pairs<<<dim3(Qs, pb), kPairThreads, 0, s>>>(bcv, top_idx, T, oth_idx, O, rc.beta,
-                                                                rc.alpha, gpair, lpart, vpart, dst);
-            if (spl_status st = after_launch(ctx, "k_rank_pairs")) return st;
-            k_rank_grad<<<Qs, 256, (size_t)(T + O) * 16 + (size_t)T * 33 * 8, s>>>(sfk, L, top_idx, T, oth_idx, O, Qs,
-                                                               gpair, Gm, dsq, dst);
-            if (spl_status st = after_launch(ctx, "k_rank_grad")) return st;
-            k_loss_finalize<<<1, 256, 0, s>>>(lpart, vpart, Qs * pb, b, tc.batch, it, drec, dst);
-            if (spl_status st = after_launch(ctx, "k_loss_finalize")) return st;
+            if (!recon) {
+                k_rank_dots<<<dim3(Qs, (T + O + 127) / 128), 128, (size_t)L * 4, s>>>(
+                    sfq, sfk, L, top_idx, T, oth_idx, O, bcv, dst, it);
+                if (spl_status st = after_launch(ctx, "k_rank_dots")) return st;
+                const uint32_t pb = (uint32_t)(((uint64_t)T * O + kPairThreads - 1) / kPairThreads);
+                k_rank_pairs<<<dim3(Qs, pb), kPairThreads, 0, s>>>(bcv, top_idx, T, oth_idx, O, rc.beta,
+                                                                    rc.alpha, gpair, lpart, vpart, dst);
+                if (spl_status st = after_launch(ctx, "k_rank_pairs")) return st;
+                k_rank_grad<<<Qs, 256, (size_t)(T + O) * 16 + (size_t)T * 33 * 8, s>>>(
+                    sfk, L, top_idx, T, oth_idx, O, Qs, gpair, Gm, dsq, dst);
+                if (spl_status st = after_launch(ctx, "k_rank_grad")) return st;
+                k_loss_finalize<<<1, 256, 0, s>>>(lpart, vpart, Qs * pb, b, tc.batch, it, drec, dst, 0.0);
+                if (spl_status st = after_launch(ctx, "k_loss_finalize")) return st;
+            } else {
+                // count = sum over the selected rows of their causal offsets
+                double count = 0.0;
+                for (uint32_t r : w.qrows) count += (double)std::min(r + 1, n);
+                const uint32_t yb = std::min<uint32_t>((n + 255) / 256, (uint32_t)pair_blocks);
+                k_recon<<<dim3(Qs, yb), 256, (size_t)L * 4, s>>>(sfq, sfk, L, p.logits, n, qrows, Qs,
+                                                                 2.0 / count, Gm, lpart, dst);
+                if (spl_status st = after_launch(ctx, "k_recon")) return st;
+                k_recon_dq<<<Qs, 128, 0, s>>>(Gm, sfk, L, n, qrows, Qs, invb, dsq, dst);
+                if (spl_status st = after_launch(ctx, "k_recon_dq")) return st;
+                SPL_CUDA_TRY(ctx, cudaMemsetAsync(vpart, 0, (size_t)Qs * yb * 8, s));
+                k_loss_finalize<<<1, 256, 0, s>>>(lpart, vpart, Qs * yb, b, tc.batch, it, drec, dst, count);
+                if (spl_status st = after_launch(ctx, "k_loss_finalize")) return st;
+            }
             k_dsoft_keys<<<(unsigned)(((uint64_t)n * L + 255) / 256), 256, 0, s>>>(Gm, sfq, Qs, n, L, invb, dsk, dst);
             if (spl_status st = after_launch(ctx, "k_dsoft_keys")) return st;
-            if (invb != 1.0f) {
+            if (invb != 1.0f && !recon) {
                 k_scale<<<(Qs * L + 255) / 256, 256, 0, s>>>(dsq, (uint64_t)Qs * L, invb, dst);
                 if (spl_status st = after_launch(ctx, "k_scale")) return st;
             }
@@ -1407,8 +1496,9 @@ extern "C" spl_status spl_train_hasher(spl_ctx* ctx, int kind, uint32_t d, uint3
                                        float gamma, float* w1, float* b1, float* w2,
                                        uint32_t n_seq, const float* queries, const float* keys,
                                        const uint32_t* seq_len, const spl_rank_config* rank,
-                                       const spl_train_config* train, double* records,
-                                       double* holdout_iou, uint32_t* skipped, void* stream) {
+                                       const spl_train_config* train, int loss_kind,
+                                       double* records, double* holdout_iou, uint32_t* skipped,
+                                       void* stream) {
     if (!ctx) return SPL_E_STATE;
     if (!rank || !train || !w1 || (kind == SPL_HASHER_MLP && (!b1 || !w2)) ||
         (n_seq && (!queries || !keys || !seq_len)))
@@ -1419,9 +1509,11 @@ extern "C" spl_status spl_train_hasher(spl_ctx* ctx, int kind, uint32_t d, uint3
         return spl::fail(ctx, SPL_E_DIMENSION, "train_hasher: dimensions must be >= 1");
     if (kind != SPL_HASHER_DOWNPROJ && L % 32 != 0)
         return spl::fail(ctx, SPL_E_DIMENSION, "train_hasher: code bits must be a multiple of 32");
+    if (loss_kind != SPL_TRAIN_LOSS_RANKING && loss_kind != SPL_TRAIN_LOSS_RECONSTRUCTION)
+        return spl::fail(ctx, SPL_E_DIMENSION, "train_hasher: unknown loss kind");
     return spl::train_impl(ctx, kind, d, h, L, gamma, w1, b1, w2, n_seq, queries, keys, seq_len,
-                           *rank, *train, records, holdout_iou, skipped,
-                           static_cast<cudaStream_t>(stream));
+                           *rank, *train, loss_kind == SPL_TRAIN_LOSS_RECONSTRUCTION, records,
+                           holdout_iou, skipped, static_cast<cudaStream_t>(stream));
 }
 
 extern "C" spl_status spl_train_partition_host(const spl_rank_config* rank, uint32_t q_train,

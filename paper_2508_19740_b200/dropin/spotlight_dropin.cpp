@@ -920,8 +920,6 @@ TrainReport train_hasher(AnyHasher& hasher, const TrainDataset& dataset,
                          TrainLoss loss_kind) {
     const auto t0 = std::chrono::steady_clock::now();
     cfg.validate();
-    if (loss_kind != TrainLoss::ranking)
-        throw DimensionError("train_hasher: only the ranking loss runs on the B200 trainer");
     if (dataset.sequences.empty()) throw DimensionError("train_hasher: dataset is empty");
     std::vector<float> qs, ks;
     std::vector<std::uint32_t> lens;
@@ -949,26 +947,28 @@ TrainReport train_hasher(AnyHasher& hasher, const TrainDataset& dataset,
             throw DimensionError("train_hasher: data dimension " + std::to_string(d) +
                                  " does not match hasher dimension " + std::to_string(in_dim));
     };
+    const int lk = loss_kind == TrainLoss::reconstruction ? SPL_TRAIN_LOSS_RECONSTRUCTION
+                                                          : SPL_TRAIN_LOSS_RANKING;
     spl_status st = SPL_OK;
     if (auto* m = std::get_if<MlpHasher>(&hasher)) {
         dim_check(m->input_dim());
         st = spl_train_hasher(ctx(), SPL_HASHER_MLP, m->input_dim(), m->hidden_dim(), m->code_bits(),
                               m->gamma, m->w1.data(), m->b1.data(), m->w2.data(),
                               static_cast<std::uint32_t>(lens.size()), qs.data(), ks.data(),
-                              lens.data(), &rc, &tc, rec.data(), &iou, &skipped, nullptr);
+                              lens.data(), &rc, &tc, lk, rec.data(), &iou, &skipped, nullptr);
     } else if (auto* l = std::get_if<LinearHasher>(&hasher)) {
         dim_check(l->input_dim());
         st = spl_train_hasher(ctx(), SPL_HASHER_LINEAR, l->input_dim(), 0, l->code_bits(), 0.0f,
                               l->projection.data(), nullptr, nullptr,
                               static_cast<std::uint32_t>(lens.size()), qs.data(), ks.data(),
-                              lens.data(), &rc, &tc, rec.data(), &iou, &skipped, nullptr);
+                              lens.data(), &rc, &tc, lk, rec.data(), &iou, &skipped, nullptr);
     } else {
         auto& e = std::get<DownProjEstimator>(hasher);
         dim_check(e.input_dim());
         st = spl_train_hasher(ctx(), SPL_HASHER_DOWNPROJ, e.input_dim(), 0, e.reduced_dim(), 0.0f,
                               e.projection.data(), nullptr, nullptr,
                               static_cast<std::uint32_t>(lens.size()), qs.data(), ks.data(),
-                              lens.data(), &rc, &tc, rec.data(), &iou, &skipped, nullptr);
+                              lens.data(), &rc, &tc, lk, rec.data(), &iou, &skipped, nullptr);
     }
     check(st);
     TrainReport report;

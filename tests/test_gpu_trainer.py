@@ -34,10 +34,10 @@ def seqs(seed, lens, d):
              rng.standard_normal((n, d)).astype(np.float32)) for n in lens]
 
 
-def run_pair(ctx, kind, weights, data, rank, cfg, gamma=64.0):
+def run_pair(ctx, kind, weights, data, rank, cfg, gamma=64.0, loss_kind=0):
     ref = RefLib()
     w1, b1, w2 = weights
-    r = ref.train(kind, w1, b1, w2, gamma, data, rank, cfg)
+    r = ref.train(kind, w1, b1, w2, gamma, data, rank, cfg, loss_kind)
     g1 = w1.copy()
     gb = None if b1 is None else b1.copy()
     g2 = None if w2 is None else w2.copy()
@@ -45,7 +45,7 @@ def run_pair(ctx, kind, weights, data, rank, cfg, gamma=64.0):
     h = w1.shape[1] if kind == 1 else 0
     L = w2.shape[1] if kind == 1 else w1.shape[1]
     out = ctx.train_hasher(kind, d, h, L, gamma, g1, gb, g2, data,
-                           capi.RankConfig(**rank), capi.TrainConfig(**cfg))
+                           capi.RankConfig(**rank), capi.TrainConfig(**cfg), loss_kind)
     return r, (g1, gb, g2, out)
 
 
@@ -174,3 +174,20 @@ def test_train_longer_run_stays_identical(ctx):
     cfg = dict(CFG, num_iters=60, warmup_iters=6, seed=5)
     r, g = run_pair(ctx, 1, w, data, RANK, cfg)
     assert compare(r, g, "60 iters n=1024")
+
+
+@pytest.mark.parametrize("kind,batch", [(1, 1), (1, 2), (0, 1)])
+def test_train_reconstruction_loss(ctx, kind, batch):
+    """TrainLoss::reconstruction (recon_soft_loss, trainer.cpp:383-419): MSE of
+    the soft-code inner products against the exact logits."""
+    ref = RefLib()
+    rng = np.random.default_rng(31)
+    if kind == 1:
+        w = ref.mlp_gaussian_init(64, 64, 64, 64.0, 4)
+    else:
+        w = ((rng.standard_normal((64, 64)) / 8).astype(np.float32), None, None)
+    data = seqs(10, [300, 257], 64)
+    cfg = dict(CFG, batch=batch, num_iters=6)
+    r, g = run_pair(ctx, kind, w, data, RANK, cfg, loss_kind=1)
+    assert np.all(g[3]["records"][:, 1] == 0.0)
+    compare(r, g, f"recon kind={kind} batch={batch}")
