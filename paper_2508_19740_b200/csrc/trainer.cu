@@ -201,97 +201,129 @@ __global__ void __launch_bounds__(1024) k_order(const float* __restrict__ logits
 // MLP z1 = x W1 (+ b1), a1 = z1 * sigmoid(z1), z2 = a1 W2; linear z2 = x P;
 // soft = soft_sign(z2) (downproj: soft = x P). 16 rows per block; each
 // thread owns output columns, one fma chain per (row, column).
-constexpr int kFwdRows = 16;
-template <int KIND>  // SPL_HASHER_MLP / SPL_HASHER_LINEAR / 2 = downproj
-__global__ void __launch_bounds__(128) k_forward(const float* __restrict__ x, const uint32_t* rows,
-                                                 uint32_t m, uint32_t d, uint32_t h, uint32_t L,
-                                                 const float* __restrict__ w1,
-                                                 const float* __restrict__ b1,
-                                                 const float* __restrict__ w2, float gamma,
-                                                 float* z1, float* a1, float* z2, float* soft,
-                                                 const TrainDev* st) {
+constexpr int kFwdRows = 16;     // rows per block
+constexpr int kFwdThreads = 256; // 128 column lanes x 2 row groups of 8
+constexpr int kFwdRg = kFwdRows / (kFwdThreads / 128);
+// one layer for this thread's row group: acc[r] = FMA chain over p of
+// in[r][p] * W[p][j] (matrix.hpp:81-99). W in shared memory (staged once per
+// block by cp.async) or, for shapes too large for it, read through L1/L2
+// 32 weights ahead.
+template <bool WSMEM>
+__device__ __forceinline__ void fwd_layer(const float* in, uint32_t K, const float* W,
+                                          uint32_t ncol, uint32_t j, float (&acc)[kFwdRg]) {
+#pragma unroll
+    for (int r = 0; r < kFwdRg; ++r) acc[r] = 0.0f;
+    uint32_t p = 0;
+    if (WSMEM) {
+        for (; p < K; ++p) {
+            const float w = W[(size_t)p * ncol + j];
+#pragma unroll
+            for (int r = 0; r < kFwdRg; ++r) acc[r] = __fmaf_rn(in[r * K + p], w, acc[r]);
+        }
+        return;
+    }
+    for (; p + 32 <= K; p += 32) {
+        float w[32];
+#pragma unroll
+        for (int u = 0; u < 32; ++u) w[u] = __ldg(W + (uint64_t)(p + u) * ncol + j);
+#pragma unroll
+        for (int u = 0; u < 32; ++u)
+#pragma unroll
+            for (int r = 0; r < kFwdRg; ++r) acc[r] = __fmaf_rn(in[r * K + p + u], w[u], acc[r]);
+    }
+    for (; p < K; ++p) {
+        const float w = W[(uint64_t)p * ncol + j];
+#pragma unroll
+        for (int r = 0; r < kFwdRg; ++r) acc[r] = __fmaf_rn(in[r * K + p], w, acc[r]);
+    }
+}
+
+__device__ __forceinline__ void cp_async_f32(float* dst, const float* src, uint64_t n) {
+    for (uint64_t e = threadIdx.x; e < n; e += blockDim.x)
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(
+                         (uint32_t)__cvta_generic_to_shared(dst + e)),
+                     "l"(src + e)
+                     : "memory");
+    asm volatile("cp.async.commit_group;" ::: "memory");
+}
+
+template <int KIND, bool WSMEM>  // KIND: SPL_HASHER_MLP / SPL_HASHER_LINEAR / 2 = downproj
+__global__ void __launch_bounds__(kFwdThreads) k_forward(const float* __restrict__ x, const uint32_t* rows,
+                                                         uint32_t m, uint32_t d, uint32_t h, uint32_t L,
+                                                         const float* __restrict__ w1,
+                                                         const float* __restrict__ b1,
+                                                         const float* __restrict__ w2, float gamma,
+                                                         float* z1, float* a1, float* z2, float* soft,
+                                                         const TrainDev* st) {
     if (st->halt) return;
     extern __shared__ float sm[];
     float* xs = sm;                       // [kFwdRows][d]
     float* as = sm + kFwdRows * d;        // [kFwdRows][h] (MLP)
+    float* w1s = as + (KIND == SPL_HASHER_MLP ? kFwdRows * h : 0);  // [d][h | L]
+    float* w2s = w1s + (size_t)d * (KIND == SPL_HASHER_MLP ? h : L);  // [h][L] (MLP)
     const uint32_t r0 = blockIdx.x * kFwdRows;
     const uint32_t nr = min((uint32_t)kFwdRows, m - r0);
-    for (uint32_t e = threadIdx.x; e < (uint32_t)kFwdRows * d; e += blockDim.x) {
-        const uint32_t r = e / d, c = e % d;
-        float v = 0.0f;
-        if (r < nr) {
-            const uint32_t src = rows ? rows[r0 + r] : r0 + r;
-            v = x[(uint64_t)src * d + c];
+    for (uint32_t r = 0; r < kFwdRows; ++r) {  // async row staging, zero rows past m
+        const bool ok = r < nr;
+        const float* src = ok ? x + (uint64_t)(rows ? rows[r0 + r] : r0 + r) * d : x;
+        for (uint32_t c = threadIdx.x; c < d; c += blockDim.x)
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(
+                             (uint32_t)__cvta_generic_to_shared(xs + r * d + c)),
+                         "l"(ok ? src + c : x), "r"(ok ? 4 : 0)
+                         : "memory");
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    if (WSMEM) {  // group 2: layer-1 weights; group 3 (MLP): layer-2 weights, under layer 1
+        cp_async_f32(w1s, w1, (uint64_t)d * (KIND == SPL_HASHER_MLP ? h : L));
+        if (KIND == SPL_HASHER_MLP) {
+            cp_async_f32(w2s, w2, (uint64_t)h * L);
+            asm volatile("cp.async.wait_group 1;" ::: "memory");
+        } else {
+            asm volatile("cp.async.wait_group 0;" ::: "memory");
         }
-        xs[e] = v;
+    } else {
+        asm volatile("cp.async.wait_group 0;" ::: "memory");
     }
     __syncthreads();
-    const float* in = xs;
+    const uint32_t lane = threadIdx.x & 127, rg = threadIdx.x >> 7;
+    const uint32_t rbase = rg * kFwdRg;  // this thread's rows: rbase .. rbase + kFwdRg - 1
+    const float* in = xs + rbase * d;
     uint32_t K = d;
-    const float* W = w1;
+    const float* W = WSMEM ? w1s : w1;
+    float acc[kFwdRg];
     if (KIND == SPL_HASHER_MLP) {
-        for (uint32_t j = threadIdx.x; j < h; j += blockDim.x) {
-            float acc[kFwdRows];
-#pragma unroll
-            for (int r = 0; r < kFwdRows; ++r) acc[r] = 0.0f;
-            uint32_t p = 0;
-            for (; p + 8 <= d; p += 8) {  // loads of 8 weights ahead of their chains
-                float w[8];
-#pragma unroll
-                for (int u = 0; u < 8; ++u) w[u] = __ldg(w1 + (uint64_t)(p + u) * h + j);
-#pragma unroll
-                for (int u = 0; u < 8; ++u)
-#pragma unroll
-                    for (int r = 0; r < kFwdRows; ++r) acc[r] = __fmaf_rn(xs[r * d + p + u], w[u], acc[r]);
-            }
-            for (; p < d; ++p) {
-                const float w = w1[(uint64_t)p * h + j];
-#pragma unroll
-                for (int r = 0; r < kFwdRows; ++r) acc[r] = __fmaf_rn(xs[r * d + p], w, acc[r]);
-            }
+        for (uint32_t j = lane; j < h; j += 128) {
+            fwd_layer<WSMEM>(in, d, W, h, j, acc);
             const float bj = b1[j];
 #pragma unroll
-            for (int r = 0; r < kFwdRows; ++r) {
+            for (int r = 0; r < kFwdRg; ++r) {
+                const uint32_t rr = rbase + r;
                 const float z = __fadd_rn(acc[r], bj);
                 const float a = __fmul_rn(z, sigmoid_f(z));
-                as[r * h + j] = a;
-                if ((uint32_t)r < nr) {
-                    z1[(uint64_t)(r0 + r) * h + j] = z;
-                    a1[(uint64_t)(r0 + r) * h + j] = a;
+                as[rr * h + j] = a;
+                if (rr < nr) {
+                    z1[(uint64_t)(r0 + rr) * h + j] = z;
+                    a1[(uint64_t)(r0 + rr) * h + j] = a;
                 }
             }
         }
+        if (WSMEM) asm volatile("cp.async.wait_group 0;" ::: "memory");
         __syncthreads();
-        in = as;
+        in = as + rbase * h;
         K = h;
-        W = w2;
+        W = WSMEM ? w2s : w2;
     }
-    for (uint32_t j = threadIdx.x; j < L; j += blockDim.x) {
-        float acc[kFwdRows];
+    for (uint32_t j = lane; j < L; j += 128) {
+        fwd_layer<WSMEM>(in, K, W, L, j, acc);
 #pragma unroll
-        for (int r = 0; r < kFwdRows; ++r) acc[r] = 0.0f;
-        uint32_t p = 0;
-        for (; p + 8 <= K; p += 8) {
-            float w[8];
-#pragma unroll
-            for (int u = 0; u < 8; ++u) w[u] = __ldg(W + (uint64_t)(p + u) * L + j);
-#pragma unroll
-            for (int u = 0; u < 8; ++u)
-#pragma unroll
-                for (int r = 0; r < kFwdRows; ++r) acc[r] = __fmaf_rn(in[r * K + p + u], w[u], acc[r]);
-        }
-        for (; p < K; ++p) {
-            const float w = W[(uint64_t)p * L + j];
-#pragma unroll
-            for (int r = 0; r < kFwdRows; ++r) acc[r] = __fmaf_rn(in[r * K + p], w, acc[r]);
-        }
-#pragma unroll
-        for (int r = 0; r < kFwdRows; ++r)
-            if ((uint32_t)r < nr) {
-                const uint64_t o = (uint64_t)(r0 + r) * L + j;
+        for (int r = 0; r < kFwdRg; ++r) {
+            const uint32_t rr = rbase + r;
+            if (rr < nr) {
+                const uint64_t o = (uint64_t)(r0 + rr) * L + j;
                 if (KIND != 2) z2[o] = acc[r];
                 soft[o] = KIND == 2 ? acc[r] : soft_sign_f(acc[r], gamma);
             }
+        }
     }
 }
 
@@ -1313,16 +1345,30 @@ spl_status train_impl(spl_ctx* ctx, int kind, uint32_t d, uint32_t h, uint32_t L
     const float* W1 = dP;
     const float* B1 = dP + n1;
     const float* W2 = dP + n1 + nb;
-    const size_t fwd_smem = (size_t)kFwdRows * (d + hw) * 4;
+    // forward: weights staged in shared memory when they fit (one block/SM)
+    const size_t wbytes = (mlp ? (size_t)d * h + (size_t)h * L : (size_t)d * L) * 4;
+    const size_t fwd_base = (size_t)kFwdRows * (d + (mlp ? h : 0)) * 4;
+    const bool wsmem = fwd_base + wbytes <= 220 * 1024;
+    const size_t fwd_smem = fwd_base + (wsmem ? wbytes : 0);
+    auto fwd_attr = [&](const void* fn) -> spl_status {
+        SPL_CUDA_TRY(ctx, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fwd_smem));
+        return SPL_OK;
+    };
+    {
+        const void* fns[6] = {(const void*)k_forward<SPL_HASHER_MLP, true>, (const void*)k_forward<SPL_HASHER_MLP, false>,
+                              (const void*)k_forward<SPL_HASHER_LINEAR, true>, (const void*)k_forward<SPL_HASHER_LINEAR, false>,
+                              (const void*)k_forward<2, true>, (const void*)k_forward<2, false>};
+        for (const void* f : fns)
+            if (spl_status st = fwd_attr(f)) return st;
+    }
     auto fwd = [&](const float* x, const uint32_t* rows, uint32_t m, float* a, float* b, float* c,
                    float* sf) -> spl_status {
         const dim3 grid((m + kFwdRows - 1) / kFwdRows);
-        if (kind == SPL_HASHER_MLP)
-            k_forward<SPL_HASHER_MLP><<<grid, 128, fwd_smem, s>>>(x, rows, m, d, h, L, W1, B1, W2, sgamma, a, b, c, sf, dst);
-        else if (kind == SPL_HASHER_LINEAR)
-            k_forward<SPL_HASHER_LINEAR><<<grid, 128, fwd_smem, s>>>(x, rows, m, d, 0, L, W1, nullptr, nullptr, sgamma, a, b, c, sf, dst);
-        else
-            k_forward<2><<<grid, 128, fwd_smem, s>>>(x, rows, m, d, 0, L, W1, nullptr, nullptr, sgamma, a, b, c, sf, dst);
+#define SPL_FWD(K_, WS_) k_forward<K_, WS_><<<grid, kFwdThreads, fwd_smem, s>>>(x, rows, m, d, K_ == SPL_HASHER_MLP ? h : 0, L, W1, K_ == SPL_HASHER_MLP ? B1 : nullptr, K_ == SPL_HASHER_MLP ? W2 : nullptr, sgamma, a, b, c, sf, dst)
+        if (kind == SPL_HASHER_MLP) { if (wsmem) SPL_FWD(SPL_HASHER_MLP, true); else SPL_FWD(SPL_HASHER_MLP, false); }
+        else if (kind == SPL_HASHER_LINEAR) { if (wsmem) SPL_FWD(SPL_HASHER_LINEAR, true); else SPL_FWD(SPL_HASHER_LINEAR, false); }
+        else { if (wsmem) SPL_FWD(2, true); else SPL_FWD(2, false); }
+#undef SPL_FWD
         return after_launch(ctx, "k_forward");
     };
     // backward of one side (trainer.cpp:219-236 / :252-258 / :279-282);

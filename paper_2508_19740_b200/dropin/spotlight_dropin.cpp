@@ -25,6 +25,7 @@
 #include <chrono>
 #include <cstdio>
 
+#include "spotlight/synthkv.hpp"
 #include "spotlight/trainer.hpp"
 #include "spotlight/attention_eval.hpp"
 #include "spotlight/bitcodes.hpp"
@@ -878,6 +879,49 @@ spl_train_config to_c(const TrainConfig& c) {
     return t;
 }
 }  // namespace
+
+// SPLQ dumps (synthkv.cpp:104-142)
+void write_dump(const std::string& path, const Matrix<float>& queries, const Matrix<float>& keys) {
+    if (queries.cols() != keys.cols()) throw DimensionError("write_dump: query and key dimensions differ");
+    auto finite = [](const Matrix<float>& m) {
+        for (std::size_t i = 0; i < m.size(); ++i)
+            if (!std::isfinite(m.data()[i])) return false;
+        return true;
+    };
+    if (!finite(queries) || !finite(keys)) throw NumericError("write_dump: tensors contain non-finite values");
+    auto os = open_out(path);
+    os.write("SPLQ", 4);
+    write_u32(os, 1);
+    write_u32(os, static_cast<std::uint32_t>(queries.rows()));
+    write_u32(os, static_cast<std::uint32_t>(keys.rows()));
+    write_u32(os, static_cast<std::uint32_t>(queries.cols()));
+    write_words(os, queries.data(), queries.size());
+    write_words(os, keys.data(), keys.size());
+    if (!os) throw IoError("write failed: " + path);
+}
+
+QkDump read_dump(const std::string& path) {
+    Reader r(path);
+    r.magic("SPLQ");
+    const std::uint32_t version = r.u32("version");
+    if (version != 1) throw FormatError(path + ": unsupported SPLQ version " + str(version));
+    const std::uint32_t nq = r.u32("n_queries");
+    const std::uint32_t nk = r.u32("n_keys");
+    const std::uint32_t d = r.u32("d");
+    QkDump dump{Matrix<float>(nq, d), Matrix<float>(nk, d)};
+    r.words(dump.queries.data(), dump.queries.size(), "query block");
+    r.words(dump.keys.data(), dump.keys.size(), "key block");
+    for (const Matrix<float>* m : {&dump.queries, &dump.keys})
+        for (std::size_t i = 0; i < m->size(); ++i)
+            if (!std::isfinite(m->data()[i])) throw FormatError(path + ": payload contains non-finite values");
+    return dump;
+}
+
+TrainDataset dataset_from_dump(QkDump dump) {
+    TrainDataset data;
+    data.sequences.push_back(QkSequence{std::move(dump.queries), std::move(dump.keys)});
+    return data;
+}
 
 void TrainConfig::validate() const {  // trainer.cpp:19-33
     if (max_lr < 0.0 || min_lr < 0.0 || min_lr > max_lr)

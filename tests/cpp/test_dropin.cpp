@@ -22,6 +22,7 @@
 #include "spotlight/bitcodes.hpp"
 #include "spotlight/errors.hpp"
 #include "spotlight/hashers.hpp"
+#include "spotlight/synthkv.hpp"
 #include "spotlight/trainer.hpp"
 
 using namespace spotlight;
@@ -766,6 +767,44 @@ TEST_CASE("trainer: drop-in == reference train_hasher (bit-identical weights)") 
         CHECK(r.records[i].violation_rate == rec[3 * i + 1]);
         CHECK(std::fabs(r.records[i].loss - rec[3 * i]) <= 1e-10 * std::fabs(rec[3 * i]));
     }
+}
+
+TEST_CASE("SPLQ dump round trip, validation and training from a dump") {
+    std::mt19937_64 eng(4);
+    const Matrix<float> q = random_matrix(120, 16, eng), k = random_matrix(120, 16, eng);
+    const std::string path = "/tmp/spl_test_dump_" + std::to_string(::getpid()) + ".splq";
+    write_dump(path, q, k);
+    const QkDump d = read_dump(path);
+    CHECK(d.queries.rows() == 120 && d.keys.cols() == 16);
+    CHECK(std::memcmp(d.queries.data(), q.data(), q.size() * 4) == 0);
+    CHECK(std::memcmp(d.keys.data(), k.data(), k.size() * 4) == 0);
+    CHECK_THROWS_AS(write_dump(path, q, random_matrix(4, 8, eng)), DimensionError);
+    Matrix<float> bad = q;
+    bad.data()[3] = std::nanf("");
+    CHECK_THROWS_AS(write_dump(path, bad, k), NumericError);
+    {
+        std::FILE* f = std::fopen(path.c_str(), "r+b");
+        std::fseek(f, 0, SEEK_SET);
+        std::fputc('X', f);
+        std::fclose(f);
+    }
+    CHECK_THROWS_WITH(read_dump(path), FormatError, "bad magic");
+    write_dump(path, q, k);
+    TrainDataset ds = dataset_from_dump(read_dump(path));
+    std::remove(path.c_str());
+    RankingLossConfig rc;
+    rc.maskout = 0.9;
+    rc.max_oth = 16;
+    rc.query_subsample = 8;
+    TrainConfig cfg;
+    cfg.num_iters = 3;
+    cfg.holdout_queries = 16;
+    AnyHasher a = mlp_gaussian_init(16, 16, 32, 64.0f, 2);
+    const TrainReport r = train_hasher(a, ds, rc, cfg);
+    CHECK(r.records.size() == 3);
+    const std::string txt = format_train_report(r, std::vector<std::string>{"dump test"});
+    CHECK(txt.rfind("# dump test\n# columns: iter loss violation_rate lr\n0 ", 0) == 0);
+    CHECK(txt.find("# skipped_steps 0") != std::string::npos);
 }
 
 int main() {
