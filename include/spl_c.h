@@ -309,8 +309,9 @@ typedef struct spl_train_config {
  * (also when an error stops the run, as the reference's in-place hasher).
  * Sequences are concatenated: sequence s has seq_len[s] query rows and as
  * many key rows (causally aligned). records: [num_iters][3] = {loss,
- * violation_rate, lr} (IterRecord, trainer.hpp:84-89). Sequences are limited
- * to 16384 keys (per-row order sort in shared memory). */
+ * violation_rate, lr} (IterRecord, trainer.hpp:84-89). Per-row orders are
+ * sorted in shared-memory chunks of 16384 keys, merged in global memory
+ * beyond that. */
 typedef enum spl_train_loss {
     SPL_TRAIN_LOSS_RANKING = 0,        /* TrainLoss::ranking */
     SPL_TRAIN_LOSS_RECONSTRUCTION = 1  /* TrainLoss::reconstruction (MSE ablation) */

@@ -54,7 +54,7 @@
 namespace spl {
 namespace {
 
-constexpr uint32_t kMaxSortKeys = 16384;  // per-row order sort in shared memory
+constexpr uint32_t kMaxSortKeys = 16384;  // order sort chunk (shared memory); longer rows merge
 
 // halt codes (device): the reference throws out of train_loop at that point
 enum : uint32_t { HALT_NONE = 0, HALT_EMPTY = 1, HALT_NONFINITE = 2 };
@@ -161,24 +161,27 @@ __device__ __forceinline__ uint32_t orderable(float f) {
     if (u == 0x80000000u) u = 0u;
     return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
 }
+// One C-key chunk (C a power of two <= kMaxSortKeys) of a row per block:
+// rows longer than C are sorted chunk by chunk here and merged below. Pads
+// (j >= n) sort last and stay unique: (0xFFFFFFFF << 32) | j.
 __global__ void __launch_bounds__(1024) k_order(const float* __restrict__ logits, uint32_t n,
-                                                uint32_t npow2, uint32_t* __restrict__ order) {
+                                                uint32_t C, uint32_t row0,
+                                                uint32_t* __restrict__ order,
+                                                unsigned long long* __restrict__ runs) {
     extern __shared__ unsigned long long keys[];
-    const uint32_t row = blockIdx.x;
+    const uint32_t row = row0 + blockIdx.y, c0 = blockIdx.x * C;
     const uint32_t valid = min(row + 1, n);
     const float* s = logits + (uint64_t)row * n;
-    for (uint32_t j = threadIdx.x; j < npow2; j += blockDim.x) {
-        unsigned long long key = ~0ull;
-        if (j < n) {
-            const uint32_t hi = j < valid ? ~orderable(s[j]) : 0xFFFFFFFFu;
-            key = ((unsigned long long)hi << 32) | j;
-        }
-        keys[j] = key;
+    for (uint32_t t = threadIdx.x; t < C; t += blockDim.x) {
+        const uint32_t j = c0 + t;
+        uint32_t hi = 0xFFFFFFFFu;
+        if (j < valid) hi = ~orderable(s[j]);
+        keys[t] = ((unsigned long long)hi << 32) | j;
     }
     __syncthreads();
-    for (uint32_t k = 2; k <= npow2; k <<= 1)
+    for (uint32_t k = 2; k <= C; k <<= 1)
         for (uint32_t j = k >> 1; j > 0; j >>= 1) {
-            for (uint32_t i = threadIdx.x; i < npow2; i += blockDim.x) {
+            for (uint32_t i = threadIdx.x; i < C; i += blockDim.x) {
                 const uint32_t l = i ^ j;
                 if (l > i) {
                     const unsigned long long a = keys[i], b = keys[l];
@@ -191,8 +194,50 @@ __global__ void __launch_bounds__(1024) k_order(const float* __restrict__ logits
             }
             __syncthreads();
         }
-    for (uint32_t j = threadIdx.x; j < n; j += blockDim.x)
-        order[(uint64_t)row * n + j] = (uint32_t)keys[j];
+    if (gridDim.x == 1) {  // the whole row fits one chunk
+        for (uint32_t j = threadIdx.x; j < n; j += blockDim.x)
+            order[(uint64_t)row * n + j] = (uint32_t)keys[j];
+    } else {
+        const uint64_t rowlen = (uint64_t)gridDim.x * C;
+        for (uint32_t t = threadIdx.x; t < C; t += blockDim.x)
+            runs[(uint64_t)blockIdx.y * rowlen + c0 + t] = keys[t];
+    }
+}
+
+// One merge pass over sorted runs of length R (keys unique): each key's
+// output position = its rank in its own run + its rank in the partner run.
+__global__ void k_order_merge(const unsigned long long* __restrict__ src,
+                              unsigned long long* __restrict__ dst, uint64_t rowlen, uint64_t R,
+                              uint64_t total) {
+    for (uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+         e += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t y = e / rowlen, i = e % rowlen;
+        const unsigned long long* row = src + y * rowlen;
+        const unsigned long long key = row[i];
+        const uint64_t r = i / R, pb = (r ^ 1) * R;
+        uint64_t pos = i;
+        if (pb < rowlen) {
+            const uint64_t plen = min(R, rowlen - pb);
+            uint64_t lo = 0, hi = plen;  // count of partner keys < key
+            while (lo < hi) {
+                const uint64_t mid = (lo + hi) >> 1;
+                if (row[pb + mid] < key) lo = mid + 1; else hi = mid;
+            }
+            pos = (r & ~1ull) * R + (i - r * R) + lo;
+        }
+        dst[y * rowlen + pos] = key;
+    }
+}
+
+__global__ void k_order_extract(const unsigned long long* __restrict__ src, uint64_t rowlen,
+                                uint32_t n, uint32_t row0, uint32_t rows,
+                                uint32_t* __restrict__ order) {
+    const uint64_t total = (uint64_t)rows * n;
+    for (uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+         e += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t y = e / n, j = e % n;
+        order[(row0 + y) * (uint64_t)n + j] = (uint32_t)src[y * rowlen + j];
+    }
 }
 
 // ------------------------------------------------------------ forward
@@ -1211,19 +1256,12 @@ spl_status train_impl(spl_ctx* ctx, int kind, uint32_t d, uint32_t h, uint32_t L
                 used[sq] = 1;
                 const std::string e = rank_cfg_error(rc, n);
                 if (!e.empty()) return fail(ctx, SPL_E_DIMENSION, e);
-                if (n > kMaxSortKeys)
-                    return fail(ctx, SPL_E_DIMENSION,
-                                "train_hasher: sequences longer than " +
-                                    std::to_string(kMaxSortKeys) + " keys are not supported");
             }
             draws.push_back(draw_partition(q_train_of(sq), n, rc, part_seed));
             draws.back().seq = sq;
         }
     }
     used[0] = 1;  // the holdout IoU reads sequence 0
-    if (seq_len[0] > kMaxSortKeys)
-        return fail(ctx, SPL_E_DIMENSION, "train_hasher: sequences longer than " +
-                                               std::to_string(kMaxSortKeys) + " keys are not supported");
 
     // ---- device state
     DevBuf db;
@@ -1286,12 +1324,40 @@ spl_status train_impl(spl_ctx* ctx, int kind, uint32_t d, uint32_t h, uint32_t L
         SPL_CUDA_TRY(ctx, cudaMemcpyAsync(p.x_k, keys + off[q] * d, (size_t)n * d * 4, cudaMemcpyHostToDevice, s));
         k_logits<<<dim3((n + 63) / 64, (n + 63) / 64), 256, 0, s>>>(p.x_q, p.x_k, n, n, d, scale, p.logits);
         if (spl_status st = after_launch(ctx, "k_logits")) return st;
-        uint32_t npow2 = 1;
-        while (npow2 < n) npow2 <<= 1;
-        const size_t smem = (size_t)npow2 * 8;
+        // build_topk_order: bitonic chunks of C keys in shared memory, then
+        // merge passes in global memory for rows longer than one chunk
+        uint32_t C = 1;
+        while (C < n && C < kMaxSortKeys) C <<= 1;
+        const uint32_t nch = (n + C - 1) / C;
+        const size_t smem = (size_t)C * 8;
         SPL_CUDA_TRY(ctx, cudaFuncSetAttribute(k_order, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        k_order<<<p.q_train, 1024, smem, s>>>(p.logits, n, npow2, p.order);
-        if (spl_status st = after_launch(ctx, "k_order")) return st;
+        if (nch == 1) {
+            k_order<<<dim3(1, p.q_train), 1024, smem, s>>>(p.logits, n, C, 0, p.order, nullptr);
+            if (spl_status st = after_launch(ctx, "k_order")) return st;
+        } else {
+            const uint64_t rowlen = (uint64_t)nch * C;
+            const uint32_t rb = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(p.q_train, (1ull << 31) / (16 * rowlen)));
+            unsigned long long* ra = db.get<unsigned long long>((size_t)rb * rowlen);
+            unsigned long long* rbuf = db.get<unsigned long long>((size_t)rb * rowlen);
+            if (!ra || !rbuf) return fail(ctx, SPL_E_CUDA, "train: out of device memory");
+            for (uint32_t r0 = 0; r0 < p.q_train; r0 += rb) {
+                const uint32_t rows = std::min(rb, p.q_train - r0);
+                k_order<<<dim3(nch, rows), 1024, smem, s>>>(p.logits, n, C, r0, nullptr, ra);
+                if (spl_status st = after_launch(ctx, "k_order")) return st;
+                unsigned long long *src = ra, *dstb = rbuf;
+                for (uint64_t R = C; R < rowlen; R <<= 1) {
+                    const uint64_t total = (uint64_t)rows * rowlen;
+                    k_order_merge<<<(unsigned)std::min<uint64_t>((total + 255) / 256, 148 * 16), 256, 0, s>>>(
+                        src, dstb, rowlen, R, total);
+                    if (spl_status st = after_launch(ctx, "k_order_merge")) return st;
+                    std::swap(src, dstb);
+                }
+                const uint64_t tot = (uint64_t)rows * n;
+                k_order_extract<<<(unsigned)std::min<uint64_t>((tot + 255) / 256, 148 * 16), 256, 0, s>>>(
+                    src, rowlen, n, r0, rows, p.order);
+                if (spl_status st = after_launch(ctx, "k_order_extract")) return st;
+            }
+        }
     }
 
     // ---- per-step buffers (sized for the largest draw)

@@ -191,3 +191,14 @@ def test_train_reconstruction_loss(ctx, kind, batch):
     r, g = run_pair(ctx, kind, w, data, RANK, cfg, loss_kind=1)
     assert np.all(g[3]["records"][:, 1] == 0.0)
     compare(r, g, f"recon kind={kind} batch={batch}")
+
+
+def test_train_long_sequence_merged_order(ctx):
+    """A sequence longer than one shared-memory sort chunk (16,384 keys): the
+    per-row order is sorted in chunks and merged in global memory."""
+    ref = RefLib()
+    w = ref.mlp_gaussian_init(32, 32, 32, 64.0, 13)
+    data = seqs(12, [17000], 32)
+    cfg = dict(CFG, num_iters=2, warmup_iters=1, seed=3)
+    r, g = run_pair(ctx, 1, w, data, dict(RANK, max_oth=64, query_subsample=16), cfg)
+    assert compare(r, g, "n=17000")
