@@ -707,7 +707,22 @@ __global__ void k_loss_finalize(const double* loss_part, const unsigned long lon
     const double inv = st->pairs ? __ddiv_rn(1.0, (double)st->pairs) : 0.0;
     double a = 0.0;
     unsigned long long c = 0;
-    for (uint32_t q = threadIdx.x; q < nparts; q += blockDim.x) {  // fixed order per thread
+    uint32_t q = threadIdx.x;
+    for (; q + 7 * blockDim.x < nparts; q += 8 * blockDim.x) {  // fixed order per thread
+        double lv[8];
+        unsigned long long vv[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            lv[u] = loss_part[q + u * blockDim.x];
+            vv[u] = viol_part[q + u * blockDim.x];
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            a = __dadd_rn(a, lv[u]);
+            c += vv[u];
+        }
+    }
+    for (; q < nparts; q += blockDim.x) {
         a = __dadd_rn(a, loss_part[q]);
         c += viol_part[q];
     }
@@ -755,7 +770,19 @@ __global__ void __launch_bounds__(256) k_dsoft_keys(const float* __restrict__ G,
     const uint64_t key = e / L;
     const uint32_t p = (uint32_t)(e % L);
     float acc = 0.0f;
-    for (uint32_t q = 0; q < Qs; ++q) {
+    uint32_t q = 0;
+    for (; q + 16 <= Qs; q += 16) {  // loads batched ahead of the chain
+        float gv[16], sv[16];
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {
+            gv[u] = G[key * Qs + q + u];
+            sv[u] = softq[(uint64_t)(q + u) * L + p];
+        }
+#pragma unroll
+        for (int u = 0; u < 16; ++u)
+            if (gv[u] != 0.0f) acc = __fmaf_rn(gv[u], sv[u], acc);
+    }
+    for (; q < Qs; ++q) {
         const float g = G[key * Qs + q];
         if (g != 0.0f) acc = __fmaf_rn(g, softq[(uint64_t)q * L + p], acc);
     }
@@ -993,11 +1020,19 @@ __global__ void __launch_bounds__(256) k_norm_partial(const float* g, uint64_t n
 __global__ void k_clip(const double* part, const int* bad, double max_norm, const double* bc1_tab,
                        const double* bc2_tab, TrainDev* st) {
     if (st->halt) return;
+    __shared__ double s_p[kNormBlocks];
+    __shared__ int s_b[kNormBlocks];
+    for (int i = threadIdx.x; i < kNormBlocks; i += blockDim.x) {
+        s_p[i] = part[i];
+        s_b[i] = bad[i];
+    }
+    __syncthreads();
+    if (threadIdx.x) return;
     double t = 0.0;
     int b = 0;
     for (int i = 0; i < kNormBlocks; ++i) {
-        t = __dadd_rn(t, part[i]);
-        b |= bad[i];
+        t = __dadd_rn(t, s_p[i]);
+        b |= s_b[i];
     }
     const double norm = __dsqrt_rn(t);
     st->scale = (max_norm > 0.0 && norm > max_norm) ? __double2float_rn(__ddiv_rn(max_norm, norm)) : 1.0f;
@@ -1547,7 +1582,7 @@ spl_status train_impl(spl_ctx* ctx, int kind, uint32_t d, uint32_t h, uint32_t L
         }
         k_norm_partial<<<kNormBlocks, 256, 0, s>>>(dG, np, npart, nbad, dst);
         if (spl_status st = after_launch(ctx, "k_norm_partial")) return st;
-        k_clip<<<1, 1, 0, s>>>(npart, nbad, tc.grad_clip, dbc1, dbc2, dst);
+        k_clip<<<1, kNormBlocks, 0, s>>>(npart, nbad, tc.grad_clip, dbc1, dbc2, dst);
         if (spl_status st = after_launch(ctx, "k_clip")) return st;
         k_adamw<<<(unsigned)std::min<uint64_t>((np + 255) / 256, 1184), 256, 0, s>>>(
             dP, dG, dM, dV, np, n1, n1 + nb, lr, tc.adam_beta1, tc.adam_beta2, tc.adam_eps,
