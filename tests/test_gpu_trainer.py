@@ -202,3 +202,51 @@ def test_train_long_sequence_merged_order(ctx):
     cfg = dict(CFG, num_iters=2, warmup_iters=1, seed=3)
     r, g = run_pair(ctx, 1, w, data, dict(RANK, max_oth=64, query_subsample=16), cfg)
     assert compare(r, g, "n=17000")
+
+
+@pytest.mark.parametrize("case", range(10))
+def test_train_randomized_configs(ctx, case):
+    """Randomised shapes and settings (coder kind, d / h / L, sequence count
+    and lengths, batch, maskout, subsample sizes, loss, schedule): trained
+    weights and records against the reference."""
+    rng = np.random.default_rng(1000 + case)
+    ref = RefLib()
+    kind = int(rng.choice([1, 1, 0, 2]))
+    d = int(rng.choice([16, 32, 64]))
+    h = int(rng.choice([32, 64, 96]))
+    L = int(rng.choice([32, 64])) if kind != 2 else int(rng.choice([4, 8, 16]))
+    gamma = float(rng.choice([16.0, 64.0]))
+    if kind == 1:
+        w = ref.mlp_gaussian_init(d, h, L, gamma, int(rng.integers(1 << 30)))
+    else:
+        w = ((rng.standard_normal((d, L)) / np.sqrt(d)).astype(np.float32), None, None)
+    lens = [int(x) for x in rng.integers(60, 700, size=int(rng.integers(1, 4)))]
+    data = seqs(int(rng.integers(1 << 30)), lens, d)
+    loss_kind = int(rng.random() < 0.25)
+    maskout = float(rng.choice([0.9, 0.95, 0.98]))
+    rank = dict(beta=float(rng.choice([0.5, 1.0, 2.0])), alpha=float(rng.choice([0.0, 3.0])),
+                maskout=maskout,
+                max_top=None if rng.random() < 0.5 else int(rng.integers(1, 8)),
+                max_oth=None if rng.random() < 0.3 else int(rng.integers(4, 128)),
+                query_subsample=None if rng.random() < 0.2 else int(rng.integers(1, 40)))
+    cfg = dict(CFG, num_iters=int(rng.integers(2, 9)), warmup_iters=int(rng.integers(0, 4)),
+               batch=int(rng.integers(1, 3)), seed=int(rng.integers(1 << 40)),
+               holdout_queries=int(rng.integers(0, 40)),
+               grad_clip=float(rng.choice([0.0, 0.01, 1.0])),
+               weight_decay=float(rng.choice([0.0, 0.1])),
+               max_lr=float(rng.choice([1e-3, 5e-3])), min_lr=0.0)
+    from oracle_lib import CheckerError
+
+    try:
+        r, g = run_pair(ctx, kind, w, data, rank, cfg, gamma=gamma, loss_kind=loss_kind)
+    except CheckerError as e:  # the reference raised: ours must raise the same error
+        assert e.code == 5
+        with pytest.raises(capi.EmptyPairError):
+            dd = w[0].shape[0]
+            hh = w[0].shape[1] if kind == 1 else 0
+            LL = w[2].shape[1] if kind == 1 else w[0].shape[1]
+            ctx.train_hasher(kind, dd, hh, LL, gamma, *(None if a is None else a.copy() for a in w),
+                             data, capi.RankConfig(**rank), capi.TrainConfig(**cfg), loss_kind)
+        return
+    compare(r, g, f"random case {case}: kind={kind} d={d} h={h} L={L} lens={lens} loss={loss_kind}")
+
