@@ -394,6 +394,7 @@ def main():
     prefill = None
     accuracy = None
     train = None
+    config1 = None
     w1 = (rng.standard_normal((H, D, D)) / np.sqrt(D)).astype(np.float32)
     b1 = np.zeros((H, D), np.float32)
     w2 = (rng.standard_normal((H, D, L)) / np.sqrt(D)).astype(np.float32)
@@ -444,6 +445,8 @@ def main():
             accuracy = bench_accuracy(torch, capi, ctx, dev, stream, args)
         if not args.no_train:
             train = bench_train(capi, ctx, args)
+        if not args.no_decode:
+            config1 = bench_config1(torch, capi, ctx, dev, stream, args)
     clk = clocks.stop()
 
     # CPU baseline (rank 0, N = 1): the reference on this host's cores
@@ -515,6 +518,8 @@ def main():
         line["retrieval_accuracy"] = accuracy
     if train:
         line["hasher_training"] = train
+    if config1:
+        line["config1_decode"] = config1
     if rank == 0:
         print(json.dumps(line), flush=True)
     ctx.close()
@@ -694,6 +699,79 @@ def bench_train(capi, ctx, args):
             "reference_threads": int(ref.lib.spotref_max_threads()),
             "speedup_vs_reference": round(ms_ref / ms_gpu, 1),
             "weights_identical_after_%d_iters" % ref_iters: bool(same)}
+
+
+def bench_config1(torch, capi, ctx, dev, stream, args):
+    """Config 1 (BASELINE configs[0]): one head, d=128, 4,096 cached f32 keys,
+    128-bit MLP codes, k=64: one decode step (append the new key + encode the
+    query + retrieve + sparse attention), latency (L2-resident), beside the
+    reference's per-query path on the host (nxor_scores_into + top_k_indices +
+    sparse_attention for the same query and cache)."""
+    from oracle_lib import RefLib
+
+    n, k, Hh = 4096, 64, 1
+    rng = np.random.default_rng(41)
+    w1 = (rng.standard_normal((Hh, D, D)) / np.sqrt(D)).astype(np.float32)
+    b1 = np.zeros((Hh, D), np.float32)
+    w2 = (rng.standard_normal((Hh, D, L)) / np.sqrt(D)).astype(np.float32)
+    hs = ctx.hasher(w1, b1, w2)
+    W = L // 32
+    keys = rng.standard_normal((n, D)).astype(np.float32)
+    vals = rng.standard_normal((n, D)).astype(np.float32)
+    qv = rng.standard_normal((1, D)).astype(np.float32)
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)
+    kc, vc = t(keys[None, None]), t(vals[None, None])
+    codes = torch.zeros((1, 1, n, W), dtype=torch.int32, device=dev)
+    hs.encode(t(keys[None, None]), 1, n, codes)  # exact codes of the cache
+    q = t(qv[None])
+    kn, vn = t(keys[None, None, n - 1]), t(vals[None, None, n - 1])
+    nvalid = torch.full((1,), n, dtype=torch.int32, device=dev)
+    idx = torch.zeros((1, k), dtype=torch.int32, device=dev)
+    cnt = torch.zeros(1, dtype=torch.int32, device=dev)
+    out = torch.zeros((1, 1, D), dtype=torch.float32, device=dev)
+    scale = float(1 / np.sqrt(D))
+
+    def step(st=None):
+        hs.decode_step(q, kn, vn, 1, codes, kc, vc, capi.SPL_F32, n, nvalid, n, k, scale, idx, cnt,
+                       out, st if st is not None else stream)
+
+    for _ in range(args.warmup):
+        step()
+    eager_ms = event_timer(torch, step, args.steps, stream)
+    ctx.reserve(1, n, L, k, D)
+    g_ms = graph_timer(torch, lambda st: step(st), args.steps, args.warmup)
+    ms = g_ms if g_ms is not None else eager_ms
+    res = {"workload": "config1: 1 head, d=128, 4096 f32 keys, 128-bit codes, k=64; append + "
+                       "encode + retrieve + sparse attend",
+           "us_per_step": round(ms * 1000, 2), "eager_us_per_step": round(eager_ms * 1000, 2),
+           "timing": "CUDA graph replay of one decode step" if g_ms is not None else "eager",
+           "bound": "latency (L2-resident: 64 KB of codes, 65 x 1 KB K/V rows)"}
+    if RefLib.available():
+        ref = RefLib()
+        c_np = codes.cpu().numpy().view(np.uint32).reshape(1, n, W)
+        qc = np.zeros((1, W), np.uint32)
+        qcode = torch.zeros((1, 1, 1, W), dtype=torch.int32, device=dev)
+        hs.encode(q[None], 1, 1, qcode)
+        qc[0] = qcode.cpu().numpy().view(np.uint32).reshape(-1)
+        h = ref.index_create(c_np, np.array([n], np.uint32))
+        try:
+            times = []
+            for i in range(25):
+                t0 = time.perf_counter()
+                sel = ref.retrieve_batch(h, qc, np.array([n], np.uint32), k, threads=1)
+                picked = sorted(set(sel[0].tolist()) | {n - 1})
+                ref.sparse_attention(qv, keys, vals, scale, np.array([n], np.uint32), [picked])
+                if i >= 5:
+                    times.append((time.perf_counter() - t0) * 1e6)
+        finally:
+            ref.index_destroy(h)
+        res["reference_us_per_step"] = round(statistics.median(times), 1)
+        res["reference_path"] = ("unmodified reference: nxor_scores_into + top_k_indices + "
+                                 "sparse_attention, one host thread (the encode of the query "
+                                 "excluded on the reference side)")
+        same = sorted(idx[0, :int(cnt[0])].cpu().numpy().view(np.uint32).tolist()) == sorted(sel[0].tolist())
+        res["indices_equal_reference"] = bool(same)
+    return res
 
 def bench_accuracy(torch, capi, ctx, dev, stream, args):
     """Retrieval accuracy (the paper's Table-1 metric) at the
