@@ -206,6 +206,30 @@ __global__ void __launch_bounds__(kAttThreads) k4_sparse_attend(AttParams prm) {
     float M = -INFINITY;
 #pragma unroll
     for (int w = 0; w < kAttWarps; ++w) M = fmaxf(M, s_m[w]);
+    if (prm.nsplit == 1) {
+        // one split (short lists, e.g. config 1): the combine below reduces to
+        // out = o / L with unit scales, so write the result directly (same
+        // arithmetic) and skip the partials round trip and the counter
+        float Ls = 0.0f;
+#pragma unroll
+        for (int w = 0; w < kAttWarps; ++w)
+            if (s_m[w] != -INFINITY) Ls += s_l[w] * exp2f(s_m[w] - M);
+        for (int i = tid; i < D; i += kAttThreads) {
+            float acc = 0.0f;
+#pragma unroll
+            for (int w = 0; w < kAttWarps; ++w)
+                if (s_m[w] != -INFINITY) acc += s_o[w][i] * exp2f(s_m[w] - M);
+            if (prm.partial_mode)
+                prm.out[(uint64_t)p * (D + 2) + 2 + i] = acc;
+            else
+                prm.out[(uint64_t)p * D + i] = acc / Ls;
+        }
+        if (tid == 0 && prm.partial_mode) {
+            prm.out[(uint64_t)p * (D + 2)] = M;
+            prm.out[(uint64_t)p * (D + 2) + 1] = Ls;
+        }
+        return;
+    }
     float* part = prm.partials + ((uint64_t)p * prm.nsplit + split) * (D + 2);
     for (int i = tid; i < D; i += kAttThreads) {
         float acc = 0.0f;
