@@ -110,7 +110,13 @@ constexpr uint64_t kSegsPerCta = 1;
 #endif
 // 32-byte units per thread per load batch (x2 double-buffered): keeps
 // ~128 KB of loads in flight per SM at 512 (4 x 128) or 768 threads/SM
+// 32-byte units per thread per load group (two groups in flight). 256-bit
+// codes (W = 8, the two-pass config-4 scan) stream best with three:
+// config-4 retrieval 418 -> 398 us; 128-bit codes with two (three: config-3
+// 57.6 -> 60.7 us, config-2 decode 49.8 -> 51.4 us; four: worse on all).
 constexpr int kU = kThreads == 128 ? 4 : 2;
+template <int W>
+constexpr int units_for() { return W == 8 ? 3 : kU; }
 
 __device__ __forceinline__ uint64_t gtimer() {
     uint64_t t;
@@ -361,6 +367,7 @@ __device__ void stream_piece(const uint32_t* base, const uint32_t* qp, uint32_t 
     constexpr bool TR = DST_SMEM && sizeof(ScoreT) == 1;  // transposed layout (tpos)
     const int tid = threadIdx.x;
     if constexpr (W > 0) {
+        constexpr int KU = units_for<W>();
         constexpr int R = 8 / W;  // rows per 32-byte unit
         constexpr bool kClamp = sizeof(ScoreT) == 1 && W == 8;
         uint32_t q[W];
@@ -398,16 +405,16 @@ __device__ void stream_piece(const uint32_t* base, const uint32_t* qp, uint32_t 
         // transposed layout: row index of this thread's unit 0 relative to a0
         const uint32_t jb = (uint32_t)(uh * R - dst_row0) + (uint32_t)tid * R;
         const uint32_t dst0_s = TR ? (uint32_t)__cvta_generic_to_shared(dst) : 0u;
-        constexpr uint32_t per_it = (uint32_t)kThreads * kU;
+        constexpr uint32_t per_it = (uint32_t)kThreads * KU;
         const uint32_t nit = (nu + per_it - 1) / per_it;
         // private u8 counters: flush before any thread can add 256 to a bin
-        // (each iteration adds at most kU * R per thread; iterations go in pairs)
-        constexpr uint32_t kFlushPairs = (255 / (kU * R)) / 2 > 0 ? (255 / (kU * R)) / 2 : 1;
-        Unit32 a[kU], b[kU];
+        // (each iteration adds at most KU * R per thread; iterations go in pairs)
+        constexpr uint32_t kFlushPairs = (255 / (KU * R)) / 2 > 0 ? (255 / (KU * R)) / 2 : 1;
+        Unit32 a[KU], b[KU];
         auto load = [&](Unit32* buf, uint32_t it, bool check) {
             const uint32_t* p = ubase + (size_t)it * per_it * 8;
 #pragma unroll
-            for (int j = 0; j < kU; ++j)
+            for (int j = 0; j < KU; ++j)
                 if (!check || it * per_it + j * kThreads + tid < nu) buf[j].load(p, (uint32_t)j * kThreads);
         };
         auto count = [&](uint32_t sc) {
@@ -473,11 +480,11 @@ __device__ void stream_piece(const uint32_t* base, const uint32_t* qp, uint32_t 
         };
         auto process_full = [&](const Unit32* buf, uint32_t it) {
 #pragma unroll
-            for (int j = 0; j < kU; ++j) process_unit(buf[j], it, j);
+            for (int j = 0; j < KU; ++j) process_unit(buf[j], it, j);
         };
         auto process_tail = [&](const Unit32* buf, uint32_t it) {
 #pragma unroll
-            for (int j = 0; j < kU; ++j)
+            for (int j = 0; j < KU; ++j)
                 if (it * per_it + j * kThreads + tid < nu) process_unit(buf[j], it, j);
         };
         const uint32_t nfull = nu / per_it;  // iterations with every unit in range
