@@ -105,9 +105,6 @@ constexpr size_t kFastCarveBytes = 196 * 1024;
 // boundary costs a pipeline drain + flush; 2/4/8 per CTA: +1/+4/+11%)
 constexpr uint64_t kSegsPerCta = 1;
 #define K3_SEL_SCRATCH_BYTES ((size_t)kThreads * 11 * 4)  // select_rows_t8 masks
-#ifndef K3_EXP
-#define K3_EXP 0  // timing experiments only (tools/k3_exp.sh); 0 = product
-#endif
 // 32-byte units per thread per load batch (x2 double-buffered): keeps
 // ~128 KB of loads in flight per SM at 512 (4 x 128) or 768 threads/SM
 // 32-byte units per thread per load group (two groups in flight). 256-bit
@@ -432,17 +429,10 @@ __device__ void stream_piece(const uint32_t* base, const uint32_t* qp, uint32_t 
             uint32_t sc[R];
 #pragma unroll
             for (int r = 0; r < R; ++r) {
-#if K3_EXP >= 2  // experiment: no popcount
-                uint32_t x = 0;
-#pragma unroll
-                for (int w = 0; w < W; ++w) x ^= u.w[r * W + w] ^ q[w];
-                sc[r] = x & 127u;
-#else
                 uint32_t mism = 0;
 #pragma unroll
                 for (int w = 0; w < W; ++w) mism += __popc(u.w[r * W + w] ^ q[w]);
                 sc[r] = L - mism;
-#endif
             }
             // u8 scores at L = 256: stored as min(score, 255) (exact for
             // every threshold <= 254; the counters below see the true score)
@@ -473,10 +463,8 @@ __device__ void stream_piece(const uint32_t* base, const uint32_t* qp, uint32_t 
             } else {
                 store_scores<ScoreT, R>(udst + off, st);
             }
-#if K3_EXP == 0
 #pragma unroll
             for (int r = 0; r < R; ++r) count(sc[r]);
-#endif
         };
         auto process_full = [&](const Unit32* buf, uint32_t it) {
 #pragma unroll
@@ -736,10 +724,6 @@ __device__ void select_rows_t8(const uint8_t* sc, uint64_t a0, uint64_t r0, uint
         uint64_t tot;
         const uint64_t ex = block_excl_scan_u64(((uint64_t)eq << 32) | gt, s_warp, tot);
         if (tr && threadIdx.x == 0) { tr[10] = gtimer(); tr[14] = clock64(); }
-#if defined(K3_SEL_EXP) && K3_SEL_EXP == 2
-        if (ex == 0x123456789ull) out[0] = gm[0] ^ em[NV - 1];
-        return;
-#endif
         if (gt | eq) {
             uint32_t eb = carry_eq + (uint32_t)(ex >> 32);  // ties before this thread's rows
             uint32_t pos = carry_gt + (uint32_t)ex + (eb < take ? eb : take);
@@ -773,12 +757,7 @@ __device__ void select_rows_t8(const uint8_t* sc, uint64_t a0, uint64_t r0, uint
                 }
                 const uint32_t bb = __ffs(m) - 1;
                 m &= m - 1;
-#if defined(K3_SEL_EXP) && K3_SEL_EXP == 1
-                if (bb == 77) out[pos] = rowb;
-                pos++;
-#else
                 out[pos++] = rowb + 16u * v + 4 * (bb >> 3) + (bb & 7);
-#endif
             }
         }
         carry_gt += (uint32_t)tot;
