@@ -172,6 +172,15 @@ __global__ void __launch_bounds__(kAttThreads) k4_sparse_attend(AttParams prm) {
 #pragma unroll
     for (int e = 0; e < E; ++e) o[e] = 0.0f;
     if (nr > 0) {
+        // the V rows do not depend on the logits: start pulling this lane's V
+        // row into L2 now so the value phase below does not pay a second
+        // DRAM round trip after the K phase (random rows, cold L2)
+        if (rid != kInv) {
+            const char* vr = reinterpret_cast<const char*>(vbase + (uint64_t)rid * D);
+#pragma unroll
+            for (int b = 0; b < (int)(D * sizeof(KV)); b += 128)
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(vr + b));
+        }
         float s = -INFINITY;
         if (rid != kInv) s = row_dot<D, KV>(kbase + (uint64_t)rid * D, q_s);
         m = warp_max(s);
