@@ -670,9 +670,21 @@ spl_status spl_decode_step(spl_ctx* ctx, const spl_hasher* hs, const float* q,
     jobs[1].codes = qcodes;
     (void)W;
     if ((st = encode_exact_launch(ctx, hs, B, jobs, 2, S(stream)))) return st;
-    if ((st = hamming_topk_impl(ctx, codes, cap, hs->L, qcodes, P, n_valid, H, n_max, k, idx,
-                                cnt, S(stream))))
-        return st;
+    // the selected K/V rows are prefetched into L2 by the select when they
+    // fit it comfortably (config 2: 43 MB; flushed-L2 step 61.5 -> 59.4 us);
+    // larger gathers would thrash L2, tiny ones (config 1) only pay latency
+    const uint32_t row_bytes = hs->d * (kv_dtype == SPL_BF16 ? 2u : 4u);
+    const uint64_t pf_bytes = (uint64_t)P * (k + 1) * row_bytes * 2;
+    if (pf_bytes >= (4ull << 20) && pf_bytes <= (64ull << 20)) {
+        ctx->k3_pf_k = kcache;
+        ctx->k3_pf_v = vcache;
+        ctx->k3_pf_row_bytes = row_bytes;
+    }
+    st = hamming_topk_impl(ctx, codes, cap, hs->L, qcodes, P, n_valid, H, n_max, k, idx, cnt,
+                           S(stream));
+    ctx->k3_pf_k = ctx->k3_pf_v = nullptr;
+    ctx->k3_pf_row_bytes = 0;
+    if (st) return st;
     return spl_sparse_attend(ctx, q, kcache, vcache, kv_dtype, cap, hs->d, P, idx, k, cnt,
                              n_valid, H, scale, out, stream);
 }

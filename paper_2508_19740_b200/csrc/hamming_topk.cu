@@ -93,6 +93,12 @@ struct K3Params {
     uint32_t R, rank, Pmax;
     uint32_t* epoch_ptr;   // the group's call counter (device; advanced by the last CTA)
     uint32_t* out_offset;  // [P] position of this rank's first index in the global list
+    // optional (decode step): K / V caches laid out like the codes ([P][stride_rows]
+    // rows of pf_row_bytes); the fused select prefetches every emitted row of
+    // both into L2 so the attention gather that follows finds them there
+    const char* pf_k;
+    const char* pf_v;
+    uint32_t pf_row_bytes;
 };
 
 constexpr int kThreads = 256;
@@ -676,7 +682,9 @@ __device__ void select_rows(const ScoreT* sc, uint64_t a0, uint64_t r0, uint64_t
 template <int NV>
 __device__ void select_rows_t8(const uint8_t* sc, uint64_t a0, uint64_t r0, uint64_t r1,
                                uint32_t T, uint32_t take, uint32_t* out, uint64_t* s_warp,
-                               uint32_t* scratch, uint64_t* tr = nullptr) {
+                               uint32_t* scratch, uint64_t* tr = nullptr,
+                               const char* pfk = nullptr, const char* pfv = nullptr,
+                               uint32_t pfb = 0) {
     constexpr int CH = 16 * NV;  // rows per thread per round
     // T == 0: every row is >= T (x + 128 would carry for x = 128);
     // T >= 128: no row is > T
@@ -757,7 +765,16 @@ __device__ void select_rows_t8(const uint8_t* sc, uint64_t a0, uint64_t r0, uint
                 }
                 const uint32_t bb = __ffs(m) - 1;
                 m &= m - 1;
-                out[pos++] = rowb + 16u * v + 4 * (bb >> 3) + (bb & 7);
+                const uint32_t id = rowb + 16u * v + 4 * (bb >> 3) + (bb & 7);
+                out[pos++] = id;
+                if (pfk) {  // warm L2 for the attention gather (decode step)
+                    const char* kr = pfk + (uint64_t)id * pfb;
+                    const char* vr = pfv + (uint64_t)id * pfb;
+                    for (uint32_t b = 0; b < pfb; b += 128) {
+                        asm volatile("prefetch.global.L2 [%0];" ::"l"(kr + b));
+                        asm volatile("prefetch.global.L2 [%0];" ::"l"(vr + b));
+                    }
+                }
             }
         }
         carry_gt += (uint32_t)tot;
@@ -1290,12 +1307,17 @@ __global__ void __launch_bounds__(kThreads, 3) k3_fused(K3Params prm) {
         if constexpr (sizeof(ScoreT) == 1) {
             uint32_t* o = prm.idx_out + (uint64_t)p * prm.idx_stride + off;
             uint64_t* trp = prm.trace ? prm.trace + (uint64_t)blockIdx.x * 16 : nullptr;
+            const uint64_t pf_off = (uint64_t)p * prm.stride_rows * prm.pf_row_bytes;
+            const char* pfk = prm.pf_k ? prm.pf_k + pf_off : nullptr;
+            const char* pfv = prm.pf_v ? prm.pf_v + pf_off : nullptr;
             if (r1 - a0 <= (uint64_t)kThreads * 16 * 3)  // uniform
                 select_rows_t8<3>(reinterpret_cast<const uint8_t*>(sc), a0, r0, r1, T, take, o,
-                                  s_warp, reinterpret_cast<uint32_t*>(priv), trp);
+                                  s_warp, reinterpret_cast<uint32_t*>(priv), trp, pfk, pfv,
+                                  prm.pf_row_bytes);
             else
                 select_rows_t8<11>(reinterpret_cast<const uint8_t*>(sc), a0, r0, r1, T, take, o,
-                                   s_warp, reinterpret_cast<uint32_t*>(priv), trp);
+                                   s_warp, reinterpret_cast<uint32_t*>(priv), trp, pfk, pfv,
+                                   prm.pf_row_bytes);
         }
         else
             select_rows<ScoreT, false>(sc, a0, r0, r1, T, take,
@@ -1822,6 +1844,9 @@ spl_status hamming_topk_impl(spl_ctx* ctx, const uint32_t* codes, uint64_t strid
                 base_params(ctx, fp.pl, ws, kst, codes, stride_rows, L, qcodes, n_valid, nvalid_div, k);
             prm.cnt_out = cnt;
             prm.idx_out = idx;
+            prm.pf_k = static_cast<const char*>(ctx->k3_pf_k);
+            prm.pf_v = static_cast<const char*>(ctx->k3_pf_v);
+            prm.pf_row_bytes = ctx->k3_pf_row_bytes;
             prm.idx_stride = k;
             prm.hist_lo = fp.pl.hist_lo;
             prm.counters2 = kst.bar;

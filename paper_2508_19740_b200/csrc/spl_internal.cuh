@@ -22,6 +22,11 @@ struct spl_ctx {
     std::string err;
     uint64_t launches = 0;
     double last_train_loop_ms = 0.0;  // device time of the last spl_train_hasher loop
+    // decode step: K/V caches whose selected rows the K3 select prefetches
+    // into L2 for K4 (set by spl_decode_step when the gathered rows fit L2)
+    const void* k3_pf_k = nullptr;
+    const void* k3_pf_v = nullptr;
+    uint32_t k3_pf_row_bytes = 0;
 
     uint32_t* dev_err = nullptr;  // device error word (bit flags above)
 
