@@ -823,7 +823,7 @@ __global__ void k_dz(const float* __restrict__ dsoft, const float* __restrict__ 
 // (every output gets its own thread), 64-row chunks of A and B double-
 // buffered in shared memory with cp.async so the loads of chunk c + 1 run
 // under the chains of chunk c.
-constexpr int kAtRows = 128;   // rows per stage
+constexpr int kAtRows = 128;   // rows per stage (== the block size: one A slice per thread)
 constexpr int kAtStages = 4;   // cp.async ring depth (3 stages in flight)
 constexpr size_t kAtSmem = (size_t)kAtStages * kAtRows * 36 * 4;
 struct AtJob {
@@ -864,8 +864,34 @@ __global__ void __launch_bounds__(128) k_add_at(AtJob j0, AtJob j1, uint32_t row
     };
     const uint32_t bj = blockIdx.x * 32 + (threadIdx.x & 31);
     const uint32_t ai = blockIdx.y * 4 + (threadIdx.x & 3);
+    // 16-byte copies when every row slice is 16-byte aligned (m, nc multiples
+    // of 4): a quarter of the staging instructions
+    const bool v16 = (m & 3u) == 0 && (nc & 3u) == 0;
+    auto cp16 = [](float* dst, const float* src, uint32_t bytes) {
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(
+                         (uint32_t)__cvta_generic_to_shared(dst)),
+                     "l"(src), "r"(bytes)
+                     : "memory");
+    };
     auto stage = [&](uint32_t c) {  // always commits a group (possibly empty)
-        if (c < nch) {
+        if (c < nch && v16) {
+            const uint32_t r0 = c * kAtRows, buf = c % kAtStages;
+            float* bsb = bs + (size_t)buf * kAtRows * 32;
+            float* asb = as + (size_t)buf * kAtRows * 4;
+            const uint32_t q = threadIdx.x & 7, cb = blockIdx.x * 32 + 4 * q;  // 8 x 16 B per B row
+#pragma unroll
+            for (uint32_t k = 0; k < kAtRows / 16; ++k) {
+                const uint32_t r = (threadIdx.x >> 3) + 16 * k;
+                const uint32_t left = (r0 + r < rows && cb < nc) ? min(4u, nc - cb) * 4u : 0u;
+                cp16(bsb + r * 32 + 4 * q, left ? B + (uint64_t)(r0 + r) * nc + cb : B, left);
+            }
+            {  // A: one 16-byte slice (4 output rows) per staged row
+                const uint32_t r = threadIdx.x;  // kAtRows == blockDim.x
+                const uint32_t a0 = blockIdx.y * 4;
+                const uint32_t left = (r0 + r < rows && a0 < m) ? min(4u, m - a0) * 4u : 0u;
+                cp16(asb + r * 4, left ? A + (uint64_t)(r0 + r) * m + a0 : A, left);
+            }
+        } else if (c < nch) {
             const uint32_t r0 = c * kAtRows, buf = c % kAtStages;
             float* bsb = bs + (size_t)buf * kAtRows * 32;
             float* asb = as + (size_t)buf * kAtRows * 4;
