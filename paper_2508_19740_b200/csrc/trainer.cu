@@ -283,12 +283,20 @@ __device__ __forceinline__ void fwd_layer(const float* in, uint32_t K, const flo
     }
 }
 
+// n floats global -> shared, 16-byte copies when both sides allow it
 __device__ __forceinline__ void cp_async_f32(float* dst, const float* src, uint64_t n) {
-    for (uint64_t e = threadIdx.x; e < n; e += blockDim.x)
-        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(
-                         (uint32_t)__cvta_generic_to_shared(dst + e)),
-                     "l"(src + e)
-                     : "memory");
+    const uint32_t ds = (uint32_t)__cvta_generic_to_shared(dst);
+    if ((n & 3u) == 0 && (ds & 15u) == 0 && (reinterpret_cast<uintptr_t>(src) & 15u) == 0) {
+        for (uint64_t e = 4 * (uint64_t)threadIdx.x; e < n; e += 4 * (uint64_t)blockDim.x)
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(ds + (uint32_t)e * 4),
+                         "l"(src + e)
+                         : "memory");
+    } else {
+        for (uint64_t e = threadIdx.x; e < n; e += blockDim.x)
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(ds + (uint32_t)e * 4),
+                         "l"(src + e)
+                         : "memory");
+    }
     asm volatile("cp.async.commit_group;" ::: "memory");
 }
 
@@ -789,6 +797,13 @@ __global__ void __launch_bounds__(256) k_dsoft_keys(const float* __restrict__ G,
     dsk[e] = invb != 1.0f ? __fmul_rn(acc, invb) : acc;
 }
 
+__global__ void k_transpose(const float* __restrict__ a, uint32_t rows, uint32_t cols,
+                            float* __restrict__ at) {  // at[c][r] = a[r][c]
+    for (uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < (uint64_t)rows * cols;
+         e += (uint64_t)gridDim.x * blockDim.x)
+        at[(e % cols) * rows + e / cols] = a[e];
+}
+
 __global__ void k_scale(float* x, uint64_t n, float s, const TrainDev* st) {
     if (st->halt) return;
     for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
@@ -945,23 +960,17 @@ __global__ void __launch_bounds__(128) k_add_at(AtJob j0, AtJob j1, uint32_t row
 // its hidden unit (rounded products summed in order, fused tail).
 constexpr int kDaRows = 16;
 __global__ void __launch_bounds__(128) k_da1(const float* __restrict__ dz2,
-                                             const float* __restrict__ w2,
+                                             const float* __restrict__ w2t,
                                              const float* __restrict__ z1, uint32_t m, uint32_t h,
                                              uint32_t L, float* __restrict__ da1,
                                              const TrainDev* st) {
     if (st->halt) return;
     extern __shared__ float sm[];
-    float* ws = sm;                       // [h][L + 1]
-    float* zs = sm + (size_t)h * (L + 1); // [kDaRows][L]
+    float* ws = sm;                       // [L][h]: W2^T
+    float* zs = sm + (size_t)h * L;       // [L][kDaRows] (p-major)
     const uint32_t r0 = blockIdx.x * kDaRows;
     const uint32_t nr = min((uint32_t)kDaRows, m - r0);
-    for (uint32_t i = 0; i < h; ++i)  // row i of W2 -> padded row of ws (async, 4-byte)
-        for (uint32_t p = threadIdx.x; p < L; p += blockDim.x)
-            asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(
-                             (uint32_t)__cvta_generic_to_shared(ws + (size_t)i * (L + 1) + p)),
-                         "l"(w2 + (uint64_t)i * L + p)
-                         : "memory");
-    asm volatile("cp.async.commit_group;" ::: "memory");
+    cp_async_f32(ws, w2t, (uint64_t)L * h);  // W2^T [L][h] (kept by k_adamw), contiguous
     for (uint32_t r = 0; r < kDaRows; ++r)  // p-major: zs[p][r] (zero rows past m)
         for (uint32_t p = threadIdx.x; p < L; p += blockDim.x)
             asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(
@@ -973,12 +982,12 @@ __global__ void __launch_bounds__(128) k_da1(const float* __restrict__ dz2,
     __syncthreads();
     const uint32_t n4 = n4_of(L);
     for (uint32_t i = threadIdx.x; i < h; i += blockDim.x) {
-        const float* wr = ws + (size_t)i * (L + 1);
+        const float* wr = ws + i;  // W2[i][p] = ws[p * h + i] (consecutive i: no conflicts)
         float acc[kDaRows];
 #pragma unroll
         for (int r = 0; r < kDaRows; ++r) acc[r] = 0.0f;
         for (uint32_t p = 0; p < L; ++p) {
-            const float wv = wr[p];
+            const float wv = wr[(size_t)p * h];
             const float4* zp = reinterpret_cast<const float4*>(zs + p * kDaRows);
             float z[kDaRows];
 #pragma unroll
@@ -1077,7 +1086,8 @@ __global__ void k_clip(const double* part, const int* bad, double max_norm, cons
 // [0, n_decay0) and [n_decay1, n) (the weight matrices, not b1).
 __global__ void k_adamw(float* w, const float* g, double* m1, double* m2, uint64_t n,
                         uint64_t n_decay0, uint64_t n_decay1, double lr, double b1, double b2,
-                        double eps, double wd, const TrainDev* st) {
+                        double eps, double wd, const TrainDev* st, float* w2t, uint32_t h,
+                        uint32_t L) {
     if (st->halt || st->skip_now) return;
     const double bc1 = st->bc1, bc2 = st->bc2;
     const double c1 = __dsub_rn(1.0, b1), c2 = __dsub_rn(1.0, b2);
@@ -1094,7 +1104,12 @@ __global__ void k_adamw(float* w, const float* g, double* m1, double* m2, uint64
         const double w_old = (double)w[i];
         double w_new = __dsub_rn(w_old, __ddiv_rn(__dmul_rn(lr, mhat), __dadd_rn(__dsqrt_rn(vhat), eps)));
         if (wd > 0.0 && (i < n_decay0 || i >= n_decay1)) w_new = __fma_rn(-lwd, w_old, w_new);
-        w[i] = __double2float_rn(w_new);
+        const float wf = __double2float_rn(w_new);
+        w[i] = wf;
+        if (w2t && i >= n_decay1) {  // MLP: keep the transposed W2 copy for k_da1
+            const uint64_t e = i - n_decay1;
+            w2t[(e % L) * h + e / L] = wf;
+        }
     }
 }
 
@@ -1472,6 +1487,14 @@ spl_status train_impl(spl_ctx* ctx, int kind, uint32_t d, uint32_t h, uint32_t L
     const float* W1 = dP;
     const float* B1 = dP + n1;
     const float* W2 = dP + n1 + nb;
+    float* W2T = nullptr;  // MLP: W2 transposed [L][h] for k_da1 (k_adamw keeps it current)
+    if (mlp) {
+        W2T = db.get<float>((size_t)h * L);
+        if (!W2T) return fail(ctx, SPL_E_CUDA, "train: out of device memory");
+        k_transpose<<<(unsigned)std::min<uint64_t>(((uint64_t)h * L + 255) / 256, 1024), 256, 0, s>>>(
+            W2, h, L, W2T);
+        if (spl_status st = after_launch(ctx, "k_transpose")) return st;
+    }
     // forward: weights staged in shared memory when they fit (one block/SM)
     const size_t wbytes = (mlp ? (size_t)d * h + (size_t)h * L : (size_t)d * L) * 4;
     const size_t fwd_base = (size_t)kFwdRows * (d + (mlp ? h : 0)) * 4;
@@ -1503,7 +1526,7 @@ spl_status train_impl(spl_ctx* ctx, int kind, uint32_t d, uint32_t h, uint32_t L
     float* xg = db.get<float>((size_t)maxQ * d);  // gathered query inputs for add_at
     if (!xg) return fail(ctx, SPL_E_CUDA, "train: out of device memory");
     SPL_CUDA_TRY(ctx, cudaFuncSetAttribute(k_add_at, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kAtSmem));
-    const size_t da1_smem = mlp ? ((size_t)h * (L + 1) + (size_t)kDaRows * L) * 4 : 0;
+    const size_t da1_smem = mlp ? ((size_t)h * L + (size_t)kDaRows * L) * 4 : 0;
     if (da1_smem > 220 * 1024)
         return fail(ctx, SPL_E_DIMENSION, "train_hasher: hidden x code width too large for the GPU trainer");
     if (mlp)
@@ -1521,7 +1544,7 @@ spl_status train_impl(spl_ctx* ctx, int kind, uint32_t d, uint32_t h, uint32_t L
         if (mlp) {
             // da1 first, then W2 += a1^T dz2 and W1 += x^T da1 (+ b1) in one
             // launch: independent accumulators, so the order between them is free
-            k_da1<<<(m + kDaRows - 1) / kDaRows, 128, da1_smem, s>>>(dzp, W2, z1, m, h, L, da1, dst);
+            k_da1<<<(m + kDaRows - 1) / kDaRows, 128, da1_smem, s>>>(dzp, W2T, z1, m, h, L, da1, dst);
             if (spl_status st = after_launch(ctx, "k_da1")) return st;
             const AtJob jw2{a1, dzp, gW2, nullptr, h, L}, jw1{x, da1, gW1, gB1, d, h};
             const dim3 grid((std::max(L, h) + 31) / 32, (std::max(h, d) + 3) / 4, 2);
@@ -1612,7 +1635,7 @@ spl_status train_impl(spl_ctx* ctx, int kind, uint32_t d, uint32_t h, uint32_t L
         if (spl_status st = after_launch(ctx, "k_clip")) return st;
         k_adamw<<<(unsigned)std::min<uint64_t>((np + 255) / 256, 1184), 256, 0, s>>>(
             dP, dG, dM, dV, np, n1, n1 + nb, lr, tc.adam_beta1, tc.adam_beta2, tc.adam_eps,
-            tc.weight_decay, dst);
+            tc.weight_decay, dst, mlp ? W2T : nullptr, h, L);
         if (spl_status st = after_launch(ctx, "k_adamw")) return st;
     }
 
