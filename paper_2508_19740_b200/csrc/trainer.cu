@@ -546,27 +546,21 @@ __global__ void __launch_bounds__(256) k_rank_grad(const float* __restrict__ sof
     // (acc starts at +0 and the pair gradients are >= 0), so the chains run
     // over every slot. gb: 32-column tiles of g staged through shared memory
     // (coalesced), each thread continuing its row's chain across tiles.
-    double* tile = gsum + T + O + (size_t)(T + O);  // after eg/ek: [T][33]
-    for (uint32_t i = threadIdx.x; i < T; i += blockDim.x) gsum[i] = 0.0;  // running chains
-    for (uint32_t j0 = 0; j0 < O; j0 += 32) {
-        const uint32_t w = min(32u, O - j0);
-        for (uint32_t e = threadIdx.x; e < T * 32; e += blockDim.x) {  // async, zero-filled
-            const uint32_t i = e >> 5, jj = e & 31;
-            const bool ok = jj < w;
-            asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(
-                             (uint32_t)__cvta_generic_to_shared(tile + i * 33 + jj)),
-                         "l"(ok ? g + (uint64_t)i * O + j0 + jj : g), "r"(ok ? 8 : 0)
-                         : "memory");
+    // gb: each thread walks its row of g in order, 32 loads in flight ahead of
+    // the chain (rows are contiguous; L1 serves the rest of each sector)
+    for (uint32_t i = threadIdx.x; i < T; i += blockDim.x) {
+        const double* row = g + (uint64_t)i * O;
+        double acc = 0.0;
+        uint32_t j = 0;
+        for (; j + 32 <= O; j += 32) {
+            double v[32];
+#pragma unroll
+            for (int u = 0; u < 32; ++u) v[u] = row[j + u];
+#pragma unroll
+            for (int u = 0; u < 32; ++u) acc = __dsub_rn(acc, v[u]);
         }
-        asm volatile("cp.async.commit_group;" ::: "memory");
-        asm volatile("cp.async.wait_group 0;" ::: "memory");
-        __syncthreads();
-        for (uint32_t i = threadIdx.x; i < T; i += blockDim.x) {
-            double acc = gsum[i];
-            for (uint32_t jj = 0; jj < w; ++jj) acc = __dsub_rn(acc, tile[i * 33 + jj]);
-            gsum[i] = acc;
-        }
-        __syncthreads();
+        for (; j < O; ++j) acc = __dsub_rn(acc, row[j]);
+        gsum[i] = acc;
     }
     for (uint32_t i = threadIdx.x; i < T; i += blockDim.x)
         if (ti[i] == ~0u) gsum[i] = 0.0;
@@ -1443,7 +1437,7 @@ spl_status train_impl(spl_ctx* ctx, int kind, uint32_t d, uint32_t h, uint32_t L
         maxT = std::max<uint32_t>(maxT, (uint32_t)w.top_pos.size());
         maxO = std::max<uint32_t>(maxO, (uint32_t)w.oth_pos.size());
     }
-    const size_t grad_smem = (size_t)(maxT + maxO) * 16 + (size_t)maxT * 33 * 8;
+    const size_t grad_smem = (size_t)(maxT + maxO) * 16;
     if (grad_smem > 200 * 1024)
         return fail(ctx, SPL_E_DIMENSION, "train_hasher: sampled pair set too large for one block "
                                           "(set max_top / max_oth)");
@@ -1597,7 +1591,7 @@ spl_status train_impl(spl_ctx* ctx, int kind, uint32_t d, uint32_t h, uint32_t L
                 k_rank_pairs<<<dim3(Qs, pb), kPairThreads, 0, s>>>(bcv, top_idx, T, oth_idx, O, rc.beta,
                                                                     rc.alpha, gpair, lpart, vpart, dst);
                 if (spl_status st = after_launch(ctx, "k_rank_pairs")) return st;
-                k_rank_grad<<<Qs, 256, (size_t)(T + O) * 16 + (size_t)T * 33 * 8, s>>>(
+                k_rank_grad<<<Qs, 256, (size_t)(T + O) * 16, s>>>(
                     sfk, L, top_idx, T, oth_idx, O, Qs, gpair, Gm, dsq, dst);
                 if (spl_status st = after_launch(ctx, "k_rank_grad")) return st;
                 k_loss_finalize<<<1, 256, 0, s>>>(lpart, vpart, Qs * pb, b, tc.batch, it, drec, dst, 0.0);
