@@ -313,7 +313,7 @@ __global__ void __launch_bounds__(kFwdThreads) k_forward(const float* __restrict
     float* xs = sm;                       // [kFwdRows][d]
     float* as = sm + kFwdRows * d;        // [kFwdRows][h] (MLP)
     float* w1s = as + (KIND == SPL_HASHER_MLP ? kFwdRows * h : 0);  // [d][h | L]
-    float* w2s = w1s + (size_t)d * (KIND == SPL_HASHER_MLP ? h : L);  // [h][L] (MLP)
+    float* w2s = w1s;  // MLP: layer-2 weights reuse the layer-1 buffer (2 blocks / SM)
     const uint32_t r0 = blockIdx.x * kFwdRows;
     const uint32_t nr = min((uint32_t)kFwdRows, m - r0);
     for (uint32_t r = 0; r < kFwdRows; ++r) {  // async row staging, zero rows past m
@@ -326,14 +326,9 @@ __global__ void __launch_bounds__(kFwdThreads) k_forward(const float* __restrict
                          : "memory");
     }
     asm volatile("cp.async.commit_group;" ::: "memory");
-    if (WSMEM) {  // group 2: layer-1 weights; group 3 (MLP): layer-2 weights, under layer 1
+    if (WSMEM) {  // group 2: layer-1 weights (layer 2's are staged after layer 1)
         cp_async_f32(w1s, w1, (uint64_t)d * (KIND == SPL_HASHER_MLP ? h : L));
-        if (KIND == SPL_HASHER_MLP) {
-            cp_async_f32(w2s, w2, (uint64_t)h * L);
-            asm volatile("cp.async.wait_group 1;" ::: "memory");
-        } else {
-            asm volatile("cp.async.wait_group 0;" ::: "memory");
-        }
+        asm volatile("cp.async.wait_group 0;" ::: "memory");
     } else {
         asm volatile("cp.async.wait_group 0;" ::: "memory");
     }
@@ -360,8 +355,12 @@ __global__ void __launch_bounds__(kFwdThreads) k_forward(const float* __restrict
                 }
             }
         }
-        if (WSMEM) asm volatile("cp.async.wait_group 0;" ::: "memory");
-        __syncthreads();
+        __syncthreads();  // layer 1 done with the weight buffer
+        if (WSMEM) {
+            cp_async_f32(w2s, w2, (uint64_t)h * L);
+            asm volatile("cp.async.wait_group 0;" ::: "memory");
+            __syncthreads();
+        }
         in = as + rbase * h;
         K = h;
         W = WSMEM ? w2s : w2;
@@ -1490,7 +1489,7 @@ spl_status train_impl(spl_ctx* ctx, int kind, uint32_t d, uint32_t h, uint32_t L
         if (spl_status st = after_launch(ctx, "k_transpose")) return st;
     }
     // forward: weights staged in shared memory when they fit (one block/SM)
-    const size_t wbytes = (mlp ? (size_t)d * h + (size_t)h * L : (size_t)d * L) * 4;
+    const size_t wbytes = (mlp ? std::max((size_t)d * h, (size_t)h * L) : (size_t)d * L) * 4;
     const size_t fwd_base = (size_t)kFwdRows * (d + (mlp ? h : 0)) * 4;
     const bool wsmem = fwd_base + wbytes <= 220 * 1024;
     const size_t fwd_smem = fwd_base + (wsmem ? wbytes : 0);
