@@ -679,7 +679,7 @@ __device__ void select_rows(const ScoreT* sc, uint64_t a0, uint64_t r0, uint64_t
 // free once the stream is over). NV = 3 for short segments (<= 12 K rows,
 // e.g. the config-2 decode shape): the per-thread work is unrolled over NV
 // vectors whether they hold rows or not.
-template <int NV>
+template <int NV, bool PF = false>
 __device__ void select_rows_t8(const uint8_t* sc, uint64_t a0, uint64_t r0, uint64_t r1,
                                uint32_t T, uint32_t take, uint32_t* out, uint64_t* s_warp,
                                uint32_t* scratch, uint64_t* tr = nullptr,
@@ -767,7 +767,7 @@ __device__ void select_rows_t8(const uint8_t* sc, uint64_t a0, uint64_t r0, uint
                 m &= m - 1;
                 const uint32_t id = rowb + 16u * v + 4 * (bb >> 3) + (bb & 7);
                 out[pos++] = id;
-                if (pfk) {  // warm L2 for the attention gather (decode step)
+                if constexpr (PF) {  // warm L2 for the attention gather (decode step)
                     const char* kr = pfk + (uint64_t)id * pfb;
                     const char* vr = pfv + (uint64_t)id * pfb;
                     for (uint32_t b = 0; b < pfb; b += 128) {
@@ -1087,7 +1087,7 @@ __device__ ShardPlanOut shard_global_plan(const K3Params& prm, uint32_t epoch, u
 // (shard_global_plan) and compacts its rows as usual — one launch, no
 // host-side collective. Local positions, plus out_offset[p] into the global
 // list (rank order = index order, as in spl_shard_select).
-template <int W, typename ScoreT, bool SHARD = false>
+template <int W, typename ScoreT, bool SHARD = false, bool PF = false>
 __global__ void __launch_bounds__(kThreads, 3) k3_fused(K3Params prm) {
     extern __shared__ __align__(16) uint8_t smem[];
     __shared__ uint64_t s_warp[kThreads / 32 + 1];
@@ -1311,13 +1311,13 @@ __global__ void __launch_bounds__(kThreads, 3) k3_fused(K3Params prm) {
             const char* pfk = prm.pf_k ? prm.pf_k + pf_off : nullptr;
             const char* pfv = prm.pf_v ? prm.pf_v + pf_off : nullptr;
             if (r1 - a0 <= (uint64_t)kThreads * 16 * 3)  // uniform
-                select_rows_t8<3>(reinterpret_cast<const uint8_t*>(sc), a0, r0, r1, T, take, o,
-                                  s_warp, reinterpret_cast<uint32_t*>(priv), trp, pfk, pfv,
-                                  prm.pf_row_bytes);
+                select_rows_t8<3, PF>(reinterpret_cast<const uint8_t*>(sc), a0, r0, r1, T, take, o,
+                                      s_warp, reinterpret_cast<uint32_t*>(priv), trp, pfk, pfv,
+                                      prm.pf_row_bytes);
             else
-                select_rows_t8<11>(reinterpret_cast<const uint8_t*>(sc), a0, r0, r1, T, take, o,
-                                   s_warp, reinterpret_cast<uint32_t*>(priv), trp, pfk, pfv,
-                                   prm.pf_row_bytes);
+                select_rows_t8<11, PF>(reinterpret_cast<const uint8_t*>(sc), a0, r0, r1, T, take, o,
+                                       s_warp, reinterpret_cast<uint32_t*>(priv), trp, pfk, pfv,
+                                       prm.pf_row_bytes);
         }
         else
             select_rows<ScoreT, false>(sc, a0, r0, r1, T, take,
@@ -1566,13 +1566,14 @@ struct K3FPlan {
     const void* fn;
 };
 
-template <int W, typename ScoreT, bool SHARD = false>
+template <int W, typename ScoreT, bool SHARD = false, bool PF = false>
 const void* fused_fn() {
-    return reinterpret_cast<const void*>(&k3_fused<W, ScoreT, SHARD>);
+    return reinterpret_cast<const void*>(&k3_fused<W, ScoreT, SHARD, PF>);
 }
 
 spl_status make_fused_plan(spl_ctx* ctx, uint32_t P, uint64_t n_max, uint32_t L, const void* codes,
-                           uint64_t stride_rows, bool* ok, K3FPlan* out, bool shard = false) {
+                           uint64_t stride_rows, bool* ok, K3FPlan* out, bool shard = false,
+                           bool pf = false) {
     *ok = false;
     const uint32_t W = L / 32;
     // Private counters cover scores [L/2, L] only: the k-th best agreement is
@@ -1588,7 +1589,10 @@ spl_status make_fused_plan(spl_ctx* ctx, uint32_t P, uint64_t n_max, uint32_t L,
         switch (W) {
             case 1: fn = shard ? fused_fn<1, uint8_t, true>() : fused_fn<1, uint8_t>(); break;
             case 2: fn = shard ? fused_fn<2, uint8_t, true>() : fused_fn<2, uint8_t>(); break;
-            case 4: fn = shard ? fused_fn<4, uint8_t, true>() : fused_fn<4, uint8_t>(); break;
+            case 4:
+                fn = shard ? fused_fn<4, uint8_t, true>()
+                           : (pf ? fused_fn<4, uint8_t, false, true>() : fused_fn<4, uint8_t>());
+                break;
             default: return SPL_OK;
         }
     } else if (shard) {
@@ -1836,7 +1840,10 @@ spl_status hamming_topk_impl(spl_ctx* ctx, const uint32_t* codes, uint64_t strid
     if (fused_allowed()) {
         bool ok = false;
         K3FPlan fp{};
-        if ((st = make_fused_plan(ctx, P, n_max, L, codes, stride_rows, &ok, &fp))) return st;
+        // the decode step's prefetching variant (select warms L2 for K4) is a
+        // separate instantiation: the plain retrieval kernel carries no trace of it
+        const bool pf = ctx->k3_pf_k != nullptr;
+        if ((st = make_fused_plan(ctx, P, n_max, L, codes, stride_rows, &ok, &fp, false, pf))) return st;
         if (ok) {
             K3Ws ws;
             if ((st = k3_workspace(ctx, fp.pl, L, s, &ws, false))) return st;
