@@ -259,14 +259,14 @@ __device__ __forceinline__ void fwd_layer(const float* in, uint32_t K, const flo
 #pragma unroll
     for (int r = 0; r < kFwdRg; ++r) acc[r] = 0.0f;
     uint32_t p = 0;
-    if (WSMEM) {
+    if constexpr (WSMEM) {
         for (; p < K; ++p) {
             const float w = W[(size_t)p * ncol + j];
 #pragma unroll
             for (int r = 0; r < kFwdRg; ++r) acc[r] = __fmaf_rn(in[r * K + p], w, acc[r]);
         }
         return;
-    }
+    } else {
     for (; p + 32 <= K; p += 32) {
         float w[32];
 #pragma unroll
@@ -280,6 +280,7 @@ __device__ __forceinline__ void fwd_layer(const float* in, uint32_t K, const flo
         const float w = W[(uint64_t)p * ncol + j];
 #pragma unroll
         for (int r = 0; r < kFwdRg; ++r) acc[r] = __fmaf_rn(in[r * K + p], w, acc[r]);
+    }
     }
 }
 
@@ -307,7 +308,7 @@ __global__ void __launch_bounds__(kFwdThreads) k_forward(const float* __restrict
                                                          const float* __restrict__ b1,
                                                          const float* __restrict__ w2, float gamma,
                                                          float* z1, float* a1, float* z2, float* soft,
-                                                         const TrainDev* st) {
+                                                         const TrainDev* st, float* xcopy) {
     if (st->halt) return;
     extern __shared__ float sm[];
     float* xs = sm;                       // [kFwdRows][d]
@@ -333,6 +334,8 @@ __global__ void __launch_bounds__(kFwdThreads) k_forward(const float* __restrict
         asm volatile("cp.async.wait_group 0;" ::: "memory");
     }
     __syncthreads();
+    if (xcopy)  // the gathered query rows, kept for the weight gradients (gather_rows)
+        for (uint32_t e = threadIdx.x; e < nr * d; e += blockDim.x) xcopy[(uint64_t)r0 * d + e] = xs[e];
     const uint32_t lane = threadIdx.x & 127, rg = threadIdx.x >> 7;
     const uint32_t rbase = rg * kFwdRg;  // this thread's rows: rbase .. rbase + kFwdRg - 1
     const float* in = xs + rbase * d;
@@ -804,14 +807,6 @@ __global__ void k_scale(float* x, uint64_t n, float s, const TrainDev* st) {
         x[i] = __fmul_rn(x[i], s);
 }
 
-__global__ void k_gather_rows(const float* __restrict__ x, const uint32_t* rows, uint32_t d,
-                              float* __restrict__ out, const TrainDev* st) {
-    if (st->halt) return;
-    const uint64_t src = rows[blockIdx.x];
-    for (uint32_t c = threadIdx.x; c < d; c += blockDim.x)
-        out[(uint64_t)blockIdx.x * d + c] = x[src * d + c];
-}
-
 // ------------------------------------------------------------ backward
 // dz = d_soft * soft_sign_grad(z) (trainer.cpp:222-225, :253-257)
 __global__ void k_dz(const float* __restrict__ dsoft, const float* __restrict__ z, uint64_t n,
@@ -1077,18 +1072,26 @@ __global__ void k_clip(const double* part, const int* bad, double max_norm, cons
 
 // adamw_step's update (trainer.cpp:122-139), f64 moments; decay on
 // [0, n_decay0) and [n_decay1, n) (the weight matrices, not b1).
-__global__ void k_adamw(float* w, const float* g, double* m1, double* m2, uint64_t n,
+__global__ void k_adamw(float* w, float* g, double* m1, double* m2, uint64_t n,
                         uint64_t n_decay0, uint64_t n_decay1, double lr, double b1, double b2,
                         double eps, double wd, const TrainDev* st, float* w2t, uint32_t h,
                         uint32_t L) {
-    if (st->halt || st->skip_now) return;
+    if (st->halt) return;
+    if (st->skip_now) {  // skipped step: gradients still restart from zero
+        for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+             i += (uint64_t)gridDim.x * blockDim.x)
+            g[i] = 0.0f;
+        return;
+    }
     const double bc1 = st->bc1, bc2 = st->bc2;
     const double c1 = __dsub_rn(1.0, b1), c2 = __dsub_rn(1.0, b2);
     const double lwd = __dmul_rn(lr, wd);
     const float sc = st->scale;
     for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
          i += (uint64_t)gridDim.x * blockDim.x) {
-        const double gv = (double)(sc != 1.0f ? __fmul_rn(g[i], sc) : g[i]);
+        const float gr = g[i];
+        g[i] = 0.0f;  // the next iteration's gradients start from zero (no memset launch)
+        const double gv = (double)(sc != 1.0f ? __fmul_rn(gr, sc) : gr);
         const double m = __fma_rn(b1, m1[i], __dmul_rn(c1, gv));
         const double v = __fma_rn(b2, m2[i], __dmul_rn(__dmul_rn(c2, gv), gv));
         m1[i] = m;
@@ -1349,6 +1352,7 @@ spl_status train_impl(spl_ctx* ctx, int kind, uint32_t d, uint32_t h, uint32_t L
         SPL_CUDA_TRY(ctx, cudaMemcpyAsync(dP + n1 + nb, w2, n2 * 4, cudaMemcpyHostToDevice, s));
     }
     SPL_CUDA_TRY(ctx, cudaMemsetAsync(dM, 0, np * 8, s));
+    SPL_CUDA_TRY(ctx, cudaMemsetAsync(dG, 0, np * 4, s));  // k_adamw re-zeroes it every step
     SPL_CUDA_TRY(ctx, cudaMemsetAsync(dV, 0, np * 8, s));
     SPL_CUDA_TRY(ctx, cudaMemsetAsync(dst, 0, sizeof(TrainDev), s));
     SPL_CUDA_TRY(ctx, cudaMemsetAsync(drec, 0, ((size_t)iters * 3 + 3) * 8, s));
@@ -1505,9 +1509,9 @@ spl_status train_impl(spl_ctx* ctx, int kind, uint32_t d, uint32_t h, uint32_t L
             if (spl_status st = fwd_attr(f)) return st;
     }
     auto fwd = [&](const float* x, const uint32_t* rows, uint32_t m, float* a, float* b, float* c,
-                   float* sf) -> spl_status {
+                   float* sf, float* xcopy) -> spl_status {
         const dim3 grid((m + kFwdRows - 1) / kFwdRows);
-#define SPL_FWD(K_, WS_) k_forward<K_, WS_><<<grid, kFwdThreads, fwd_smem, s>>>(x, rows, m, d, K_ == SPL_HASHER_MLP ? h : 0, L, W1, K_ == SPL_HASHER_MLP ? B1 : nullptr, K_ == SPL_HASHER_MLP ? W2 : nullptr, sgamma, a, b, c, sf, dst)
+#define SPL_FWD(K_, WS_) k_forward<K_, WS_><<<grid, kFwdThreads, fwd_smem, s>>>(x, rows, m, d, K_ == SPL_HASHER_MLP ? h : 0, L, W1, K_ == SPL_HASHER_MLP ? B1 : nullptr, K_ == SPL_HASHER_MLP ? W2 : nullptr, sgamma, a, b, c, sf, dst, xcopy)
         if (kind == SPL_HASHER_MLP) { if (wsmem) SPL_FWD(SPL_HASHER_MLP, true); else SPL_FWD(SPL_HASHER_MLP, false); }
         else if (kind == SPL_HASHER_LINEAR) { if (wsmem) SPL_FWD(SPL_HASHER_LINEAR, true); else SPL_FWD(SPL_HASHER_LINEAR, false); }
         else { if (wsmem) SPL_FWD(2, true); else SPL_FWD(2, false); }
@@ -1566,7 +1570,6 @@ spl_status train_impl(spl_ctx* ctx, int kind, uint32_t d, uint32_t h, uint32_t L
     const std::chrono::steady_clock::time_point pt0 = std::chrono::steady_clock::now();
     for (uint32_t it = 0; it < iters; ++it) {
         const double lr = train_lr_at(it, tc);
-        SPL_CUDA_TRY(ctx, cudaMemsetAsync(dG, 0, np * 4, s));
         for (uint32_t b = 0; b < tc.batch; ++b) {
             const size_t di = (size_t)it * tc.batch + b;
             const Sample& w = draws[di];
@@ -1580,8 +1583,8 @@ spl_status train_impl(spl_ctx* ctx, int kind, uint32_t d, uint32_t h, uint32_t L
             SPL_CUDA_TRY(ctx, cudaMemsetAsync(Gm, 0, (size_t)n * Qs * 4, s));
             k_partition<<<Qs, 256, 0, s>>>(p.order, n, w.k_full, qrows, tpos, T, opos, O, top_idx, oth_idx, dst);
             if (spl_status st = after_launch(ctx, "k_partition")) return st;
-            if (spl_status st = fwd(p.x_q, qrows, Qs, z1q, a1q, z2q, sfq)) return st;
-            if (spl_status st = fwd(p.x_k, nullptr, n, z1k, a1k, z2k, sfk)) return st;
+            if (spl_status st = fwd(p.x_q, qrows, Qs, z1q, a1q, z2q, sfq, xg)) return st;
+            if (spl_status st = fwd(p.x_k, nullptr, n, z1k, a1k, z2k, sfk, nullptr)) return st;
             if (!recon) {
                 k_rank_dots<<<dim3(Qs, (T + O + 127) / 128), 128, (size_t)L * 4, s>>>(
                     sfq, sfk, L, top_idx, T, oth_idx, O, bcv, dst, it);
@@ -1615,10 +1618,6 @@ spl_status train_impl(spl_ctx* ctx, int kind, uint32_t d, uint32_t h, uint32_t L
                 k_scale<<<(Qs * L + 255) / 256, 256, 0, s>>>(dsq, (uint64_t)Qs * L, invb, dst);
                 if (spl_status st = after_launch(ctx, "k_scale")) return st;
             }
-            // the selected query rows (gather_rows, trainer.cpp:455-464) for
-            // the query-side weight gradients
-            k_gather_rows<<<Qs, 128, 0, s>>>(p.x_q, qrows, d, xg, dst);
-            if (spl_status st = after_launch(ctx, "k_gather_rows")) return st;
             if (spl_status st = bwd(xg, Qs, z1q, a1q, z2q, dsq)) return st;
             if (spl_status st = bwd(p.x_k, n, z1k, a1k, z2k, dsk)) return st;
         }
