@@ -482,6 +482,7 @@ __global__ void __launch_bounds__(128) k_rank_dots(const float* __restrict__ sof
 }
 
 constexpr int kPairThreads = 256;
+constexpr int kPairsPerThread = 4;
 __global__ void __launch_bounds__(kPairThreads) k_rank_pairs(const double* __restrict__ bc,
                                                              const uint32_t* top_idx, uint32_t T,
                                                              const uint32_t* oth_idx, uint32_t O,
@@ -495,18 +496,20 @@ __global__ void __launch_bounds__(kPairThreads) k_rank_pairs(const double* __res
     __shared__ unsigned long long s_viol[kPairThreads / 32];
     const uint32_t qi = blockIdx.x;
     const double inv = __ddiv_rn(1.0, (double)st->pairs);
-    const uint64_t e = (uint64_t)blockIdx.y * kPairThreads + threadIdx.x;
     double loss = 0.0;
     unsigned long long viol = 0;
-    if (e < (uint64_t)T * O) {
+    // kPairsPerThread pairs per thread (block-strided): fewer loss partials
+    for (int u = 0; u < kPairsPerThread; ++u) {
+        const uint64_t e = ((uint64_t)blockIdx.y * kPairsPerThread + u) * kPairThreads + threadIdx.x;
+        if (e >= (uint64_t)T * O) break;
         const uint32_t i = (uint32_t)(e / O), j = (uint32_t)(e % O);
         double g = 0.0;
         if (top_idx[(uint64_t)qi * T + i] != ~0u && oth_idx[(uint64_t)qi * O + j] != ~0u) {
             const double* row = bc + (uint64_t)qi * (T + O);
             const double z = __dsub_rn(row[i], row[T + j]);
             const double logit = __fma_rn(beta, z, -alpha);
-            loss = softplus_d(-logit);
-            viol = z < 0.0;
+            loss = __dadd_rn(loss, softplus_d(-logit));
+            viol += z < 0.0;
             g = pair_g(logit, beta, inv);
         }
         gp[(uint64_t)qi * T * O + e] = g;
@@ -1445,7 +1448,9 @@ spl_status train_impl(spl_ctx* ctx, int kind, uint32_t d, uint32_t h, uint32_t L
         return fail(ctx, SPL_E_DIMENSION, "train_hasher: sampled pair set too large for one block "
                                           "(set max_top / max_oth)");
     SPL_CUDA_TRY(ctx, cudaFuncSetAttribute(k_rank_grad, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)grad_smem));
-    const uint64_t pair_blocks = ((uint64_t)maxT * maxO + kPairThreads - 1) / kPairThreads;
+    const uint64_t pair_blocks = std::max<uint64_t>(
+        ((uint64_t)maxT * maxO + kPairThreads * kPairsPerThread - 1) / (kPairThreads * kPairsPerThread),
+        (max_n + 255) / 256);  // also the reconstruction loss's blocks per query
     const uint32_t hw = mlp ? h : 1;
     float *z1q = db.get<float>((size_t)maxQ * hw), *a1q = db.get<float>((size_t)maxQ * hw);
     float *z2q = db.get<float>((size_t)maxQ * L), *sfq = db.get<float>((size_t)maxQ * L);
@@ -1589,7 +1594,8 @@ spl_status train_impl(spl_ctx* ctx, int kind, uint32_t d, uint32_t h, uint32_t L
                 k_rank_dots<<<dim3(Qs, (T + O + 127) / 128), 128, (size_t)L * 4, s>>>(
                     sfq, sfk, L, top_idx, T, oth_idx, O, bcv, dst, it);
                 if (spl_status st = after_launch(ctx, "k_rank_dots")) return st;
-                const uint32_t pb = (uint32_t)(((uint64_t)T * O + kPairThreads - 1) / kPairThreads);
+                const uint32_t pb = (uint32_t)(((uint64_t)T * O + kPairThreads * kPairsPerThread - 1) /
+                                               (kPairThreads * kPairsPerThread));
                 k_rank_pairs<<<dim3(Qs, pb), kPairThreads, 0, s>>>(bcv, top_idx, T, oth_idx, O, rc.beta,
                                                                     rc.alpha, gpair, lpart, vpart, dst);
                 if (spl_status st = after_launch(ctx, "k_rank_pairs")) return st;
