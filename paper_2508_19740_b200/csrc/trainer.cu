@@ -767,33 +767,60 @@ __global__ void k_loss_finalize(const double* loss_part, const unsigned long lon
 // d soft_k = G^T-chain: dk[key][p] = fma over the selected queries in order
 // of G[key][qi] * sq[qi][p] (zero G entries are the reference's skipped
 // pairs); x (1/batch) when batch > 1 (trainer.cpp:591-595).
-__global__ void __launch_bounds__(256) k_dsoft_keys(const float* __restrict__ G,
-                                                    const float* __restrict__ softq, uint32_t Qs,
-                                                    uint32_t n, uint32_t L, float invb,
-                                                    float* __restrict__ dsk, const TrainDev* st) {
+// large query sets (no query_subsample): one thread per (key, code position)
+__global__ void __launch_bounds__(256) k_dsoft_keys_flat(const float* __restrict__ G,
+                                                         const float* __restrict__ softq, uint32_t Qs,
+                                                         uint32_t n, uint32_t L, float invb,
+                                                         float* __restrict__ dsk, const TrainDev* st) {
     if (st->halt) return;
     const uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (e >= (uint64_t)n * L) return;
     const uint64_t key = e / L;
     const uint32_t p = (uint32_t)(e % L);
     float acc = 0.0f;
-    uint32_t q = 0;
-    for (; q + 16 <= Qs; q += 16) {  // loads batched ahead of the chain
-        float gv[16], sv[16];
-#pragma unroll
-        for (int u = 0; u < 16; ++u) {
-            gv[u] = G[key * Qs + q + u];
-            sv[u] = softq[(uint64_t)(q + u) * L + p];
-        }
-#pragma unroll
-        for (int u = 0; u < 16; ++u)
-            if (gv[u] != 0.0f) acc = __fmaf_rn(gv[u], sv[u], acc);
-    }
-    for (; q < Qs; ++q) {
+    for (uint32_t q = 0; q < Qs; ++q) {
         const float g = G[key * Qs + q];
         if (g != 0.0f) acc = __fmaf_rn(g, softq[(uint64_t)q * L + p], acc);
     }
     dsk[e] = invb != 1.0f ? __fmul_rn(acc, invb) : acc;
+}
+
+// softq and this block's G rows staged in shared memory; each thread runs the
+// chains of 8 keys for one code position
+constexpr int kDkKeys = 16;  // keys per block (2 groups of 8 per 128-column lane set)
+__global__ void __launch_bounds__(256) k_dsoft_keys(const float* __restrict__ G,
+                                                    const float* __restrict__ softq, uint32_t Qs,
+                                                    uint32_t n, uint32_t L, float invb,
+                                                    float* __restrict__ dsk, const TrainDev* st) {
+    if (st->halt) return;
+    extern __shared__ float dk_sm[];
+    float* sq = dk_sm;                        // [Qs][L] soft query codes
+    float* gs = dk_sm + (size_t)Qs * L;       // [kDkKeys][Qs] g values of this block's keys
+    const uint32_t key0 = blockIdx.x * kDkKeys;
+    const uint32_t nk = min((uint32_t)kDkKeys, n - key0);
+    cp_async_f32(sq, softq, (uint64_t)Qs * L);
+    for (uint32_t e = threadIdx.x; e < kDkKeys * Qs; e += blockDim.x)
+        gs[e] = e < nk * Qs ? G[(uint64_t)key0 * Qs + e] : 0.0f;
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+    __syncthreads();
+    const uint32_t kg = (threadIdx.x >> 7) * (kDkKeys / 2);  // this thread's 8 keys
+    for (uint32_t p = threadIdx.x & 127; p < L; p += 128) {
+        float acc[kDkKeys / 2];
+#pragma unroll
+        for (int k = 0; k < kDkKeys / 2; ++k) acc[k] = 0.0f;
+        for (uint32_t q = 0; q < Qs; ++q) {  // one fma chain per key, queries in order
+            const float sv = sq[(size_t)q * L + p];
+#pragma unroll
+            for (int k = 0; k < kDkKeys / 2; ++k) {
+                const float g = gs[(kg + k) * Qs + q];
+                if (g != 0.0f) acc[k] = __fmaf_rn(g, sv, acc[k]);
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < kDkKeys / 2; ++k)
+            if (kg + k < nk)
+                dsk[(uint64_t)(key0 + kg + k) * L + p] = invb != 1.0f ? __fmul_rn(acc[k], invb) : acc[k];
+    }
 }
 
 __global__ void k_transpose(const float* __restrict__ a, uint32_t rows, uint32_t cols,
@@ -1443,6 +1470,10 @@ spl_status train_impl(spl_ctx* ctx, int kind, uint32_t d, uint32_t h, uint32_t L
         maxT = std::max<uint32_t>(maxT, (uint32_t)w.top_pos.size());
         maxO = std::max<uint32_t>(maxO, (uint32_t)w.oth_pos.size());
     }
+    auto dk_smem = [&](uint32_t qs) { return ((size_t)qs * L + (size_t)kDkKeys * qs) * 4; };
+    const bool dk_staged = dk_smem(maxQ) <= 200 * 1024;
+    if (dk_staged)
+        SPL_CUDA_TRY(ctx, cudaFuncSetAttribute(k_dsoft_keys, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dk_smem(maxQ)));
     const size_t grad_smem = (size_t)(maxT + maxO) * 16;
     if (grad_smem > 200 * 1024)
         return fail(ctx, SPL_E_DIMENSION, "train_hasher: sampled pair set too large for one block "
@@ -1618,7 +1649,10 @@ spl_status train_impl(spl_ctx* ctx, int kind, uint32_t d, uint32_t h, uint32_t L
                 k_loss_finalize<<<1, 256, 0, s>>>(lpart, vpart, Qs * yb, b, tc.batch, it, drec, dst, count);
                 if (spl_status st = after_launch(ctx, "k_loss_finalize")) return st;
             }
-            k_dsoft_keys<<<(unsigned)(((uint64_t)n * L + 255) / 256), 256, 0, s>>>(Gm, sfq, Qs, n, L, invb, dsk, dst);
+            if (dk_staged)
+                k_dsoft_keys<<<(n + kDkKeys - 1) / kDkKeys, 256, dk_smem(Qs), s>>>(Gm, sfq, Qs, n, L, invb, dsk, dst);
+            else
+                k_dsoft_keys_flat<<<(unsigned)(((uint64_t)n * L + 255) / 256), 256, 0, s>>>(Gm, sfq, Qs, n, L, invb, dsk, dst);
             if (spl_status st = after_launch(ctx, "k_dsoft_keys")) return st;
             if (invb != 1.0f && !recon) {
                 k_scale<<<(Qs * L + 255) / 256, 256, 0, s>>>(dsq, (uint64_t)Qs * L, invb, dst);
