@@ -76,6 +76,11 @@ spl_status spl_reserve(spl_ctx* ctx, uint32_t P, uint64_t n_max, uint32_t L, uin
 spl_status spl_check_device_error(spl_ctx* ctx, void* stream);
 /* Number of kernels this context launched so far (bench gpu_launches). */
 uint64_t spl_launch_count(const spl_ctx* ctx);
+/* Names of the kernels this context launched since the previous call, ';'-
+ * separated (e.g. "k1_encode_cluster;k3_fused_pf;k4_gather;"), copied into buf
+ * (host, NUL-terminated, truncated to len) and cleared. Returns the full
+ * length. Lets tests assert which kernel variant a call ran. */
+size_t spl_launch_log(spl_ctx* ctx, char* buf, size_t len);
 
 /* memory helpers for callers that do not link the CUDA runtime (the C++
  * drop-in uses these; `kind`: 0 = default/UVA). */

@@ -80,6 +80,7 @@ _SIGS = {
     "spl_reserve": [vp, u32, u64, u32, u32, u32],
     "spl_check_device_error": [vp, vp],
     "spl_launch_count": [vp],
+    "spl_launch_log": [vp, C.c_char_p, C.c_size_t],
     "spl_device_alloc": [vp, C.c_size_t, C.POINTER(vp)],
     "spl_device_free": [vp, vp],
     "spl_memcpy": [vp, vp, vp, C.c_size_t, vp],
@@ -124,7 +125,8 @@ _SIGS = {
 _RESTYPE = {"spl_version": C.c_char_p, "spl_train_lr_at": C.c_double,
             "spl_train_last_loop_ms": C.c_double, "spl_last_error": C.c_char_p, "spl_ctx_destroy": None,
             "spl_peer_destroy": None,
-            "spl_hasher_destroy": None, "spl_launch_count": C.c_uint64}
+            "spl_hasher_destroy": None, "spl_launch_count": C.c_uint64,
+            "spl_launch_log": C.c_size_t}
 
 
 def header_symbols() -> list[str]:
@@ -280,6 +282,12 @@ class Context:
 
     def launches(self) -> int:
         return self.lib.spl_launch_count(self.h)
+
+    def launch_log(self) -> list[str]:
+        """Kernel names launched since the previous call (then cleared)."""
+        buf = C.create_string_buffer(8192)
+        self.lib.spl_launch_log(self.h, buf, len(buf))
+        return [x for x in buf.value.decode().split(";") if x]
 
     def reserve(self, P, n_max, L, k, d=0):
         self.check(self.lib.spl_reserve(self.h, P, n_max, L, k, d))

@@ -117,6 +117,18 @@ const char* spl_last_error(const spl_ctx* ctx) { return ctx ? ctx->err.c_str() :
 
 uint64_t spl_launch_count(const spl_ctx* ctx) { return ctx ? ctx->launches : 0; }
 
+size_t spl_launch_log(spl_ctx* ctx, char* buf, size_t len) {
+    if (!ctx) return 0;
+    const size_t n = ctx->launch_log.size();
+    if (buf && len) {
+        const size_t m = n < len - 1 ? n : len - 1;
+        memcpy(buf, ctx->launch_log.data(), m);
+        buf[m] = '\0';
+    }
+    ctx->launch_log.clear();
+    return n;
+}
+
 spl_status spl_reserve(spl_ctx* ctx, uint32_t P, uint64_t n_max, uint32_t L, uint32_t k,
                        uint32_t d) {
     if (!ctx) return SPL_E_STATE;
@@ -137,7 +149,8 @@ spl_status spl_reserve(spl_ctx* ctx, uint32_t P, uint64_t n_max, uint32_t L, uin
     if (st) return st;
     ctx->k3_state_words = have / 4;
     if (d > 0) {
-        const size_t splits_max = ((size_t)k + 1 + 63) / 64 + 1;
+        const size_t rps = att_rows_per_split();
+        const size_t splits_max = ((size_t)k + 1 + rps - 1) / rps;
         st = ensure_buffer(ctx, reinterpret_cast<void**>(&ctx->att_ws), &ctx->att_ws_bytes,
                            (size_t)P * splits_max * (d + 2) * 4, false, 0, "spl_reserve");
         if (st) return st;
@@ -160,7 +173,8 @@ spl_status spl_check_device_error(spl_ctx* ctx, void* stream) {
     if (flags & SPL_DEV_ERR_NUMERIC)
         return fail(ctx, SPL_E_NUMERIC, "mlp input contains non-finite values");
     if (flags & SPL_DEV_ERR_DIMENSION)
-        return fail(ctx, SPL_E_DIMENSION, "attention: causal offset outside the cache");
+        return fail(ctx, SPL_E_DIMENSION,
+                    "decode: causal offset / append slot outside the cache (n_valid == 0 or >= capacity)");
     if (flags & SPL_DEV_ERR_STALL)
         return fail(ctx, SPL_E_CUDA,
                     "hamming_topk: fused kernel CTAs were not co-resident (watchdog); "
@@ -644,6 +658,10 @@ spl_status spl_decode_step(spl_ctx* ctx, const spl_hasher* hs, const float* q,
                            float scale, uint32_t* idx, uint32_t* cnt, float* out, void* stream) {
     NvtxRange nvtx_("spl_decode_step");
     if (!ctx || !hs) return SPL_E_STATE;
+    if (n_max > cap)
+        return fail(ctx, SPL_E_DIMENSION,
+                    "decode_step: n_max=" + std::to_string(n_max) + " exceeds the cache capacity " +
+                        std::to_string(cap));
     const uint32_t H = hs->H, W = hs->L / 32, P = B * H;
     // query codes live in the context scratch
     spl_status st = ensure_buffer(ctx, &ctx->scratch, &ctx->scratch_bytes,
@@ -670,6 +688,15 @@ spl_status spl_decode_step(spl_ctx* ctx, const spl_hasher* hs, const float* q,
     jobs[1].codes = qcodes;
     (void)W;
     if ((st = encode_exact_launch(ctx, hs, B, jobs, 2, S(stream)))) return st;
+    // retrieval and attention in one launch when the fused geometry applies
+    // (L = d = 128, scores on chip): each K3 CTA attends the rows it selects
+    bool done = false;
+    if (!(scale > 0.0f)) return fail(ctx, SPL_E_DIMENSION, "attention: scale must be positive");
+    if ((st = hamming_topk_attend_impl(ctx, codes, cap, hs->L, qcodes, P, n_valid, H, n_max, k, idx,
+                                       cnt, q, kcache, vcache, kv_dtype, hs->d, scale * kLog2e, out,
+                                       S(stream), &done)))
+        return st;
+    if (done) return SPL_OK;
     // the selected K/V rows are prefetched into L2 by the select when they
     // fit it comfortably (config 2: 43 MB; flushed-L2 step 61.5 -> 59.4 us);
     // larger gathers would thrash L2, tiny ones (config 1) only pay latency

@@ -59,6 +59,20 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
         : "memory");
 }
 
+// Append slot of batch b: pos[b] - pos_minus_one, or ~0 when it falls outside
+// [0, cap) (n_valid == 0 in a decode step, a full cache): the caller skips the
+// write and the device error word reports a DimensionError instead of a wild
+// store into the next head's rows.
+__device__ __forceinline__ uint64_t append_slot(const EncJob& job, uint32_t b, uint32_t* dev_err,
+                                                bool report) {
+    const uint32_t pos = job.pos[b];
+    if (pos < (uint32_t)job.pos_minus_one || (uint64_t)(pos - job.pos_minus_one) >= job.cap) {
+        if (report) raise_dev_err(dev_err, SPL_DEV_ERR_DIMENSION);
+        return ~0ull;
+    }
+    return pos - job.pos_minus_one;
+}
+
 __global__ void __launch_bounds__(kEncThreads) k1_encode_exact(EncParams prm) {
     extern __shared__ __align__(128) float esm[];
     __shared__ __align__(8) uint64_t s_bar;
@@ -175,11 +189,13 @@ __global__ void __launch_bounds__(kEncThreads) k1_encode_exact(EncParams prm) {
                     const uint32_t bits = __ballot_sync(0xffffffffu, acc[v] >= 0.0f);
                     if (lane == 0) {
                         uint64_t row;
-                        if (job.out_mode == ENC_APPEND)
-                            row = ((uint64_t)b * H + head) * job.cap + (job.pos[b] - job.pos_minus_one);
-                        else
+                        if (job.out_mode == ENC_APPEND) {
+                            const uint64_t slot = append_slot(job, b, prm.dev_err, w == 0);
+                            row = slot == ~0ull ? ~0ull : ((uint64_t)b * H + head) * job.cap + slot;
+                        } else {
                             row = ((uint64_t)b * H + head) * job.m + mi;
-                        job.codes[row * W + w] = __brev(bits);
+                        }
+                        if (row != ~0ull) job.codes[row * W + w] = __brev(bits);
                     }
                 }
             }
@@ -191,8 +207,9 @@ __global__ void __launch_bounds__(kEncThreads) k1_encode_exact(EncParams prm) {
                 const uint32_t v = i / d, c = i % d;
                 const uint32_t b = v0 + v;  // m == 1
                 const uint64_t src = ((uint64_t)b * H + head) * d + c;
-                const uint64_t dst =
-                    (((uint64_t)b * H + head) * job.cap + (job.pos[b] - job.pos_minus_one)) * d + c;
+                const uint64_t slot = append_slot(job, b, prm.dev_err, false);
+                if (slot == ~0ull) continue;
+                const uint64_t dst = (((uint64_t)b * H + head) * job.cap + slot) * d + c;
                 const float kv = xs[v * d + c];
                 const float vv = job.v_new[src];
                 if (job.kv_dtype == SPL_BF16) {
@@ -410,11 +427,13 @@ __global__ void __cluster_dims__(kCS, 1, 1) __launch_bounds__(kEncThreads)
                     const uint32_t bits = __ballot_sync(0xffffffffu, z >= 0.0f);
                     if (lane == 0) {
                         uint64_t row;
-                        if (job.out_mode == ENC_APPEND)
-                            row = ((uint64_t)b * H + head) * job.cap + (job.pos[b] - job.pos_minus_one);
-                        else
+                        if (job.out_mode == ENC_APPEND) {
+                            const uint64_t slot = append_slot(job, b, prm.dev_err, w == 0);
+                            row = slot == ~0ull ? ~0ull : ((uint64_t)b * H + head) * job.cap + slot;
+                        } else {
                             row = ((uint64_t)b * H + head) * job.m + mi;
-                        job.codes[row * W + w] = __brev(bits);
+                        }
+                        if (row != ~0ull) job.codes[row * W + w] = __brev(bits);
                     }
                 }
             }
@@ -425,8 +444,9 @@ __global__ void __cluster_dims__(kCS, 1, 1) __launch_bounds__(kEncThreads)
                 const uint32_t v = i / d, c = i % d;
                 const uint32_t b = v0 + v;  // m == 1
                 const uint64_t src = ((uint64_t)b * H + head) * d + c;
-                const uint64_t dst =
-                    (((uint64_t)b * H + head) * job.cap + (job.pos[b] - job.pos_minus_one)) * d + c;
+                const uint64_t slot = append_slot(job, b, prm.dev_err, false);
+                if (slot == ~0ull) continue;
+                const uint64_t dst = (((uint64_t)b * H + head) * job.cap + slot) * d + c;
                 const float kv = xs[v * d + c];
                 const float vv = job.v_new[src];
                 if (job.kv_dtype == SPL_BF16) {

@@ -35,6 +35,7 @@
 #include <vector>
 #include <cstring>
 
+#include "spl_attend.cuh"
 #include "spl_launch.cuh"
 #include "spl_plan.cuh"
 
@@ -99,6 +100,17 @@ struct K3Params {
     const char* pf_k;
     const char* pf_v;
     uint32_t pf_row_bytes;
+    // decode step (k3_fused<.., ATT>): every CTA attends the rows it just
+    // selected (K/V rows at pf_k / pf_v, head dim 128) and the CTA finishing a
+    // problem's last segment combines the per-segment partials (log-sum-exp)
+    const float* att_q;    // [P][128] f32 queries
+    float att_qscale;      // scale * log2(e)
+    float* att_part;       // [(G + P)][130] per-segment (m, l, o[128])
+    uint32_t* att_cnt;     // [P] segments attended (self-resetting)
+    float* att_out;        // [P][128]
+    int att_pf;            // 1: the select also prefetches the emitted rows into L2
+                           // (SPL_ATT_PF=1; measured no faster than without: the
+                           // gather is DRAM-bound either way)
 };
 
 constexpr int kThreads = 256;
@@ -679,12 +691,15 @@ __device__ void select_rows(const ScoreT* sc, uint64_t a0, uint64_t r0, uint64_t
 // free once the stream is over). NV = 3 for short segments (<= 12 K rows,
 // e.g. the config-2 decode shape): the per-thread work is unrolled over NV
 // vectors whether they hold rows or not.
+// PF (decode step): prefetch each emitted row's K and V lines into L2 (when
+// pfk is set); ids (optional, shared memory): a copy of the first n_ids
+// emitted ids for the attention that follows in the same kernel.
 template <int NV, bool PF = false>
 __device__ void select_rows_t8(const uint8_t* sc, uint64_t a0, uint64_t r0, uint64_t r1,
                                uint32_t T, uint32_t take, uint32_t* out, uint64_t* s_warp,
                                uint32_t* scratch, uint64_t* tr = nullptr,
                                const char* pfk = nullptr, const char* pfv = nullptr,
-                               uint32_t pfb = 0) {
+                               uint32_t pfb = 0, uint32_t* ids = nullptr, uint32_t n_ids = 0) {
     constexpr int CH = 16 * NV;  // rows per thread per round
     // T == 0: every row is >= T (x + 128 would carry for x = 128);
     // T >= 128: no row is > T
@@ -766,8 +781,12 @@ __device__ void select_rows_t8(const uint8_t* sc, uint64_t a0, uint64_t r0, uint
                 const uint32_t bb = __ffs(m) - 1;
                 m &= m - 1;
                 const uint32_t id = rowb + 16u * v + 4 * (bb >> 3) + (bb & 7);
+                if constexpr (PF) {
+                    if (pos < n_ids) ids[pos] = id;
+                }
                 out[pos++] = id;
                 if constexpr (PF) {  // warm L2 for the attention gather (decode step)
+                    if (!pfk) continue;
                     const char* kr = pfk + (uint64_t)id * pfb;
                     const char* vr = pfv + (uint64_t)id * pfb;
                     for (uint32_t b = 0; b < pfb; b += 128) {
@@ -1067,6 +1086,166 @@ __device__ ShardPlanOut shard_global_plan(const K3Params& prm, uint32_t epoch, u
     return o;
 }
 
+// ------------------------------------------------------------ fused attend
+// Shared-memory layout of the private-counter region once the stream is over
+// (decode step, k3_fused<.., ATT>): [select masks: NV x kThreads words]
+// [attention merge / combine scratch: kAttScratch floats] [emitted ids].
+// The select copies the first att_ids_cap ids it emits there, so the
+// attention that follows does not read them back from L2.
+constexpr uint32_t kAttScratchWords = 2 * 8 + 8 * 128;  // warp merge (the combine needs less)
+__device__ __forceinline__ uint32_t att_ids_off_words(uint32_t nv_sel) {
+    const uint32_t masks = nv_sel * kThreads;
+    return masks > kAttScratchWords ? masks : kAttScratchWords;
+}
+template <bool ATT>
+__device__ __forceinline__ uint32_t* att_ids(uint8_t* priv, size_t priv_bytes, uint32_t nv_sel) {
+    if constexpr (!ATT) return nullptr;
+    return reinterpret_cast<uint32_t*>(priv) + att_ids_off_words(nv_sel);
+}
+template <bool ATT>
+__device__ __forceinline__ uint32_t att_ids_cap(size_t priv_bytes, uint32_t nv_sel) {
+    if constexpr (!ATT) return 0;
+    const size_t words = priv_bytes / 4, off = att_ids_off_words(nv_sel);
+    return words > off ? (uint32_t)(words - off) : 0u;
+}
+
+// Decode step, after a CTA compacted its rows of problem p (count entries at
+// idx_out[p][off..), the first ids_cap of them also in shared memory): attend
+// them (sparse_attention, attention_eval.cpp:234-264) right here instead of
+// in a K4 launch. The CTA whose segment holds the own row nv - 1 adds it when
+// it was not selected (:249-260). The 8 warps split the CTA's entries
+// (warp_attend: 8-row batches, the K and V slices of a batch in flight
+// together), merge (m, l, o) in shared memory and write the segment's
+// partial; the CTA completing the problem's last segment merges the nseg
+// partials (log-sum-exp, every load of the merge issued in one round) into
+// att_out[p]. Every CTA of the problem calls this (those with no rows write
+// an empty partial). scratch: kAttScratchWords floats.
+template <typename KV>
+__device__ void fused_attend(const K3Params& prm, uint32_t p, uint32_t seg, uint32_t c0,
+                             uint32_t nseg, uint32_t nv, bool owner, uint64_t off, uint32_t count,
+                             float* scratch, const uint32_t* sids, uint32_t ids_cap,
+                             uint32_t* s_flag) {
+    constexpr int E = 4, D = 128, NW = kThreads / 32;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    float qv[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) qv[e] = __ldg(prm.att_q + (uint64_t)p * D + lane * E + e) * prm.att_qscale;
+    const uint32_t* gids = prm.idx_out + (uint64_t)p * prm.idx_stride + off;
+    const bool smem_ids = count <= ids_cap;
+    __syncthreads();  // the emitted ids (shared / global) and the select's masks are complete
+    uint32_t extra = kAttInv;
+    if (owner && nv > 0) {
+        const uint32_t last = count == 0 ? kAttInv : (smem_ids ? sids[count - 1] : __ldcg(gids + count - 1));
+        if (last != nv - 1) extra = nv - 1;
+    }
+    const uint32_t total = count + (extra != kAttInv ? 1u : 0u);
+    const uint32_t per = (total + NW - 1) / NW;
+    const uint32_t j0 = min(total, warp * per), j1 = min(total, j0 + per);
+    const uint64_t rb = (uint64_t)p * prm.stride_rows;
+    const KV* kbase = reinterpret_cast<const KV*>(prm.pf_k) + rb * D;
+    const KV* vbase = reinterpret_cast<const KV*>(prm.pf_v) + rb * D;
+    float m = -INFINITY, lsum = 0.0f, o[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) o[e] = 0.0f;
+    if (j0 < j1) {
+        if (smem_ids)
+            warp_attend<E, KV, true>(kbase, vbase, sids, count, extra, j0, j1, qv, m, lsum, o);
+        else
+            warp_attend<E, KV, false>(kbase, vbase, gids, count, extra, j0, j1, qv, m, lsum, o);
+    }
+    const float l = attend_lsum_total(lsum);
+    // merge the warps -> this segment's partial (m, l, o)
+    float* s_m = scratch;            // [NW]
+    float* s_l = scratch + NW;       // [NW]
+    float* s_o = scratch + 2 * NW;   // [NW][D]
+    __syncthreads();  // every warp is done with the ids (they may share the region)
+    if (lane == 0) {
+        s_m[warp] = m;
+        s_l[warp] = l;
+    }
+#pragma unroll
+    for (int e = 0; e < E; ++e) s_o[warp * D + lane * E + e] = o[e];
+    __syncthreads();
+    float M = -INFINITY;
+#pragma unroll
+    for (int w = 0; w < NW; ++w) M = fmaxf(M, s_m[w]);
+    float* part = prm.att_part + (uint64_t)(seg + p) * (D + 2);
+    if (tid < D) {
+        float acc = 0.0f;
+#pragma unroll
+        for (int w = 0; w < NW; ++w)
+            if (s_m[w] != -INFINITY) acc += s_o[w * D + tid] * exp2f(s_m[w] - M);
+        part[2 + tid] = acc;
+    } else if (tid == D) {
+        float Ls = 0.0f;
+#pragma unroll
+        for (int w = 0; w < NW; ++w)
+            if (s_m[w] != -INFINITY) Ls += s_l[w] * exp2f(s_m[w] - M);
+        part[0] = M;
+        part[1] = Ls;
+    }
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) *s_flag = (atomicAdd(prm.att_cnt + p, 1u) + 1 == nseg) ? 1u : 0u;
+    __syncthreads();
+    if (!*s_flag) return;
+    // last segment of p: combine the nseg partials (slots c + p, c in [c0, c0 + nseg)).
+    // Thread (half, dim) takes the partials i = half, half + 2, ...; their m,
+    // l and o[dim] are loaded together (one round), scaled after the max.
+    __threadfence();
+    const float* base = prm.att_part + (uint64_t)(c0 + p) * (D + 2);
+    const uint32_t dim = tid & (D - 1), half = tid / D;
+    constexpr int kMaxPer = 8;  // partials per thread per round
+    float Mx = -INFINITY, Lx = 0.0f, acc = 0.0f;
+    for (uint32_t i0 = half; i0 < nseg; i0 += 2 * kMaxPer) {
+        float mv[kMaxPer], lv[kMaxPer], ov[kMaxPer];
+#pragma unroll
+        for (int j = 0; j < kMaxPer; ++j) {
+            const uint32_t i = i0 + 2 * j;
+            mv[j] = -INFINITY;
+            lv[j] = ov[j] = 0.0f;
+            if (i < nseg) {
+                const float* pp = base + (uint64_t)i * (D + 2);
+                mv[j] = __ldcg(pp);
+                lv[j] = __ldcg(pp + 1);
+                ov[j] = __ldcg(pp + 2 + dim);
+            }
+        }
+        float Mn = Mx;
+#pragma unroll
+        for (int j = 0; j < kMaxPer; ++j) Mn = fmaxf(Mn, mv[j]);
+        const float r = Mx == -INFINITY ? 0.0f : exp2f(Mx - Mn);
+        acc *= r;
+        Lx *= r;
+#pragma unroll
+        for (int j = 0; j < kMaxPer; ++j) {
+            const float sc = mv[j] == -INFINITY ? 0.0f : exp2f(mv[j] - Mn);
+            acc = fmaf(ov[j], sc, acc);
+            Lx = fmaf(lv[j], sc, Lx);
+        }
+        Mx = Mn;
+    }
+    // merge the two halves
+    float* s_hm = scratch;           // [2] per-half max (all threads of a half agree)
+    float* s_hl = scratch + 2;       // [2]
+    float* s_ha = scratch + 4;       // [2][D]
+    __syncthreads();
+    if (dim == 0) {
+        s_hm[half] = Mx;
+        s_hl[half] = Lx;
+    }
+    s_ha[half * D + dim] = acc;
+    __syncthreads();
+    if (tid < D) {
+        const float M2 = fmaxf(s_hm[0], s_hm[1]);
+        const float f0 = s_hm[0] == -INFINITY ? 0.0f : exp2f(s_hm[0] - M2);
+        const float f1 = s_hm[1] == -INFINITY ? 0.0f : exp2f(s_hm[1] - M2);
+        const float Lt = s_hl[0] * f0 + s_hl[1] * f1;
+        prm.att_out[(uint64_t)p * D + tid] = (s_ha[tid] * f0 + s_ha[D + tid] * f1) / Lt;
+    }
+    if (tid == 0) prm.att_cnt[p] = 0u;  // self-reset for the next launch / graph replay
+}
+
 // ------------------------------------------------------------ fused
 // Single-launch path for caches whose scores fit on chip (the headline
 // 32 x 512K case). Contiguous segments, a whole number per problem (G <= SMs
@@ -1087,7 +1266,10 @@ __device__ ShardPlanOut shard_global_plan(const K3Params& prm, uint32_t epoch, u
 // (shard_global_plan) and compacts its rows as usual — one launch, no
 // host-side collective. Local positions, plus out_offset[p] into the global
 // list (rank order = index order, as in spl_shard_select).
-template <int W, typename ScoreT, bool SHARD = false, bool PF = false>
+// ATT (decode step): also attend the selected rows (fused_attend; KV = K/V
+// cache element type, head dim 128), writing the attention output.
+template <int W, typename ScoreT, bool SHARD = false, bool PF = false, bool ATT = false,
+          typename KV = __nv_bfloat16>
 __global__ void __launch_bounds__(kThreads, 3) k3_fused(K3Params prm) {
     extern __shared__ __align__(16) uint8_t smem[];
     __shared__ uint64_t s_warp[kThreads / 32 + 1];
@@ -1132,7 +1314,9 @@ __global__ void __launch_bounds__(kThreads, 3) k3_fused(K3Params prm) {
     uint32_t epoch = 0;
     if constexpr (SHARD) {
         epoch = __ldcg(prm.epoch_ptr) + 1u;
-        if (epoch == 0) epoch = 1;  // 0 marks never-written entries
+        // 0 marks never-written entries; wrap 0xFFFFFFFF -> 2 (not 1) so the
+        // parity keeps alternating between consecutive calls
+        if (epoch == 0) epoch = 2;
     }
 
     const uint64_t g0 = (uint64_t)seg * g.S;
@@ -1278,50 +1462,64 @@ __global__ void __launch_bounds__(kThreads, 3) k3_fused(K3Params prm) {
                 prm.cnt_out[p] = kk;
             }
         }
-        if (r0 >= r1) continue;
-        if (T == SPL_PLAN_SKIP) continue;
-        // (gt, eq) of the earlier segments of this problem, from their records
-        uint64_t gt_before = 0, eq_before = 0;
-        for (uint32_t cb = c0; cb < seg; cb += kThreads) {
-            const uint32_t c = cb + tid;
-            uint32_t gtv = 0, eqv = 0;
-            if (c < seg) {
-                const uint32_t* r = prm.records + (uint64_t)(c + p) * (L + 2);
-                const uint32_t geT = __ldcg(r + T), geT1 = __ldcg(r + T + 1);
-                gtv = geT1;
-                eqv = geT - geT1;
+        uint64_t off = 0;
+        uint32_t my_count = 0;
+        if (r0 < r1 && T != SPL_PLAN_SKIP) {
+            // (gt, eq) of the earlier segments of this problem, from their records
+            uint64_t gt_before = 0, eq_before = 0;
+            for (uint32_t cb = c0; cb < seg; cb += kThreads) {
+                const uint32_t c = cb + tid;
+                uint32_t gtv = 0, eqv = 0;
+                if (c < seg) {
+                    const uint32_t* r = prm.records + (uint64_t)(c + p) * (L + 2);
+                    const uint32_t geT = __ldcg(r + T), geT1 = __ldcg(r + T + 1);
+                    gtv = geT1;
+                    eqv = geT - geT1;
+                }
+                uint64_t totv;
+                block_excl_scan_u64(((uint64_t)eqv << 32) | gtv, s_warp, totv);
+                gt_before += totv & 0xffffffffu;
+                eq_before += totv >> 32;
             }
-            uint64_t totv;
-            block_excl_scan_u64(((uint64_t)eqv << 32) | gtv, s_warp, totv);
-            gt_before += totv & 0xffffffffu;
-            eq_before += totv >> 32;
-        }
-        K3_STAMP(4);
-        const uint32_t* own = prm.records + (uint64_t)(seg + p) * (L + 2);
-        const uint64_t eq_mine = (uint64_t)__ldcg(own + T) - __ldcg(own + T + 1);
-        const uint64_t left = quota > eq_before ? quota - eq_before : 0;
-        const uint32_t take = (uint32_t)(eq_mine < left ? eq_mine : left);
-        const uint64_t off = gt_before + (eq_before < quota ? eq_before : quota);
-        K3_STAMP(8);
-        if (prm.trace && threadIdx.x == 0) prm.trace[blockIdx.x * 16 + 12] = clock64();
-        if constexpr (sizeof(ScoreT) == 1) {
-            uint32_t* o = prm.idx_out + (uint64_t)p * prm.idx_stride + off;
-            uint64_t* trp = prm.trace ? prm.trace + (uint64_t)blockIdx.x * 16 : nullptr;
-            const uint64_t pf_off = (uint64_t)p * prm.stride_rows * prm.pf_row_bytes;
-            const char* pfk = prm.pf_k ? prm.pf_k + pf_off : nullptr;
-            const char* pfv = prm.pf_v ? prm.pf_v + pf_off : nullptr;
-            if (r1 - a0 <= (uint64_t)kThreads * 16 * 3)  // uniform
-                select_rows_t8<3, PF>(reinterpret_cast<const uint8_t*>(sc), a0, r0, r1, T, take, o,
-                                      s_warp, reinterpret_cast<uint32_t*>(priv), trp, pfk, pfv,
-                                      prm.pf_row_bytes);
+            K3_STAMP(4);
+            const uint32_t* own = prm.records + (uint64_t)(seg + p) * (L + 2);
+            const uint64_t eq_mine = (uint64_t)__ldcg(own + T) - __ldcg(own + T + 1);
+            const uint64_t left = quota > eq_before ? quota - eq_before : 0;
+            const uint32_t take = (uint32_t)(eq_mine < left ? eq_mine : left);
+            off = gt_before + (eq_before < quota ? eq_before : quota);
+            my_count = __ldcg(own + T + 1) + take;
+            K3_STAMP(8);
+            if (prm.trace && threadIdx.x == 0) prm.trace[blockIdx.x * 16 + 12] = clock64();
+            if constexpr (sizeof(ScoreT) == 1) {
+                uint32_t* o = prm.idx_out + (uint64_t)p * prm.idx_stride + off;
+                uint64_t* trp = prm.trace ? prm.trace + (uint64_t)blockIdx.x * 16 : nullptr;
+                const uint64_t pf_off = (uint64_t)p * prm.stride_rows * prm.pf_row_bytes;
+                const bool pf_emit = prm.pf_k && (!ATT || prm.att_pf == 1);
+                const char* pfk = pf_emit ? prm.pf_k + pf_off : nullptr;
+                const char* pfv = pf_emit ? prm.pf_v + pf_off : nullptr;
+                if (r1 - a0 <= (uint64_t)kThreads * 16 * 3)  // uniform
+                    select_rows_t8<3, PF>(reinterpret_cast<const uint8_t*>(sc), a0, r0, r1, T, take, o,
+                                          s_warp, reinterpret_cast<uint32_t*>(priv), trp, pfk, pfv,
+                                          prm.pf_row_bytes, att_ids<ATT>(priv, priv_bytes, 3),
+                                          att_ids_cap<ATT>(priv_bytes, 3));
+                else
+                    select_rows_t8<11, PF>(reinterpret_cast<const uint8_t*>(sc), a0, r0, r1, T, take, o,
+                                           s_warp, reinterpret_cast<uint32_t*>(priv), trp, pfk, pfv,
+                                           prm.pf_row_bytes, att_ids<ATT>(priv, priv_bytes, 11),
+                                           att_ids_cap<ATT>(priv_bytes, 11));
+            }
             else
-                select_rows_t8<11, PF>(reinterpret_cast<const uint8_t*>(sc), a0, r0, r1, T, take, o,
-                                       s_warp, reinterpret_cast<uint32_t*>(priv), trp, pfk, pfv,
-                                       prm.pf_row_bytes);
+                select_rows<ScoreT, false>(sc, a0, r0, r1, T, take,
+                                           prm.idx_out + (uint64_t)p * prm.idx_stride + off, s_warp);
         }
-        else
-            select_rows<ScoreT, false>(sc, a0, r0, r1, T, take,
-                                       prm.idx_out + (uint64_t)p * prm.idx_stride + off, s_warp);
+        if constexpr (ATT) {
+            K3_STAMP(7);
+            const bool owner = r0 < r1 && r1 == (uint64_t)nv;  // this segment holds row nv - 1
+            const uint32_t nvs = (r1 - a0 <= (uint64_t)kThreads * 16 * 3) ? 3u : 11u;  // select's NV
+            fused_attend<KV>(prm, p, seg, c0, nseg, nv, owner, off, my_count,
+                             reinterpret_cast<float*>(priv), att_ids<ATT>(priv, priv_bytes, nvs),
+                             att_ids_cap<ATT>(priv_bytes, nvs), &s_flag);
+        }
     }
     K3_STAMP(5);
 
@@ -1463,7 +1661,13 @@ spl_status ensure_buffer(spl_ctx* ctx, void** buf, size_t* have, size_t bytes, b
     }
     size_t want = std::max(bytes, (size_t)256);
     SPL_CUDA_TRY(ctx, cudaMalloc(buf, want));
-    if (zero) SPL_CUDA_TRY(ctx, cudaMemset(*buf, 0, want));
+    if (zero) {
+        // zeroed on the caller's stream and completed before any kernel of
+        // any stream can see the buffer (a legacy-stream cudaMemset is not
+        // ordered before work on non-blocking streams)
+        SPL_CUDA_TRY(ctx, cudaMemsetAsync(*buf, 0, want, s));
+        SPL_CUDA_TRY(ctx, cudaStreamSynchronize(s));
+    }
     *have = want;
     return SPL_OK;
 }
@@ -1566,15 +1770,19 @@ struct K3FPlan {
     const void* fn;
 };
 
-template <int W, typename ScoreT, bool SHARD = false, bool PF = false>
+template <int W, typename ScoreT, bool SHARD = false, bool PF = false, bool ATT = false,
+          typename KV = __nv_bfloat16>
 const void* fused_fn() {
-    return reinterpret_cast<const void*>(&k3_fused<W, ScoreT, SHARD, PF>);
+    return reinterpret_cast<const void*>(&k3_fused<W, ScoreT, SHARD, PF, ATT, KV>);
 }
 
+// att: 0 = plain retrieval, 1 / 2 = decode step attending bf16 / f32 K/V rows
+// (k3_fused<4, u8, false, true, true, KV>; L = 128 only)
 spl_status make_fused_plan(spl_ctx* ctx, uint32_t P, uint64_t n_max, uint32_t L, const void* codes,
                            uint64_t stride_rows, bool* ok, K3FPlan* out, bool shard = false,
-                           bool pf = false) {
+                           bool pf = false, int att = 0) {
     *ok = false;
+    if (att && (L != 128 || shard)) return SPL_OK;
     const uint32_t W = L / 32;
     // Private counters cover scores [L/2, L] only: the k-th best agreement is
     // >= L/2 whenever at least k rows agree on half their bits (retrieval
@@ -1590,8 +1798,13 @@ spl_status make_fused_plan(spl_ctx* ctx, uint32_t P, uint64_t n_max, uint32_t L,
             case 1: fn = shard ? fused_fn<1, uint8_t, true>() : fused_fn<1, uint8_t>(); break;
             case 2: fn = shard ? fused_fn<2, uint8_t, true>() : fused_fn<2, uint8_t>(); break;
             case 4:
-                fn = shard ? fused_fn<4, uint8_t, true>()
-                           : (pf ? fused_fn<4, uint8_t, false, true>() : fused_fn<4, uint8_t>());
+                if (att == 1)
+                    fn = fused_fn<4, uint8_t, false, true, true, __nv_bfloat16>();
+                else if (att == 2)
+                    fn = fused_fn<4, uint8_t, false, true, true, float>();
+                else
+                    fn = shard ? fused_fn<4, uint8_t, true>()
+                               : (pf ? fused_fn<4, uint8_t, false, true>() : fused_fn<4, uint8_t>());
                 break;
             default: return SPL_OK;
         }
@@ -1764,20 +1977,20 @@ void k3_trace_report(uint64_t* dtrace, uint32_t G, uint64_t S, cudaStream_t s) {
     const char* tr = getenv("SPL_K3_TRACE");
     {
                 // stamps per CTA (16 slots): 0 start, 1 stream end, 2 (= 1), 3 T known,
-                // 4 prefix, 5 select end, 6 smid, 8 own record read, 9 select counts,
-                // 10 select scan, 11 select emitted
+                // 4 prefix, 5 end, 6 smid, 7 attention start (decode step), 8 own
+                // record read, 9 select counts, 10 select scan, 11 select emitted
                 constexpr int kSlots = 16;
-                const int cols[] = {0, 1, 3, 4, 8, 9, 10, 11, 5};
-                const char* names = "start stream thresh prefix rec counts scan emit end";
+                const int cols[] = {0, 1, 3, 4, 8, 9, 10, 11, 7, 5};
+                const char* names = "start stream thresh prefix rec counts scan emit attend end";
                 std::vector<uint64_t> h((size_t)G * kSlots);
                 cudaStreamSynchronize(s);
                 cudaMemcpy(h.data(), dtrace, h.size() * 8, cudaMemcpyDeviceToHost);
                 cudaFree(dtrace);
                 uint64_t t0 = ~0ull;
                 for (uint32_t i = 0; i < G; ++i) t0 = std::min(t0, h[i * kSlots]);
-                double mx[9] = {0}, mean[9] = {0};
+                double mx[10] = {0}, mean[10] = {0};
                 for (uint32_t i = 0; i < G; ++i)
-                    for (int j = 0; j < 9; ++j) {
+                    for (int j = 0; j < 10; ++j) {
                         const uint64_t raw = h[i * kSlots + cols[j]];
                         const double v = raw ? (double)(raw - t0) / 1000.0 : 0.0;
                         mx[j] = std::max(mx[j], v);
@@ -1785,9 +1998,9 @@ void k3_trace_report(uint64_t* dtrace, uint32_t G, uint64_t S, cudaStream_t s) {
                     }
                 fprintf(stderr, "k3_fused trace G=%u S=%llu [%s] mean:", G,
                         (unsigned long long)S, names);
-                for (int j = 0; j < 9; ++j) fprintf(stderr, " %.1f", mean[j]);
+                for (int j = 0; j < 10; ++j) fprintf(stderr, " %.1f", mean[j]);
                 fprintf(stderr, "  max:");
-                for (int j = 0; j < 9; ++j) fprintf(stderr, " %.1f", mx[j]);
+                for (int j = 0; j < 10; ++j) fprintf(stderr, " %.1f", mx[j]);
                 fprintf(stderr, " us");
                 double cyc[3] = {0, 0, 0};
                 for (uint32_t i = 0; i < G; ++i)
@@ -1835,6 +2048,10 @@ spl_status hamming_topk_impl(spl_ctx* ctx, const uint32_t* codes, uint64_t strid
         return SPL_OK;
     }
     if (n_max > 0xFFFFFFFFull) return fail(ctx, SPL_E_DIMENSION, "hamming_topk: n_max exceeds 2^32 rows");
+    if (stride_rows != 0 && n_max > stride_rows)
+        return fail(ctx, SPL_E_DIMENSION,
+                    "hamming_topk: n_max=" + std::to_string(n_max) + " exceeds the problem stride of " +
+                        std::to_string(stride_rows) + " rows");
     K3State kst;
     if ((st = k3_state(ctx, P, L, s, &kst))) return st;
     if (fused_allowed()) {
@@ -1871,7 +2088,7 @@ spl_status hamming_topk_impl(spl_ctx* ctx, const uint32_t* codes, uint64_t strid
                 SPL_CUDA_TRY(ctx, cudaLaunchCooperativeKernel(fp.fn, dim3(G), dim3(kThreads), args, fp.smem, s));
             else
                 SPL_CUDA_TRY(ctx, launch_pdl(fp.fn, dim3(G), dim3(kThreads), fp.smem, s, args));
-            st = after_launch(ctx, "k3_fused");
+            st = after_launch(ctx, pf ? "k3_fused_pf" : "k3_fused");
             if (dtrace) k3_trace_report(dtrace, G, fp.pl.g.S, s);
             return st;
         }
@@ -1909,6 +2126,84 @@ spl_status hamming_topk_impl(spl_ctx* ctx, const uint32_t* codes, uint64_t strid
         for (auto& e : ev) cudaEventDestroy(e);
     }
     return st;
+}
+
+// Decode-step retrieval + attention in ONE launch (k3_fused<.., ATT>): same
+// indices as hamming_topk_impl, plus out[p] = sparse attention of q[p] over
+// the selected rows U {own}. *done = false (and nothing launched) when the
+// fused geometry does not apply (L != 128, d != 128, scores too large for
+// shared memory, SPL_K3_PATH=twopass): the caller then runs K3 + K4.
+spl_status hamming_topk_attend_impl(spl_ctx* ctx, const uint32_t* codes, uint64_t stride_rows,
+                                    uint32_t L, const uint32_t* qcodes, uint32_t P,
+                                    const uint32_t* n_valid, uint32_t nvalid_div, uint64_t n_max,
+                                    uint32_t k, uint32_t* idx, uint32_t* cnt, const float* q,
+                                    const void* kcache, const void* vcache, int kv_dtype, uint32_t d,
+                                    float qscale, float* out, cudaStream_t s, bool* done) {
+    *done = false;
+    if (d != 128 || L != 128 || (kv_dtype != SPL_BF16 && kv_dtype != SPL_F32) || !fused_allowed())
+        return SPL_OK;
+    const char* e = getenv("SPL_DECODE_FUSED");
+    if (e && *e == '0') return SPL_OK;
+    spl_status st = validate_common(ctx, "hamming_topk", codes, qcodes, n_valid, L, nvalid_div);
+    if (st) return st;
+    if (k == 0) return fail(ctx, SPL_E_DIMENSION, "hash_topk: k must be >= 1");
+    if (P == 0 || n_max == 0 || n_max > 0xFFFFFFFFull) return SPL_OK;
+    if (stride_rows == 0 || n_max > stride_rows) return SPL_OK;
+    bool ok = false;
+    K3FPlan fp{};
+    if ((st = make_fused_plan(ctx, P, n_max, L, codes, stride_rows, &ok, &fp, false, true,
+                              kv_dtype == SPL_BF16 ? 1 : 2)))
+        return st;
+    if (!ok) return SPL_OK;
+    K3State kst;
+    if ((st = k3_state(ctx, P, L, s, &kst))) return st;
+    K3Ws ws;
+    if ((st = k3_workspace(ctx, fp.pl, L, s, &ws, false))) return st;
+    const uint32_t G = fp.pl.g.G;
+    if ((st = ensure_buffer(ctx, reinterpret_cast<void**>(&ctx->att_ws), &ctx->att_ws_bytes,
+                            (size_t)(G + P) * (d + 2) * sizeof(float), false, s, "decode_step")))
+        return st;
+    size_t have = ctx->att_counters_n * 4;
+    if ((st = ensure_buffer(ctx, reinterpret_cast<void**>(&ctx->att_counters), &have, (size_t)P * 4,
+                            true, s, "decode_step")))
+        return st;
+    ctx->att_counters_n = have / 4;
+    K3Params prm = base_params(ctx, fp.pl, ws, kst, codes, stride_rows, L, qcodes, n_valid, nvalid_div, k);
+    prm.cnt_out = cnt;
+    prm.idx_out = idx;
+    prm.idx_stride = k;
+    prm.hist_lo = fp.pl.hist_lo;
+    prm.counters2 = kst.bar;
+    const uint32_t row_bytes = d * (kv_dtype == SPL_BF16 ? 2u : 4u);
+    prm.pf_k = static_cast<const char*>(kcache);
+    prm.pf_v = static_cast<const char*>(vcache);
+    prm.pf_row_bytes = row_bytes;
+    prm.att_q = q;
+    prm.att_qscale = qscale;
+    prm.att_part = ctx->att_ws;
+    prm.att_cnt = ctx->att_counters;
+    prm.att_out = out;
+    {
+        const char* e = getenv("SPL_ATT_PF");
+        prm.att_pf = (e && *e == '1') ? 1 : 0;
+    }
+    const char* tr = getenv("SPL_K3_TRACE");
+    uint64_t* dtrace = nullptr;
+    if (tr && *tr && !stream_capturing(s)) {
+        SPL_CUDA_TRY(ctx, cudaMalloc(&dtrace, (size_t)G * 16 * 8));
+        SPL_CUDA_TRY(ctx, cudaMemsetAsync(dtrace, 0, (size_t)G * 16 * 8, s));
+    }
+    prm.trace = dtrace;
+    void* args[] = {&prm};
+    const char* coop = getenv("SPL_K3_COOP");
+    if (coop && *coop == '1')
+        SPL_CUDA_TRY(ctx, cudaLaunchCooperativeKernel(fp.fn, dim3(G), dim3(kThreads), args, fp.smem, s));
+    else
+        SPL_CUDA_TRY(ctx, launch_pdl(fp.fn, dim3(G), dim3(kThreads), fp.smem, s, args));
+    if ((st = after_launch(ctx, "k3_fused_attend"))) return st;
+    if (dtrace) k3_trace_report(dtrace, G, fp.pl.g.S, s);
+    *done = true;
+    return SPL_OK;
 }
 
 spl_status shard_histogram_impl(spl_ctx* ctx, const uint32_t* codes, uint64_t stride_rows,

@@ -25,6 +25,7 @@
 #include <algorithm>
 #include <string>
 
+#include "spl_attend.cuh"
 #include "spl_launch.cuh"
 
 namespace spl {
@@ -32,10 +33,7 @@ namespace spl {
 constexpr int kAttThreads = 128;
 constexpr int kAttWarps = kAttThreads / 32;
 constexpr uint32_t kWarpRows = 32;  // one row per lane for the logits
-constexpr uint32_t kInv = 0xFFFFFFFFu;
-
-__device__ __forceinline__ float bf16lo(uint32_t w) { return __uint_as_float(w << 16); }
-__device__ __forceinline__ float bf16hi(uint32_t w) { return __uint_as_float(w & 0xffff0000u); }
+constexpr uint32_t kInv = kAttInv;
 
 // dot(q_s, K row) over D values, the row read as 16-byte chunks.
 template <int D, typename KV>
@@ -75,51 +73,6 @@ __device__ __forceinline__ float row_dot(const KV* row, const float* q_s) {
     return (a0 + a1) + (a2 + a3);
 }
 
-// A lane's E-element slice of a V row.
-template <int E, typename KV>
-struct VSlice;
-template <int E>
-struct VSlice<E, __nv_bfloat16> {
-    uint32_t u[(E + 1) / 2];
-    __device__ __forceinline__ void load(const __nv_bfloat16* row, int lane) {
-        const __nv_bfloat16* p = row + lane * E;
-        if constexpr (E == 8) {
-            const uint4 v = __ldg(reinterpret_cast<const uint4*>(p));
-            u[0] = v.x; u[1] = v.y; u[2] = v.z; u[3] = v.w;
-        } else if constexpr (E == 4) {
-            const uint2 v = __ldg(reinterpret_cast<const uint2*>(p));
-            u[0] = v.x; u[1] = v.y;
-        } else if constexpr (E == 2) {
-            u[0] = __ldg(reinterpret_cast<const unsigned int*>(p));
-        } else {
-            u[0] = __ldg(reinterpret_cast<const unsigned short*>(p));
-        }
-    }
-    __device__ __forceinline__ float get(int e) const {
-        return (e & 1) ? bf16hi(u[e / 2]) : bf16lo(u[e / 2]);
-    }
-};
-template <int E>
-struct VSlice<E, float> {
-    float f[E];
-    __device__ __forceinline__ void load(const float* row, int lane) {
-        const float* p = row + lane * E;
-        if constexpr (E % 4 == 0) {
-#pragma unroll
-            for (int i = 0; i < E; i += 4) {
-                const float4 v = __ldg(reinterpret_cast<const float4*>(p + i));
-                f[i] = v.x; f[i + 1] = v.y; f[i + 2] = v.z; f[i + 3] = v.w;
-            }
-        } else if constexpr (E == 2) {
-            const float2 v = __ldg(reinterpret_cast<const float2*>(p));
-            f[0] = v.x; f[1] = v.y;
-        } else {
-            f[0] = __ldg(p);
-        }
-    }
-    __device__ __forceinline__ float get(int e) const { return f[e]; }
-};
-
 __device__ __forceinline__ float warp_max(float v) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
@@ -131,79 +84,31 @@ __device__ __forceinline__ float warp_sum(float v) {
     return v;
 }
 
-// E = d / 32 elements per lane (d in {32, 64, 128, 256}).
-template <int E, typename KV>
-__global__ void __launch_bounds__(kAttThreads) k4_sparse_attend(AttParams prm) {
+// Shared memory of a K4 CTA: per-warp (m, l, o) for the merge, the
+// combine's per-split scales, the last-split flag.
+template <int D>
+struct AttSmem {
+    float s_m[kAttWarps], s_l[kAttWarps];
+    float s_o[kAttWarps][D];
+    float s_cmb[2][kAttThreads];
+    uint32_t s_last;
+};
+
+// End of a K4 CTA: merge the warps' (m, l, o) (lane-per-dims o: lane owns
+// dims [lane*E, lane*E + E); l is the warp's total), then either write the
+// result directly (one split) or write this split's partial and let the CTA
+// finishing the problem's last split combine all of them (K5, log-sum-exp).
+template <int E>
+__device__ __forceinline__ void att_cta_finish(const AttParams& prm, AttSmem<32 * E>& sm,
+                                               uint32_t p, uint32_t split, float m, float l,
+                                               const float (&o)[E]) {
     constexpr int D = 32 * E;
-    constexpr int VB = sizeof(KV) * E >= 16 ? 8 : 16;  // V rows in flight per lane
-    __shared__ __align__(16) float q_s[D];
-    __shared__ float s_m[kAttWarps], s_l[kAttWarps];
-    __shared__ float s_o[kAttWarps][D];
-    __shared__ float s_cmb[2][kAttThreads];  // combine: per-split scale, l
-    __shared__ uint32_t s_last;
-    const uint32_t p = blockIdx.y, split = blockIdx.x;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    pdl_trigger();
-    pdl_wait();  // the row lists (and the appended own row) come from the previous kernels
-
-    for (int i = tid; i < D; i += kAttThreads) q_s[i] = prm.q[(uint64_t)p * D + i] * prm.qscale;
-
-    const uint32_t c = prm.cnt[p];
-    const uint32_t* list = prm.idx + (uint64_t)p * prm.idx_stride;
-    uint32_t own;
-    if (prm.partial_mode)
-        own = prm.own_row ? prm.own_row[p] : kInv;
-    else
-        own = prm.n_valid[p / prm.nvalid_div] - 1u;
-    const bool has_own = own != kInv;
-    const bool own_listed = has_own && c > 0 && __ldg(list + c - 1) == own;
-    const uint32_t nrows = c + ((has_own && !own_listed) ? 1u : 0u);
-    const KV* kbase = static_cast<const KV*>(prm.kc) + (uint64_t)p * prm.stride_rows * D;
-    const KV* vbase = static_cast<const KV*>(prm.vc) + (uint64_t)p * prm.stride_rows * D;
-
-    const uint32_t wb = split * prm.rows_per_split + warp * kWarpRows;
-    const uint32_t we = min(wb + kWarpRows, nrows);
-    const uint32_t nr = we > wb ? we - wb : 0;  // rows of this warp (warp-uniform)
-    const uint32_t j = wb + lane;
-    const uint32_t rid = j < we ? (j < c ? __ldg(list + j) : own) : kInv;
-    __syncthreads();  // q_s
-
-    float m = -INFINITY, l = 0.0f, o[E];
-#pragma unroll
-    for (int e = 0; e < E; ++e) o[e] = 0.0f;
-    if (nr > 0) {
-        // the V rows do not depend on the logits: start pulling this lane's V
-        // row into L2 now so the value phase below does not pay a second
-        // DRAM round trip after the K phase (random rows, cold L2)
-        if (rid != kInv) {
-            const char* vr = reinterpret_cast<const char*>(vbase + (uint64_t)rid * D);
-#pragma unroll
-            for (int b = 0; b < (int)(D * sizeof(KV)); b += 128)
-                asm volatile("prefetch.global.L2 [%0];" ::"l"(vr + b));
-        }
-        float s = -INFINITY;
-        if (rid != kInv) s = row_dot<D, KV>(kbase + (uint64_t)rid * D, q_s);
-        m = warp_max(s);
-        const float pr = rid != kInv ? exp2f(s - m) : 0.0f;
-        l = warp_sum(pr);
-        for (uint32_t r0 = 0; r0 < nr; r0 += VB) {
-            VSlice<E, KV> vv[VB];
-            float pw[VB];
-#pragma unroll
-            for (int i = 0; i < VB; ++i) {
-                const uint32_t rr = __shfl_sync(0xffffffffu, rid, (r0 + i) & 31);
-                pw[i] = __shfl_sync(0xffffffffu, pr, (r0 + i) & 31);
-                if (r0 + i < nr) vv[i].load(vbase + (uint64_t)rr * D, lane);
-            }
-#pragma unroll
-            for (int i = 0; i < VB; ++i) {
-                if (r0 + i >= nr) break;
-#pragma unroll
-                for (int e = 0; e < E; ++e) o[e] = fmaf(pw[i], vv[i].get(e), o[e]);
-            }
-        }
-    }
-
+    float* s_m = sm.s_m;
+    float* s_l = sm.s_l;
+    auto& s_o = sm.s_o;
+    auto& s_cmb = sm.s_cmb;
+    uint32_t& s_last = sm.s_last;
     // merge warps
     if (lane == 0) {
         s_m[warp] = m;
@@ -329,6 +234,130 @@ __global__ void __launch_bounds__(kAttThreads) k4_sparse_attend(AttParams prm) {
     }
 }
 
+// Lane-per-row form (round 1; kept for A/B measurement, SPL_K4=lane): a
+// warp takes 32 consecutive entries, lane i gathers row i's K with 16-byte
+// loads, then the V rows lane-per-dims. E = d / 32 elements per lane.
+template <int E, typename KV>
+__global__ void __launch_bounds__(kAttThreads) k4_lane(AttParams prm) {
+    constexpr int D = 32 * E;
+    constexpr int VB = sizeof(KV) * E >= 16 ? 8 : 16;  // V rows in flight per lane
+    __shared__ __align__(16) float q_s[D];
+    __shared__ AttSmem<D> sm;
+    const uint32_t p = blockIdx.y, split = blockIdx.x;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    pdl_trigger();
+    pdl_wait();  // the row lists (and the appended own row) come from the previous kernels
+
+    for (int i = tid; i < D; i += kAttThreads) q_s[i] = prm.q[(uint64_t)p * D + i] * prm.qscale;
+
+    const uint32_t c = prm.cnt[p];
+    const uint32_t* list = prm.idx + (uint64_t)p * prm.idx_stride;
+    uint32_t own;
+    if (prm.partial_mode)
+        own = prm.own_row ? prm.own_row[p] : kInv;
+    else
+        own = prm.n_valid[p / prm.nvalid_div] - 1u;
+    const bool has_own = own != kInv;
+    const bool own_listed = has_own && c > 0 && __ldg(list + c - 1) == own;
+    const uint32_t nrows = c + ((has_own && !own_listed) ? 1u : 0u);
+    const KV* kbase = static_cast<const KV*>(prm.kc) + (uint64_t)p * prm.stride_rows * D;
+    const KV* vbase = static_cast<const KV*>(prm.vc) + (uint64_t)p * prm.stride_rows * D;
+
+    const uint32_t wb = split * prm.rows_per_split + warp * kWarpRows;
+    const uint32_t we = min(wb + kWarpRows, nrows);
+    const uint32_t nr = we > wb ? we - wb : 0;  // rows of this warp (warp-uniform)
+    const uint32_t j = wb + lane;
+    const uint32_t rid = j < we ? (j < c ? __ldg(list + j) : own) : kInv;
+    __syncthreads();  // q_s
+
+    float m = -INFINITY, l = 0.0f, o[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) o[e] = 0.0f;
+    if (nr > 0) {
+        // the V rows do not depend on the logits: start pulling this lane's V
+        // row into L2 now so the value phase below does not pay a second
+        // DRAM round trip after the K phase (random rows, cold L2)
+        if (rid != kInv) {
+            const char* vr = reinterpret_cast<const char*>(vbase + (uint64_t)rid * D);
+#pragma unroll
+            for (int b = 0; b < (int)(D * sizeof(KV)); b += 128)
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(vr + b));
+        }
+        float s = -INFINITY;
+        if (rid != kInv) s = row_dot<D, KV>(kbase + (uint64_t)rid * D, q_s);
+        m = warp_max(s);
+        const float pr = rid != kInv ? exp2f(s - m) : 0.0f;
+        l = warp_sum(pr);
+        for (uint32_t r0 = 0; r0 < nr; r0 += VB) {
+            VSlice<E, KV> vv[VB];
+            float pw[VB];
+#pragma unroll
+            for (int i = 0; i < VB; ++i) {
+                const uint32_t rr = __shfl_sync(0xffffffffu, rid, (r0 + i) & 31);
+                pw[i] = __shfl_sync(0xffffffffu, pr, (r0 + i) & 31);
+                if (r0 + i < nr) vv[i].load(vbase + (uint64_t)rr * D, lane);
+            }
+#pragma unroll
+            for (int i = 0; i < VB; ++i) {
+                if (r0 + i >= nr) break;
+#pragma unroll
+                for (int e = 0; e < E; ++e) o[e] = fmaf(pw[i], vv[i].get(e), o[e]);
+            }
+        }
+    }
+
+    att_cta_finish<E>(prm, sm, p, split, m, l, o);
+}
+
+// Warp-per-row gather form (the default): a warp takes RB x NB consecutive
+// entries of the problem's row list and walks them in batches of RB = 8
+// rows. For a batch, every lane issues its d/32-element slice of all 8 K rows
+// AND all 8 V rows at once (the V rows do not depend on the logits), so one
+// batch is one memory round trip with 16 coalesced row-slice loads in flight
+// per lane (a warp reads each 256-byte bf16 row as one contiguous request);
+// logits = rsum8 of the per-lane partial dots, online softmax in base 2 (q
+// pre-scaled by scale * log2 e), o[lane's dims] += p_i * v_i. Measured on
+// this B200 (tools/gather_sweep.cu): warp-per-row gathers of random 256-byte
+// rows stream at the copy rate once enough are in flight, lane-per-row ones
+// (k4_lane) do not.
+template <int E, typename KV, int NB>
+__global__ void __launch_bounds__(kAttThreads) k4_gather(AttParams prm) {
+    constexpr int D = 32 * E;
+    __shared__ AttSmem<D> sm;
+    const uint32_t p = blockIdx.y, split = blockIdx.x;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    pdl_trigger();
+    pdl_wait();
+
+    const uint32_t c = prm.cnt[p];
+    const uint32_t* list = prm.idx + (uint64_t)p * prm.idx_stride;
+    uint32_t own;
+    if (prm.partial_mode)
+        own = prm.own_row ? prm.own_row[p] : kInv;
+    else
+        own = prm.n_valid[p / prm.nvalid_div] - 1u;
+    const bool has_own = own != kInv;
+    const bool own_listed = has_own && c > 0 && __ldg(list + c - 1) == own;
+    const uint32_t nrows = c + ((has_own && !own_listed) ? 1u : 0u);
+    const KV* kbase = static_cast<const KV*>(prm.kc) + (uint64_t)p * prm.stride_rows * D;
+    const KV* vbase = static_cast<const KV*>(prm.vc) + (uint64_t)p * prm.stride_rows * D;
+    // this lane's slice of q, pre-scaled
+    float qv[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) qv[e] = __ldg(prm.q + (uint64_t)p * D + lane * E + e) * prm.qscale;
+
+    constexpr uint32_t kWR = kAttRB * NB;  // entries per warp (<= 32)
+    static_assert(kWR <= 32, "one row id per lane");
+    const uint32_t wb = split * prm.rows_per_split + warp * kWR;
+    const uint32_t we = min(wb + kWR, nrows);
+    float m = -INFINITY, lsum = 0.0f, o[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) o[e] = 0.0f;
+    if (wb < we) warp_attend<E, KV>(kbase, vbase, list, c, own, wb, we, qv, m, lsum, o);
+    const float l = attend_lsum_total(lsum);
+    att_cta_finish<E>(prm, sm, p, split, m, l, o);
+}
+
 // Any head dim (the reference's API accepts every d; the tuned kernel above
 // covers d in {32, 64, 128, 256}). One warp per problem, rows processed one
 // at a time with a warp-reduced dot product; f32 only (the drop-in API feeds
@@ -399,13 +428,44 @@ __global__ void k5_combine(const float* partials, uint32_t R, uint32_t P, uint32
 
 namespace {
 
+// SPL_K4=lane selects the round-1 lane-per-row kernel (A/B measurements);
+// SPL_K4_NB=1|2|4 the batches per warp of the gather kernel.
+int k4_mode() {
+    static const int m = [] {
+        const char* e = getenv("SPL_K4");
+        return (e && e[0] == 'l') ? 1 : 0;
+    }();
+    return m;
+}
+int k4_nb() {
+    static const int nb = [] {
+        const char* e = getenv("SPL_K4_NB");
+        const int v = e ? atoi(e) : 0;
+        return (v == 1 || v == 2 || v == 4) ? v : 2;
+    }();
+    return nb;
+}
+template <int E, typename KV>
+const void* gather_fn(int nb) {
+    if (nb == 1) return reinterpret_cast<const void*>(&k4_gather<E, KV, 1>);
+    if (nb == 4) return reinterpret_cast<const void*>(&k4_gather<E, KV, 4>);
+    return reinterpret_cast<const void*>(&k4_gather<E, KV, 2>);
+}
 template <int E>
 const void* att_fn(int kv_dtype) {
-    if (kv_dtype == SPL_BF16) return reinterpret_cast<const void*>(&k4_sparse_attend<E, __nv_bfloat16>);
-    return reinterpret_cast<const void*>(&k4_sparse_attend<E, float>);
+    if (k4_mode() == 1) {
+        if (kv_dtype == SPL_BF16) return reinterpret_cast<const void*>(&k4_lane<E, __nv_bfloat16>);
+        return reinterpret_cast<const void*>(&k4_lane<E, float>);
+    }
+    if (kv_dtype == SPL_BF16) return gather_fn<E, __nv_bfloat16>(k4_nb());
+    return gather_fn<E, float>(k4_nb());
 }
 
 }  // namespace
+
+uint32_t att_rows_per_split() {
+    return k4_mode() == 1 ? (uint32_t)(kAttWarps * kWarpRows) : (uint32_t)(kAttWarps * kAttRB * k4_nb());
+}
 
 spl_status sparse_attend_launch(spl_ctx* ctx, AttParams prm, uint32_t kmax, int kv_dtype,
                                 cudaStream_t s) {
@@ -435,7 +495,7 @@ spl_status sparse_attend_launch(spl_ctx* ctx, AttParams prm, uint32_t kmax, int 
     }
     if (prm.P == 0) return SPL_OK;
     const uint64_t rows_max = (uint64_t)kmax + 1;
-    const uint64_t R = (uint64_t)kAttWarps * kWarpRows;  // rows per split (CTA)
+    const uint64_t R = att_rows_per_split();  // rows per split (CTA)
     const uint32_t nsplit = (uint32_t)((rows_max + R - 1) / R);
     prm.rows_per_split = (uint32_t)R;
     prm.nsplit = nsplit;
@@ -452,7 +512,7 @@ spl_status sparse_attend_launch(spl_ctx* ctx, AttParams prm, uint32_t kmax, int 
     prm.counters = ctx->att_counters;
     void* args[] = {&prm};
     SPL_CUDA_TRY(ctx, launch_pdl(fn, dim3(nsplit, prm.P), dim3(kAttThreads), 0, s, args));
-    return after_launch(ctx, "k4_sparse_attend");
+    return after_launch(ctx, k4_mode() == 1 ? "k4_lane" : "k4_gather");
 }
 
 spl_status attend_combine_launch(spl_ctx* ctx, const float* partials, uint32_t R, uint32_t P,

@@ -21,6 +21,7 @@ struct spl_ctx {
     int num_sms = 148;
     std::string err;
     uint64_t launches = 0;
+    std::string launch_log;  // kernel names since the last spl_launch_log (bounded)
     double last_train_loop_ms = 0.0;  // device time of the last spl_train_hasher loop
     // decode step: K/V caches whose selected rows the K3 select prefetches
     // into L2 for K4 (set by spl_decode_step when the gathered rows fit L2)
@@ -106,6 +107,10 @@ inline spl_status cuda_fail(spl_ctx* ctx, cudaError_t e, const char* where) {
 // After a launch: count it, surface launch-config errors.
 inline spl_status after_launch(spl_ctx* ctx, const char* name) {
     ctx->launches++;
+    if (ctx->launch_log.size() < 4096) {
+        ctx->launch_log += name;
+        ctx->launch_log += ';';
+    }
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(ctx, e, name);
     return SPL_OK;

@@ -47,6 +47,10 @@ struct AttParams {
 spl_status hamming_topk_impl(spl_ctx*, const uint32_t*, uint64_t, uint32_t, const uint32_t*,
                              uint32_t, const uint32_t*, uint32_t, uint64_t, uint32_t, uint32_t*,
                              uint32_t*, cudaStream_t);
+spl_status hamming_topk_attend_impl(spl_ctx*, const uint32_t*, uint64_t, uint32_t,
+                                    const uint32_t*, uint32_t, const uint32_t*, uint32_t, uint64_t,
+                                    uint32_t, uint32_t*, uint32_t*, const float*, const void*,
+                                    const void*, int, uint32_t, float, float*, cudaStream_t, bool*);
 spl_status shard_histogram_impl(spl_ctx*, const uint32_t*, uint64_t, uint32_t, const uint32_t*,
                                 uint32_t, const uint32_t*, uint32_t, uint64_t, uint32_t*,
                                 cudaStream_t);
@@ -87,6 +91,7 @@ spl_status encode_tc_launch(spl_ctx*, const spl_hasher*, const void* x, int x_dt
 bool encode_tc_eligible(uint32_t kind, uint32_t d, uint32_t h, uint32_t L);
 // sparse_attend.cu
 spl_status sparse_attend_launch(spl_ctx*, AttParams, uint32_t, int, cudaStream_t);
+uint32_t att_rows_per_split();  // list entries per K4 CTA (sizes the partials)
 spl_status attend_combine_launch(spl_ctx*, const float*, uint32_t, uint32_t, uint32_t, float*,
                                  cudaStream_t);
 

@@ -213,3 +213,54 @@ def test_encode_tc_non_finite_bf16_raises(ctx, bad, L):
     torch.cuda.synchronize()
     with pytest.raises(capi.NumericError):
         ctx.check_device_error()
+
+
+def bf16_band(x, w1, b1, w2):
+    """First-order bound on |z2_K2 - z2_ref| per output for K2's arithmetic
+    (hashers.cpp:84-108 in bf16 operands / fp32 accumulation): x and W1
+    rounded to bf16 (relative 2u per layer-1 product), SiLU through
+    tanh.approx (relative <= 2^-10) and its output rounded to bf16 (u), W2
+    rounded (u); |silu'| <= 1.1; u = 2^-8. fp32 accumulation error
+    (~128 x 2^-24 relative) is far below it. x [m][d] -> [m][L] (float64)."""
+    u = 2.0 ** -8
+    xd, w1d, w2d = x.astype(np.float64), w1.astype(np.float64), w2.astype(np.float64)
+    z1 = xd @ w1d + b1.astype(np.float64)
+    a1 = z1 / (1.0 + np.exp(-z1))
+    s1 = np.abs(xd) @ np.abs(w1d)  # sum_p |x_p W1_pj|
+    da1 = 1.1 * 2 * u * s1 + (u + 2.0 ** -10) * np.abs(a1)
+    return da1 @ np.abs(w2d) + u * (np.abs(a1) @ np.abs(w2d))
+
+
+@pytest.mark.parametrize("L,x_dtype", [(128, capi.SPL_F32), (256, capi.SPL_F32), (128, capi.SPL_BF16)])
+def test_encode_tc_bits_differ_only_in_reference_band(ctx, ref, L, x_dtype):
+    """K2's parity contract against the REFERENCE itself: every code bit on
+    which K2 disagrees with the reference's mlp_hash (sign of its f32
+    mlp_forward, hashers.cpp:84-108, run from the unmodified sources in
+    oracle/_ref) has a reference pre-activation inside the bf16 error band
+    bf16_band() of that output; outside the band the bits are identical."""
+    rng = np.random.default_rng(40 + L)
+    H, d, h, B, m = 4, 128, 128, 1, 2048
+    ws = [ref.mlp_gaussian_init(d, h, L, 64.0, ref.derive_seed(7, i)) for i in range(H)]
+    w1 = np.stack([w[0] for w in ws])
+    b1 = np.stack([w[1] for w in ws])
+    w2 = np.stack([w[2] for w in ws])
+    x = rng.standard_normal((B, H, m, d)).astype(np.float32)
+    if x_dtype == capi.SPL_BF16:  # the reference sees the same bf16-rounded keys
+        x = torch.from_numpy(x).bfloat16().float().numpy()
+    hs = ctx.hasher(w1, b1, w2)
+    codes, _ = run_tc(ctx, hs, x, L, x_dtype)
+    total = outside = differ = 0
+    for hd in range(H):
+        z_ref = ref.mlp_forward(w1[hd], b1[hd], w2[hd], x[0, hd])
+        want_words = pack_a7(z_ref >= 0)
+        bad = np.bitwise_xor(codes[0, hd], want_words)
+        # column j of the code sits in word j % W, bit 31 - j // W
+        W = L // 32
+        cols = np.arange(L)
+        diff = ((bad[:, cols % W] >> (31 - cols // W).astype(np.uint32)) & 1).astype(bool)
+        band = bf16_band(x[0, hd], w1[hd], b1[hd], w2[hd])
+        outside += int(np.count_nonzero(diff & (np.abs(z_ref) > band)))
+        differ += int(np.count_nonzero(diff))
+        total += diff.size
+    assert outside == 0, (outside, differ, total)
+    assert differ <= 0.01 * total, (differ, total)

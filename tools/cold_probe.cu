@@ -1,0 +1,148 @@
+// Microbenchmark (not part of the product): where does the fixed ~8 us of a
+// short HBM-bound kernel go after an L2 flush? Times a 67 MB contiguous
+// stream and a 43 MB random row gather
+//   (a) after the flush used by the bench (512 MB write + 256 MB read),
+//   (b) back to back, rotating over 4 disjoint copies (268 MB > L2, so every
+//       launch still reads from HBM, but the translations stay warm),
+//   (c) after touching one 4-byte word per 64 KB of the data (page walks
+//       paid, data still cold),
+// plus an empty kernel and a 1-CTA single-load kernel after the flush.
+// nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o cold_probe cold_probe.cu
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+#include <cstdio>
+#include <random>
+#include <vector>
+
+__device__ __forceinline__ void ld256(const void* p, uint32_t* w) {
+    asm volatile("ld.global.nc.L1::no_allocate.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3]), "=r"(w[4]), "=r"(w[5]),
+                   "=r"(w[6]), "=r"(w[7])
+                 : "l"(p));
+}
+__global__ void __launch_bounds__(256) stream_chunk(const uint8_t* __restrict__ a, uint64_t units,
+                                                    uint32_t* out) {
+    const uint64_t per = (units + gridDim.x - 1) / gridDim.x;
+    const uint64_t u0 = blockIdx.x * per, u1 = min(units, u0 + per);
+    uint32_t acc = 0;
+    for (uint64_t base = u0; base < u1; base += 4 * 256) {
+        uint32_t w[4][8];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const uint64_t i = base + u * 256 + threadIdx.x;
+            if (i < u1) ld256(a + i * 32, w[u]);
+            else for (int k = 0; k < 8; ++k) w[u][k] = 0;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+            for (int k = 0; k < 8; ++k) acc ^= w[u][k];
+    }
+    if (acc == 0x12345678u) out[0] = acc;
+}
+__global__ void g_warp8(const uint8_t* __restrict__ base, const uint32_t* __restrict__ rows, uint32_t n,
+                        uint32_t* out) {
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t w = (blockIdx.x * blockDim.x + threadIdx.x) / 32;
+    uint32_t acc = 0;
+    if (w * 8 < n) {
+        uint2 v[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const uint32_t r = w * 8 + k < n ? rows[w * 8 + k] : rows[w * 8];
+            v[k] = __ldg(reinterpret_cast<const uint2*>(base + (uint64_t)r * 256) + lane);
+        }
+#pragma unroll
+        for (int k = 0; k < 8; ++k) acc ^= v[k].x ^ v[k].y;
+    }
+    if (acc == 0x12345678u) out[0] = acc;
+}
+__global__ void touch(const uint8_t* __restrict__ a, uint64_t bytes, uint64_t step, uint32_t* out) {
+    uint32_t acc = 0;
+    for (uint64_t o = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) * step; o < bytes;
+         o += (uint64_t)gridDim.x * blockDim.x * step)
+        acc ^= __ldcg(reinterpret_cast<const uint32_t*>(a + o));
+    if (acc == 0x12345678u) out[0] = acc;
+}
+__global__ void empty_k(uint32_t* out) {
+    if (threadIdx.x == 1234) out[0] = 1;
+}
+__global__ void one_load(const uint32_t* a, uint32_t* out) {
+    const uint32_t v = __ldcg(a + threadIdx.x);
+    if (v == 0x12345678u) out[0] = v;
+}
+
+int main() {
+    const uint64_t SB = 67108864ull;  // one code cache copy
+    const uint64_t KVB = 2ull << 30;  // K/V cache for the gather
+    uint8_t *codes, *kv, *flush;
+    uint32_t *o, *d_rows;
+    cudaMalloc(&codes, 4 * SB);
+    cudaMalloc(&kv, KVB);
+    cudaMalloc(&flush, 512ull << 20);
+    cudaMalloc(&o, 4);
+    cudaMemset(codes, 1, 4 * SB);
+    cudaMemset(kv, 1, KVB);
+    const uint32_t n = 2622 * 64;
+    std::vector<uint32_t> rows(n);
+    std::mt19937 g(3);
+    const uint64_t prow = KVB / 256 / 64;
+    for (uint32_t p = 0; p < 64; ++p) {
+        std::vector<uint32_t> r(2622);
+        for (auto& x : r) x = (uint32_t)(p * prow + g() % prow);
+        std::sort(r.begin(), r.end());
+        std::copy(r.begin(), r.end(), rows.begin() + p * 2622);
+    }
+    cudaMalloc(&d_rows, n * 4);
+    cudaMemcpy(d_rows, rows.data(), n * 4, cudaMemcpyHostToDevice);
+    cudaStream_t s;
+    cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    auto flush_l2 = [&](int i) {
+        cudaMemsetAsync(flush, i, 512ull << 20, s);
+        stream_chunk<<<444, 256, 0, s>>>(flush, (256ull << 20) / 32, o);
+    };
+    auto run = [&](const char* name, auto pre, auto fn, int reps = 40) {
+        for (int i = 0; i < 3; ++i) { pre(i); fn(i); }
+        double tot = 0;
+        for (int i = 0; i < reps; ++i) {
+            pre(i);
+            cudaEventRecord(e0, s);
+            fn(i);
+            cudaEventRecord(e1, s);
+            cudaEventSynchronize(e1);
+            float t;
+            cudaEventElapsedTime(&t, e0, e1);
+            tot += t;
+        }
+        printf("%-58s %8.2f us  %s\n", name, tot / reps * 1000, cudaGetErrorString(cudaGetLastError()));
+    };
+    auto nothing = [](int) {};
+    auto stream0 = [&](int) { stream_chunk<<<444, 256, 0, s>>>(codes, SB / 32, o); };
+    auto streamR = [&](int i) { stream_chunk<<<444, 256, 0, s>>>(codes + (i % 4) * SB, SB / 32, o); };
+    auto gather = [&](int) { g_warp8<<<(n / 8 * 32 + 127) / 128, 128, 0, s>>>(kv, d_rows, n, o); };
+    run("empty kernel after flush", flush_l2, [&](int) { empty_k<<<1, 32, 0, s>>>(o); });
+    run("empty kernel back to back", nothing, [&](int) { empty_k<<<1, 32, 0, s>>>(o); });
+    run("1-CTA one load after flush", flush_l2, [&](int) { one_load<<<1, 32, 0, s>>>((uint32_t*)codes, o); });
+    run("stream 67MB after flush", flush_l2, stream0);
+    run("stream 67MB rotating 4 copies (268MB), no flush", nothing, streamR);
+    run("stream 67MB after flush + 64KB-stride touch", [&](int i) {
+        flush_l2(i);
+        touch<<<148, 256, 0, s>>>(codes, SB, 65536, o);
+    }, stream0);
+    run("gather 43MB after flush", flush_l2, gather);
+    run("gather 43MB after flush + 64KB-stride touch of K/V", [&](int i) {
+        flush_l2(i);
+        touch<<<148, 256, 0, s>>>(kv, KVB, 65536, o);
+    }, gather);
+    run("gather 43MB after a 268MB stream of other data (no flush)", [&](int i) { streamR(i); }, gather);
+    run("stream 67MB + gather 43MB, one stream, after flush", flush_l2, [&](int i) {
+        stream0(i);
+        gather(i);
+    });
+    return 0;
+}
