@@ -290,6 +290,30 @@ spl_status spl_decode_step(spl_ctx* ctx, const spl_hasher* hasher, const float* 
                            uint64_t cap, const uint32_t* n_valid, uint64_t n_max, uint32_t k,
                            float scale, uint32_t* idx, uint32_t* cnt, float* out, void* stream);
 
+/* One decode step of one layer on ONE RANK of a sequence-sharded KV cache
+ * (SURVEY §8 e, config 5): every rank holds a contiguous slice of each
+ * sequence's tokens (codes/K/V [B][H][cap][.], its local n_valid[B]); the
+ * step's new token belongs to exactly one rank (owner != 0 there, e.g. the
+ * last rank), which appends it at its local n_valid[b] - 1 — the own token
+ * sparse_attention always attends (attention_eval.cpp:249-260).
+ *   every rank: encode q; retrieval of the GLOBAL top-k (k = the global
+ *   budget) with the histogram exchange inside the kernel over peer memory;
+ *   partial attention over its own selected rows; exchange of the (m, l, o)
+ *   partials, again inside the kernel; log-sum-exp combine.
+ * idx/cnt/out_offset: this rank's share of the reference's index list (as
+ * spl_hamming_topk_sharded: local ids, position in the global list);
+ * out [B][H][d]: the full attention output, identical on every rank.
+ * All ranks of the peer group must make the same sequence of calls. One
+ * launch after the encoder when L = d = 128 and the local scores fit on
+ * chip; otherwise sharded retrieval + partial attention + peer combine. */
+spl_status spl_sharded_decode_step(spl_ctx* ctx, spl_peer* peer, const spl_hasher* hasher,
+                                   const float* q, const float* k_new, const float* v_new,
+                                   uint32_t B, int owner, uint32_t* codes, void* kcache,
+                                   void* vcache, int kv_dtype, uint64_t cap,
+                                   const uint32_t* n_valid, uint64_t n_max, uint32_t k, float scale,
+                                   uint32_t* idx, uint32_t* cnt, uint32_t* out_offset, float* out,
+                                   void* stream);
+
 /* budget_from_rate (attention_eval.hpp:70, attention_eval.cpp:266-272). */
 spl_status spl_budget_from_rate(double rate, uint64_t n, uint32_t* k);
 

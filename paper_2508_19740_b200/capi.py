@@ -107,6 +107,8 @@ _SIGS = {
     "spl_decode_step": [vp, vp, vp, vp, vp, u32, vp, vp, vp, i32, u64, vp, u64, u32, f32, vp, vp,
                         vp, vp],
     "spl_budget_from_rate": [dbl, u64, u32p],
+    "spl_sharded_decode_step": [vp, vp, vp, vp, vp, vp, u32, i32, vp, vp, vp, i32, u64, vp, u64,
+                                u32, f32, vp, vp, vp, vp, vp],
     "spl_oracle_topk": [vp, vp, vp, i32, u64, u32, u32, vp, u32, u64, f32, u32, vp, vp, vp, vp],
     "spl_iou": [vp, vp, vp, u64, vp, vp, u64, u32, vp, vp],
     "spl_project": [vp, vp, u64, u32, vp, u32, vp, vp],
@@ -507,3 +509,11 @@ class Hasher:
                                                     _ptr(vcache), kv_dtype, cap, _ptr(n_valid),
                                                     n_max, k, scale, _ptr(idx), _ptr(cnt),
                                                     _ptr(out), _stream(stream)))
+
+    def sharded_decode_step(self, peer, q, k_new, v_new, B, owner, codes, kcache, vcache, kv_dtype,
+                            cap, n_valid, n_max, k, scale, idx, cnt, out_offset, out, stream=None):
+        """One rank of a sequence-sharded decode step (spl_sharded_decode_step)."""
+        self.ctx.check(self.ctx.lib.spl_sharded_decode_step(
+            self.ctx.h, peer.h, self.h, _ptr(q), _ptr(k_new), _ptr(v_new), B, 1 if owner else 0,
+            _ptr(codes), _ptr(kcache), _ptr(vcache), kv_dtype, cap, _ptr(n_valid), n_max, k, scale,
+            _ptr(idx), _ptr(cnt), _ptr(out_offset), _ptr(out), _stream(stream)))

@@ -129,9 +129,12 @@ size_t spl_launch_log(spl_ctx* ctx, char* buf, size_t len) {
     return n;
 }
 
-spl_status spl_reserve(spl_ctx* ctx, uint32_t P, uint64_t n_max, uint32_t L, uint32_t k,
-                       uint32_t d) {
-    if (!ctx) return SPL_E_STATE;
+// Size every workspace a call on up to (P, n_max, L, k, d) can touch, on
+// stream s (spl_reserve: the legacy stream), so the calls themselves never
+// allocate: required before CUDA-graph capture, and before the first step
+// of a peer group whose kernels wait for each other inside.
+spl_status reserve_impl(spl_ctx* ctx, uint32_t P, uint64_t n_max, uint32_t L, uint32_t k,
+                        uint32_t d, cudaStream_t s) {
     // Run each path once on a dummy problem set sized like the real one is
     // not possible without data; size the buffers from the same formulas.
     const size_t score_bytes = L <= 256 ? 1 : 2;
@@ -141,26 +144,35 @@ spl_status spl_reserve(spl_ctx* ctx, uint32_t P, uint64_t n_max, uint32_t L, uin
     const size_t rec = ((G + P) * (L + 2) * 4 + 255) / 256 * 256;
     const size_t plans = ((G + P) * 16 + 255) / 256 * 256;
     spl_status st = ensure_buffer(ctx, &ctx->k3_ws, &ctx->k3_ws_bytes, sc + rec + plans, false,
-                                  0, "spl_reserve");
+                                  s, "spl_reserve");
     if (st) return st;
     size_t have = ctx->k3_state_words * 4;
     st = ensure_buffer(ctx, reinterpret_cast<void**>(&ctx->k3_state), &have,
-                       (2 + (size_t)P * (1 + (L + 2) + 4)) * 4, true, 0, "spl_reserve");
+                       (2 + (size_t)P * (1 + (L + 2) + 4)) * 4, true, s, "spl_reserve");
     if (st) return st;
     ctx->k3_state_words = have / 4;
+    // decode-step query codes
+    st = ensure_buffer(ctx, &ctx->scratch, &ctx->scratch_bytes, (size_t)P * (L / 32) * 4 + 4 * (size_t)P,
+                       false, s, "spl_reserve");
+    if (st) return st;
     if (d > 0) {
-        const size_t rps = att_rows_per_split();
-        const size_t splits_max = ((size_t)k + 1 + rps - 1) / rps;
+        if ((st = sparse_attend_reserve(ctx, P, k, d, s))) return st;
+        // the fused decode step's per-segment partials [(G + P)][d + 2]
         st = ensure_buffer(ctx, reinterpret_cast<void**>(&ctx->att_ws), &ctx->att_ws_bytes,
-                           (size_t)P * splits_max * (d + 2) * 4, false, 0, "spl_reserve");
+                           (G + P) * ((size_t)(d > 128 ? d : 128) + 2) * 4, false, s, "spl_reserve");
         if (st) return st;
-        have = ctx->att_counters_n * 4;
-        st = ensure_buffer(ctx, reinterpret_cast<void**>(&ctx->att_counters), &have,
-                           (size_t)P * 4, true, 0, "spl_reserve");
+        // the sharded step's partials [P][d + 2]
+        st = ensure_buffer(ctx, &ctx->dense_ws, &ctx->dense_ws_bytes, (size_t)P * (d + 2) * 4, false, s,
+                           "spl_reserve");
         if (st) return st;
-        ctx->att_counters_n = have / 4;
     }
     return SPL_OK;
+}
+
+spl_status spl_reserve(spl_ctx* ctx, uint32_t P, uint64_t n_max, uint32_t L, uint32_t k,
+                       uint32_t d) {
+    if (!ctx) return SPL_E_STATE;
+    return reserve_impl(ctx, P, n_max, L, k, d, 0);
 }
 
 spl_status spl_check_device_error(spl_ctx* ctx, void* stream) {
@@ -253,6 +265,11 @@ spl_status spl_peer_create(spl_ctx* ctx, uint32_t R, uint32_t rank, uint32_t P_m
     *out = nullptr;
     if (R == 0 || rank >= R || P_max == 0 || L_max == 0 || L_max % 32 != 0 || L_max > (1u << 15))
         return fail(ctx, SPL_E_DIMENSION, "peer_create: need 0 <= rank < R, P_max >= 1, L_max % 32 == 0");
+    // the group's kernels wait for each other inside: load every kernel a
+    // sharded call can launch now, not lazily in the middle of a step
+    encode_preload();
+    attend_preload();
+    k3_preload();
     auto* pe = new spl_peer;
     pe->R = R;
     pe->rank = rank;
@@ -714,6 +731,90 @@ spl_status spl_decode_step(spl_ctx* ctx, const spl_hasher* hs, const float* q,
     if (st) return st;
     return spl_sparse_attend(ctx, q, kcache, vcache, kv_dtype, cap, hs->d, P, idx, k, cnt,
                              n_valid, H, scale, out, stream);
+}
+
+spl_status spl_sharded_decode_step(spl_ctx* ctx, spl_peer* peer, const spl_hasher* hs,
+                                   const float* q, const float* k_new, const float* v_new,
+                                   uint32_t B, int owner, uint32_t* codes, void* kcache,
+                                   void* vcache, int kv_dtype, uint64_t cap,
+                                   const uint32_t* n_valid, uint64_t n_max, uint32_t k, float scale,
+                                   uint32_t* idx, uint32_t* cnt, uint32_t* out_offset, float* out,
+                                   void* stream) {
+    NvtxRange nvtx_("spl_sharded_decode_step");
+    if (!ctx || !hs || !peer) return SPL_E_STATE;
+    if (!peer->connected) return fail(ctx, SPL_E_STATE, "sharded_decode_step: peer group not connected");
+    if (!(scale > 0.0f)) return fail(ctx, SPL_E_DIMENSION, "attention: scale must be positive");
+    if (n_max > cap)
+        return fail(ctx, SPL_E_DIMENSION,
+                    "sharded_decode_step: n_max=" + std::to_string(n_max) +
+                        " exceeds the cache capacity " + std::to_string(cap));
+    const uint32_t H = hs->H, W = hs->L / 32, P = B * H;
+    spl_status st = ensure_buffer(ctx, &ctx->scratch, &ctx->scratch_bytes,
+                                  (size_t)P * W * 4 + 4 * (size_t)B, false, S(stream),
+                                  "sharded_decode_step");
+    if (st) return st;
+    uint32_t* qcodes = static_cast<uint32_t*>(ctx->scratch);
+    // every workspace of the step is sized before its first launch: the
+    // retrieval kernel waits for the peers inside, and an allocation (or a
+    // zero-fill synchronisation) behind it would stall the group
+    if ((st = reserve_impl(ctx, P, n_max, hs->L, k, hs->d, S(stream)))) return st;
+    // every rank encodes the query; the rank the new token belongs to appends it
+    EncJob jobs[2]{};
+    int nj = 0;
+    if (owner) {
+        jobs[nj].x = k_new;
+        jobs[nj].m = 1;
+        jobs[nj].out_mode = ENC_APPEND;
+        jobs[nj].codes = codes;
+        jobs[nj].cap = cap;
+        jobs[nj].pos = n_valid;
+        jobs[nj].pos_minus_one = 1;
+        jobs[nj].v_new = v_new;
+        jobs[nj].kcache = kcache;
+        jobs[nj].vcache = vcache;
+        jobs[nj].kv_dtype = kv_dtype;
+        ++nj;
+    }
+    jobs[nj].x = q;
+    jobs[nj].m = 1;
+    jobs[nj].out_mode = ENC_CODES;
+    jobs[nj].codes = qcodes;
+    ++nj;
+    if ((st = encode_exact_launch(ctx, hs, B, jobs, nj, S(stream)))) return st;
+    bool done = false;
+    if ((st = hamming_topk_attend_impl(ctx, codes, cap, hs->L, qcodes, P, n_valid, H, n_max, k, idx,
+                                       cnt, q, kcache, vcache, kv_dtype, hs->d, scale * kLog2e, out,
+                                       S(stream), &done, peer, out_offset, owner)))
+        return st;
+    if (done) return SPL_OK;
+    // unfused: sharded retrieval, this rank's partial attention, peer combine
+    if ((st = hamming_topk_sharded_impl(ctx, peer, codes, cap, hs->L, qcodes, P, n_valid, H, n_max,
+                                        k, idx, cnt, out_offset, S(stream))))
+        return st;
+    const uint32_t d = hs->d;
+    st = ensure_buffer(ctx, &ctx->dense_ws, &ctx->dense_ws_bytes, (size_t)P * (d + 2) * sizeof(float),
+                       false, S(stream), "sharded_decode_step");
+    if (st) return st;
+    float* part = static_cast<float*>(ctx->dense_ws);
+    AttParams prm{};
+    prm.q = q;
+    prm.kc = kcache;
+    prm.vc = vcache;
+    prm.stride_rows = cap;
+    prm.d = d;
+    prm.P = P;
+    prm.idx = idx;
+    prm.idx_stride = k;
+    prm.cnt = cnt;
+    prm.n_valid = n_valid;
+    prm.nvalid_div = H;
+    prm.own_row = nullptr;  // not the owner: no own row
+    prm.own_nvalid = owner ? 1 : 0;
+    prm.qscale = scale * kLog2e;
+    prm.out = part;
+    prm.partial_mode = 1;
+    if ((st = sparse_attend_launch(ctx, prm, k, kv_dtype, S(stream)))) return st;
+    return peer_combine_launch(ctx, peer, part, P, d, out, S(stream));
 }
 
 spl_status spl_budget_from_rate(double rate, uint64_t n, uint32_t* k) {

@@ -552,4 +552,13 @@ spl_status encode_exact_launch(spl_ctx* ctx, const spl_hasher* hs, uint32_t B,
     return after_launch(ctx, "k1_encode_exact");
 }
 
+// Force the lazy (CUDA_MODULE_LOADING=LAZY) load of the encoder kernels now:
+// a first launch loads its module and synchronises the context, which must
+// not happen while a kernel of a peer group spins waiting for the others.
+void encode_preload() {
+    cudaFuncAttributes a;
+    cudaFuncGetAttributes(&a, reinterpret_cast<const void*>(&k1_encode_exact));
+    cudaFuncGetAttributes(&a, reinterpret_cast<const void*>(&k1_encode_cluster));
+}
+
 }  // namespace spl

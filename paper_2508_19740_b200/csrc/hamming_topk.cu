@@ -108,6 +108,10 @@ struct K3Params {
     float* att_part;       // [(G + P)][130] per-segment (m, l, o[128])
     uint32_t* att_cnt;     // [P] segments attended (self-resetting)
     float* att_out;        // [P][128]
+    int att_own;           // this rank holds the own row (n_valid - 1): always 1
+                           // unsharded; sharded decode: the rank the new token went to
+    uint32_t part_off;     // sharded decode: u32 offset of the partial-exchange area in
+                           // every rank's peer buffer (after the histogram area)
     int att_pf;            // 1: the select also prefetches the emitted rows into L2
                            // (SPL_ATT_PF=1; measured no faster than without: the
                            // gather is DRAM-bound either way)
@@ -1086,6 +1090,66 @@ __device__ ShardPlanOut shard_global_plan(const K3Params& prm, uint32_t epoch, u
     return o;
 }
 
+// ------------------------------------------------ partial exchange (sharded decode)
+// Second area of every rank's peer buffer (after the histograms): per (epoch
+// parity, source rank, problem) D + 2 tagged u64 entries {value bits, epoch}
+// = (m, l, o[D]) of that rank's partial attention. Same LL protocol as the
+// histograms: value and tag land in one 8-byte store, double-buffered by
+// parity (a rank cannot run two calls ahead of a peer).
+constexpr uint32_t kPartDMax = 256;  // head dims the exchange supports
+__host__ __device__ __forceinline__ uint64_t part_slot(uint32_t R, uint32_t Pmax, uint32_t par,
+                                                       uint32_t r, uint32_t p) {
+    return 2ull * ((((uint64_t)par * R + r) * Pmax + p) * (kPartDMax + 2));  // u32 words
+}
+__host__ __device__ __forceinline__ uint64_t part_words(uint32_t R, uint32_t Pmax) {
+    return part_slot(R, Pmax, 2, 0, 0);
+}
+// Entry i of this rank's partial of problem p -> every rank's area.
+__device__ __forceinline__ void part_push(const K3Params& prm, uint32_t epoch, uint32_t p,
+                                          uint32_t i, float v) {
+    const uint64_t at = prm.part_off + part_slot(prm.R, prm.Pmax, epoch & 1u, prm.rank, p) + 2 * i;
+    for (uint32_t r = 0; r < prm.R; ++r) st_tagged(prm.peer_bufs[r] + at, __float_as_uint(v), epoch);
+}
+// Entry i of rank r's partial of problem p, from this rank's own area.
+__device__ __forceinline__ float part_wait(const K3Params& prm, uint32_t epoch, uint32_t r,
+                                           uint32_t p, uint32_t i) {
+    const uint64_t at = prm.part_off + part_slot(prm.R, prm.Pmax, epoch & 1u, r, p) + 2 * i;
+    return __uint_as_float(wait_tagged(prm.own_buf + at, epoch, prm.dev_err));
+}
+// Thread `dim` (< D) of the CTA that finished problem p on this rank: push
+// the rank's (M, L, o[dim]) (thread 0 also M and L), collect all R ranks'
+// and return the normalised output (flash-decoding log-sum-exp combine).
+__device__ float part_exchange_combine(const K3Params& prm, uint32_t epoch, uint32_t p,
+                                       uint32_t dim, float M, float Ls, float o) {
+    if (dim == 0) {
+        part_push(prm, epoch, p, 0, M);
+        part_push(prm, epoch, p, 1, Ls);
+    }
+    part_push(prm, epoch, p, 2 + dim, o);
+    float Mx = -INFINITY;
+    for (uint32_t r = 0; r < prm.R; ++r) Mx = fmaxf(Mx, part_wait(prm, epoch, r, p, 0));
+    float acc = 0.0f, Lt = 0.0f;
+    for (uint32_t r = 0; r < prm.R; ++r) {
+        const float m = part_wait(prm, epoch, r, p, 0);
+        if (m == -INFINITY) continue;
+        const float f = exp2f(m - Mx);
+        Lt = fmaf(part_wait(prm, epoch, r, p, 1), f, Lt);
+        acc = fmaf(part_wait(prm, epoch, r, p, 2 + dim), f, acc);
+    }
+    return acc / Lt;
+}
+
+// Sharded decode step, unfused form (head dims other than 128): this rank's
+// partial attention partials [P][D + 2] (spl_sparse_attend_partial) are
+// exchanged with the peer group and combined; one CTA of D threads per
+// problem. The epoch is the one the preceding k3_fused<SHARD> call stored.
+__global__ void k5_peer_combine(K3Params prm, const float* partials, uint32_t D, float* out) {
+    const uint32_t p = blockIdx.x, dim = threadIdx.x;
+    const uint32_t epoch = __ldcg(prm.epoch_ptr);
+    const float* pp = partials + (uint64_t)p * (D + 2);
+    if (dim < D) out[(uint64_t)p * D + dim] = part_exchange_combine(prm, epoch, p, dim, pp[0], pp[1], pp[2 + dim]);
+}
+
 // ------------------------------------------------------------ fused attend
 // Shared-memory layout of the private-counter region once the stream is over
 // (decode step, k3_fused<.., ATT>): [select masks: NV x kThreads words]
@@ -1120,11 +1184,14 @@ __device__ __forceinline__ uint32_t att_ids_cap(size_t priv_bytes, uint32_t nv_s
 // partials (log-sum-exp, every load of the merge issued in one round) into
 // att_out[p]. Every CTA of the problem calls this (those with no rows write
 // an empty partial). scratch: kAttScratchWords floats.
-template <typename KV>
+// SHARD (sequence-sharded decode step): the problem's combined partial is
+// this rank's only; it is exchanged with the other ranks through peer memory
+// (part_exchange_combine) and every rank writes the same final output.
+template <typename KV, bool SHARD>
 __device__ void fused_attend(const K3Params& prm, uint32_t p, uint32_t seg, uint32_t c0,
                              uint32_t nseg, uint32_t nv, bool owner, uint64_t off, uint32_t count,
                              float* scratch, const uint32_t* sids, uint32_t ids_cap,
-                             uint32_t* s_flag) {
+                             uint32_t* s_flag, uint32_t epoch) {
     constexpr int E = 4, D = 128, NW = kThreads / 32;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     float qv[E];
@@ -1241,7 +1308,11 @@ __device__ void fused_attend(const K3Params& prm, uint32_t p, uint32_t seg, uint
         const float f0 = s_hm[0] == -INFINITY ? 0.0f : exp2f(s_hm[0] - M2);
         const float f1 = s_hm[1] == -INFINITY ? 0.0f : exp2f(s_hm[1] - M2);
         const float Lt = s_hl[0] * f0 + s_hl[1] * f1;
-        prm.att_out[(uint64_t)p * D + tid] = (s_ha[tid] * f0 + s_ha[D + tid] * f1) / Lt;
+        const float ov = s_ha[tid] * f0 + s_ha[D + tid] * f1;
+        if constexpr (SHARD)
+            prm.att_out[(uint64_t)p * D + tid] = part_exchange_combine(prm, epoch, p, tid, M2, Lt, ov);
+        else
+            prm.att_out[(uint64_t)p * D + tid] = ov / Lt;
     }
     if (tid == 0) prm.att_cnt[p] = 0u;  // self-reset for the next launch / graph replay
 }
@@ -1514,11 +1585,11 @@ __global__ void __launch_bounds__(kThreads, 3) k3_fused(K3Params prm) {
         }
         if constexpr (ATT) {
             K3_STAMP(7);
-            const bool owner = r0 < r1 && r1 == (uint64_t)nv;  // this segment holds row nv - 1
+            const bool owner = prm.att_own && r0 < r1 && r1 == (uint64_t)nv;  // holds row nv - 1
             const uint32_t nvs = (r1 - a0 <= (uint64_t)kThreads * 16 * 3) ? 3u : 11u;  // select's NV
-            fused_attend<KV>(prm, p, seg, c0, nseg, nv, owner, off, my_count,
-                             reinterpret_cast<float*>(priv), att_ids<ATT>(priv, priv_bytes, nvs),
-                             att_ids_cap<ATT>(priv_bytes, nvs), &s_flag);
+            fused_attend<KV, SHARD>(prm, p, seg, c0, nseg, nv, owner, off, my_count,
+                                    reinterpret_cast<float*>(priv), att_ids<ATT>(priv, priv_bytes, nvs),
+                                    att_ids_cap<ATT>(priv_bytes, nvs), &s_flag, epoch);
         }
     }
     K3_STAMP(5);
@@ -1782,7 +1853,7 @@ spl_status make_fused_plan(spl_ctx* ctx, uint32_t P, uint64_t n_max, uint32_t L,
                            uint64_t stride_rows, bool* ok, K3FPlan* out, bool shard = false,
                            bool pf = false, int att = 0) {
     *ok = false;
-    if (att && (L != 128 || shard)) return SPL_OK;
+    if (att && L != 128) return SPL_OK;
     const uint32_t W = L / 32;
     // Private counters cover scores [L/2, L] only: the k-th best agreement is
     // >= L/2 whenever at least k rows agree on half their bits (retrieval
@@ -1799,9 +1870,11 @@ spl_status make_fused_plan(spl_ctx* ctx, uint32_t P, uint64_t n_max, uint32_t L,
             case 2: fn = shard ? fused_fn<2, uint8_t, true>() : fused_fn<2, uint8_t>(); break;
             case 4:
                 if (att == 1)
-                    fn = fused_fn<4, uint8_t, false, true, true, __nv_bfloat16>();
+                    fn = shard ? fused_fn<4, uint8_t, true, true, true, __nv_bfloat16>()
+                               : fused_fn<4, uint8_t, false, true, true, __nv_bfloat16>();
                 else if (att == 2)
-                    fn = fused_fn<4, uint8_t, false, true, true, float>();
+                    fn = shard ? fused_fn<4, uint8_t, true, true, true, float>()
+                               : fused_fn<4, uint8_t, false, true, true, float>();
                 else
                     fn = shard ? fused_fn<4, uint8_t, true>()
                                : (pf ? fused_fn<4, uint8_t, false, true>() : fused_fn<4, uint8_t>());
@@ -2133,13 +2206,22 @@ spl_status hamming_topk_impl(spl_ctx* ctx, const uint32_t* codes, uint64_t strid
 // the selected rows U {own}. *done = false (and nothing launched) when the
 // fused geometry does not apply (L != 128, d != 128, scores too large for
 // shared memory, SPL_K3_PATH=twopass): the caller then runs K3 + K4.
+// peer != nullptr: one rank of a sequence-sharded cache (k3_fused<SHARD,
+// ATT>): histograms and then the per-problem partial attention are exchanged
+// with the other ranks inside the kernel; idx / cnt / out_offset are this
+// rank's share (as spl_hamming_topk_sharded), out the full result on every
+// rank; own != 0 on the rank that holds the own row (its local n_valid - 1).
 spl_status hamming_topk_attend_impl(spl_ctx* ctx, const uint32_t* codes, uint64_t stride_rows,
                                     uint32_t L, const uint32_t* qcodes, uint32_t P,
                                     const uint32_t* n_valid, uint32_t nvalid_div, uint64_t n_max,
                                     uint32_t k, uint32_t* idx, uint32_t* cnt, const float* q,
                                     const void* kcache, const void* vcache, int kv_dtype, uint32_t d,
-                                    float qscale, float* out, cudaStream_t s, bool* done) {
+                                    float qscale, float* out, cudaStream_t s, bool* done,
+                                    spl_peer* peer, uint32_t* out_offset, int own) {
     *done = false;
+    if (peer && (!peer->connected || P > peer->Pmax || L > peer->Lmax ||
+                 (size_t)peer->R * (L + 2) * 4 > K3_SEL_SCRATCH_BYTES))
+        return SPL_OK;
     if (d != 128 || L != 128 || (kv_dtype != SPL_BF16 && kv_dtype != SPL_F32) || !fused_allowed())
         return SPL_OK;
     const char* e = getenv("SPL_DECODE_FUSED");
@@ -2151,7 +2233,7 @@ spl_status hamming_topk_attend_impl(spl_ctx* ctx, const uint32_t* codes, uint64_
     if (stride_rows == 0 || n_max > stride_rows) return SPL_OK;
     bool ok = false;
     K3FPlan fp{};
-    if ((st = make_fused_plan(ctx, P, n_max, L, codes, stride_rows, &ok, &fp, false, true,
+    if ((st = make_fused_plan(ctx, P, n_max, L, codes, stride_rows, &ok, &fp, peer != nullptr, true,
                               kv_dtype == SPL_BF16 ? 1 : 2)))
         return st;
     if (!ok) return SPL_OK;
@@ -2183,6 +2265,17 @@ spl_status hamming_topk_attend_impl(spl_ctx* ctx, const uint32_t* codes, uint64_
     prm.att_part = ctx->att_ws;
     prm.att_cnt = ctx->att_counters;
     prm.att_out = out;
+    prm.att_own = peer ? (own ? 1 : 0) : 1;
+    if (peer) {
+        prm.peer_bufs = peer->d_table;
+        prm.own_buf = peer->buf;
+        prm.R = peer->R;
+        prm.rank = peer->rank;
+        prm.Pmax = peer->Pmax;
+        prm.epoch_ptr = peer->d_epoch;
+        prm.out_offset = out_offset;
+        prm.part_off = (uint32_t)xwords(peer->R, peer->Pmax, peer->Lmax + 2);
+    }
     {
         const char* e = getenv("SPL_ATT_PF");
         prm.att_pf = (e && *e == '1') ? 1 : 0;
@@ -2200,10 +2293,29 @@ spl_status hamming_topk_attend_impl(spl_ctx* ctx, const uint32_t* codes, uint64_
         SPL_CUDA_TRY(ctx, cudaLaunchCooperativeKernel(fp.fn, dim3(G), dim3(kThreads), args, fp.smem, s));
     else
         SPL_CUDA_TRY(ctx, launch_pdl(fp.fn, dim3(G), dim3(kThreads), fp.smem, s, args));
-    if ((st = after_launch(ctx, "k3_fused_attend"))) return st;
+    if ((st = after_launch(ctx, peer ? "k3_fused_shard_attend" : "k3_fused_attend"))) return st;
     if (dtrace) k3_trace_report(dtrace, G, fp.pl.g.S, s);
     *done = true;
     return SPL_OK;
+}
+
+spl_status peer_combine_launch(spl_ctx* ctx, spl_peer* peer, const float* partials, uint32_t P,
+                               uint32_t d, float* out, cudaStream_t s) {
+    if (!peer || !peer->connected) return fail(ctx, SPL_E_STATE, "peer_combine: peer group not connected");
+    if (d == 0 || d > kPartDMax)
+        return fail(ctx, SPL_E_DIMENSION, "sharded_decode_step: head dim must be 1 .. 256");
+    if (P == 0) return SPL_OK;
+    K3Params prm{};
+    prm.peer_bufs = peer->d_table;
+    prm.own_buf = peer->buf;
+    prm.R = peer->R;
+    prm.rank = peer->rank;
+    prm.Pmax = peer->Pmax;
+    prm.epoch_ptr = peer->d_epoch;
+    prm.part_off = (uint32_t)xwords(peer->R, peer->Pmax, peer->Lmax + 2);
+    prm.dev_err = ctx->dev_err;
+    k5_peer_combine<<<P, (d + 31) / 32 * 32, 0, s>>>(prm, partials, d, out);
+    return after_launch(ctx, "k5_peer_combine");
 }
 
 spl_status shard_histogram_impl(spl_ctx* ctx, const uint32_t* codes, uint64_t stride_rows,
@@ -2277,7 +2389,7 @@ spl_status shard_select_impl(spl_ctx* ctx, const uint32_t* all_hist, uint32_t R,
 }
 
 uint64_t peer_area_words(uint32_t R, uint32_t Pmax, uint32_t Lmax) {
-    return xwords(R, Pmax, Lmax + 2);
+    return xwords(R, Pmax, Lmax + 2) + part_words(R, Pmax);  // histograms + partials
 }
 
 // ------------------------------------------------ fused sharded retrieval
@@ -2332,6 +2444,19 @@ spl_status hamming_topk_sharded_impl(spl_ctx* ctx, spl_peer* peer, const uint32_
     st = after_launch(ctx, "k3_fused_shard");
     if (dtrace) k3_trace_report(dtrace, fp.pl.g.G, fp.pl.g.S, s);
     return st;
+}
+
+// Force the lazy load of the sharded-path kernels (see encode_preload): a
+// peer group's kernels wait for each other inside, so no member may hit a
+// module load (a context synchronisation) in the middle of a step.
+void k3_preload() {
+    cudaFuncAttributes a;
+    const void* fns[] = {fused_fn<1, uint8_t, true>(), fused_fn<2, uint8_t, true>(),
+                         fused_fn<4, uint8_t, true>(),
+                         fused_fn<4, uint8_t, true, true, true, __nv_bfloat16>(),
+                         fused_fn<4, uint8_t, true, true, true, float>(),
+                         reinterpret_cast<const void*>(&k5_peer_combine)};
+    for (const void* f : fns) cudaFuncGetAttributes(&a, f);
 }
 
 }  // namespace spl

@@ -253,7 +253,7 @@ __global__ void __launch_bounds__(kAttThreads) k4_lane(AttParams prm) {
     const uint32_t c = prm.cnt[p];
     const uint32_t* list = prm.idx + (uint64_t)p * prm.idx_stride;
     uint32_t own;
-    if (prm.partial_mode)
+    if (prm.partial_mode && !prm.own_nvalid)
         own = prm.own_row ? prm.own_row[p] : kInv;
     else
         own = prm.n_valid[p / prm.nvalid_div] - 1u;
@@ -332,7 +332,7 @@ __global__ void __launch_bounds__(kAttThreads) k4_gather(AttParams prm) {
     const uint32_t c = prm.cnt[p];
     const uint32_t* list = prm.idx + (uint64_t)p * prm.idx_stride;
     uint32_t own;
-    if (prm.partial_mode)
+    if (prm.partial_mode && !prm.own_nvalid)
         own = prm.own_row ? prm.own_row[p] : kInv;
     else
         own = prm.n_valid[p / prm.nvalid_div] - 1u;
@@ -369,7 +369,7 @@ __global__ void k4_attend_generic(AttParams prm) {
     const uint32_t c = prm.cnt[p];
     const uint32_t* list = prm.idx + (uint64_t)p * prm.idx_stride;
     uint32_t own;
-    if (prm.partial_mode)
+    if (prm.partial_mode && !prm.own_nvalid)
         own = prm.own_row ? prm.own_row[p] : kInv;
     else
         own = prm.n_valid[p / prm.nvalid_div] - 1u;
@@ -463,6 +463,27 @@ const void* att_fn(int kv_dtype) {
 
 }  // namespace
 
+// Size K4's workspace (partials + counters) for P problems of up to kmax
+// listed rows and head dim d, before any launch of a call that must not
+// allocate between its kernels (the sharded step: an allocation or a
+// zero-fill synchronisation while a kernel of the step waits for its peers
+// would stall it).
+spl_status sparse_attend_reserve(spl_ctx* ctx, uint32_t P, uint32_t kmax, uint32_t d, cudaStream_t s) {
+    const uint64_t R = att_rows_per_split();
+    const uint64_t nsplit = ((uint64_t)kmax + 1 + R - 1) / R;
+    const size_t dd = d > 128 ? d : 128;  // the fused decode step's partials use d = 128 too
+    spl_status st = ensure_buffer(ctx, reinterpret_cast<void**>(&ctx->att_ws), &ctx->att_ws_bytes,
+                                  (size_t)P * nsplit * (dd + 2) * sizeof(float), false, s,
+                                  "sparse_attend");
+    if (st) return st;
+    size_t have = ctx->att_counters_n * 4;
+    st = ensure_buffer(ctx, reinterpret_cast<void**>(&ctx->att_counters), &have, (size_t)P * 4, true,
+                       s, "sparse_attend");
+    if (st) return st;
+    ctx->att_counters_n = have / 4;
+    return SPL_OK;
+}
+
 uint32_t att_rows_per_split() {
     return k4_mode() == 1 ? (uint32_t)(kAttWarps * kWarpRows) : (uint32_t)(kAttWarps * kAttRB * k4_nb());
 }
@@ -520,6 +541,17 @@ spl_status attend_combine_launch(spl_ctx* ctx, const float* partials, uint32_t R
     if (P == 0) return SPL_OK;
     k5_combine<<<P, 128, 0, s>>>(partials, R, P, d, out);
     return after_launch(ctx, "k5_combine");
+}
+
+// Force the lazy load of every K4 variant (see encode_preload).
+void attend_preload() {
+    cudaFuncAttributes a;
+    const void* fns[] = {att_fn<1>(SPL_BF16), att_fn<1>(SPL_F32), att_fn<2>(SPL_BF16),
+                         att_fn<2>(SPL_F32),  att_fn<4>(SPL_BF16), att_fn<4>(SPL_F32),
+                         att_fn<8>(SPL_BF16), att_fn<8>(SPL_F32),
+                         reinterpret_cast<const void*>(&k4_attend_generic),
+                         reinterpret_cast<const void*>(&k5_combine)};
+    for (const void* f : fns) cudaFuncGetAttributes(&a, f);
 }
 
 }  // namespace spl

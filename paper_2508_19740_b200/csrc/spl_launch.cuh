@@ -41,6 +41,7 @@ struct AttParams {
     uint32_t* counters;        // [P]
     float* out;                // normal: [P][d]; partial mode: [P][d + 2] (m, l, o)
     int partial_mode;
+    int own_nvalid;            // partial mode: own = n_valid[p / div] - 1 (own_row unused)
 };
 
 // hamming_topk.cu
@@ -50,7 +51,10 @@ spl_status hamming_topk_impl(spl_ctx*, const uint32_t*, uint64_t, uint32_t, cons
 spl_status hamming_topk_attend_impl(spl_ctx*, const uint32_t*, uint64_t, uint32_t,
                                     const uint32_t*, uint32_t, const uint32_t*, uint32_t, uint64_t,
                                     uint32_t, uint32_t*, uint32_t*, const float*, const void*,
-                                    const void*, int, uint32_t, float, float*, cudaStream_t, bool*);
+                                    const void*, int, uint32_t, float, float*, cudaStream_t, bool*,
+                                    spl_peer* = nullptr, uint32_t* = nullptr, int = 1);
+spl_status peer_combine_launch(spl_ctx*, spl_peer*, const float*, uint32_t, uint32_t, float*,
+                               cudaStream_t);
 spl_status shard_histogram_impl(spl_ctx*, const uint32_t*, uint64_t, uint32_t, const uint32_t*,
                                 uint32_t, const uint32_t*, uint32_t, uint64_t, uint32_t*,
                                 cudaStream_t);
@@ -62,6 +66,10 @@ spl_status hamming_topk_sharded_impl(spl_ctx*, spl_peer*, const uint32_t*, uint6
                                      uint64_t, uint32_t, uint32_t*, uint32_t*, uint32_t*,
                                      cudaStream_t);
 uint64_t peer_area_words(uint32_t R, uint32_t Pmax, uint32_t Lmax);
+// lazy-module preloads (spl_peer_create): encoder, K4 / K5, sharded K3
+void encode_preload();
+void attend_preload();
+void k3_preload();
 // bitcodes_misc.cu
 spl_status pack_bits_launch(spl_ctx*, const uint8_t*, uint64_t, uint32_t, uint32_t*, cudaStream_t);
 spl_status unpack_bits_launch(spl_ctx*, const uint32_t*, uint64_t, uint32_t, uint8_t*,
@@ -92,6 +100,7 @@ bool encode_tc_eligible(uint32_t kind, uint32_t d, uint32_t h, uint32_t L);
 // sparse_attend.cu
 spl_status sparse_attend_launch(spl_ctx*, AttParams, uint32_t, int, cudaStream_t);
 uint32_t att_rows_per_split();  // list entries per K4 CTA (sizes the partials)
+spl_status sparse_attend_reserve(spl_ctx*, uint32_t P, uint32_t kmax, uint32_t d, cudaStream_t);
 spl_status attend_combine_launch(spl_ctx*, const float*, uint32_t, uint32_t, uint32_t, float*,
                                  cudaStream_t);
 
