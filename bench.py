@@ -157,6 +157,45 @@ def flushed_timer(torch, fn, steps, stream):
     return statistics.median(a.elapsed_time(b) for a, b in evs)
 
 
+def flushed_graph_timer(torch, fn, steps, warmup):
+    """Device ms per call with L2 flushed before every call and without the
+    per-launch host/driver gap: one CUDA graph holds `steps` x (flush, call),
+    a second one the same `steps` flushes alone; both are timed with CUDA
+    events around a replay, and the difference / steps is the call's device
+    time (the flush = a 512 MB write then a 256 MB read, so L2 holds only
+    clean unrelated lines when the call starts). Returns (ms, flush_ms) or
+    None if capture fails."""
+    if "buf" not in _FLUSH:
+        flushed_timer(torch, lambda: None, 1, torch.cuda.current_stream())
+    buf, rd, acc = _FLUSH["buf"], _FLUSH["rd"], _FLUSH["acc"]
+
+    def flush():
+        buf.fill_(1)
+        acc.add_(rd.sum())
+    try:
+        gs = torch.cuda.Stream()
+        gs.wait_stream(torch.cuda.current_stream())
+        g1, g0 = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g1, stream=gs, capture_error_mode="relaxed"):
+            for _ in range(steps):
+                flush()
+                fn(gs)
+        with torch.cuda.graph(g0, stream=gs, capture_error_mode="relaxed"):
+            for _ in range(steps):
+                flush()
+        cur = torch.cuda.current_stream()
+        for _ in range(max(1, warmup // 2)):
+            g1.replay()
+            g0.replay()
+        torch.cuda.synchronize()
+        t1 = min(event_timer(torch, g1.replay, 1, cur) for _ in range(3))
+        t0 = min(event_timer(torch, g0.replay, 1, cur) for _ in range(3))
+        del g1, g0
+        return (t1 - t0) / steps, t0 / steps
+    except Exception:
+        return None
+
+
 def graph_timer(torch, fn, steps, warmup, flush=False):
     """Capture one call of fn (our kernels on a side stream) in a CUDA graph
     and time `steps` replays; None if capture is not possible. flush: L2
@@ -231,14 +270,11 @@ def run_reference_arm(args):
             "n_gpus": world, "steps": steps, "warmup": args.warmup,
             "ms_per_step": round(v / 1000, 4), "higher_is_better": False, "scaling": "weak",
             "vs_baseline": None, "dtype": "u32", "data": "synthetic",
-            "config": {"workload": (f"config3: 32 heads x 524288 tokens x 128-bit codes, k={k} "
-                                    if world == 1 else
-                                    f"config5: 32 heads x {n_tot} tokens x 128-bit codes, k={k} ")
-                                   + "(per head nxor_scores_into + top_k_indices)", "heads": H,
-                       "tokens": n_tot, "code_bits": L, "k": k},
+            "config": workload_config(world),
             "cpu_baseline": {"value": round(v, 2), "unit": "µs", "cores": threads, "kind": kind,
-                             "sample": f"full workload per step ({H} heads x {n_tot} rows), "
-                                       f"heads spread over {threads} OpenMP threads"},
+                             "sample": f"full workload per step ({H} heads x {n_tot} rows: per head "
+                                       f"nxor_scores_into + top_k_indices), heads spread over "
+                                       f"{threads} OpenMP threads"},
             "e2e": {"value": round(v, 2), "unit": "µs", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -246,6 +282,19 @@ def run_reference_arm(args):
 
 def budget(n):
     return min(max(int(0.02 * n), 20), n)
+
+
+def workload_config(world):
+    """The `config` of the JSON line — identical in both arms (ours and
+    --impl reference) so the driver can match them."""
+    n_total = N_TOK * world
+    k = budget(n_total)
+    return {"workload": ("config3: 32 heads x 524288 tokens x 128-bit codes, k=10485" if world == 1 else
+                         f"config5: sequence-sharded {n_total} tokens x 32 heads x 128-bit codes, "
+                         f"k={k}, per-head histograms exchanged across ranks"),
+            "heads": H, "tokens_per_gpu": N_TOK, "tokens_total": n_total, "code_bits": L, "k": k,
+            "l2": "inputs (268 MB of codes per GPU) larger than the 126 MB L2; value without flush, "
+                  "value_l2_flushed with L2 flushed before every retrieval"}
 
 
 # ---------------------------------------------------------------- GPU arm
@@ -401,6 +450,15 @@ def main():
             graph_note = "CUDA graph replay, 1 retrieval per replay"
         except Exception as e:  # capture unsupported: keep the eager number
             graph_note = f"eager (graph capture failed: {str(e)[:80]})"
+    # the same retrieval with L2 flushed before every call (device time from
+    # CUDA graphs of steps x (flush, call) minus steps x flush): the inputs
+    # already exceed L2, this shows the number does not lean on L2 residue
+    flushed_ms = None
+    if world == 1:
+        fl = flushed_graph_timer(
+            torch, lambda st: ctx.hamming_topk(codes, n_local, L, qcodes, P, nvalid, 1, n_local, k, idx,
+                                               cnt, st), min(args.steps, 20), args.warmup)
+        flushed_ms = fl[0] if fl else None
     if dist:
         t = torch.tensor([ms], device=dev)
         all_reduce_dev(t, dist.ReduceOp.MAX)
@@ -461,9 +519,16 @@ def main():
            "h2d_bytes_per_step": int(q_host.numel() * 4),
            "d2h_bytes_per_step": int(d2h),
            "path": ("spl_encode(query, exact) + spl_hamming_topk, pinned host buffers" if world == 1
-                    else "spl_encode(query, exact) + spl_shard_histogram + NCCL all-gather + "
-                         "spl_shard_select, pinned host buffers (max over ranks)"),
+                    else "spl_encode(query, exact) + " + (shard_path or "") +
+                         ", pinned host buffers (max over ranks)"),
            "encode_us": round(enc_ms * 1000, 2)}
+    sharded = heads = None
+    if not args.no_decode:
+        sharded = bench_sharded_decode(torch, capi, ctx, dev, stream, args, world, rank, dist, same_gpu,
+                                       all_reduce_dev)
+        if world > 1:
+            heads = bench_head_sharded(torch, capi, ctx, dev, stream, args, world, rank, dist, same_gpu,
+                                       all_reduce_dev)
     if world == 1:
         if not args.no_decode:
             decode = bench_decode(torch, capi, ctx, dev, stream, args, hasher)
@@ -504,30 +569,31 @@ def main():
     alg_bytes = P * n_local * W * 4 + P * W * 4 + P * k * 4  # SURVEY 8(d), per rank
     achieved = alg_bytes / (us * 1e-6) / 1e9
     scan_bytes = P * n_local * W * 4
-    traffic = None
-    tpath = ROOT / "profiles" / "r01_k3_traffic.json"
-    if tpath.exists():
+    # dram bytes per retrieval: ncu cannot run inside the timed process, so
+    # this is the newest committed `ncu --set full` capture of the same kernel
+    # on the same workload, stamped with the commit it was taken at
+    traffic = traffic_src = None
+    for tpath in sorted((ROOT / "profiles").glob("r*_k3_traffic.json"), reverse=True):
         try:
-            traffic = json.loads(tpath.read_text()).get("bytes_per_retrieval")
+            tj = json.loads(tpath.read_text())
+            traffic = tj.get("bytes_per_retrieval")
+            traffic_src = f"{tpath.relative_to(ROOT)} (commit {tj.get('commit', 'unrecorded')})"
+            break
         except Exception:
-            traffic = None
+            continue
     line = {
         "metric": METRIC, "value": round(us, 2), "unit": "µs", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 5),
         "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "u32",
         "data": "synthetic",
-        "config": {"workload": ("config3: 32 heads x 524288 tokens x 128-bit codes, k=10485"
-                                if world == 1 else
-                                f"config5: sequence-sharded {n_total} tokens x 32 heads x 128-bit, "
-                                f"k={k}, per-head histograms exchanged across ranks"),
-                   "heads": H, "tokens_per_gpu": n_local, "tokens_total": n_total, "code_bits": L,
-                   "k": k, "l2": "inputs (268 MB codes) larger than the 126 MB L2; no flush"},
+        "config": workload_config(world),
         "roofline": {"bound": "hbm",
                      "kernel": ("one retrieval = k3_fused (single launch)" if world == 1
                                 else shard_path),
                      "achieved": round(achieved, 1), "peak": hbm, "peak_kind": peak_kind,
                      "unit": "GB/s", "frac": round(achieved / hbm, 4),
                      "algorithmic_bytes": alg_bytes, "traffic": traffic,
+                     "traffic_source": traffic_src,
                      "scan_kernel_us": round(scan_ms * 1000, 2),
                      "scan_kernel_frac": round(scan_bytes / (scan_ms * 1e-3) / 1e9 / hbm, 4)},
         "timing": {"value_source": graph_note or "eager launches", "eager_us": round(eager_ms * 1000, 2)},
@@ -538,6 +604,14 @@ def main():
         "throughput": {"value": round(P * n_total / (us * 1e-6) / 1e9, 2),
                        "unit": "G (token, head) codes scanned per s"},
     }
+    if flushed_ms is not None:
+        fa = alg_bytes / (flushed_ms * 1e-3) / 1e9
+        line["value_l2_flushed"] = round(flushed_ms * 1000, 2)
+        line["roofline"]["frac_l2_flushed"] = round(fa / hbm, 4)
+    if sharded:
+        line["sharded_decode"] = sharded
+    if heads:
+        line["head_sharded_decode"] = heads
     if decode:
         line["sparse_decode"] = decode
     if prefill:
@@ -839,14 +913,35 @@ def bench_accuracy(torch, capi, ctx, dev, stream, args):
     o_ms = event_timer(torch, oracle, 5, stream)
     out = torch.zeros(Hh, dtype=torch.float64, device=dev)
     ctx.iou(hidx, hcnt, k, oidx, ocnt, k, Hh, out, stream)
+    # K2 fast-mode drift (BASELINE parity contract): the same retrieval from
+    # the tcgen05 encoder's codes (bf16 operands) of the same keys — IoU with
+    # the dense oracle, and with the exact (K1) hash top-k
+    codes2 = torch.empty_like(codes)
+    hs.encode_tc(keys, capi.SPL_F32, 1, n, codes2, None, stream)
+    t_idx = torch.zeros((Hh, k), dtype=torch.int32, device=dev)
+    t_cnt = torch.zeros(Hh, dtype=torch.int32, device=dev)
+    ctx.hamming_topk(codes2, n, L2, qc, Hh, nv, Hh, n, k, t_idx, t_cnt, stream)
+    out_tc = torch.zeros(Hh, dtype=torch.float64, device=dev)
+    ctx.iou(t_idx, t_cnt, k, oidx, ocnt, k, Hh, out_tc, stream)
+    out_x = torch.zeros(Hh, dtype=torch.float64, device=dev)
+    ctx.iou(t_idx, t_cnt, k, hidx, hcnt, k, Hh, out_x, stream)
     torch.cuda.synchronize()
+    diff_bits = int(np.unpackbits(torch.bitwise_xor(codes, codes2).cpu().numpy().view(np.uint8)).sum())
     ious = out.cpu().numpy()
-    del keys, codes
+    ious_tc, ious_x = out_tc.cpu().numpy(), out_x.cpu().numpy()
+    del keys, codes, codes2
     return {"workload": "config2 shape: 32 heads x 131072 f32 keys, d=128, 128-bit exact MLP codes, "
                         "k=2621; IoU(hash top-k, exact dense top-k) per head",
             "mean_iou": round(float(ious.mean()), 4), "min_iou": round(float(ious.min()), 4),
             "max_iou": round(float(ious.max()), 4),
             "oracle_topk_us": round(o_ms * 1000, 1),
+            "k2_fast_mode": {"mean_iou_vs_oracle": round(float(ious_tc.mean()), 4),
+                             "mean_iou_vs_exact_hash_topk": round(float(ious_x.mean()), 4),
+                             "min_iou_vs_exact_hash_topk": round(float(ious_x.min()), 4),
+                             "code_bits_differing_from_exact": diff_bits,
+                             "code_bits_total": int(Hh * n * L2),
+                             "note": "keys encoded by K2 (tcgen05, bf16 operands, fp32 accumulation) "
+                                     "instead of K1 (bit-exact); the query code is exact in both"},
             "data": "synthetic Gaussian keys/queries, random-init hasher (untrained baseline)"}
 
 
@@ -879,30 +974,231 @@ def bench_decode(torch, capi, ctx, dev, stream, args, hasher_c3):
     for _ in range(args.warmup):
         step()
     l0 = ctx.launches()
+    ctx.launch_log()
     eager_ms = event_timer(torch, step, args.steps, stream)
     launches = ctx.launches() - l0
+    kernels = ctx.launch_log()[: launches // args.steps]
     ctx.reserve(P, cap, L, k, D)
     # the step's working set (67 MB of codes + 43 MB of gathered K/V rows) fits
-    # the 126 MB L2, so replays are timed with L2 flushed before each one
+    # the 126 MB L2, so it is timed with L2 flushed before every step: the
+    # device time per step from CUDA graphs of steps x (flush, step) minus
+    # steps x flush, and (second number) the median of CUDA events around
+    # single graph replays, which also holds the replay's launch gap
     g_warm = graph_timer(torch, lambda st: step(st), args.steps, args.warmup)
+    fl = flushed_graph_timer(torch, lambda st: step(st), min(args.steps, 20), args.warmup)
     g_ms = graph_timer(torch, lambda st: step(st), args.steps, args.warmup, flush=True)
-    ms = g_ms if g_ms is not None else eager_ms
-    def att():
+    ms = fl[0] if fl else (g_ms if g_ms is not None else eager_ms)
+    def att():  # K4 alone over the same lists (the two-launch form of the step)
         ctx.sparse_attend(q, kc, vc, capi.SPL_BF16, cap, D, P, idx, k, cnt, nvalid, H, scale, out, stream)
     att_ms = flushed_timer(torch, att, args.steps, stream)
     hbm, _ = peaks()
     alg = P * n * W * 4 + P * (k + 1) * D * 2 * 2 + H * (D * D + D + D * L) * 4 + P * k * 4
     return {"workload": "config2: B=1, 32 heads, 131072-token bf16 K/V cache, 128-bit codes, k=2621",
             "us_per_step": round(ms * 1000, 2), "tok_per_s": round(B / (ms * 1e-3), 1),
-            "timing": ("CUDA graph replay of one decode step, L2 flushed before each (median)"
-                       if g_ms is not None else "eager"),
+            "timing": ("device time per step, L2 flushed before each: CUDA graphs of steps x "
+                       "(flush, step) minus steps x flush" if fl else "eager"),
+            "us_per_step_events": round(g_ms * 1000, 2) if g_ms is not None else None,
+            "us_per_step_events_note": "median of CUDA events around one graph replay each, L2 "
+                                       "flushed before each (includes the replay launch gap)",
             "us_per_step_l2_warm": round(g_warm * 1000, 2) if g_warm is not None else None,
             "eager_us_per_step": round(eager_ms * 1000, 2),
             "unit": "tok/s (one 32-head layer)", "gpu_launches_per_step": launches / args.steps,
-            "attend_us": round(att_ms * 1000, 2),
+            "kernels_per_step": kernels,
+            "k4_standalone_attend_us": round(att_ms * 1000, 2),
             "roofline": {"bound": "hbm", "algorithmic_bytes": alg,
                          "achieved": round(alg / (ms * 1e-3) / 1e9, 1), "peak": hbm,
                          "frac": round(alg / (ms * 1e-3) / 1e9 / hbm, 4)}}
+
+
+
+def bench_sharded_decode(torch, capi, ctx, dev, stream, args, world, rank, dist, same_gpu,
+                         all_reduce_dev):
+    """Config 5: one decode step of a 32-head layer over a sequence-sharded KV
+    cache — 512K tokens per GPU (weak scaling: N x 512K in total), 128-bit
+    codes, bf16 K/V, k = 2% of the whole cache — through
+    spl_sharded_decode_step on every rank: encode (the last rank appends the
+    new token), retrieval with the in-kernel histogram exchange, partial
+    attention, in-kernel exchange of the (m, l, o) partials, combine. At
+    N = 1 the same call runs with a 1-rank group (the point the scaling curve
+    starts from). tok/s = 1 / step (one sequence)."""
+    n = N_TOK
+    n_total = n * world
+    k = budget(n_total)
+    P = H
+    W = L // 32
+    rng = np.random.default_rng(50)
+    w1 = (rng.standard_normal((H, D, D)) / np.sqrt(D)).astype(np.float32)
+    b1 = np.zeros((H, D), np.float32)
+    w2 = (rng.standard_normal((H, D, L)) / np.sqrt(D)).astype(np.float32)
+    hs = ctx.hasher(w1, b1, w2)
+    codes = random_codes(torch, P, n, W, seed=500 + rank, dev=dev)
+    g = torch.Generator(device=dev)
+    g.manual_seed(600 + rank)
+    kc = torch.empty((1, H, n, D), device=dev, dtype=torch.bfloat16)
+    vc = torch.empty((1, H, n, D), device=dev, dtype=torch.bfloat16)
+    for h0 in range(0, H, 8):
+        kc[0, h0:h0 + 8].copy_(torch.randn((8, n, D), generator=g, device=dev))
+        vc[0, h0:h0 + 8].copy_(torch.randn((8, n, D), generator=g, device=dev))
+    gq = torch.Generator(device=dev)
+    gq.manual_seed(7)  # the step's inputs are the same on every rank
+    q = torch.randn((1, H, D), generator=gq, device=dev)
+    kn = torch.randn((1, H, D), generator=gq, device=dev)
+    vn = torch.randn((1, H, D), generator=gq, device=dev)
+    nvalid = torch.full((1,), n, dtype=torch.int32, device=dev)
+    idx = torch.zeros((P, k), dtype=torch.int32, device=dev)
+    cnt = torch.zeros(P, dtype=torch.int32, device=dev)
+    off = torch.zeros(P, dtype=torch.int32, device=dev)
+    out = torch.zeros((1, H, D), dtype=torch.float32, device=dev)
+    scale = float(1 / np.sqrt(D))
+    owner = rank == world - 1
+    peer = ctx.peer(world, rank, P, L)
+    if world == 1:
+        capi.Peer.connect_local(ctx, [peer])
+    else:
+        handles = [None] * world
+        dist.all_gather_object(handles, peer.ipc_handle())
+        peer.open(handles)
+    ctx.reserve(P, n, L, k, D)
+    # the step appends at n_valid - 1: keep the cache length fixed across the
+    # timed steps (each step rewrites the same slot), as a decode loop at a
+    # fixed context would
+
+    def step(st=None):
+        hs.sharded_decode_step(peer, q, kn, vn, 1, owner, codes, kc, vc, capi.SPL_BF16, n, nvalid, n,
+                               k, scale, idx, cnt, off, out, st if st is not None else stream)
+
+    def barrier():
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+
+    ctx.launch_log()
+    for _ in range(args.warmup):
+        step()
+    barrier()
+    ctx.check_device_error()
+    kernels = ctx.launch_log()
+    launches = len(kernels) / max(1, args.warmup)
+    steps = min(args.steps, 20)
+    barrier()
+    eager_ms = event_timer(torch, step, steps, stream)
+    barrier()
+    fl = flushed_graph_timer(torch, lambda st: step(st), steps, args.warmup) if not same_gpu else None
+    barrier()
+    ctx.check_device_error()
+    ms = fl[0] if fl else eager_ms
+    # e2e through the C-ABI with host buffers: H2D of the step's q / k_new /
+    # v_new, the sharded step, D2H of the attention output
+    qh, knh, vnh = (t.cpu().pin_memory() for t in (q, kn, vn))
+    outh = torch.empty_like(out, device="cpu").pin_memory()
+
+    def e2e_step():
+        q.copy_(qh, non_blocking=True)
+        kn.copy_(knh, non_blocking=True)
+        vn.copy_(vnh, non_blocking=True)
+        step()
+        outh.copy_(out, non_blocking=True)
+    for _ in range(3):
+        e2e_step()
+    barrier()
+    e2e_ms = event_timer(torch, e2e_step, steps, stream)
+    barrier()
+    t = torch.tensor([ms, eager_ms, e2e_ms], device=dev)
+    if dist:
+        all_reduce_dev(t, dist.ReduceOp.MAX)
+    ms, eager_ms, e2e_ms = (float(x) for x in t.tolist())
+    hbm, _ = peaks()
+    # algorithmic bytes per rank (SURVEY 8(d) config 5): codes + this rank's
+    # share of the gathered K/V rows (k/N on average) + weights + indices +
+    # the exchanged histograms and partials
+    alg = (P * n * W * 4 + P * (k // world + 1) * D * 2 * 2 + H * (D * D + D + D * L) * 4
+           + P * (k // world) * 4 + world * P * ((L + 2) + (D + 2)) * 8)
+    peer.close()
+    del kc, vc, codes
+    torch.cuda.empty_cache()
+    return {"workload": f"config5: one sequence, {n_total} tokens sequence-sharded over {world} GPU(s) "
+                        f"({n} per GPU), 32 heads, d=128, bf16 K/V, 128-bit codes, k={k}; encode + "
+                        "append (last rank) + retrieval + partial attention + combine",
+            "us_per_step": round(ms * 1000, 2), "tok_per_s": round(1.0 / (ms * 1e-3), 1),
+            "unit": "tok/s (one 32-head layer, one sequence; max over ranks)",
+            "timing": ("device time per step with L2 flushed before each, from CUDA graphs of "
+                       "steps x (flush, step) minus steps x flush" if fl else "eager launches"),
+            "eager_us_per_step": round(eager_ms * 1000, 2),
+            "e2e": {"value": round(1.0 / (e2e_ms * 1e-3), 1), "unit": "tok/s",
+                    "us_per_step": round(e2e_ms * 1000, 2),
+                    "h2d_bytes_per_step": 3 * H * D * 4, "d2h_bytes_per_step": H * D * 4,
+                    "path": "spl_sharded_decode_step with pinned host q / k_new / v_new in and the "
+                            "attention output out, every rank"},
+            "kernels_per_step": kernels[: int(launches)], "gpu_launches_per_step": launches,
+            "exchange": ("in-kernel over IPC-mapped peer memory (NVLink between GPUs): per-head "
+                         "score histograms, then the (m, l, o) attention partials"),
+            "roofline": {"bound": "hbm", "algorithmic_bytes_per_rank": alg,
+                         "achieved": round(alg / (ms * 1e-3) / 1e9, 1), "peak": hbm,
+                         "frac": round(alg / (ms * 1e-3) / 1e9 / hbm, 4)}}
+
+
+def bench_head_sharded(torch, capi, ctx, dev, stream, args, world, rank, dist, same_gpu,
+                       all_reduce_dev):
+    """Head sharding (SURVEY §8 e): the same config-5 cache split by heads
+    instead — every rank holds all N x 512K tokens of 32 / N heads (equal
+    bytes per rank to the sequence split) and runs the unsharded decode step
+    on them; heads are independent (one hasher per head), so there is no
+    exchange and the output stays head-sharded."""
+    if H % world:
+        return None
+    Hr = H // world
+    n = N_TOK * world
+    k = budget(n)
+    W = L // 32
+    rng = np.random.default_rng(51 + rank)
+    w1 = (rng.standard_normal((Hr, D, D)) / np.sqrt(D)).astype(np.float32)
+    b1 = np.zeros((Hr, D), np.float32)
+    w2 = (rng.standard_normal((Hr, D, L)) / np.sqrt(D)).astype(np.float32)
+    hs = ctx.hasher(w1, b1, w2)
+    codes = random_codes(torch, Hr, n, W, seed=700 + rank, dev=dev)
+    g = torch.Generator(device=dev)
+    g.manual_seed(800 + rank)
+    kc = torch.empty((1, Hr, n, D), device=dev, dtype=torch.bfloat16)
+    vc = torch.empty((1, Hr, n, D), device=dev, dtype=torch.bfloat16)
+    for h in range(Hr):
+        kc[0, h].copy_(torch.randn((n, D), generator=g, device=dev))
+        vc[0, h].copy_(torch.randn((n, D), generator=g, device=dev))
+    q = torch.randn((1, Hr, D), generator=g, device=dev)
+    kn = torch.randn((1, Hr, D), generator=g, device=dev)
+    vn = torch.randn((1, Hr, D), generator=g, device=dev)
+    nvalid = torch.full((1,), n, dtype=torch.int32, device=dev)
+    idx = torch.zeros((Hr, k), dtype=torch.int32, device=dev)
+    cnt = torch.zeros(Hr, dtype=torch.int32, device=dev)
+    out = torch.zeros((1, Hr, D), dtype=torch.float32, device=dev)
+    scale = float(1 / np.sqrt(D))
+    ctx.reserve(Hr, n, L, k, D)
+
+    def step(st=None):
+        hs.decode_step(q, kn, vn, 1, codes, kc, vc, capi.SPL_BF16, n, nvalid, n, k, scale, idx, cnt,
+                       out, st if st is not None else stream)
+    ctx.launch_log()
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    kernels = ctx.launch_log()
+    steps = min(args.steps, 20)
+    if dist:
+        dist.barrier()
+    fl = flushed_graph_timer(torch, lambda st: step(st), steps, args.warmup) if not same_gpu else None
+    ms = fl[0] if fl else event_timer(torch, step, steps, stream)
+    t = torch.tensor([ms], device=dev)
+    if dist:
+        all_reduce_dev(t, dist.ReduceOp.MAX)
+    ms = float(t.item())
+    del kc, vc, codes
+    torch.cuda.empty_cache()
+    return {"workload": f"config5 by heads: {n} tokens x {Hr} heads per GPU ({world} GPUs x {Hr} = 32 "
+                        f"heads), bf16 K/V, 128-bit codes, k={k}; no exchange",
+            "us_per_step": round(ms * 1000, 2), "tok_per_s": round(1.0 / (ms * 1e-3), 1),
+            "unit": "tok/s (one 32-head layer, one sequence; max over ranks)",
+            "timing": ("device time per step with L2 flushed before each (graph difference)" if fl
+                       else "eager launches"),
+            "kernels_per_step": kernels[: len(kernels) // max(1, args.warmup)]}
 
 
 if __name__ == "__main__":
