@@ -340,7 +340,12 @@ typedef struct spl_train_config {
  * many key rows (causally aligned). records: [num_iters][3] = {loss,
  * violation_rate, lr} (IterRecord, trainer.hpp:84-89). Per-row orders are
  * sorted in shared-memory chunks of 16384 keys, merged in global memory
- * beyond that. */
+ * beyond that.
+ * Limits the reference does not have (it streams each query): the sampled
+ * top + other keys per query must be <= 12800 (one block's shared memory),
+ * and the pair gradients (queries x top x other doubles) must fit in half
+ * the free device memory; beyond either, SPL_E_DIMENSION ("GPU trainer
+ * limit: ...") — set max_top / max_oth / query_subsample, as the CLI does. */
 typedef enum spl_train_loss {
     SPL_TRAIN_LOSS_RANKING = 0,        /* TrainLoss::ranking */
     SPL_TRAIN_LOSS_RECONSTRUCTION = 1  /* TrainLoss::reconstruction (MSE ablation) */

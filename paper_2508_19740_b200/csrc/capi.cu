@@ -92,7 +92,8 @@ spl_status spl_ctx_create(int device, spl_ctx** out) {
     c->device = device;
     c->num_sms = prop.multiProcessorCount;
     if (cudaMalloc(&c->dev_err, sizeof(uint32_t)) != cudaSuccess ||
-        cudaMemset(c->dev_err, 0, sizeof(uint32_t)) != cudaSuccess) {
+        cudaMemset(c->dev_err, 0, sizeof(uint32_t)) != cudaSuccess ||
+        cudaDeviceSynchronize() != cudaSuccess) {
         delete c;
         return SPL_E_CUDA;
     }
@@ -282,6 +283,9 @@ spl_status spl_peer_create(spl_ctx* ctx, uint32_t R, uint32_t rank, uint32_t P_m
     if (e == cudaSuccess) e = cudaMalloc(&pe->d_table, sizeof(uint32_t*) * R);
     if (e == cudaSuccess) e = cudaMalloc(&pe->d_epoch, sizeof(uint32_t));
     if (e == cudaSuccess) e = cudaMemset(pe->d_epoch, 0, sizeof(uint32_t));
+    // legacy-stream memsets are not ordered before non-blocking streams:
+    // complete them before any kernel can touch the exchange area
+    if (e == cudaSuccess) e = cudaDeviceSynchronize();
     if (e != cudaSuccess) {
         cudaFree(pe->buf);
         delete pe;

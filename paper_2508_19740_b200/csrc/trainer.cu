@@ -1475,9 +1475,26 @@ spl_status train_impl(spl_ctx* ctx, int kind, uint32_t d, uint32_t h, uint32_t L
     if (dk_staged)
         SPL_CUDA_TRY(ctx, cudaFuncSetAttribute(k_dsoft_keys, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dk_smem(maxQ)));
     const size_t grad_smem = (size_t)(maxT + maxO) * 16;
+    // Limits of the GPU trainer (the reference streams each query and has
+    // none): the top + other keys of one draw are staged in one block's shared
+    // memory, and the pair gradients are materialised as maxQ x maxT x maxO
+    // doubles. Both are stated here rather than failing inside an allocation.
     if (grad_smem > 200 * 1024)
-        return fail(ctx, SPL_E_DIMENSION, "train_hasher: sampled pair set too large for one block "
-                                          "(set max_top / max_oth)");
+        return fail(ctx, SPL_E_DIMENSION,
+                    "train_hasher: GPU trainer limit: max_top + max_oth = " +
+                        std::to_string(maxT + maxO) +
+                        " sampled keys per query exceed one block's shared memory (<= 12800); "
+                        "set RankingLossConfig max_top / max_oth");
+    {
+        size_t free_b = 0, total_b = 0;
+        const size_t gpair_b = (size_t)maxQ * maxT * maxO * sizeof(double);
+        if (cudaMemGetInfo(&free_b, &total_b) == cudaSuccess && gpair_b > free_b / 2)
+            return fail(ctx, SPL_E_DIMENSION,
+                        "train_hasher: GPU trainer limit: the pair-gradient buffer (queries x top x "
+                        "other = " + std::to_string(gpair_b >> 20) +
+                            " MiB of doubles) exceeds half the free device memory; set "
+                            "query_subsample / max_top / max_oth");
+    }
     SPL_CUDA_TRY(ctx, cudaFuncSetAttribute(k_rank_grad, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)grad_smem));
     const uint64_t pair_blocks = std::max<uint64_t>(
         ((uint64_t)maxT * maxO + kPairThreads * kPairsPerThread - 1) / (kPairThreads * kPairsPerThread),
