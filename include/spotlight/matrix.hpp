@@ -54,6 +54,20 @@ private:
     std::vector<T> v_;
 };
 
+/// Sequential dot product and Euclidean norm (matrix.hpp:145-155): scalar
+/// host helpers callers use on rows of a Matrix.
+template <typename T>
+T dot(std::span<const T> a, std::span<const T> b) {
+    T acc = T(0);
+    for (std::size_t i = 0; i < a.size(); ++i) acc += a[i] * b[i];
+    return acc;
+}
+
+template <typename T>
+T norm2(std::span<const T> a) {
+    return std::sqrt(dot(a, a));
+}
+
 template <typename To, typename From>
 Matrix<To> matrix_cast(const Matrix<From>& m) {
     std::vector<To> v(m.values().begin(), m.values().end());

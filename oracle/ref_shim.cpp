@@ -24,6 +24,7 @@
 #include "spotlight/bitcodes.hpp"
 #include "spotlight/errors.hpp"
 #include "spotlight/hashers.hpp"
+#include "spotlight/linalg.hpp"
 #include "spotlight/rng.hpp"
 #include "spotlight/ranking_loss.hpp"
 #include "spotlight/trainer.hpp"
@@ -119,6 +120,85 @@ int spotref_qr_rotation_init(std::uint32_t d, std::uint64_t seed, float* proj) {
     return guard([&] {
         const LinearHasher l = qr_rotation_init(d, seed);
         std::memcpy(proj, l.projection.data(), sizeof(float) * l.projection.size());
+    });
+}
+
+// downproj_init (hashers.cpp:65-74) -> d x r projection.
+int spotref_downproj_init(std::uint32_t d, std::uint32_t r, std::uint64_t seed, float* proj) {
+    return guard([&] {
+        const DownProjEstimator e = downproj_init(d, r, seed);
+        std::memcpy(proj, e.projection.data(), sizeof(float) * e.projection.size());
+    });
+}
+
+// random_rotation (linalg.cpp:80-92), f64 d x d.
+int spotref_random_rotation(std::uint32_t d, std::uint64_t seed, double* q) {
+    return guard([&] {
+        const Matrix<double> m = random_rotation(d, seed);
+        std::memcpy(q, m.data(), sizeof(double) * m.size());
+    });
+}
+
+// write_hasher (hashers.cpp:184-215): kind 0 linear (w1 = d x L projection),
+// 1 mlp (w1 d x h, b1 h, w2 h x L, gamma), 2 downproj (w1 = d x L).
+int spotref_write_hasher(const char* path, int kind, std::uint32_t d, std::uint32_t h,
+                         std::uint32_t L, float gamma, const float* w1, const float* b1,
+                         const float* w2) {
+    return guard([&] {
+        if (kind == 1) {
+            MlpHasher m = make_mlp(w1, b1, w2, d, h, L);
+            m.gamma = gamma;
+            write_hasher(path, AnyHasher{m});
+        } else if (kind == 0) {
+            write_hasher(path, AnyHasher{LinearHasher{mat(w1, d, L)}});
+        } else {
+            write_hasher(path, AnyHasher{DownProjEstimator{mat(w1, d, L)}});
+        }
+    });
+}
+
+// read_hasher (hashers.cpp:217-246): dims[4] = {kind, d, h, L}; the
+// parameter buffers (may be null on a first call that only asks for dims)
+// are filled when non-null.
+int spotref_read_hasher(const char* path, std::uint32_t* dims, float* gamma, float* w1, float* b1,
+                        float* w2) {
+    return guard([&] {
+        const AnyHasher a = read_hasher(path);
+        if (const auto* m = std::get_if<MlpHasher>(&a)) {
+            dims[0] = 1;
+            dims[1] = m->input_dim();
+            dims[2] = m->hidden_dim();
+            dims[3] = m->code_bits();
+            *gamma = m->gamma;
+            if (w1) std::memcpy(w1, m->w1.data(), sizeof(float) * m->w1.size());
+            if (b1) std::memcpy(b1, m->b1.data(), sizeof(float) * m->b1.size());
+            if (w2) std::memcpy(w2, m->w2.data(), sizeof(float) * m->w2.size());
+        } else {
+            const Matrix<float>& p = std::holds_alternative<LinearHasher>(a)
+                                         ? std::get<LinearHasher>(a).projection
+                                         : std::get<DownProjEstimator>(a).projection;
+            dims[0] = std::holds_alternative<LinearHasher>(a) ? 0 : 2;
+            dims[1] = (std::uint32_t)p.rows();
+            dims[2] = 0;
+            dims[3] = (std::uint32_t)p.cols();
+            *gamma = 0.0f;
+            if (w1) std::memcpy(w1, p.data(), sizeof(float) * p.size());
+        }
+    });
+}
+
+// write_code_index / read_code_index (bitcodes.cpp:138-160), SPLC.
+int spotref_write_code_index(const char* path, const std::uint32_t* words, std::uint32_t n,
+                             std::uint32_t L) {
+    return guard([&] { write_code_index(path, codes_from(words, n, L)); });
+}
+int spotref_read_code_index(const char* path, std::uint32_t* n, std::uint32_t* L,
+                            std::uint32_t* words) {
+    return guard([&] {
+        const CodeMatrix c = read_code_index(path);
+        *n = c.rows();
+        *L = c.length_bits();
+        if (words) std::memcpy(words, c.raw().data(), sizeof(std::uint32_t) * c.raw().size());
     });
 }
 

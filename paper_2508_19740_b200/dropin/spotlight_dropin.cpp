@@ -177,10 +177,12 @@ public:
     }
     std::uint32_t u32(const char* field) {
         unsigned char b[4];
-        const auto at = static_cast<long long>(is_.tellg());
+        // the offset is the stream position after the failed read, as the
+        // reference reports it (binary_io.hpp:36-41): tellg() of a failed
+        // stream, i.e. -1
         if (!is_.read(reinterpret_cast<char*>(b), 4))
             throw FormatError(path_ + ": truncated while reading " + field + " at offset " +
-                              std::to_string(at));
+                              std::to_string(static_cast<long long>(is_.tellg())));
         return b[0] | (b[1] << 8) | (b[2] << 16) | (static_cast<std::uint32_t>(b[3]) << 24);
     }
     std::uint8_t u8(const char* field) {

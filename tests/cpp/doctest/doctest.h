@@ -121,9 +121,9 @@ inline State& state() {
 }
 
 inline void report_failure(const char* kind, const char* expr, const char* file, int line,
-                           const std::string& extra = "") {
+                           const std::string& extra = "", bool assertion = true) {
     State& s = state();
-    ++s.failed_assertions;
+    if (assertion) ++s.failed_assertions;
     s.case_failed = true;
     std::string where;
     for (const auto& p : s.path) where += " / " + p;
@@ -237,9 +237,9 @@ inline int run_all(int argc, char** argv) {
             } catch (const RequireAbort&) {
             } catch (const std::exception& e) {
                 report_failure("TEST_CASE", tc.name, tc.file, tc.line,
-                               std::string("threw exception: ") + e.what());
+                               std::string("threw exception: ") + e.what(), false);
             } catch (...) {
-                report_failure("TEST_CASE", tc.name, tc.file, tc.line, "threw unknown exception");
+                report_failure("TEST_CASE", tc.name, tc.file, tc.line, "threw unknown exception", false);
             }
             if (!s.pending[0] || run > 100000) break;
         }
