@@ -115,6 +115,9 @@ struct K3Params {
     int att_pf;            // 1: the select also prefetches the emitted rows into L2
                            // (SPL_ATT_PF=1; measured no faster than without: the
                            // gather is DRAM-bound either way)
+    int att_pre;           // fused attention: each warp prefetches all its K / V rows
+                           // into L2 before its batches (SPL_ATT_PRE=1; measured no
+                           // faster: the prefetches are hints, many are dropped)
 };
 
 constexpr int kThreads = 256;
@@ -681,34 +684,82 @@ __device__ void select_rows(const ScoreT* sc, uint64_t a0, uint64_t r0, uint64_t
 // Fused-path select over u8 scores in the transposed layout (tpos), L <= 128
 // so every score is <= 128: with c = (128 - t) * 0x01010101, byte x >= t
 // iff bit 7 of byte (x + c) is set, and x + c never carries into the next
-// byte. Per 4 rows: ge, gt (2 x IADD + LOP), eq = ge & ~gt, then the shifted
-// OR that turns the 0x80 flags of words 0..3 into one bit per row, in row
-// order (bit 8b + i <-> row 4b + i). Same contract as select_rows.
+// byte. Flags per word: (w + c) >> (7 - i) masked with 0x01010101 << i and
+// OR-ed (IADD, SHF, LOP3), so bit 8b + i of a vector's mask is row 4b + i
+// (row order = bit order). Same contract as select_rows.
 // Each thread owns NV consecutive 16-row vectors per round; NV odd makes the
 // per-lane stride (16 * NV bytes) hit 8 distinct 16-byte bank groups across
 // any 8 lanes, so every LDS.128 is conflict-free (4 wavefronts). NV = 11
-// covers the headline segment (40448 rows) in one round (one block scan).
-// Offsets are 32-bit, relative to a0. Flags: per word (w + c) >> (7 - i)
-// masked with 0x01010101 << i and OR-ed (IADD, SHF, LOP3), so bit 8b + i of
-// a vector's mask is row 4b + i.
-// scratch: kThreads x NV words of shared memory (the private counters,
-// free once the stream is over). NV = 3 for short segments (<= 12 K rows,
-// e.g. the config-2 decode shape): the per-thread work is unrolled over NV
-// vectors whether they hold rows or not.
+// covers the headline segment (40448 rows) in one round (one block scan);
+// NV = 3 short segments (<= 12 K rows, the config-2 decode shape).
+// The select is issue-bound (all CTAs of an SM select at once), so the
+// per-vector work is kept to ~30 instructions: the stream zeroes the rows of
+// the first / last vector outside [r0, r1), and a zero byte never reaches a
+// threshold T >= 1, so only EDGE (T == 0: every row qualifies) masks them;
+// the tie quota is resolved per thread (keep all / none), and only the one
+// thread whose ties straddle `take` trims a vector; ids are emitted straight
+// from the per-vector masks in registers.
+// Output: when the CTA's `count` ids fit the shared-memory stage (stage_cap
+// entries), they are compacted there and written to out[0..count) with
+// coalesced stores at the end (the scattered 4-byte stores of the emission
+// loop cost more than the compaction itself); the decode step's attention
+// then reads them from the stage. Otherwise they go straight to out.
 // PF (decode step): prefetch each emitted row's K and V lines into L2 (when
-// pfk is set); ids (optional, shared memory): a copy of the first n_ids
-// emitted ids for the attention that follows in the same kernel.
-template <int NV, bool PF = false>
+// pfk is set).
+__device__ __forceinline__ uint32_t keep_lowest_bits(uint32_t e, uint32_t n) {
+    uint32_t r = 0;
+    for (uint32_t c = 0; c < n; ++c) {
+        r |= e & (0u - e);
+        e &= e - 1;
+    }
+    return r;
+}
+
+// Per-vector flags: gt = rows with score > T, ge = rows with score >= T (one
+// bit per row, bit 8b + i <-> row 4b + i). EDGE (T == 0): every row inside
+// [lo, hi) is >= T and nothing outside.
+template <bool EDGE>
+__device__ __forceinline__ void t8_flags(const uint8_t* sc, uint32_t at, uint32_t lo, uint32_t hi,
+                                         uint32_t c_gt, uint32_t c_ge, uint32_t m_gt, uint32_t& g,
+                                         uint32_t& ge) {
+    uint4 x = make_uint4(0, 0, 0, 0);
+    if (at < hi) x = *reinterpret_cast<const uint4*>(sc + at);
+    const uint32_t w[4] = {x.x, x.y, x.z, x.w};
+    g = 0;
+    ge = 0;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        g |= ((w[i] + c_gt) >> (7 - i)) & (0x01010101u << i);
+        if constexpr (!EDGE) ge |= ((w[i] + c_ge) >> (7 - i)) & (0x01010101u << i);
+    }
+    g &= m_gt;
+    if constexpr (EDGE) {
+        uint32_t valid = 0;
+        if (at < hi) {
+            valid = 0x0F0F0F0Fu;
+            if (at < lo || at + 16 > hi)
+                for (uint32_t j = 0; j < 16; ++j)
+                    if (at + j < lo || at + j >= hi) valid &= ~(1u << (8 * (j >> 2) + (j & 3)));
+        }
+        ge = valid;
+        g &= valid;
+    }
+}
+
+// Rolled loops (the select runs once per CTA per launch, so its instructions
+// come cold from L2: ncu showed it stalled on instruction fetch, not on
+// arithmetic), two passes over the scores (count, then emit), both ~40
+// instructions of loop body.
+template <int NV, bool PF = false, bool EDGE = false>
 __device__ void select_rows_t8(const uint8_t* sc, uint64_t a0, uint64_t r0, uint64_t r1,
                                uint32_t T, uint32_t take, uint32_t* out, uint64_t* s_warp,
-                               uint32_t* scratch, uint64_t* tr = nullptr,
-                               const char* pfk = nullptr, const char* pfv = nullptr,
-                               uint32_t pfb = 0, uint32_t* ids = nullptr, uint32_t n_ids = 0) {
+                               uint64_t* tr, const char* pfk, const char* pfv, uint32_t pfb,
+                               uint32_t* stage, uint32_t stage_cap, uint32_t count,
+                               uint32_t* masks) {
     constexpr int CH = 16 * NV;  // rows per thread per round
-    // T == 0: every row is >= T (x + 128 would carry for x = 128);
-    // T >= 128: no row is > T
-    const uint32_t c_ge = T >= 1 ? (128u - T) * 0x01010101u : 0u;
-    const uint32_t all_ge = T == 0 ? 0x0F0F0F0Fu : 0u;
+    const bool staged = stage != nullptr && count <= stage_cap;  // uniform
+    // T >= 128: no row is > T (c_gt masked off); EDGE is the T == 0 case
+    const uint32_t c_ge = EDGE ? 0u : (128u - T) * 0x01010101u;
     const uint32_t c_gt = T < 128 ? (127u - T) * 0x01010101u : 0u;
     const uint32_t m_gt = T < 128 ? 0x0F0F0F0Fu : 0u;
     const uint32_t lo = (uint32_t)(r0 - a0), hi = (uint32_t)(r1 - a0);  // rows [lo, hi)
@@ -718,90 +769,66 @@ __device__ void select_rows_t8(const uint8_t* sc, uint64_t a0, uint64_t r0, uint
     uint32_t carry_gt = 0, carry_eq = 0;
     for (uint32_t base = 0; base < hi; base += round_rows) {
         const uint32_t my = base + (uint32_t)tid * CH;
-        uint32_t gm[NV], em[NV];
-        uint32_t gt = 0, eq = 0;
+        uint32_t gt = 0, eq = 0, nzv = 0;  // nzv: vectors holding candidate rows
 #pragma unroll
         for (int v = 0; v < NV; ++v) {
-            const uint32_t at = my + 16u * v;
-            uint32_t g = 0, ge = 0;
-            if (at < hi) {
-                const uint4 x = *reinterpret_cast<const uint4*>(sc + at);
-                const uint32_t w[4] = {x.x, x.y, x.z, x.w};
-#pragma unroll
-                for (int i = 0; i < 4; ++i) {
-                    g |= ((w[i] + c_gt) >> (7 - i)) & (0x01010101u << i);
-                    ge |= ((w[i] + c_ge) >> (7 - i)) & (0x01010101u << i);
-                }
-                g &= m_gt;
-                ge |= all_ge;
-                if (at < lo || at + 16 > hi) {  // edge vector: rows outside [lo, hi)
-                    uint32_t valid = 0;
-                    for (uint32_t j = 0; j < 16; ++j)
-                        if (at + j >= lo && at + j < hi) valid |= 1u << (8 * (j >> 2) + (j & 3));
-                    g &= valid;
-                    ge &= valid;
-                }
-            }
-            gm[v] = g;
-            em[v] = ge & ~g;
-            gt += __popc(gm[v]);
-            eq += __popc(em[v]);
+            uint32_t g, ge;
+            t8_flags<EDGE>(sc, my + 16u * v, lo, hi, c_gt, c_ge, m_gt, g, ge);
+            gt += __popc(g);
+            eq += __popc(ge & ~g);
+            nzv |= (ge != 0u ? 1u : 0u) << v;
+            // both masks use bits 8b + i (i < 4): pack > T in the low, == T in the high nibbles
+            if (ge) masks[(uint32_t)tid * NV + v] = g | ((ge & ~g) << 4);
         }
         if (tr && threadIdx.x == 0) { tr[9] = gtimer(); tr[13] = clock64(); }
         uint64_t tot;
         const uint64_t ex = block_excl_scan_u64(((uint64_t)eq << 32) | gt, s_warp, tot);
         if (tr && threadIdx.x == 0) { tr[10] = gtimer(); tr[14] = clock64(); }
         if (gt | eq) {
-            uint32_t eb = carry_eq + (uint32_t)(ex >> 32);  // ties before this thread's rows
+            const uint32_t eb = carry_eq + (uint32_t)(ex >> 32);  // ties before this thread's rows
             uint32_t pos = carry_gt + (uint32_t)ex + (eb < take ? eb : take);
-            // final per-vector masks (ties trimmed where the quota runs out)
-            // go to this thread's scratch row; one flat loop then walks the
-            // set bits of the non-empty vectors only — small code (the
-            // unrolled per-vector loops missed the instruction cache) and
-            // fewer divergent iterations per warp
-            uint32_t nz = 0;
-#pragma unroll
-            for (int v = 0; v < NV; ++v) {
-                uint32_t e = em[v];
-                const uint32_t ne = __popc(e);
-                if (eb >= take) {
-                    e = 0;
-                } else if (eb + ne > take) {
-                    for (uint32_t drop = eb + ne - take; drop; --drop) e &= ~(0x80000000u >> __clz(e));
-                }
-                eb += ne;
-                const uint32_t m = gm[v] | e;
-                scratch[(uint32_t)tid * NV + v] = m;
-                nz |= (m != 0u ? 1u : 0u) << v;
-            }
+            // ties this thread keeps: all (~0), none (0), or the first `left`
+            uint32_t left = eb >= take ? 0u : (eb + eq <= take ? 0xFFFFFFFFu : take - eb);
             const uint32_t rowb = rb + my;
-            uint32_t v = 0, m = 0;
-            while (nz | m) {
-                if (m == 0u) {
-                    v = __ffs(nz) - 1;
-                    nz &= nz - 1;
-                    m = scratch[(uint32_t)tid * NV + v];
+            while (nzv) {  // only the vectors with candidates, in row order
+                const int v = __ffs(nzv) - 1;
+                nzv &= nzv - 1;
+                const uint32_t pk = masks[(uint32_t)tid * NV + v];
+                const uint32_t g = pk & 0x0F0F0F0Fu;
+                uint32_t e = left == 0u ? 0u : (pk >> 4) & 0x0F0F0F0Fu;
+                if (left - 1u < 0xFFFFFFFEu) {  // the straddling thread
+                    const uint32_t ne = __popc(e);
+                    if (left < ne) e = keep_lowest_bits(e, left);
+                    left -= left < ne ? left : ne;
                 }
-                const uint32_t bb = __ffs(m) - 1;
-                m &= m - 1;
-                const uint32_t id = rowb + 16u * v + 4 * (bb >> 3) + (bb & 7);
-                if constexpr (PF) {
-                    if (pos < n_ids) ids[pos] = id;
-                }
-                out[pos++] = id;
-                if constexpr (PF) {  // warm L2 for the attention gather (decode step)
-                    if (!pfk) continue;
-                    const char* kr = pfk + (uint64_t)id * pfb;
-                    const char* vr = pfv + (uint64_t)id * pfb;
-                    for (uint32_t b = 0; b < pfb; b += 128) {
-                        asm volatile("prefetch.global.L2 [%0];" ::"l"(kr + b));
-                        asm volatile("prefetch.global.L2 [%0];" ::"l"(vr + b));
+                uint32_t m = g | e;
+                while (m) {
+                    const uint32_t bb = __ffs(m) - 1;
+                    m &= m - 1;
+                    const uint32_t id = rowb + 16u * v + 4 * (bb >> 3) + (bb & 7);
+                    if (staged)
+                        stage[pos] = id;
+                    else
+                        out[pos] = id;
+                    ++pos;
+                    if constexpr (PF) {  // warm L2 for the attention gather (decode step)
+                        if (!pfk) continue;
+                        const char* kr = pfk + (uint64_t)id * pfb;
+                        const char* vr = pfv + (uint64_t)id * pfb;
+                        for (uint32_t b = 0; b < pfb; b += 128) {
+                            asm volatile("prefetch.global.L2 [%0];" ::"l"(kr + b));
+                            asm volatile("prefetch.global.L2 [%0];" ::"l"(vr + b));
+                        }
                     }
                 }
             }
         }
         carry_gt += (uint32_t)tot;
         carry_eq += (uint32_t)(tot >> 32);
+    }
+    if (staged) {
+        __syncthreads();
+        for (uint32_t i = tid; i < count; i += kThreads) out[i] = stage[i];
     }
     if (tr && threadIdx.x == 0) { tr[11] = gtimer(); tr[15] = clock64(); }
 }
@@ -1152,15 +1179,12 @@ __global__ void k5_peer_combine(K3Params prm, const float* partials, uint32_t D,
 
 // ------------------------------------------------------------ fused attend
 // Shared-memory layout of the private-counter region once the stream is over
-// (decode step, k3_fused<.., ATT>): [select masks: NV x kThreads words]
-// [attention merge / combine scratch: kAttScratch floats] [emitted ids].
-// The select copies the first att_ids_cap ids it emits there, so the
-// attention that follows does not read them back from L2.
+// (decode step, k3_fused<.., ATT>): [attention merge / combine scratch:
+// kAttScratch floats] [emitted ids]. The select compacts the CTA's ids there
+// when they fit (att_ids_cap), so the attention that follows does not read
+// them back from L2.
 constexpr uint32_t kAttScratchWords = 2 * 8 + 8 * 128;  // warp merge (the combine needs less)
-__device__ __forceinline__ uint32_t att_ids_off_words(uint32_t nv_sel) {
-    const uint32_t masks = nv_sel * kThreads;
-    return masks > kAttScratchWords ? masks : kAttScratchWords;
-}
+__device__ __forceinline__ uint32_t att_ids_off_words(uint32_t) { return kAttScratchWords; }
 template <bool ATT>
 __device__ __forceinline__ uint32_t* att_ids(uint8_t* priv, size_t priv_bytes, uint32_t nv_sel) {
     if constexpr (!ATT) return nullptr;
@@ -1169,7 +1193,8 @@ __device__ __forceinline__ uint32_t* att_ids(uint8_t* priv, size_t priv_bytes, u
 template <bool ATT>
 __device__ __forceinline__ uint32_t att_ids_cap(size_t priv_bytes, uint32_t nv_sel) {
     if constexpr (!ATT) return 0;
-    const size_t words = priv_bytes / 4, off = att_ids_off_words(nv_sel);
+    // the select's packed masks (nv_sel x kThreads words) sit at the end
+    const size_t words = priv_bytes / 4 - (size_t)nv_sel * kThreads, off = att_ids_off_words(nv_sel);
     return words > off ? (uint32_t)(words - off) : 0u;
 }
 
@@ -1214,6 +1239,21 @@ __device__ void fused_attend(const K3Params& prm, uint32_t p, uint32_t seg, uint
     float m = -INFINITY, lsum = 0.0f, o[E];
 #pragma unroll
     for (int e = 0; e < E; ++e) o[e] = 0.0f;
+    if (prm.att_pre && j0 < j1) {
+        // ask L2 for every K and V row of this warp's entries first (one DRAM
+        // round trip for all of them), so the 8-row batches below hit L2
+        constexpr uint32_t kRowBytes = D * sizeof(KV);
+        for (uint32_t j = j0 + lane; j < j1; j += 32) {
+            const uint32_t id = j < count ? (smem_ids ? sids[j] : __ldcg(gids + j)) : extra;
+            const char* kr = reinterpret_cast<const char*>(kbase + (uint64_t)id * D);
+            const char* vr = reinterpret_cast<const char*>(vbase + (uint64_t)id * D);
+#pragma unroll
+            for (uint32_t b = 0; b < kRowBytes; b += 128) {
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(kr + b));
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(vr + b));
+            }
+        }
+    }
     if (j0 < j1) {
         if (smem_ids)
             warp_attend<E, KV, true>(kbase, vbase, sids, count, extra, j0, j1, qv, m, lsum, o);
@@ -1380,6 +1420,7 @@ __global__ void __launch_bounds__(kThreads, 3) k3_fused(K3Params prm) {
     for (uint32_t i = tid; i < priv_bytes / 16; i += kThreads)
         reinterpret_cast<uint4*>(priv)[i] = make_uint4(0, 0, 0, 0);
     pdl_wait();  // query codes / appended code rows come from the previous kernel
+    K3_STAMP(2);
     // SHARD: this call's epoch = the group's device-side counter + 1 (the
     // last CTA stores it back), so CUDA-graph replays advance it too
     uint32_t epoch = 0;
@@ -1446,7 +1487,6 @@ __global__ void __launch_bounds__(kThreads, 3) k3_fused(K3Params prm) {
         }
     }
     K3_STAMP(1);
-    K3_STAMP(2);
 
     // ---------------- plan + select from shared memory
     region_off = 0;
@@ -1568,16 +1608,29 @@ __global__ void __launch_bounds__(kThreads, 3) k3_fused(K3Params prm) {
                 const bool pf_emit = prm.pf_k && (!ATT || prm.att_pf == 1);
                 const char* pfk = pf_emit ? prm.pf_k + pf_off : nullptr;
                 const char* pfv = pf_emit ? prm.pf_v + pf_off : nullptr;
-                if (r1 - a0 <= (uint64_t)kThreads * 16 * 3)  // uniform
-                    select_rows_t8<3, PF>(reinterpret_cast<const uint8_t*>(sc), a0, r0, r1, T, take, o,
-                                          s_warp, reinterpret_cast<uint32_t*>(priv), trp, pfk, pfv,
-                                          prm.pf_row_bytes, att_ids<ATT>(priv, priv_bytes, 3),
-                                          att_ids_cap<ATT>(priv_bytes, 3));
-                else
-                    select_rows_t8<11, PF>(reinterpret_cast<const uint8_t*>(sc), a0, r0, r1, T, take, o,
-                                           s_warp, reinterpret_cast<uint32_t*>(priv), trp, pfk, pfv,
-                                           prm.pf_row_bytes, att_ids<ATT>(priv, priv_bytes, 11),
-                                           att_ids_cap<ATT>(priv_bytes, 11));
+                const uint8_t* sc8 = reinterpret_cast<const uint8_t*>(sc);
+                const uint32_t pfb = prm.pf_row_bytes;
+                const bool nv3 = r1 - a0 <= (uint64_t)kThreads * 16 * 3;  // uniform
+                // stage for the emitted ids: the decode step's id region (its
+                // attention reads them there), else the whole free counter region
+                uint32_t* stg = ATT ? att_ids<ATT>(priv, priv_bytes, nv3 ? 3 : 11) : nullptr;
+                // per-thread packed candidate masks (kThreads x NV words) behind
+                // the stage in the free counter region
+                const uint32_t nvw = (nv3 ? 3u : 11u) * kThreads;
+                uint32_t* msk = reinterpret_cast<uint32_t*>(priv) + (priv_bytes / 4 - nvw);
+                const uint32_t cap = ATT ? att_ids_cap<ATT>(priv_bytes, nv3 ? 3 : 11)
+                                         : (uint32_t)(priv_bytes / 4 - nvw);
+                if (nv3) {
+                    if (T == 0)
+                        select_rows_t8<3, PF, true>(sc8, a0, r0, r1, T, take, o, s_warp, trp, pfk, pfv, pfb, stg, cap, my_count, msk);
+                    else
+                        select_rows_t8<3, PF, false>(sc8, a0, r0, r1, T, take, o, s_warp, trp, pfk, pfv, pfb, stg, cap, my_count, msk);
+                } else {
+                    if (T == 0)
+                        select_rows_t8<11, PF, true>(sc8, a0, r0, r1, T, take, o, s_warp, trp, pfk, pfv, pfb, stg, cap, my_count, msk);
+                    else
+                        select_rows_t8<11, PF, false>(sc8, a0, r0, r1, T, take, o, s_warp, trp, pfk, pfv, pfb, stg, cap, my_count, msk);
+                }
             }
             else
                 select_rows<ScoreT, false>(sc, a0, r0, r1, T, take,
@@ -2049,21 +2102,23 @@ K3Params base_params(spl_ctx* ctx, const K3Plan& pl, const K3Ws& ws, const K3Sta
 void k3_trace_report(uint64_t* dtrace, uint32_t G, uint64_t S, cudaStream_t s) {
     const char* tr = getenv("SPL_K3_TRACE");
     {
-                // stamps per CTA (16 slots): 0 start, 1 stream end, 2 (= 1), 3 T known,
-                // 4 prefix, 5 end, 6 smid, 7 attention start (decode step), 8 own
-                // record read, 9 select counts, 10 select scan, 11 select emitted
+                // stamps per CTA (16 slots): 0 start, 1 stream end, 2 past
+                // griddepcontrol.wait, 3 T known, 4 prefix, 5 end, 6 smid, 7 attention
+                // start (decode step), 8 own record read, 9 select counts, 10 select
+                // scan, 11 select emitted
                 constexpr int kSlots = 16;
-                const int cols[] = {0, 1, 3, 4, 8, 9, 10, 11, 7, 5};
-                const char* names = "start stream thresh prefix rec counts scan emit attend end";
+                constexpr int kCols = 11;
+                const int cols[kCols] = {0, 2, 1, 3, 4, 8, 9, 10, 11, 7, 5};
+                const char* names = "start waited stream thresh prefix rec counts scan emit attend end";
                 std::vector<uint64_t> h((size_t)G * kSlots);
                 cudaStreamSynchronize(s);
                 cudaMemcpy(h.data(), dtrace, h.size() * 8, cudaMemcpyDeviceToHost);
                 cudaFree(dtrace);
                 uint64_t t0 = ~0ull;
                 for (uint32_t i = 0; i < G; ++i) t0 = std::min(t0, h[i * kSlots]);
-                double mx[10] = {0}, mean[10] = {0};
+                double mx[kCols] = {0}, mean[kCols] = {0};
                 for (uint32_t i = 0; i < G; ++i)
-                    for (int j = 0; j < 10; ++j) {
+                    for (int j = 0; j < kCols; ++j) {
                         const uint64_t raw = h[i * kSlots + cols[j]];
                         const double v = raw ? (double)(raw - t0) / 1000.0 : 0.0;
                         mx[j] = std::max(mx[j], v);
@@ -2071,9 +2126,9 @@ void k3_trace_report(uint64_t* dtrace, uint32_t G, uint64_t S, cudaStream_t s) {
                     }
                 fprintf(stderr, "k3_fused trace G=%u S=%llu [%s] mean:", G,
                         (unsigned long long)S, names);
-                for (int j = 0; j < 10; ++j) fprintf(stderr, " %.1f", mean[j]);
+                for (int j = 0; j < kCols; ++j) fprintf(stderr, " %.1f", mean[j]);
                 fprintf(stderr, "  max:");
-                for (int j = 0; j < 10; ++j) fprintf(stderr, " %.1f", mx[j]);
+                for (int j = 0; j < kCols; ++j) fprintf(stderr, " %.1f", mx[j]);
                 fprintf(stderr, " us");
                 double cyc[3] = {0, 0, 0};
                 for (uint32_t i = 0; i < G; ++i)
@@ -2082,12 +2137,14 @@ void k3_trace_report(uint64_t* dtrace, uint32_t G, uint64_t S, cudaStream_t s) {
                 fprintf(stderr, "  select thread-0 cycles: counts %.0f scan %.0f emit %.0f\n", cyc[0], cyc[1],
                         cyc[2]);
                 if (*tr == '2') {  // per-CTA dump: cta, smid, stamps (us)
-                    FILE* f = fopen("gpurun_out/k3_trace.csv", "w");
+                    const char* path = getenv("SPL_K3_TRACE_CSV");
+                    FILE* f = fopen(path && *path ? path : "gpurun_out/k3_trace.csv", "w");
+                    if (!f) fprintf(stderr, "k3 trace: cannot write %s\n", path ? path : "gpurun_out/k3_trace.csv");
                     if (f) {
-                        fprintf(f, "cta,smid,start,stream,thresh,prefix,rec,counts,scan,emit,end\n");
+                        fprintf(f, "cta,smid,start,waited,stream,thresh,prefix,rec,counts,scan,emit,attend,end\n");
                         for (uint32_t i = 0; i < G; ++i) {
                             fprintf(f, "%u,%llu", i, (unsigned long long)h[i * kSlots + 6]);
-                            for (int j = 0; j < 9; ++j) {
+                            for (int j = 0; j < kCols; ++j) {
                                 const uint64_t raw = h[i * kSlots + cols[j]];
                                 fprintf(f, ",%.3f", raw ? (double)(raw - t0) / 1000.0 : 0.0);
                             }
@@ -2279,6 +2336,10 @@ spl_status hamming_topk_attend_impl(spl_ctx* ctx, const uint32_t* codes, uint64_
     {
         const char* e = getenv("SPL_ATT_PF");
         prm.att_pf = (e && *e == '1') ? 1 : 0;
+    }
+    {
+        const char* e = getenv("SPL_ATT_PRE");
+        prm.att_pre = (e && *e == '1') ? 1 : 0;
     }
     const char* tr = getenv("SPL_K3_TRACE");
     uint64_t* dtrace = nullptr;

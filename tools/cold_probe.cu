@@ -66,6 +66,21 @@ __global__ void touch(const uint8_t* __restrict__ a, uint64_t bytes, uint64_t st
         acc ^= __ldcg(reinterpret_cast<const uint32_t*>(a + o));
     if (acc == 0x12345678u) out[0] = acc;
 }
+// L2 prefetch of a contiguous range: cp.async.bulk.prefetch (chunk bytes per
+// request) or prefetch.global.L2 per 128-byte line
+__global__ void pf_bulk(const uint8_t* a, uint64_t bytes, uint32_t chunk) {
+    const uint64_t per = ((bytes + gridDim.x - 1) / gridDim.x + 15) & ~15ull;
+    const uint64_t b0 = blockIdx.x * per, b1 = min(bytes, b0 + per);
+    for (uint64_t b = b0 + (uint64_t)threadIdx.x * chunk; b < b1; b += (uint64_t)blockDim.x * chunk) {
+        const uint32_t n = (uint32_t)min((uint64_t)chunk, b1 - b) & ~15u;
+        if (n) asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a + b), "r"(n) : "memory");
+    }
+}
+__global__ void pf_line(const uint8_t* a, uint64_t bytes) {
+    for (uint64_t b = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) * 128; b < bytes;
+         b += (uint64_t)gridDim.x * blockDim.x * 128)
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(a + b));
+}
 __global__ void empty_k(uint32_t* out) {
     if (threadIdx.x == 1234) out[0] = 1;
 }
@@ -135,6 +150,16 @@ int main() {
         touch<<<148, 256, 0, s>>>(codes, SB, 65536, o);
     }, stream0);
     run("gather 43MB after flush", flush_l2, gather);
+    run("stream 67MB after flush + stream (L2-warm: second pass)", [&](int i) { flush_l2(i); stream0(i); }, stream0);
+    for (uint32_t chunk : {4096u, 32768u}) {
+        char nm[96];
+        snprintf(nm, sizeof nm, "stream 67MB after flush + bulk prefetch %u B (sync)", chunk);
+        run(nm, [&](int i) { flush_l2(i); pf_bulk<<<444, 256, 0, s>>>(codes, SB, chunk); cudaStreamSynchronize(s); }, stream0);
+        snprintf(nm, sizeof nm, "bulk prefetch 67MB alone, %u B requests", chunk);
+        run(nm, flush_l2, [&](int) { pf_bulk<<<444, 256, 0, s>>>(codes, SB, chunk); });
+    }
+    run("stream 67MB after flush + line prefetch (sync)", [&](int i) { flush_l2(i); pf_line<<<444, 256, 0, s>>>(codes, SB); cudaStreamSynchronize(s); }, stream0);
+    run("line prefetch 67MB alone", flush_l2, [&](int) { pf_line<<<444, 256, 0, s>>>(codes, SB); });
     run("gather 43MB after flush + 64KB-stride touch of K/V", [&](int i) {
         flush_l2(i);
         touch<<<148, 256, 0, s>>>(kv, KVB, 65536, o);
