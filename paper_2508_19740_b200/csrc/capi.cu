@@ -2,6 +2,7 @@
 // reference's error wording, context / workspace management, dispatch to the
 // sm_100a kernels. No CPU compute path exists: every compute entry point
 // launches a kernel or fails.
+#include <cuda.h>  // driver types only (entry points fetched through cudart)
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -72,6 +73,43 @@ extern "C" {
 
 const char* spl_version(void) { return "spotlight-b200 0.1 (sm_100a)"; }
 
+namespace {
+// SMs this context may actually use. A green context (or any context created
+// on an SM partition) reports its share through cuCtxGetDevResource; MPS
+// clients are capped by CUDA_MPS_ACTIVE_THREAD_PERCENTAGE. Either way the
+// fused K3 kernel's CTAs may not all be resident at once, so such contexts
+// launch it cooperatively (the driver then guarantees co-residency or refuses,
+// and the retrieval falls back to the two-pass kernels). Returns the usable
+// SM count; *limited is set when it is below the device's.
+int usable_sms(int device_sms, bool* limited) {
+    *limited = false;
+    int sms = device_sms;
+    using GetCurrent = CUresult (*)(CUcontext*);
+    using GetRes = CUresult (*)(CUcontext, CUdevResource*, CUdevResourceType);
+    void* f_cur = nullptr;
+    void* f_res = nullptr;
+    cudaDriverEntryPointQueryResult q1, q2;
+    if (cudaGetDriverEntryPoint("cuCtxGetCurrent", &f_cur, cudaEnableDefault, &q1) == cudaSuccess &&
+        cudaGetDriverEntryPoint("cuCtxGetDevResource", &f_res, cudaEnableDefault, &q2) == cudaSuccess &&
+        q1 == cudaDriverEntryPointSuccess && q2 == cudaDriverEntryPointSuccess && f_cur && f_res) {
+        CUcontext cu = nullptr;
+        CUdevResource res;
+        memset(&res, 0, sizeof(res));
+        if (reinterpret_cast<GetCurrent>(f_cur)(&cu) == CUDA_SUCCESS && cu &&
+            reinterpret_cast<GetRes>(f_res)(cu, &res, CU_DEV_RESOURCE_TYPE_SM) == CUDA_SUCCESS &&
+            res.sm.smCount > 0 && (int)res.sm.smCount < sms)
+            sms = (int)res.sm.smCount;
+    }
+    cudaGetLastError();
+    if (const char* e = getenv("CUDA_MPS_ACTIVE_THREAD_PERCENTAGE")) {
+        const double pct = atof(e);
+        if (pct > 0.0 && pct < 100.0) sms = std::max(1, std::min(sms, (int)(device_sms * pct / 100.0)));
+    }
+    *limited = sms < device_sms;
+    return sms;
+}
+}  // namespace
+
 spl_status spl_ctx_create(int device, spl_ctx** out) {
     if (!out) return SPL_E_STATE;
     *out = nullptr;
@@ -90,7 +128,9 @@ spl_status spl_ctx_create(int device, spl_ctx** out) {
     }
     spl_ctx* c = new spl_ctx;
     c->device = device;
-    c->num_sms = prop.multiProcessorCount;
+    bool limited = false;
+    c->num_sms = usable_sms(prop.multiProcessorCount, &limited);
+    c->k3_coop = limited;
     if (cudaMalloc(&c->dev_err, sizeof(uint32_t)) != cudaSuccess ||
         cudaMemset(c->dev_err, 0, sizeof(uint32_t)) != cudaSuccess ||
         cudaDeviceSynchronize() != cudaSuccess) {

@@ -1408,13 +1408,17 @@ __global__ void __launch_bounds__(kThreads, 3) k3_fused(K3Params prm) {
         asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
         prm.trace[(uint64_t)blockIdx.x * 16 + 6] = smid;
     }
-    // The readiness waits below need every CTA of a problem resident: the
-    // plan keeps G <= SMs x CTAs/SM (occupancy API) and the launch is a plain
-    // one (a cooperative launch costs ~3 us more per graph replay; opt in
-    // with SPL_K3_COOP=1 where other work may hold SMs, e.g. MPS caps). If
-    // that ever fails, the watchdog in wait_count turns the hang into a
-    // device error. (Arrival tickets would remove the requirement but their
-    // single-address atomic delays the last CTAs' start by ~2 us.)
+    // The readiness waits below need the CTAs of a problem to run together:
+    // the plan keeps G <= usable SMs x CTAs/SM (occupancy API). Plain launch
+    // by default: CTAs are dispatched in index order and a problem's segments
+    // are neighbours, so a concurrent kernel holding SMs only delays the
+    // retrieval (tests/test_gpu_coresidency.py). SM-limited contexts (green
+    // contexts, MPS caps: detected at spl_ctx_create) or SPL_K3_COOP=1 launch
+    // cooperatively (a cooperative launch costs ~3 us more per graph replay);
+    // if the driver refuses, the two-pass kernels run instead. The watchdog in
+    // wait_count turns any remaining hang into a device error. (Arrival
+    // tickets would remove the dispatch-order assumption, but measured +4 us
+    // on the back-to-back headline: segment-to-SM placement changes per launch.)
     const uint32_t seg = blockIdx.x;
     pdl_trigger();
     for (uint32_t i = tid; i < priv_bytes / 16; i += kThreads)
@@ -2156,6 +2160,14 @@ void k3_trace_report(uint64_t* dtrace, uint32_t G, uint64_t S, cudaStream_t s) {
             }
 }
 
+// Cooperative launch of the fused kernels: SM-limited contexts (detected at
+// spl_ctx_create) or SPL_K3_COOP=1 (read per call).
+bool k3_coop(const spl_ctx* ctx) {
+    if (ctx->k3_coop) return true;
+    const char* e = getenv("SPL_K3_COOP");
+    return e && *e == '1';
+}
+
 // SPL_K3_PATH=twopass forces the two-kernel path (A/B measurement, tests).
 bool fused_allowed() {
     const char* e = getenv("SPL_K3_PATH");
@@ -2213,14 +2225,27 @@ spl_status hamming_topk_impl(spl_ctx* ctx, const uint32_t* codes, uint64_t strid
             }
             prm.trace = dtrace;
             void* args[] = {&prm};
-            const char* coop = getenv("SPL_K3_COOP");
-            if (coop && *coop == '1')
-                SPL_CUDA_TRY(ctx, cudaLaunchCooperativeKernel(fp.fn, dim3(G), dim3(kThreads), args, fp.smem, s));
-            else
+            bool launched = true;
+            if (k3_coop(ctx)) {
+                // cooperative: co-residency guaranteed by the driver, or the
+                // launch is refused and the two-pass kernels below run instead
+                const cudaError_t e = cudaLaunchCooperativeKernel(fp.fn, dim3(G), dim3(kThreads), args, fp.smem, s);
+                if (e == cudaErrorCooperativeLaunchTooLarge) {
+                    cudaGetLastError();
+                    launched = false;
+                } else {
+                    SPL_CUDA_TRY(ctx, e);
+                }
+            } else {
                 SPL_CUDA_TRY(ctx, launch_pdl(fp.fn, dim3(G), dim3(kThreads), fp.smem, s, args));
+            }
+            if (!launched) {
+                if (dtrace) cudaFree(dtrace);
+            } else {
             st = after_launch(ctx, pf ? "k3_fused_pf" : "k3_fused");
             if (dtrace) k3_trace_report(dtrace, G, fp.pl.g.S, s);
             return st;
+            }
         }
     }
     K3Plan pl;
@@ -2349,11 +2374,18 @@ spl_status hamming_topk_attend_impl(spl_ctx* ctx, const uint32_t* codes, uint64_
     }
     prm.trace = dtrace;
     void* args[] = {&prm};
-    const char* coop = getenv("SPL_K3_COOP");
-    if (coop && *coop == '1')
-        SPL_CUDA_TRY(ctx, cudaLaunchCooperativeKernel(fp.fn, dim3(G), dim3(kThreads), args, fp.smem, s));
-    else
+    if (k3_coop(ctx)) {
+        const cudaError_t e = cudaLaunchCooperativeKernel(fp.fn, dim3(G), dim3(kThreads), args, fp.smem, s);
+        if (e == cudaErrorCooperativeLaunchTooLarge && !peer) {
+            // the unfused decode step (K3 then K4) runs instead
+            cudaGetLastError();
+            if (dtrace) cudaFree(dtrace);
+            return SPL_OK;
+        }
+        SPL_CUDA_TRY(ctx, e);
+    } else {
         SPL_CUDA_TRY(ctx, launch_pdl(fp.fn, dim3(G), dim3(kThreads), fp.smem, s, args));
+    }
     if ((st = after_launch(ctx, peer ? "k3_fused_shard_attend" : "k3_fused_attend"))) return st;
     if (dtrace) k3_trace_report(dtrace, G, fp.pl.g.S, s);
     *done = true;
@@ -2501,7 +2533,10 @@ spl_status hamming_topk_sharded_impl(spl_ctx* ctx, spl_peer* peer, const uint32_
     }
     prm.trace = dtrace;
     void* args[] = {&prm};
-    SPL_CUDA_TRY(ctx, cudaLaunchKernel(fp.fn, dim3(fp.pl.g.G), dim3(kThreads), args, fp.smem, s));
+    if (k3_coop(ctx))
+        SPL_CUDA_TRY(ctx, cudaLaunchCooperativeKernel(fp.fn, dim3(fp.pl.g.G), dim3(kThreads), args, fp.smem, s));
+    else
+        SPL_CUDA_TRY(ctx, cudaLaunchKernel(fp.fn, dim3(fp.pl.g.G), dim3(kThreads), args, fp.smem, s));
     st = after_launch(ctx, "k3_fused_shard");
     if (dtrace) k3_trace_report(dtrace, fp.pl.g.G, fp.pl.g.S, s);
     return st;

@@ -18,7 +18,8 @@
 // during stream capture).
 struct spl_ctx {
     int device = 0;
-    int num_sms = 148;
+    int num_sms = 148;        // SMs this context can use (see usable_sms in capi.cu)
+    bool k3_coop = false;     // SM-limited context: fused K3 launches are cooperative
     std::string err;
     uint64_t launches = 0;
     std::string launch_log;  // kernel names since the last spl_launch_log (bounded)
