@@ -191,6 +191,17 @@ __device__ __forceinline__ void tmem_ld16_nowait(uint32_t taddr, uint32_t (&r)[1
           "=r"(r[14]), "=r"(r[15])
         : "r"(taddr));
 }
+__device__ __forceinline__ void tmem_ld32_nowait(uint32_t taddr, uint32_t (&r)[32]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+          "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+          "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]),
+          "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]),
+          "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+        : "r"(taddr));
+}
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
 // Epilogue 2 for one column half: code bit of column j = (z_j >= 0) goes to
@@ -626,12 +637,13 @@ __global__ void __launch_bounds__(kWsThreads, 1)
             // 16-byte chunk j of the row sits at chunk j ^ (row % 8)
             uint8_t* a1row = sA1 + (i & 1) * XB + ch * (kTcTileM * 128u) + row * 128u;
             const uint32_t tD = tmem + (i & 1) * 128u + lane_addr + ch * 64u;
+            uint32_t rr[2][32];
+            tmem_ld32_nowait(tD, rr[0]);
+            tmem_ld32_nowait(tD + 32, rr[1]);
+            tmem_wait_ld();
 #pragma unroll
             for (uint32_t c0 = 0; c0 < 64; c0 += 32) {
-                uint32_t r[2][16];
-                tmem_ld16_nowait(tD + c0, r[0]);
-                tmem_ld16_nowait(tD + c0 + 16, r[1]);
-                tmem_wait_ld();
+                uint32_t (&r)[32] = rr[c0 >> 5];
 #pragma unroll
                 for (uint32_t hh = 0; hh < 2; ++hh) {
                     const float4* bp = reinterpret_cast<const float4*>(s_b1 + ch * 64u + c0 + 16 * hh);
@@ -648,7 +660,7 @@ __global__ void __launch_bounds__(kWsThreads, 1)
                         float a[2];
 #pragma unroll
                         for (int u = 0; u < 2; ++u) {
-                            const float hv = fmaf(__uint_as_float(r[hh][e + u]), 0.5f, hb[e + u]);
+                            const float hv = fmaf(__uint_as_float(r[16 * hh + e + u]), 0.5f, hb[e + u]);
                             float t;
                             asm("tanh.approx.f32 %0, %1;" : "=f"(t) : "f"(hv));
                             a[u] = fmaf(hv, t, hv);
@@ -686,15 +698,16 @@ __global__ void __launch_bounds__(kWsThreads, 1)
             // column (x * w, NaN * 0 = NaN), every a1 and every z2 column, so
             // column 0 of D2 decides the row (one check instead of L)
             float z0 = 0.0f;
+            constexpr uint32_t kCols = L >= 64 ? 64u : 32u;  // columns per TMEM wait
 #pragma unroll
-            for (uint32_t c0 = 0; c0 < L; c0 += 32) {
-                uint32_t r[2][16];
-                tmem_ld16_nowait(tD + c0, r[0]);
-                tmem_ld16_nowait(tD + c0 + 16, r[1]);
+            for (uint32_t c0 = 0; c0 < L; c0 += kCols) {
+                uint32_t r[kCols / 32][32];
+#pragma unroll
+                for (uint32_t h = 0; h < kCols / 32; ++h) tmem_ld32_nowait(tD + c0 + 32 * h, r[h]);
                 tmem_wait_ld();
 #pragma unroll
-                for (uint32_t e = 0; e < 32; ++e) {
-                    const uint32_t u = r[e >> 4][e & 15];
+                for (uint32_t e = 0; e < kCols; ++e) {
+                    const uint32_t u = r[e >> 5][e & 31];
                     if (c0 == 0 && e == 0) z0 = __uint_as_float(u);
                     neg[(c0 + e) % W] = __funnelshift_l(u, neg[(c0 + e) % W], 1);
                 }
