@@ -572,12 +572,15 @@ def main():
     # dram bytes per retrieval: ncu cannot run inside the timed process, so
     # this is the newest committed `ncu --set full` capture of the same kernel
     # on the same workload, stamped with the commit it was taken at
-    traffic = traffic_src = None
+    traffic = traffic_src = traffic_b2b = None
     for tpath in sorted((ROOT / "profiles").glob("r*_k3_traffic.json"), reverse=True):
         try:
             tj = json.loads(tpath.read_text())
             traffic = tj.get("bytes_per_retrieval")
             traffic_src = f"{tpath.relative_to(ROOT)} (commit {tj.get('commit', 'unrecorded')})"
+            # back-to-back retrievals (the `value` timing) read part of the
+            # codes from L2: DRAM bytes per retrieval in that state
+            traffic_b2b = (tj.get("back_to_back") or {}).get("dram_bytes_read_median")
             break
         except Exception:
             continue
@@ -594,6 +597,7 @@ def main():
                      "unit": "GB/s", "frac": round(achieved / hbm, 4),
                      "algorithmic_bytes": alg_bytes, "traffic": traffic,
                      "traffic_source": traffic_src,
+                     "traffic_back_to_back_dram_read": traffic_b2b,
                      "scan_kernel_us": round(scan_ms * 1000, 2),
                      "scan_kernel_frac": round(scan_bytes / (scan_ms * 1e-3) / 1e9 / hbm, 4)},
         "timing": {"value_source": graph_note or "eager launches", "eager_us": round(eager_ms * 1000, 2)},

@@ -7,8 +7,14 @@
 // explicit fma (read from the shipped libm.so.6 disassembly: __expf_fma at
 // 0x7dc40), and the table/constants read from its .rodata. Pure IEEE double
 // arithmetic, so host (g++ -ffp-contract=off) and device (__fma_rn/__dmul_rn)
-// evaluate identically; tests/test_expf_port.py checks it against libm's expf
-// over a dense sweep (tools/check_expf_exhaustive.c: all 2^32 inputs).
+// evaluate identically; tools/check_expf_exhaustive.cpp compares it with
+// libm's expf over all 2^32 inputs (0 mismatches), and the GPU parity tests
+// check K1's pre-activations bitwise against the reference.
+// Origin / licence: the algorithm, its 32-entry table and constants are
+// glibc's (sysdeps/ieee754/flt-32/e_expf.c, contributed by Arm from
+// optimized-routines; LGPL-2.1+ in glibc, MIT / Apache-2.0 WITH LLVM-exception
+// in Arm optimized-routines). This is a restatement for bit parity, not a copy
+// of the reference repository.
 #pragma once
 #include <stdint.h>
 #include <string.h>
