@@ -47,7 +47,7 @@ typedef enum spl_status {
     SPL_E_EMPTY_PAIRS = 8 /* EmptyPairError (errors.hpp:27-30): no valid ranking pairs */
 } spl_status;
 
-typedef enum spl_dtype { SPL_F32 = 0, SPL_BF16 = 1 } spl_dtype;
+typedef enum spl_dtype { SPL_F32 = 0, SPL_BF16 = 1, SPL_F64 = 2 /* spl_matmul / spl_map only */ } spl_dtype;
 typedef enum spl_hasher_kind {
     SPL_HASHER_MLP = 1,
     SPL_HASHER_LINEAR = 0,
@@ -134,6 +134,29 @@ spl_status spl_oracle_topk(spl_ctx* ctx, const float* q, const void* keys, int k
  * and queries, then spl_oracle_topk on the projections with scale 1. */
 spl_status spl_project(spl_ctx* ctx, const float* a, uint64_t m, uint32_t k, const float* b,
                        uint32_t n, float* c, void* stream);
+/* Generic dense helpers behind the reference's templated host API, for f32
+ * and f64 (row-major device arrays). Not on the decode path: the drop-in
+ * composes them for matmul<T> (matrix.hpp:81-99) and the double
+ * instantiations of mlp_forward / linear_hash / mlp_hash, soft_sign,
+ * soft_codes and downproj_scores (hashers.hpp:70-98).
+ * spl_matmul: c[m][n] = a[m][k] . b[k][n], each output a fused multiply-add
+ * chain over the inner index in order from 0 (the reference build's
+ * contraction; bit-exact). k == 0 gives zeros.
+ * spl_map: elementwise over x[rows][cols]:
+ *   SPL_MAP_BIAS_SILU  out = silu(x + bias[col]), silu(z) = z / (1 + exp(-z))
+ *                      (f32: glibc expf port, bit-exact; f64: CUDA exp)
+ *   SPL_MAP_SOFT_SIGN  out = gamma x / (1 + gamma |x|), gamma > 0
+ *   SPL_MAP_SIGN_BITS  out = u8 (x >= 0), sign(0) -> 1 */
+typedef enum spl_map_op {
+    SPL_MAP_BIAS_SILU = 0,
+    SPL_MAP_SOFT_SIGN = 1,
+    SPL_MAP_SIGN_BITS = 2
+} spl_map_op;
+spl_status spl_matmul(spl_ctx* ctx, int dtype, const void* a, uint64_t m, uint64_t k,
+                      const void* b, uint64_t n, void* c, void* stream);
+spl_status spl_map(spl_ctx* ctx, int dtype, int op, const void* x, uint64_t rows,
+                   uint64_t cols, const void* bias, double gamma, void* out, void* stream);
+
 /* iou (attention_eval.hpp:63, attention_eval.cpp:216-232) per problem of two
  * ascending index lists a[p][0..cnt_a[p]) and b[p][0..cnt_b[p]) (row strides
  * a_stride, b_stride): |a ∩ b| / |a ∪ b| as double, 1.0 when both are empty. */

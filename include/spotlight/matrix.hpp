@@ -1,7 +1,8 @@
 // Drop-in for the container half of proj/include/spotlight/matrix.hpp: a
 // dense row-major Matrix<T> with the same accessors, so code written against
-// the reference compiles unchanged. The reference's CPU matmul kernels are not
-// re-exposed — the B200 path computes its products on the GPU (hashers.hpp).
+// the reference compiles unchanged. matmul<T> (float / double) runs on the
+// GPU (spl_matmul) with the reference build's per-output FMA order; the
+// training-side products matmul_bt / add_matmul_at are not re-exposed.
 #pragma once
 
 #include <algorithm>
@@ -67,6 +68,14 @@ template <typename T>
 T norm2(std::span<const T> a) {
     return std::sqrt(dot(a, a));
 }
+
+/// C = A * B (matrix.hpp:81-99): every output an FMA chain over the inner
+/// index in order, as the reference's Release build computes it. GPU.
+/// DimensionError("matmul: inner dimensions ... do not match").
+template <typename T>
+Matrix<T> matmul(const Matrix<T>& a, const Matrix<T>& b);
+extern template Matrix<float> matmul<float>(const Matrix<float>&, const Matrix<float>&);
+extern template Matrix<double> matmul<double>(const Matrix<double>&, const Matrix<double>&);
 
 template <typename To, typename From>
 Matrix<To> matrix_cast(const Matrix<From>& m) {

@@ -86,6 +86,7 @@ public:
     }
     DevBuf(const DevBuf&) = delete;
     DevBuf& operator=(const DevBuf&) = delete;
+    DevBuf(DevBuf&& o) noexcept : p_(o.p_), n_(o.n_) { o.p_ = nullptr; }
     void upload(const void* host, std::size_t bytes) {
         if (bytes) check(spl_memcpy(ctx(), p_, host, bytes, nullptr));
     }
@@ -354,24 +355,138 @@ MlpHasher mlp_gaussian_init(std::uint32_t d, std::uint32_t h, std::uint32_t code
     return m;
 }
 
-Matrix<float> mlp_forward(const MlpHasher& h, const Matrix<float>& x) {
+namespace {
+
+// Code widths the exact encoder takes: whole 32-bit words. Wider layer-2 /
+// projection copies with zero columns give the same pre-activations for the
+// real columns (each column is its own FMA chain); the extra ones are dropped.
+std::uint32_t padded_bits(std::size_t L) { return static_cast<std::uint32_t>((L + 31) / 32 * 32); }
+
+Matrix<float> pad_cols(const Matrix<float>& m, std::size_t cols) {
+    if (m.cols() == cols) return m;
+    Matrix<float> out(m.rows(), cols);
+    for (std::size_t i = 0; i < m.rows(); ++i)
+        std::copy(m.row(i).begin(), m.row(i).end(), out.row(i).begin());
+    return out;
+}
+
+template <typename T>
+void require_finite(const Matrix<T>& m, const char* what) {
+    if (!m.all_finite()) throw NumericError(std::string(what) + " contains non-finite values");
+}
+
+// The double instances: spl_matmul / spl_map on device buffers.
+template <typename T>
+constexpr int dtype_of() {
+    return std::is_same_v<T, double> ? SPL_F64 : SPL_F32;
+}
+
+template <typename T>
+void device_matmul(const void* a, std::size_t m, std::size_t k, const void* b, std::size_t n, void* c) {
+    check(spl_matmul(ctx(), dtype_of<T>(), a, m, k, b, n, c, nullptr));
+}
+
+template <typename T>
+void check_mm(const Matrix<T>& a, const Matrix<T>& b) {
+    if (a.cols() != b.rows())
+        throw DimensionError("matmul: inner dimensions " + std::to_string(a.cols()) + " and " +
+                             std::to_string(b.rows()) + " do not match");
+}
+
+// pre-activations of an f64 MLP hasher, left on the device
+template <typename T>
+DevBuf mlp_forward_dev(const MlpHasherT<T>& h, const Matrix<T>& x) {
+    const std::size_t m = x.rows(), d = h.w1.rows(), hd = h.w1.cols(), L = h.w2.cols();
+    DevBuf dx(x.data(), x.size() * sizeof(T)), dw1(h.w1.data(), h.w1.size() * sizeof(T));
+    DevBuf db1(h.b1.data(), h.b1.size() * sizeof(T)), dw2(h.w2.data(), h.w2.size() * sizeof(T));
+    DevBuf z1(m * hd * sizeof(T)), z2(m * L * sizeof(T));
+    device_matmul<T>(dx.as<void>(), m, d, dw1.as<void>(), hd, z1.as<void>());
+    check(spl_map(ctx(), dtype_of<T>(), SPL_MAP_BIAS_SILU, z1.as<void>(), m, hd, db1.as<void>(), 0.0,
+                  z1.as<void>(), nullptr));
+    device_matmul<T>(z1.as<void>(), m, hd, dw2.as<void>(), L, z2.as<void>());
+    return z2;
+}
+
+template <typename T>
+void mlp_checks(const MlpHasherT<T>& h, const Matrix<T>& x) {
     if (x.cols() != h.w1.rows())
         throw DimensionError("mlp_forward: input dim " + str(x.cols()) + " != hasher dim " +
                              str(h.w1.rows()));
-    Matrix<float> pre(x.rows(), h.code_bits());
-    if (x.rows() == 0 || h.code_bits() == 0) return pre;
-    if (h.code_bits() % 32 != 0)
-        throw DimensionError("mlp_forward: the GPU encoder needs code_bits % 32 == 0 (got " +
-                             str(h.code_bits()) + ")");
-    DevHasher dh(h);
-    DevBuf dx(x.data(), x.size() * 4);
-    DevBuf dp(pre.size() * 4);
-    check(spl_mlp_forward(ctx(), dh.get(), dx.as<float>(), 1, static_cast<std::uint32_t>(x.rows()),
-                          dp.as<float>(), nullptr));
-    finish();
-    dp.download(pre.data(), pre.size() * 4);
-    return pre;
+    if (h.w2.rows() != h.w1.cols() || h.b1.size() != h.w1.cols())
+        throw DimensionError("mlp_forward: inconsistent hasher shapes");
+    require_finite(h.w1, "mlp w1");
+    require_finite(h.w2, "mlp w2");
+    for (const T& v : h.b1)
+        if (!std::isfinite(static_cast<double>(v))) throw NumericError("mlp b1 is non-finite");
+    require_finite(x, "mlp input");
 }
+
+template <typename T>
+BitMatrix sign_bits_dev(const DevBuf& pre, std::size_t m, std::size_t L) {
+    BitMatrix bits(m, L);
+    if (m == 0 || L == 0) return bits;
+    DevBuf db(m * L);
+    check(spl_map(ctx(), dtype_of<T>(), SPL_MAP_SIGN_BITS, pre.as<void>(), m, L, nullptr, 0.0,
+                  db.as<void>(), nullptr));
+    finish();
+    db.download(bits.data(), m * L);
+    return bits;
+}
+
+}  // namespace
+
+template <typename T>
+Matrix<T> matmul(const Matrix<T>& a, const Matrix<T>& b) {
+    check_mm(a, b);
+    Matrix<T> c(a.rows(), b.cols());
+    if (c.size() == 0) return c;
+    DevBuf da(a.data(), a.size() * sizeof(T)), dbm(b.data(), b.size() * sizeof(T)), dc(c.size() * sizeof(T));
+    device_matmul<T>(da.as<void>(), a.rows(), a.cols(), dbm.as<void>(), b.cols(), dc.as<void>());
+    finish();
+    dc.download(c.data(), c.size() * sizeof(T));
+    return c;
+}
+template Matrix<float> matmul<float>(const Matrix<float>&, const Matrix<float>&);
+template Matrix<double> matmul<double>(const Matrix<double>&, const Matrix<double>&);
+
+template <typename T>
+Matrix<T> mlp_forward(const MlpHasherT<T>& h, const Matrix<T>& x) {
+    if constexpr (std::is_same_v<T, float>) {
+        if (x.cols() != h.w1.rows())
+            throw DimensionError("mlp_forward: input dim " + str(x.cols()) + " != hasher dim " +
+                                 str(h.w1.rows()));
+        Matrix<float> pre(x.rows(), h.code_bits());
+        if (x.rows() == 0 || h.code_bits() == 0) return pre;
+        const std::uint32_t Lp = padded_bits(h.code_bits());
+        MlpHasher hp = h;
+        hp.w2 = pad_cols(h.w2, Lp);
+        DevHasher dh(hp);  // require_finite on the weights (spl_hasher_create)
+        DevBuf dx(x.data(), x.size() * 4);
+        DevBuf dp((std::size_t)x.rows() * Lp * 4);
+        check(spl_mlp_forward(ctx(), dh.get(), dx.as<float>(), 1, static_cast<std::uint32_t>(x.rows()),
+                              dp.as<float>(), nullptr));
+        finish();
+        if (Lp == h.code_bits()) {
+            dp.download(pre.data(), pre.size() * 4);
+        } else {
+            Matrix<float> full(x.rows(), Lp);
+            dp.download(full.data(), full.size() * 4);
+            for (std::size_t i = 0; i < x.rows(); ++i)
+                std::copy(full.row(i).begin(), full.row(i).begin() + h.code_bits(), pre.row(i).begin());
+        }
+        return pre;
+    } else {
+        mlp_checks(h, x);
+        Matrix<T> pre(x.rows(), h.code_bits());
+        if (pre.size() == 0) return pre;
+        DevBuf z2 = mlp_forward_dev(h, x);
+        finish();
+        z2.download(pre.data(), pre.size() * sizeof(T));
+        return pre;
+    }
+}
+template Matrix<float> mlp_forward<float>(const MlpHasherT<float>&, const Matrix<float>&);
+template Matrix<double> mlp_forward<double>(const MlpHasherT<double>&, const Matrix<double>&);
 
 CodeMatrix mlp_hash_packed(const MlpHasher& h, const Matrix<float>& x) {
     if (x.cols() != h.w1.rows())
@@ -387,13 +502,105 @@ CodeMatrix linear_hash_packed(const LinearHasher& h, const Matrix<float>& x) {
     return encode_codes(h, x, h.code_bits());
 }
 
-BitMatrix mlp_hash(const MlpHasher& h, const Matrix<float>& x) {
-    return unpack_bits(mlp_hash_packed(h, x));
+namespace {
+// the first L columns of a padded-width code
+BitMatrix first_cols(const BitMatrix& b, std::size_t L) {
+    if (b.cols() == L) return b;
+    BitMatrix out(b.rows(), L);
+    for (std::size_t i = 0; i < b.rows(); ++i)
+        std::copy(b.row(i).begin(), b.row(i).begin() + L, out.row(i).begin());
+    return out;
 }
+}  // namespace
 
-BitMatrix linear_hash(const LinearHasher& h, const Matrix<float>& x) {
-    return unpack_bits(linear_hash_packed(h, x));
+template <typename T>
+BitMatrix mlp_hash(const MlpHasherT<T>& h, const Matrix<T>& x) {
+    if constexpr (std::is_same_v<T, float>) {
+        if (x.cols() != h.w1.rows())
+            throw DimensionError("mlp_forward: input dim " + str(x.cols()) + " != hasher dim " +
+                                 str(h.w1.rows()));
+        if (x.rows() == 0 || h.code_bits() == 0) return BitMatrix(x.rows(), h.code_bits());
+        MlpHasher hp = h;
+        hp.w2 = pad_cols(h.w2, padded_bits(h.code_bits()));
+        return first_cols(unpack_bits(encode_codes(hp, x, padded_bits(h.code_bits()))), h.code_bits());
+    } else {
+        mlp_checks(h, x);
+        if (x.rows() == 0 || h.code_bits() == 0) return BitMatrix(x.rows(), h.code_bits());
+        DevBuf z2 = mlp_forward_dev(h, x);
+        return sign_bits_dev<T>(z2, x.rows(), h.code_bits());
+    }
 }
+template BitMatrix mlp_hash<float>(const MlpHasherT<float>&, const Matrix<float>&);
+template BitMatrix mlp_hash<double>(const MlpHasherT<double>&, const Matrix<double>&);
+
+template <typename T>
+BitMatrix linear_hash(const LinearHasherT<T>& h, const Matrix<T>& x) {
+    if (x.cols() != h.projection.rows())
+        throw DimensionError("linear_hash: input dim " + str(x.cols()) + " != hasher dim " +
+                             str(h.projection.rows()));
+    if (x.rows() == 0 || h.code_bits() == 0) return BitMatrix(x.rows(), h.code_bits());
+    if constexpr (std::is_same_v<T, float>) {
+        LinearHasher hp{pad_cols(h.projection, padded_bits(h.code_bits()))};
+        return first_cols(unpack_bits(encode_codes(hp, x, padded_bits(h.code_bits()))), h.code_bits());
+    } else {
+        require_finite(h.projection, "linear projection");
+        require_finite(x, "linear input");
+        const std::size_t m = x.rows(), L = h.code_bits();
+        DevBuf dx(x.data(), x.size() * sizeof(T)), dp(h.projection.data(), h.projection.size() * sizeof(T));
+        DevBuf pre(m * L * sizeof(T));
+        device_matmul<T>(dx.as<void>(), m, x.cols(), dp.as<void>(), L, pre.as<void>());
+        return sign_bits_dev<T>(pre, m, L);
+    }
+}
+template BitMatrix linear_hash<float>(const LinearHasherT<float>&, const Matrix<float>&);
+template BitMatrix linear_hash<double>(const LinearHasherT<double>&, const Matrix<double>&);
+
+template <typename T>
+Matrix<T> soft_sign(const Matrix<T>& z, T gamma) {
+    if (!(gamma > T(0))) throw DimensionError("soft_sign: gamma must be positive");
+    Matrix<T> out(z.rows(), z.cols());
+    if (out.size() == 0) return out;
+    DevBuf dz(z.data(), z.size() * sizeof(T));
+    check(spl_map(ctx(), dtype_of<T>(), SPL_MAP_SOFT_SIGN, dz.as<void>(), z.rows(), z.cols(), nullptr,
+                  static_cast<double>(gamma), dz.as<void>(), nullptr));
+    finish();
+    dz.download(out.data(), out.size() * sizeof(T));
+    return out;
+}
+template Matrix<float> soft_sign<float>(const Matrix<float>&, float);
+template Matrix<double> soft_sign<double>(const Matrix<double>&, double);
+
+template <typename T>
+Matrix<T> soft_codes(const MlpHasherT<T>& h, const Matrix<T>& x) {
+    return soft_sign(mlp_forward(h, x), h.gamma);
+}
+template Matrix<float> soft_codes<float>(const MlpHasherT<float>&, const Matrix<float>&);
+template Matrix<double> soft_codes<double>(const MlpHasherT<double>&, const Matrix<double>&);
+
+template <typename T>
+std::vector<T> downproj_scores(const DownProjEstimatorT<T>& e, std::span<const T> q,
+                               const Matrix<T>& keys) {
+    const std::size_t d = e.projection.rows(), r = e.projection.cols(), n = keys.rows();
+    if (q.size() != d || keys.cols() != d) throw DimensionError("downproj_scores: shape mismatch");
+    std::vector<T> scores(n);
+    if (n == 0) return scores;
+    if (r == 0) return scores;
+    // qp = q P and kp = K P (the reference's per-output FMA order), then
+    // score_i = kp_i . qp: kp (n x r) times qp as an r x 1 matrix
+    DevBuf dq(q.data(), d * sizeof(T)), dP(e.projection.data(), e.projection.size() * sizeof(T));
+    DevBuf dk(keys.data(), keys.size() * sizeof(T)), qp(r * sizeof(T)), kp(n * r * sizeof(T));
+    DevBuf ds(n * sizeof(T));
+    device_matmul<T>(dq.as<void>(), 1, d, dP.as<void>(), r, qp.as<void>());
+    device_matmul<T>(dk.as<void>(), n, d, dP.as<void>(), r, kp.as<void>());
+    device_matmul<T>(kp.as<void>(), n, r, qp.as<void>(), 1, ds.as<void>());
+    finish();
+    ds.download(scores.data(), n * sizeof(T));
+    return scores;
+}
+template std::vector<float> downproj_scores<float>(const DownProjEstimatorT<float>&, std::span<const float>,
+                                                   const Matrix<float>&);
+template std::vector<double> downproj_scores<double>(const DownProjEstimatorT<double>&, std::span<const double>,
+                                                     const Matrix<double>&);
 
 void write_hasher(const std::string& path, const AnyHasher& hasher) {
     auto os = open_out(path);

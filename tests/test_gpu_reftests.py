@@ -1,5 +1,6 @@
 """The reference's OWN doctest translation units, unmodified, through the
-drop-in: proj/tests/test_bitcodes.cpp and test_attention_eval.cpp compiled
+drop-in: proj/tests/test_bitcodes.cpp, test_hashers.cpp and
+test_attention_eval.cpp compiled
 against include/spotlight/ and linked against libspotlight_b200.so
 (oracle/Makefile `reftests`; tests/cpp/doctest/doctest.h stands in for the
 unshipped vendor/doctest.h). Every compute call inside them is a B200 launch.
@@ -22,5 +23,6 @@ def test_reference_doctest_suites_through_dropin():
     print(r.stderr[-2000:])
     assert r.returncode == 0, r.stdout[-4000:]
     assert "Status: SUCCESS" in r.stdout
-    # all 19 reference cases ran (11 in test_bitcodes.cpp, 8 in test_attention_eval.cpp)
-    assert "test cases: 19 | 19 passed | 0 failed | 0 skipped" in r.stdout
+    # all 31 reference cases ran (11 in test_bitcodes.cpp, 12 in test_hashers.cpp,
+    # 8 in test_attention_eval.cpp)
+    assert "test cases: 31 | 31 passed | 0 failed | 0 skipped" in r.stdout

@@ -1,1 +1,2 @@
-timeout 900 python -m pytest -q -x tests/test_gpu_coresidency.py tests/test_gpu_parity.py tests/test_gpu_bench_shapes.py tests/test_gpu_sharded_decode.py tests/test_gpu_multiproc.py tests/test_gpu_graphs.py 2>&1 | grep -E "FAIL|Error|assert|passed|failed" | head -20
+./oracle/_ref/reftests 2>&1 | tail -30
+timeout 900 python -m pytest -q -x tests/test_gpu_reftests.py tests/test_gpu_dropin.py tests/test_gpu_parity.py 2>&1 | grep -E "FAIL|Error|assert|passed|failed" | head -20
