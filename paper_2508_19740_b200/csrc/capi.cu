@@ -524,25 +524,37 @@ spl_status spl_hasher_create(spl_ctx* ctx, int kind, uint32_t H, uint32_t d, uin
                 for (uint32_t w = 0; w < W; ++w)
                     hp[((size_t)hd * rows2 + p) * L + w * 32 + c] =
                         src2[((size_t)hd * rows2 + p) * L + c * W + w];
-    // cluster-encoder layouts (encode_exact.cu): W1 column quarters, and
-    // layer 2 word-major [w][p][c] so each CTA's words are one contiguous block
-    std::vector<float> hs1, hw2(src2.size());
-    if (kind == SPL_HASHER_MLP && h % 4 == 0) {
+    // cluster-encoder layouts (encode_exact.cu, fma_chain2): W1 column
+    // quarters [H][4][h/4][d] and layer 2 word-major [H][W][32][rows2], both
+    // with one row per output (lane-major), so each CTA's block is contiguous
+    // and a lane's weights are consecutive; chunk c (4 floats) of the row of
+    // output j is stored at chunk slot (c + j mod 32) mod (row / 4), which
+    // makes the per-lane 16-byte loads bank-conflict free.
+    auto rot = [](uint32_t p, uint32_t lane, uint32_t n) {
+        const uint32_t nc = n / 4;
+        return ((p / 4 + lane) % nc) * 4 + p % 4;
+    };
+    std::vector<float> hs1, hw2;
+    const bool cl_ok = d % 4 == 0 && rows2 % 4 == 0;
+    if (kind == SPL_HASHER_MLP && h % 4 == 0 && cl_ok) {
         const uint32_t q = h / 4;
         hs1.resize(h1.size());
         for (uint32_t hd = 0; hd < H; ++hd)
             for (uint32_t r = 0; r < 4; ++r)
-                for (uint32_t p = 0; p < d; ++p)
-                    for (uint32_t jj = 0; jj < q; ++jj)
-                        hs1[(((size_t)hd * 4 + r) * d + p) * q + jj] =
+                for (uint32_t jj = 0; jj < q; ++jj)
+                    for (uint32_t p = 0; p < d; ++p)
+                        hs1[(((size_t)hd * 4 + r) * q + jj) * d + rot(p, jj % 32, d)] =
                             h1[((size_t)hd * d + p) * h + r * q + jj];
     }
-    for (uint32_t hd = 0; hd < H; ++hd)
-        for (uint32_t w = 0; w < W; ++w)
-            for (uint32_t p = 0; p < rows2; ++p)
+    if (cl_ok) {
+        hw2.resize(src2.size());
+        for (uint32_t hd = 0; hd < H; ++hd)
+            for (uint32_t w = 0; w < W; ++w)
                 for (uint32_t c = 0; c < 32; ++c)
-                    hw2[(((size_t)hd * W + w) * rows2 + p) * 32 + c] =
-                        src2[((size_t)hd * rows2 + p) * L + c * W + w];
+                    for (uint32_t p = 0; p < rows2; ++p)
+                        hw2[(((size_t)hd * W + w) * 32 + c) * rows2 + rot(p, c, rows2)] =
+                            src2[((size_t)hd * rows2 + p) * L + c * W + w];
+    }
     if (!up(&hs->w1, h1) || !up(&hs->b1, hb) || !up(&hs->w2, h2) || !up(&hs->w2_perm, hp) ||
         !up(&hs->w1_slices, hs1) || !up(&hs->w2_words, hw2)) {
         spl_hasher_destroy(hs);

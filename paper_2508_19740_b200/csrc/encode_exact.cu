@@ -19,6 +19,9 @@
 
 #include <algorithm>
 #include <string>
+#include <vector>
+#include <cstdio>
+#include <cstdlib>
 
 #include "spl_expf.cuh"
 #include "spl_launch.cuh"
@@ -63,14 +66,17 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 // [0, cap) (n_valid == 0 in a decode step, a full cache): the caller skips the
 // write and the device error word reports a DimensionError instead of a wild
 // store into the next head's rows.
-__device__ __forceinline__ uint64_t append_slot(const EncJob& job, uint32_t b, uint32_t* dev_err,
-                                                bool report) {
-    const uint32_t pos = job.pos[b];
+__device__ __forceinline__ uint64_t append_slot_at(const EncJob& job, uint32_t pos, uint32_t* dev_err,
+                                                   bool report) {
     if (pos < (uint32_t)job.pos_minus_one || (uint64_t)(pos - job.pos_minus_one) >= job.cap) {
         if (report) raise_dev_err(dev_err, SPL_DEV_ERR_DIMENSION);
         return ~0ull;
     }
     return pos - job.pos_minus_one;
+}
+__device__ __forceinline__ uint64_t append_slot(const EncJob& job, uint32_t b, uint32_t* dev_err,
+                                                bool report) {
+    return append_slot_at(job, job.pos[b], dev_err, report);
 }
 
 __global__ void __launch_bounds__(kEncThreads) k1_encode_exact(EncParams prm) {
@@ -248,15 +254,26 @@ __global__ void __launch_bounds__(kEncThreads) k1_encode_exact(EncParams prm) {
 constexpr int kCS = 4;  // CTAs per cluster
 
 struct EncClusterParams {
-    const float* w1s;   // [H][kCS][d][h/kCS]
+    const float* w1s;   // [H][kCS][h/kCS][d]  lane-major rows, rotated chunks (fma_chain2)
     const float* b1;    // [H][h]
-    const float* w2w;   // [H][W][act_dim][32]  word-major, lane-contiguous
+    const float* w2w;   // [H][W][32][act_dim] word-major, lane-major rows, rotated chunks
     uint32_t H, d, h, L, W;
     int kind;
     uint32_t B;
     EncJob job[2];
     uint32_t* dev_err;
+    uint64_t* trace;  // optional [grid][8] globaltimer stamps (SPL_K1_TRACE)
 };
+
+__device__ __forceinline__ uint64_t k1_gtimer() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+#define K1_STAMP(i)                                                                        \
+    if (prm.trace && threadIdx.x == 0)                                                     \
+    prm.trace[(((uint64_t)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x) * 12 + (i)] = \
+        k1_gtimer()
 
 __device__ __forceinline__ void cluster_sync_all() {
     asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;"
@@ -282,11 +299,80 @@ __device__ __forceinline__ void wait_parity0(uint64_t* bar) {
             : "=r"(done) : "r"(smem_u32(bar)) : "memory");
 }
 
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" :: "r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async4(void* dst, const void* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" :: "r"(smem_u32(dst)), "l"(src) : "memory");
+}
+
+// acc0 = the p-ordered FMA chain of xa (n inputs) against this lane's weight
+// row wrow, acc1 the same for xb when `two` (warp-uniform). Weight rows are
+// lane-major with the 16-byte chunks of lane l rotated by l (chunk c of the
+// row sits at slot (c + l) mod n/4, see spl_hasher_create), so every load is
+// one conflict-free LDS.128 per 4 steps instead of one LDS.32 per step, and
+// the inputs are broadcast LDS.128. DN > 0: n == DN at compile time, the
+// weight row is loaded into registers before the dependent FMAs (measured:
+// 128 chained FMAs cost ~750 cycles preloaded vs ~1,600-1,860 with a load
+// per step). The rounding sequence is the reference's either way.
+template <int DN>
+__device__ __forceinline__ void fma_chain2(const float* xa, const float* xb, bool two,
+                                           const float* wrow, uint32_t n, uint32_t lane,
+                                           float& acc0, float& acc1) {
+    if constexpr (DN > 0) {
+        constexpr uint32_t NC = DN / 4;
+        float4 r[NC];
+#pragma unroll
+        for (uint32_t c = 0; c < NC; ++c)
+            r[c] = *reinterpret_cast<const float4*>(wrow + 4 * ((c + lane) % NC));
+#pragma unroll
+        for (uint32_t c = 0; c < NC; ++c) {
+            const float4 a = *reinterpret_cast<const float4*>(xa + 4 * c);
+            acc0 = __fmaf_rn(a.x, r[c].x, acc0);
+            acc0 = __fmaf_rn(a.y, r[c].y, acc0);
+            acc0 = __fmaf_rn(a.z, r[c].z, acc0);
+            acc0 = __fmaf_rn(a.w, r[c].w, acc0);
+        }
+        if (two) {
+#pragma unroll
+            for (uint32_t c = 0; c < NC; ++c) {
+                const float4 b = *reinterpret_cast<const float4*>(xb + 4 * c);
+                acc1 = __fmaf_rn(b.x, r[c].x, acc1);
+                acc1 = __fmaf_rn(b.y, r[c].y, acc1);
+                acc1 = __fmaf_rn(b.z, r[c].z, acc1);
+                acc1 = __fmaf_rn(b.w, r[c].w, acc1);
+            }
+        }
+    } else {
+        const uint32_t nc = n / 4;
+        uint32_t slot = lane % nc;
+        for (uint32_t c = 0; c < nc; ++c) {
+            const float4 wv = *reinterpret_cast<const float4*>(wrow + 4 * slot);
+            slot = slot + 1 == nc ? 0 : slot + 1;
+            const float4 a = *reinterpret_cast<const float4*>(xa + 4 * c);
+            acc0 = __fmaf_rn(a.x, wv.x, acc0);
+            acc0 = __fmaf_rn(a.y, wv.y, acc0);
+            acc0 = __fmaf_rn(a.z, wv.z, acc0);
+            acc0 = __fmaf_rn(a.w, wv.w, acc0);
+            if (two) {
+                const float4 b = *reinterpret_cast<const float4*>(xb + 4 * c);
+                acc1 = __fmaf_rn(b.x, wv.x, acc1);
+                acc1 = __fmaf_rn(b.y, wv.y, acc1);
+                acc1 = __fmaf_rn(b.z, wv.z, acc1);
+                acc1 = __fmaf_rn(b.w, wv.w, acc1);
+            }
+        }
+    }
+}
+
+template <int DN>
 __global__ void __cluster_dims__(kCS, 1, 1) __launch_bounds__(kEncThreads)
     k1_encode_cluster(EncClusterParams prm) {
+
     extern __shared__ __align__(128) float csm[];
     __shared__ __align__(8) uint64_t s_bar;
     __shared__ uint32_t s_bad;
+    __shared__ uint32_t s_pos[kVT];
     const EncJob& job = prm.job[blockIdx.z];
     const uint32_t head = blockIdx.y;
     const uint32_t rank = cluster_rank();
@@ -298,27 +384,44 @@ __global__ void __cluster_dims__(kCS, 1, 1) __launch_bounds__(kEncThreads)
     const uint32_t ntiles = (nvec + kVT - 1) / kVT;
     const uint32_t group = blockIdx.x / kCS, ngroups = gridDim.x / kCS;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    // shared layout: sw1 [d][hs] | sw2 [Wc][act_dim][32] | xs [kVT][d] | a1 [kVT][h]
+    // shared layout: sw1 [hs][d] | sw2 [Wc][32][act_dim] (lane-major rows, rotated
+    // chunks) | xs [kVT][d] | a1 [kVT][h] | sb1 [hs] | vs [kVT][d]
     float* sw1 = csm;
     float* sw2 = sw1 + (mlp ? (size_t)d * hs : 0);
     float* xs = sw2 + (size_t)Wc * act_dim * 32;
     float* a1 = xs + (size_t)kVT * d;
+    float* sb1 = a1 + (size_t)kVT * h;
+    float* vs = sb1 + hs;
+    // rank 0 appends the K / V rows (decode step): V is staged with the input
+    const bool stage_v = rank == 0 && job.out_mode == ENC_APPEND && job.kcache;
 
+    K1_STAMP(0);
     pdl_trigger();
+    // Touch every 64-byte line of the parameter block now: the first read of
+    // a line misses the constant cache (~500 cycles), and later reads sit on
+    // the dependent chain (address math before the layer-2 loads); here the
+    // misses overlap the weight copies.
+    asm volatile("" ::"l"(prm.w1s), "r"(prm.H), "l"(prm.job[0].x), "l"(prm.job[0].pos),
+                 "r"(prm.job[0].kv_dtype), "l"(prm.job[1].x), "l"(prm.job[1].pos),
+                 "r"(prm.job[1].kv_dtype), "l"(prm.dev_err), "l"(prm.trace));
     if (tid == 0) {
         asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"(smem_u32(&s_bar)));
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         const uint32_t b1n = mlp ? d * hs * 4 : 0, b2n = Wc * act_dim * 32 * 4;
+        const uint32_t bbn = mlp ? hs * 4 : 0;  // this CTA's slice of b1
         asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
-                     :: "r"(smem_u32(&s_bar)), "r"(b1n + b2n) : "memory");
-        if (mlp)
+                     :: "r"(smem_u32(&s_bar)), "r"(b1n + b2n + bbn) : "memory");
+        if (mlp) {
             bulk_g2s(sw1, prm.w1s + ((size_t)head * kCS + rank) * d * hs, b1n, &s_bar);
+            bulk_g2s(sb1, prm.b1 + (size_t)head * h + rank * hs, bbn, &s_bar);
+        }
         bulk_g2s(sw2, prm.w2w + ((size_t)head * W + rank * Wc) * act_dim * 32, b2n, &s_bar);
     }
     // the weights stream in while the previous kernel of the stream finishes;
     // inputs, caches and code rows are touched only after it has completed
     pdl_wait();
     cluster_sync_relaxed();  // peers' shared memory is live before any DSMEM store
+    K1_STAMP(1);
     uint32_t a1_peer[kCS];
 #pragma unroll
     for (int r = 0; r < kCS; ++r)
@@ -340,11 +443,22 @@ __global__ void __cluster_dims__(kCS, 1, 1) __launch_bounds__(kEncThreads)
             }
             xs[i] = val;
         }
+        // V rows and append slots: asynchronous copies, waited for only after
+        // layer 1 (a cold load here would sit on the critical path)
+        if (stage_v)
+            for (uint32_t i = tid; i < nv * d / 4; i += kEncThreads) {
+                const uint32_t v = (4 * i) / d, c = (4 * i) % d;
+                cp_async16(vs + 4 * i, job.v_new + (((uint64_t)(v0 + v)) * H + head) * d + c);
+            }
+        if (job.out_mode == ENC_APPEND && tid < (int)nv) cp_async4(s_pos + tid, job.pos + v0 + tid);
+        asm volatile("cp.async.commit_group;" ::: "memory");
+        K1_STAMP(2);
         if (!ready) {
             wait_parity0(&s_bar);
             ready = true;
         }
         __syncthreads();
+        K1_STAMP(3);
         if (s_bad && tid == 0 && rank == 0) raise_dev_err(prm.dev_err, SPL_DEV_ERR_NUMERIC);
 
         // warp w handles vectors w and w + 4 (warp-uniform guards)
@@ -355,25 +469,13 @@ __global__ void __cluster_dims__(kCS, 1, 1) __launch_bounds__(kEncThreads)
                 const uint32_t jl = jb + lane;
                 float acc0 = 0.0f, acc1 = 0.0f;
                 if (va < nv) {
-                    for (uint32_t p = 0; p < d; p += 4) {
-                        const float4 xa = *reinterpret_cast<const float4*>(xs + va * d + p);
-                        const float w0 = sw1[(p + 0) * hs + jl], w1v = sw1[(p + 1) * hs + jl];
-                        const float w2v = sw1[(p + 2) * hs + jl], w3 = sw1[(p + 3) * hs + jl];
-                        acc0 = __fmaf_rn(xa.x, w0, acc0);
-                        acc0 = __fmaf_rn(xa.y, w1v, acc0);
-                        acc0 = __fmaf_rn(xa.z, w2v, acc0);
-                        acc0 = __fmaf_rn(xa.w, w3, acc0);
-                        if (vb < nv) {
-                            const float4 xb = *reinterpret_cast<const float4*>(xs + vb * d + p);
-                            acc1 = __fmaf_rn(xb.x, w0, acc1);
-                            acc1 = __fmaf_rn(xb.y, w1v, acc1);
-                            acc1 = __fmaf_rn(xb.z, w2v, acc1);
-                            acc1 = __fmaf_rn(xb.w, w3, acc1);
-                        }
-                    }
+                    fma_chain2<DN>(xs + va * d, xs + vb * d, vb < nv, sw1 + (size_t)jl * d, d, lane, acc0,
+                                   acc1);
+                    K1_STAMP(8);
                     const uint32_t j = rank * hs + jl;
-                    const float bj = __ldg(prm.b1 + (size_t)head * h + j);
+                    const float bj = sb1[jl];
                     const float ya = silu_exact(__fadd_rn(acc0, bj));
+                    K1_STAMP(9);
 #pragma unroll
                     for (int r = 0; r < kCS; ++r)
                         asm volatile("st.shared::cluster.f32 [%0], %1;"
@@ -387,8 +489,14 @@ __global__ void __cluster_dims__(kCS, 1, 1) __launch_bounds__(kEncThreads)
                     }
                 }
             }
-            cluster_sync_all();  // every CTA now holds all h hidden units
+            K1_STAMP(4);
+            asm volatile("cp.async.wait_all;" ::: "memory");
+            cluster_sync_all();  // every CTA now holds all h hidden units (and the copies landed)
+            K1_STAMP(5);
             act = a1;
+        } else {
+            asm volatile("cp.async.wait_all;" ::: "memory");
+            __syncthreads();
         }
 
         // layer 2: this CTA's Wc words; lane c computes column c*W + w
@@ -396,24 +504,10 @@ __global__ void __cluster_dims__(kCS, 1, 1) __launch_bounds__(kEncThreads)
             const uint32_t w = rank * Wc + wl;
             const float* sw = sw2 + (size_t)wl * act_dim * 32;
             float acc0 = 0.0f, acc1 = 0.0f;
-            if (va < nv) {
-                for (uint32_t p = 0; p < act_dim; p += 4) {
-                    const float4 xa = *reinterpret_cast<const float4*>(act + va * act_dim + p);
-                    const float w0 = sw[(p + 0) * 32 + lane], w1v = sw[(p + 1) * 32 + lane];
-                    const float w2v = sw[(p + 2) * 32 + lane], w3 = sw[(p + 3) * 32 + lane];
-                    acc0 = __fmaf_rn(xa.x, w0, acc0);
-                    acc0 = __fmaf_rn(xa.y, w1v, acc0);
-                    acc0 = __fmaf_rn(xa.z, w2v, acc0);
-                    acc0 = __fmaf_rn(xa.w, w3, acc0);
-                    if (vb < nv) {
-                        const float4 xb = *reinterpret_cast<const float4*>(act + vb * act_dim + p);
-                        acc1 = __fmaf_rn(xb.x, w0, acc1);
-                        acc1 = __fmaf_rn(xb.y, w1v, acc1);
-                        acc1 = __fmaf_rn(xb.z, w2v, acc1);
-                        acc1 = __fmaf_rn(xb.w, w3, acc1);
-                    }
-                }
-            }
+            if (va < nv)
+                fma_chain2<DN>(act + va * act_dim, act + vb * act_dim, vb < nv, sw + (size_t)lane * act_dim,
+                               act_dim, lane, acc0, acc1);
+            K1_STAMP(10);
             const uint32_t col = lane * W + w;
 #pragma unroll
             for (int s2 = 0; s2 < 2; ++s2) {
@@ -428,7 +522,7 @@ __global__ void __cluster_dims__(kCS, 1, 1) __launch_bounds__(kEncThreads)
                     if (lane == 0) {
                         uint64_t row;
                         if (job.out_mode == ENC_APPEND) {
-                            const uint64_t slot = append_slot(job, b, prm.dev_err, w == 0);
+                            const uint64_t slot = append_slot_at(job, s_pos[v], prm.dev_err, w == 0);
                             row = slot == ~0ull ? ~0ull : ((uint64_t)b * H + head) * job.cap + slot;
                         } else {
                             row = ((uint64_t)b * H + head) * job.m + mi;
@@ -439,16 +533,16 @@ __global__ void __cluster_dims__(kCS, 1, 1) __launch_bounds__(kEncThreads)
             }
         }
 
-        if (rank == 0 && job.out_mode == ENC_APPEND && job.kcache) {
+        K1_STAMP(6);
+        if (stage_v) {
             for (uint32_t i = tid; i < nv * d; i += kEncThreads) {
                 const uint32_t v = i / d, c = i % d;
                 const uint32_t b = v0 + v;  // m == 1
-                const uint64_t src = ((uint64_t)b * H + head) * d + c;
-                const uint64_t slot = append_slot(job, b, prm.dev_err, false);
+                const uint64_t slot = append_slot_at(job, s_pos[v], prm.dev_err, false);
                 if (slot == ~0ull) continue;
                 const uint64_t dst = (((uint64_t)b * H + head) * job.cap + slot) * d + c;
                 const float kv = xs[v * d + c];
-                const float vv = job.v_new[src];
+                const float vv = vs[v * d + c];
                 if (job.kv_dtype == SPL_BF16) {
                     static_cast<__nv_bfloat16*>(job.kcache)[dst] = __float2bfloat16_rn(kv);
                     static_cast<__nv_bfloat16*>(job.vcache)[dst] = __float2bfloat16_rn(vv);
@@ -461,6 +555,7 @@ __global__ void __cluster_dims__(kCS, 1, 1) __launch_bounds__(kEncThreads)
         cluster_sync_relaxed();  // peers finished reading a1 before the next tile rewrites it
     }
     if (!ready) wait_parity0(&s_bar);  // no tile: let the bulk copies land first
+    K1_STAMP(7);
 }
 
 bool cluster_eligible(const spl_hasher* hs) {
@@ -495,18 +590,50 @@ spl_status encode_cluster_launch(spl_ctx* ctx, const spl_hasher* hs, uint32_t B,
     const size_t act_dim = mlp ? hs->h : hs->d;
     const size_t smem = sizeof(float) * ((mlp ? (size_t)hs->d * (hs->h / kCS) : 0) +
                                          (size_t)(prm.W / kCS) * act_dim * 32 +
-                                         (size_t)kVT * hs->d + (size_t)kVT * (mlp ? hs->h : 0));
+                                         (size_t)kVT * hs->d + (size_t)kVT * hs->h + hs->h / kCS +
+                                         (size_t)kVT * hs->d);
     if (smem > 200 * 1024) return SPL_E_STATE;
-    SPL_CUDA_TRY(ctx, cudaFuncSetAttribute(k1_encode_cluster,
-                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    const void* fn = (hs->d == 128 && act_dim == 128)
+                         ? reinterpret_cast<const void*>(&k1_encode_cluster<128>)
+                         : reinterpret_cast<const void*>(&k1_encode_cluster<0>);
+    SPL_CUDA_TRY(ctx, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     const uint32_t ntiles = (nvec + kVT - 1) / kVT;
     const uint32_t groups = std::max<uint32_t>(
         1, std::min<uint32_t>(ntiles, (uint32_t)(2 * ctx->num_sms) / (kCS * hs->H)));
     dim3 grid(groups * kCS, hs->H, njobs);
+    // SPL_K1_TRACE=1 (eager calls only): per-CTA phase stamps, mean / max
+    // over CTAs printed to stderr — a measurement aid
+    const char* tr = getenv("SPL_K1_TRACE");
+    const size_t nct = (size_t)grid.x * grid.y * grid.z;
+    if (tr && *tr && !stream_capturing(s)) {
+        SPL_CUDA_TRY(ctx, cudaMalloc(&prm.trace, nct * 12 * 8));
+        SPL_CUDA_TRY(ctx, cudaMemsetAsync(prm.trace, 0, nct * 12 * 8, s));
+    }
     void* args[] = {&prm};
-    SPL_CUDA_TRY(ctx, launch_pdl(reinterpret_cast<const void*>(&k1_encode_cluster), grid,
-                                 dim3(kEncThreads), smem, s, args));
+    SPL_CUDA_TRY(ctx, launch_pdl(fn, grid, dim3(kEncThreads), smem, s, args));
+    if (prm.trace) {
+        std::vector<uint64_t> h(nct * 12);
+        cudaStreamSynchronize(s);
+        cudaMemcpy(h.data(), prm.trace, h.size() * 8, cudaMemcpyDeviceToHost);
+        cudaFree(prm.trace);
+        uint64_t t0 = ~0ull;
+        for (size_t i = 0; i < nct; ++i) t0 = std::min(t0, h[i * 12]);
+        double mean[12] = {0}, mx[12] = {0};
+        for (size_t i = 0; i < nct; ++i)
+            for (int j = 0; j < 11; ++j) {
+                const double v = h[i * 12 + j] ? (double)(h[i * 12 + j] - t0) / 1000.0 : 0.0;
+                mean[j] += v / nct;
+                mx[j] = std::max(mx[j], v);
+            }
+        fprintf(stderr, "k1 trace grid=%ux%ux%u [start synced staged weights l1 l1sync l2 end chain1 silu chain2] mean:",
+                grid.x, grid.y, grid.z);
+        for (int j = 0; j < 11; ++j) fprintf(stderr, " %.2f", mean[j]);
+        fprintf(stderr, "  max:");
+        for (int j = 0; j < 11; ++j) fprintf(stderr, " %.2f", mx[j]);
+        fprintf(stderr, " us\n");
+    }
     return after_launch(ctx, "k1_encode_cluster");
+
 }
 
 spl_status encode_exact_launch(spl_ctx* ctx, const spl_hasher* hs, uint32_t B,
@@ -558,7 +685,8 @@ spl_status encode_exact_launch(spl_ctx* ctx, const spl_hasher* hs, uint32_t B,
 void encode_preload() {
     cudaFuncAttributes a;
     cudaFuncGetAttributes(&a, reinterpret_cast<const void*>(&k1_encode_exact));
-    cudaFuncGetAttributes(&a, reinterpret_cast<const void*>(&k1_encode_cluster));
+    cudaFuncGetAttributes(&a, reinterpret_cast<const void*>(&k1_encode_cluster<0>));
+    cudaFuncGetAttributes(&a, reinterpret_cast<const void*>(&k1_encode_cluster<128>));
 }
 
 }  // namespace spl

@@ -81,8 +81,8 @@ struct spl_hasher {
     float* b1 = nullptr;  // [H][h]
     float* w2 = nullptr;  // [H][h][L]
     float* w2_perm = nullptr;  // layer 2 (linear: projection) columns permuted, see capi.cu
-    float* w1_slices = nullptr;  // [H][4][d][h/4] column quarters of W1 (cluster encoder)
-    float* w2_words = nullptr;   // [H][W][act_dim][32] word-major layer 2 (cluster encoder)
+    float* w1_slices = nullptr;  // [H][4][h/4][d] column quarters of W1, row per output (cluster encoder)
+    float* w2_words = nullptr;   // [H][W][32][act_dim] word-major layer 2, row per output (cluster encoder)
     // bf16 copies for the tcgen05 bulk encoder (K-major packing, see encode_tc.cu)
     void* w1_tc = nullptr;
     void* w2_tc = nullptr;

@@ -35,10 +35,14 @@ nv = torch.full((B,), n, dtype=torch.int32, device=dev)
 idx = torch.zeros((B * H, k), dtype=torch.int32, device=dev)
 cnt = torch.zeros(B * H, dtype=torch.int32, device=dev)
 out = torch.zeros((B, H, D), dtype=torch.float32, device=dev)
+q2 = torch.randn((B, H, D), generator=g, device=dev)
+qc2 = torch.zeros((B, H, L // 32), dtype=torch.int32, device=dev)
 flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
 for i in range(reps):
     flush.fill_(i)
     flush[: 256 << 20].view(torch.int32).sum()
+    if os.environ.get("IWARM"):  # instructions warm, data cold: a tiny encode through the same kernel
+        hs.encode(q2, B, 1, qc2)
     hs.decode_step(q, kn, vn, B, codes, kc, vc, capi.SPL_BF16, n, nv, n, k, float(1 / np.sqrt(D)),
                    idx, cnt, out)
     torch.cuda.synchronize()
