@@ -29,6 +29,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 
@@ -53,6 +54,7 @@ struct TcParams {
     uint32_t tiles_per_problem;
     uint64_t total_tiles;
     uint32_t* dev_err;
+    long long* trace;  // optional (SPL_K2_TRACE): CTA 0's per-tile role clocks [64][8]
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -508,6 +510,10 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
         : "memory");
 }
 
+#define K2T(i, k)                                                   \
+    if (prm.trace && blockIdx.x == 0 && (i) < 64 && (threadIdx.x & 31) == 0) \
+    prm.trace[(i) * 12 + (k)] = clock64()
+
 template <uint32_t W>
 __global__ void __launch_bounds__(kWsThreads, 1)
     k2_encode_ws(const __grid_constant__ CUtensorMap tmap, TcParams prm) {
@@ -558,9 +564,12 @@ __global__ void __launch_bounds__(kWsThreads, 1)
             // problem (consecutive problems have consecutive heads; H = 1
             // reloads the same head, harmless)
             auto g2 = [&](uint32_t j, bool ends_head) {
+                K2T(j, 2);
                 mbar_wait(&bar[kA1Full + (j & 1)], (j >> 1) & 1u);
+                K2T(j, 3);
                 if (j >= 1) mbar_wait(&bar[kD2Empty], (j - 1) & 1u);
                 fence_after();
+                K2T(j, 4);
                 gemm_k128(tmem + 256u, smem_u32(sA1 + (j & 1) * XB), smem_u32(sW2), L);
                 umma_commit(&bar[kA1Empty + (j & 1)]);
                 umma_commit(&bar[kD2Full]);
@@ -577,9 +586,11 @@ __global__ void __launch_bounds__(kWsThreads, 1)
                     mbar_wait(&bar[kWFull], nw & 1u);
                     ++nw;
                 }
+                K2T(i, 0);
                 mbar_wait(&bar[kXFull + (i & 1)], (i >> 1) & 1u);
                 if (i >= 2) mbar_wait(&bar[kD1Empty + (i & 1)], ((i - 2) >> 1) & 1u);
                 fence_after();
+                K2T(i, 1);
                 gemm_k128(tmem + (i & 1) * 128u, smem_u32(sX + (i & 1) * XB), smem_u32(sW1), kTcK);
                 umma_commit(&bar[kXEmpty + (i & 1)]);
                 umma_commit(&bar[kD1Full + (i & 1)]);
@@ -607,9 +618,12 @@ __global__ void __launch_bounds__(kWsThreads, 1)
                     bulk_g2s(sW2, prm.w2_tc + (uint64_t)h * L * 256u, L * 256u, &bar[kWFull]);
                     ++nw;
                 }
+                K2T(i, 8);
                 if (i >= 2) mbar_wait_sleep(&bar[kXEmpty + (i & 1)], ((i - 2) >> 1) & 1u);
+                K2T(i, 9);
                 tma_x(&tmap, sX + (i & 1) * XB, &bar[kXFull + (i & 1)],
                       pos.bh * prm.m + (uint64_t)pos.mb * kTcTileM);
+
                 prev_ends = pos.last_of_head();
                 pos.advance();
             }
@@ -633,6 +647,7 @@ __global__ void __launch_bounds__(kWsThreads, 1)
             mbar_wait_sleep(&bar[kD1Full + (i & 1)], (i >> 1) & 1u);
             if (i >= 2) mbar_wait_sleep(&bar[kA1Empty + (i & 1)], ((i - 2) >> 1) & 1u);
             fence_after();
+            if (warp == 2) K2T(i, 5);
             // this thread's half row of A1: K block ch (64 columns), row `row`;
             // 16-byte chunk j of the row sits at chunk j ^ (row % 8)
             uint8_t* a1row = sA1 + (i & 1) * XB + ch * (kTcTileM * 128u) + row * 128u;
@@ -676,6 +691,7 @@ __global__ void __launch_bounds__(kWsThreads, 1)
             mbar_arrive(&bar[kD1Empty + (i & 1)]);
             fence_async_smem();
             mbar_arrive(&bar[kA1Full + (i & 1)]);
+            if (warp == 2) K2T(i, 6);
         }
     } else {
         // ------------------------------------------------ epilogue 2
@@ -687,6 +703,7 @@ __global__ void __launch_bounds__(kWsThreads, 1)
             const uint32_t grow = pos.mb * kTcTileM + row;
             mbar_wait_sleep(&bar[kD2Full], i & 1u);
             fence_after();
+            if (warp == 10) K2T(i, 7);
             // column j -> word j % W, bit 31 - j / W: feeding the sign bits of
             // columns w, w + W, w + 2W, ... into word w with a funnel shift
             // puts column w + W*b at bit 31 - b. Raw sign bits (see sign_half
@@ -825,8 +842,30 @@ spl_status encode_tc_launch(spl_ctx* ctx, const spl_hasher* hs, const void* x, i
         const size_t wsmem = 1024 + 5 * (size_t)tc_operand_bytes(kTcTileM) + (size_t)prm.L * 256u;
         const void* wfn = k2_ws_fn(prm.W);
         SPL_CUDA_TRY(ctx, cudaFuncSetAttribute(wfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wsmem));
+        const char* tr = getenv("SPL_K2_TRACE");
+        if (tr && *tr && !stream_capturing(s)) {
+            SPL_CUDA_TRY(ctx, cudaMalloc(&prm.trace, 64 * 12 * 8));
+            SPL_CUDA_TRY(ctx, cudaMemsetAsync(prm.trace, 0, 64 * 12 * 8, s));
+        }
         void* wargs[] = {&tmap, &prm};
         SPL_CUDA_TRY(ctx, cudaLaunchKernel(wfn, dim3((uint32_t)G), dim3(kWsThreads), wargs, wsmem, s));
+        if (prm.trace) {
+            // per-tile role clocks of CTA 0, relative to tile 8's GEMM1 wait (a
+            // measurement aid): mma-wait-X, G1 issue, G2 wait-A1, G2 wait-D2, G2
+            // issue, epi1 start, epi1 done, epi2 start
+            long long h[64 * 12];
+            cudaStreamSynchronize(s);
+            cudaMemcpy(h, prm.trace, sizeof(h), cudaMemcpyDeviceToHost);
+            cudaFree(prm.trace);
+            const long long b = h[8 * 12];
+            fprintf(stderr, "k2 trace (cycles, tile: x-wait g1 g2-a1wait g2-d2wait g2 e1start e1done e2start prod-wait prod-tma)\n");
+            for (int i = 8; i < 24; ++i) {
+                fprintf(stderr, "  %2d:", i);
+                for (int k = 0; k < 10; ++k) fprintf(stderr, " %7lld", h[i * 12 + k] ? h[i * 12 + k] - b : -1);
+                fprintf(stderr, "\n");
+            }
+            fprintf(stderr, "  period over tiles 8..56: %.0f cycles/tile\n", (double)(h[56 * 12 + 1] - h[8 * 12 + 1]) / 48);
+        }
         return after_launch(ctx, "k2_encode_ws");
     }
     const void* fn = prm.x_bf16 ? k2_fn<true>(prm.W) : k2_fn<false>(prm.W);
