@@ -675,10 +675,14 @@ def bench_prefill(torch, capi, ctx, dev, stream, args):
 
     for _ in range(args.warmup):
         step()
-    steps = min(args.steps, 10)
+    steps = max(3, min(args.steps, 40))
+    clk = ClockSampler(torch.cuda.current_device())
+    clk.start()
+    time.sleep(0.3)
     l0 = ctx.launches()
     ms = event_timer(torch, step, steps, stream)
     launches = (ctx.launches() - l0) / steps
+    clocks = clk.stop()
     keys = B * H * n
     flops = keys * (2 * D * D + 2 * D * L4)
     nbytes = keys * D * 2 + keys * (L4 // 32) * 4 + H * (D * D + D * L4) * 2
@@ -692,6 +696,7 @@ def bench_prefill(torch, capi, ctx, dev, stream, args):
                         "(K2 tcgen05, bf16 operands, fp32 TMEM accumulation)",
             "ms_per_step": round(ms, 3), "keys_per_s": round(keys / (ms * 1e-3) / 1e9, 3),
             "unit_keys": "G keys/s", "gpu_launches_per_step": launches,
+            "clocks": clocks, "steps_timed": steps,
             "roofline": {"tensor": {"achieved": round(tf, 1), "unit": "TFLOP/s", "peak": burst,
                                     "peak_kind": f"{kind} burst", "frac": round(tf / burst, 4),
                                     "frac_of_sustained": round(tf / sustained, 4),

@@ -54,7 +54,8 @@ struct TcParams {
     uint32_t tiles_per_problem;
     uint64_t total_tiles;
     uint32_t* dev_err;
-    long long* trace;  // optional (SPL_K2_TRACE): CTA 0's per-tile role clocks [64][8]
+    long long* trace;  // optional (SPL_K2_TRACE=<first tile>): CTA 0's per-tile role clocks [64][12]
+    uint32_t trace_from;
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -87,6 +88,30 @@ __device__ __forceinline__ void gemm_k128(uint32_t tmem_d, uint32_t sa, uint32_t
         const uint64_t db = umma_desc(sb + (s >> 2) * N * 128u + (s & 3u) * 32u);
         umma_bf16(tmem_d, da, db, idesc, s > 0 ? 1u : 0u);
     }
+}
+// D[128 x N] = A[128 x 128] . B[N x 128]^T with A in TMEM (row r = lane r,
+// k-step s = 16 bf16 = columns [8s, 8s + 8), element 2c in the low half of
+// column c) and B in shared memory as in gemm_k128
+__device__ __forceinline__ void gemm_k128_ta(uint32_t tmem_d, uint32_t tmem_a, uint32_t sb, uint32_t N) {
+    const uint32_t idesc = umma_idesc(N);
+#pragma unroll
+    for (uint32_t s = 0; s < kTcK / 16; ++s) {
+        const uint64_t db = umma_desc(sb + (s >> 2) * N * 128u + (s & 3u) * 32u);
+        asm volatile(
+            "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+            "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+            "r"(tmem_a + 8u * s), "l"(db), "r"(idesc), "r"(s > 0 ? 1u : 0u));
+    }
+}
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&r)[32]) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+        "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+        "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]),
+        "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]),
+        "r"(r[17]), "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]),
+        "r"(r[25]), "r"(r[26]), "r"(r[27]), "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
+        : "memory");
 }
 __device__ __forceinline__ void umma_commit(uint64_t* bar) {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
@@ -485,13 +510,12 @@ struct TilePos {
     }
     __device__ __forceinline__ bool last_of_head() const { return mb + 1 == tpp; }
 };
+constexpr uint32_t kXSlots = 4;  // X ring depth (A1 lives in TMEM: its 64 KB went to X)
 enum WsBar {
-    kXFull = 0,      // [2] producer -> MMA (TMA tx)
-    kXEmpty = 2,     // [2] GEMM1 done reading X
-    kD1Full = 4,     // [2] GEMM1 done -> epilogue 1
-    kD1Empty = 6,    // [2] epilogue 1 drained D1 (256 arrivals)
-    kA1Full = 8,     // [2] epilogue 1 wrote A1 (256 arrivals)
-    kA1Empty = 10,   // [2] GEMM2 done reading A1
+    kXFull = 0,      // [4] producer -> MMA (TMA tx)
+    kXEmpty = 4,     // [4] GEMM1 done reading X
+    kD1Full = 8,     // [2] GEMM1 done -> epilogue 1
+    kA1Full = 10,    // [2] epilogue 1 wrote A1 into the D1 slot (256 arrivals)
     kD2Full = 12,    // GEMM2 done -> epilogue 2
     kD2Empty = 13,   // epilogue 2 drained D2 (128 arrivals)
     kWFull = 14,     // head weights landed (bulk tx)
@@ -510,9 +534,10 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
         : "memory");
 }
 
-#define K2T(i, k)                                                   \
-    if (prm.trace && blockIdx.x == 0 && (i) < 64 && (threadIdx.x & 31) == 0) \
-    prm.trace[(i) * 12 + (k)] = clock64()
+#define K2T(i, k)                                                                      \
+    if (prm.trace && blockIdx.x == 0 && (i) >= prm.trace_from && (i) < prm.trace_from + 64 && \
+        (threadIdx.x & 31) == 0)                                                           \
+    prm.trace[((i) - prm.trace_from) * 12 + (k)] = clock64()
 
 template <uint32_t W>
 __global__ void __launch_bounds__(kWsThreads, 1)
@@ -526,9 +551,8 @@ __global__ void __launch_bounds__(kWsThreads, 1)
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint32_t base_s = (smem_u32(smem_raw) + 1023u) & ~1023u;
     uint8_t* base = smem_raw + (base_s - smem_u32(smem_raw));
-    uint8_t* sX = base;             // 2 slots
-    uint8_t* sA1 = sX + 2 * XB;     // 2 slots
-    uint8_t* sW1 = sA1 + 2 * XB;
+    uint8_t* sX = base;             // kXSlots slots
+    uint8_t* sW1 = sX + kXSlots * XB;
     uint8_t* sW2 = sW1 + XB;
 
     const uint64_t T = prm.total_tiles;
@@ -544,7 +568,7 @@ __global__ void __launch_bounds__(kWsThreads, 1)
     }
     if (tid == 32) {
         for (int i = 0; i < kWsBars; ++i) {
-            const bool e1 = (i >= kD1Empty && i < kD1Empty + 2) || (i >= kA1Full && i < kA1Full + 2);
+            const bool e1 = i >= kA1Full && i < kA1Full + 2;
             asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&bar[i])),
                          "r"(e1 ? kEpi1Threads : i == kD2Empty ? 128u : 1u));
         }
@@ -570,8 +594,9 @@ __global__ void __launch_bounds__(kWsThreads, 1)
                 if (j >= 1) mbar_wait(&bar[kD2Empty], (j - 1) & 1u);
                 fence_after();
                 K2T(j, 4);
-                gemm_k128(tmem + 256u, smem_u32(sA1 + (j & 1) * XB), smem_u32(sW2), L);
-                umma_commit(&bar[kA1Empty + (j & 1)]);
+                // A1(j) in TMEM, in the D1 slot it was computed from; GEMM1(j + 2)
+                // reuses the slot only after this GEMM2 (tcgen05.mma runs in issue order)
+                gemm_k128_ta(tmem + 256u, tmem + (j & 1) * 128u, smem_u32(sW2), L);
                 umma_commit(&bar[kD2Full]);
                 if (j + 1 < n && ends_head) umma_commit(&bar[kWEmpty]);
             };
@@ -587,12 +612,12 @@ __global__ void __launch_bounds__(kWsThreads, 1)
                     ++nw;
                 }
                 K2T(i, 0);
-                mbar_wait(&bar[kXFull + (i & 1)], (i >> 1) & 1u);
-                if (i >= 2) mbar_wait(&bar[kD1Empty + (i & 1)], ((i - 2) >> 1) & 1u);
+                const uint32_t xs = i % kXSlots;
+                mbar_wait(&bar[kXFull + xs], (i / kXSlots) & 1u);
                 fence_after();
                 K2T(i, 1);
-                gemm_k128(tmem + (i & 1) * 128u, smem_u32(sX + (i & 1) * XB), smem_u32(sW1), kTcK);
-                umma_commit(&bar[kXEmpty + (i & 1)]);
+                gemm_k128(tmem + (i & 1) * 128u, smem_u32(sX + xs * XB), smem_u32(sW1), kTcK);
+                umma_commit(&bar[kXEmpty + xs]);
                 umma_commit(&bar[kD1Full + (i & 1)]);
                 if (i >= 1 && !newhead) g2(i - 1, false);
                 prev_ends = pos.last_of_head();
@@ -619,10 +644,10 @@ __global__ void __launch_bounds__(kWsThreads, 1)
                     ++nw;
                 }
                 K2T(i, 8);
-                if (i >= 2) mbar_wait_sleep(&bar[kXEmpty + (i & 1)], ((i - 2) >> 1) & 1u);
+                const uint32_t xs = i % kXSlots;
+                if (i >= kXSlots) mbar_wait_sleep(&bar[kXEmpty + xs], ((i - kXSlots) / kXSlots) & 1u);
                 K2T(i, 9);
-                tma_x(&tmap, sX + (i & 1) * XB, &bar[kXFull + (i & 1)],
-                      pos.bh * prm.m + (uint64_t)pos.mb * kTcTileM);
+                tma_x(&tmap, sX + xs * XB, &bar[kXFull + xs], pos.bh * prm.m + (uint64_t)pos.mb * kTcTileM);
 
                 prev_ends = pos.last_of_head();
                 pos.advance();
@@ -630,11 +655,10 @@ __global__ void __launch_bounds__(kWsThreads, 1)
         }
     } else if (warp < 10) {
         // ------------------------------------------------ epilogue 1
-        const uint32_t q = (uint32_t)(warp & 3), row = q * 32 + lane;
+        const uint32_t q = (uint32_t)(warp & 3);
         const uint32_t ch = (uint32_t)(warp - 2) >> 2;  // column half
         const uint32_t lane_addr = (q * 32) << 16;
         const int et = tid - 64;  // 0..255 within the group
-        const uint32_t r7 = row & 7u;
         TilePos pos(t0, tpp, prm.H);
         uint32_t cur_head = ~0u;
         for (uint32_t i = 0; i < n; ++i, pos.advance()) {
@@ -645,17 +669,23 @@ __global__ void __launch_bounds__(kWsThreads, 1)
                 cur_head = pos.head;
             }
             mbar_wait_sleep(&bar[kD1Full + (i & 1)], (i >> 1) & 1u);
-            if (i >= 2) mbar_wait_sleep(&bar[kA1Empty + (i & 1)], ((i - 2) >> 1) & 1u);
             fence_after();
             if (warp == 2) K2T(i, 5);
-            // this thread's half row of A1: K block ch (64 columns), row `row`;
-            // 16-byte chunk j of the row sits at chunk j ^ (row % 8)
-            uint8_t* a1row = sA1 + (i & 1) * XB + ch * (kTcTileM * 128u) + row * 128u;
-            const uint32_t tD = tmem + (i & 1) * 128u + lane_addr + ch * 64u;
+            // this thread's half row of D1 (64 columns) -> SiLU -> bf16 pairs
+            // -> A1 columns [32 ch, 32 ch + 32) of the same TMEM slot (k-major
+            // A operand of GEMM2: unit j at column j / 2, half j % 2)
+            const uint32_t tS = tmem + (i & 1) * 128u + lane_addr;
+            const uint32_t tD = tS + ch * 64u;
             uint32_t rr[2][32];
             tmem_ld32_nowait(tD, rr[0]);
             tmem_ld32_nowait(tD + 32, rr[1]);
             tmem_wait_ld();
+            // both column halves of the quarter have their D1 values in
+            // registers before either overwrites part of D1 with A1
+            fence_before();
+            asm volatile("bar.sync 1, 256;" ::: "memory");
+            fence_after();
+            uint32_t pk[32];
 #pragma unroll
             for (uint32_t c0 = 0; c0 < 64; c0 += 32) {
                 uint32_t (&r)[32] = rr[c0 >> 5];
@@ -668,7 +698,6 @@ __global__ void __launch_bounds__(kWsThreads, 1)
                         const float4 x = bp[v];
                         hb[4 * v] = x.x; hb[4 * v + 1] = x.y; hb[4 * v + 2] = x.z; hb[4 * v + 3] = x.w;
                     }
-                    uint32_t pk[8];
 #pragma unroll
                     for (int e = 0; e < 16; e += 2) {
                         // SiLU(z) = h (1 + tanh h), h = z / 2 = acc / 2 + b1 / 2
@@ -680,16 +709,13 @@ __global__ void __launch_bounds__(kWsThreads, 1)
                             asm("tanh.approx.f32 %0, %1;" : "=f"(t) : "f"(hv));
                             a[u] = fmaf(hv, t, hv);
                         }
-                        pk[e / 2] = pack_bf16(a[0], a[1]);
+                        pk[(c0 + 16 * hh + e) / 2] = pack_bf16(a[0], a[1]);
                     }
-                    const uint32_t j = (c0 + 16 * hh) >> 3;  // chunk index in the K block
-                    *reinterpret_cast<uint4*>(a1row + (((j) ^ r7) << 4)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
-                    *reinterpret_cast<uint4*>(a1row + (((j + 1) ^ r7) << 4)) = make_uint4(pk[4], pk[5], pk[6], pk[7]);
                 }
             }
+            tmem_st32(tS + ch * 32u, pk);
+            asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
             fence_before();
-            mbar_arrive(&bar[kD1Empty + (i & 1)]);
-            fence_async_smem();
             mbar_arrive(&bar[kA1Full + (i & 1)]);
             if (warp == 2) K2T(i, 6);
         }
@@ -839,11 +865,12 @@ spl_status encode_tc_launch(spl_ctx* ctx, const spl_hasher* hs, const void* x, i
     // warp-specialised kernel (SPL_K2_WS=0 forces the single-team kernel)
     const char* ws_env = getenv("SPL_K2_WS");
     if (prm.x_bf16 && !prm.linear && !pre && !(ws_env && *ws_env == '0')) {
-        const size_t wsmem = 1024 + 5 * (size_t)tc_operand_bytes(kTcTileM) + (size_t)prm.L * 256u;
+        const size_t wsmem = 1024 + (kXSlots + 1) * (size_t)tc_operand_bytes(kTcTileM) + (size_t)prm.L * 256u;
         const void* wfn = k2_ws_fn(prm.W);
         SPL_CUDA_TRY(ctx, cudaFuncSetAttribute(wfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wsmem));
         const char* tr = getenv("SPL_K2_TRACE");
         if (tr && *tr && !stream_capturing(s)) {
+            prm.trace_from = (uint32_t)atoi(tr);
             SPL_CUDA_TRY(ctx, cudaMalloc(&prm.trace, 64 * 12 * 8));
             SPL_CUDA_TRY(ctx, cudaMemsetAsync(prm.trace, 0, 64 * 12 * 8, s));
         }
