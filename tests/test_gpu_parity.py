@@ -322,6 +322,40 @@ def test_encode_exact_multihead_vs_oracle(ctx, oracle, ref):
             assert np.array_equal(got[b, hd], want)
 
 
+@pytest.mark.parametrize("d,h,L", [(64, 256, 128), (96, 128, 256), (128, 384, 128), (36, 128, 128)])
+def test_encode_exact_cluster_generic_dims(ctx, oracle, ref, d, h, L):
+    """The cluster encoder's runtime-length path (d or h != 128): lane-major
+    rotated weight rows (spl_hasher_create) for other row lengths, incl. a
+    chunk count (d / 4 = 9) that does not divide 32 — codes bit-exact."""
+    rng = np.random.default_rng(23 + d + h)
+    H, B, m = 2, 2, 9
+    ws = [ref.mlp_gaussian_init(d, h, L, 64.0, ref.derive_seed(3, i)) for i in range(H)]
+    w1 = np.stack([w[0] for w in ws])
+    b1 = np.stack([rng.standard_normal(h).astype(np.float32) * 0.1 for _ in ws])
+    w2 = np.stack([w[2] for w in ws])
+    x = rng.standard_normal((B, H, m, d)).astype(np.float32)
+    hs = ctx.hasher(w1, b1, w2)
+    codes = torch.zeros((B, H, m, L // 32), dtype=torch.int32, device=DEV)
+    hs.encode(T(x), B, m, codes)
+    got = U(codes)
+    for b in range(B):
+        for hd in range(H):
+            assert np.array_equal(got[b, hd], oracle.mlp_hash_packed(w1[hd], b1[hd], w2[hd], x[b, hd]))
+
+
+def test_encode_linear_d128(ctx, oracle, ref):
+    """Linear hasher with d = 128: the cluster encoder's unrolled (DN = 128)
+    layer with the projection as its only layer."""
+    rng = np.random.default_rng(24)
+    proj = np.stack([ref.qr_rotation_init(128, 7 + i) for i in range(2)])
+    x = rng.standard_normal((1, 2, 17, 128)).astype(np.float32)
+    hs = ctx.hasher(proj, kind=capi.SPL_HASHER_LINEAR)
+    codes = torch.zeros((1, 2, 17, 4), dtype=torch.int32, device=DEV)
+    hs.encode(T(x), 1, 17, codes)
+    for hd in range(2):
+        assert np.array_equal(U(codes)[0, hd], oracle.linear_hash_packed(proj[hd], x[0, hd]))
+
+
 def test_encode_linear(ctx, oracle, ref):
     rng = np.random.default_rng(22)
     proj = np.stack([ref.qr_rotation_init(64, 5 + i) for i in range(2)])
