@@ -11,7 +11,7 @@ fname = "?"
 hdr = None
 agg = defaultdict(lambda: [0, 0, "", defaultdict(int)])
 for r in rows:
-    if len(r) == 2 and r[0] == "File Name":
+    if len(r) == 2 and r[0] in ("File Name", "File Path"):
         fname = r[1].split("/")[-1]
         continue
     if r and r[0] == "Line No":
