@@ -275,6 +275,10 @@ __device__ __forceinline__ uint64_t k1_gtimer() {
     prm.trace[(((uint64_t)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x) * 12 + (i)] = \
         k1_gtimer()
 
+// bar.warp.sync the compiler cannot drop: lanes that took different paths
+// (lane-0 stores, per-lane loop trip counts) meet before an aligned barrier
+__device__ __forceinline__ void warp_converge() { asm volatile("bar.warp.sync 0xffffffff;" ::: "memory"); }
+
 __device__ __forceinline__ void cluster_sync_all() {
     asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;"
                  ::: "memory");
@@ -432,6 +436,7 @@ __global__ void __cluster_dims__(kCS, 1, 1) __launch_bounds__(kEncThreads)
         const uint32_t v0 = tile * kVT;
         const uint32_t nv = min((uint32_t)kVT, nvec - v0);
         if (tid == 0) s_bad = 0;
+        warp_converge();  // each warp converged at the block barrier (compute-sanitizer synccheck)
         __syncthreads();
         for (uint32_t i = tid; i < kVT * d; i += kEncThreads) {
             const uint32_t v = i / d, c = i % d;
@@ -457,6 +462,7 @@ __global__ void __cluster_dims__(kCS, 1, 1) __launch_bounds__(kEncThreads)
             wait_parity0(&s_bar);
             ready = true;
         }
+        warp_converge();
         __syncthreads();
         K1_STAMP(3);
         if (s_bad && tid == 0 && rank == 0) raise_dev_err(prm.dev_err, SPL_DEV_ERR_NUMERIC);
@@ -491,6 +497,7 @@ __global__ void __cluster_dims__(kCS, 1, 1) __launch_bounds__(kEncThreads)
             }
             K1_STAMP(4);
             asm volatile("cp.async.wait_all;" ::: "memory");
+            warp_converge();
             cluster_sync_all();  // every CTA now holds all h hidden units (and the copies landed)
             K1_STAMP(5);
             act = a1;
@@ -552,6 +559,7 @@ __global__ void __cluster_dims__(kCS, 1, 1) __launch_bounds__(kEncThreads)
                 }
             }
         }
+        warp_converge();
         cluster_sync_relaxed();  // peers finished reading a1 before the next tile rewrites it
     }
     if (!ready) wait_parity0(&s_bar);  // no tile: let the bulk copies land first
