@@ -140,3 +140,42 @@ def two_stream(steps=50):
 
 
 print(f"pipelined (2 streams)    {two_stream():7.2f} us")
+
+
+# variant: graph i = retrieval(i) ‖ [D2H(i-1)] ‖ [H2D(i+1) -> encode(i+1)]
+# (double-buffered query vectors / codes / indices): the next query's encode
+# runs on the SMs the retrieval's last CTAs leave free
+qd = [torch.empty((1, P, D), device=dev) for _ in range(2)]
+qcs = [torch.zeros((1, P, L // 32), dtype=torch.int32, device=dev) for _ in range(2)]
+cs2 = torch.cuda.Stream()
+
+
+def pipe3(b):
+    def body():
+        fork = torch.cuda.Event()
+        fork.record(gs)
+        cps.wait_event(fork)
+        cs2.wait_event(fork)
+        with torch.cuda.stream(cps):
+            d2h(1 - b)
+        with torch.cuda.stream(cs2):
+            qd[1 - b].copy_(q_host, non_blocking=True)
+            hs.encode(qd[1 - b], 1, 1, qcs[1 - b], capi.SPL_ENCODE_EXACT, cs2)
+        ctx.hamming_topk(codes, n, L, qcs[b], P, nv, 1, n, k, idx[b], cnt[b], gs)
+        j1, j2 = torch.cuda.Event(), torch.cuda.Event()
+        j1.record(cps)
+        j2.record(cs2)
+        gs.wait_event(j1)
+        gs.wait_event(j2)
+    return body
+
+
+def prologue():
+    qd[0].copy_(q_host, non_blocking=True)
+    hs.encode(qd[0], 1, 1, qcs[0], capi.SPL_ENCODE_EXACT)
+
+
+prologue()
+torch.cuda.synchronize()
+p3 = [capture(pipe3(0)), capture(pipe3(1))]
+print(f"pipelined (D2H and next encode in parallel) {timeit(p3, tail=lambda: d2h(1)):7.2f} us")
