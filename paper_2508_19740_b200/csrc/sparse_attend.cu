@@ -429,7 +429,7 @@ __global__ void k5_combine(const float* partials, uint32_t R, uint32_t P, uint32
 namespace {
 
 // SPL_K4=lane selects the round-1 lane-per-row kernel (A/B measurements);
-// SPL_K4_NB=1|2|4 the batches per warp of the gather kernel.
+// SPL_K4_NB=1|2|4 the batches per warp of the gather kernel (default 4).
 int k4_mode() {
     static const int m = [] {
         const char* e = getenv("SPL_K4");
@@ -441,7 +441,7 @@ int k4_nb() {
     static const int nb = [] {
         const char* e = getenv("SPL_K4_NB");
         const int v = e ? atoi(e) : 0;
-        return (v == 1 || v == 2 || v == 4) ? v : 2;
+        return (v == 1 || v == 2 || v == 4) ? v : 4;  // 4: config-4 step 590 -> 570 us
     }();
     return nb;
 }
