@@ -112,9 +112,6 @@ struct K3Params {
                            // unsharded; sharded decode: the rank the new token went to
     uint32_t part_off;     // sharded decode: u32 offset of the partial-exchange area in
                            // every rank's peer buffer (after the histogram area)
-    int att_pf;            // 1: the select also prefetches the emitted rows into L2
-                           // (SPL_ATT_PF=1; measured no faster than without: the
-                           // gather is DRAM-bound either way)
     int att_pre;           // fused attention: each warp prefetches all its K / V rows
                            // into L2 before its batches (SPL_ATT_PRE=1; measured no
                            // faster: the prefetches are hints, many are dropped)
@@ -1609,7 +1606,7 @@ __global__ void __launch_bounds__(kThreads, 3) k3_fused(K3Params prm) {
                 uint32_t* o = prm.idx_out + (uint64_t)p * prm.idx_stride + off;
                 uint64_t* trp = prm.trace ? prm.trace + (uint64_t)blockIdx.x * 16 : nullptr;
                 const uint64_t pf_off = (uint64_t)p * prm.stride_rows * prm.pf_row_bytes;
-                const bool pf_emit = prm.pf_k && (!ATT || prm.att_pf == 1);
+                const bool pf_emit = prm.pf_k && !ATT;  // the decode step attends the rows itself
                 const char* pfk = pf_emit ? prm.pf_k + pf_off : nullptr;
                 const char* pfv = pf_emit ? prm.pf_v + pf_off : nullptr;
                 const uint8_t* sc8 = reinterpret_cast<const uint8_t*>(sc);
@@ -1926,12 +1923,14 @@ spl_status make_fused_plan(spl_ctx* ctx, uint32_t P, uint64_t n_max, uint32_t L,
             case 1: fn = shard ? fused_fn<1, uint8_t, true>() : fused_fn<1, uint8_t>(); break;
             case 2: fn = shard ? fused_fn<2, uint8_t, true>() : fused_fn<2, uint8_t>(); break;
             case 4:
+                // the decode-step kernels attend their rows themselves: no
+                // L2 prefetch in the select (PF = false keeps its loop small)
                 if (att == 1)
-                    fn = shard ? fused_fn<4, uint8_t, true, true, true, __nv_bfloat16>()
-                               : fused_fn<4, uint8_t, false, true, true, __nv_bfloat16>();
+                    fn = shard ? fused_fn<4, uint8_t, true, false, true, __nv_bfloat16>()
+                               : fused_fn<4, uint8_t, false, false, true, __nv_bfloat16>();
                 else if (att == 2)
-                    fn = shard ? fused_fn<4, uint8_t, true, true, true, float>()
-                               : fused_fn<4, uint8_t, false, true, true, float>();
+                    fn = shard ? fused_fn<4, uint8_t, true, false, true, float>()
+                               : fused_fn<4, uint8_t, false, false, true, float>();
                 else
                     fn = shard ? fused_fn<4, uint8_t, true>()
                                : (pf ? fused_fn<4, uint8_t, false, true>() : fused_fn<4, uint8_t>());
@@ -2357,10 +2356,6 @@ spl_status hamming_topk_attend_impl(spl_ctx* ctx, const uint32_t* codes, uint64_
         prm.epoch_ptr = peer->d_epoch;
         prm.out_offset = out_offset;
         prm.part_off = (uint32_t)xwords(peer->R, peer->Pmax, peer->Lmax + 2);
-    }
-    {
-        const char* e = getenv("SPL_ATT_PF");
-        prm.att_pf = (e && *e == '1') ? 1 : 0;
     }
     {
         const char* e = getenv("SPL_ATT_PRE");
