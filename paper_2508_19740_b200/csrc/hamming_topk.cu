@@ -112,9 +112,6 @@ struct K3Params {
                            // unsharded; sharded decode: the rank the new token went to
     uint32_t part_off;     // sharded decode: u32 offset of the partial-exchange area in
                            // every rank's peer buffer (after the histogram area)
-    int att_pre;           // fused attention: each warp prefetches all its K / V rows
-                           // into L2 before its batches (SPL_ATT_PRE=1; measured no
-                           // faster: the prefetches are hints, many are dropped)
 };
 
 constexpr int kThreads = 256;
@@ -1236,21 +1233,6 @@ __device__ void fused_attend(const K3Params& prm, uint32_t p, uint32_t seg, uint
     float m = -INFINITY, lsum = 0.0f, o[E];
 #pragma unroll
     for (int e = 0; e < E; ++e) o[e] = 0.0f;
-    if (prm.att_pre && j0 < j1) {
-        // ask L2 for every K and V row of this warp's entries first (one DRAM
-        // round trip for all of them), so the 8-row batches below hit L2
-        constexpr uint32_t kRowBytes = D * sizeof(KV);
-        for (uint32_t j = j0 + lane; j < j1; j += 32) {
-            const uint32_t id = j < count ? (smem_ids ? sids[j] : __ldcg(gids + j)) : extra;
-            const char* kr = reinterpret_cast<const char*>(kbase + (uint64_t)id * D);
-            const char* vr = reinterpret_cast<const char*>(vbase + (uint64_t)id * D);
-#pragma unroll
-            for (uint32_t b = 0; b < kRowBytes; b += 128) {
-                asm volatile("prefetch.global.L2 [%0];" ::"l"(kr + b));
-                asm volatile("prefetch.global.L2 [%0];" ::"l"(vr + b));
-            }
-        }
-    }
     if (j0 < j1) {
         if (smem_ids)
             warp_attend<E, KV, true>(kbase, vbase, sids, count, extra, j0, j1, qv, m, lsum, o);
@@ -2356,10 +2338,6 @@ spl_status hamming_topk_attend_impl(spl_ctx* ctx, const uint32_t* codes, uint64_
         prm.epoch_ptr = peer->d_epoch;
         prm.out_offset = out_offset;
         prm.part_off = (uint32_t)xwords(peer->R, peer->Pmax, peer->Lmax + 2);
-    }
-    {
-        const char* e = getenv("SPL_ATT_PRE");
-        prm.att_pre = (e && *e == '1') ? 1 : 0;
     }
     const char* tr = getenv("SPL_K3_TRACE");
     uint64_t* dtrace = nullptr;
