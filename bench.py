@@ -389,12 +389,21 @@ def main():
         # the NCCL flow for the timed run.
         retrieval = retrieval_nccl
         shard_path = "nccl (k3_scan + all-gather + k3_shard_plan + k3_select)"
+
+        def agree(flag):  # every rank takes the same branch
+            t = torch.tensor([1 if flag else 0], device=dev)
+            all_reduce_dev(t, dist.ReduceOp.MIN)
+            return int(t.item()) == 1
+
+        peer, err = None, None
         try:
             peer = ctx.peer(world, rank, P, L)
             handles = [None] * world
             dist.all_gather_object(handles, peer.ipc_handle())
             peer.open(handles)
-
+        except Exception as e:  # no IPC / peer access: keep the NCCL flow
+            err = str(e)[:60]
+        if agree(err is None):
             def retrieval_fused():
                 ctx.hamming_topk_sharded(peer, codes, n_local, L, qcodes, P, nvalid, 1, n_local, k,
                                          idx, cnt, off, stream)
@@ -402,20 +411,21 @@ def main():
             torch.cuda.synchronize()
             ref = (idx.clone(), cnt.clone(), off.clone())
             dist.barrier()
-            torch.cuda.synchronize()
-            retrieval_fused()
-            torch.cuda.synchronize()
-            ctx.check_device_error()
-            same = all(torch.equal(a, b) for a, b in zip(ref, (idx, cnt, off)))
-            ok = torch.tensor([1 if same else 0], device=dev)
-            all_reduce_dev(ok, dist.ReduceOp.MIN)
-            if int(ok.item()) == 1:
+            same = False
+            try:
+                retrieval_fused()
+                torch.cuda.synchronize()
+                ctx.check_device_error()
+                same = all(torch.equal(a, b) for a, b in zip(ref, (idx, cnt, off)))
+            except Exception as e:
+                err = str(e)[:60]
+            if agree(same):
                 retrieval = retrieval_fused
                 shard_path = "fused (one k3_fused<SHARD> per rank, in-kernel exchange over NVLink peer memory)"
             else:
-                shard_path = "nccl (fused path disagreed with it on this run)"
-        except Exception as e:  # no IPC / peer access: keep the NCCL flow
-            shard_path = f"nccl (fused path unavailable: {str(e)[:60]})"
+                shard_path = f"nccl (fused path {'failed: ' + err if err else 'disagreed with it on this run'})"
+        else:
+            shard_path = f"nccl (fused path unavailable: {err or 'on another rank'})"
 
     for _ in range(args.warmup):
         retrieval()
@@ -1154,14 +1164,33 @@ def bench_sharded_decode(torch, capi, ctx, dev, stream, args, world, rank, dist,
     out = torch.zeros((1, H, D), dtype=torch.float32, device=dev)
     scale = float(1 / np.sqrt(D))
     owner = rank == world - 1
-    peer = ctx.peer(world, rank, P, L)
-    if world == 1:
-        capi.Peer.connect_local(ctx, [peer])
-    else:
-        handles = [None] * world
-        dist.all_gather_object(handles, peer.ipc_handle())
-        peer.open(handles)
-    ctx.reserve(P, n, L, k, D)
+
+    def agree(ok):
+        """All ranks leave together: a failure on any rank (peer mapping,
+        device error) ends the leg on every rank instead of leaving the others
+        inside a collective."""
+        if not dist:
+            return ok
+        t = torch.tensor([1 if ok else 0], device=dev)
+        all_reduce_dev(t, dist.ReduceOp.MIN)
+        return int(t.item()) == 1
+
+    peer, err = None, None
+    try:
+        peer = ctx.peer(world, rank, P, L)
+        if world == 1:
+            capi.Peer.connect_local(ctx, [peer])
+        else:
+            handles = [None] * world
+            dist.all_gather_object(handles, peer.ipc_handle())
+            peer.open(handles)
+        ctx.reserve(P, n, L, k, D)
+    except Exception as e:  # e.g. no CUDA IPC / peer access between these GPUs
+        err = f"peer setup: {str(e)[:120]}"
+    if not agree(err is None):
+        if peer is not None:
+            peer.close()
+        return {"workload": f"config5 over {world} GPU(s)", "error": err or "peer setup failed on another rank"}
     # the step appends at n_valid - 1: keep the cache length fixed across the
     # timed steps (each step rewrites the same slot), as a decode loop at a
     # fixed context would
@@ -1176,10 +1205,17 @@ def bench_sharded_decode(torch, capi, ctx, dev, stream, args, world, rank, dist,
             dist.barrier()
 
     ctx.launch_log()
-    for _ in range(args.warmup):
-        step()
+    try:
+        for _ in range(args.warmup):
+            step()
+        torch.cuda.synchronize()
+        ctx.check_device_error()
+    except Exception as e:
+        err = f"sharded step: {str(e)[:120]}"
+    if not agree(err is None):
+        peer.close()
+        return {"workload": f"config5 over {world} GPU(s)", "error": err or "sharded step failed on another rank"}
     barrier()
-    ctx.check_device_error()
     kernels = ctx.launch_log()
     launches = len(kernels) / max(1, args.warmup)
     steps = min(args.steps, 20)
