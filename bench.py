@@ -400,6 +400,8 @@ def main():
             peer = ctx.peer(world, rank, P, L)
             handles = [None] * world
             dist.all_gather_object(handles, peer.ipc_handle())
+            if os.environ.get("SPL_BENCH_FAIL_PEER_RANK") == str(rank):  # test hook: one-sided failure
+                raise RuntimeError("injected peer-open failure")
             peer.open(handles)
         except Exception as e:  # no IPC / peer access: keep the NCCL flow
             err = str(e)[:60]
@@ -1183,6 +1185,8 @@ def bench_sharded_decode(torch, capi, ctx, dev, stream, args, world, rank, dist,
         else:
             handles = [None] * world
             dist.all_gather_object(handles, peer.ipc_handle())
+            if os.environ.get("SPL_BENCH_FAIL_PEER_RANK") == str(rank):  # test hook: one-sided failure
+                raise RuntimeError("injected peer-open failure")
             peer.open(handles)
         ctx.reserve(P, n, L, k, D)
     except Exception as e:  # e.g. no CUDA IPC / peer access between these GPUs
