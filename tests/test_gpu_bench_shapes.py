@@ -78,7 +78,8 @@ def _run_step(ctx, oracle, B, H, n, L, k, seed, expect_kernels, sample_att=None)
     torch.cuda.synchronize()
     ctx.check_device_error()
     ran = ctx.launch_log()
-    assert ran == expect_kernels, ran
+    if expect_kernels is not None:
+        assert ran == expect_kernels, ran
     got_codes = U(codes)
     # appended rows: code = exact hash of the new key, K/V rows = the new vectors (bf16)
     qcodes = np.zeros((P, W), np.uint32)
@@ -132,3 +133,19 @@ def test_decode_step_config4_full(ctx, oracle):
     sample = list(range(0, 512, 8))
     _run_step(ctx, oracle, 16, 32, n, 256, k, 404,
               ["k1_encode_cluster", "k3_scan", "k3_select", "k4_gather"], sample_att=sample)
+
+
+@pytest.mark.parametrize("seed", list(range(12)))
+def test_decode_step_random(ctx, oracle, seed):
+    """Random decode-step geometries (batch, heads, cache length, code width,
+    budget; ragged n_valid across the batch) through spl_decode_step, whichever
+    kernels it picks: appended rows, indices and attention output as above."""
+    rng = np.random.default_rng(1000 + seed)
+    B = int(rng.integers(1, 4))
+    H = int(rng.integers(1, 9))
+    L = int(rng.choice([128, 128, 256]))
+    n = int(rng.integers(37 * (B - 1) + 64, 20000))
+    nmin = n - 37 * (B - 1)
+    k = int(rng.choice([1, int(rng.integers(1, 64)), max(1, int(0.02 * n)), int(rng.integers(1, nmin + 1))]))
+    k = min(k, nmin)
+    _run_step(ctx, oracle, B, H, n, L, k, 2000 + seed, None)
