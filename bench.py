@@ -479,6 +479,36 @@ def main():
                           f"(median of 3 replays) / {args.steps}")
         except Exception as e:  # capture unsupported: keep the eager number
             graph_note = f"eager (graph capture failed: {str(e)[:80]})"
+    elif shard_path and shard_path.startswith("fused"):
+        # the fused sharded retrieval has no host collective inside: every
+        # rank captures `steps` of them in one graph and replays it at the
+        # same time (the kernels meet through peer memory), as at N = 1
+        gk, err = None, None
+        try:
+            gs = torch.cuda.Stream()
+            gs.wait_stream(torch.cuda.current_stream())
+            gk = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(gk, stream=gs, capture_error_mode="relaxed"):
+                for _ in range(args.steps):
+                    ctx.hamming_topk_sharded(peer, codes, n_local, L, qcodes, P, nvalid, 1, n_local, k,
+                                             idx, cnt, off, gs)
+        except Exception as e:
+            err = str(e)[:80]
+        if agree(err is None):
+            dist.barrier()
+            gk.replay()
+            torch.cuda.synchronize()
+            res = []
+            for _ in range(3):
+                dist.barrier()
+                res.append(event_timer(torch, gk.replay, 1, torch.cuda.current_stream()) / args.steps)
+            ctx.check_device_error()
+            ms = statistics.median(res)
+            graph_note = (f"one CUDA graph of {args.steps} back-to-back sharded retrievals per rank, "
+                          "replayed together (median of 3) / steps, max over ranks")
+        else:
+            graph_note = f"eager (graph capture failed: {err or 'on another rank'})"
+        del gk
     # the same retrieval with L2 flushed before every call (device time from
     # CUDA graphs of steps x (flush, call) minus steps x flush): the inputs
     # already exceed L2, this shows the number does not lean on L2 residue
