@@ -149,3 +149,51 @@ def test_decode_step_random(ctx, oracle, seed):
     k = int(rng.choice([1, int(rng.integers(1, 64)), max(1, int(0.02 * n)), int(rng.integers(1, nmin + 1))]))
     k = min(k, nmin)
     _run_step(ctx, oracle, B, H, n, L, k, 2000 + seed, None)
+
+
+@pytest.mark.parametrize("bad", ["nvalid0", "past_cap"])
+def test_append_out_of_range_is_rejected_without_writes(ctx, bad):
+    """An append slot outside [0, cap) (n_valid == 0 in a decode step, a full
+    cache) raises a DimensionError through the device error word and writes
+    nothing: the code / K / V caches sit between canary regions that must
+    stay untouched (no wild store into a neighbouring head)."""
+    B, H, cap, d, L = 2, 2, 256, 128, 128
+    W = L // 32
+    rng = np.random.default_rng(77)
+    w1, b1, w2 = _weights(rng, H, d, d, L)
+    hs = ctx.hasher(w1, b1, w2)
+    pad = 4096
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(DEV)
+    codes_big = torch.full((pad * 2 + B * H * cap * W,), 0x5A5A5A5A, dtype=torch.int32, device=DEV)
+    kc_big = torch.full((pad * 2 + B * H * cap * d,), 7.0, dtype=torch.float32, device=DEV)
+    vc_big = torch.full((pad * 2 + B * H * cap * d,), 9.0, dtype=torch.float32, device=DEV)
+    codes = codes_big[pad:pad + B * H * cap * W].view(B, H, cap, W)
+    kc = kc_big[pad:pad + B * H * cap * d].view(B, H, cap, d)
+    vc = vc_big[pad:pad + B * H * cap * d].view(B, H, cap, d)
+    before = (codes_big.clone(), kc_big.clone(), vc_big.clone())
+    q = t(rng.standard_normal((B, H, d)).astype(np.float32))
+    kn = t(rng.standard_normal((B, H, d)).astype(np.float32))
+    vn = t(rng.standard_normal((B, H, d)).astype(np.float32))
+    if bad == "nvalid0":
+        nv = np.array([0, 0], np.int32)
+    else:
+        nv = np.array([cap + 1, cap + 5], np.int32)
+    P, k = B * H, 8
+    idx = torch.zeros((P, k), dtype=torch.int32, device=DEV)
+    cnt = torch.zeros(P, dtype=torch.int32, device=DEV)
+    out = torch.zeros((B, H, d), dtype=torch.float32, device=DEV)
+    with pytest.raises(capi.DimensionError):
+        hs.decode_step(q, kn, vn, B, codes, kc, vc, capi.SPL_F32, cap, t(nv), cap, k,
+                       float(1 / np.sqrt(d)), idx, cnt, out)
+        torch.cuda.synchronize()
+        ctx.check_device_error()
+    torch.cuda.synchronize()
+    try:
+        ctx.check_device_error()
+    except capi.SpotlightError:
+        pass
+    for a, b in zip((codes_big, kc_big, vc_big), before):
+        assert torch.equal(a[:pad], b[:pad]) and torch.equal(a[-pad:], b[-pad:])
+    # no row of any head was written either
+    assert torch.equal(codes_big, before[0])
+    assert torch.equal(kc_big, before[1]) and torch.equal(vc_big, before[2])
