@@ -450,11 +450,18 @@ __global__ void __cluster_dims__(kCS, 1, 1) __launch_bounds__(kEncThreads)
         }
         // V rows and append slots: asynchronous copies, waited for only after
         // layer 1 (a cold load here would sit on the critical path)
-        if (stage_v)
-            for (uint32_t i = tid; i < nv * d / 4; i += kEncThreads) {
-                const uint32_t v = (4 * i) / d, c = (4 * i) % d;
-                cp_async16(vs + 4 * i, job.v_new + (((uint64_t)(v0 + v)) * H + head) * d + c);
-            }
+        if (stage_v) {
+            if ((reinterpret_cast<uintptr_t>(job.v_new) & 15u) == 0)
+                for (uint32_t i = tid; i < nv * d / 4; i += kEncThreads) {
+                    const uint32_t v = (4 * i) / d, c = (4 * i) % d;
+                    cp_async16(vs + 4 * i, job.v_new + (((uint64_t)(v0 + v)) * H + head) * d + c);
+                }
+            else  // a caller's V rows need not be 16-byte aligned
+                for (uint32_t i = tid; i < nv * d; i += kEncThreads) {
+                    const uint32_t v = i / d, c = i % d;
+                    cp_async4(vs + i, job.v_new + (((uint64_t)(v0 + v)) * H + head) * d + c);
+                }
+        }
         if (job.out_mode == ENC_APPEND && tid < (int)nv) cp_async4(s_pos + tid, job.pos + v0 + tid);
         asm volatile("cp.async.commit_group;" ::: "memory");
         K1_STAMP(2);

@@ -197,3 +197,37 @@ def test_append_out_of_range_is_rejected_without_writes(ctx, bad):
     # no row of any head was written either
     assert torch.equal(codes_big, before[0])
     assert torch.equal(kc_big, before[1]) and torch.equal(vc_big, before[2])
+
+
+def test_append_unaligned_inputs(ctx):
+    """New K / V rows passed at addresses that are only 4-byte aligned: the
+    encoder stages V with 4-byte asynchronous copies then (16-byte copies
+    need 16-byte alignment); the appended rows and codes must be exact."""
+    B, H, cap, d, L = 2, 3, 64, 128, 128
+    W = L // 32
+    rng = np.random.default_rng(78)
+    w1, b1, w2 = _weights(rng, H, d, d, L)
+    hs = ctx.hasher(w1, b1, w2)
+    kn = rng.standard_normal((B, H, d)).astype(np.float32)
+    vn = rng.standard_normal((B, H, d)).astype(np.float32)
+    kbuf = torch.zeros(B * H * d + 1, dtype=torch.float32, device=DEV)
+    vbuf = torch.zeros(B * H * d + 1, dtype=torch.float32, device=DEV)
+    kbuf[1:] = torch.from_numpy(kn.ravel()).to(DEV)
+    vbuf[1:] = torch.from_numpy(vn.ravel()).to(DEV)
+    k_view, v_view = kbuf[1:].view(B, H, d), vbuf[1:].view(B, H, d)  # 4-byte aligned only
+    codes = torch.zeros((B, H, cap, W), dtype=torch.int32, device=DEV)
+    kc = torch.zeros((B, H, cap, d), dtype=torch.float32, device=DEV)
+    vc = torch.zeros((B, H, cap, d), dtype=torch.float32, device=DEV)
+    pos = torch.tensor([5, 17], dtype=torch.int32, device=DEV)
+    hs.encode_append(k_view, v_view, B, codes, kc, vc, capi.SPL_F32, cap, pos)
+    torch.cuda.synchronize()
+    ctx.check_device_error()
+    kc_h, vc_h = kc.cpu().numpy(), vc.cpu().numpy()
+    for b, slot in ((0, 5), (1, 17)):
+        assert np.array_equal(kc_h[b, :, slot], kn[b]) and np.array_equal(vc_h[b, :, slot], vn[b])
+    ref = torch.zeros((B, H, 1, W), dtype=torch.int32, device=DEV)
+    hs.encode(torch.from_numpy(kn[:, :, None]).to(DEV), B, 1, ref)
+    torch.cuda.synchronize()
+    got = codes.cpu().numpy()
+    want = ref.cpu().numpy()
+    assert np.array_equal(got[0, :, 5], want[0, :, 0]) and np.array_equal(got[1, :, 17], want[1, :, 0])
