@@ -724,6 +724,11 @@ spl_status spl_attend_combine(spl_ctx* ctx, const float* partials, uint32_t R, u
 }
 
 // ------------------------------------------------------------ decode step
+// The attention kernels read K / V row slices with 8- and 16-byte loads
+static bool kv_aligned(const void* k, const void* v) {
+    return ((reinterpret_cast<uintptr_t>(k) | reinterpret_cast<uintptr_t>(v)) & 15u) == 0;
+}
+
 spl_status spl_decode_step(spl_ctx* ctx, const spl_hasher* hs, const float* q,
                            const float* k_new, const float* v_new, uint32_t B,
                            uint32_t* codes, void* kcache, void* vcache, int kv_dtype,
@@ -765,7 +770,8 @@ spl_status spl_decode_step(spl_ctx* ctx, const spl_hasher* hs, const float* q,
     // (L = d = 128, scores on chip): each K3 CTA attends the rows it selects
     bool done = false;
     if (!(scale > 0.0f)) return fail(ctx, SPL_E_DIMENSION, "attention: scale must be positive");
-    if ((st = hamming_topk_attend_impl(ctx, codes, cap, hs->L, qcodes, P, n_valid, H, n_max, k, idx,
+    if (kv_aligned(kcache, vcache) &&
+        (st = hamming_topk_attend_impl(ctx, codes, cap, hs->L, qcodes, P, n_valid, H, n_max, k, idx,
                                        cnt, q, kcache, vcache, kv_dtype, hs->d, scale * kLog2e, out,
                                        S(stream), &done)))
         return st;
@@ -800,6 +806,8 @@ spl_status spl_sharded_decode_step(spl_ctx* ctx, spl_peer* peer, const spl_hashe
     if (!ctx || !hs || !peer) return SPL_E_STATE;
     if (!peer->connected) return fail(ctx, SPL_E_STATE, "sharded_decode_step: peer group not connected");
     if (!(scale > 0.0f)) return fail(ctx, SPL_E_DIMENSION, "attention: scale must be positive");
+    if (!kv_aligned(kcache, vcache))
+        return fail(ctx, SPL_E_DIMENSION, "sharded_decode_step: K / V caches must be 16-byte aligned");
     if (n_max > cap)
         return fail(ctx, SPL_E_DIMENSION,
                     "sharded_decode_step: n_max=" + std::to_string(n_max) +

@@ -494,13 +494,19 @@ spl_status sparse_attend_launch(spl_ctx* ctx, AttParams prm, uint32_t kmax, int 
     const void* fn = nullptr;
     if (kv_dtype != SPL_F32 && kv_dtype != SPL_BF16)
         return fail(ctx, SPL_E_DIMENSION, "sparse_attend: unknown kv dtype");
-    switch (d) {
+    // the tuned kernels read K / V row slices with 8- / 16-byte loads: caches
+    // that are not 16-byte aligned take the generic kernel (f32) or fail
+    const bool aligned =
+        ((reinterpret_cast<uintptr_t>(prm.kc) | reinterpret_cast<uintptr_t>(prm.vc)) & 15u) == 0;
+    if (!aligned && kv_dtype == SPL_BF16 && (d == 32 || d == 64 || d == 128 || d == 256))
+        return fail(ctx, SPL_E_DIMENSION, "sparse_attend: bf16 K / V caches must be 16-byte aligned");
+    switch (aligned ? d : 0u) {
         case 32: fn = att_fn<1>(kv_dtype); break;
         case 64: fn = att_fn<2>(kv_dtype); break;
         case 128: fn = att_fn<4>(kv_dtype); break;
         case 256: fn = att_fn<8>(kv_dtype); break;
         default: {
-            if (d == 0) return fail(ctx, SPL_E_DIMENSION, "attention: embedding dimensions differ");
+            if (prm.d == 0) return fail(ctx, SPL_E_DIMENSION, "attention: embedding dimensions differ");
             if (kv_dtype != SPL_F32)
                 return fail(ctx, SPL_E_DIMENSION,
                             "sparse_attend: bf16 K/V needs head dim 32, 64, 128 or 256");

@@ -231,3 +231,36 @@ def test_append_unaligned_inputs(ctx):
     got = codes.cpu().numpy()
     want = ref.cpu().numpy()
     assert np.array_equal(got[0, :, 5], want[0, :, 0]) and np.array_equal(got[1, :, 17], want[1, :, 0])
+
+
+def test_sparse_attend_unaligned_caches(ctx):
+    """K / V caches that are only 4-byte aligned: f32 takes the generic
+    kernel and gives the aligned result (to rounding); bf16 is rejected."""
+    H, n, d, k = 3, 500, 128, 40
+    rng = np.random.default_rng(79)
+    kk = rng.standard_normal((H * n * d,)).astype(np.float32)
+    vv = rng.standard_normal((H * n * d,)).astype(np.float32)
+    q = torch.from_numpy(rng.standard_normal((1, H, d)).astype(np.float32)).to(DEV)
+    idx = torch.from_numpy(np.stack([np.sort(rng.choice(n - 1, k, replace=False)) for _ in range(H)])
+                           .astype(np.int32)).to(DEV)
+    cnt = torch.full((H,), k, dtype=torch.int32, device=DEV)
+    nv = torch.full((1,), n, dtype=torch.int32, device=DEV)
+    scale = float(1 / np.sqrt(d))
+    outs = []
+    for off in (0, 1):
+        kb = torch.zeros(H * n * d + 4, dtype=torch.float32, device=DEV)
+        vb = torch.zeros(H * n * d + 4, dtype=torch.float32, device=DEV)
+        kb[off:off + H * n * d] = torch.from_numpy(kk).to(DEV)
+        vb[off:off + H * n * d] = torch.from_numpy(vv).to(DEV)
+        kc, vc = kb[off:off + H * n * d].view(1, H, n, d), vb[off:off + H * n * d].view(1, H, n, d)
+        out = torch.zeros((1, H, d), dtype=torch.float32, device=DEV)
+        ctx.sparse_attend(q, kc, vc, capi.SPL_F32, n, d, H, idx, k, cnt, nv, H, scale, out)
+        torch.cuda.synchronize()
+        ctx.check_device_error()
+        outs.append(out.cpu().numpy())
+    assert np.abs(outs[0] - outs[1]).max() <= 1e-5
+    kb16 = torch.zeros(H * n * d + 8, dtype=torch.bfloat16, device=DEV)
+    kc16 = kb16[1:1 + H * n * d].view(1, H, n, d)
+    with pytest.raises(capi.DimensionError, match="16-byte aligned"):
+        ctx.sparse_attend(q, kc16, kc16, capi.SPL_BF16, n, d, H, idx, k, cnt, nv, H, scale,
+                          torch.zeros((1, H, d), dtype=torch.float32, device=DEV))
