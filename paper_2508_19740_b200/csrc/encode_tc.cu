@@ -814,6 +814,9 @@ spl_status encode_tc_launch(spl_ctx* ctx, const spl_hasher* hs, const void* x, i
         return fail(ctx, SPL_E_DIMENSION, "encode: unknown input dtype");
     if (B == 0 || m == 0) return SPL_OK;
     if (!x || !codes) return fail(ctx, SPL_E_STATE, "encode: null device pointer");
+    // keys are staged with 16-byte loads (f32) / TMA (bf16), codes stored as 16-byte vectors
+    if ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(codes)) % 16 != 0)
+        return fail(ctx, SPL_E_DIMENSION, "encode: SPL_ENCODE_TC input and codes must be 16-byte aligned");
     TcParams prm{};
     prm.x = x;
     prm.x_bf16 = x_dtype == SPL_BF16;
