@@ -71,8 +71,12 @@ const char* spl_last_error(const spl_ctx* ctx);
 spl_status spl_reserve(spl_ctx* ctx, uint32_t P, uint64_t n_max, uint32_t L, uint32_t k,
                        uint32_t d);
 /* Device error word (non-finite encoder input -> NumericError, out-of-range
- * n_valid -> DimensionError). Synchronises `stream`, returns the recorded
- * status and clears it. */
+ * n_valid or append slot -> DimensionError, a retrieval whose CTAs could not
+ * all run at once -> SPL_E_CUDA after the in-kernel 2 s watchdog: its indices
+ * are then invalid). Kernels never fail the launch itself, so a caller that
+ * replays captured decode steps should check this word at least once per
+ * batch of steps. Synchronises `stream`, returns the recorded status and
+ * clears it. */
 spl_status spl_check_device_error(spl_ctx* ctx, void* stream);
 /* Number of kernels this context launched so far (bench gpu_launches). */
 uint64_t spl_launch_count(const spl_ctx* ctx);
