@@ -48,6 +48,29 @@ for path in ("fused", "twopass"):
     os.environ.pop("SPL_K3_PATH", None)
 out = torch.zeros((1, H, d), dtype=torch.float32, device=dev)
 ctx.sparse_attend(T(q), T(keys), T(vals), capi.SPL_F32, n, d, H, idx, k, cnt, nv, H, float(1 / np.sqrt(d)), out)
+# decode step: K1 append + encode, fused K3 + attention over bf16 K/V
+# (attention_eval.cpp:234-264: the selected rows plus the own row nv - 1)
+nvd = 2500
+kcb = T(keys).bfloat16()
+vcb = T(vals).bfloat16()
+cd = codes.clone()
+kn = rng.standard_normal((1, H, d)).astype(np.float32)
+vn = rng.standard_normal((1, H, d)).astype(np.float32)
+nvt = torch.full((1,), nvd, dtype=torch.int32, device=dev)
+di = torch.zeros((H, k), dtype=torch.int32, device=dev)
+dc = torch.zeros(H, dtype=torch.int32, device=dev)
+do = torch.zeros((1, H, d), dtype=torch.float32, device=dev)
+hs.decode_step(T(q), T(kn), T(vn), 1, cd, kcb, vcb, capi.SPL_BF16, n, nvt, n, k, float(1 / np.sqrt(d)),
+               di, dc, do, torch.cuda.current_stream().cuda_stream)
+torch.cuda.synchronize()
+want = orc.retrieve_batch(cd.cpu().numpy().view(np.uint32)[0], qc.cpu().numpy().view(np.uint32)[0],
+                          np.full(H, nvd, np.uint32), k)
+fails += int(not np.array_equal(di.cpu().numpy().view(np.uint32), want))
+for h in range(H):
+    rows = sorted(set(di[h, :int(dc[h])].tolist()) | {nvd - 1})
+    kr, vr = kcb[0, h, rows].float(), vcb[0, h, rows].float()
+    p = torch.softmax(kr @ T(q)[0, h] / np.sqrt(d), 0)
+    fails += int(float((p @ vr - do[0, h]).abs().max()) > 1e-3)
 # K2 (both kernels)
 x = T(keys).bfloat16()
 c2 = torch.zeros_like(codes)
