@@ -701,8 +701,8 @@ def main():
     achieved = alg_bytes / (us * 1e-6) / 1e9
     scan_bytes = P * n_local * W * 4
     # dram bytes per retrieval: ncu cannot run inside the timed process, so
-    # this is the newest committed `ncu --set full` capture of the same kernel
-    # on the same workload, stamped with the commit it was taken at
+    # this is the newest committed ncu capture of the same kernel on the same
+    # workload (caches flushed by ncu), stamped with the commit it was taken at
     traffic = traffic_src = traffic_b2b = None
     for tpath in sorted((ROOT / "profiles").glob("r*_k3_traffic.json"), reverse=True):
         try:
